@@ -1,0 +1,260 @@
+/*
+ * hifuse.h -- C ABI of the B200 (sm_100a) HiFuse hot path.
+ *
+ * HiFuse (arXiv 2408.08490) speeds up mini-batch HGNN training by merging the
+ * per-semantic-graph work of every HGNN layer.  A layer has four stages
+ * (PAPER.md lines 112-125): semantic graph build, feature projection,
+ * neighbour aggregation, semantic fusion.  This library runs all four on the
+ * GPU, each as a small, fixed number of kernels that does not grow with the
+ * number of relations R:
+ *
+ *   hifuse_build_semantic_graphs  Alg. 2 (lines 310-324) + merging: one
+ *                                 segmented CSR over all relations (and its
+ *                                 CSC transpose); integer work, bit-exact.
+ *   hifuse_project                per-relation / per-type projection (line 119),
+ *                                 one grouped GEMM launch; layer 0 gathers its
+ *                                 rows from the type-major feature store
+ *                                 (reorganisation, lines 199-221).
+ *   hifuse_aggregate_fwd          Alg. 1 (lines 246-262): ONE gather-reduce
+ *                                 kernel for every relation (sum / mean / GAT
+ *                                 edge softmax).
+ *   hifuse_semantic_fuse          fusion (line 123): sum over relations + root
+ *                                 + bias, activation.
+ *   *_bwd                         the adjoints (line 156, "backward pass on GPU
+ *                                 for gradient computation").
+ *
+ * Conventions:
+ *  - Pointers named d_* are device memory; *_h are host memory.  The caller
+ *    owns every buffer, including workspace; the library never allocates on
+ *    the hot path and keeps no global state except cached device attributes.
+ *  - Every call is asynchronous and stream-ordered on `stream`; no call
+ *    synchronises the device (except hifuse_read_status, for tests).  All
+ *    sizes a launch needs are host-known from hifuse_layer_shape, so a whole
+ *    step is CUDA-graph capturable; the one data-dependent size, the number U
+ *    of rows of the merged projected matrix, lives in device memory (U_dev).
+ *  - fp32 row-major everywhere; feature widths K, D must be 64 or 128
+ *    (HIFUSE_ERR_UNSUPPORTED otherwise); heads H must divide D with D/H a
+ *    multiple of 4.  int32 local ids and offsets (N < 2^31), int64 edge ids.
+ *  - Host-detectable errors (null pointer, bad sizes, misalignment) return
+ *    synchronously and launch nothing.  Data errors found on the device
+ *    (edge id out of range, relation id out of range, local id out of range)
+ *    OR bits into *d_status (HIFUSE_ST_*) and the offending edge is dropped:
+ *    no out-of-bounds access ever happens.
+ *  - Results are deterministic: the build is bit-exact against the CPU oracle
+ *    (oracle/hifuse_oracle.c), reductions use fixed orders, no float atomics.
+ */
+#ifndef HIFUSE_H
+#define HIFUSE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *hifuse_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+  HIFUSE_OK = 0,
+  HIFUSE_ERR_INVALID_ARG = 1,   /* null pointer / negative or inconsistent size */
+  HIFUSE_ERR_ALIGNMENT = 2,     /* a float pointer is not 16-byte aligned       */
+  HIFUSE_ERR_UNSUPPORTED = 3,   /* K, D, H or layout outside the supported set   */
+  HIFUSE_ERR_WORKSPACE = 4,     /* ws_bytes smaller than the *_sizes() answer    */
+  HIFUSE_ERR_CUDA = 5           /* a CUDA launch failed (cudaGetLastError)       */
+} hifuse_status;
+
+/* device status bits (ORed into d_status by the build) */
+#define HIFUSE_ST_BAD_EDGE_ID 1   /* edge_id < 0 or >= num_graph_edges          */
+#define HIFUSE_ST_BAD_REL     2   /* edge_type[edge_id] not in [0, R)           */
+#define HIFUSE_ST_BAD_SRC     4   /* src_local >= n_src(src type of relation)   */
+#define HIFUSE_ST_BAD_DST     8   /* dst_local >= n_dst(dst type of relation)   */
+
+typedef enum { HIFUSE_AGG_SUM = 0, HIFUSE_AGG_MEAN = 1, HIFUSE_AGG_GAT = 2 } hifuse_agg;
+typedef enum { HIFUSE_ACT_NONE = 0, HIFUSE_ACT_RELU = 1 } hifuse_act;
+/* Layout of the merged projected matrix Y (reading C3).  COMPACT:
+ * per relation, one row per distinct source vertex of the layer, ascending.
+ * SLOTS (every source vertex x every live relation) is reserved. */
+typedef enum { HIFUSE_LAYOUT_SLOTS = 0, HIFUSE_LAYOUT_COMPACT = 1 } hifuse_layout;
+/* Projection arithmetic.  FP32: CUDA-core fp32 FMA.  TF32: tcgen05 kind::tf32
+ * tensor cores, fp32 accumulate (reading C17/C18). */
+typedef enum { HIFUSE_PREC_FP32 = 0, HIFUSE_PREC_TF32 = 1 } hifuse_prec;
+
+#define HIFUSE_MAX_TYPES 64
+#define HIFUSE_MAX_RELS 512
+
+/* Host metadata of one layer's sampled block (Alg. 2 inputs EdgeIndex[i],
+ * EdgeID[i] are device arrays passed separately).  Per vertex type t the
+ * layer's destination vertices are the first n_dst[t] of its n_src[t] source
+ * vertices (reading C12).  Relation r maps type rel_src_type[r] to type
+ * rel_dst_type[r].  Derived (host, no sync):
+ *   rows = sum_r n_dst[rel_dst_type[r]]   merged (relation, destination) rows,
+ *          row (r, i) = rel_row_off[r] + i, relation-major (reading C2);
+ *   S    = sum_r n_src[rel_src_type[r]]   (relation, source) slots;
+ *   U    <= U_max = min(N, S)             rows of Y (device-resident U_dev). */
+typedef struct {
+  int32_t num_types, num_rels;
+  const int32_t *rel_src_type_h;   /* [R] */
+  const int32_t *rel_dst_type_h;   /* [R] */
+  const int32_t *n_src_h;          /* [T] */
+  const int32_t *n_dst_h;          /* [T] */
+  int64_t num_edges;               /* N   */
+} hifuse_layer_shape;
+
+/* Caller-allocated device outputs of the build of one layer (int32).
+ * CSR: row_ptr over the merged rows; inside a row, edges in ascending original
+ * column (Alg. 2 keeps column order); col[p] = Y row read by CSR position p;
+ * eperm[p] = original column of position p.  Y rows of relation r are
+ * [rel_y_off[r], rel_y_off[r+1]); y_src[u] = source local id of Y row u;
+ * slot_y[slot(r, j)] = Y row of (r, j) or -1, slot(r, j) = sum_{r'<r}
+ * n_src(src type of r') + j.  CSC over Y rows: col_ptr, csc_pos (CSR
+ * position, ascending inside a column), csc_row (merged row of that
+ * position).  Entries past the valid count are -1; col_ptr entries past U
+ * equal the number of valid edges. */
+typedef struct {
+  int32_t *rel_row_off;  /* [R+1]      */
+  int32_t *row_ptr;      /* [rows+1]   */
+  int32_t *col;          /* [N]        */
+  int32_t *eperm;        /* [N]        */
+  int32_t *rel_y_off;    /* [R+1]      */
+  int32_t *y_src;        /* [U_max]    */
+  int32_t *col_ptr;      /* [U_max+1]  */
+  int32_t *csc_pos;      /* [N]        */
+  int32_t *csc_row;      /* [N]        */
+  int32_t *slot_y;       /* [S]        */
+  int32_t *U_dev;        /* [1]        */
+} hifuse_csr;
+
+/* Sizes of one layer (host only, no device work, no sync). */
+hifuse_status hifuse_csr_sizes(const hifuse_layer_shape *shape, hifuse_layout layout,
+                               int64_t *rows, int64_t *U_max, int64_t *S,
+                               size_t *build_ws_bytes);
+
+/* A1. Semantic graph build for `num_layers` layers (Alg. 2 lines
+ * 310-324: EdgeTypeLayer = EdgeType[EdgeID], per-relation compare + select),
+ * producing the merged segmented CSR/CSC of each layer in `out[l]`.
+ *   d_src_local[l], d_dst_local[l]: int32 [N_l] batch-local endpoint ids;
+ *   d_edge_id[l]: int64 [N_l] graph-global edge ids;
+ *   d_edge_type: int32 [num_graph_edges] relation of every graph edge.
+ * Workspace: d_ws of at least max_l build_ws_bytes(l).  d_status: int32 [1],
+ * bits ORed (never cleared by the library).  Layers run back to back on
+ * `stream`; kernel count is independent of R. */
+hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape *shapes, int num_layers,
+                                           const int32_t *const *d_src_local,
+                                           const int32_t *const *d_dst_local,
+                                           const int64_t *const *d_edge_id,
+                                           const int32_t *d_edge_type, int64_t num_graph_edges,
+                                           hifuse_layout layout, const hifuse_csr *out,
+                                           void *d_ws, size_t ws_bytes, int32_t *d_status,
+                                           hifuse_stream_t stream);
+
+/* A2+A3. Feature projection (readings C3, C4, C6, C7), one
+ * grouped GEMM launch over groups {relation r} u {root type t}:
+ *   Y[u]        = X_{s(r)}[y_src[u]] . W_rel[r]         u in relation r's rows
+ *   R0[t,i]     = X_t[i] . W_root[t]                     i < n_dst[t] (if W_root)
+ *   s_src[u,h]  = <Y[u, head h], att[r,0,head h]>        (if att, RGAT)
+ *   s_dst[(r,i),h] = <(X_{t(r)}[i] W_rel[r])[head h], att[r,1,head h]>
+ * X: fp32 [x_rows, K].  Row of (type t, local j) is type_src_off[t] + j, or,
+ * when d_gather_ids != NULL, d_gather_ids[type_src_off[t] + j] (layer 0 reads
+ * straight from the type-major feature store).
+ * W_rel [R,K,D]; W_root [T,K,D] or NULL; att [R,2,D] or NULL.
+ * Outputs: Y [U_max,D], R0 [sum_t n_dst[t], D] (if W_root), s_src [U_max,H],
+ * s_dst [rows,H] (if att).  Workspace: hifuse_project_ws_bytes(). */
+size_t hifuse_project_ws_bytes(const hifuse_layer_shape *shape, int K, int D, int heads);
+hifuse_status hifuse_project(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                             hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
+                             const float *d_X, int64_t x_rows, const int32_t *d_gather_ids,
+                             const float *d_W_rel, const float *d_W_root, const float *d_att,
+                             float *d_Y, float *d_R0, float *d_s_src, float *d_s_dst,
+                             void *d_ws, size_t ws_bytes, hifuse_stream_t stream);
+
+/* A4. Merged neighbour aggregation (Alg. 1): ONE
+ * kernel for all relations.  For every merged row m = (r, i):
+ *   SUM : Z[m] = sum_{p in row m} Y[col[p]]
+ *   MEAN: Z[m] = SUM / |row m|                 (reading C1; IEEE division)
+ *   GAT : per head h, alpha_p = softmax_{p in row m}(LeakyReLU_slope(
+ *         s_src[col[p],h] + s_dst[m,h])); Z[m,head h] = sum alpha_p Y[col[p],head h]
+ *         (readings C5, C6, C8); d_stats [rows, 2H] = (max, sum of exp) per
+ *         (row, head), saved for the backward (reading C9).
+ * Empty rows give Z = 0.  Relation-agnostic: only row_ptr/col are read. */
+hifuse_status hifuse_aggregate_fwd(const hifuse_csr *csr, int64_t rows, hifuse_agg agg, int D,
+                                   int heads, float slope, const float *d_Y,
+                                   const float *d_s_src, const float *d_s_dst, float *d_Z,
+                                   float *d_stats, hifuse_stream_t stream);
+
+/* A5. Semantic fusion (readings C2, C4, C10):
+ *   H_t[i] = act(R0_t[i] + bias_t + sum_{r: t(r)=t} Z[rel_row_off[r] + i]).
+ * Z [rows, D]; R0 [sum n_dst, D] or NULL; bias [T, D] or NULL; H [sum n_dst, D]
+ * type-major (the next layer's X). */
+hifuse_status hifuse_semantic_fuse(const hifuse_layer_shape *shape, int D, hifuse_act act,
+                                   const float *d_Z, const float *d_R0, const float *d_bias,
+                                   float *d_H, hifuse_stream_t stream);
+
+/* A6a. Fusion backward: G = dH * act'(H) (ReLU' = 1[H > 0]); G is dR0 and
+ * the gradient of every Z row (r, i) (= G_{t(r)}[i]); dbias_t = sum_i G_t[i]
+ * (fixed-order two-stage reduction).  dbias may be NULL.  Workspace:
+ * hifuse_fuse_bwd_ws_bytes(). */
+size_t hifuse_fuse_bwd_ws_bytes(const hifuse_layer_shape *shape, int D);
+hifuse_status hifuse_semantic_fuse_bwd(const hifuse_layer_shape *shape, int D, hifuse_act act,
+                                       const float *d_dH, const float *d_H, float *d_G,
+                                       float *d_dbias, void *d_ws, size_t ws_bytes,
+                                       hifuse_stream_t stream);
+
+/* A6b. Aggregation backward: the transpose gather over the CSC.
+ *   SUM/MEAN: dY[u] = sum_{q in col u} w(row_q) G[g(row_q)],  w = 1 or 1/|row|
+ *   GAT: pass 1 (row-major) recomputes alpha from d_stats and forms
+ *        dpre = alpha (dalpha - sum alpha dalpha) LeakyReLU', ds_dst[m,h] = sum dpre;
+ *        pass 2 (CSC): dY[u,head h] = sum alpha G[g(row),head h], ds_src[u,h] = sum dpre.
+ * g(r, i) = type_dst_off[t(r)] + i maps a merged row to its row of G.  dY
+ * excludes the score-chain term (hifuse_project_bwd adds it).  Workspace:
+ * hifuse_aggregate_bwd_ws_bytes() (GAT: 2 N H floats). */
+size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape *shape, hifuse_agg agg, int heads);
+hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                   hifuse_agg agg, int D, int heads, float slope,
+                                   const float *d_G, const float *d_Y, const float *d_s_src,
+                                   const float *d_s_dst, const float *d_stats, float *d_dY,
+                                   float *d_ds_src, float *d_ds_dst, void *d_ws, size_t ws_bytes,
+                                   hifuse_stream_t stream);
+
+/* A6c. Projection backward, the adjoint of hifuse_project:
+ *   dYt = dY + ds_src (x) att[r,0]             (score chain, RGAT; d_dY updated in place)
+ *   dW_rel[r]  = sum_u X_row(u)^T dYt[u] (+ s_dst chain)   dW_root[t] = sum_i X_t[i]^T G_t[i]
+ *   datt[r]    = (sum_u ds_src[u,h] Y[u,head h] | sum_i ds_dst v-chain)
+ *   dX (optional, NULL for layer 0) = sum of dYt W_r^T + G W_root^T + ds_dst-chain.
+ * Fixed-order chunked reductions (deterministic).  Workspace:
+ * hifuse_project_bwd_ws_bytes(). */
+size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape *shape, int K, int D, int heads);
+hifuse_status hifuse_project_bwd(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                 hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
+                                 const float *d_X, int64_t x_rows, const int32_t *d_gather_ids,
+                                 const float *d_W_rel, const float *d_W_root, const float *d_att,
+                                 const float *d_Y, float *d_dY, const float *d_G,
+                                 const float *d_ds_src, const float *d_ds_dst, float *d_dX,
+                                 float *d_dW_rel, float *d_dW_root, float *d_datt,
+                                 void *d_ws, size_t ws_bytes, hifuse_stream_t stream);
+
+/* Training-step helpers outside the paper's four stages:
+ * linear classifier + mean softmax cross-entropy on the seed rows, its
+ * gradients, and the SGD update p -= lr * g over a flat parameter buffer.
+ *   logits = Hs Wc + bc  (Hs [B, D] rows of d_H starting at row h_row0)
+ *   loss   = mean_b (logsumexp(logits_b) - logits_b[label_b])    -> d_loss [1]
+ *   dH (rows h_row0.. of d_dH; all other rows zeroed), dWc [D,C], dbc [C]. */
+size_t hifuse_xent_ws_bytes(int B, int D, int C);
+hifuse_status hifuse_linear_xent(int B, int D, int C, const float *d_H, int64_t h_rows,
+                                 int64_t h_row0, const int32_t *d_labels, const float *d_Wc,
+                                 const float *d_bc, float *d_loss, float *d_dH, float *d_dWc,
+                                 float *d_dbc, void *d_ws, size_t ws_bytes,
+                                 hifuse_stream_t stream);
+hifuse_status hifuse_sgd(float *d_param, const float *d_grad, int64_t n, float lr, float grad_scale,
+                         hifuse_stream_t stream);
+
+/* Tests / debugging: copies *d_status to *out_h and synchronises `stream`. */
+hifuse_status hifuse_read_status(const int32_t *d_status, hifuse_stream_t stream, int32_t *out_h);
+const char *hifuse_status_string(hifuse_status s);
+/* Number of kernels launched by this process so far (host counter). */
+int64_t hifuse_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIFUSE_H */

@@ -1,0 +1,477 @@
+// aggregate.cu -- A4 (merged neighbour aggregation, Alg. 1 lines
+// 246-268) and A6b (its transpose, the aggregation backward).
+//
+// Merging (Alg. 1) concatenates every semantic graph's gathered
+// source features and destination indices so that ONE Aggregate call serves
+// all relations.  Here the concatenation is virtual: the build's segmented
+// CSR indexes the merged projected matrix Y directly, so FeatureCat is never
+// materialised and A4 is a single relation-agnostic CSR gather-reduce.
+//
+// Mapping (B200): one warp per merged (relation, destination) row; a row of D
+// fp32 is D/4 float4 lanes, so D = 128 uses the whole warp on one edge and
+// D = 64 runs two half-warp edge streams that merge at the end.  Up to 32
+// column indices are fetched with one coalesced load and broadcast with
+// shuffles; the gathers of UNROLL edges per stream are issued back to back to
+// keep several 256-512 B row loads in flight per warp (HBM latency hiding).
+#include "common.cuh"
+
+namespace hf {
+
+static constexpr int kWarpsPerBlock = 8;
+static constexpr int kUnroll = 4;
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4fma(float s, float4 y, float4 a) {
+  return make_float4(fmaf(s, y.x, a.x), fmaf(s, y.y, a.y), fmaf(s, y.z, a.z), fmaf(s, y.w, a.w));
+}
+__device__ __forceinline__ float4 f4shfl_xor(float4 v, int o) {
+  return make_float4(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o),
+                     __shfl_xor_sync(0xffffffffu, v.z, o), __shfl_xor_sync(0xffffffffu, v.w, o));
+}
+__device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? x : slope * x; }
+__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+
+// ------------------------------------------------------------ forward SUM/MEAN
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict__ col,
+          const float4* __restrict__ Y, float4* __restrict__ Z) {
+  constexpr int LPR = D / 4;              // lanes per row stream
+  constexpr int NS = 32 / LPR;            // edge streams per warp
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % LPR, sid = lane / LPR;
+  long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int b = row_ptr[row], e = row_ptr[row + 1];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = b; base < e; base += 32) {
+    const int n = min(32, e - base);
+    const int my_col = lane < n ? __ldg(col + base + lane) : 0;
+    int k = 0;
+    for (; k + NS * kUnroll <= n; k += NS * kUnroll) {
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        int c = __shfl_sync(0xffffffffu, my_col, k + u * NS + sid);
+        v[u] = ldg4(Y + (long long)c * LPR + sl);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) acc = f4add(acc, v[u]);
+    }
+    for (; k < n; k += NS) {
+      int idx = k + sid;
+      int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+      if (idx < n) acc = f4add(acc, ldg4(Y + (long long)c * LPR + sl));
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
+  if (sid == 0) {
+    if (MEAN && e > b) {
+      float dg = (float)(e - b);
+      acc = make_float4(__fdiv_rn(acc.x, dg), __fdiv_rn(acc.y, dg), __fdiv_rn(acc.z, dg),
+                        __fdiv_rn(acc.w, dg));
+    }
+    Z[row * LPR + sl] = acc;
+  }
+}
+
+// ------------------------------------------------------------- forward GAT
+// Per head h: two passes over the row's edges (rows are short): the max of the
+// logits, then p = exp(l - max), sum p and sum p * Y.  stats = (max, sum p).
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_ptr,
+              const int* __restrict__ col, const float4* __restrict__ Y,
+              const float* __restrict__ s_src, const float* __restrict__ s_dst,
+              float4* __restrict__ Z, float* __restrict__ stats) {
+  constexpr int LPR = D / 4;
+  constexpr int NS = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % LPR, sid = lane / LPR;
+  long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int dh4 = (D / H) / 4;            // lanes per head
+  const int h = sl / dh4;
+  const int b = row_ptr[row], e = row_ptr[row + 1];
+  const float sd = s_dst[row * H + h];
+  float m = -INFINITY;
+  for (int base = b; base < e; base += 32) {
+    const int n = min(32, e - base);
+    const int my_col = lane < n ? __ldg(col + base + lane) : 0;
+    for (int k = 0; k < n; k += NS) {
+      int idx = k + sid;
+      int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+      if (idx < n) m = fmaxf(m, leaky(__ldg(s_src + (long long)c * H + h) + sd, slope));
+    }
+  }
+  // all streams agree on the max
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float l = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = b; base < e; base += 32) {
+    const int n = min(32, e - base);
+    const int my_col = lane < n ? __ldg(col + base + lane) : 0;
+    int k = 0;
+    for (; k + NS * kUnroll <= n; k += NS * kUnroll) {
+      float4 v[kUnroll];
+      float sc[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        int c = __shfl_sync(0xffffffffu, my_col, k + u * NS + sid);
+        v[u] = ldg4(Y + (long long)c * LPR + sl);
+        sc[u] = __ldg(s_src + (long long)c * H + h);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        float p = expf(leaky(sc[u] + sd, slope) - m);
+        l += p;
+        acc = f4fma(p, v[u], acc);
+      }
+    }
+    for (; k < n; k += NS) {
+      int idx = k + sid;
+      int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+      if (idx < n) {
+        float p = expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - m);
+        l += p;
+        acc = f4fma(p, ldg4(Y + (long long)c * LPR + sl), acc);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) {
+    acc = f4add(acc, f4shfl_xor(acc, o));
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+  }
+  if (sid == 0) {
+    if (e > b) {
+      acc = make_float4(__fdiv_rn(acc.x, l), __fdiv_rn(acc.y, l), __fdiv_rn(acc.z, l),
+                        __fdiv_rn(acc.w, l));
+    } else {
+      m = 0.f;
+      l = 0.f;
+    }
+    Z[row * LPR + sl] = acc;
+    if (sl % dh4 == 0) {
+      stats[row * 2 * H + h] = m;
+      stats[row * 2 * H + H + h] = l;
+    }
+  }
+}
+
+// ---------------------------------------------------- backward SUM/MEAN (CSC)
+// dY[u] = sum_{q in column u} w(row_q) G[row_q + shift(r(u))]; all rows of a
+// column belong to Y row u's relation r(u), found once per warp.
+struct BwdMeta {
+  int R;
+  int shift[HF_MAX_R];   // type_dst_off[t(r)] - rel_row_off[r]
+};
+
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __restrict__ rel_y_off,
+          const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
+          const int* __restrict__ row_ptr, const float4* __restrict__ G, float4* __restrict__ dY) {
+  constexpr int LPR = D / 4;
+  constexpr int NS = 32 / LPR;
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % LPR, sid = lane / LPR;
+  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (u >= *U_dev) return;
+  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
+  const int shift = bm.shift[r];
+  const int b = col_ptr[u], e = col_ptr[u + 1];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = b; base < e; base += 32) {
+    const int n = min(32, e - base);
+    int my_row = 0;
+    float my_w = 1.f;
+    if (lane < n) {
+      my_row = __ldg(csc_row + base + lane);
+      if (MEAN) my_w = 1.f / (float)(__ldg(row_ptr + my_row + 1) - __ldg(row_ptr + my_row));
+    }
+    int k = 0;
+    for (; k + NS * kUnroll <= n; k += NS * kUnroll) {
+      float4 v[kUnroll];
+      float w[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; q++) {
+        int src_lane = k + q * NS + sid;
+        int rr = __shfl_sync(0xffffffffu, my_row, src_lane);
+        w[q] = __shfl_sync(0xffffffffu, my_w, src_lane);
+        v[q] = ldg4(G + (long long)(rr + shift) * LPR + sl);
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; q++) acc = MEAN ? f4fma(w[q], v[q], acc) : f4add(acc, v[q]);
+    }
+    for (; k < n; k += NS) {
+      int idx = k + sid;
+      int src_lane = idx < n ? idx : 0;
+      int rr = __shfl_sync(0xffffffffu, my_row, src_lane);
+      float w = __shfl_sync(0xffffffffu, my_w, src_lane);
+      if (idx < n) {
+        float4 v = ldg4(G + (long long)(rr + shift) * LPR + sl);
+        acc = MEAN ? f4fma(w, v, acc) : f4add(acc, v);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
+  if (sid == 0) dY[(long long)u * LPR + sl] = acc;
+}
+
+// ------------------------------------------------ backward GAT, pass 1 (rows)
+// For row m=(r,i), head h, with g = G[g(m)] and alpha_p recomputed from stats:
+//   dalpha_p = <g_h, Y[col_p]_h>,  za = sum_p alpha_p dalpha_p,
+//   dpre_p   = alpha_p (dalpha_p - za) LeakyReLU'(pre_p),  ds_dst[m,h] = sum_p dpre_p.
+// alpha and dpre are stored per CSR position for pass 2.
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long rows, int H,
+                   float slope, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                   const float4* __restrict__ Y, const float* __restrict__ s_src,
+                   const float* __restrict__ s_dst, const float* __restrict__ stats,
+                   const float4* __restrict__ G, float* __restrict__ alpha,
+                   float* __restrict__ dpre, float* __restrict__ ds_dst) {
+  constexpr int LPR = D / 4;
+  constexpr int NS = 32 / LPR;
+  __shared__ int s_roff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_roff[i] = rel_row_off_d[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % LPR, sid = lane / LPR;
+  long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int dh4 = (D / H) / 4;
+  const int h = sl / dh4;
+  const bool head_lead = (sl % dh4) == 0;
+  const int b = row_ptr[row], e = row_ptr[row + 1];
+  if (e == b) {
+    if (sid == 0 && head_lead) ds_dst[row * H + h] = 0.f;
+    return;
+  }
+  const int r = upper_bound_i(s_roff, bm.R + 1, (int)row) - 1;
+  const float4 g = ldg4(G + (row + bm.shift[r]) * LPR + sl);
+  const float sd = s_dst[row * H + h];
+  const float mx = stats[row * 2 * H + h];
+  const float inv_l = 1.f / stats[row * 2 * H + H + h];
+  float za = 0.f;
+  for (int base = b; base < e; base += 32) {
+    const int n = min(32, e - base);
+    const int my_col = lane < n ? __ldg(col + base + lane) : 0;
+    for (int k = 0; k < n; k += NS) {
+      int idx = k + sid;
+      int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+      float part = 0.f, a = 0.f;
+      if (idx < n) {
+        float4 y = ldg4(Y + (long long)c * LPR + sl);
+        part = g.x * y.x + g.y * y.y + g.z * y.z + g.w * y.w;
+        a = expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - mx) * inv_l;
+      }
+      for (int o = 1; o < dh4; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (idx < n) {
+        za += a * part;
+        if (head_lead) {
+          alpha[(long long)(base + idx) * H + h] = a;
+          dpre[(long long)(base + idx) * H + h] = part;   // dalpha, overwritten below
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) za += __shfl_xor_sync(0xffffffffu, za, o);
+  __syncwarp();
+  float dsd = 0.f;
+  if (head_lead) {
+    for (int p = b + sid; p < e; p += NS) {
+      int c = __ldg(col + p);
+      float pre = __ldg(s_src + (long long)c * H + h) + sd;
+      float a = alpha[(long long)p * H + h];
+      float da = dpre[(long long)p * H + h];
+      float dp = a * (da - za) * (pre > 0.f ? 1.f : slope);
+      dpre[(long long)p * H + h] = dp;
+      dsd += dp;
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) dsd += __shfl_xor_sync(0xffffffffu, dsd, o);
+  if (sid == 0 && head_lead) ds_dst[row * H + h] = dsd;
+}
+
+// ------------------------------------------------- backward GAT, pass 2 (CSC)
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
+                   const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
+                   const int* __restrict__ csc_pos, const int* __restrict__ csc_row,
+                   const float* __restrict__ alpha, const float* __restrict__ dpre,
+                   const float4* __restrict__ G, float4* __restrict__ dY,
+                   float* __restrict__ ds_src) {
+  constexpr int LPR = D / 4;
+  constexpr int NS = 32 / LPR;
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % LPR, sid = lane / LPR;
+  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (u >= *U_dev) return;
+  const int dh4 = (D / H) / 4;
+  const int h = sl / dh4;
+  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
+  const int shift = bm.shift[r];
+  const int b = col_ptr[u], e = col_ptr[u + 1];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float dss = 0.f;
+  for (int base = b; base < e; base += 32) {
+    const int n = min(32, e - base);
+    int my_row = 0, my_pos = 0;
+    if (lane < n) {
+      my_row = __ldg(csc_row + base + lane);
+      my_pos = __ldg(csc_pos + base + lane);
+    }
+    for (int k = 0; k < n; k += NS) {
+      int idx = k + sid;
+      int src_lane = idx < n ? idx : 0;
+      int rr = __shfl_sync(0xffffffffu, my_row, src_lane);
+      int p = __shfl_sync(0xffffffffu, my_pos, src_lane);
+      if (idx < n) {
+        float a = __ldg(alpha + (long long)p * H + h);
+        dss += __ldg(dpre + (long long)p * H + h);
+        acc = f4fma(a, ldg4(G + (long long)(rr + shift) * LPR + sl), acc);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) {
+    acc = f4add(acc, f4shfl_xor(acc, o));
+    dss += __shfl_xor_sync(0xffffffffu, dss, o);
+  }
+  if (sid == 0) {
+    dY[(long long)u * LPR + sl] = acc;
+    if (sl % dh4 == 0) ds_src[(long long)u * H + h] = dss;
+  }
+}
+
+static bool heads_ok(int D, int H) {
+  if (H <= 0 || D % H) return false;
+  int dh = D / H;
+  return dh % 4 == 0 && (dh & (dh - 1)) == 0;
+}
+
+}  // namespace hf
+
+using namespace hf;
+
+extern "C" {
+
+hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_agg agg, int D,
+                                   int heads, float slope, const float* d_Y, const float* d_s_src,
+                                   const float* d_s_dst, float* d_Z, float* d_stats,
+                                   hifuse_stream_t stream) {
+  if (!csr || rows < 0 || !csr->row_ptr || (rows > 0 && (!d_Z || !csr->col || !d_Y)))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (D != 64 && D != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!aligned16(d_Y) || !aligned16(d_Z)) return HIFUSE_ERR_ALIGNMENT;
+  cudaStream_t s = st(stream);
+  unsigned grid = ceil_div(rows, kWarpsPerBlock);
+  const int TB = kWarpsPerBlock * 32;
+  if (agg == HIFUSE_AGG_GAT) {
+    if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
+    if (rows > 0 && (!d_s_src || !d_s_dst || !d_stats)) return HIFUSE_ERR_INVALID_ARG;
+    if (D == 128)
+      HF_LAUNCH(k_agg_fwd_gat<128>, grid, TB, 0, s, (long long)rows, heads, slope, csr->row_ptr,
+                csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z, d_stats);
+    else
+      HF_LAUNCH(k_agg_fwd_gat<64>, grid, TB, 0, s, (long long)rows, heads, slope, csr->row_ptr,
+                csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z, d_stats);
+  } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
+    bool mean = agg == HIFUSE_AGG_MEAN;
+#define HF_AGG(DD, MM)                                                                   \
+  HF_LAUNCH((k_agg_fwd<DD, MM>), grid, TB, 0, s, (long long)rows, csr->row_ptr, csr->col, \
+            (const float4*)d_Y, (float4*)d_Z)
+    if (D == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
+    else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }
+#undef HF_AGG
+  } else {
+    return HIFUSE_ERR_INVALID_ARG;
+  }
+  return last_cuda();
+}
+
+size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg agg, int heads) {
+  LayerMeta m;
+  if (make_meta(shape, &m) != HIFUSE_OK) return 0;
+  if (agg != HIFUSE_AGG_GAT) return 256;
+  return 2 * carve_bytes((long long)m.N * heads, 4);
+}
+
+hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                   hifuse_agg agg, int D, int heads, float slope,
+                                   const float* d_G, const float* d_Y, const float* d_s_src,
+                                   const float* d_s_dst, const float* d_stats, float* d_dY,
+                                   float* d_ds_src, float* d_ds_dst, void* d_ws, size_t ws_bytes,
+                                   hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!csr || !csr->col_ptr || !csr->csc_row || !csr->U_dev || !csr->rel_y_off || !d_dY || !d_G)
+    return HIFUSE_ERR_INVALID_ARG;
+  if (D != 64 && D != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!aligned16(d_G) || !aligned16(d_dY)) return HIFUSE_ERR_ALIGNMENT;
+  cudaStream_t s = st(stream);
+  BwdMeta bm;
+  bm.R = m.R;
+  for (int r = 0; r < m.R; r++) bm.shift[r] = m.type_dst_off[m.rel_dst[r]] - m.rel_row_off[r];
+  long long U_max = m.N < m.S ? m.N : m.S;
+  unsigned gridU = ceil_div(U_max, kWarpsPerBlock);
+  const int TB = kWarpsPerBlock * 32;
+  if (agg == HIFUSE_AGG_GAT) {
+    if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
+    if (!d_Y || !d_s_src || !d_s_dst || !d_stats || !d_ds_src || !d_ds_dst || !csr->csc_pos ||
+        !csr->row_ptr || !csr->col || !csr->rel_row_off)
+      return HIFUSE_ERR_INVALID_ARG;
+    if (ws_bytes < hifuse_aggregate_bwd_ws_bytes(shape, agg, heads) || (!d_ws && m.N > 0))
+      return HIFUSE_ERR_WORKSPACE;
+    char* p = (char*)d_ws;
+    float* alpha = carve<float>(p, (long long)m.N * heads);
+    float* dpre = carve<float>(p, (long long)m.N * heads);
+    unsigned gridR = ceil_div(m.rows, kWarpsPerBlock);
+    if (D == 128) {
+      HF_LAUNCH(k_agg_bwd_gat_rows<128>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows,
+                heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,
+                d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);
+      HF_LAUNCH(k_agg_bwd_gat_cols<128>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,
+                csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,
+                (float4*)d_dY, d_ds_src);
+    } else {
+      HF_LAUNCH(k_agg_bwd_gat_rows<64>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows,
+                heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,
+                d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);
+      HF_LAUNCH(k_agg_bwd_gat_cols<64>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,
+                csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,
+                (float4*)d_dY, d_ds_src);
+    }
+  } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
+    if (agg == HIFUSE_AGG_MEAN && !csr->row_ptr) return HIFUSE_ERR_INVALID_ARG;
+#define HF_BWD(DD, MM)                                                                      \
+  HF_LAUNCH((k_agg_bwd<DD, MM>), gridU, TB, 0, s, bm, (int)U_max, csr->U_dev, csr->rel_y_off, \
+            csr->col_ptr, csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY)
+    bool mean = agg == HIFUSE_AGG_MEAN;
+    if (D == 128) { if (mean) HF_BWD(128, true); else HF_BWD(128, false); }
+    else { if (mean) HF_BWD(64, true); else HF_BWD(64, false); }
+#undef HF_BWD
+  } else {
+    return HIFUSE_ERR_INVALID_ARG;
+  }
+  return last_cuda();
+}
+
+}  // extern "C"

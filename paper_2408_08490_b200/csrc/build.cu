@@ -1,0 +1,361 @@
+// build.cu -- A1: semantic graph build (Alg. 2) as a
+// merged segmented CSR + CSC, on the GPU, with a kernel count independent of
+// the number of relations R.
+//
+// Alg. 2 runs, per layer, 1 gather (line 316) + R compares (318) + R
+// index-selects (319): 2R+1 short kernels that the paper offloads to the CPU
+// (lines 299-336).  Here the relation of each edge only decides a KEY,
+//   key(e) = rel_row_off[r(e)] + dst(e)      (merged row, relation-major),
+// and one counting sort by key performs every relation's selection at once:
+//   k_classify   EdgeTypeLayer gather + validation + row histogram + source
+//                presence flags per (relation, source) slot
+//   scan         row_ptr and the compact Y-row numbering (one scan over both)
+//   k_finish     rel_y_off, y_src, slot_y, U
+//   k_scatter    unstable atomic placement into rows + column histogram
+//   scan         col_ptr
+//   k_rows       per row: sort by original column (restores Alg. 2's
+//                column order, so the result is bit-exact and deterministic),
+//                then CSC placement
+//   k_cols       per Y row: sort CSC entries by CSR position
+//   k_*_long     the same two sorts for segments longer than 32 (block-wide)
+#include <vector>
+#include "common.cuh"
+
+namespace hf {
+
+static constexpr int kShort = 32;        // segments up to this length: one thread
+static constexpr int kLongCap = 8192;    // block bitonic in shared memory up to this
+
+__global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* __restrict__ dst,
+                           const long long* __restrict__ eid, const int* __restrict__ edge_type,
+                           long long E, int* __restrict__ key_e, int* __restrict__ slot_e,
+                           int* __restrict__ cnt, int* __restrict__ status) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m.N) return;
+  long long id = eid[e];
+  int bad = 0, r = -1;
+  int s = src[e], d = dst[e];
+  if (id < 0 || id >= E) {
+    bad = HIFUSE_ST_BAD_EDGE_ID;
+  } else {
+    r = edge_type[id];                                   // Alg. 2
+    if (r < 0 || r >= m.R) bad = HIFUSE_ST_BAD_REL;
+    else if (s < 0 || s >= m.n_src[m.rel_src[r]]) bad = HIFUSE_ST_BAD_SRC;
+    else if (d < 0 || d >= m.n_dst[m.rel_dst[r]]) bad = HIFUSE_ST_BAD_DST;
+  }
+  if (bad) {
+    atomicOr(status, bad);
+    key_e[e] = -1;
+    return;
+  }
+  int key = m.rel_row_off[r] + d;                        // lines 318-319, all r at once
+  int slot = m.slot_off[r] + s;
+  key_e[e] = key;
+  slot_e[e] = slot;
+  atomicAdd(&cnt[key], 1);
+  cnt[m.rows + slot] = 1;                                // presence flag (idempotent)
+}
+
+// pre = exclusive scan of [row counts | slot flags]; pre[rows] = valid edges,
+// pre[rows + S] - pre[rows] = U.
+__global__ void k_finish(LayerMeta m, const int* __restrict__ cnt, const int* __restrict__ pre,
+                         int* __restrict__ row_ptr, int* __restrict__ rel_row_off,
+                         int* __restrict__ rel_y_off, int* __restrict__ y_src,
+                         int* __restrict__ slot_y, int* __restrict__ U_dev) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int nvalid = pre[m.rows];
+  if (i <= m.rows) row_ptr[i] = pre[i];
+  if (i < m.S) {
+    int u = -1;
+    if (cnt[m.rows + i]) {
+      u = pre[m.rows + i] - nvalid;
+      int r = upper_bound_i(m.slot_off, m.R + 1, i) - 1;
+      y_src[u] = i - m.slot_off[r];
+    }
+    slot_y[i] = u;
+  }
+  if (i <= m.R) {
+    rel_row_off[i] = m.rel_row_off[i];
+    rel_y_off[i] = pre[m.rows + m.slot_off[i]] - nvalid;
+  }
+  if (i == 0) U_dev[0] = pre[m.rows + m.S] - nvalid;
+}
+
+__global__ void k_scatter(LayerMeta m, const int* __restrict__ key_e, const int* __restrict__ slot_e,
+                          const int* __restrict__ row_ptr, const int* __restrict__ slot_y,
+                          int* __restrict__ cur, int* __restrict__ ccnt, int* __restrict__ eperm,
+                          int* __restrict__ col, int* __restrict__ csc_pos,
+                          int* __restrict__ csc_row) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m.N) return;
+  int nvalid = row_ptr[m.rows];
+  if (e >= nvalid) {  // tail positions [nvalid, N): exactly one writer each
+    eperm[e] = -1; col[e] = -1; csc_pos[e] = -1; csc_row[e] = -1;
+  }
+  int key = key_e[e];
+  if (key < 0) return;
+  int pos = row_ptr[key] + atomicAdd(&cur[key], 1);
+  int c = slot_y[slot_e[e]];
+  eperm[pos] = e;
+  col[pos] = c;
+  atomicAdd(&ccnt[c], 1);
+}
+
+// Insertion sort of keys[0..n) ascending, carrying vals (n <= kShort).
+__device__ __forceinline__ void thread_sort(int* keys, int* vals, int n) {
+  for (int i = 1; i < n; i++) {
+    int k = keys[i], v = vals[i];
+    int j = i - 1;
+    while (j >= 0 && keys[j] > k) {
+      keys[j + 1] = keys[j];
+      vals[j + 1] = vals[j];
+      j--;
+    }
+    keys[j + 1] = k;
+    vals[j + 1] = v;
+  }
+}
+
+// Block-wide sort of one long segment (unique keys).  Shared-memory bitonic
+// up to kLongCap, else rank sort through the scratch buffers.
+__device__ void block_sort(int* keys, int* vals, int n, int* sk, int* sv, int* gk, int* gv) {
+  if (n <= kLongCap) {
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      sk[i] = i < n ? keys[i] : 0x7fffffff;
+      sv[i] = i < n ? vals[i] : 0;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          int l = i ^ j;
+          if (l > i) {
+            bool up = (i & k) == 0;
+            int a = sk[i], b = sk[l];
+            if ((a > b) == up) {
+              sk[i] = b; sk[l] = a;
+              int t = sv[i]; sv[i] = sv[l]; sv[l] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      keys[i] = sk[i];
+      vals[i] = sv[i];
+    }
+    __syncthreads();
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int k = keys[i], rank = 0;
+    for (int j = 0; j < n; j++) rank += keys[j] < k;
+    gk[rank] = k;
+    gv[rank] = vals[i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    keys[i] = gk[i];
+    vals[i] = gv[i];
+  }
+  __syncthreads();
+}
+
+// Scatter one sorted CSR row into the CSC (atomic slot, fixed up by k_cols).
+__device__ __forceinline__ void csc_place(int row, int b, int e_, const int* col,
+                                          const int* col_ptr, int* ccur, int* csc_pos,
+                                          int* csc_row, int step, int first) {
+  for (int p = b + first; p < e_; p += step) {
+    int c = col[p];
+    int w = col_ptr[c] + atomicAdd(&ccur[c], 1);
+    csc_pos[w] = p;
+    csc_row[w] = row;
+  }
+}
+
+__global__ void k_rows(int rows, const int* __restrict__ row_ptr, int* eperm, int* col,
+                       const int* __restrict__ col_ptr, int* ccur, int* csc_pos, int* csc_row,
+                       int* long_list, int* long_cnt) {
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  int b = row_ptr[row], e_ = row_ptr[row + 1];
+  if (e_ - b > kShort) {
+    long_list[atomicAdd(long_cnt, 1)] = row;
+    return;
+  }
+  thread_sort(eperm + b, col + b, e_ - b);
+  csc_place(row, b, e_, col, col_ptr, ccur, csc_pos, csc_row, 1, 0);
+}
+
+__global__ void k_rows_long(const int* __restrict__ row_ptr, int* eperm, int* col,
+                            const int* __restrict__ col_ptr, int* ccur, int* csc_pos,
+                            int* csc_row, const int* long_list, const int* long_cnt, int* gk,
+                            int* gv) {
+  extern __shared__ int smem[];
+  int n_long = *long_cnt;
+  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
+    int row = long_list[k];
+    int b = row_ptr[row], e_ = row_ptr[row + 1];
+    block_sort(eperm + b, col + b, e_ - b, smem, smem + kLongCap, gk + b, gv + b);
+    csc_place(row, b, e_, col, col_ptr, ccur, csc_pos, csc_row, blockDim.x, threadIdx.x);
+    __syncthreads();
+  }
+}
+
+__global__ void k_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* csc_pos,
+                       int* csc_row, int* long_list, int* long_cnt) {
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= *U_dev) return;
+  int b = col_ptr[u], e_ = col_ptr[u + 1];
+  if (e_ - b > kShort) {
+    long_list[atomicAdd(long_cnt, 1)] = u;
+    return;
+  }
+  thread_sort(csc_pos + b, csc_row + b, e_ - b);
+}
+
+__global__ void k_cols_long(const int* __restrict__ col_ptr, int* csc_pos, int* csc_row,
+                            const int* long_list, const int* long_cnt, int* gk, int* gv) {
+  extern __shared__ int smem[];
+  int n_long = *long_cnt;
+  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
+    int u = long_list[k];
+    int b = col_ptr[u], e_ = col_ptr[u + 1];
+    block_sort(csc_pos + b, csc_row + b, e_ - b, smem, smem + kLongCap, gk + b, gv + b);
+  }
+}
+
+struct BuildWs {
+  int *cnt, *pre, *key_e, *slot_e, *cur, *ccnt, *ccur, *scan, *lists, *counters, *gk, *gv;
+};
+
+static size_t build_ws(const LayerMeta& m, long long U_max, char* base, BuildWs* w) {
+  long long nz = (long long)m.rows + m.S;
+  long long sc = (long long)scan_ws_ints(nz > U_max ? nz : U_max);
+  size_t b = 0;
+  b += carve_bytes(nz, 4);              // cnt
+  b += carve_bytes(nz + 1, 4);          // pre
+  b += carve_bytes(m.N, 4) * 2;         // key_e, slot_e
+  b += carve_bytes(m.rows, 4);          // cur
+  b += carve_bytes(U_max + 1, 4) * 2;   // ccnt, ccur
+  b += carve_bytes(sc, 4);              // scan
+  b += carve_bytes((long long)m.rows + U_max, 4);  // long lists
+  b += carve_bytes(2, 4);               // counters
+  b += carve_bytes(m.N, 4) * 2;         // gk, gv
+  if (base && w) {
+    char* p = base;
+    w->cnt = carve<int>(p, nz);
+    w->pre = carve<int>(p, nz + 1);
+    w->key_e = carve<int>(p, m.N);
+    w->slot_e = carve<int>(p, m.N);
+    w->cur = carve<int>(p, m.rows);
+    w->ccnt = carve<int>(p, U_max + 1);
+    w->ccur = carve<int>(p, U_max + 1);
+    w->scan = carve<int>(p, sc);
+    w->lists = carve<int>(p, (long long)m.rows + U_max);
+    w->counters = carve<int>(p, 2);
+    w->gk = carve<int>(p, m.N);
+    w->gv = carve<int>(p, m.N);
+  }
+  return b;
+}
+
+static long long umax_of(const LayerMeta& m) { return m.N < m.S ? m.N : m.S; }
+
+}  // namespace hf
+
+using namespace hf;
+
+extern "C" {
+
+hifuse_status hifuse_csr_sizes(const hifuse_layer_shape* shape, hifuse_layout layout,
+                               int64_t* rows, int64_t* U_max, int64_t* S, size_t* ws_bytes) {
+  if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
+  LayerMeta m;
+  hifuse_status st = make_meta(shape, &m);
+  if (st != HIFUSE_OK) return st;
+  if (rows) *rows = m.rows;
+  if (U_max) *U_max = umax_of(m);
+  if (S) *S = m.S;
+  if (ws_bytes) *ws_bytes = build_ws(m, umax_of(m), nullptr, nullptr);
+  return HIFUSE_OK;
+}
+
+hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int num_layers,
+                                           const int32_t* const* d_src_local,
+                                           const int32_t* const* d_dst_local,
+                                           const int64_t* const* d_edge_id,
+                                           const int32_t* d_edge_type, int64_t num_graph_edges,
+                                           hifuse_layout layout, const hifuse_csr* out,
+                                           void* d_ws, size_t ws_bytes, int32_t* d_status,
+                                           hifuse_stream_t stream) {
+  if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
+  if (!shapes || num_layers <= 0 || !d_src_local || !d_dst_local || !d_edge_id || !out ||
+      !d_status || num_graph_edges < 0 || (num_graph_edges > 0 && !d_edge_type))
+    return HIFUSE_ERR_INVALID_ARG;
+  cudaStream_t s = st(stream);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_rows_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2 * kLongCap * (int)sizeof(int));
+    cudaFuncSetAttribute(k_cols_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2 * kLongCap * (int)sizeof(int));
+    attr_done = true;
+  }
+  std::vector<LayerMeta> metas(num_layers);
+  LayerMeta* mv = metas.data();
+  hifuse_status rc = HIFUSE_OK;
+  for (int l = 0; l < num_layers && rc == HIFUSE_OK; l++) {
+    rc = make_meta(&shapes[l], &mv[l]);
+    if (rc != HIFUSE_OK) break;
+    const hifuse_csr& o = out[l];
+    if (!o.rel_row_off || !o.row_ptr || !o.rel_y_off || !o.U_dev ||
+        (mv[l].N > 0 && (!d_src_local[l] || !d_dst_local[l] || !d_edge_id[l] || !o.col ||
+                         !o.eperm || !o.y_src || !o.col_ptr || !o.csc_pos || !o.csc_row)) ||
+        (mv[l].S > 0 && !o.slot_y))
+      rc = HIFUSE_ERR_INVALID_ARG;
+    else if (build_ws(mv[l], umax_of(mv[l]), nullptr, nullptr) > ws_bytes || !d_ws)
+      rc = HIFUSE_ERR_WORKSPACE;
+  }
+  if (rc != HIFUSE_OK) return rc;
+  for (int l = 0; l < num_layers; l++) {
+    const LayerMeta& m = mv[l];
+    const hifuse_csr& o = out[l];
+    long long U_max = umax_of(m);
+    BuildWs w;
+    build_ws(m, U_max, (char*)d_ws, &w);
+    long long nz = (long long)m.rows + m.S;
+    cudaMemsetAsync(w.cnt, 0, sizeof(int) * (nz > 0 ? nz : 1), s);
+    cudaMemsetAsync(w.cur, 0, sizeof(int) * (m.rows > 0 ? m.rows : 1), s);
+    cudaMemsetAsync(w.ccnt, 0, sizeof(int) * (U_max + 1), s);
+    cudaMemsetAsync(w.ccur, 0, sizeof(int) * (U_max + 1), s);
+    cudaMemsetAsync(w.counters, 0, sizeof(int) * 2, s);
+    const int TB = 256;
+    HF_LAUNCH(k_classify, ceil_div(m.N, TB), TB, 0, s, m, d_src_local[l], d_dst_local[l],
+              (const long long*)d_edge_id[l], d_edge_type, (long long)num_graph_edges, w.key_e,
+              w.slot_e, w.cnt, d_status);
+    exclusive_scan(w.cnt, w.pre, nz, w.scan, s);
+    long long fin = nz + 1 > m.R + 1 ? nz + 1 : m.R + 1;
+    HF_LAUNCH(k_finish, ceil_div(fin, TB), TB, 0, s, m, w.cnt, w.pre, o.row_ptr, o.rel_row_off,
+              o.rel_y_off, o.y_src, o.slot_y, o.U_dev);
+    HF_LAUNCH(k_scatter, ceil_div(m.N, TB), TB, 0, s, m, w.key_e, w.slot_e, o.row_ptr, o.slot_y,
+              w.cur, w.ccnt, o.eperm, o.col, o.csc_pos, o.csc_row);
+    exclusive_scan(w.ccnt, o.col_ptr, U_max, w.scan, s);
+    int* rows_long = w.lists;
+    int* cols_long = w.lists + m.rows;
+    const int smem = 2 * kLongCap * sizeof(int);
+    HF_LAUNCH(k_rows, ceil_div(m.rows, TB), TB, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
+              o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
+    HF_LAUNCH(k_rows_long, 148, 256, smem, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
+              o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv);
+    HF_LAUNCH(k_cols, ceil_div(U_max, TB), TB, 0, s, o.U_dev, o.col_ptr, o.csc_pos, o.csc_row,
+              cols_long, w.counters + 1);
+    HF_LAUNCH(k_cols_long, 148, 256, smem, s, o.col_ptr, o.csc_pos, o.csc_row, cols_long,
+              w.counters + 1, w.gk, w.gv);
+  }
+  return last_cuda();
+}
+
+}  // extern "C"

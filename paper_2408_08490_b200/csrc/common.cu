@@ -1,0 +1,182 @@
+// common.cu -- layer metadata, device-wide scan, status helpers.
+#include "common.cuh"
+
+namespace hf {
+
+std::atomic<int64_t> g_launches{0};
+
+hifuse_status make_meta(const hifuse_layer_shape* s, LayerMeta* m) {
+  if (!s || !m) return HIFUSE_ERR_INVALID_ARG;
+  if (s->num_types <= 0 || s->num_types > HF_MAX_T) return HIFUSE_ERR_UNSUPPORTED;
+  if (s->num_rels <= 0 || s->num_rels > HF_MAX_R) return HIFUSE_ERR_UNSUPPORTED;
+  if (!s->rel_src_type_h || !s->rel_dst_type_h || !s->n_src_h || !s->n_dst_h)
+    return HIFUSE_ERR_INVALID_ARG;
+  if (s->num_edges < 0 || s->num_edges >= (1ll << 31)) return HIFUSE_ERR_INVALID_ARG;
+  m->T = s->num_types;
+  m->R = s->num_rels;
+  m->N = (int)s->num_edges;
+  long long so = 0, dof = 0;
+  for (int t = 0; t < m->T; t++) {
+    int ns = s->n_src_h[t], nd = s->n_dst_h[t];
+    if (ns < 0 || nd < 0 || nd > ns) return HIFUSE_ERR_INVALID_ARG;
+    m->n_src[t] = ns;
+    m->n_dst[t] = nd;
+    m->type_src_off[t] = (int)so;
+    m->type_dst_off[t] = (int)dof;
+    so += ns;
+    dof += nd;
+  }
+  m->type_src_off[m->T] = (int)so;
+  m->type_dst_off[m->T] = (int)dof;
+  long long rows = 0, S = 0;
+  for (int r = 0; r < m->R; r++) {
+    int a = s->rel_src_type_h[r], b = s->rel_dst_type_h[r];
+    if (a < 0 || a >= m->T || b < 0 || b >= m->T) return HIFUSE_ERR_INVALID_ARG;
+    m->rel_src[r] = a;
+    m->rel_dst[r] = b;
+    m->rel_row_off[r] = (int)rows;
+    m->slot_off[r] = (int)S;
+    rows += m->n_dst[b];
+    S += m->n_src[a];
+  }
+  m->rel_row_off[m->R] = (int)rows;
+  m->slot_off[m->R] = (int)S;
+  if (so >= (1ll << 31) || rows >= (1ll << 31) || S >= (1ll << 31)) return HIFUSE_ERR_UNSUPPORTED;
+  m->rows = (int)rows;
+  m->S = (int)S;
+  m->src_rows = (int)so;
+  m->dst_rows = (int)dof;
+  return HIFUSE_OK;
+}
+
+// ------------------------------------------------------------------ scan ---
+static constexpr int kScanThreads = 256;
+static constexpr int kScanItems = 16;
+static constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix and writes the block total to *total.
+__device__ __forceinline__ int block_excl_scan(int v, int* total) {
+  __shared__ int warp_sums[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = warp_incl_scan(v);
+  if (lane == 31) warp_sums[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int s = lane < kScanThreads / 32 ? warp_sums[lane] : 0;
+    s = warp_incl_scan(s);
+    if (lane < kScanThreads / 32) warp_sums[lane] = s;
+  }
+  __syncthreads();
+  int base = w ? warp_sums[w - 1] : 0;
+  *total = warp_sums[kScanThreads / 32 - 1];
+  __syncthreads();
+  return base + inc - v;
+}
+
+__global__ void k_scan_reduce(const int* __restrict__ in, long long n, int* __restrict__ bsum) {
+  long long base = (long long)blockIdx.x * kScanTile;
+  int s = 0;
+  for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
+    long long k = base + i;
+    if (k < n) s += in[k];
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ int ws[kScanThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < kScanThreads / 32; i++) t += ws[i];
+    bsum[blockIdx.x] = t;
+  }
+}
+
+// Single block: exclusive scan of the nb block sums in place; bsum[nb] = total.
+__global__ void k_scan_bsums(int* bsum, int nb) {
+  int carry = 0;
+  for (int base = 0; base < nb; base += kScanThreads) {
+    int i = base + threadIdx.x;
+    int v = i < nb ? bsum[i] : 0;
+    int tot;
+    int ex = block_excl_scan(v, &tot);
+    if (i < nb) bsum[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) bsum[nb] = carry;
+}
+
+__global__ void k_scan_down(const int* __restrict__ in, long long n, const int* __restrict__ bsum,
+                            int* __restrict__ out, int nb) {
+  long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
+  int v[kScanItems];
+  int s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; j++) {
+    long long k = base + j;
+    v[j] = k < n ? in[k] : 0;
+    s += v[j];
+  }
+  int tot;
+  int ex = block_excl_scan(s, &tot) + bsum[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; j++) {
+    long long k = base + j;
+    if (k < n) out[k] = ex;
+    ex += v[j];
+  }
+  if (blockIdx.x == nb - 1 && threadIdx.x == 0) out[n] = bsum[nb];
+}
+
+__global__ void k_scan_empty(int* out) { out[0] = 0; }
+
+size_t scan_ws_ints(long long n) { return (size_t)ceil_div(n > 0 ? n : 1, kScanTile) + 1; }
+
+void exclusive_scan(const int* in, int* out, long long n, int* ws, cudaStream_t s) {
+  if (n <= 0) {
+    HF_LAUNCH(k_scan_empty, 1, 1, 0, s, out);
+    return;
+  }
+  int nb = (int)ceil_div(n, kScanTile);
+  HF_LAUNCH(k_scan_reduce, nb, kScanThreads, 0, s, in, n, ws);
+  HF_LAUNCH(k_scan_bsums, 1, kScanThreads, 0, s, ws, nb);
+  HF_LAUNCH(k_scan_down, nb, kScanThreads, 0, s, in, n, ws, out, nb);
+}
+
+}  // namespace hf
+
+extern "C" {
+
+const char* hifuse_status_string(hifuse_status s) {
+  switch (s) {
+    case HIFUSE_OK: return "ok";
+    case HIFUSE_ERR_INVALID_ARG: return "invalid argument";
+    case HIFUSE_ERR_ALIGNMENT: return "pointer not 16-byte aligned";
+    case HIFUSE_ERR_UNSUPPORTED: return "unsupported size or mode";
+    case HIFUSE_ERR_WORKSPACE: return "workspace too small";
+    case HIFUSE_ERR_CUDA: return "CUDA launch failed";
+  }
+  return "unknown status";
+}
+
+hifuse_status hifuse_read_status(const int32_t* d_status, hifuse_stream_t stream, int32_t* out_h) {
+  if (!d_status || !out_h) return HIFUSE_ERR_INVALID_ARG;
+  if (cudaMemcpyAsync(out_h, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, hf::st(stream)) !=
+      cudaSuccess)
+    return HIFUSE_ERR_CUDA;
+  return cudaStreamSynchronize(hf::st(stream)) == cudaSuccess ? HIFUSE_OK : HIFUSE_ERR_CUDA;
+}
+
+int64_t hifuse_kernel_launches(void) { return hf::g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// common.cuh -- shared device/host helpers of libhifuse (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <atomic>
+#include "hifuse.h"
+
+#define HF_MAX_T 64
+#define HF_MAX_R 256
+
+namespace hf {
+
+extern std::atomic<int64_t> g_launches;
+
+inline cudaStream_t st(hifuse_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Host-derived metadata of one layer, passed by value to kernels (kernel
+// parameter space is 32 KB on sm_70+ with CUDA >= 12.1; this is ~6 KB).
+struct LayerMeta {
+  int T, R;
+  int rows;            // sum_r n_dst(t(r))
+  int S;               // sum_r n_src(s(r))
+  int N;               // edges
+  int src_rows;        // sum_t n_src
+  int dst_rows;        // sum_t n_dst
+  int rel_src[HF_MAX_R];
+  int rel_dst[HF_MAX_R];
+  int rel_row_off[HF_MAX_R + 1];
+  int slot_off[HF_MAX_R + 1];
+  int n_src[HF_MAX_T];
+  int n_dst[HF_MAX_T];
+  int type_src_off[HF_MAX_T + 1];
+  int type_dst_off[HF_MAX_T + 1];
+};
+
+// Fills `m` from a public shape; returns HIFUSE_OK or an error code.
+hifuse_status make_meta(const hifuse_layer_shape* s, LayerMeta* m);
+
+inline hifuse_status last_cuda() {
+  return cudaGetLastError() == cudaSuccess ? HIFUSE_OK : HIFUSE_ERR_CUDA;
+}
+
+template <typename T>
+inline T* carve(char*& p, size_t n) {
+  T* r = reinterpret_cast<T*>(p);
+  size_t b = (n * sizeof(T) + 255) & ~size_t(255);
+  p += b;
+  return r;
+}
+inline size_t carve_bytes(size_t n, size_t elt) { return (n * elt + 255) & ~size_t(255); }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+#define HF_LAUNCH(kernel, grid, block, smem, stream, ...)                      \
+  do {                                                                         \
+    if ((grid) > 0) {                                                          \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+      hf::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
+    }                                                                          \
+  } while (0)
+
+// ---------------------------------------------------------------- device ---
+__device__ __forceinline__ int upper_bound_i(const int* a, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Device-wide exclusive scan of int32 counts (reduce-then-scan, 3 kernels).
+// out[0..n] receives the exclusive prefix, out[n] = total.  ws: scan_ws_ints(n).
+size_t scan_ws_ints(long long n);
+void exclusive_scan(const int* in, int* out, long long n, int* ws, cudaStream_t s);
+
+}  // namespace hf

@@ -1,0 +1,723 @@
+// project.cu -- A2+A3 feature projection and its backward.
+//
+// Groups: relation r (rows = the relation's compact Y rows, A = X_{s(r)} rows
+// gathered through y_src; B = W_rel[r]) and root type t (rows = the
+// destination prefix of type t, A = X_t rows, B = W_root[t]).  Layer 0 reads
+// A rows straight from the type-major global feature store through
+// gather_ids, so feature collection (A2, the paper's "reorganize and retrieve
+// features" kernel, line 219) is fused into the projection's A loads.
+//
+// This file holds the CUDA-core fp32 path (HIFUSE_PREC_FP32) and the
+// backward; the tcgen05 TF32 forward lives in project_tc.cu.
+#include "project.cuh"
+
+namespace hf {
+
+// ------------------------------------------------------------ group table --
+// tile_off[g] = first tile of group g (tiles of kBM rows), chunk_off[g] =
+// first wgrad chunk (kCH rows); groups: R relations then T root types.
+__global__ void k_group_table(ProjMeta pm, const int* __restrict__ rel_y_off, int* tile_off,
+                              int* chunk_off, int BM, int CH) {
+  if (threadIdx.x != 0) return;
+  int t_acc = 0, c_acc = 0;
+  for (int g = 0; g < pm.R + pm.T; g++) {
+    int rows = g < pm.R ? rel_y_off[g + 1] - rel_y_off[g] : (pm.has_root ? pm.n_dst[g - pm.R] : 0);
+    tile_off[g] = t_acc;
+    chunk_off[g] = c_acc;
+    t_acc += (rows + BM - 1) / BM;
+    c_acc += (rows + CH - 1) / CH;
+  }
+  tile_off[pm.R + pm.T] = t_acc;
+  chunk_off[pm.R + pm.T] = c_acc;
+}
+
+// Resolves tile/chunk `bid` to (group, first local row, row count).
+__device__ __forceinline__ bool resolve(const ProjMeta& pm, const int* table, const int* rel_y_off,
+                                        int bid, int step, int* g_out, int* r0, int* nrows) {
+  int G = pm.R + pm.T;
+  if (bid >= table[G]) return false;
+  int lo = 0, hi = G;   // last g with table[g] <= bid
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (table[mid] <= bid) lo = mid; else hi = mid;
+  }
+  // skip empty groups sharing the same start
+  while (lo + 1 < G && table[lo + 1] <= bid) lo++;
+  int g = lo;
+  int total = g < pm.R ? rel_y_off[g + 1] - rel_y_off[g] : pm.n_dst[g - pm.R];
+  int local0 = (bid - table[g]) * step;
+  *g_out = g;
+  *r0 = local0;
+  *nrows = min(step, total - local0);
+  return *nrows > 0;
+}
+
+// X row of the A operand for local row `j` of group g.
+__device__ __forceinline__ long long a_row(const ProjMeta& pm, const int* rel_y_off,
+                                           const int* y_src, const int* gather_ids, int g, int j) {
+  int x;
+  if (g < pm.R) x = pm.type_src_off[pm.rel_src[g]] + y_src[rel_y_off[g] + j];
+  else x = pm.type_src_off[g - pm.R] + j;
+  return gather_ids ? (long long)gather_ids[x] : (long long)x;
+}
+
+// ------------------------------------------------------ SIMT forward GEMM --
+// Tile: kBM x D outputs, 256 threads, each 4 rows x (D/16) cols, BK = 32.
+template <int K, int D>
+__global__ void __launch_bounds__(256)
+k_proj_fwd_simt(ProjMeta pm, const int* __restrict__ tile_off, const int* __restrict__ rel_y_off,
+                const int* __restrict__ y_src, const int* __restrict__ gather_ids,
+                const float* __restrict__ X, const float* __restrict__ W_rel,
+                const float* __restrict__ W_root, float* __restrict__ Y, float* __restrict__ R0) {
+  constexpr int BM = kBM, BK = 32, TN = D / 16;
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][D];
+  int g, r0, nrows;
+  if (!resolve(pm, tile_off, rel_y_off, blockIdx.x, BM, &g, &r0, &nrows)) return;
+  const int tid = threadIdx.x;
+  const float* W = g < pm.R ? W_rel + (long long)g * K * D : W_root + (long long)(g - pm.R) * K * D;
+  // A rows this thread loads: tid/8 and tid/8 + 32
+  long long xr[2];
+#pragma unroll
+  for (int i = 0; i < 2; i++) {
+    int rr = tid / 8 + 32 * i;
+    xr[i] = rr < nrows ? a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + rr) : -1;
+  }
+  const int ty = tid / 16, tx = tid % 16;
+  float acc[4][TN];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++) acc[i][j] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      int rr = tid / 8 + 32 * i, k4 = tid % 8;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (xr[i] >= 0) v = __ldg(reinterpret_cast<const float4*>(X + xr[i] * K + k0) + k4);
+      As[k4 * 4 + 0][rr] = v.x;
+      As[k4 * 4 + 1][rr] = v.y;
+      As[k4 * 4 + 2][rr] = v.z;
+      As[k4 * 4 + 3][rr] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < BK * D / 4 / 256; i++) {
+      int idx = tid + 256 * i;
+      int kr = idx / (D / 4), c4 = idx % (D / 4);
+      *reinterpret_cast<float4*>(&Bs[kr][c4 * 4]) =
+          __ldg(reinterpret_cast<const float4*>(W + (long long)(k0 + kr) * D) + c4);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < BK; kk++) {
+      float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      float av[4] = {a.x, a.y, a.z, a.w};
+      float bv[TN];
+#pragma unroll
+      for (int j = 0; j < TN / 4; j++) {
+        float4 b = *reinterpret_cast<const float4*>(&Bs[kk][j * 64 + tx * 4]);
+        bv[j * 4 + 0] = b.x; bv[j * 4 + 1] = b.y; bv[j * 4 + 2] = b.z; bv[j * 4 + 3] = b.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* out = g < pm.R ? Y + (long long)rel_y_off[g] * D
+                        : R0 + (long long)pm.type_dst_off[g - pm.R] * D;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    int rr = ty * 4 + i;
+    if (rr >= nrows) continue;
+#pragma unroll
+    for (int j = 0; j < TN / 4; j++)
+      *reinterpret_cast<float4*>(out + (long long)(r0 + rr) * D + j * 64 + tx * 4) =
+          make_float4(acc[i][j * 4], acc[i][j * 4 + 1], acc[i][j * 4 + 2], acc[i][j * 4 + 3]);
+  }
+}
+
+// ---------------------------------------------------------- RGAT scores ----
+// v[r][k][h] = sum_c W_r[k, h dh + c] a_dst[r, h, c]   (reading C7 fold)
+__global__ void k_att_fold(int R, int K, int D, int H, const float* __restrict__ W_rel,
+                           const float* __restrict__ att, float* __restrict__ v) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * K * H) return;
+  int h = idx % H, k = (idx / H) % K, r = idx / (H * K);
+  int dh = D / H;
+  const float* w = W_rel + ((long long)r * K + k) * D + h * dh;
+  const float* a = att + (long long)r * 2 * D + D + h * dh;
+  float s = 0.f;
+  for (int c = 0; c < dh; c++) s = fmaf(w[c], a[c], s);
+  v[idx] = s;
+}
+
+// s_src[u,h] = <Y[u, head h], a_src[r(u), head h]>, one warp per Y row.
+__global__ void k_scores_src(int R, int D, int H, const int* __restrict__ U_dev,
+                             const int* __restrict__ rel_y_off, const float* __restrict__ Y,
+                             const float* __restrict__ att, float* __restrict__ s_src) {
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (u >= *U_dev) return;
+  int r = upper_bound_i(s_yoff, R + 1, u) - 1;
+  const float* a = att + (long long)r * 2 * D;
+  int dh = D / H;
+  for (int h = 0; h < H; h++) {
+    float s = 0.f;
+    for (int c = lane; c < dh; c += 32) s = fmaf(Y[(long long)u * D + h * dh + c], a[h * dh + c], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) s_src[(long long)u * H + h] = s;
+  }
+}
+
+// s_dst[(r,i),h] = <X_{t(r)}[i], v[r][:,h]>, one warp per merged row.
+__global__ void k_scores_dst(ProjMeta pm, int K, int H, const int* __restrict__ gather_ids,
+                             const float* __restrict__ X, const float* __restrict__ v,
+                             float* __restrict__ s_dst) {
+  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (row >= pm.rows) return;
+  int r = upper_bound_i(pm.rel_row_off, pm.R + 1, row) - 1;
+  int t = pm.rel_dst[r];
+  int x = pm.type_src_off[t] + (row - pm.rel_row_off[r]);
+  long long xr = gather_ids ? (long long)gather_ids[x] : (long long)x;
+  float acc[HIFUSE_MAX_HEADS];
+  for (int h = 0; h < H; h++) acc[h] = 0.f;
+  for (int k = lane; k < K; k += 32) {
+    float xv = X[xr * K + k];
+    const float* vr = v + ((long long)r * K + k) * H;
+    for (int h = 0; h < H; h++) acc[h] = fmaf(xv, vr[h], acc[h]);
+  }
+  for (int h = 0; h < H; h++) {
+    float s = acc[h];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) s_dst[(long long)row * H + h] = s;
+  }
+}
+
+// ------------------------------------------------------------- backward ----
+// dYt = dY + ds_src (x) a_src  (score chain), in place, one warp per Y row.
+__global__ void k_dy_score(int R, int D, int H, const int* __restrict__ U_dev,
+                           const int* __restrict__ rel_y_off, const float* __restrict__ att,
+                           const float* __restrict__ ds_src, float* __restrict__ dY) {
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (u >= *U_dev) return;
+  int r = upper_bound_i(s_yoff, R + 1, u) - 1;
+  const float* a = att + (long long)r * 2 * D;
+  int dh = D / H;
+  for (int c = lane; c < D; c += 32)
+    dY[(long long)u * D + c] += ds_src[(long long)u * H + c / dh] * a[c];
+}
+
+// wgrad partials: chunk c of group g: P[c][k][d] = sum_{rows} A[row][k] B[row][d]
+// A = X rows (gathered), B = dYt rows (relations) or G rows (root types).
+template <int K, int D>
+__global__ void __launch_bounds__(256)
+k_wgrad_partial(ProjMeta pm, const int* __restrict__ chunk_off, const int* __restrict__ rel_y_off,
+                const int* __restrict__ y_src, const int* __restrict__ gather_ids,
+                const float* __restrict__ X, const float* __restrict__ dY,
+                const float* __restrict__ G, float* __restrict__ partial) {
+  constexpr int RB = 32, TM = K / 16, TN = D / 16;
+  __shared__ __align__(16) float As[RB][K];
+  __shared__ __align__(16) float Bs[RB][D];
+  __shared__ long long s_xr[RB];
+  int g, r0, nrows;
+  if (!resolve(pm, chunk_off, rel_y_off, blockIdx.x, kCH, &g, &r0, &nrows)) return;
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const float* Bbase = g < pm.R ? dY + (long long)rel_y_off[g] * D
+                                : G + (long long)pm.type_dst_off[g - pm.R] * D;
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++) acc[i][j] = 0.f;
+  for (int rb = 0; rb < nrows; rb += RB) {
+    if (tid < RB) {
+      int rr = rb + tid;
+      s_xr[tid] = rr < nrows ? a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + rr) : -1;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < RB * K / 4; idx += 256) {
+      int rr = idx / (K / 4), c4 = idx % (K / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (s_xr[rr] >= 0) v = __ldg(reinterpret_cast<const float4*>(X + s_xr[rr] * K) + c4);
+      *reinterpret_cast<float4*>(&As[rr][c4 * 4]) = v;
+    }
+    for (int idx = tid; idx < RB * D / 4; idx += 256) {
+      int rr = idx / (D / 4), c4 = idx % (D / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rb + rr < nrows)
+        v = __ldg(reinterpret_cast<const float4*>(Bbase + (long long)(r0 + rb + rr) * D) + c4);
+      *reinterpret_cast<float4*>(&Bs[rr][c4 * 4]) = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < RB; rr++) {
+      float av[TM], bv[TN];
+#pragma unroll
+      for (int i = 0; i < TM / 4; i++) {
+        float4 a = *reinterpret_cast<const float4*>(&As[rr][i * 64 + ty * 4]);
+        av[i * 4] = a.x; av[i * 4 + 1] = a.y; av[i * 4 + 2] = a.z; av[i * 4 + 3] = a.w;
+      }
+#pragma unroll
+      for (int j = 0; j < TN / 4; j++) {
+        float4 b = *reinterpret_cast<const float4*>(&Bs[rr][j * 64 + tx * 4]);
+        bv[j * 4] = b.x; bv[j * 4 + 1] = b.y; bv[j * 4 + 2] = b.z; bv[j * 4 + 3] = b.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* P = partial + (long long)blockIdx.x * K * D;
+#pragma unroll
+  for (int i = 0; i < TM; i++) {
+    int k = (i / 4) * 64 + ty * 4 + (i % 4);
+#pragma unroll
+    for (int j = 0; j < TN / 4; j++)
+      *reinterpret_cast<float4*>(P + (long long)k * D + j * 64 + tx * 4) =
+          make_float4(acc[i][j * 4], acc[i][j * 4 + 1], acc[i][j * 4 + 2], acc[i][j * 4 + 3]);
+  }
+}
+
+// dW[g] = sum of group g's chunk partials, in chunk order (deterministic).
+__global__ void k_wgrad_reduce(int R, int T, int KD, const int* __restrict__ chunk_off,
+                               const float4* __restrict__ partial, float4* __restrict__ dW_rel,
+                               float4* __restrict__ dW_root) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int KD4 = KD / 4;
+  int G = dW_root ? R + T : R;
+  if (idx >= (long long)G * KD4) return;
+  int g = (int)(idx / KD4), e = (int)(idx % KD4);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c = chunk_off[g]; c < chunk_off[g + 1]; c++) {
+    float4 v = partial[(long long)c * KD4 + e];
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  if (g < R) dW_rel[(long long)g * KD4 + e] = s;
+  else dW_root[(long long)(g - R) * KD4 + e] = s;
+}
+
+// dgrad: dX[type s tile] = sum_{r: s(r)=s} dYt[slot_y(r,j)] W_r^T
+//                          + [j < n_dst(s)] G_s[j] W_root,s^T
+template <int K, int D>
+__global__ void __launch_bounds__(256)
+k_dgrad(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
+        const float* __restrict__ G, const float* __restrict__ W_rel,
+        const float* __restrict__ W_root, float* __restrict__ dX) {
+  constexpr int BM = kBM, BK = 32, TN = K / 16;
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][K];
+  const int s = upper_bound_i(dm.tile_off, dm.T + 1, blockIdx.x) - 1;
+  const int j0 = (blockIdx.x - dm.tile_off[s]) * BM;
+  const int nrows = min(BM, dm.n_src[s] - j0);
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  float acc[4][TN];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++) acc[i][j] = 0.f;
+  const int nterm = dm.out_off[s + 1] - dm.out_off[s] + (dm.has_root ? 1 : 0);
+  for (int term = 0; term < nterm; term++) {
+    const bool root = term == dm.out_off[s + 1] - dm.out_off[s];
+    const int r = root ? -1 : dm.out_rel[dm.out_off[s] + term];
+    const float* W = root ? W_root + (long long)s * K * D : W_rel + (long long)r * K * D;
+    // A rows: tid/8 + 32 i, columns k4
+    long long arow[2];
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      int rr = tid / 8 + 32 * i;
+      long long a = -1;
+      if (rr < nrows) {
+        int j = j0 + rr;
+        if (root) a = j < dm.n_dst[s] ? (long long)dm.type_dst_off[s] + j : -1;
+        else a = slot_y[dm.slot_off[r] + j];
+      }
+      arow[i] = a;
+    }
+    const float* A = root ? G : dY;
+    for (int d0 = 0; d0 < D; d0 += BK) {
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        int rr = tid / 8 + 32 * i, k4 = tid % 8;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (arow[i] >= 0) v = __ldg(reinterpret_cast<const float4*>(A + arow[i] * D + d0) + k4);
+        As[k4 * 4 + 0][rr] = v.x;
+        As[k4 * 4 + 1][rr] = v.y;
+        As[k4 * 4 + 2][rr] = v.z;
+        As[k4 * 4 + 3][rr] = v.w;
+      }
+      // Bs[dd][k] = W[k][d0 + dd]
+      for (int idx = tid; idx < BK * K; idx += 256) {
+        int k = idx / BK, dd = idx % BK;
+        Bs[dd][k] = __ldg(W + (long long)k * D + d0 + dd);
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < BK; kk++) {
+        float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+        float av[4] = {a.x, a.y, a.z, a.w};
+        float bv[TN];
+#pragma unroll
+        for (int j = 0; j < TN / 4; j++) {
+          float4 b = *reinterpret_cast<const float4*>(&Bs[kk][j * 64 + tx * 4]);
+          bv[j * 4] = b.x; bv[j * 4 + 1] = b.y; bv[j * 4 + 2] = b.z; bv[j * 4 + 3] = b.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+          for (int j = 0; j < TN; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+  }
+  float* out = dX + (long long)dm.type_src_off[s] * K;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    int rr = ty * 4 + i;
+    if (rr >= nrows) continue;
+#pragma unroll
+    for (int j = 0; j < TN / 4; j++)
+      *reinterpret_cast<float4*>(out + (long long)(j0 + rr) * K + j * 64 + tx * 4) =
+          make_float4(acc[i][j * 4], acc[i][j * 4 + 1], acc[i][j * 4 + 2], acc[i][j * 4 + 3]);
+  }
+}
+
+// RGAT attention-vector partials over chunks of kCH rows of one relation:
+//   src (mode 0): P[c][h][w] = sum_u ds_src[u,h] Y[u,w]          rows = Y rows of r
+//   dst (mode 1): P[c][h][w] = sum_i ds_dst[(r,i),h] X_t(r)[i][w] rows = merged rows of r
+__global__ void __launch_bounds__(256)
+k_att_partial(int R, int H, int W, int mode, const int* __restrict__ chunk_off,
+              const int* __restrict__ row_off, const float* __restrict__ A,
+              const float* __restrict__ B, ProjMeta pm, const int* __restrict__ gather_ids,
+              float* __restrict__ partial) {
+  int c = blockIdx.x;
+  if (c >= chunk_off[R]) return;
+  int r = upper_bound_i(chunk_off, R + 1, c) - 1;
+  while (r > 0 && chunk_off[r] > c) r--;
+  int first = row_off[r] + (c - chunk_off[r]) * kCH;
+  int last = min(first + kCH, row_off[r + 1]);
+  for (int o = threadIdx.x; o < H * W; o += blockDim.x) {
+    int h = o / W, w = o % W;
+    float s = 0.f;
+    for (int row = first; row < last; row++) {
+      long long brow = row;
+      if (mode == 1) {
+        int x = pm.type_src_off[pm.rel_dst[r]] + (row - pm.rel_row_off[r]);
+        brow = gather_ids ? (long long)gather_ids[x] : (long long)x;
+      }
+      s = fmaf(A[(long long)row * H + h], B[brow * W + w], s);
+    }
+    partial[((long long)c * H + h) * W + w] = s;
+  }
+}
+
+__global__ void k_att_chunks(int R, const int* __restrict__ row_off, int* chunk_off) {
+  if (threadIdx.x != 0) return;
+  int acc = 0;
+  for (int r = 0; r < R; r++) {
+    chunk_off[r] = acc;
+    acc += (row_off[r + 1] - row_off[r] + kCH - 1) / kCH;
+  }
+  chunk_off[R] = acc;
+}
+
+// Final RGAT parameter gradients.  Per relation r, head h:
+//   datt[r,0,hc] = sum_chunks Psrc[h][hc]
+//   dv[h][k]     = sum_chunks Pdst[h][k]
+//   dW_r[k,hc]  += dv[h][k] a_dst[r,h,c]
+//   datt[r,1,hc] = sum_k W_r[k,hc] dv[h][k]
+__global__ void k_att_final(int R, int K, int D, int H, const int* __restrict__ src_chunk,
+                            const int* __restrict__ dst_chunk, const float* __restrict__ Psrc,
+                            const float* __restrict__ Pdst, const float* __restrict__ W_rel,
+                            const float* __restrict__ att, float* __restrict__ dW_rel,
+                            float* __restrict__ datt, float* __restrict__ dv_out) {
+  int r = blockIdx.x;
+  int dh = D / H;
+  extern __shared__ float dv[];   // [H][K]
+  for (int o = threadIdx.x; o < H * K; o += blockDim.x) {
+    float s = 0.f;
+    for (int c = dst_chunk[r]; c < dst_chunk[r + 1]; c++) s += Pdst[(long long)c * H * K + o];
+    dv[o] = s;
+    if (dv_out) dv_out[(long long)r * H * K + o] = s;
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    int h = d / dh;
+    float s = 0.f;
+    for (int c = src_chunk[r]; c < src_chunk[r + 1]; c++) s += Psrc[((long long)c * H + h) * D + d];
+    datt[(long long)r * 2 * D + d] = s;
+    float a = att[(long long)r * 2 * D + D + d];
+    float t = 0.f;
+    for (int k = 0; k < K; k++) {
+      float dvk = dv[h * K + k];
+      dW_rel[((long long)r * K + k) * D + d] += dvk * a;
+      t = fmaf(W_rel[((long long)r * K + k) * D + d], dvk, t);
+    }
+    datt[(long long)r * 2 * D + D + d] = t;
+  }
+}
+
+// dX_t[i] += sum_{r: t(r)=t} sum_h ds_dst[(r,i),h] v[r][:,h]   (s_dst chain);
+// one thread per (destination row of the layer, k), relations in fixed order.
+__global__ void k_dx_sdst(DgradMeta dm, int dst_rows, int K, int H, const float* __restrict__ v,
+                          const float* __restrict__ ds_dst, float* __restrict__ dX) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)dst_rows * K) return;
+  int o = (int)(idx / K), k = (int)(idx % K);
+  int t = upper_bound_i(dm.type_dst_off, dm.T + 1, o) - 1;
+  int i = o - dm.type_dst_off[t];
+  float s = 0.f;
+  for (int q = dm.in_off[t]; q < dm.in_off[t + 1]; q++) {
+    int r = dm.in_rel[q];
+    long long row = dm.rel_row_off[r] + i;
+    for (int h = 0; h < H; h++)
+      s = fmaf(ds_dst[row * H + h], v[((long long)r * K + k) * H + h], s);
+  }
+  dX[(long long)(dm.type_src_off[t] + i) * K + k] += s;
+}
+
+void make_dgrad_meta(const LayerMeta& m, bool has_root, DgradMeta* dm) {
+  dm->T = m.T;
+  dm->has_root = has_root ? 1 : 0;
+  int tiles = 0, ko = 0, ki = 0;
+  for (int t = 0; t < m.T; t++) {
+    dm->tile_off[t] = tiles;
+    tiles += (m.n_src[t] + kBM - 1) / kBM;
+    dm->n_src[t] = m.n_src[t];
+    dm->n_dst[t] = m.n_dst[t];
+    dm->out_off[t] = ko;
+    for (int r = 0; r < m.R; r++)
+      if (m.rel_src[r] == t) dm->out_rel[ko++] = r;
+    dm->in_off[t] = ki;
+    for (int r = 0; r < m.R; r++)
+      if (m.rel_dst[r] == t) dm->in_rel[ki++] = r;
+  }
+  dm->tile_off[m.T] = tiles;
+  dm->out_off[m.T] = ko;
+  dm->in_off[m.T] = ki;
+  for (int t = 0; t <= m.T; t++) {
+    dm->type_src_off[t] = m.type_src_off[t];
+    dm->type_dst_off[t] = m.type_dst_off[t];
+  }
+  for (int r = 0; r <= m.R; r++) {
+    dm->slot_off[r] = m.slot_off[r];
+    dm->rel_row_off[r] = m.rel_row_off[r];
+  }
+}
+
+void make_proj_meta(const LayerMeta& m, bool has_root, ProjMeta* pm) {
+  pm->R = m.R;
+  pm->T = m.T;
+  pm->rows = m.rows;
+  pm->has_root = has_root ? 1 : 0;
+  for (int r = 0; r < m.R; r++) {
+    pm->rel_src[r] = m.rel_src[r];
+    pm->rel_dst[r] = m.rel_dst[r];
+  }
+  for (int r = 0; r <= m.R; r++) pm->rel_row_off[r] = m.rel_row_off[r];
+  for (int t = 0; t < m.T; t++) pm->n_dst[t] = m.n_dst[t];
+  for (int t = 0; t <= m.T; t++) {
+    pm->type_src_off[t] = m.type_src_off[t];
+    pm->type_dst_off[t] = m.type_dst_off[t];
+  }
+}
+
+long long proj_max_tiles(const LayerMeta& m, int step) {
+  long long U_max = m.N < m.S ? m.N : m.S;
+  return (U_max + m.dst_rows) / step + m.R + m.T + 1;
+}
+
+}  // namespace hf
+
+using namespace hf;
+
+static bool kd_ok(int K, int D) { return (K == 64 || K == 128) && (D == 64 || D == 128); }
+
+static bool heads_ok2(int D, int H) {
+  if (H <= 0 || H > HIFUSE_MAX_HEADS || D % H) return false;
+  int dh = D / H;
+  return dh % 4 == 0 && (dh & (dh - 1)) == 0;
+}
+
+extern "C" {
+
+size_t hifuse_project_ws_bytes(const hifuse_layer_shape* shape, int K, int D, int heads) {
+  LayerMeta m;
+  if (make_meta(shape, &m) != HIFUSE_OK) return 0;
+  size_t b = 2 * carve_bytes(m.R + m.T + 1, 4);            // tile_off, chunk_off
+  b += carve_bytes((long long)m.R * K * (heads > 0 ? heads : 1), 4);   // v
+  return b;
+}
+
+hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                             hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
+                             const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
+                             const float* d_W_rel, const float* d_W_root, const float* d_att,
+                             float* d_Y, float* d_R0, float* d_s_src, float* d_s_dst, void* d_ws,
+                             size_t ws_bytes, hifuse_stream_t stream) {
+  if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!kd_ok(K, D)) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !csr->rel_y_off || !csr->y_src || !csr->U_dev || !d_X || !d_W_rel || !d_Y ||
+      x_rows < 0 || (d_W_root && !d_R0))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (d_att && (!heads_ok2(D, heads) || !d_s_src || !d_s_dst)) return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_X) || !aligned16(d_W_rel) || !aligned16(d_W_root) || !aligned16(d_Y) ||
+      !aligned16(d_R0))
+    return HIFUSE_ERR_ALIGNMENT;
+  if (ws_bytes < hifuse_project_ws_bytes(shape, K, D, heads) || !d_ws) return HIFUSE_ERR_WORKSPACE;
+  cudaStream_t s = st(stream);
+  ProjMeta pm;
+  make_proj_meta(m, d_W_root != nullptr, &pm);
+  char* p = (char*)d_ws;
+  int* tile_off = carve<int>(p, m.R + m.T + 1);
+  int* chunk_off = carve<int>(p, m.R + m.T + 1);
+  float* v = carve<float>(p, (long long)m.R * K * (heads > 0 ? heads : 1));
+  if (prec == HIFUSE_PREC_TF32) {
+    rc = project_tc_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0, s);
+    if (rc != HIFUSE_OK) return rc;
+  } else if (prec == HIFUSE_PREC_FP32) {
+    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
+    unsigned grid = (unsigned)proj_max_tiles(m, kBM);
+#define HF_FWD(KK, DD)                                                                    \
+  HF_LAUNCH((k_proj_fwd_simt<KK, DD>), grid, 256, 0, s, pm, tile_off, csr->rel_y_off,     \
+            csr->y_src, d_gather_ids, d_X, d_W_rel, d_W_root, d_Y, d_R0)
+    if (K == 128 && D == 128) HF_FWD(128, 128);
+    else if (K == 128 && D == 64) HF_FWD(128, 64);
+    else if (K == 64 && D == 128) HF_FWD(64, 128);
+    else HF_FWD(64, 64);
+#undef HF_FWD
+  } else {
+    return HIFUSE_ERR_UNSUPPORTED;
+  }
+  if (d_att) {
+    HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * heads, 256), 256, 0, s, m.R, K, D, heads,
+              d_W_rel, d_att, v);
+    long long U_max = m.N < m.S ? m.N : m.S;
+    HF_LAUNCH(k_scores_src, ceil_div(U_max, 8), 256, 0, s, m.R, D, heads, csr->U_dev,
+              csr->rel_y_off, d_Y, d_att, d_s_src);
+    HF_LAUNCH(k_scores_dst, ceil_div(m.rows, 8), 256, 0, s, pm, K, heads, d_gather_ids, d_X, v,
+              d_s_dst);
+  }
+  return last_cuda();
+}
+
+size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D, int heads) {
+  LayerMeta m;
+  if (make_meta(shape, &m) != HIFUSE_OK) return 0;
+  int H = heads > 0 ? heads : 1;
+  long long chunks = proj_max_tiles(m, kCH);
+  size_t b = 2 * carve_bytes(m.R + m.T + 1, 4);
+  b += carve_bytes(chunks * K * D, 4);                       // wgrad partials
+  b += carve_bytes((long long)m.R * K * H, 4);               // v
+  b += 2 * carve_bytes(m.R + 1, 4);                          // att chunk tables
+  long long U_max = m.N < m.S ? m.N : m.S;
+  long long ach = U_max / kCH + m.rows / kCH + 2 * m.R + 2;
+  b += carve_bytes(ach * H * (K > D ? K : D), 4) * 2;        // att partials
+  b += carve_bytes(m.R + 1, 4);                              // host row table copy
+  return b;
+}
+
+hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                 hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
+                                 const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
+                                 const float* d_W_rel, const float* d_W_root, const float* d_att,
+                                 const float* d_Y, float* d_dY, const float* d_G,
+                                 const float* d_ds_src, const float* d_ds_dst, float* d_dX,
+                                 float* d_dW_rel, float* d_dW_root, float* d_datt, void* d_ws,
+                                 size_t ws_bytes, hifuse_stream_t stream) {
+  (void)prec;
+  if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!kd_ok(K, D)) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !d_X || !d_W_rel || !d_dY || !d_dW_rel || x_rows < 0 ||
+      (d_W_root && (!d_dW_root || !d_G)))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (d_att && (!heads_ok2(D, heads) || !d_ds_src || !d_ds_dst || !d_datt || !d_Y))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (d_dX && d_gather_ids) return HIFUSE_ERR_UNSUPPORTED;
+  if (ws_bytes < hifuse_project_bwd_ws_bytes(shape, K, D, heads) || !d_ws)
+    return HIFUSE_ERR_WORKSPACE;
+  cudaStream_t s = st(stream);
+  ProjMeta pm;
+  make_proj_meta(m, d_W_root != nullptr, &pm);
+  int H = heads > 0 ? heads : 1;
+  long long chunks = proj_max_tiles(m, kCH);
+  char* p = (char*)d_ws;
+  int* tile_off = carve<int>(p, m.R + m.T + 1);
+  int* chunk_off = carve<int>(p, m.R + m.T + 1);
+  float* partial = carve<float>(p, chunks * K * D);
+  float* v = carve<float>(p, (long long)m.R * K * H);
+  int* src_chunk = carve<int>(p, m.R + 1);
+  int* dst_chunk = carve<int>(p, m.R + 1);
+  long long U_max = m.N < m.S ? m.N : m.S;
+  long long ach = U_max / kCH + m.rows / kCH + 2 * m.R + 2;
+  float* Psrc = carve<float>(p, ach * H * (K > D ? K : D));
+  float* Pdst = carve<float>(p, ach * H * (K > D ? K : D));
+  int* rro_dev = carve<int>(p, m.R + 1);
+  if (d_att) {
+    HF_LAUNCH(k_dy_score, ceil_div(U_max, 8), 256, 0, s, m.R, D, H, csr->U_dev, csr->rel_y_off,
+              d_att, d_ds_src, d_dY);
+  }
+  HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
+  unsigned grid = (unsigned)chunks;
+#define HF_WG(KK, DD)                                                                          \
+  HF_LAUNCH((k_wgrad_partial<KK, DD>), grid, 256, 0, s, pm, chunk_off, csr->rel_y_off,         \
+            csr->y_src, d_gather_ids, d_X, d_dY, d_G, partial)
+  if (K == 128 && D == 128) HF_WG(128, 128);
+  else if (K == 128 && D == 64) HF_WG(128, 64);
+  else if (K == 64 && D == 128) HF_WG(64, 128);
+  else HF_WG(64, 64);
+#undef HF_WG
+  int G = d_W_root ? m.R + m.T : m.R;
+  HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
+            chunk_off, (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root);
+  if (d_att) {
+    HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, s, m.R, K, D, H, d_W_rel,
+              d_att, v);
+    cudaMemcpyAsync(rro_dev, m.rel_row_off, sizeof(int) * (m.R + 1), cudaMemcpyHostToDevice, s);
+    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, csr->rel_y_off, src_chunk);
+    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, rro_dev, dst_chunk);
+    unsigned gs = (unsigned)(U_max / kCH + m.R + 1);
+    unsigned gdst = (unsigned)(m.rows / kCH + m.R + 1);
+    HF_LAUNCH(k_att_partial, gs, 256, 0, s, m.R, H, D, 0, src_chunk, csr->rel_y_off, d_ds_src,
+              d_Y, pm, d_gather_ids, Psrc);
+    HF_LAUNCH(k_att_partial, gdst, 256, 0, s, m.R, H, K, 1, dst_chunk, rro_dev, d_ds_dst, d_X,
+              pm, d_gather_ids, Pdst);
+    HF_LAUNCH(k_att_final, m.R, 256, H * K * sizeof(float), s, m.R, K, D, H, src_chunk, dst_chunk,
+              Psrc, Pdst, d_W_rel, d_att, d_dW_rel, d_datt, (float*)nullptr);
+  }
+  if (d_dX) {
+    DgradMeta dm;
+    make_dgrad_meta(m, d_W_root != nullptr, &dm);
+    unsigned gd = dm.tile_off[m.T];
+#define HF_DG(KK, DD)                                                                         \
+  HF_LAUNCH((k_dgrad<KK, DD>), gd, 256, 0, s, dm, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX)
+    if (K == 128 && D == 128) HF_DG(128, 128);
+    else if (K == 128 && D == 64) HF_DG(128, 64);
+    else if (K == 64 && D == 128) HF_DG(64, 128);
+    else HF_DG(64, 64);
+#undef HF_DG
+    if (d_att)
+      HF_LAUNCH(k_dx_sdst, ceil_div((long long)m.dst_rows * K, 256), 256, 0, s, dm, m.dst_rows, K,
+                H, v, d_ds_dst, d_dX);
+  }
+  return last_cuda();
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// project.cuh -- shared declarations of the projection kernels.
+#pragma once
+#include "common.cuh"
+
+#define HIFUSE_MAX_HEADS 16
+
+namespace hf {
+
+static constexpr int kBM = 64;     // SIMT forward / dgrad tile rows
+static constexpr int kCH = 256;    // wgrad chunk rows
+
+struct ProjMeta {
+  int R, T, rows, has_root;
+  int rel_src[HF_MAX_R];
+  int rel_dst[HF_MAX_R];
+  int rel_row_off[HF_MAX_R + 1];
+  int n_dst[HF_MAX_T];
+  int type_src_off[HF_MAX_T + 1];
+  int type_dst_off[HF_MAX_T + 1];
+};
+
+struct DgradMeta {
+  int T, has_root;
+  int tile_off[HF_MAX_T + 1];      // kBM-row tiles of each type's source rows
+  int n_src[HF_MAX_T];
+  int n_dst[HF_MAX_T];
+  int type_src_off[HF_MAX_T + 1];
+  int type_dst_off[HF_MAX_T + 1];
+  int slot_off[HF_MAX_R + 1];
+  int rel_row_off[HF_MAX_R + 1];
+  int out_off[HF_MAX_T + 1];       // relations out of type s: out_rel[out_off[s]..]
+  int out_rel[HF_MAX_R];
+  int in_off[HF_MAX_T + 1];        // relations into type t: in_rel[in_off[t]..]
+  int in_rel[HF_MAX_R];
+};
+
+void make_proj_meta(const LayerMeta& m, bool has_root, ProjMeta* pm);
+void make_dgrad_meta(const LayerMeta& m, bool has_root, DgradMeta* dm);
+long long proj_max_tiles(const LayerMeta& m, int step);
+
+// tcgen05 TF32 forward projection (project_tc.cu).
+hifuse_status project_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
+                                const hifuse_csr* csr, const float* X, const int* gather_ids,
+                                const float* W_rel, const float* W_root, float* Y, float* R0,
+                                cudaStream_t s);
+
+}  // namespace hf

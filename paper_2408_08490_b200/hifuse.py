@@ -1,0 +1,260 @@
+"""Thin ctypes binding of libhifuse.so (include/hifuse.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  Tensors are torch CUDA tensors (torch provides device memory and
+streams); host metadata are numpy int32 arrays.  There is no CPU fallback:
+importing this module on a machine without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhifuse.so")
+
+AGG = {"sum": 0, "mean": 1, "gat": 2}
+ACT = {"none": 0, "relu": 1}
+LAYOUT_COMPACT = 1
+PREC = {"fp32": 0, "tf32": 1}
+STATUS = {0: "ok", 1: "invalid argument", 2: "alignment", 3: "unsupported", 4: "workspace",
+          5: "cuda"}
+
+
+class HifuseError(RuntimeError):
+    def __init__(self, fn, code):
+        super().__init__(f"{fn} failed: {STATUS.get(code, code)} ({code})")
+        self.code = code
+
+
+class LayerShape(ctypes.Structure):
+    _fields_ = [("num_types", ctypes.c_int32), ("num_rels", ctypes.c_int32),
+                ("rel_src_type_h", ctypes.c_void_p), ("rel_dst_type_h", ctypes.c_void_p),
+                ("n_src_h", ctypes.c_void_p), ("n_dst_h", ctypes.c_void_p),
+                ("num_edges", ctypes.c_int64)]
+
+
+class Csr(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("rel_row_off", "row_ptr", "col", "eperm", "rel_y_off", "y_src", "col_ptr",
+                 "csc_pos", "csc_row", "slot_y", "U_dev")]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make -C paper_2408_08490_b200` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, f32, sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float,
+                                 ctypes.c_size_t)
+        sig = {
+            "hifuse_csr_sizes": [vp, i32, vp, vp, vp, vp],
+            "hifuse_build_semantic_graphs": [vp, i32, vp, vp, vp, vp, i64, i32, vp, vp, sz, vp, vp],
+            "hifuse_project_ws_bytes": [vp, i32, i32, i32],
+            "hifuse_project": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp,
+                               vp, vp, vp, sz, vp],
+            "hifuse_aggregate_fwd": [vp, i64, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp],
+            "hifuse_semantic_fuse": [vp, i32, i32, vp, vp, vp, vp, vp],
+            "hifuse_fuse_bwd_ws_bytes": [vp, i32],
+            "hifuse_semantic_fuse_bwd": [vp, i32, i32, vp, vp, vp, vp, vp, sz, vp],
+            "hifuse_aggregate_bwd_ws_bytes": [vp, i32, i32],
+            "hifuse_aggregate_bwd": [vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp,
+                                     vp, sz, vp],
+            "hifuse_project_bwd_ws_bytes": [vp, i32, i32, i32],
+            "hifuse_project_bwd": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp,
+                                   vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
+            "hifuse_xent_ws_bytes": [i32, i32, i32],
+            "hifuse_linear_xent": [i32, i32, i32, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp,
+                                   sz, vp],
+            "hifuse_sgd": [vp, vp, i64, f32, f32, vp],
+            "hifuse_read_status": [vp, vp, vp],
+            "hifuse_kernel_launches": [],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        for name in ("hifuse_project_ws_bytes", "hifuse_fuse_bwd_ws_bytes",
+                     "hifuse_aggregate_bwd_ws_bytes", "hifuse_project_bwd_ws_bytes",
+                     "hifuse_xent_ws_bytes"):
+            getattr(L, name).restype = ctypes.c_size_t
+        L.hifuse_kernel_launches.restype = ctypes.c_int64
+        L.hifuse_status_string.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _check(fn, rc):
+    if rc != 0:
+        raise HifuseError(fn, rc)
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Shape:
+    """Host metadata of one layer; keeps the numpy arrays alive."""
+
+    def __init__(self, rel_src, rel_dst, n_src, n_dst, num_edges):
+        self.rel_src = np.ascontiguousarray(rel_src, np.int32)
+        self.rel_dst = np.ascontiguousarray(rel_dst, np.int32)
+        self.n_src = np.ascontiguousarray(n_src, np.int32)
+        self.n_dst = np.ascontiguousarray(n_dst, np.int32)
+        self.N = int(num_edges)
+        self.T, self.R = len(self.n_src), len(self.rel_src)
+        self.c = LayerShape(self.T, self.R, self.rel_src.ctypes.data, self.rel_dst.ctypes.data,
+                            self.n_src.ctypes.data, self.n_dst.ctypes.data, self.N)
+        rows, umax, S = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        ws = ctypes.c_size_t()
+        _check("hifuse_csr_sizes", lib().hifuse_csr_sizes(
+            ctypes.byref(self.c), LAYOUT_COMPACT, ctypes.byref(rows), ctypes.byref(umax),
+            ctypes.byref(S), ctypes.byref(ws)))
+        self.rows, self.U_max, self.S, self.build_ws = rows.value, umax.value, S.value, ws.value
+        self.src_rows = int(self.n_src.sum())
+        self.dst_rows = int(self.n_dst.sum())
+        self.rel_row_off = np.concatenate([[0], np.cumsum(self.n_dst[self.rel_dst])]).astype(np.int64)
+        self.type_src_off = np.concatenate([[0], np.cumsum(self.n_src)]).astype(np.int64)
+        self.type_dst_off = np.concatenate([[0], np.cumsum(self.n_dst)]).astype(np.int64)
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.c)
+
+
+class CsrBuffers:
+    """Device buffers of one layer's build output (torch int32 tensors)."""
+
+    def __init__(self, shape: Shape, device, cap=None):
+        import torch
+        cap = cap or {}
+        N = max(cap.get("N", shape.N), 1)
+        rows = max(cap.get("rows", shape.rows), 1)
+        umax = max(cap.get("U_max", shape.U_max), 1)
+        S = max(cap.get("S", shape.S), 1)
+        R = cap.get("R", shape.R)
+        z = lambda n: torch.empty(n, dtype=torch.int32, device=device)
+        self.t = dict(rel_row_off=z(R + 1), row_ptr=z(rows + 1), col=z(N), eperm=z(N),
+                      rel_y_off=z(R + 1), y_src=z(umax), col_ptr=z(umax + 1), csc_pos=z(N),
+                      csc_row=z(N), slot_y=z(S), U_dev=z(1))
+        self.c = Csr(**{k: v.data_ptr() for k, v in self.t.items()})
+
+    def __getitem__(self, k):
+        return self.t[k]
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.c)
+
+
+def build_semantic_graphs(shapes, csrs, src_local, dst_local, edge_id, edge_type, ws, status,
+                          stream=None):
+    n = len(shapes)
+    arr_s = (ctypes.c_void_p * n)(*[t.data_ptr() for t in src_local])
+    arr_d = (ctypes.c_void_p * n)(*[t.data_ptr() for t in dst_local])
+    arr_e = (ctypes.c_void_p * n)(*[t.data_ptr() for t in edge_id])
+    sh = (LayerShape * n)(*[s.c for s in shapes])
+    cs = (Csr * n)(*[c.c for c in csrs])
+    _check("hifuse_build_semantic_graphs", lib().hifuse_build_semantic_graphs(
+        sh, n, arr_s, arr_d, arr_e, _ptr(edge_type), edge_type.numel(), LAYOUT_COMPACT, cs,
+        _ptr(ws), ws.numel() * ws.element_size(), _ptr(status), _stream(stream)))
+
+
+def project_ws_bytes(shape, K, D, heads):
+    return int(lib().hifuse_project_ws_bytes(shape.ref, K, D, heads))
+
+
+def project(shape, csr, K, D, heads, X, gather_ids, W_rel, W_root, att, Y, R0, s_src, s_dst, ws,
+            prec="fp32", stream=None):
+    _check("hifuse_project", lib().hifuse_project(
+        shape.ref, csr.ref, LAYOUT_COMPACT, PREC[prec], K, D, heads, _ptr(X), X.shape[0],
+        _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(att), _ptr(Y), _ptr(R0), _ptr(s_src),
+        _ptr(s_dst), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def aggregate_fwd(csr, rows, agg, D, heads, slope, Y, s_src, s_dst, Z, stats, stream=None):
+    _check("hifuse_aggregate_fwd", lib().hifuse_aggregate_fwd(
+        csr.ref, rows, AGG[agg], D, heads, slope, _ptr(Y), _ptr(s_src), _ptr(s_dst), _ptr(Z),
+        _ptr(stats), _stream(stream)))
+
+
+def semantic_fuse(shape, D, act, Z, R0, bias, H, stream=None):
+    _check("hifuse_semantic_fuse", lib().hifuse_semantic_fuse(
+        shape.ref, D, ACT[act], _ptr(Z), _ptr(R0), _ptr(bias), _ptr(H), _stream(stream)))
+
+
+def fuse_bwd_ws_bytes(shape, D):
+    return int(lib().hifuse_fuse_bwd_ws_bytes(shape.ref, D))
+
+
+def semantic_fuse_bwd(shape, D, act, dH, H, G, dbias, ws, stream=None):
+    _check("hifuse_semantic_fuse_bwd", lib().hifuse_semantic_fuse_bwd(
+        shape.ref, D, ACT[act], _ptr(dH), _ptr(H), _ptr(G), _ptr(dbias), _ptr(ws),
+        0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def aggregate_bwd_ws_bytes(shape, agg, heads):
+    return int(lib().hifuse_aggregate_bwd_ws_bytes(shape.ref, AGG[agg], heads))
+
+
+def aggregate_bwd(shape, csr, agg, D, heads, slope, G, Y, s_src, s_dst, stats, dY, ds_src, ds_dst,
+                  ws, stream=None):
+    _check("hifuse_aggregate_bwd", lib().hifuse_aggregate_bwd(
+        shape.ref, csr.ref, AGG[agg], D, heads, slope, _ptr(G), _ptr(Y), _ptr(s_src), _ptr(s_dst),
+        _ptr(stats), _ptr(dY), _ptr(ds_src), _ptr(ds_dst), _ptr(ws),
+        0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def project_bwd_ws_bytes(shape, K, D, heads):
+    return int(lib().hifuse_project_bwd_ws_bytes(shape.ref, K, D, heads))
+
+
+def project_bwd(shape, csr, K, D, heads, X, gather_ids, W_rel, W_root, att, Y, dY, G, ds_src,
+                ds_dst, dX, dW_rel, dW_root, datt, ws, prec="fp32", stream=None):
+    _check("hifuse_project_bwd", lib().hifuse_project_bwd(
+        shape.ref, csr.ref, LAYOUT_COMPACT, PREC[prec], K, D, heads, _ptr(X), X.shape[0],
+        _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(att), _ptr(Y), _ptr(dY), _ptr(G),
+        _ptr(ds_src), _ptr(ds_dst), _ptr(dX), _ptr(dW_rel), _ptr(dW_root), _ptr(datt), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def xent_ws_bytes(B, D, C):
+    return int(lib().hifuse_xent_ws_bytes(B, D, C))
+
+
+def linear_xent(B, D, C, H, h_row0, labels, Wc, bc, loss, dH, dWc, dbc, ws, stream=None):
+    _check("hifuse_linear_xent", lib().hifuse_linear_xent(
+        B, D, C, _ptr(H), H.shape[0], h_row0, _ptr(labels), _ptr(Wc), _ptr(bc), _ptr(loss),
+        _ptr(dH), _ptr(dWc), _ptr(dbc), _ptr(ws), ws.numel() * ws.element_size(),
+        _stream(stream)))
+
+
+def sgd(param, grad, lr, grad_scale=1.0, stream=None):
+    _check("hifuse_sgd", lib().hifuse_sgd(_ptr(param), _ptr(grad), param.numel(), lr, grad_scale,
+                                          _stream(stream)))
+
+
+def read_status(status, stream=None):
+    out = ctypes.c_int32()
+    _check("hifuse_read_status", lib().hifuse_read_status(_ptr(status), _stream(stream),
+                                                          ctypes.byref(out)))
+    return out.value
+
+
+def kernel_launches():
+    return int(lib().hifuse_kernel_launches())

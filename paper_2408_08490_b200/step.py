@@ -1,0 +1,214 @@
+"""One mini-batch HGNN training step through the C ABI (Fig. 2 step
+(4), line 156: forward through the four stages of every layer, backward,
+parameter update).
+
+torch supplies device memory, the stream and (for N > 1) the NCCL process
+group; every arithmetic step runs in libhifuse kernels:
+
+  hifuse_build_semantic_graphs   all layers (A1)
+  per layer, outer first:        hifuse_project (A2+A3) -> hifuse_aggregate_fwd
+                                 (A4) -> hifuse_semantic_fuse (A5)
+  hifuse_linear_xent             classifier + loss + its gradients
+  per layer, inner first:        hifuse_semantic_fuse_bwd -> hifuse_aggregate_bwd
+                                 -> hifuse_project_bwd (A6)
+  [dist.all_reduce of the flat gradient buffer when world_size > 1]
+  hifuse_sgd                     parameter update
+
+Parameters and gradients each live in ONE flat fp32 buffer so the data-parallel
+exchange is a single NCCL all-reduce.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import hifuse as hf
+
+
+def _align4(n):
+    return (n + 3) // 4 * 4
+
+
+class ParamLayout:
+    """Offsets of every parameter inside the flat buffer (16-byte aligned)."""
+
+    def __init__(self, T, R, K0, D, H, C, L, model):
+        self.entries = []
+        off = 0
+
+        def add(name, shape):
+            nonlocal off
+            n = int(np.prod(shape))
+            self.entries.append((name, off, shape))
+            off += _align4(n)
+
+        for l in range(L):
+            K = K0 if l == 0 else D
+            add(f"{l}.W_rel", (R, K, D))
+            if model == "rgcn":
+                add(f"{l}.W_root", (T, K, D))
+            add(f"{l}.bias", (T, D))
+            if model == "rgat":
+                add(f"{l}.att", (R, 2, D))
+        add("Wc", (D, C))
+        add("bc", (C,))
+        self.size = off
+
+    def views(self, flat):
+        return {name: flat[o:o + int(np.prod(s))].view(*s) for name, o, s in self.entries}
+
+
+class DeviceBatch:
+    """A sampled mini-batch resident on the device (sampling is outside the
+    library boundary, Fig. 2 step (1))."""
+
+    def __init__(self, mb, rel_src, rel_dst, feat_off, target_type, device, pin=False):
+        self.shapes = [hf.Shape(rel_src, rel_dst, b.n_src, b.n_dst, b.num_edges) for b in mb.layers]
+        self.host = dict(
+            src=[np.ascontiguousarray(b.src_local, np.int32) for b in mb.layers],
+            dst=[np.ascontiguousarray(b.dst_local, np.int32) for b in mb.layers],
+            eid=[np.ascontiguousarray(b.edge_id, np.int64) for b in mb.layers],
+            gid=mb.gather_ids(feat_off).astype(np.int32),
+            labels=np.ascontiguousarray(mb.labels, np.int32))
+        self.B = len(mb.labels)
+        self.target_type = target_type
+        self.h_row0 = int(self.shapes[-1].type_dst_off[target_type])
+        self.device = device
+        self.dev = None
+        self.pinned = None
+        if pin:
+            self.pinned = {k: ([torch.from_numpy(a).pin_memory() for a in v] if isinstance(v, list)
+                               else torch.from_numpy(v).pin_memory())
+                           for k, v in self.host.items()}
+        if device is not None:
+            self.to_device()
+
+    def to_device(self, non_blocking=False):
+        src = self.pinned if self.pinned is not None else {
+            k: ([torch.from_numpy(a) for a in v] if isinstance(v, list) else torch.from_numpy(v))
+            for k, v in self.host.items()}
+        self.dev = {k: ([t.to(self.device, non_blocking=non_blocking) for t in v]
+                        if isinstance(v, list) else v.to(self.device, non_blocking=non_blocking))
+                    for k, v in src.items()}
+        return self
+
+    def h2d_bytes(self):
+        return int(sum(a.nbytes for v in self.host.values()
+                       for a in (v if isinstance(v, list) else [v])))
+
+
+class Trainer:
+    """Owns parameters, gradients, activations and workspaces of the step."""
+
+    def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
+                 prec="fp32", slope=0.2):
+        self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
+        self.rel_src = np.asarray(rel_src, np.int32)
+        self.rel_dst = np.asarray(rel_dst, np.int32)
+        self.model, self.agg, self.device, self.lr, self.prec, self.slope = (
+            model, agg, device, lr, prec, slope)
+        self.layout = ParamLayout(T, R, K0, D, H, C, L, model)
+        self.params = torch.zeros(self.layout.size, dtype=torch.float32, device=device)
+        self.grads = torch.zeros_like(self.params)
+        self.P = self.layout.views(self.params)
+        self.Gd = self.layout.views(self.grads)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=device)
+        self._bufs = {}
+        self.heads = H if model == "rgat" else 1
+
+    def load_params(self, p):
+        for l, lay in enumerate(p["layers"]):
+            for k in ("W_rel", "W_root", "bias", "att"):
+                if lay.get(k) is not None and f"{l}.{k}" in self.P:
+                    self.P[f"{l}.{k}"].copy_(torch.from_numpy(np.asarray(lay[k], np.float32)))
+        self.P["Wc"].copy_(torch.from_numpy(np.asarray(p["Wc"], np.float32)))
+        self.P["bc"].copy_(torch.from_numpy(np.asarray(p["bc"], np.float32)))
+
+    # -------------------------------------------------------------- buffers
+    def _buf(self, key, n, dtype=torch.float32):
+        t = self._bufs.get(key)
+        if t is None or t.numel() < n:
+            t = torch.empty(max(int(n * 1.25), 16), dtype=dtype, device=self.device)
+            self._bufs[key] = t
+        return t
+
+    def _mat(self, key, rows, cols):
+        return self._buf(key, max(rows, 1) * cols)[:max(rows, 1) * cols].view(max(rows, 1), cols)
+
+    def _csr(self, l, shape):
+        key = f"csr{l}"
+        c = self._bufs.get(key)
+        need = dict(N=shape.N, rows=shape.rows, U_max=shape.U_max, S=shape.S, R=shape.R)
+        if c is None or any(need[k] > c.cap[k] for k in need):
+            cap = {k: int(v * 1.25) + 1 for k, v in need.items()}
+            cap["R"] = shape.R
+            c = hf.CsrBuffers(shape, self.device, cap)
+            c.cap = cap
+            self._bufs[key] = c
+        return c
+
+    def _ws(self, nbytes):
+        return self._buf("ws", (nbytes + 3) // 4 + 64)
+
+    # ----------------------------------------------------------------- step
+    def step(self, db: DeviceBatch, feat, edge_type, allreduce=None, world=1, update=True):
+        """Runs one training step on the current stream; returns the device
+        loss tensor (no host synchronisation)."""
+        L, D, H, C = self.L, self.D, self.heads, self.C
+        dev = db.dev
+        shapes = db.shapes
+        csrs = [self._csr(l, s) for l, s in enumerate(shapes)]
+        ws_build = max(s.build_ws for s in shapes)
+        hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"], edge_type,
+                                 self._ws(ws_build), self.status)
+        acts = []
+        X, gid = feat, dev["gid"]
+        for l, sh in enumerate(shapes):
+            K = self.K0 if l == 0 else D
+            P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
+            Y = self._mat(f"Y{l}", sh.U_max, D)
+            R0 = self._mat(f"R0{l}", sh.dst_rows, D) if P["W_root"] is not None else None
+            s_src = self._mat(f"ss{l}", sh.U_max, H) if P["att"] is not None else None
+            s_dst = self._mat(f"sd{l}", sh.rows, H) if P["att"] is not None else None
+            hf.project(sh, csrs[l], K, D, H, X, gid, P["W_rel"], P["W_root"], P["att"], Y, R0,
+                       s_src, s_dst, self._ws(hf.project_ws_bytes(sh, K, D, H)), prec=self.prec)
+            Z = self._mat(f"Z{l}", sh.rows, D)
+            stats = self._mat(f"st{l}", sh.rows, 2 * H) if self.agg == "gat" else None
+            hf.aggregate_fwd(csrs[l], sh.rows, self.agg, D, H, self.slope, Y, s_src, s_dst, Z, stats)
+            Hout = self._mat(f"H{l}", sh.dst_rows, D)
+            act = "relu" if l < L - 1 else "none"
+            hf.semantic_fuse(sh, D, act, Z, R0, P["bias"], Hout)
+            acts.append(dict(X=X, gid=gid, Y=Y, R0=R0, s_src=s_src, s_dst=s_dst, stats=stats,
+                             H=Hout, act=act, K=K))
+            X, gid = Hout, None
+        last = shapes[-1]
+        dH = self._mat(f"dH{L - 1}", last.dst_rows, D)
+        hf.linear_xent(db.B, D, C, acts[-1]["H"][:last.dst_rows], db.h_row0, dev["labels"],
+                       self.P["Wc"], self.P["bc"], self.loss, dH[:last.dst_rows], self.Gd["Wc"],
+                       self.Gd["bc"], self._ws(hf.xent_ws_bytes(db.B, D, C)))
+        for l in range(L - 1, -1, -1):
+            sh, a = shapes[l], acts[l]
+            P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
+            Gr = {k: self.Gd.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
+            G = self._mat(f"G{l}", sh.dst_rows, D)
+            hf.semantic_fuse_bwd(sh, D, a["act"], dH, a["H"], G, Gr["bias"],
+                                 self._ws(hf.fuse_bwd_ws_bytes(sh, D)))
+            dY = self._mat(f"dY{l}", sh.U_max, D)
+            ds_src = self._mat(f"dss{l}", sh.U_max, H) if P["att"] is not None else None
+            ds_dst = self._mat(f"dsd{l}", sh.rows, H) if P["att"] is not None else None
+            hf.aggregate_bwd(sh, csrs[l], self.agg, D, H, self.slope, G, a["Y"], a["s_src"],
+                             a["s_dst"], a["stats"], dY, ds_src, ds_dst,
+                             self._ws(hf.aggregate_bwd_ws_bytes(sh, self.agg, H)))
+            dX = self._mat(f"dH{l - 1}", sh.src_rows, D) if l > 0 else None
+            hf.project_bwd(sh, csrs[l], a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"],
+                           P["att"], a["Y"], dY, G, ds_src, ds_dst, dX, Gr["W_rel"], Gr["W_root"],
+                           Gr["att"], self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H)),
+                           prec=self.prec)
+            dH = dX
+        if allreduce is not None:
+            allreduce(self.grads)
+        if update:
+            hf.sgd(self.params, self.grads, self.lr, 1.0 / world)
+        self.last = dict(acts=acts, csrs=csrs)
+        return self.loss

@@ -1,0 +1,85 @@
+"""-m gpu: hifuse_build_semantic_graphs bit-exact against the oracle's O1
+(Alg. 2), on random blocks (empty, ragged, hub columns, many
+relations, invalid edges) and on sampled batches of every configuration."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import CONFIGS, generate_graph, make_batch, random_block, random_schema
+from synth.sampler import LayerBlock
+
+from gpu_util import needs_gpu, gpu_build, csr_host, assert_build_equal
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+def _check(blk, et, rs, rd):
+    sh, csr, st = gpu_build(blk, et, rs, rd)
+    ref = oracle.build(oracle.Shape.of(blk, rs, rd), blk, et)
+    assert_build_equal(csr_host(sh, csr), ref)
+    assert int(st.item()) == ref["status"]
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_blocks(seed):
+    rng = np.random.default_rng(1000 + seed)
+    T = int(rng.integers(1, 6))
+    R = int(rng.integers(1, 40))
+    rs, rd = random_schema(rng, T, R)
+    n_src = rng.integers(0, 300, T)
+    n_dst = np.minimum(rng.integers(0, 200, T), n_src)
+    if not any(n_src[rs[k]] > 0 and n_dst[rd[k]] > 0 for k in range(R)):
+        n_src[:] = 50; n_dst[:] = 20
+    N = int(rng.integers(0, 5000))
+    blk, et = random_block(rng, n_src, n_dst, rs, rd, N, hub_frac=[0, 0.05, 0.5][seed % 3])
+    _check(blk, et, rs, rd)
+
+
+def test_empty_block():
+    rng = np.random.default_rng(1)
+    blk, et = random_block(rng, [5, 3], [2, 1], [0, 1], [1, 0], 0)
+    _check(blk, et, [0, 1], [1, 0])
+
+
+def test_long_rows_and_huge_column():
+    """Rows longer than 32 and a column beyond the shared-memory bitonic cap
+    (8192) exercise both long-segment sort paths."""
+    rng = np.random.default_rng(2)
+    n = 20000
+    src = np.zeros(n, np.int32)
+    src[::3] = rng.integers(0, 50, len(src[::3]))
+    dst = rng.integers(0, 40, n).astype(np.int32)
+    blk = LayerBlock(n_src=np.array([100], np.int32), n_dst=np.array([40], np.int32),
+                     src_local=src, dst_local=dst, edge_id=rng.integers(0, 10, n),
+                     src_global=[np.arange(100)])
+    _check(blk, np.zeros(10, np.int32), [0], [0])
+
+
+def test_invalid_edges_status_and_drop():
+    blk = LayerBlock(n_src=np.array([3], np.int32), n_dst=np.array([2], np.int32),
+                     src_local=np.array([0, 5, 1, 0, 2], np.int32),
+                     dst_local=np.array([0, 0, 9, 1, 1], np.int32),
+                     edge_id=np.array([0, 1, 2, 99, 3], np.int64), src_global=[np.arange(3)])
+    _check(blk, np.array([0, 0, 0, 7], np.int32), [0], [0])
+
+
+@pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag"])
+def test_sampled_batches(key):
+    cfg = CONFIGS[key]
+    g = generate_graph(cfg)
+    mb = make_batch(cfg, g, 0)
+    rs = np.array([r.src for r in cfg.rels], np.int32)
+    rd = np.array([r.dst for r in cfg.rels], np.int32)
+    for blk in mb.layers:
+        _check(blk, g.edge_type, rs, rd)
+
+
+def test_deterministic_across_runs():
+    rng = np.random.default_rng(9)
+    rs, rd = random_schema(rng, 3, 12)
+    blk, et = random_block(rng, [400, 300, 200], [100, 80, 60], rs, rd, 8000, hub_frac=0.1)
+    a = csr_host(*gpu_build(blk, et, rs, rd)[:2])
+    for _ in range(3):
+        b = csr_host(*gpu_build(blk, et, rs, rd)[:2])
+        assert_build_equal(b, a)

@@ -1,0 +1,234 @@
+"""-m gpu: stage-isolated parity of the CUDA path against the oracle.
+
+Each stage's oracle consumes the GPU's own inputs of that stage (e.g. A4's
+oracle reads the GPU's Y), so error never leaks between stages.  Tolerances
+(DESIGN.md §Tolerances): fp32 aggregation / fusion / their backward
+|g - r| <= 1e-5 max(|r|, A) with A the absolute-sum scale of the element;
+projection row-relative L2 <= 2e-3; integer-valued inputs are bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import random_block, random_schema
+
+from gpu_util import needs_gpu, gpu_build, csr_host, close_scaled, row_rel_l2, t, DEV, hf
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+def make_case(seed, D=128, H=1, N=None, T=None, R=None, hub=0.0):
+    rng = np.random.default_rng(seed)
+    T = T or int(rng.integers(1, 5))
+    R = R or int(rng.integers(1, 12))
+    rs, rd = random_schema(rng, T, R)
+    n_src = rng.integers(1, 400, T)
+    n_dst = np.maximum(np.minimum(rng.integers(0, 250, T), n_src), 1)
+    N = int(rng.integers(100, 6000)) if N is None else N
+    blk, et = random_block(rng, n_src, n_dst, rs, rd, N, hub_frac=hub)
+    sh, csr, st = gpu_build(blk, et, rs, rd)
+    ch = csr_host(sh, csr)
+    return rng, blk, et, rs, rd, sh, csr, ch
+
+
+def agg_oracle(blk, et, rs, rd, ch, agg, D, H, Y, ss=None, sd=None):
+    osh = oracle.Shape.of(blk, rs, rd)
+    return oracle.aggregate_fwd(osh, blk, et, ch, agg, D, H, Y, ss, sd)
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("agg", ["sum", "mean"])
+@pytest.mark.parametrize("seed", range(4))
+def test_aggregate_fwd(seed, agg, D):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(10 + seed, D=D, hub=0.1 * (seed % 2))
+    U = ch["U"]
+    Y = rng.standard_normal((max(U, 1), D)).astype(np.float32)
+    Z = torch.zeros(max(sh.rows, 1), D, device=DEV)
+    hf().aggregate_fwd(csr, sh.rows, agg, D, 1, 0.2, t(Y), None, None, Z, None)
+    ref = agg_oracle(blk, et, rs, rd, ch, agg, D, 1, Y[:U])
+    A = agg_oracle(blk, et, rs, rd, ch, agg, D, 1, np.abs(Y[:U]))["Z"]
+    close_scaled(Z.cpu().numpy()[:sh.rows], ref["Z"], A, what=f"Z {agg}")
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_aggregate_integer_inputs_bit_exact(D):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(77, D=D, N=5000)
+    U = ch["U"]
+    Y = rng.integers(-8, 9, (U, D)).astype(np.float32)
+    for agg in ("sum", "mean"):
+        Z = torch.zeros(sh.rows, D, device=DEV)
+        hf().aggregate_fwd(csr, sh.rows, agg, D, 1, 0.2, t(Y), None, None, Z, None)
+        ref = agg_oracle(blk, et, rs, rd, ch, "sum", D, 1, Y)
+        exp = ref["Z"].astype(np.float32)
+        if agg == "mean":   # reading C19: float32(sum) / float32(deg), IEEE division
+            deg = ref["deg"].astype(np.float32)
+            exp = np.where(deg[:, None] > 0, exp / np.maximum(deg, 1)[:, None], 0).astype(np.float32)
+        assert np.array_equal(Z.cpu().numpy(), exp), agg
+
+
+@pytest.mark.parametrize("D,H", [(128, 8), (64, 8), (128, 1), (64, 2)])
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_fwd_gat(seed, D, H):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(30 + seed, D=D, H=H, hub=0.05)
+    U = ch["U"]
+    Y = rng.standard_normal((U, D)).astype(np.float32)
+    ss = (rng.standard_normal((U, H)) * 2).astype(np.float32)
+    sd = (rng.standard_normal((sh.rows, H)) * 2).astype(np.float32)
+    Z = torch.zeros(sh.rows, D, device=DEV)
+    stats = torch.zeros(sh.rows, 2 * H, device=DEV)
+    hf().aggregate_fwd(csr, sh.rows, "gat", D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
+    ref = agg_oracle(blk, et, rs, rd, ch, "gat", D, H, Y, ss, sd)
+    A = agg_oracle(blk, et, rs, rd, ch, "gat", D, H, np.abs(Y), ss, sd)["Z"]
+    close_scaled(Z.cpu().numpy(), ref["Z"], A, what="Z gat")
+    # stats reproduce sum of alpha = 1: l = sum exp(l_e - m)
+    st = stats.cpu().numpy()
+    nz = ref["deg"] > 0
+    assert np.all(st[nz, H:] >= 1.0 - 1e-6)
+
+
+def test_gat_zero_attention_equals_mean():
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(41, D=128, H=8)
+    U = ch["U"]
+    Y = t(rng.standard_normal((U, 128)).astype(np.float32))
+    Zg = torch.zeros(sh.rows, 128, device=DEV)
+    Zm = torch.zeros(sh.rows, 128, device=DEV)
+    st = torch.zeros(sh.rows, 16, device=DEV)
+    hf().aggregate_fwd(csr, sh.rows, "gat", 128, 8, 0.2, Y, torch.zeros(U, 8, device=DEV),
+                       torch.zeros(sh.rows, 8, device=DEV), Zg, st)
+    hf().aggregate_fwd(csr, sh.rows, "mean", 128, 1, 0.2, Y, None, None, Zm, None)
+    torch.testing.assert_close(Zg, Zm, rtol=2e-6, atol=1e-7)
+
+
+def _gmap_rows(sh, ch, G):
+    tdo = sh.type_dst_off
+    out = np.zeros((sh.rows, G.shape[1]))
+    for r in range(sh.R):
+        tt = sh.rel_dst[r]
+        a = ch["rel_row_off"][r]
+        out[a:a + sh.n_dst[tt]] = G[tdo[tt]:tdo[tt + 1]]
+    return out
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("agg", ["sum", "mean"])
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_bwd(seed, agg, D):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(50 + seed, D=D, hub=0.2 * (seed % 2))
+    U = ch["U"]
+    G = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    dY = torch.zeros(max(sh.U_max, 1), D, device=DEV)
+    hf().aggregate_bwd(sh, csr, agg, D, 1, 0.2, t(G), None, None, None, None, dY, None, None,
+                       None)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, 1, G, np.zeros((U, D)))
+    A = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, 1, np.abs(G), np.zeros((U, D)))["dY"]
+    close_scaled(dY.cpu().numpy()[:U], ref["dY"], A, what="dY")
+
+
+@pytest.mark.parametrize("D,H", [(128, 8), (64, 8)])
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_bwd_gat(seed, D, H):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(60 + seed, D=D, H=H, hub=0.1)
+    U = ch["U"]
+    Y = rng.standard_normal((U, D)).astype(np.float32)
+    ss = rng.standard_normal((U, H)).astype(np.float32)
+    sd = rng.standard_normal((sh.rows, H)).astype(np.float32)
+    G = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    Z = torch.zeros(sh.rows, D, device=DEV)
+    stats = torch.zeros(sh.rows, 2 * H, device=DEV)
+    hf().aggregate_fwd(csr, sh.rows, "gat", D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
+    dY = torch.zeros(U, D, device=DEV)
+    dss = torch.zeros(U, H, device=DEV)
+    dsd = torch.zeros(sh.rows, H, device=DEV)
+    ws = torch.empty(hf().aggregate_bwd_ws_bytes(sh, "gat", H) // 4 + 16, device=DEV)
+    hf().aggregate_bwd(sh, csr, "gat", D, H, 0.2, t(G), t(Y), t(ss), t(sd), stats, dY, dss, dsd,
+                       ws)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.aggregate_bwd(osh, blk, et, ch, "gat", D, H, G, Y, ss, sd)
+    # scale: magnitude of the per-element sums (|G| |Y| bound), row-wise
+    sc_y = oracle.aggregate_bwd(osh, blk, et, ch, "gat", D, H, np.abs(G), np.abs(Y), ss, sd)
+    close_scaled(dY.cpu().numpy(), ref["dY"], sc_y["dY"], rtol=2e-5, what="dY gat")
+    # ds: compare against the scale of |alpha * dalpha| sums (sum |.| of terms)
+    scale_s = np.abs(sc_y["ds_src"]) + np.abs(ref["ds_src"]) + 1e-3
+    close_scaled(dss.cpu().numpy(), ref["ds_src"], scale_s, rtol=5e-5, what="ds_src")
+    scale_d = np.abs(sc_y["ds_dst"]) + np.abs(ref["ds_dst"]) + 1e-3
+    close_scaled(dsd.cpu().numpy(), ref["ds_dst"], scale_d, rtol=5e-5, what="ds_dst")
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_fuse_and_fuse_bwd(D):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(70, D=D, T=4, R=9)
+    Z = rng.standard_normal((sh.rows, D)).astype(np.float32)
+    R0 = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    b = rng.standard_normal((sh.T, D)).astype(np.float32)
+    Hg = torch.zeros(sh.dst_rows, D, device=DEV)
+    hf().semantic_fuse(sh, D, "relu", t(Z), t(R0), t(b), Hg)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.fuse(osh, D, 1, Z, R0, b)
+    A = oracle.fuse(osh, D, 0, np.abs(Z), np.abs(R0), np.abs(b))
+    close_scaled(Hg.cpu().numpy(), ref, A, what="H")
+    dH = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    G = torch.zeros(sh.dst_rows, D, device=DEV)
+    db = torch.zeros(sh.T, D, device=DEV)
+    ws = torch.empty(hf().fuse_bwd_ws_bytes(sh, D) // 4 + 16, device=DEV)
+    hf().semantic_fuse_bwd(sh, D, "relu", t(dH), Hg, G, db, ws)
+    Gr, dbr = oracle.fuse_bwd(osh, D, 1, dH, Hg.cpu().numpy())
+    assert np.array_equal(G.cpu().numpy(), Gr.astype(np.float32))
+    _, dbA = oracle.fuse_bwd(osh, D, 1, np.abs(dH), Hg.cpu().numpy())
+    close_scaled(db.cpu().numpy(), dbr, dbA, what="dbias")
+
+
+@pytest.mark.parametrize("K,D,H,att", [(128, 128, 1, False), (64, 64, 1, False), (128, 64, 1, False),
+                                       (64, 128, 1, False), (128, 128, 8, True), (64, 64, 8, True)])
+@pytest.mark.parametrize("prec", ["fp32"])
+def test_project_fwd_bwd(K, D, H, att, prec):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(90 + K + D, D=D, H=H, T=3, R=7, hub=0.05)
+    U = ch["U"]
+    xr = sh.src_rows + 11
+    X = rng.standard_normal((xr, K)).astype(np.float32)
+    gid = rng.permutation(xr)[:sh.src_rows].astype(np.int32)
+    W = (rng.standard_normal((sh.R, K, D)) / np.sqrt(K)).astype(np.float32)
+    Wr = None if att else (rng.standard_normal((sh.T, K, D)) / np.sqrt(K)).astype(np.float32)
+    A = (rng.standard_normal((sh.R, 2, D))).astype(np.float32) if att else None
+    Y = torch.zeros(max(sh.U_max, 1), D, device=DEV)
+    R0 = torch.zeros(sh.dst_rows, D, device=DEV) if Wr is not None else None
+    ss = torch.zeros(max(sh.U_max, 1), H, device=DEV) if att else None
+    sd = torch.zeros(sh.rows, H, device=DEV) if att else None
+    ws = torch.empty(hf().project_ws_bytes(sh, K, D, H) // 4 + 16, device=DEV)
+    tn = lambda a: None if a is None else t(a)
+    hf().project(sh, csr, K, D, H, t(X), t(gid, torch.int32), t(W), tn(Wr), tn(A), Y, R0, ss, sd,
+                 ws, prec=prec)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.project(osh, ch, K, D, H, X, gid, W, Wr, A)
+    tol = 2e-3 if prec != "fp32" else 1e-5
+    row_rel_l2(Y.cpu().numpy()[:U], ref["Y"], tol, "Y")
+    if Wr is not None:
+        row_rel_l2(R0.cpu().numpy(), ref["R0"], tol, "R0")
+    if att:
+        row_rel_l2(ss.cpu().numpy()[:U], ref["s_src"], 1e-4, "s_src")
+        row_rel_l2(sd.cpu().numpy(), ref["s_dst"], 1e-4, "s_dst")
+    # backward (X without gather for dX)
+    Xl = rng.standard_normal((sh.src_rows, K)).astype(np.float32)
+    dYn = rng.standard_normal((max(U, 1), D)).astype(np.float32)
+    Gn = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    dssn = rng.standard_normal((max(U, 1), H)).astype(np.float32) if att else None
+    dsdn = rng.standard_normal((sh.rows, H)).astype(np.float32) if att else None
+    Yl = rng.standard_normal((max(U, 1), D)).astype(np.float32)
+    dYg = t(dYn)
+    dX = torch.zeros(sh.src_rows, K, device=DEV)
+    dW = torch.zeros(sh.R, K, D, device=DEV)
+    dWr = torch.zeros(sh.T, K, D, device=DEV) if Wr is not None else None
+    datt = torch.zeros(sh.R, 2, D, device=DEV) if att else None
+    wsb = torch.empty(hf().project_bwd_ws_bytes(sh, K, D, H) // 4 + 16, device=DEV)
+    hf().project_bwd(sh, csr, K, D, H, t(Xl), None, t(W), tn(Wr), tn(A), t(Yl), dYg, t(Gn),
+                     tn(dssn), tn(dsdn), dX, dW, dWr, datt, wsb, prec=prec)
+    ob = oracle.project_bwd(osh, ch, K, D, H, Xl, None, W, Wr, A, Yl[:U], dYn[:U], Gn,
+                            None if dssn is None else dssn[:U], dsdn)
+    wt = 1e-4
+    row_rel_l2(dW.cpu().numpy().reshape(-1, D), ob["dW_rel"].reshape(-1, D), wt, "dW_rel")
+    if Wr is not None:
+        row_rel_l2(dWr.cpu().numpy().reshape(-1, D), ob["dW_root"].reshape(-1, D), wt, "dW_root")
+    row_rel_l2(dX.cpu().numpy(), ob["dX"], wt, "dX")
+    if att:
+        row_rel_l2(datt.cpu().numpy().reshape(-1, D), ob["datt"].reshape(-1, D), wt, "datt")

@@ -1,0 +1,113 @@
+"""-m gpu: a whole training step (build, forward, loss, backward, SGD) through
+the C ABI against the oracle model, on the first sampled batch of every
+BASELINE.json configuration at full size, plus launch-count independence
+from R (the paper's kernel-count claim)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle.model as om
+from synth import CONFIGS, generate_graph, generate_features, make_batch, make_params
+
+from gpu_util import needs_gpu, DEV, hf
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+_cache = {}
+
+
+def setup(key):
+    if key not in _cache:
+        cfg = CONFIGS[key]
+        g = generate_graph(cfg)
+        feat, foff = generate_features(cfg.type_counts, cfg.feat_dim)
+        _cache[key] = (cfg, g, feat, foff)
+    return _cache[key]
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag"])
+def test_step_matches_oracle(key):
+    from paper_2408_08490_b200.step import Trainer, DeviceBatch
+    cfg, g, feat, foff = setup(key)
+    mb = make_batch(cfg, g, 0)
+    rs = np.array([r.src for r in cfg.rels], np.int32)
+    rd = np.array([r.dst for r in cfg.rels], np.int32)
+    params = make_params(cfg)
+    tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
+                 cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0)
+    tr.load_params(params)
+    db = DeviceBatch(mb, rs, rd, foff, cfg.target_type, DEV)
+    feat_d = torch.from_numpy(feat).to(DEV)
+    et_d = torch.from_numpy(g.edge_type).to(DEV)
+    loss = tr.step(db, feat_d, et_d, update=False)
+    torch.cuda.synchronize()
+    assert hf().read_status(tr.status) == 0
+    # oracle on the gathered layer-0 rows (same values as the global store)
+    gid = mb.gather_ids(foff)
+    X0 = feat[gid].astype(np.float64)
+    fw = om.forward(mb.layers, g.edge_type, rs, rd, X0, np.arange(len(gid), dtype=np.int32),
+                    params, cfg.agg, cfg.heads, labels=mb.labels, target_type=cfg.target_type)
+    gr = om.backward(fw, mb.layers, g.edge_type, params, mb.labels, cfg.agg, cfg.heads)
+    assert abs(float(loss.item()) - fw["loss"]) <= 1e-5 * max(1.0, abs(fw["loss"]))
+    tol = 2e-4
+    checks = [("Wc", gr["Wc"]), ("bc", gr["bc"])]
+    for l in range(cfg.num_layers):
+        for k in ("W_rel", "W_root", "bias", "att"):
+            if gr["layers"][l][k] is not None and f"{l}.{k}" in tr.Gd:
+                checks.append((f"{l}.{k}", gr["layers"][l][k]))
+    for name, ref in checks:
+        err = rel_l2(tr.Gd[name].cpu().numpy(), ref)
+        assert err <= tol, f"{key} grad {name}: rel L2 {err:.3e}"
+    # logits-level: the last layer's H on the seeds
+    last = tr.last["acts"][-1]["H"][db.h_row0:db.h_row0 + db.B].cpu().numpy()
+    err = rel_l2(last, fw["hs"])
+    assert err <= 1e-5, f"{key} H: {err:.3e}"
+
+
+def test_sgd_update_and_determinism():
+    from paper_2408_08490_b200.step import Trainer, DeviceBatch
+    cfg, g, feat, foff = setup("dblp")
+    rs = np.array([r.src for r in cfg.rels], np.int32)
+    rd = np.array([r.dst for r in cfg.rels], np.int32)
+    feat_d = torch.from_numpy(feat).to(DEV)
+    et_d = torch.from_numpy(g.edge_type).to(DEV)
+    outs = []
+    for _ in range(2):
+        tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
+                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.05)
+        tr.load_params(make_params(cfg))
+        p0 = tr.params.clone()
+        losses = []
+        for b in range(3):
+            db = DeviceBatch(make_batch(cfg, g, b), rs, rd, foff, cfg.target_type, DEV)
+            losses.append(float(tr.step(db, feat_d, et_d).item()))
+        outs.append((losses, tr.params.clone()))
+        assert not torch.equal(p0, tr.params)
+    assert outs[0][0] == outs[1][0]
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
+def test_kernel_count_independent_of_relations():
+    """Forward kernels per layer do not grow with R (merged path)."""
+    from synth import random_block, random_schema
+    from gpu_util import gpu_build
+    counts = []
+    for R in (4, 36, 144):
+        rng = np.random.default_rng(R)
+        rs, rd = random_schema(rng, 4, R)
+        blk, et = random_block(rng, [500] * 4, [100] * 4, rs, rd, 3000)
+        sh, csr, _ = gpu_build(blk, et, rs, rd)
+        Y = torch.randn(max(sh.U_max, 1), 128, device=DEV)
+        Z = torch.zeros(sh.rows, 128, device=DEV)
+        H = torch.zeros(sh.dst_rows, 128, device=DEV)
+        n0 = hf().kernel_launches()
+        hf().aggregate_fwd(csr, sh.rows, "mean", 128, 1, 0.2, Y, None, None, Z, None)
+        hf().semantic_fuse(sh, 128, "relu", Z, None, None, H)
+        counts.append(hf().kernel_launches() - n0)
+    assert counts[0] == counts[1] == counts[2] == 2
