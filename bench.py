@@ -1,0 +1,411 @@
+"""bench.py -- mini-batches/s of the HiFuse hot path on B200 (BASELINE.json metric).
+
+One step = one pass of the whole hot path over one sampled mini-batch:
+semantic-graph build of every layer (A1), per layer projection (A2+A3),
+merged aggregation (A4) and fusion (A5), classifier + loss, the backward of
+every stage (A6), the NCCL gradient all-reduce (N > 1) and the SGD update.
+Inputs (sampled batch pool, type-major feature store) are device resident when
+the timed region starts; sampling is outside the library boundary (PAPER.md
+Fig. 2 step (1)) and is done on the host before timing.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config mag] [--impl hifuse|reference]
+
+N > 1 runs under torch.distributed.run, one rank per GPU, data-parallel over
+independent mini-batches (rank k takes batches k, k+N, ...), weak scaling.
+`--impl reference` times the CPU oracle (oracle/, plain C, fp64) on the host
+as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, generate_graph, generate_features, make_batch, make_params  # noqa: E402
+
+ALU_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # CUDA-core fp32 FMA peak at max clock
+TF32_OVER_BF16 = 1.1 / 2.25                         # nominal dense ratio (B200_PROFILING.md)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d["bf16_tflops_sustained"],
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    FIELDS = ("index,timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(gpu_index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        sel = [r for (ts, r) in self.rows if t0 - 0.06 <= ts <= t1 + 0.06] or \
+              [r for (_, r) in self.rows[-3:]]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[2]) for r in sel if r[2].replace(".", "").isdigit()]
+        mx = [float(r[3]) for r in sel if r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in sel for i in range(4)
+                          if len(r) > 6 + i and r[6 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sel)}
+
+
+# --------------------------------------------------------- algorithmic cost --
+def layer_sizes(cfg, g, mb, rs, rd):
+    """Per layer: N, rows, U (compact Y rows), dst_rows, src_rows (host-side
+    counts of the sampled block; used only for the roofline arithmetic)."""
+    out = []
+    for blk in mb.layers:
+        r = g.edge_type[blk.edge_id]
+        U = len(np.unique(r.astype(np.int64) * (1 << 32) + blk.src_local)) if blk.num_edges else 0
+        rows = int(sum(int(blk.n_dst[rd[k]]) for k in range(len(rd))))
+        out.append(dict(N=blk.num_edges, rows=rows, U=U, dst=int(blk.n_dst.sum()),
+                        src=int(blk.n_src.sum())))
+    return out
+
+
+def stage_cost(stage, l, cfg, sz):
+    """(bytes, flops) an ideal implementation must move / execute per launch
+    (DESIGN.md §Roofline)."""
+    s = sz[l]
+    D = cfg.hidden
+    K = cfg.feat_dim if l == 0 else D
+    H = cfg.heads if cfg.model == "rgat" else 1
+    root = cfg.model == "rgcn"
+    R, T = cfg.num_rels, cfg.num_types
+    if stage == "aggregate_fwd":
+        b = 4 * D * s["U"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * D * s["rows"]
+        if cfg.model == "rgat":
+            b += 4 * H * s["U"] + 4 * H * s["rows"] + 8 * H * s["rows"]
+        return b, 0
+    if stage == "aggregate_bwd":
+        b = 4 * D * s["dst"] + 8 * s["N"] + 4 * (s["U"] + 1) + 4 * D * s["U"]
+        if cfg.model == "rgat":
+            b += 4 * D * s["U"] + 4 * H * s["N"]
+        return b, 0
+    if stage == "project":
+        m = s["U"] + (s["dst"] if root else 0)
+        return 4 * K * m + 4 * D * m + 4 * (R + T) * K * D, 2 * K * D * m
+    if stage == "project_bwd":
+        m = s["U"] + (s["dst"] if root else 0)
+        f = 2 * K * D * m * (2 if l > 0 else 1)
+        return 4 * K * m + 4 * D * m + (4 * s["src"] * K if l > 0 else 0), f
+    if stage == "fuse":
+        return 4 * D * (s["rows"] + 2 * s["dst"]), 0
+    if stage == "fuse_bwd":
+        return 4 * D * 3 * s["dst"], 0
+    return 0, 0
+
+
+# -------------------------------------------------------------- reference ---
+def run_reference(args, cfg):
+    """The CPU oracle as the reference arm: each step = oracle forward +
+    backward of one full mini-batch (fp64, 1 thread)."""
+    import oracle.model as om
+    from threadpoolctl import threadpool_limits
+    g = generate_graph(cfg)
+    feat, foff = generate_features(cfg.type_counts, cfg.feat_dim)
+    params = make_params(cfg)
+    rs = np.array([r.src for r in cfg.rels], np.int32)
+    rd = np.array([r.dst for r in cfg.rels], np.int32)
+    nb = -(-cfg.type_counts[cfg.target_type] // cfg.batch_size)
+    pool = [make_batch(cfg, g, b % nb, epoch=b // nb)
+            for b in range(max(1, min(4, args.steps + args.warmup)))]
+
+    def one(mb):
+        gid = mb.gather_ids(foff)
+        fw = om.forward(mb.layers, g.edge_type, rs, rd, feat[gid].astype(np.float64),
+                        np.arange(len(gid), dtype=np.int32), params, cfg.agg, cfg.heads,
+                        labels=mb.labels, target_type=cfg.target_type)
+        om.backward(fw, mb.layers, g.edge_type, params, mb.labels, cfg.agg, cfg.heads)
+
+    with threadpool_limits(1):
+        for i in range(args.warmup):
+            one(pool[i % len(pool)])
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            one(pool[i % len(pool)])
+        dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": "mini-batches/sec", "value": v,
+            "unit": "mini-batches/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_obj(cfg, args),
+            "cpu_baseline": {"value": v, "unit": "mini-batches/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} full {cfg.key} mini-batches, fwd+bwd, "
+                                       "plain-C fp64 oracle, 1 thread"},
+            "e2e": {"value": v, "unit": "mini-batches/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def config_obj(cfg, args, extra=None):
+    d = {"workload": f"{cfg.key}: {cfg.description}", "model": cfg.model,
+         "global_batch": cfg.batch_size * args.gpus, "fanout": list(cfg.fanout),
+         "hidden": cfg.hidden, "heads": cfg.heads, "relations": cfg.num_rels,
+         "parallelism": f"dp{args.gpus}", "precision": args.prec,
+         "l2": "inputs larger than L2: a pool of distinct sampled batches, per-step working "
+               "set above the 126 MB L2 for mag"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ------------------------------------------------------------------- main ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="mag", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="hifuse", choices=["hifuse", "reference"])
+    ap.add_argument("--pool", type=int, default=16)
+    ap.add_argument("--prec", default="fp32", choices=["fp32", "tf32"])
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+    from paper_2408_08490_b200 import hifuse as hf
+    from paper_2408_08490_b200.step import Trainer, DeviceBatch
+
+    g = generate_graph(cfg)
+    feat, foff = generate_features(cfg.type_counts, cfg.feat_dim)
+    params = make_params(cfg)
+    rs = np.array([r.src for r in cfg.rels], np.int32)
+    rd = np.array([r.dst for r in cfg.rels], np.int32)
+    nb = -(-cfg.type_counts[cfg.target_type] // cfg.batch_size)   # batches per epoch
+    ids = [rank + s * world for s in range(args.pool)]
+    mbs = [make_batch(cfg, g, b % nb, epoch=b // nb) for b in ids]
+    pool = [DeviceBatch(mb, rs, rd, foff, cfg.target_type, dev, pin=True) for mb in mbs]
+    sizes = [layer_sizes(cfg, g, mb, rs, rd) for mb in mbs]
+    feat_d = torch.from_numpy(feat).to(dev)
+    et_d = torch.from_numpy(g.edge_type).to(dev)
+    tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
+                 cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
+                 prec=args.prec)
+    tr.load_params(params)
+    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    # sizing pass: every pool batch once, eagerly (buffers reach final size)
+    for db in pool:
+        tr.step(db, feat_d, et_d, allreduce=allreduce, world=world, update=False)
+    torch.cuda.synchronize()
+    if hf.read_status(tr.status) != 0:
+        raise RuntimeError("device reported invalid edges in the batch pool")
+    # one CUDA graph per pool batch: the whole step is replayed without host
+    # launch overhead (all sizes are host-known, nothing syncs inside)
+    graphs = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_step(i, e2e=False, loss_host=None):
+        db = pool[i % len(pool)]
+        if e2e:
+            db.to_device(non_blocking=True)
+        graphs[i % len(pool)][0].replay()
+        if world > 1:
+            dist.all_reduce(tr.grads)
+            hf.sgd(tr.params, tr.grads, tr.lr, 1.0 / world)
+        if e2e:
+            loss_host.copy_(tr.loss, non_blocking=True)
+
+    def timed(K, e2e=False):
+        loss_host = torch.empty(1, dtype=torch.float32).pin_memory() if e2e else None
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        t0 = time.time()
+        a.record()
+        for i in range(K):
+            one_step(i, e2e, loss_host)
+        b.record()
+        b.synchronize()
+        t1 = time.time()
+        barrier()
+        ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, t0, t1
+
+    for i in range(args.warmup):
+        one_step(i)
+    clocks = ClockSampler(local)
+    time.sleep(0.25)
+    ms, t0, t1 = timed(args.steps)
+    launches = sum(graphs[i % len(pool)][1] for i in range(args.steps)) + \
+        (args.steps if world > 1 else 0)
+    clk = clocks.summary(t0, t1)
+    # end-to-end through the public API with host (pinned) buffers
+    for i in range(args.warmup):
+        one_step(i, True, torch.empty(1).pin_memory())
+    ms_e2e, _, _ = timed(args.steps, e2e=True)
+    clocks.stop()
+    # per-stage device time: every library call of the step captured as its
+    # own graph and replayed back to back between CUDA events (the dominant
+    # kernel's roofline below comes from these)
+    stage_ms = {}
+    reps = 5
+    for pi, db in enumerate(pool[:min(len(pool), 8)]):
+        for name, g_, _ in tr.capture_stages(db, feat_d, et_d):
+            g_.replay()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                g_.replay()
+            b.record()
+            b.synchronize()
+            stage_ms.setdefault(name, []).append((pi, a.elapsed_time(b) / reps))
+        del g_
+    # restore a consistent state (stage replays repeat in-place updates)
+    tr.load_params(params)
+
+    value = world * args.steps / (ms / 1e3)
+    e2e_v = world * args.steps / (ms_e2e / 1e3)
+    h2d = float(np.mean([pool[i % len(pool)].h2d_bytes() for i in range(args.steps)]))
+    pk = peaks()
+    step_ms = ms / args.steps
+    per_step = {k: float(np.mean([t for _, t in v])) for k, v in stage_ms.items()}
+    dom = max(per_step, key=lambda k: per_step[k])
+    name, _, layer = dom.partition(".")
+    l = int(layer) if layer else 0
+    used = [pi for pi, _ in stage_ms[dom]]
+    avg_bytes = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[0] for pi in used]))
+    avg_flops = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[1] for pi in used]))
+    t_s = per_step[dom] / 1e3
+    if name in ("project", "project_bwd") and args.prec == "fp32":
+        roof = {"bound": "alu", "achieved": avg_flops / t_s / 1e12, "peak": ALU_FP32_TFLOPS,
+                "unit": "TFLOP/s"}
+    elif name in ("project", "project_bwd"):
+        bw_time = avg_bytes / (pk["hbm"] * 1e9)
+        fl_time = avg_flops / (pk["bf16"] * TF32_OVER_BF16 * 1e12)
+        if bw_time >= fl_time:
+            roof = {"bound": "hbm", "achieved": avg_bytes / t_s / 1e9, "peak": pk["hbm"],
+                    "unit": "GB/s"}
+        else:
+            roof = {"bound": "tensor", "achieved": avg_flops / t_s / 1e12,
+                    "peak": pk["bf16"] * TF32_OVER_BF16, "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": avg_bytes / t_s / 1e9, "peak": pk["hbm"],
+                "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = dom
+    roof["peak_source"] = pk["src"]
+    roof["algorithmic"] = {"bytes": avg_bytes, "flops": avg_flops, "us": per_step[dom] * 1e3}
+    roof["share_of_step"] = per_step[dom] / step_ms
+    agg_gbs = {}
+    for k in per_step:
+        if k.startswith("aggregate_fwd"):
+            ll = int(k.split(".")[1])
+            b = float(np.mean([stage_cost("aggregate_fwd", ll, cfg, sizes[pi])[0]
+                               for pi, _ in stage_ms[k]]))
+            agg_gbs[k] = {"GB/s": b / (per_step[k] / 1e3) / 1e9, "us": per_step[k] * 1e3,
+                          "frac_of_hbm": b / (per_step[k] / 1e3) / 1e9 / pk["hbm"]}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, g, feat, foff, params, rs, rd, mbs)
+    line = {
+        "metric": "mini-batches/sec", "value": value, "unit": "mini-batches/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded heterograph + sampler, random-init weights)",
+        "config": config_obj(cfg, args),
+        "clocks": clk,
+        "e2e": {"value": e2e_v, "unit": "mini-batches/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "aggregation_hbm": agg_gbs,
+        "stage_us_per_step": {k: round(v * 1e3, 2) for k, v in sorted(per_step.items())},
+        "launch_mode": "one CUDA graph per pool batch (whole step)",
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cfg, g, feat, foff, params, rs, rd, mbs):
+    """The oracle, as it stands, on a bounded sample of the same workload."""
+    import oracle.model as om
+    from threadpoolctl import threadpool_limits
+    n = 2 if cfg.key == "mag" else 8
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        for mb in mbs[:n]:
+            gid = mb.gather_ids(foff)
+            fw = om.forward(mb.layers, g.edge_type, rs, rd, feat[gid].astype(np.float64),
+                            np.arange(len(gid), dtype=np.int32), params, cfg.agg, cfg.heads,
+                            labels=mb.labels, target_type=cfg.target_type)
+            om.backward(fw, mb.layers, g.edge_type, params, mb.labels, cfg.agg, cfg.heads)
+        dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "mini-batches/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} {cfg.key} mini-batches (fwd+bwd, plain-C fp64 oracle, 1 thread)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -171,23 +171,18 @@ struct BwdMeta {
   int shift[HF_MAX_R];   // type_dst_off[t(r)] - rel_row_off[r]
 };
 
+// Columns longer than kLongCol (hub sources) are handed to a block-wide
+// kernel so that no single warp serialises thousands of gathers.
+static constexpr int kLongCol = 128;
+
 template <int D, bool MEAN>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __restrict__ rel_y_off,
-          const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
-          const int* __restrict__ row_ptr, const float4* __restrict__ G, float4* __restrict__ dY) {
+__device__ __forceinline__ float4 col_slice_sum(int b, int e, int shift,
+                                                const int* __restrict__ csc_row,
+                                                const int* __restrict__ row_ptr,
+                                                const float4* __restrict__ G, int lane) {
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
-  __shared__ int s_yoff[HF_MAX_R + 1];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
   const int sl = lane % LPR, sid = lane / LPR;
-  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (u >= *U_dev) return;
-  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
-  const int shift = bm.shift[r];
-  const int b = col_ptr[u], e = col_ptr[u + 1];
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int base = b; base < e; base += 32) {
     const int n = min(32, e - base);
@@ -224,7 +219,61 @@ k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __res
   }
 #pragma unroll
   for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
-  if (sid == 0) dY[(long long)u * LPR + sl] = acc;
+  return acc;
+}
+
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_long(BwdMeta bm, const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
+               const int* __restrict__ csc_row, const int* __restrict__ row_ptr,
+               const float4* __restrict__ G, float4* __restrict__ dY, const int* __restrict__ list,
+               const int* __restrict__ cnt) {
+  constexpr int LPR = D / 4;
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  __shared__ float4 red[kWarpsPerBlock][LPR];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n_long = *cnt;
+  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
+    const int u = list[k];
+    const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
+    const int b = col_ptr[u], e = col_ptr[u + 1];
+    const int per = (e - b + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int wb = min(e, b + w * per), we = min(e, wb + per);
+    float4 acc = col_slice_sum<D, MEAN>(wb, we, bm.shift[r], csc_row, row_ptr, G, lane);
+    if (lane < LPR) red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && lane < LPR) {
+      float4 t = red[0][lane];
+      for (int q = 1; q < kWarpsPerBlock; q++) t = f4add(t, red[q][lane]);
+      dY[(long long)u * LPR + lane] = t;
+    }
+    __syncthreads();
+  }
+}
+
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __restrict__ rel_y_off,
+          const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
+          const int* __restrict__ row_ptr, const float4* __restrict__ G, float4* __restrict__ dY,
+          int* __restrict__ long_list, int* __restrict__ long_cnt) {
+  constexpr int LPR = D / 4;
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (u >= *U_dev) return;
+  const int b = col_ptr[u], e = col_ptr[u + 1];
+  if (e - b > kLongCol) {
+    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = u;
+    return;
+  }
+  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
+  float4 acc = col_slice_sum<D, MEAN>(b, e, bm.shift[r], csc_row, row_ptr, G, lane);
+  if (lane < LPR) dY[(long long)u * LPR + lane] = acc;
 }
 
 // ------------------------------------------------ backward GAT, pass 1 (rows)
@@ -307,27 +356,17 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
 
 // ------------------------------------------------- backward GAT, pass 2 (CSC)
 template <int D>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
-                   const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
-                   const int* __restrict__ csc_pos, const int* __restrict__ csc_row,
-                   const float* __restrict__ alpha, const float* __restrict__ dpre,
-                   const float4* __restrict__ G, float4* __restrict__ dY,
-                   float* __restrict__ ds_src) {
+__device__ __forceinline__ void gat_col_slice(int b, int e, int shift, int H,
+                                              const int* __restrict__ csc_pos,
+                                              const int* __restrict__ csc_row,
+                                              const float* __restrict__ alpha,
+                                              const float* __restrict__ dpre,
+                                              const float4* __restrict__ G, int lane,
+                                              float4* acc_out, float* dss_out) {
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
-  __shared__ int s_yoff[HF_MAX_R + 1];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
   const int sl = lane % LPR, sid = lane / LPR;
-  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (u >= *U_dev) return;
-  const int dh4 = (D / H) / 4;
-  const int h = sl / dh4;
-  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
-  const int shift = bm.shift[r];
-  const int b = col_ptr[u], e = col_ptr[u + 1];
+  const int h = sl / ((D / H) / 4);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float dss = 0.f;
   for (int base = b; base < e; base += 32) {
@@ -354,9 +393,84 @@ k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
     acc = f4add(acc, f4shfl_xor(acc, o));
     dss += __shfl_xor_sync(0xffffffffu, dss, o);
   }
-  if (sid == 0) {
-    dY[(long long)u * LPR + sl] = acc;
-    if (sl % dh4 == 0) ds_src[(long long)u * H + h] = dss;
+  *acc_out = acc;
+  *dss_out = dss;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
+                   const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
+                   const int* __restrict__ csc_pos, const int* __restrict__ csc_row,
+                   const float* __restrict__ alpha, const float* __restrict__ dpre,
+                   const float4* __restrict__ G, float4* __restrict__ dY,
+                   float* __restrict__ ds_src, int* __restrict__ long_list,
+                   int* __restrict__ long_cnt) {
+  constexpr int LPR = D / 4;
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (u >= *U_dev) return;
+  const int b = col_ptr[u], e = col_ptr[u + 1];
+  if (e - b > kLongCol) {
+    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = u;
+    return;
+  }
+  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
+  float4 acc;
+  float dss;
+  gat_col_slice<D>(b, e, bm.shift[r], H, csc_pos, csc_row, alpha, dpre, G, lane, &acc, &dss);
+  const int dh4 = (D / H) / 4;
+  if (lane < LPR) {
+    dY[(long long)u * LPR + lane] = acc;
+    if (lane % dh4 == 0) ds_src[(long long)u * H + lane / dh4] = dss;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
+                        const int* __restrict__ col_ptr, const int* __restrict__ csc_pos,
+                        const int* __restrict__ csc_row, const float* __restrict__ alpha,
+                        const float* __restrict__ dpre, const float4* __restrict__ G,
+                        float4* __restrict__ dY, float* __restrict__ ds_src,
+                        const int* __restrict__ list, const int* __restrict__ cnt) {
+  constexpr int LPR = D / 4;
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  __shared__ float4 red[kWarpsPerBlock][LPR];
+  __shared__ float reds[kWarpsPerBlock][LPR];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int dh4 = (D / H) / 4;
+  const int n_long = *cnt;
+  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
+    const int u = list[k];
+    const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
+    const int b = col_ptr[u], e = col_ptr[u + 1];
+    const int per = (e - b + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int wb = min(e, b + w * per), we = min(e, wb + per);
+    float4 acc;
+    float dss;
+    gat_col_slice<D>(wb, we, bm.shift[r], H, csc_pos, csc_row, alpha, dpre, G, lane, &acc, &dss);
+    if (lane < LPR) {
+      red[w][lane] = acc;
+      reds[w][lane] = dss;
+    }
+    __syncthreads();
+    if (w == 0 && lane < LPR) {
+      float4 t = red[0][lane];
+      float ts = reds[0][lane];
+      for (int q = 1; q < kWarpsPerBlock; q++) {
+        t = f4add(t, red[q][lane]);
+        ts += reds[q][lane];
+      }
+      dY[(long long)u * LPR + lane] = t;
+      if (lane % dh4 == 0) ds_src[(long long)u * H + lane / dh4] = ts;
+    }
+    __syncthreads();
   }
 }
 
@@ -409,8 +523,10 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_a
 size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg agg, int heads) {
   LayerMeta m;
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
-  if (agg != HIFUSE_AGG_GAT) return 256;
-  return 2 * carve_bytes((long long)m.N * heads, 4);
+  long long U_max = m.N < m.S ? m.N : m.S;
+  size_t b = carve_bytes(U_max + 1, 4) + carve_bytes(2, 4);
+  if (agg == HIFUSE_AGG_GAT) b += 2 * carve_bytes((long long)m.N * heads, 4);
+  return b;
 }
 
 hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
@@ -426,47 +542,51 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
     return HIFUSE_ERR_INVALID_ARG;
   if (D != 64 && D != 128) return HIFUSE_ERR_UNSUPPORTED;
   if (!aligned16(d_G) || !aligned16(d_dY)) return HIFUSE_ERR_ALIGNMENT;
+  if (ws_bytes < hifuse_aggregate_bwd_ws_bytes(shape, agg, heads) || !d_ws)
+    return HIFUSE_ERR_WORKSPACE;
   cudaStream_t s = st(stream);
   BwdMeta bm;
   bm.R = m.R;
   for (int r = 0; r < m.R; r++) bm.shift[r] = m.type_dst_off[m.rel_dst[r]] - m.rel_row_off[r];
   long long U_max = m.N < m.S ? m.N : m.S;
+  char* p = (char*)d_ws;
+  int* long_list = carve<int>(p, U_max + 1);
+  int* long_cnt = carve<int>(p, 2);
+  cudaMemsetAsync(long_cnt, 0, sizeof(int), s);
   unsigned gridU = ceil_div(U_max, kWarpsPerBlock);
   const int TB = kWarpsPerBlock * 32;
+  const unsigned gridL = 296;
   if (agg == HIFUSE_AGG_GAT) {
     if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
     if (!d_Y || !d_s_src || !d_s_dst || !d_stats || !d_ds_src || !d_ds_dst || !csr->csc_pos ||
         !csr->row_ptr || !csr->col || !csr->rel_row_off)
       return HIFUSE_ERR_INVALID_ARG;
-    if (ws_bytes < hifuse_aggregate_bwd_ws_bytes(shape, agg, heads) || (!d_ws && m.N > 0))
-      return HIFUSE_ERR_WORKSPACE;
-    char* p = (char*)d_ws;
     float* alpha = carve<float>(p, (long long)m.N * heads);
     float* dpre = carve<float>(p, (long long)m.N * heads);
     unsigned gridR = ceil_div(m.rows, kWarpsPerBlock);
-    if (D == 128) {
-      HF_LAUNCH(k_agg_bwd_gat_rows<128>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows,
-                heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,
-                d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);
-      HF_LAUNCH(k_agg_bwd_gat_cols<128>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,
-                csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,
-                (float4*)d_dY, d_ds_src);
-    } else {
-      HF_LAUNCH(k_agg_bwd_gat_rows<64>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows,
-                heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,
-                d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);
-      HF_LAUNCH(k_agg_bwd_gat_cols<64>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,
-                csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,
-                (float4*)d_dY, d_ds_src);
-    }
+#define HF_GAT(DD)                                                                             \
+  HF_LAUNCH(k_agg_bwd_gat_rows<DD>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows, \
+            heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,       \
+            d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                              \
+  HF_LAUNCH(k_agg_bwd_gat_cols<DD>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,   \
+            csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
+            (float4*)d_dY, d_ds_src, long_list, long_cnt);                                    \
+  HF_LAUNCH(k_agg_bwd_gat_cols_long<DD>, gridL, TB, 0, s, bm, heads, csr->rel_y_off,          \
+            csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
+            (float4*)d_dY, d_ds_src, long_list, long_cnt)
+    if (D == 128) { HF_GAT(128); } else { HF_GAT(64); }
+#undef HF_GAT
   } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
     if (agg == HIFUSE_AGG_MEAN && !csr->row_ptr) return HIFUSE_ERR_INVALID_ARG;
-#define HF_BWD(DD, MM)                                                                      \
-  HF_LAUNCH((k_agg_bwd<DD, MM>), gridU, TB, 0, s, bm, (int)U_max, csr->U_dev, csr->rel_y_off, \
-            csr->col_ptr, csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY)
+#define HF_BWD(DD, MM)                                                                        \
+  HF_LAUNCH((k_agg_bwd<DD, MM>), gridU, TB, 0, s, bm, (int)U_max, csr->U_dev, csr->rel_y_off,   \
+            csr->col_ptr, csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY,        \
+            long_list, long_cnt);                                                               \
+  HF_LAUNCH((k_agg_bwd_long<DD, MM>), gridL, TB, 0, s, bm, csr->rel_y_off, csr->col_ptr,        \
+            csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY, long_list, long_cnt)
     bool mean = agg == HIFUSE_AGG_MEAN;
-    if (D == 128) { if (mean) HF_BWD(128, true); else HF_BWD(128, false); }
-    else { if (mean) HF_BWD(64, true); else HF_BWD(64, false); }
+    if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }
+    else { if (mean) { HF_BWD(64, true); } else { HF_BWD(64, false); } }
 #undef HF_BWD
   } else {
     return HIFUSE_ERR_INVALID_ARG;

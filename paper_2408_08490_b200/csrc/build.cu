@@ -13,17 +13,16 @@
 //   k_finish     rel_y_off, y_src, slot_y, U
 //   k_scatter    unstable atomic placement into rows + column histogram
 //   scan         col_ptr
-//   k_rows       per row: sort by original column (restores Alg. 2's
+//   k_fix_segments<rows>  warp per row: sort by original column (restores Alg. 2's
 //                column order, so the result is bit-exact and deterministic),
 //                then CSC placement
-//   k_cols       per Y row: sort CSC entries by CSR position
-//   k_*_long     the same two sorts for segments longer than 32 (block-wide)
+//   k_fix_segments<cols>  warp per Y row: sort CSC entries by CSR position
+//   k_*_long     the same two sorts for segments longer than 512 (block-wide)
 #include <vector>
 #include "common.cuh"
 
 namespace hf {
 
-static constexpr int kShort = 32;        // segments up to this length: one thread
 static constexpr int kLongCap = 8192;    // block bitonic in shared memory up to this
 
 __global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* __restrict__ dst,
@@ -175,18 +174,98 @@ __device__ __forceinline__ void csc_place(int row, int b, int e_, const int* col
   }
 }
 
-__global__ void k_rows(int rows, const int* __restrict__ row_ptr, int* eperm, int* col,
-                       const int* __restrict__ col_ptr, int* ccur, int* csc_pos, int* csc_row,
-                       int* long_list, int* long_cnt) {
-  int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= rows) return;
-  int b = row_ptr[row], e_ = row_ptr[row + 1];
-  if (e_ - b > kShort) {
-    long_list[atomicAdd(long_cnt, 1)] = row;
+// Warp-level sort of one segment of n <= kWarpCap unique keys (+ values):
+// n <= 32 in registers (shuffle bitonic), else bitonic in this warp's shared
+// memory slice.  Returns with keys/vals written back in ascending key order.
+static constexpr int kWarpCap = 512;
+
+__device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      int pk = __shfl_xor_sync(0xffffffffu, key, j);
+      int pv = __shfl_xor_sync(0xffffffffu, val, j);
+      bool up = (lane & k) == 0;
+      bool lower = (lane & j) == 0;
+      bool take_min = lower == up;
+      bool swap = take_min ? (pk < key) : (pk > key);
+      if (swap) { key = pk; val = pv; }
+    }
+}
+
+__device__ void warp_sort_smem(int* keys, int* vals, int n, int* sk, int* sv, int lane) {
+  int P = 64;
+  while (P < n) P <<= 1;
+  for (int i = lane; i < P; i += 32) {
+    sk[i] = i < n ? keys[i] : 0x7fffffff;
+    sv[i] = i < n ? vals[i] : 0;
+  }
+  __syncwarp();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        int l = i ^ j;
+        if (l > i) {
+          bool up = (i & k) == 0;
+          int a = sk[i], b = sk[l];
+          if ((a > b) == up) {
+            sk[i] = b; sk[l] = a;
+            int t = sv[i]; sv[i] = sv[l]; sv[l] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  for (int i = lane; i < n; i += 32) {
+    keys[i] = sk[i];
+    vals[i] = sv[i];
+  }
+  __syncwarp();
+}
+
+// One warp per segment.  ROWS: segments are CSR rows (keys eperm, vals col),
+// followed by CSC placement of the sorted row.  !ROWS: CSC columns (keys
+// csc_pos, vals csc_row).  Segments longer than kWarpCap go to the block path.
+template <bool ROWS>
+__global__ void __launch_bounds__(256)
+k_fix_segments(int nseg_host, const int* __restrict__ nseg_dev, const int* __restrict__ ptr,
+               int* keys, int* vals, const int* __restrict__ col_ptr, int* ccur, int* csc_pos,
+               int* csc_row, int* long_list, int* long_cnt) {
+  __shared__ int sk[8][kWarpCap];
+  __shared__ int sv[8][kWarpCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int seg = blockIdx.x * 8 + w;
+  const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+  if (seg >= nseg) return;
+  const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
+  if (n > kWarpCap) {
+    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = seg;
     return;
   }
-  thread_sort(eperm + b, col + b, e_ - b);
-  csc_place(row, b, e_, col, col_ptr, ccur, csc_pos, csc_row, 1, 0);
+  if (n <= 32) {
+    int key = lane < n ? keys[b + lane] : 0x7fffffff;
+    int val = lane < n ? vals[b + lane] : 0;
+    if (n > 1) warp_sort_regs(key, val, lane);
+    if (lane < n) {
+      keys[b + lane] = key;
+      vals[b + lane] = val;
+      if (ROWS) {
+        int w_ = col_ptr[val] + atomicAdd(&ccur[val], 1);
+        csc_pos[w_] = b + lane;
+        csc_row[w_] = seg;
+      }
+    }
+    return;
+  }
+  warp_sort_smem(keys + b, vals + b, n, sk[w], sv[w], lane);
+  if (ROWS)
+    for (int p = b + lane; p < e; p += 32) {
+      int c = vals[p];
+      int w_ = col_ptr[c] + atomicAdd(&ccur[c], 1);
+      csc_pos[w_] = p;
+      csc_row[w_] = seg;
+    }
 }
 
 __global__ void k_rows_long(const int* __restrict__ row_ptr, int* eperm, int* col,
@@ -202,18 +281,6 @@ __global__ void k_rows_long(const int* __restrict__ row_ptr, int* eperm, int* co
     csc_place(row, b, e_, col, col_ptr, ccur, csc_pos, csc_row, blockDim.x, threadIdx.x);
     __syncthreads();
   }
-}
-
-__global__ void k_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* csc_pos,
-                       int* csc_row, int* long_list, int* long_cnt) {
-  int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= *U_dev) return;
-  int b = col_ptr[u], e_ = col_ptr[u + 1];
-  if (e_ - b > kShort) {
-    long_list[atomicAdd(long_cnt, 1)] = u;
-    return;
-  }
-  thread_sort(csc_pos + b, csc_row + b, e_ - b);
 }
 
 __global__ void k_cols_long(const int* __restrict__ col_ptr, int* csc_pos, int* csc_row,
@@ -346,12 +413,14 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     int* rows_long = w.lists;
     int* cols_long = w.lists + m.rows;
     const int smem = 2 * kLongCap * sizeof(int);
-    HF_LAUNCH(k_rows, ceil_div(m.rows, TB), TB, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
-              o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
+    HF_LAUNCH(k_fix_segments<true>, ceil_div(m.rows, 8), 256, 0, s, m.rows, (const int*)nullptr,
+              o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long,
+              w.counters);
     HF_LAUNCH(k_rows_long, 148, 256, smem, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
               o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv);
-    HF_LAUNCH(k_cols, ceil_div(U_max, TB), TB, 0, s, o.U_dev, o.col_ptr, o.csc_pos, o.csc_row,
-              cols_long, w.counters + 1);
+    HF_LAUNCH(k_fix_segments<false>, ceil_div(U_max, 8), 256, 0, s, 0, o.U_dev, o.col_ptr,
+              o.csc_pos, o.csc_row, (const int*)nullptr, (int*)nullptr, (int*)nullptr,
+              (int*)nullptr, cols_long, w.counters + 1);
     HF_LAUNCH(k_cols_long, 148, 256, smem, s, o.col_ptr, o.csc_pos, o.csc_row, cols_long,
               w.counters + 1, w.gk, w.gv);
   }

@@ -53,9 +53,12 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
+inline bool grid_nonempty(long long g) { return g > 0; }
+inline bool grid_nonempty(dim3 g) { return g.x > 0 && g.y > 0 && g.z > 0; }
+
 #define HF_LAUNCH(kernel, grid, block, smem, stream, ...)                      \
   do {                                                                         \
-    if ((grid) > 0) {                                                          \
+    if (hf::grid_nonempty(grid)) {                                             \
       kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
       hf::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
     }                                                                          \

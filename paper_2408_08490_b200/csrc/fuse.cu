@@ -95,17 +95,27 @@ k_fuse_bwd_chunks(FuseBwdMeta f, const float4* __restrict__ dH, const float4* __
   }
 }
 
-__global__ void k_fuse_bwd_bias(FuseBwdMeta f, const float4* __restrict__ partial,
-                                float4* __restrict__ dbias) {
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= f.T * f.D4) return;
-  int t = idx / f.D4, c = idx % f.D4;
+// one block per type: threads split the type's chunks, fixed-order smem reduce
+__global__ void __launch_bounds__(256)
+k_fuse_bwd_bias(FuseBwdMeta f, const float4* __restrict__ partial, float4* __restrict__ dbias) {
+  __shared__ float4 red[256];
+  int t = blockIdx.x;
+  int c = threadIdx.x % f.D4, sub = threadIdx.x / f.D4, nsub = 256 / f.D4;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int k = f.chunk_off[t]; k < f.chunk_off[t + 1]; k++) {
+  for (int k = f.chunk_off[t] + sub; k < f.chunk_off[t + 1]; k += nsub) {
     float4 v = partial[(long long)k * f.D4 + c];
     s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
   }
-  dbias[idx] = s;
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < f.D4) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < nsub; k++) {
+      float4 v = red[k * f.D4 + threadIdx.x];
+      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    }
+    dbias[t * f.D4 + threadIdx.x] = a;
+  }
 }
 
 static void make_fbm(const LayerMeta& m, int D, FuseBwdMeta* f) {
@@ -186,8 +196,7 @@ hifuse_status hifuse_semantic_fuse_bwd(const hifuse_layer_shape* shape, int D, h
     HF_LAUNCH(k_fuse_bwd_chunks<false>, nch, 256, 0, s, f, (const float4*)d_dH,
               (const float4*)d_H, (float4*)d_G, partial);
   if (d_dbias)
-    HF_LAUNCH(k_fuse_bwd_bias, ceil_div(m.T * (D / 4), 256), 256, 0, s, f, partial,
-              (float4*)d_dbias);
+    HF_LAUNCH(k_fuse_bwd_bias, m.T, 256, 0, s, f, partial, (float4*)d_dbias);
   return last_cuda();
 }
 

@@ -20,36 +20,84 @@ __device__ __forceinline__ float block_reduce(float v, float* sm, bool is_max) {
   return r;
 }
 
-// one block per seed row: logits, softmax, per-row loss and dlogits
-__global__ void k_xent_rows(int B, int D, int C, const float* __restrict__ H, long long h_row0,
-                            const int* __restrict__ labels, const float* __restrict__ Wc,
-                            const float* __restrict__ bc, float* __restrict__ dlog,
-                            float* __restrict__ row_loss) {
-  extern __shared__ float sm[];   // [D] h row, [C] logits, [32] scratch
-  float* hrow = sm;
-  float* lg = sm + D;
-  float* red = lg + C;
-  int b = blockIdx.x;
-  for (int d = threadIdx.x; d < D; d += blockDim.x) hrow[d] = H[(h_row0 + b) * D + d];
-  __syncthreads();
+// Small SIMT GEMM: C[M,N] = op(A)[M,K] op(B)[K,N]; TA: A stored [K,M]; TB: B
+// stored [N,K].  64x64 tiles, 256 threads, 4x4 outputs per thread.
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256)
+k_gemm_small(int M, int N, int K, const float* __restrict__ A, int lda,
+             const float* __restrict__ B, int ldb, float* __restrict__ C, int ldc,
+             long long a_row0, long long c_row0) {
+  __shared__ float As[16][64 + 1];
+  __shared__ float Bs[16][64 + 1];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = tid; i < 16 * 64; i += 256) {
+      int kk = TA ? i / 64 : i % 16, mm = TA ? i % 64 : i / 16;
+      int m = m0 + mm, k = k0 + kk;
+      float v = 0.f;
+      if (m < M && k < K) v = TA ? A[(long long)k * lda + a_row0 + m] : A[(a_row0 + m) * lda + k];
+      As[kk][mm] = v;
+      int kb = TB ? i % 16 : i / 64, nb = TB ? i / 16 : i % 64;
+      int n = n0 + nb, k2 = k0 + kb;
+      float w = 0.f;
+      if (n < N && k2 < K) w = TB ? B[(long long)n * ldb + k2] : B[(long long)k2 * ldb + n];
+      Bs[kb][nb] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; kk++) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; j++) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    int m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      int n = n0 + tx + 16 * j;
+      if (n < N) C[(c_row0 + m) * ldc + n] = acc[i][j];
+    }
+  }
+}
+
+// One warp per seed row: bias, softmax over the C logits (in place ->
+// dlogits = (softmax - onehot) / B), per-row loss.
+__global__ void k_xent_softmax(int B, int C, const float* __restrict__ bc,
+                               const int* __restrict__ labels, float* __restrict__ lg,
+                               float* __restrict__ row_loss) {
+  int b = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  float* x = lg + (long long)b * C;
   float mx = -INFINITY;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = bc[c];
-    for (int d = 0; d < D; d++) s = fmaf(hrow[d], Wc[(long long)d * C + c], s);
-    lg[c] = s;
-    mx = fmaxf(mx, s);
+  for (int c = lane; c < C; c += 32) {
+    float v = x[c] + bc[c];
+    x[c] = v;
+    mx = fmaxf(mx, v);
   }
-  mx = block_reduce(mx, red, true);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   float se = 0.f;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) se += expf(lg[c] - mx);
-  se = block_reduce(se, red, false);
+  for (int c = lane; c < C; c += 32) se += expf(x[c] - mx);
+  for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
   int y = labels[b];
+  __syncwarp();
+  float ly = x[y];
+  __syncwarp();
   float inv = 1.f / (float)B;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float p = expf(lg[c] - mx) / se;
-    dlog[(long long)b * C + c] = (p - (c == y ? 1.f : 0.f)) * inv;
-  }
-  if (threadIdx.x == 0) row_loss[b] = logf(se) + mx - lg[y];
+  for (int c = lane; c < C; c += 32) x[c] = (expf(x[c] - mx) / se - (c == y ? 1.f : 0.f)) * inv;
+  if (lane == 0) row_loss[b] = logf(se) + mx - ly;
 }
 
 __global__ void k_xent_loss(int B, const float* __restrict__ row_loss, float* __restrict__ loss) {
@@ -60,32 +108,13 @@ __global__ void k_xent_loss(int B, const float* __restrict__ row_loss, float* __
   if (threadIdx.x == 0) loss[0] = s / (float)B;
 }
 
-// dH[h_row0 + b][d] = sum_c dlog[b][c] Wc[d][c]
-__global__ void k_xent_dh(int B, int D, int C, long long h_row0, const float* __restrict__ dlog,
-                          const float* __restrict__ Wc, float* __restrict__ dH) {
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)B * D) return;
-  int b = (int)(idx / D), d = (int)(idx % D);
+// dbc[c] = sum_b dlog[b][c]  (fixed order)
+__global__ void k_xent_dbias(int B, int C, const float* __restrict__ dlog, float* __restrict__ dbc) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
   float s = 0.f;
-  for (int c = 0; c < C; c++) s = fmaf(dlog[(long long)b * C + c], Wc[(long long)d * C + c], s);
-  dH[(h_row0 + b) * D + d] = s;
-}
-
-// dWc[d][c] = sum_b H[b][d] dlog[b][c];  dbc[c] = sum_b dlog[b][c]
-__global__ void k_xent_dw(int B, int D, int C, long long h_row0, const float* __restrict__ H,
-                          const float* __restrict__ dlog, float* __restrict__ dWc,
-                          float* __restrict__ dbc) {
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)(D + 1) * C) return;
-  int d = (int)(idx / C), c = (int)(idx % C);
-  float s = 0.f;
-  if (d < D) {
-    for (int b = 0; b < B; b++) s = fmaf(H[(h_row0 + b) * D + d], dlog[(long long)b * C + c], s);
-    dWc[(long long)d * C + c] = s;
-  } else {
-    for (int b = 0; b < B; b++) s += dlog[(long long)b * C + c];
-    dbc[c] = s;
-  }
+  for (int b = 0; b < B; b++) s += dlog[(long long)b * C + c];
+  dbc[c] = s;
 }
 
 __global__ void k_sgd(float4* __restrict__ p, const float4* __restrict__ g, long long n4, float lr) {
@@ -122,20 +151,26 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
       !d_Wc || !d_bc || !d_loss || !d_dH || !d_dWc || !d_dbc)
     return HIFUSE_ERR_INVALID_ARG;
   if (ws_bytes < hifuse_xent_ws_bytes(B, D, C) || !d_ws) return HIFUSE_ERR_WORKSPACE;
-  size_t smem = (size_t)(D + C + 32) * sizeof(float);
-  if (smem > 48 * 1024) return HIFUSE_ERR_UNSUPPORTED;
   cudaStream_t s = st(stream);
   char* p = (char*)d_ws;
   float* dlog = carve<float>(p, (long long)B * C);
   float* row_loss = carve<float>(p, B);
   cudaMemsetAsync(d_dH, 0, sizeof(float) * h_rows * D, s);
-  HF_LAUNCH(k_xent_rows, B, 128, smem, s, B, D, C, d_H, (long long)h_row0, d_labels, d_Wc, d_bc,
-            dlog, row_loss);
+  // logits = Hs Wc
+  dim3 g1(ceil_div(C, 64), ceil_div(B, 64));
+  HF_LAUNCH((k_gemm_small<false, false>), g1, 256, 0, s, B, C, D, d_H, D, d_Wc, C, dlog, C,
+            (long long)h_row0, 0ll);
+  HF_LAUNCH(k_xent_softmax, ceil_div(B, 8), 256, 0, s, B, C, d_bc, d_labels, dlog, row_loss);
   HF_LAUNCH(k_xent_loss, 1, 256, 0, s, B, row_loss, d_loss);
-  HF_LAUNCH(k_xent_dh, ceil_div((long long)B * D, 256), 256, 0, s, B, D, C, (long long)h_row0,
-            dlog, d_Wc, d_dH);
-  HF_LAUNCH(k_xent_dw, ceil_div((long long)(D + 1) * C, 256), 256, 0, s, B, D, C,
-            (long long)h_row0, d_H, dlog, d_dWc, d_dbc);
+  // dHs = dlog Wc^T   (Wc is [D, C]: op(B) = Wc^T stored [N = D, K = C])
+  dim3 g2(ceil_div(D, 64), ceil_div(B, 64));
+  HF_LAUNCH((k_gemm_small<false, true>), g2, 256, 0, s, B, D, C, dlog, C, d_Wc, C, d_dH, D, 0ll,
+            (long long)h_row0);
+  // dWc = Hs^T dlog
+  dim3 g3(ceil_div(C, 64), ceil_div(D, 64));
+  HF_LAUNCH((k_gemm_small<true, false>), g3, 256, 0, s, D, C, B, d_H + h_row0 * D, D, dlog, C,
+            d_dWc, C, 0ll, 0ll);
+  HF_LAUNCH(k_xent_dbias, ceil_div(C, 128), 128, 0, s, B, C, dlog, d_dbc);
   return last_cuda();
 }
 

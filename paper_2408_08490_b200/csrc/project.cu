@@ -299,13 +299,27 @@ __global__ void k_wgrad_reduce(int R, int T, int KD, const int* __restrict__ chu
   int G = dW_root ? R + T : R;
   if (idx >= (long long)G * KD4) return;
   int g = (int)(idx / KD4), e = (int)(idx % KD4);
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int c = chunk_off[g]; c < chunk_off[g + 1]; c++) {
-    float4 v = partial[(long long)c * KD4 + e];
-    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  // four independent accumulators (fixed pairing: deterministic)
+  float4 s[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) s[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int c0 = chunk_off[g], c1 = chunk_off[g + 1];
+  int c = c0;
+  for (; c + 4 <= c1; c += 4) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      float4 v = partial[(long long)(c + q) * KD4 + e];
+      s[q].x += v.x; s[q].y += v.y; s[q].z += v.z; s[q].w += v.w;
+    }
   }
-  if (g < R) dW_rel[(long long)g * KD4 + e] = s;
-  else dW_root[(long long)(g - R) * KD4 + e] = s;
+  for (; c < c1; c++) {
+    float4 v = partial[(long long)c * KD4 + e];
+    s[0].x += v.x; s[0].y += v.y; s[0].z += v.z; s[0].w += v.w;
+  }
+  float4 t = make_float4((s[0].x + s[1].x) + (s[2].x + s[3].x), (s[0].y + s[1].y) + (s[2].y + s[3].y),
+                         (s[0].z + s[1].z) + (s[2].z + s[3].z), (s[0].w + s[1].w) + (s[2].w + s[3].w));
+  if (g < R) dW_rel[(long long)g * KD4 + e] = t;
+  else dW_root[(long long)(g - R) * KD4 + e] = t;
 }
 
 // dgrad: dX[type s tile] = sum_{r: s(r)=s} dYt[slot_y(r,j)] W_r^T
@@ -405,8 +419,9 @@ k_att_partial(int R, int H, int W, int mode, const int* __restrict__ chunk_off,
   if (c >= chunk_off[R]) return;
   int r = upper_bound_i(chunk_off, R + 1, c) - 1;
   while (r > 0 && chunk_off[r] > c) r--;
-  int first = row_off[r] + (c - chunk_off[r]) * kCH;
-  int last = min(first + kCH, row_off[r + 1]);
+  const int* ro = mode == 1 ? pm.rel_row_off : row_off;   // merged rows: host-known offsets
+  int first = ro[r] + (c - chunk_off[r]) * kCH;
+  int last = min(first + kCH, ro[r + 1]);
   for (int o = threadIdx.x; o < H * W; o += blockDim.x) {
     int h = o / W, w = o % W;
     float s = 0.f;
@@ -422,12 +437,14 @@ k_att_partial(int R, int H, int W, int mode, const int* __restrict__ chunk_off,
   }
 }
 
-__global__ void k_att_chunks(int R, const int* __restrict__ row_off, int* chunk_off) {
+__global__ void k_att_chunks(int R, const int* __restrict__ row_off, ProjMeta pm,
+                             int* chunk_off) {
   if (threadIdx.x != 0) return;
+  const int* ro = row_off ? row_off : pm.rel_row_off;
   int acc = 0;
   for (int r = 0; r < R; r++) {
     chunk_off[r] = acc;
-    acc += (row_off[r + 1] - row_off[r] + kCH - 1) / kCH;
+    acc += (ro[r + 1] - ro[r] + kCH - 1) / kCH;
   }
   chunk_off[R] = acc;
 }
@@ -669,7 +686,6 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   long long ach = U_max / kCH + m.rows / kCH + 2 * m.R + 2;
   float* Psrc = carve<float>(p, ach * H * (K > D ? K : D));
   float* Pdst = carve<float>(p, ach * H * (K > D ? K : D));
-  int* rro_dev = carve<int>(p, m.R + 1);
   if (d_att) {
     HF_LAUNCH(k_dy_score, ceil_div(U_max, 8), 256, 0, s, m.R, D, H, csr->U_dev, csr->rel_y_off,
               d_att, d_ds_src, d_dY);
@@ -690,14 +706,13 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   if (d_att) {
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, s, m.R, K, D, H, d_W_rel,
               d_att, v);
-    cudaMemcpyAsync(rro_dev, m.rel_row_off, sizeof(int) * (m.R + 1), cudaMemcpyHostToDevice, s);
-    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, csr->rel_y_off, src_chunk);
-    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, rro_dev, dst_chunk);
+    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, csr->rel_y_off, pm, src_chunk);
+    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, (const int*)nullptr, pm, dst_chunk);
     unsigned gs = (unsigned)(U_max / kCH + m.R + 1);
     unsigned gdst = (unsigned)(m.rows / kCH + m.R + 1);
     HF_LAUNCH(k_att_partial, gs, 256, 0, s, m.R, H, D, 0, src_chunk, csr->rel_y_off, d_ds_src,
               d_Y, pm, d_gather_ids, Psrc);
-    HF_LAUNCH(k_att_partial, gdst, 256, 0, s, m.R, H, K, 1, dst_chunk, rro_dev, d_ds_dst, d_X,
+    HF_LAUNCH(k_att_partial, gdst, 256, 0, s, m.R, H, K, 1, dst_chunk, (const int*)nullptr, d_ds_dst, d_X,
               pm, d_gather_ids, Pdst);
     HF_LAUNCH(k_att_final, m.R, 256, H * K * sizeof(float), s, m.R, K, D, H, src_chunk, dst_chunk,
               Psrc, Pdst, d_W_rel, d_att, d_dW_rel, d_datt, (float*)nullptr);

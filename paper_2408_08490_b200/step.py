@@ -84,12 +84,22 @@ class DeviceBatch:
             self.to_device()
 
     def to_device(self, non_blocking=False):
+        """Host -> device copy of the batch inputs; re-uses the device tensors
+        after the first call (so captured CUDA graphs stay valid)."""
         src = self.pinned if self.pinned is not None else {
             k: ([torch.from_numpy(a) for a in v] if isinstance(v, list) else torch.from_numpy(v))
             for k, v in self.host.items()}
-        self.dev = {k: ([t.to(self.device, non_blocking=non_blocking) for t in v]
-                        if isinstance(v, list) else v.to(self.device, non_blocking=non_blocking))
-                    for k, v in src.items()}
+        if self.dev is None:
+            self.dev = {k: ([t.to(self.device, non_blocking=non_blocking) for t in v]
+                            if isinstance(v, list) else v.to(self.device, non_blocking=non_blocking))
+                        for k, v in src.items()}
+        else:
+            for k, v in src.items():
+                if isinstance(v, list):
+                    for d, h in zip(self.dev[k], v):
+                        d.copy_(h, non_blocking=non_blocking)
+                else:
+                    self.dev[k].copy_(v, non_blocking=non_blocking)
         return self
 
     def h2d_bytes(self):
@@ -151,64 +161,126 @@ class Trainer:
     def _ws(self, nbytes):
         return self._buf("ws", (nbytes + 3) // 4 + 64)
 
-    # ----------------------------------------------------------------- step
-    def step(self, db: DeviceBatch, feat, edge_type, allreduce=None, world=1, update=True):
-        """Runs one training step on the current stream; returns the device
-        loss tensor (no host synchronisation)."""
+    # ----------------------------------------------------------------- plan
+    def plan(self, db: DeviceBatch, feat, edge_type):
+        """The step's library calls as a list of (stage name, closure).  All
+        buffers are bound here, so the closures can be run eagerly or captured
+        into a CUDA graph (no allocation, no host sync inside)."""
         L, D, H, C = self.L, self.D, self.heads, self.C
         dev = db.dev
         shapes = db.shapes
+        ops = []
         csrs = [self._csr(l, s) for l, s in enumerate(shapes)]
-        ws_build = max(s.build_ws for s in shapes)
-        hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"], edge_type,
-                                 self._ws(ws_build), self.status)
+        wsb = self._ws(max(s.build_ws for s in shapes))
+        ops.append(("build", lambda: hf.build_semantic_graphs(
+            shapes, csrs, dev["src"], dev["dst"], dev["eid"], edge_type, wsb, self.status)))
         acts = []
         X, gid = feat, dev["gid"]
         for l, sh in enumerate(shapes):
             K = self.K0 if l == 0 else D
             P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
-            Y = self._mat(f"Y{l}", sh.U_max, D)
-            R0 = self._mat(f"R0{l}", sh.dst_rows, D) if P["W_root"] is not None else None
-            s_src = self._mat(f"ss{l}", sh.U_max, H) if P["att"] is not None else None
-            s_dst = self._mat(f"sd{l}", sh.rows, H) if P["att"] is not None else None
-            hf.project(sh, csrs[l], K, D, H, X, gid, P["W_rel"], P["W_root"], P["att"], Y, R0,
-                       s_src, s_dst, self._ws(hf.project_ws_bytes(sh, K, D, H)), prec=self.prec)
-            Z = self._mat(f"Z{l}", sh.rows, D)
-            stats = self._mat(f"st{l}", sh.rows, 2 * H) if self.agg == "gat" else None
-            hf.aggregate_fwd(csrs[l], sh.rows, self.agg, D, H, self.slope, Y, s_src, s_dst, Z, stats)
-            Hout = self._mat(f"H{l}", sh.dst_rows, D)
-            act = "relu" if l < L - 1 else "none"
-            hf.semantic_fuse(sh, D, act, Z, R0, P["bias"], Hout)
-            acts.append(dict(X=X, gid=gid, Y=Y, R0=R0, s_src=s_src, s_dst=s_dst, stats=stats,
-                             H=Hout, act=act, K=K))
-            X, gid = Hout, None
+            a = dict(X=X, gid=gid, K=K, act="relu" if l < L - 1 else "none",
+                     Y=self._mat(f"Y{l}", sh.U_max, D),
+                     R0=self._mat(f"R0{l}", sh.dst_rows, D) if P["W_root"] is not None else None,
+                     s_src=self._mat(f"ss{l}", sh.U_max, H) if P["att"] is not None else None,
+                     s_dst=self._mat(f"sd{l}", sh.rows, H) if P["att"] is not None else None,
+                     Z=self._mat(f"Z{l}", sh.rows, D),
+                     stats=self._mat(f"st{l}", sh.rows, 2 * H) if self.agg == "gat" else None,
+                     H=self._mat(f"H{l}", sh.dst_rows, D),
+                     wsp=self._ws(hf.project_ws_bytes(sh, K, D, H)))
+            ops.append((f"project.{l}", lambda sh=sh, c=csrs[l], a=a, P=P: hf.project(
+                sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"], P["att"], a["Y"],
+                a["R0"], a["s_src"], a["s_dst"], a["wsp"], prec=self.prec)))
+            ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a: hf.aggregate_fwd(
+                c, sh.rows, self.agg, D, H, self.slope, a["Y"], a["s_src"], a["s_dst"], a["Z"],
+                a["stats"])))
+            ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
+                sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
+            acts.append(a)
+            X, gid = a["H"], None
         last = shapes[-1]
         dH = self._mat(f"dH{L - 1}", last.dst_rows, D)
-        hf.linear_xent(db.B, D, C, acts[-1]["H"][:last.dst_rows], db.h_row0, dev["labels"],
-                       self.P["Wc"], self.P["bc"], self.loss, dH[:last.dst_rows], self.Gd["Wc"],
-                       self.Gd["bc"], self._ws(hf.xent_ws_bytes(db.B, D, C)))
+        wsx = self._ws(hf.xent_ws_bytes(db.B, D, C))
+        ops.append(("xent", lambda dH=dH: hf.linear_xent(
+            db.B, D, C, acts[-1]["H"][:last.dst_rows], db.h_row0, dev["labels"], self.P["Wc"],
+            self.P["bc"], self.loss, dH[:last.dst_rows], self.Gd["Wc"], self.Gd["bc"], wsx)))
         for l in range(L - 1, -1, -1):
             sh, a = shapes[l], acts[l]
             P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
             Gr = {k: self.Gd.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
-            G = self._mat(f"G{l}", sh.dst_rows, D)
-            hf.semantic_fuse_bwd(sh, D, a["act"], dH, a["H"], G, Gr["bias"],
-                                 self._ws(hf.fuse_bwd_ws_bytes(sh, D)))
-            dY = self._mat(f"dY{l}", sh.U_max, D)
-            ds_src = self._mat(f"dss{l}", sh.U_max, H) if P["att"] is not None else None
-            ds_dst = self._mat(f"dsd{l}", sh.rows, H) if P["att"] is not None else None
-            hf.aggregate_bwd(sh, csrs[l], self.agg, D, H, self.slope, G, a["Y"], a["s_src"],
-                             a["s_dst"], a["stats"], dY, ds_src, ds_dst,
-                             self._ws(hf.aggregate_bwd_ws_bytes(sh, self.agg, H)))
-            dX = self._mat(f"dH{l - 1}", sh.src_rows, D) if l > 0 else None
-            hf.project_bwd(sh, csrs[l], a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"],
-                           P["att"], a["Y"], dY, G, ds_src, ds_dst, dX, Gr["W_rel"], Gr["W_root"],
-                           Gr["att"], self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H)),
-                           prec=self.prec)
-            dH = dX
-        if allreduce is not None:
-            allreduce(self.grads)
-        if update:
-            hf.sgd(self.params, self.grads, self.lr, 1.0 / world)
+            b = dict(dH=dH, G=self._mat(f"G{l}", sh.dst_rows, D),
+                     dY=self._mat(f"dY{l}", sh.U_max, D),
+                     ds_src=self._mat(f"dss{l}", sh.U_max, H) if P["att"] is not None else None,
+                     ds_dst=self._mat(f"dsd{l}", sh.rows, H) if P["att"] is not None else None,
+                     dX=self._mat(f"dH{l - 1}", sh.src_rows, D) if l > 0 else None,
+                     wsf=self._ws(hf.fuse_bwd_ws_bytes(sh, D)),
+                     wsa=self._ws(hf.aggregate_bwd_ws_bytes(sh, self.agg, H)),
+                     wsq=self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H)))
+            ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
+                sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
+            ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b: hf.aggregate_bwd(
+                sh, c, self.agg, D, H, self.slope, b["G"], a["Y"], a["s_src"], a["s_dst"],
+                a["stats"], b["dY"], b["ds_src"], b["ds_dst"], b["wsa"])))
+            ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
+                        hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
+                                       P["W_root"], P["att"], a["Y"], b["dY"], b["G"],
+                                       b["ds_src"], b["ds_dst"], b["dX"], Gr["W_rel"],
+                                       Gr["W_root"], Gr["att"], b["wsq"], prec=self.prec)))
+            dH = b["dX"]
         self.last = dict(acts=acts, csrs=csrs)
+        return ops
+
+    # ----------------------------------------------------------------- step
+    def step(self, db: DeviceBatch, feat, edge_type, allreduce=None, world=1, update=True,
+             prof=None):
+        """Runs one training step eagerly on the current stream; returns the
+        device loss tensor (no host synchronisation).  ``prof``: optional dict
+        receiving (start, end) CUDA events around every library call."""
+        def timed(name, fn):
+            if prof is None:
+                fn()
+                return
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            prof.setdefault(name, []).append((a, b))
+
+        for name, fn in self.plan(db, feat, edge_type):
+            timed(name, fn)
+        if allreduce is not None:
+            timed("allreduce", lambda: allreduce(self.grads))
+        if update:
+            timed("sgd", lambda: hf.sgd(self.params, self.grads, self.lr, 1.0 / world))
         return self.loss
+
+    def capture(self, db: DeviceBatch, feat, edge_type, update=True, world=1):
+        """CUDA graph of the whole step for batch ``db`` (compute + SGD when
+        ``world == 1``; for world > 1 the SGD runs after the eager NCCL
+        all-reduce).  Buffers must already have their final size (run one eager
+        step per batch first).  Returns (graph, kernels launched per replay)."""
+        ops = self.plan(db, feat, edge_type)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = hf.kernel_launches()
+        with torch.cuda.graph(g):
+            for _, fn in ops:
+                fn()
+            if update and world == 1:
+                hf.sgd(self.params, self.grads, self.lr, 1.0)
+        return g, hf.kernel_launches() - n0
+
+    def capture_stages(self, db: DeviceBatch, feat, edge_type):
+        """One CUDA graph per library call of the step (for per-stage device
+        timing); returns [(name, graph, kernels)]."""
+        out = []
+        ops = self.plan(db, feat, edge_type)
+        torch.cuda.synchronize()
+        for name, fn in ops:
+            g = torch.cuda.CUDAGraph()
+            n0 = hf.kernel_launches()
+            with torch.cuda.graph(g):
+                fn()
+            out.append((name, g, hf.kernel_launches() - n0))
+        return out

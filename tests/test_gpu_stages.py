@@ -114,12 +114,14 @@ def _gmap_rows(sh, ch, G):
 @pytest.mark.parametrize("agg", ["sum", "mean"])
 @pytest.mark.parametrize("seed", range(3))
 def test_aggregate_bwd(seed, agg, D):
-    rng, blk, et, rs, rd, sh, csr, ch = make_case(50 + seed, D=D, hub=0.2 * (seed % 2))
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(50 + seed, D=D, hub=0.2 * (seed % 2),
+                                                     N=[800, 6000, 20000][seed])
     U = ch["U"]
     G = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
     dY = torch.zeros(max(sh.U_max, 1), D, device=DEV)
+    ws = torch.empty(hf().aggregate_bwd_ws_bytes(sh, agg, 1) // 4 + 16, device=DEV)
     hf().aggregate_bwd(sh, csr, agg, D, 1, 0.2, t(G), None, None, None, None, dY, None, None,
-                       None)
+                       ws)
     osh = oracle.Shape.of(blk, rs, rd)
     ref = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, 1, G, np.zeros((U, D)))
     A = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, 1, np.abs(G), np.zeros((U, D)))["dY"]
@@ -129,7 +131,8 @@ def test_aggregate_bwd(seed, agg, D):
 @pytest.mark.parametrize("D,H", [(128, 8), (64, 8)])
 @pytest.mark.parametrize("seed", range(3))
 def test_aggregate_bwd_gat(seed, D, H):
-    rng, blk, et, rs, rd, sh, csr, ch = make_case(60 + seed, D=D, H=H, hub=0.1)
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(60 + seed, D=D, H=H, hub=0.1,
+                                                     N=[800, 6000, 20000][seed])
     U = ch["U"]
     Y = rng.standard_normal((U, D)).astype(np.float32)
     ss = rng.standard_normal((U, H)).astype(np.float32)

@@ -111,3 +111,33 @@ def test_kernel_count_independent_of_relations():
         hf().semantic_fuse(sh, 128, "relu", Z, None, None, H)
         counts.append(hf().kernel_launches() - n0)
     assert counts[0] == counts[1] == counts[2] == 2
+
+
+def test_graph_replay_matches_eager():
+    """The captured whole-step CUDA graph computes exactly what eager launches do."""
+    from paper_2408_08490_b200.step import Trainer, DeviceBatch
+    cfg, g, feat, foff = setup("imdb")
+    rs = np.array([r.src for r in cfg.rels], np.int32)
+    rd = np.array([r.dst for r in cfg.rels], np.int32)
+    feat_d = torch.from_numpy(feat).to(DEV)
+    et_d = torch.from_numpy(g.edge_type).to(DEV)
+    dbs = [DeviceBatch(make_batch(cfg, g, b), rs, rd, foff, cfg.target_type, DEV) for b in range(2)]
+    res = []
+    for mode in ("eager", "graph"):
+        tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
+                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.05)
+        tr.load_params(make_params(cfg))
+        for db in dbs:
+            tr.step(db, feat_d, et_d, update=False)
+        losses = []
+        if mode == "graph":
+            graphs = [tr.capture(db, feat_d, et_d)[0] for db in dbs]
+        for i in range(4):
+            if mode == "eager":
+                tr.step(dbs[i % 2], feat_d, et_d)
+            else:
+                graphs[i % 2].replay()
+            losses.append(float(tr.loss.item()))
+        res.append((losses, tr.params.clone()))
+    assert res[0][0] == res[1][0]
+    assert torch.equal(res[0][1], res[1][1])
