@@ -201,7 +201,7 @@ def main():
     ap.add_argument("--config", default="mag", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="hifuse", choices=["hifuse", "reference"])
     ap.add_argument("--pool", type=int, default=16)
-    ap.add_argument("--prec", default="fp32", choices=["fp32", "tf32"])
+    ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

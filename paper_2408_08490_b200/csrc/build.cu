@@ -13,11 +13,11 @@
 //   k_finish     rel_y_off, y_src, slot_y, U
 //   k_scatter    unstable atomic placement into rows + column histogram
 //   scan         col_ptr
-//   k_fix_segments<rows>  warp per row: sort by original column (restores Alg. 2's
+//   k_fix_rows   warp per row: sort by original column (restores Alg. 2's
 //                column order, so the result is bit-exact and deterministic),
 //                then CSC placement
-//   k_fix_segments<cols>  warp per Y row: sort CSC entries by CSR position
-//   k_*_long     the same two sorts for segments longer than 512 (block-wide)
+//   k_fix_cols   thread per Y row: sort CSC entries by CSR position
+//   k_*_long     the same two sorts for longer segments (block-wide)
 #include <vector>
 #include "common.cuh"
 
@@ -100,21 +100,6 @@ __global__ void k_scatter(LayerMeta m, const int* __restrict__ key_e, const int*
   atomicAdd(&ccnt[c], 1);
 }
 
-// Insertion sort of keys[0..n) ascending, carrying vals (n <= kShort).
-__device__ __forceinline__ void thread_sort(int* keys, int* vals, int n) {
-  for (int i = 1; i < n; i++) {
-    int k = keys[i], v = vals[i];
-    int j = i - 1;
-    while (j >= 0 && keys[j] > k) {
-      keys[j + 1] = keys[j];
-      vals[j + 1] = vals[j];
-      j--;
-    }
-    keys[j + 1] = k;
-    vals[j + 1] = v;
-  }
-}
-
 // Block-wide sort of one long segment (unique keys).  Shared-memory bitonic
 // up to kLongCap, else rank sort through the scratch buffers.
 __device__ void block_sort(int* keys, int* vals, int n, int* sk, int* sv, int* gk, int* gv) {
@@ -174,10 +159,12 @@ __device__ __forceinline__ void csc_place(int row, int b, int e_, const int* col
   }
 }
 
-// Warp-level sort of one segment of n <= kWarpCap unique keys (+ values):
-// n <= 32 in registers (shuffle bitonic), else bitonic in this warp's shared
-// memory slice.  Returns with keys/vals written back in ascending key order.
-static constexpr int kWarpCap = 512;
+// Segment fix-up sorts (unique keys, carried values).
+//  k_fix_rows: one warp per CSR row, n <= 32 sorted in registers (shuffle
+//              bitonic), then the sorted row is placed into the CSC.
+//  k_fix_cols: one thread per CSC column, n <= kThreadCap sorted in place.
+//  Longer segments go to the block-wide kernels (k_rows_long / k_cols_long).
+static constexpr int kThreadCap = 16;
 
 __device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
 #pragma unroll
@@ -194,78 +181,54 @@ __device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
     }
 }
 
-__device__ void warp_sort_smem(int* keys, int* vals, int n, int* sk, int* sv, int lane) {
-  int P = 64;
-  while (P < n) P <<= 1;
-  for (int i = lane; i < P; i += 32) {
-    sk[i] = i < n ? keys[i] : 0x7fffffff;
-    sv[i] = i < n ? vals[i] : 0;
+__global__ void __launch_bounds__(256)
+k_fix_rows(int rows, const int* __restrict__ row_ptr, int* eperm, int* col,
+           const int* __restrict__ col_ptr, int* ccur, int* csc_pos, int* csc_row, int* long_list,
+           int* long_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int b = row_ptr[row], e = row_ptr[row + 1], n = e - b;
+  if (n > 32) {
+    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = row;
+    return;
   }
-  __syncwarp();
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < P; i += 32) {
-        int l = i ^ j;
-        if (l > i) {
-          bool up = (i & k) == 0;
-          int a = sk[i], b = sk[l];
-          if ((a > b) == up) {
-            sk[i] = b; sk[l] = a;
-            int t = sv[i]; sv[i] = sv[l]; sv[l] = t;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  for (int i = lane; i < n; i += 32) {
-    keys[i] = sk[i];
-    vals[i] = sv[i];
+  int key = lane < n ? eperm[b + lane] : 0x7fffffff;
+  int val = lane < n ? col[b + lane] : 0;
+  if (n > 1) warp_sort_regs(key, val, lane);
+  if (lane < n) {
+    eperm[b + lane] = key;
+    col[b + lane] = val;
+    int w = col_ptr[val] + atomicAdd(&ccur[val], 1);
+    csc_pos[w] = b + lane;
+    csc_row[w] = row;
   }
-  __syncwarp();
 }
 
-// One warp per segment.  ROWS: segments are CSR rows (keys eperm, vals col),
-// followed by CSC placement of the sorted row.  !ROWS: CSC columns (keys
-// csc_pos, vals csc_row).  Segments longer than kWarpCap go to the block path.
-template <bool ROWS>
 __global__ void __launch_bounds__(256)
-k_fix_segments(int nseg_host, const int* __restrict__ nseg_dev, const int* __restrict__ ptr,
-               int* keys, int* vals, const int* __restrict__ col_ptr, int* ccur, int* csc_pos,
-               int* csc_row, int* long_list, int* long_cnt) {
-  __shared__ int sk[8][kWarpCap];
-  __shared__ int sv[8][kWarpCap];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int seg = blockIdx.x * 8 + w;
-  const int nseg = nseg_dev ? *nseg_dev : nseg_host;
-  if (seg >= nseg) return;
-  const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
-  if (n > kWarpCap) {
-    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = seg;
+k_fix_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* csc_pos,
+           int* csc_row, int* long_list, int* long_cnt) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= *U_dev) return;
+  const int b = col_ptr[u], e = col_ptr[u + 1], n = e - b;
+  if (n <= 1) return;
+  if (n > kThreadCap) {
+    long_list[atomicAdd(long_cnt, 1)] = u;
     return;
   }
-  if (n <= 32) {
-    int key = lane < n ? keys[b + lane] : 0x7fffffff;
-    int val = lane < n ? vals[b + lane] : 0;
-    if (n > 1) warp_sort_regs(key, val, lane);
-    if (lane < n) {
-      keys[b + lane] = key;
-      vals[b + lane] = val;
-      if (ROWS) {
-        int w_ = col_ptr[val] + atomicAdd(&ccur[val], 1);
-        csc_pos[w_] = b + lane;
-        csc_row[w_] = seg;
-      }
+  int* k_ = csc_pos + b;
+  int* v_ = csc_row + b;
+  for (int i = 1; i < n; i++) {
+    int k = k_[i], v = v_[i];
+    int j = i - 1;
+    while (j >= 0 && k_[j] > k) {
+      k_[j + 1] = k_[j];
+      v_[j + 1] = v_[j];
+      j--;
     }
-    return;
+    k_[j + 1] = k;
+    v_[j + 1] = v;
   }
-  warp_sort_smem(keys + b, vals + b, n, sk[w], sv[w], lane);
-  if (ROWS)
-    for (int p = b + lane; p < e; p += 32) {
-      int c = vals[p];
-      int w_ = col_ptr[c] + atomicAdd(&ccur[c], 1);
-      csc_pos[w_] = p;
-      csc_row[w_] = seg;
-    }
 }
 
 __global__ void k_rows_long(const int* __restrict__ row_ptr, int* eperm, int* col,
@@ -413,14 +376,12 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     int* rows_long = w.lists;
     int* cols_long = w.lists + m.rows;
     const int smem = 2 * kLongCap * sizeof(int);
-    HF_LAUNCH(k_fix_segments<true>, ceil_div(m.rows, 8), 256, 0, s, m.rows, (const int*)nullptr,
-              o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long,
-              w.counters);
+    HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 8), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
+              o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
     HF_LAUNCH(k_rows_long, 148, 256, smem, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
               o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv);
-    HF_LAUNCH(k_fix_segments<false>, ceil_div(U_max, 8), 256, 0, s, 0, o.U_dev, o.col_ptr,
-              o.csc_pos, o.csc_row, (const int*)nullptr, (int*)nullptr, (int*)nullptr,
-              (int*)nullptr, cols_long, w.counters + 1);
+    HF_LAUNCH(k_fix_cols, ceil_div(U_max, 256), 256, 0, s, o.U_dev, o.col_ptr, o.csc_pos,
+              o.csc_row, cols_long, w.counters + 1);
     HF_LAUNCH(k_cols_long, 148, 256, smem, s, o.col_ptr, o.csc_pos, o.csc_row, cols_long,
               w.counters + 1, w.gk, w.gv);
   }

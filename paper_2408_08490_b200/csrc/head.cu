@@ -6,6 +6,8 @@
 
 namespace hf {
 
+static constexpr int kSplit = 16;
+
 __device__ __forceinline__ float block_reduce(float v, float* sm, bool is_max) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int o = 16; o; o >>= 1) {
@@ -31,18 +33,21 @@ k_gemm_small(int M, int N, int K, const float* __restrict__ A, int lda,
   __shared__ float Bs[16][64 + 1];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int kper = (K + gridDim.z - 1) / gridDim.z;
+  const int kb0 = blockIdx.z * kper, kb1 = min(K, kb0 + kper);
+  C += (long long)blockIdx.z * M * ldc;
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += 16) {
+  for (int k0 = kb0; k0 < kb1; k0 += 16) {
     for (int i = tid; i < 16 * 64; i += 256) {
       int kk = TA ? i / 64 : i % 16, mm = TA ? i % 64 : i / 16;
       int m = m0 + mm, k = k0 + kk;
       float v = 0.f;
-      if (m < M && k < K) v = TA ? A[(long long)k * lda + a_row0 + m] : A[(a_row0 + m) * lda + k];
+      if (m < M && k < kb1) v = TA ? A[(long long)k * lda + a_row0 + m] : A[(a_row0 + m) * lda + k];
       As[kk][mm] = v;
       int kb = TB ? i % 16 : i / 64, nb = TB ? i / 16 : i % 64;
       int n = n0 + nb, k2 = k0 + kb;
       float w = 0.f;
-      if (n < N && k2 < K) w = TB ? B[(long long)n * ldb + k2] : B[(long long)k2 * ldb + n];
+      if (n < N && k2 < kb1) w = TB ? B[(long long)n * ldb + k2] : B[(long long)k2 * ldb + n];
       Bs[kb][nb] = w;
     }
     __syncthreads();
@@ -108,13 +113,32 @@ __global__ void k_xent_loss(int B, const float* __restrict__ row_loss, float* __
   if (threadIdx.x == 0) loss[0] = s / (float)B;
 }
 
-// dbc[c] = sum_b dlog[b][c]  (fixed order)
-__global__ void k_xent_dbias(int B, int C, const float* __restrict__ dlog, float* __restrict__ dbc) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+// dbc[c] = sum_b dlog[b][c]: 32 columns x 8 row groups per block, fixed-order
+// shared-memory combine (deterministic).
+__global__ void __launch_bounds__(256)
+k_xent_dbias(int B, int C, const float* __restrict__ dlog, float* __restrict__ dbc) {
+  __shared__ float red[8][33];
+  int c = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
   float s = 0.f;
-  for (int b = 0; b < B; b++) s += dlog[(long long)b * C + c];
-  dbc[c] = s;
+  if (c < C)
+    for (int b = g; b < B; b += 8) s += dlog[(long long)b * C + c];
+  red[g][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (g == 0 && c < C) {
+    float t = red[0][threadIdx.x];
+    for (int q = 1; q < 8; q++) t += red[q][threadIdx.x];
+    dbc[c] = t;
+  }
+}
+
+// sum of split-K partials, fixed order
+__global__ void k_sum_splits(int n, int splits, const float* __restrict__ part,
+                             float* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = 0.f;
+  for (int z = 0; z < splits; z++) s += part[(long long)z * n + i];
+  out[i] = s;
 }
 
 __global__ void k_sgd(float4* __restrict__ p, const float4* __restrict__ g, long long n4, float lr) {
@@ -139,7 +163,8 @@ extern "C" {
 
 size_t hifuse_xent_ws_bytes(int B, int D, int C) {
   (void)D;
-  return carve_bytes((long long)B * C, 4) + carve_bytes(B, 4);
+  return carve_bytes((long long)B * C, 4) + carve_bytes(B, 4) +
+         carve_bytes((long long)kSplit * D * C, 4);
 }
 
 hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t h_rows,
@@ -155,6 +180,7 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   char* p = (char*)d_ws;
   float* dlog = carve<float>(p, (long long)B * C);
   float* row_loss = carve<float>(p, B);
+  float* part = carve<float>(p, (long long)kSplit * D * C);
   cudaMemsetAsync(d_dH, 0, sizeof(float) * h_rows * D, s);
   // logits = Hs Wc
   dim3 g1(ceil_div(C, 64), ceil_div(B, 64));
@@ -166,11 +192,12 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   dim3 g2(ceil_div(D, 64), ceil_div(B, 64));
   HF_LAUNCH((k_gemm_small<false, true>), g2, 256, 0, s, B, D, C, dlog, C, d_Wc, C, d_dH, D, 0ll,
             (long long)h_row0);
-  // dWc = Hs^T dlog
-  dim3 g3(ceil_div(C, 64), ceil_div(D, 64));
+  // dWc = Hs^T dlog: split-K over the batch, then a fixed-order sum
+  dim3 g3(ceil_div(C, 64), ceil_div(D, 64), kSplit);
   HF_LAUNCH((k_gemm_small<true, false>), g3, 256, 0, s, D, C, B, d_H + h_row0 * D, D, dlog, C,
-            d_dWc, C, 0ll, 0ll);
-  HF_LAUNCH(k_xent_dbias, ceil_div(C, 128), 128, 0, s, B, C, dlog, d_dbc);
+            part, C, 0ll, 0ll);
+  HF_LAUNCH(k_sum_splits, ceil_div((long long)D * C, 256), 256, 0, s, D * C, kSplit, part, d_dWc);
+  HF_LAUNCH(k_xent_dbias, ceil_div(C, 32), 256, 0, s, B, C, dlog, d_dbc);
   return last_cuda();
 }
 

@@ -504,13 +504,14 @@ __global__ void k_dx_sdst(DgradMeta dm, int dst_rows, int K, int H, const float*
   dX[(long long)(dm.type_src_off[t] + i) * K + k] += s;
 }
 
-void make_dgrad_meta(const LayerMeta& m, bool has_root, DgradMeta* dm) {
+void make_dgrad_meta(const LayerMeta& m, bool has_root, DgradMeta* dm, int bm) {
   dm->T = m.T;
   dm->has_root = has_root ? 1 : 0;
+  dm->bm = bm;
   int tiles = 0, ko = 0, ki = 0;
   for (int t = 0; t < m.T; t++) {
     dm->tile_off[t] = tiles;
-    tiles += (m.n_src[t] + kBM - 1) / kBM;
+    tiles += (m.n_src[t] + bm - 1) / bm;
     dm->n_src[t] = m.n_src[t];
     dm->n_dst[t] = m.n_dst[t];
     dm->out_off[t] = ko;
@@ -574,6 +575,7 @@ size_t hifuse_project_ws_bytes(const hifuse_layer_shape* shape, int K, int D, in
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
   size_t b = 2 * carve_bytes(m.R + m.T + 1, 4);            // tile_off, chunk_off
   b += carve_bytes((long long)m.R * K * (heads > 0 ? heads : 1), 4);   // v
+  b += carve_bytes((long long)(m.R + m.T) * K * D, 4);     // transposed weights (tf32 path)
   return b;
 }
 
@@ -603,8 +605,11 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   int* tile_off = carve<int>(p, m.R + m.T + 1);
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
   float* v = carve<float>(p, (long long)m.R * K * (heads > 0 ? heads : 1));
+  float* Wt = carve<float>(p, (long long)(m.R + m.T) * K * D);
   if (prec == HIFUSE_PREC_TF32) {
-    rc = project_tc_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0, s);
+    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, 128, kCH);
+    rc = project_tc_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0,
+                           tile_off, Wt, s);
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
@@ -656,8 +661,8 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
                                  const float* d_ds_src, const float* d_ds_dst, float* d_dX,
                                  float* d_dW_rel, float* d_dW_root, float* d_datt, void* d_ws,
                                  size_t ws_bytes, hifuse_stream_t stream) {
-  (void)prec;
   if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
+  if (prec != HIFUSE_PREC_FP32 && prec != HIFUSE_PREC_TF32) return HIFUSE_ERR_UNSUPPORTED;
   LayerMeta m;
   hifuse_status rc = make_meta(shape, &m);
   if (rc != HIFUSE_OK) return rc;
@@ -690,16 +695,22 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
     HF_LAUNCH(k_dy_score, ceil_div(U_max, 8), 256, 0, s, m.R, D, H, csr->U_dev, csr->rel_y_off,
               d_att, d_ds_src, d_dY);
   }
-  HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
-  unsigned grid = (unsigned)chunks;
+  if (prec == HIFUSE_PREC_TF32) {
+    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCHT);
+    wgrad_tc_launch(m, pm, K, D, chunk_off, csr->rel_y_off, csr->y_src, d_gather_ids, d_X, d_dY,
+                    d_G, partial, (unsigned)proj_max_tiles(m, kCHT), s);
+  } else {
+    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
+    unsigned grid = (unsigned)chunks;
 #define HF_WG(KK, DD)                                                                          \
   HF_LAUNCH((k_wgrad_partial<KK, DD>), grid, 256, 0, s, pm, chunk_off, csr->rel_y_off,         \
             csr->y_src, d_gather_ids, d_X, d_dY, d_G, partial)
-  if (K == 128 && D == 128) HF_WG(128, 128);
-  else if (K == 128 && D == 64) HF_WG(128, 64);
-  else if (K == 64 && D == 128) HF_WG(64, 128);
-  else HF_WG(64, 64);
+    if (K == 128 && D == 128) HF_WG(128, 128);
+    else if (K == 128 && D == 64) HF_WG(128, 64);
+    else if (K == 64 && D == 128) HF_WG(64, 128);
+    else HF_WG(64, 64);
 #undef HF_WG
+  }
   int G = d_W_root ? m.R + m.T : m.R;
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
             chunk_off, (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root);
@@ -719,15 +730,20 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   }
   if (d_dX) {
     DgradMeta dm;
-    make_dgrad_meta(m, d_W_root != nullptr, &dm);
-    unsigned gd = dm.tile_off[m.T];
+    if (prec == HIFUSE_PREC_TF32) {
+      make_dgrad_meta(m, d_W_root != nullptr, &dm, 128);
+      dgrad_tc_launch(dm, K, D, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX, s);
+    } else {
+      make_dgrad_meta(m, d_W_root != nullptr, &dm);
+      unsigned gd = dm.tile_off[m.T];
 #define HF_DG(KK, DD)                                                                         \
   HF_LAUNCH((k_dgrad<KK, DD>), gd, 256, 0, s, dm, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX)
-    if (K == 128 && D == 128) HF_DG(128, 128);
-    else if (K == 128 && D == 64) HF_DG(128, 64);
-    else if (K == 64 && D == 128) HF_DG(64, 128);
-    else HF_DG(64, 64);
+      if (K == 128 && D == 128) HF_DG(128, 128);
+      else if (K == 128 && D == 64) HF_DG(128, 64);
+      else if (K == 64 && D == 128) HF_DG(64, 128);
+      else HF_DG(64, 64);
 #undef HF_DG
+    }
     if (d_att)
       HF_LAUNCH(k_dx_sdst, ceil_div((long long)m.dst_rows * K, 256), 256, 0, s, dm, m.dst_rows, K,
                 H, v, d_ds_dst, d_dX);

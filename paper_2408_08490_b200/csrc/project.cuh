@@ -20,7 +20,7 @@ struct ProjMeta {
 };
 
 struct DgradMeta {
-  int T, has_root;
+  int T, has_root, bm;
   int tile_off[HF_MAX_T + 1];      // kBM-row tiles of each type's source rows
   int n_src[HF_MAX_T];
   int n_dst[HF_MAX_T];
@@ -35,13 +35,27 @@ struct DgradMeta {
 };
 
 void make_proj_meta(const LayerMeta& m, bool has_root, ProjMeta* pm);
-void make_dgrad_meta(const LayerMeta& m, bool has_root, DgradMeta* dm);
+void make_dgrad_meta(const LayerMeta& m, bool has_root, DgradMeta* dm, int bm = kBM);
 long long proj_max_tiles(const LayerMeta& m, int step);
 
 // tcgen05 TF32 forward projection (project_tc.cu).
+// tcgen05 TF32 dgrad: dX[type s rows] = sum_terms A_term W_term^T (A = dYt rows
+// through slot_y, or G for the root term).  dm built with bm = 128.
+hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
+                              const float* dY, const float* G, const float* W_rel,
+                              const float* W_root, float* dX, cudaStream_t s);
+// tcgen05 TF32 wgrad partials: P[c] = sum_{rows of chunk c} X_row^T dYt_row
+// (chunks of kCHT rows per group from chunk_off).
+static constexpr int kCHT = 1024;
+hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
+                              const int* chunk_off, const int* rel_y_off, const int* y_src,
+                              const int* gather_ids, const float* X, const float* dY,
+                              const float* G, float* partial, unsigned grid, cudaStream_t s);
+// tile_off: 128-row tile table of the groups (k_group_table); Wt: workspace
+// for the transposed weights [(R+T)][D][K].
 hifuse_status project_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
                                 const hifuse_csr* csr, const float* X, const int* gather_ids,
                                 const float* W_rel, const float* W_root, float* Y, float* R0,
-                                cudaStream_t s);
+                                int* tile_off, float* Wt, cudaStream_t s);
 
 }  // namespace hf

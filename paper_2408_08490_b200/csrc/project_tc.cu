@@ -1,15 +1,497 @@
-// project_tc.cu -- tcgen05 (5th-gen tensor core) TF32 grouped projection.
+// project_tc.cu -- A3 projection on the 5th-generation tensor cores:
+// tcgen05.mma kind::tf32, fp32 accumulators in TMEM (readings C17/C18).
+//
+// Grouped GEMM: every 128-row output tile belongs to one group (relation r:
+// compact Y rows, A rows gathered through y_src [and gather_ids for layer 0,
+// i.e. the feature collection A2 is fused into the operand load]; or root
+// type t: the destination prefix of X_t).  Per tile:
+//   * 128 threads; thread t owns output row t of the tile;
+//   * K is streamed in 32-element (128-byte) chunks through a 2-stage shared
+//     memory ring; A rows are gathered with 16-byte cp.async straight into the
+//     128B-swizzled K-major layout the MMA descriptors describe; B = W_g^T
+//     (pre-transposed to [D][K], K-major) the same way;
+//   * one elected thread issues 4 tcgen05.mma (M=128, N=D, K=8) per chunk and
+//     commits them to the stage's mbarrier, which frees the stage;
+//   * epilogue: warp w reads TMEM lanes 32w..32w+31 (its 32 rows) with
+//     tcgen05.ld and stores fp32 rows.
+// The projection is HBM-bound at K = D = 64/128 (32 flop/B), so the design
+// goal is streaming A at full bandwidth with enough CTAs per SM (64 KB smem,
+// <=128 TMEM columns each -> 3-4 CTAs/SM) rather than peak MMA rate.
 #include "project.cuh"
+#include "tc_common.cuh"
 
 namespace hf {
+
+using namespace tc;
+
+__device__ __forceinline__ bool tc_resolve(const ProjMeta& pm, const int* table,
+                                           const int* rel_y_off, int bid, int step, int* g_out,
+                                           int* r0, int* nrows) {
+  int G = pm.R + pm.T;
+  if (bid >= table[G]) return false;
+  int lo = 0, hi = G;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (table[mid] <= bid) lo = mid; else hi = mid;
+  }
+  int g = lo;
+  int total = g < pm.R ? rel_y_off[g + 1] - rel_y_off[g] : pm.n_dst[g - pm.R];
+  int local0 = (bid - table[g]) * step;
+  *g_out = g;
+  *r0 = local0;
+  *nrows = min(step, total - local0);
+  return *nrows > 0;
+}
+
+__device__ __forceinline__ long long tc_a_row(const ProjMeta& pm, const int* rel_y_off,
+                                              const int* y_src, const int* gather_ids, int g,
+                                              int j) {
+  int x;
+  if (g < pm.R) x = pm.type_src_off[pm.rel_src[g]] + y_src[rel_y_off[g] + j];
+  else x = pm.type_src_off[g - pm.R] + j;
+  return gather_ids ? (long long)gather_ids[x] : (long long)x;
+}
+
+// Wt[g][n][k] = W_g[k][n]  (groups: relations then root types)
+__global__ void k_wt_transpose(int R, int G, int K, int D, const float* __restrict__ W_rel,
+                               const float* __restrict__ W_root, float* __restrict__ Wt) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)G * K * D) return;
+  int g = (int)(idx / ((long long)K * D));
+  int rem = (int)(idx % ((long long)K * D));
+  int n = rem / K, k = rem % K;
+  const float* W = g < R ? W_rel + (long long)g * K * D : W_root + (long long)(g - R) * K * D;
+  Wt[idx] = W[(long long)k * D + n];
+}
+
+template <int K, int D>
+__global__ void __launch_bounds__(128)
+k_proj_fwd_tc(ProjMeta pm, const int* __restrict__ tile_off, const int* __restrict__ rel_y_off,
+              const int* __restrict__ y_src, const int* __restrict__ gather_ids,
+              const float* __restrict__ X, const float* __restrict__ Wt, float* __restrict__ Y,
+              float* __restrict__ R0) {
+  constexpr int BM = 128, NC = K / 32;
+  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = D * 128, STAGE = A_STAGE + B_STAGE;
+  constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 0);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_slot;
+  int g, r0, nrows;
+  if (!tc_resolve(pm, tile_off, rel_y_off, blockIdx.x, BM, &g, &r0, &nrows)) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar0 = smem_u32(&bars[0]), bar1 = smem_u32(&bars[1]);
+  if (tid == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar1, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), D);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  const float* arow = X;
+  uint32_t abytes = 0;
+  if (tid < nrows) {
+    arow = X + tc_a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + tid) * K;
+    abytes = 16;
+  }
+  const float* brow = Wt + ((long long)g * D + (tid < D ? tid : 0)) * K;
+
+  auto load = [&](int c, int s) {
+    const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+    for (int j = 0; j < 8; j++) cp_async16(sa + sw128_off(tid, j), arow + c * 32 + j * 4, abytes);
+    if (tid < D) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) cp_async16(sb + sw128_off(tid, j), brow + c * 32 + j * 4, 16);
+    }
+    cp_async_commit();
+  };
+
+  load(0, 0);
+#pragma unroll
+  for (int c = 0; c < NC; c++) {
+    const int s = c & 1;
+    if (c + 1 < NC) {
+      if (c + 1 >= 2) mbar_wait((c + 1) & 1 ? bar1 : bar0, ((c - 1) >> 1) & 1);
+      load(c + 1, (c + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        mma_tf32(tmem, sw128_desc(sa + k * 32, 16, 1024), sw128_desc(sb + k * 32, 16, 1024), IDESC,
+                 (c | k) ? 1u : 0u);
+      mma_commit(s ? bar1 : bar0);
+    }
+    __syncwarp();
+  }
+  mbar_wait((NC - 1) & 1 ? bar1 : bar0, ((NC - 1) >> 1) & 1);
+  tc_fence_after();
+
+  float* out = g < pm.R ? Y + (long long)rel_y_off[g] * D
+                        : R0 + (long long)pm.type_dst_off[g - pm.R] * D;
+  const int row = warp * 32 + lane;
+  float* orow = out + (long long)(r0 + row) * D;
+#pragma unroll
+  for (int c0 = 0; c0 < D; c0 += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    if (row < nrows) {
+      float4* o = reinterpret_cast<float4*>(orow + c0);
+      o[0] = make_float4(v[0], v[1], v[2], v[3]);
+      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+      o[2] = make_float4(v[8], v[9], v[10], v[11]);
+      o[3] = make_float4(v[12], v[13], v[14], v[15]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, D);
+}
+
+template <int K, int D>
+static constexpr int fwd_smem() {
+  return 2 * (128 * 128 + D * 128) + 1024;
+}
 
 hifuse_status project_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
                                 const hifuse_csr* csr, const float* X, const int* gather_ids,
                                 const float* W_rel, const float* W_root, float* Y, float* R0,
-                                cudaStream_t s) {
-  (void)m; (void)pm; (void)K; (void)D; (void)csr; (void)X; (void)gather_ids; (void)W_rel;
-  (void)W_root; (void)Y; (void)R0; (void)s;
-  return HIFUSE_ERR_UNSUPPORTED;
+                                int* tile_off, float* Wt, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_proj_fwd_tc<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<128, 128>());
+    cudaFuncSetAttribute(k_proj_fwd_tc<128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<128, 64>());
+    cudaFuncSetAttribute(k_proj_fwd_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<64, 128>());
+    cudaFuncSetAttribute(k_proj_fwd_tc<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<64, 64>());
+    attr = true;
+  }
+  const int G = pm.has_root ? m.R + m.T : m.R;
+  HF_LAUNCH(k_wt_transpose, ceil_div((long long)G * K * D, 256), 256, 0, s, m.R, G, K, D, W_rel,
+            W_root, Wt);
+  unsigned grid = (unsigned)proj_max_tiles(m, 128);
+#define HF_TC(KK, DD)                                                                          \
+  HF_LAUNCH((k_proj_fwd_tc<KK, DD>), grid, 128, (fwd_smem<KK, DD>()), s, pm, tile_off,         \
+            csr->rel_y_off, csr->y_src, gather_ids, X, Wt, Y, R0)
+  if (K == 128 && D == 128) HF_TC(128, 128);
+  else if (K == 128 && D == 64) HF_TC(128, 64);
+  else if (K == 64 && D == 128) HF_TC(64, 128);
+  else HF_TC(64, 64);
+#undef HF_TC
+  return HIFUSE_OK;
+}
+
+}  // namespace hf
+
+namespace hf {
+
+// ----------------------------------------------------------------- dgrad ----
+// Tile = 128 source rows of one type s; the "K loop" runs over the terms
+// (relations out of s, then the root weight) x D/32 chunks.  A chunk: 32
+// columns of dYt rows gathered through slot_y (zero rows where the source has
+// no edge of that relation); B chunk: W_term[k][d0..d0+32) for every k, which
+// is already K-major (row k contiguous in d).  N = K.
+template <int K, int D>
+__global__ void __launch_bounds__(128)
+k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
+           const float* __restrict__ G, const float* __restrict__ W_rel,
+           const float* __restrict__ W_root, float* __restrict__ dX) {
+  constexpr int BM = 128, DC = D / 32;
+  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = K * 128, STAGE = A_STAGE + B_STAGE;
+  constexpr uint32_t IDESC = idesc_tf32(BM, K, 0, 0);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_slot;
+  const int s_ = upper_bound_i(dm.tile_off, dm.T + 1, blockIdx.x) - 1;
+  const int j0 = (blockIdx.x - dm.tile_off[s_]) * BM;
+  const int nrows = min(BM, dm.n_src[s_] - j0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar0 = smem_u32(&bars[0]), bar1 = smem_u32(&bars[1]);
+  if (tid == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar1, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), K);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int nout = dm.out_off[s_ + 1] - dm.out_off[s_];
+  const int nterm = nout + (dm.has_root ? 1 : 0);
+  const int NC = nterm * DC;
+  const int j = j0 + tid;
+
+  auto load = [&](int c, int st) {
+    const int term = c / DC, d0 = (c % DC) * 32;
+    const bool root = term == nout;
+    long long a = -1;
+    const float* W;
+    if (root) {
+      if (tid < nrows && j < dm.n_dst[s_]) a = (long long)dm.type_dst_off[s_] + j;
+      W = W_root + (long long)s_ * K * D;
+    } else {
+      const int r = dm.out_rel[dm.out_off[s_] + term];
+      if (tid < nrows) a = slot_y[dm.slot_off[r] + j];
+      W = W_rel + (long long)r * K * D;
+    }
+    const float* A = root ? G : dY;
+    const float* arow = a >= 0 ? A + a * D + d0 : A;
+    const uint32_t abytes = a >= 0 ? 16u : 0u;
+    const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+    for (int q = 0; q < 8; q++) cp_async16(sa + sw128_off(tid, q), arow + q * 4, abytes);
+    if (tid < K) {
+      const float* brow = W + (long long)tid * D + d0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) cp_async16(sb + sw128_off(tid, q), brow + q * 4, 16);
+    }
+    cp_async_commit();
+  };
+
+  if (NC > 0) load(0, 0);
+  for (int c = 0; c < NC; c++) {
+    const int st = c & 1;
+    if (c + 1 < NC) {
+      if (c + 1 >= 2) mbar_wait((c + 1) & 1 ? bar1 : bar0, ((c - 1) >> 1) & 1);
+      load(c + 1, (c + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        mma_tf32(tmem, sw128_desc(sa + k * 32, 16, 1024), sw128_desc(sb + k * 32, 16, 1024), IDESC,
+                 (c | k) ? 1u : 0u);
+      mma_commit(st ? bar1 : bar0);
+    }
+    __syncwarp();
+  }
+  if (NC > 0) {
+    mbar_wait((NC - 1) & 1 ? bar1 : bar0, ((NC - 1) >> 1) & 1);
+    tc_fence_after();
+  }
+  const int row = warp * 32 + lane;
+  float* orow = dX + (long long)(dm.type_src_off[s_] + j0 + row) * K;
+#pragma unroll
+  for (int c0 = 0; c0 < K; c0 += 16) {
+    float v[16];
+    if (NC > 0) {
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; q++) v[q] = 0.f;
+    }
+    if (row < nrows) {
+      float4* o = reinterpret_cast<float4*>(orow + c0);
+      o[0] = make_float4(v[0], v[1], v[2], v[3]);
+      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+      o[2] = make_float4(v[8], v[9], v[10], v[11]);
+      o[3] = make_float4(v[12], v[13], v[14], v[15]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, K);
+}
+
+// ----------------------------------------------------------------- wgrad ----
+// Chunk = up to kCHT rows of one group; partial[chunk] = A^T B over the rows,
+// A = X rows (features = M, padded to 128 when K = 64), B = dYt / G rows
+// (N = D).  The reduction runs over rows, so both operands are MN-major
+// (SWIZZLE_128B_BASE32B): a stage holds 32 rows; per 32-feature block the 32
+// rows are 8 atoms of 4 rows x 128 B (512 B each, SBO = 512), blocks at
+// LBO = 4096; each 16-byte cp.async (4 features of one row) lands inside one
+// swizzled 32-byte chunk.
+static constexpr int kWgStages = 3;
+
+template <int K, int D>
+__global__ void __launch_bounds__(128)
+k_wgrad_tc(ProjMeta pm, const int* __restrict__ chunk_off, const int* __restrict__ rel_y_off,
+           const int* __restrict__ y_src, const int* __restrict__ gather_ids,
+           const float* __restrict__ X, const float* __restrict__ dY, const float* __restrict__ G,
+           float* __restrict__ partial) {
+  constexpr int MA = 128;                               // padded M (features)
+  constexpr uint32_t BLK = 4096;                        // one 32-feature block of 32 rows
+  constexpr uint32_t A_STAGE = (MA / 32) * BLK, B_STAGE = (D / 32) * BLK, STAGE = A_STAGE + B_STAGE;
+  constexpr uint32_t IDESC = idesc_tf32(MA, D, 1, 1);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[kWgStages];
+  __shared__ uint32_t tmem_slot;
+  int g, r0, nrows;
+  if (!tc_resolve(pm, chunk_off, rel_y_off, blockIdx.x, kCHT, &g, &r0, &nrows)) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  if (tid == 0) {
+    for (int q = 0; q < kWgStages; q++) mbar_init(smem_u32(&bars[q]), 1);
+    fence_barrier_init();
+  }
+  if (K < MA) {   // zero the padded feature blocks of every stage once
+    for (int q = 0; q < kWgStages; q++)
+      for (int i = tid; i < (int)((MA - K) / 32 * BLK / 16); i += 128)
+        asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(
+                         base + q * STAGE + (K / 32) * BLK + i * 16),
+                     "r"(0));
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), D);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const float* Bbase = g < pm.R ? dY + (long long)rel_y_off[g] * D
+                                : G + (long long)pm.type_dst_off[g - pm.R] * D;
+  const int NST = (nrows + 31) / 32;
+
+  auto load = [&](int c, int st) {
+    const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+    for (int q = 0; q < 32 * K / 4 / 128; q++) {
+      const int i = tid + 128 * q;
+      const int row = i / (K / 4), f = (i % (K / 4)) * 4;
+      const int rr = c * 32 + row;
+      const float* src = X;
+      uint32_t nb = 0;
+      if (rr < nrows) {
+        src = X + tc_a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + rr) * K + f;
+        nb = 16;
+      }
+      cp_async16(sa + (f >> 5) * BLK + (row >> 2) * 512 + sw128b32_off(row, (f & 31) * 4), src, nb);
+    }
+#pragma unroll
+    for (int q = 0; q < 32 * D / 4 / 128; q++) {
+      const int i = tid + 128 * q;
+      const int row = i / (D / 4), f = (i % (D / 4)) * 4;
+      const int rr = c * 32 + row;
+      const float* src = Bbase;
+      uint32_t nb = 0;
+      if (rr < nrows) {
+        src = Bbase + (long long)(r0 + rr) * D + f;
+        nb = 16;
+      }
+      cp_async16(sb + (f >> 5) * BLK + (row >> 2) * 512 + sw128b32_off(row, (f & 31) * 4), src, nb);
+    }
+    cp_async_commit();
+  };
+
+  for (int c = 0; c < kWgStages - 1; c++) {
+    if (c < NST) load(c, c);
+    else cp_async_commit();
+  }
+  for (int c = 0; c < NST; c++) {
+    const int st = c % kWgStages;
+    const int nxt = c + kWgStages - 1;
+    if (nxt < NST) {
+      const int ns = nxt % kWgStages;
+      if (nxt >= kWgStages) mbar_wait(smem_u32(&bars[ns]), ((nxt / kWgStages) - 1) & 1);
+      load(nxt, ns);
+    } else {
+      cp_async_commit();
+    }
+    cp_async_wait<kWgStages - 1>();
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        mma_tf32(tmem, sw128b32_desc(sa + k * 1024, BLK, 512), sw128b32_desc(sb + k * 1024, BLK, 512),
+                 IDESC, (c | k) ? 1u : 0u);
+      mma_commit(smem_u32(&bars[st]));
+    }
+    __syncwarp();
+  }
+  {
+    const int c = NST - 1;
+    mbar_wait(smem_u32(&bars[c % kWgStages]), (c / kWgStages) & 1);
+    tc_fence_after();
+  }
+  // epilogue: TMEM lane = feature k (row of dW), columns = d
+  const int k = warp * 32 + lane;
+  float* P = partial + (long long)blockIdx.x * K * D + (long long)k * D;
+#pragma unroll
+  for (int c0 = 0; c0 < D; c0 += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    if (k < K) {
+      float4* o = reinterpret_cast<float4*>(P + c0);
+      o[0] = make_float4(v[0], v[1], v[2], v[3]);
+      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+      o[2] = make_float4(v[8], v[9], v[10], v[11]);
+      o[3] = make_float4(v[12], v[13], v[14], v[15]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, D);
+}
+
+template <int K, int D>
+static constexpr int dgrad_smem() { return 2 * (128 * 128 + K * 128) + 1024; }
+template <int K, int D>
+static constexpr int wgrad_smem() { return kWgStages * (4 * 4096 + (D / 32) * 4096) + 1024; }
+
+hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
+                              const float* dY, const float* G, const float* W_rel,
+                              const float* W_root, float* dX, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dgrad_tc<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<128, 128>());
+    cudaFuncSetAttribute(k_dgrad_tc<128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<128, 64>());
+    cudaFuncSetAttribute(k_dgrad_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<64, 128>());
+    cudaFuncSetAttribute(k_dgrad_tc<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<64, 64>());
+    attr = true;
+  }
+  unsigned grid = dm.tile_off[dm.T];
+#define HF_DG(KK, DD)                                                                        \
+  HF_LAUNCH((k_dgrad_tc<KK, DD>), grid, 128, (dgrad_smem<KK, DD>()), s, dm, slot_y, dY, G,   \
+            W_rel, W_root, dX)
+  if (K == 128 && D == 128) HF_DG(128, 128);
+  else if (K == 128 && D == 64) HF_DG(128, 64);
+  else if (K == 64 && D == 128) HF_DG(64, 128);
+  else HF_DG(64, 64);
+#undef HF_DG
+  return HIFUSE_OK;
+}
+
+hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
+                              const int* chunk_off, const int* rel_y_off, const int* y_src,
+                              const int* gather_ids, const float* X, const float* dY,
+                              const float* G, float* partial, unsigned grid, cudaStream_t s) {
+  (void)m;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_wgrad_tc<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<128, 128>());
+    cudaFuncSetAttribute(k_wgrad_tc<128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<128, 64>());
+    cudaFuncSetAttribute(k_wgrad_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<64, 128>());
+    cudaFuncSetAttribute(k_wgrad_tc<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<64, 64>());
+    attr = true;
+  }
+#define HF_WG(KK, DD)                                                                          \
+  HF_LAUNCH((k_wgrad_tc<KK, DD>), grid, 128, (wgrad_smem<KK, DD>()), s, pm, chunk_off,         \
+            rel_y_off, y_src, gather_ids, X, dY, G, partial)
+  if (K == 128 && D == 128) HF_WG(128, 128);
+  else if (K == 128 && D == 64) HF_WG(128, 64);
+  else if (K == 64 && D == 128) HF_WG(64, 128);
+  else HF_WG(64, 64);
+#undef HF_WG
+  return HIFUSE_OK;
 }
 
 }  // namespace hf

@@ -111,7 +111,7 @@ class Trainer:
     """Owns parameters, gradients, activations and workspaces of the step."""
 
     def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
-                 prec="fp32", slope=0.2):
+                 prec="tf32", slope=0.2):
         self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
         self.rel_src = np.asarray(rel_src, np.int32)
         self.rel_dst = np.asarray(rel_dst, np.int32)

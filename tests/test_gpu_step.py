@@ -31,8 +31,9 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
 @pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag"])
-def test_step_matches_oracle(key):
+def test_step_matches_oracle(key, prec):
     from paper_2408_08490_b200.step import Trainer, DeviceBatch
     cfg, g, feat, foff = setup(key)
     mb = make_batch(cfg, g, 0)
@@ -40,7 +41,7 @@ def test_step_matches_oracle(key):
     rd = np.array([r.dst for r in cfg.rels], np.int32)
     params = make_params(cfg)
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
-                 cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0)
+                 cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0, prec=prec)
     tr.load_params(params)
     db = DeviceBatch(mb, rs, rd, foff, cfg.target_type, DEV)
     feat_d = torch.from_numpy(feat).to(DEV)
@@ -54,8 +55,14 @@ def test_step_matches_oracle(key):
     fw = om.forward(mb.layers, g.edge_type, rs, rd, X0, np.arange(len(gid), dtype=np.int32),
                     params, cfg.agg, cfg.heads, labels=mb.labels, target_type=cfg.target_type)
     gr = om.backward(fw, mb.layers, g.edge_type, params, mb.labels, cfg.agg, cfg.heads)
-    assert abs(float(loss.item()) - fw["loss"]) <= 1e-5 * max(1.0, abs(fw["loss"]))
-    tol = 2e-4
+    # fp32: CUDA-core projection -> tight; tf32: tcgen05 projection (reading
+    # C18: kind::tf32 drops the low 13 mantissa bits, u = 2^-10).  The layer-0
+    # weight gradients sit behind ~5 chained TF32 GEMMs (fwd proj 0, proj 1,
+    # bwd dgrad 1, wgrad 0 + attention), so DESIGN.md §Tolerances allows
+    # 5 u x 4 (conditioning) = 2e-2 there; the GEMM kernels themselves are
+    # pinned bit-exact on TF32-representable inputs (test_gpu_stages).
+    ltol, tol, htol = (1e-5, 2e-4, 1e-5) if prec == "fp32" else (2e-3, 2e-2, 5e-3)
+    assert abs(float(loss.item()) - fw["loss"]) <= ltol * max(1.0, abs(fw["loss"]))
     checks = [("Wc", gr["Wc"]), ("bc", gr["bc"])]
     for l in range(cfg.num_layers):
         for k in ("W_rel", "W_root", "bias", "att"):
@@ -67,7 +74,7 @@ def test_step_matches_oracle(key):
     # logits-level: the last layer's H on the seeds
     last = tr.last["acts"][-1]["H"][db.h_row0:db.h_row0 + db.B].cpu().numpy()
     err = rel_l2(last, fw["hs"])
-    assert err <= 1e-5, f"{key} H: {err:.3e}"
+    assert err <= htol, f"{key} H: {err:.3e}"
 
 
 def test_sgd_update_and_determinism():
@@ -80,7 +87,7 @@ def test_sgd_update_and_determinism():
     outs = []
     for _ in range(2):
         tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
-                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.05)
+                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.05, prec="tf32")
         tr.load_params(make_params(cfg))
         p0 = tr.params.clone()
         losses = []
@@ -125,7 +132,7 @@ def test_graph_replay_matches_eager():
     res = []
     for mode in ("eager", "graph"):
         tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
-                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.05)
+                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.05, prec="tf32")
         tr.load_params(make_params(cfg))
         for db in dbs:
             tr.step(db, feat_d, et_d, update=False)
