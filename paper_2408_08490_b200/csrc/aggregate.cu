@@ -173,7 +173,7 @@ struct BwdMeta {
 
 // Columns longer than kLongCol (hub sources) are handed to a block-wide
 // kernel so that no single warp serialises thousands of gathers.
-static constexpr int kLongCol = 128;
+static constexpr int kLongCol = 64;
 
 template <int D, bool MEAN>
 __device__ __forceinline__ float4 col_slice_sum(int b, int e, int shift,
@@ -222,15 +222,17 @@ __device__ __forceinline__ float4 col_slice_sum(int b, int e, int shift,
   return acc;
 }
 
+static constexpr int kLongWarps = 32;
+
 template <int D, bool MEAN>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kLongWarps * 32)
 k_agg_bwd_long(BwdMeta bm, const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
                const int* __restrict__ csc_row, const int* __restrict__ row_ptr,
                const float4* __restrict__ G, float4* __restrict__ dY, const int* __restrict__ list,
                const int* __restrict__ cnt) {
   constexpr int LPR = D / 4;
   __shared__ int s_yoff[HF_MAX_R + 1];
-  __shared__ float4 red[kWarpsPerBlock][LPR];
+  __shared__ float4 red[kLongWarps][LPR];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -239,19 +241,26 @@ k_agg_bwd_long(BwdMeta bm, const int* __restrict__ rel_y_off, const int* __restr
     const int u = list[k];
     const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
     const int b = col_ptr[u], e = col_ptr[u + 1];
-    const int per = (e - b + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int per = (e - b + kLongWarps - 1) / kLongWarps;
     const int wb = min(e, b + w * per), we = min(e, wb + per);
     float4 acc = col_slice_sum<D, MEAN>(wb, we, bm.shift[r], csc_row, row_ptr, G, lane);
     if (lane < LPR) red[w][lane] = acc;
     __syncthreads();
     if (w == 0 && lane < LPR) {
       float4 t = red[0][lane];
-      for (int q = 1; q < kWarpsPerBlock; q++) t = f4add(t, red[q][lane]);
+      for (int q = 1; q < kLongWarps; q++) t = f4add(t, red[q][lane]);
       dY[(long long)u * LPR + lane] = t;
     }
     __syncthreads();
   }
 }
+
+// Columns hold 1-3 entries on average, so a warp per column would spend its
+// time in one dependent chain (col_ptr -> csc_row -> row_ptr -> G) per 512 B
+// of output.  Instead kLPC lanes serve one column: a warp covers 32/kLPC
+// columns, each lane gathers D/4/kLPC float4 per entry (independent loads in
+// flight), and the kLPC lanes of a group read 16*kLPC contiguous bytes.
+static constexpr int kLPC = 4;
 
 template <int D, bool MEAN>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -259,21 +268,39 @@ k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __res
           const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
           const int* __restrict__ row_ptr, const float4* __restrict__ G, float4* __restrict__ dY,
           int* __restrict__ long_list, int* __restrict__ long_cnt) {
-  constexpr int LPR = D / 4;
+  constexpr int LPR = D / 4;            // float4 per row
+  constexpr int V = LPR / kLPC;         // float4 per lane
   __shared__ int s_yoff[HF_MAX_R + 1];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (u >= *U_dev) return;
+  const int U = *U_dev;
+  const int u = (blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * (32 / kLPC) + lane / kLPC;
+  const int j = lane % kLPC;
+  if (u >= U) return;
   const int b = col_ptr[u], e = col_ptr[u + 1];
   if (e - b > kLongCol) {
-    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = u;
+    if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
     return;
   }
-  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
-  float4 acc = col_slice_sum<D, MEAN>(b, e, bm.shift[r], csc_row, row_ptr, G, lane);
-  if (lane < LPR) dY[(long long)u * LPR + lane] = acc;
+  const int shift = bm.shift[upper_bound_i(s_yoff, bm.R + 1, u) - 1];
+  float4 acc[V];
+#pragma unroll
+  for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = b; p < e; p++) {
+    const int row = __ldg(csc_row + p);
+    float w = 1.f;
+    if (MEAN) w = 1.f / (float)(__ldg(row_ptr + row + 1) - __ldg(row_ptr + row));
+    const float4* g = G + (long long)(row + shift) * LPR + j;
+    float4 x[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) x[v] = ldg4(g + v * kLPC);
+#pragma unroll
+    for (int v = 0; v < V; v++) acc[v] = MEAN ? f4fma(w, x[v], acc[v]) : f4add(acc[v], x[v]);
+  }
+  float4* o = dY + (long long)u * LPR + j;
+#pragma unroll
+  for (int v = 0; v < V; v++) o[v * kLPC] = acc[v];
 }
 
 // ------------------------------------------------ backward GAT, pass 1 (rows)
@@ -430,7 +457,7 @@ k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
 }
 
 template <int D>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kLongWarps * 32)
 k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
                         const int* __restrict__ col_ptr, const int* __restrict__ csc_pos,
                         const int* __restrict__ csc_row, const float* __restrict__ alpha,
@@ -439,8 +466,8 @@ k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
                         const int* __restrict__ list, const int* __restrict__ cnt) {
   constexpr int LPR = D / 4;
   __shared__ int s_yoff[HF_MAX_R + 1];
-  __shared__ float4 red[kWarpsPerBlock][LPR];
-  __shared__ float reds[kWarpsPerBlock][LPR];
+  __shared__ float4 red[kLongWarps][LPR];
+  __shared__ float reds[kLongWarps][LPR];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -450,7 +477,7 @@ k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
     const int u = list[k];
     const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
     const int b = col_ptr[u], e = col_ptr[u + 1];
-    const int per = (e - b + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int per = (e - b + kLongWarps - 1) / kLongWarps;
     const int wb = min(e, b + w * per), we = min(e, wb + per);
     float4 acc;
     float dss;
@@ -463,7 +490,7 @@ k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
     if (w == 0 && lane < LPR) {
       float4 t = red[0][lane];
       float ts = reds[0][lane];
-      for (int q = 1; q < kWarpsPerBlock; q++) {
+      for (int q = 1; q < kLongWarps; q++) {
         t = f4add(t, red[q][lane]);
         ts += reds[q][lane];
       }
@@ -554,6 +581,7 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
   int* long_cnt = carve<int>(p, 2);
   cudaMemsetAsync(long_cnt, 0, sizeof(int), s);
   unsigned gridU = ceil_div(U_max, kWarpsPerBlock);
+  unsigned gridU4 = ceil_div(U_max, kWarpsPerBlock * (32 / kLPC));
   const int TB = kWarpsPerBlock * 32;
   const unsigned gridL = 296;
   if (agg == HIFUSE_AGG_GAT) {
@@ -571,7 +599,7 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
   HF_LAUNCH(k_agg_bwd_gat_cols<DD>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,   \
             csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
             (float4*)d_dY, d_ds_src, long_list, long_cnt);                                    \
-  HF_LAUNCH(k_agg_bwd_gat_cols_long<DD>, gridL, TB, 0, s, bm, heads, csr->rel_y_off,          \
+  HF_LAUNCH(k_agg_bwd_gat_cols_long<DD>, gridL, kLongWarps * 32, 0, s, bm, heads, csr->rel_y_off,          \
             csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
             (float4*)d_dY, d_ds_src, long_list, long_cnt)
     if (D == 128) { HF_GAT(128); } else { HF_GAT(64); }
@@ -579,10 +607,10 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
   } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
     if (agg == HIFUSE_AGG_MEAN && !csr->row_ptr) return HIFUSE_ERR_INVALID_ARG;
 #define HF_BWD(DD, MM)                                                                        \
-  HF_LAUNCH((k_agg_bwd<DD, MM>), gridU, TB, 0, s, bm, (int)U_max, csr->U_dev, csr->rel_y_off,   \
+  HF_LAUNCH((k_agg_bwd<DD, MM>), gridU4, TB, 0, s, bm, (int)U_max, csr->U_dev, csr->rel_y_off,  \
             csr->col_ptr, csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY,        \
             long_list, long_cnt);                                                               \
-  HF_LAUNCH((k_agg_bwd_long<DD, MM>), gridL, TB, 0, s, bm, csr->rel_y_off, csr->col_ptr,        \
+  HF_LAUNCH((k_agg_bwd_long<DD, MM>), gridL, kLongWarps * 32, 0, s, bm, csr->rel_y_off, csr->col_ptr,        \
             csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY, long_list, long_cnt)
     bool mean = agg == HIFUSE_AGG_MEAN;
     if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }

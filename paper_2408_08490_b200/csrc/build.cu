@@ -205,29 +205,51 @@ k_fix_rows(int rows, const int* __restrict__ row_ptr, int* eperm, int* col,
   }
 }
 
+// One warp per 32 consecutive CSC columns: lane l sorts column 32w+l in place
+// when it has <= kThreadCap entries; columns of (kThreadCap, 32] are sorted by
+// the whole warp in registers, one after another; longer ones go to the
+// block-wide kernel.
 __global__ void __launch_bounds__(256)
 k_fix_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* csc_pos,
            int* csc_row, int* long_list, int* long_cnt) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= *U_dev) return;
-  const int b = col_ptr[u], e = col_ptr[u + 1], n = e - b;
-  if (n <= 1) return;
-  if (n > kThreadCap) {
-    long_list[atomicAdd(long_cnt, 1)] = u;
-    return;
+  const int lane = threadIdx.x & 31;
+  const int U = *U_dev;
+  const int u0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+  if (u0 >= U) return;
+  const int u = u0 + lane;
+  int b = 0, n = 0;
+  if (u < U) {
+    b = col_ptr[u];
+    n = col_ptr[u + 1] - b;
   }
-  int* k_ = csc_pos + b;
-  int* v_ = csc_row + b;
-  for (int i = 1; i < n; i++) {
-    int k = k_[i], v = v_[i];
-    int j = i - 1;
-    while (j >= 0 && k_[j] > k) {
-      k_[j + 1] = k_[j];
-      v_[j + 1] = v_[j];
-      j--;
+  if (n > 1 && n <= kThreadCap) {
+    int* k_ = csc_pos + b;
+    int* v_ = csc_row + b;
+    for (int i = 1; i < n; i++) {
+      int k = k_[i], v = v_[i];
+      int j = i - 1;
+      while (j >= 0 && k_[j] > k) {
+        k_[j + 1] = k_[j];
+        v_[j + 1] = v_[j];
+        j--;
+      }
+      k_[j + 1] = k;
+      v_[j + 1] = v;
     }
-    k_[j + 1] = k;
-    v_[j + 1] = v;
+  }
+  if (n > 32) long_list[atomicAdd(long_cnt, 1)] = u;
+  unsigned mid = __ballot_sync(0xffffffffu, n > kThreadCap && n <= 32);
+  while (mid) {
+    const int src = __ffs(mid) - 1;
+    mid &= mid - 1;
+    const int bb = __shfl_sync(0xffffffffu, b, src), nn = __shfl_sync(0xffffffffu, n, src);
+    int key = lane < nn ? csc_pos[bb + lane] : 0x7fffffff;
+    int val = lane < nn ? csc_row[bb + lane] : 0;
+    warp_sort_regs(key, val, lane);
+    if (lane < nn) {
+      csc_pos[bb + lane] = key;
+      csc_row[bb + lane] = val;
+    }
   }
 }
 
@@ -378,11 +400,11 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     const int smem = 2 * kLongCap * sizeof(int);
     HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 8), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
               o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
-    HF_LAUNCH(k_rows_long, 148, 256, smem, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
+    HF_LAUNCH(k_rows_long, 148, 1024, smem, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
               o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv);
     HF_LAUNCH(k_fix_cols, ceil_div(U_max, 256), 256, 0, s, o.U_dev, o.col_ptr, o.csc_pos,
-              o.csc_row, cols_long, w.counters + 1);
-    HF_LAUNCH(k_cols_long, 148, 256, smem, s, o.col_ptr, o.csc_pos, o.csc_row, cols_long,
+              o.csc_row, cols_long, w.counters + 1);   // 8 warps x 32 columns per block
+    HF_LAUNCH(k_cols_long, 148, 1024, smem, s, o.col_ptr, o.csc_pos, o.csc_row, cols_long,
               w.counters + 1, w.gk, w.gv);
   }
   return last_cuda();

@@ -84,63 +84,64 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total) {
   return base + inc - v;
 }
 
-__global__ void k_scan_reduce(const int* __restrict__ in, long long n, int* __restrict__ bsum) {
-  long long base = (long long)blockIdx.x * kScanTile;
-  int s = 0;
-  for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
-    long long k = base + i;
-    if (k < n) s += in[k];
-  }
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  __shared__ int ws[kScanThreads / 32];
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+// Single-pass exclusive scan with decoupled look-back (tiles claimed in
+// order through an atomic ticket, so every predecessor is already running).
+// status[t] = (flag << 30) | value: flag 1 = tile aggregate, 2 = inclusive
+// prefix.  Values must stay below 2^30 (counts of edges / rows / slots).
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_lookback(const int* __restrict__ in, long long n, int* __restrict__ out,
+                int* __restrict__ ticket, int* __restrict__ status) {
+  __shared__ int s_tile, s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int i = 0; i < kScanThreads / 32; i++) t += ws[i];
-    bsum[blockIdx.x] = t;
-  }
-}
-
-// Single block: exclusive scan of the nb block sums in place; bsum[nb] = total.
-__global__ void k_scan_bsums(int* bsum, int nb) {
-  int carry = 0;
-  for (int base = 0; base < nb; base += kScanThreads) {
-    int i = base + threadIdx.x;
-    int v = i < nb ? bsum[i] : 0;
-    int tot;
-    int ex = block_excl_scan(v, &tot);
-    if (i < nb) bsum[i] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) bsum[nb] = carry;
-}
-
-__global__ void k_scan_down(const int* __restrict__ in, long long n, const int* __restrict__ bsum,
-                            int* __restrict__ out, int nb) {
-  long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
+  const int tile = s_tile;
+  const long long base = (long long)tile * kScanTile + (long long)threadIdx.x * kScanItems;
   int v[kScanItems];
-  int s = 0;
+  int sum = 0;
 #pragma unroll
   for (int j = 0; j < kScanItems; j++) {
     long long k = base + j;
     v[j] = k < n ? in[k] : 0;
-    s += v[j];
+    sum += v[j];
   }
   int tot;
-  int ex = block_excl_scan(s, &tot) + bsum[blockIdx.x];
+  int ex = block_excl_scan(sum, &tot);
+  if (threadIdx.x == 0) {
+    volatile int* st_ = status;
+    int prefix = 0;
+    if (tile == 0) {
+      st_[0] = (2 << 30) | tot;
+    } else {
+      st_[tile] = (1 << 30) | tot;
+      __threadfence();
+      int t = tile - 1;
+      while (true) {
+        int w = st_[t];
+        int flag = (w >> 30) & 3;
+        if (flag == 0) continue;            // predecessor not published yet
+        prefix += w & 0x3fffffff;
+        if (flag == 2) break;
+        t--;
+      }
+      st_[tile] = (2 << 30) | (prefix + tot);
+    }
+    s_prefix = prefix;
+  }
+  __syncthreads();
+  ex += s_prefix;
 #pragma unroll
   for (int j = 0; j < kScanItems; j++) {
     long long k = base + j;
     if (k < n) out[k] = ex;
     ex += v[j];
   }
-  if (blockIdx.x == nb - 1 && threadIdx.x == 0) out[n] = bsum[nb];
+  if ((long long)(tile + 1) * kScanTile >= n && threadIdx.x == kScanThreads - 1)
+    out[n] = s_prefix + tot;
 }
 
 __global__ void k_scan_empty(int* out) { out[0] = 0; }
 
-size_t scan_ws_ints(long long n) { return (size_t)ceil_div(n > 0 ? n : 1, kScanTile) + 1; }
+size_t scan_ws_ints(long long n) { return (size_t)ceil_div(n > 0 ? n : 1, kScanTile) + 2; }
 
 void exclusive_scan(const int* in, int* out, long long n, int* ws, cudaStream_t s) {
   if (n <= 0) {
@@ -148,9 +149,8 @@ void exclusive_scan(const int* in, int* out, long long n, int* ws, cudaStream_t 
     return;
   }
   int nb = (int)ceil_div(n, kScanTile);
-  HF_LAUNCH(k_scan_reduce, nb, kScanThreads, 0, s, in, n, ws);
-  HF_LAUNCH(k_scan_bsums, 1, kScanThreads, 0, s, ws, nb);
-  HF_LAUNCH(k_scan_down, nb, kScanThreads, 0, s, in, n, ws, out, nb);
+  cudaMemsetAsync(ws, 0, sizeof(int) * (nb + 1), s);
+  HF_LAUNCH(k_scan_lookback, nb, kScanThreads, 0, s, in, n, out, ws + nb, ws);
 }
 
 }  // namespace hf

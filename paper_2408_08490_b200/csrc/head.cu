@@ -163,8 +163,8 @@ extern "C" {
 
 size_t hifuse_xent_ws_bytes(int B, int D, int C) {
   (void)D;
-  return carve_bytes((long long)B * C, 4) + carve_bytes(B, 4) +
-         carve_bytes((long long)kSplit * D * C, 4);
+  long long np = (long long)kSplit * D * C > 4ll * B * D ? (long long)kSplit * D * C : 4ll * B * D;
+  return carve_bytes((long long)B * C, 4) + carve_bytes(B, 4) + carve_bytes(np, 4);
 }
 
 hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t h_rows,
@@ -180,7 +180,8 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   char* p = (char*)d_ws;
   float* dlog = carve<float>(p, (long long)B * C);
   float* row_loss = carve<float>(p, B);
-  float* part = carve<float>(p, (long long)kSplit * D * C);
+  float* part = carve<float>(p, (long long)kSplit * D * C > 4ll * B * D ? (long long)kSplit * D * C
+                                                                        : 4ll * B * D);
   cudaMemsetAsync(d_dH, 0, sizeof(float) * h_rows * D, s);
   // logits = Hs Wc
   dim3 g1(ceil_div(C, 64), ceil_div(B, 64));
@@ -189,9 +190,11 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   HF_LAUNCH(k_xent_softmax, ceil_div(B, 8), 256, 0, s, B, C, d_bc, d_labels, dlog, row_loss);
   HF_LAUNCH(k_xent_loss, 1, 256, 0, s, B, row_loss, d_loss);
   // dHs = dlog Wc^T   (Wc is [D, C]: op(B) = Wc^T stored [N = D, K = C])
-  dim3 g2(ceil_div(D, 64), ceil_div(B, 64));
-  HF_LAUNCH((k_gemm_small<false, true>), g2, 256, 0, s, B, D, C, dlog, C, d_Wc, C, d_dH, D, 0ll,
-            (long long)h_row0);
+  dim3 g2(ceil_div(D, 64), ceil_div(B, 64), 4);
+  HF_LAUNCH((k_gemm_small<false, true>), g2, 256, 0, s, B, D, C, dlog, C, d_Wc, C, part, D, 0ll,
+            0ll);
+  HF_LAUNCH(k_sum_splits, ceil_div((long long)B * D, 256), 256, 0, s, B * D, 4, part,
+            d_dH + h_row0 * D);
   // dWc = Hs^T dlog: split-K over the batch, then a fixed-order sum
   dim3 g3(ceil_div(C, 64), ceil_div(D, 64), kSplit);
   HF_LAUNCH((k_gemm_small<true, false>), g3, 256, 0, s, D, C, B, d_H + h_row0 * D, D, dlog, C,
