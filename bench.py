@@ -204,6 +204,9 @@ def main():
     ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", type=int, default=1,
+                    help="1: overlap the next batch's semantic-graph build with this "
+                         "batch's compute (side stream); 0: serial steps")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", 0))
@@ -232,6 +235,8 @@ def main():
     ids = [rank + s * world for s in range(args.pool)]
     mbs = [make_batch(cfg, g, b % nb, epoch=b // nb) for b in ids]
     pool = [DeviceBatch(mb, rs, rd, foff, cfg.target_type, dev, pin=True) for mb in mbs]
+    for i, db in enumerate(pool):
+        db.slot = i                      # private CSR buffers per pool batch
     sizes = [layer_sizes(cfg, g, mb, rs, rd) for mb in mbs]
     feat_d = torch.from_numpy(feat).to(dev)
     et_d = torch.from_numpy(g.edge_type).to(dev)
@@ -247,8 +252,17 @@ def main():
     if hf.read_status(tr.status) != 0:
         raise RuntimeError("device reported invalid edges in the batch pool")
     # one CUDA graph per pool batch: the whole step is replayed without host
-    # launch overhead (all sizes are host-known, nothing syncs inside)
-    graphs = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
+    # launch overhead (all sizes are host-known, nothing syncs inside).
+    # Pipelined (default, N = 1): graph i computes batch i while a side stream
+    # builds the semantic graphs of batch i+1 (Fig. 6 pipeline).
+    serial_graphs = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
+    graphs = serial_graphs
+    side = torch.cuda.Stream()
+    if args.pipeline and world == 1:
+        graphs = [tr.capture_pipelined(db, pool[(i + 1) % len(pool)], feat_d, et_d, side)
+                  for i, db in enumerate(pool)]
+        tr.build_op(pool[0], et_d)()       # batch 0's CSR for the first replay
+        torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -258,7 +272,10 @@ def main():
     def one_step(i, e2e=False, loss_host=None):
         db = pool[i % len(pool)]
         if e2e:
-            db.to_device(non_blocking=True)
+            # host -> device copy of the batch the graph builds: this batch
+            # (serial) or the next one (pipelined build of batch i+1)
+            (db if graphs is serial_graphs else pool[(i + 1) % len(pool)]).to_device(
+                non_blocking=True)
         graphs[i % len(pool)][0].replay()
         if world > 1:
             dist.all_reduce(tr.grads)
@@ -294,6 +311,16 @@ def main():
     launches = sum(graphs[i % len(pool)][1] for i in range(args.steps)) + \
         (args.steps if world > 1 else 0)
     clk = clocks.summary(t0, t1)
+    # the same steps without the build/compute overlap (every graph builds
+    # its own batch first), for reference
+    graphs_pipe = graphs
+    graphs = serial_graphs
+    for i in range(args.warmup):
+        one_step(i)
+    ms_serial, _, _ = timed(args.steps)
+    graphs = graphs_pipe
+    if graphs is not serial_graphs:
+        tr.build_op(pool[0], et_d)()
     # end-to-end through the public API with host (pinned) buffers
     for i in range(args.warmup):
         one_step(i, True, torch.empty(1).pin_memory())
@@ -381,7 +408,10 @@ def main():
         "roofline": roof,
         "aggregation_hbm": agg_gbs,
         "stage_us_per_step": {k: round(v * 1e3, 2) for k, v in sorted(per_step.items())},
-        "launch_mode": "one CUDA graph per pool batch (whole step)",
+        "launch_mode": ("one CUDA graph per pool batch; build of batch i+1 on a side stream "
+                        "overlaps compute of batch i" if graphs is not serial_graphs else
+                        "one CUDA graph per pool batch (whole step, serial)"),
+        "serial_ms_per_step": ms_serial / args.steps,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))

@@ -24,6 +24,7 @@
 namespace hf {
 
 static constexpr int kLongCap = 8192;    // block bitonic in shared memory up to this
+static constexpr int kWarpCap = 512;     // warp bitonic in shared memory up to this
 
 __global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* __restrict__ dst,
                            const long long* __restrict__ eid, const int* __restrict__ edge_type,
@@ -102,8 +103,9 @@ __global__ void k_scatter(LayerMeta m, const int* __restrict__ key_e, const int*
 
 // Block-wide sort of one long segment (unique keys).  Shared-memory bitonic
 // up to kLongCap, else rank sort through the scratch buffers.
-__device__ void block_sort(int* keys, int* vals, int n, int* sk, int* sv, int* gk, int* gv) {
-  if (n <= kLongCap) {
+__device__ void block_sort(int* keys, int* vals, int n, int* sk, int* sv, int* gk, int* gv,
+                           int cap = kLongCap) {
+  if (n <= cap) {
     int P = 1;
     while (P < n) P <<= 1;
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
@@ -163,7 +165,7 @@ __device__ __forceinline__ void csc_place(int row, int b, int e_, const int* col
 //  k_fix_rows: one warp per CSR row, n <= 32 sorted in registers (shuffle
 //              bitonic), then the sorted row is placed into the CSC.
 //  k_fix_cols: one thread per CSC column, n <= kThreadCap sorted in place.
-//  Longer segments go to the block-wide kernels (k_rows_long / k_cols_long).
+//  Longer segments go to k_sort_long (warp-level, block-level beyond kWarpCap).
 static constexpr int kThreadCap = 16;
 
 __device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
@@ -223,19 +225,28 @@ k_fix_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* 
     n = col_ptr[u + 1] - b;
   }
   if (n > 1 && n <= kThreadCap) {
-    int* k_ = csc_pos + b;
-    int* v_ = csc_row + b;
-    for (int i = 1; i < n; i++) {
-      int k = k_[i], v = v_[i];
-      int j = i - 1;
-      while (j >= 0 && k_[j] > k) {
-        k_[j + 1] = k_[j];
-        v_[j + 1] = v_[j];
-        j--;
-      }
-      k_[j + 1] = k;
-      v_[j + 1] = v;
+    // registers + odd-even transposition network (compile-time indices, no
+    // dependent global-memory round trips)
+    int kk[kThreadCap], vv[kThreadCap];
+#pragma unroll
+    for (int i = 0; i < kThreadCap; i++) {
+      kk[i] = i < n ? csc_pos[b + i] : 0x7fffffff;
+      vv[i] = i < n ? csc_row[b + i] : 0;
     }
+#pragma unroll
+    for (int ph = 0; ph < kThreadCap; ph++)
+#pragma unroll
+      for (int i = ph & 1; i + 1 < kThreadCap; i += 2)
+        if (kk[i] > kk[i + 1]) {
+          int t = kk[i]; kk[i] = kk[i + 1]; kk[i + 1] = t;
+          t = vv[i]; vv[i] = vv[i + 1]; vv[i + 1] = t;
+        }
+#pragma unroll
+    for (int i = 0; i < kThreadCap; i++)
+      if (i < n) {
+        csc_pos[b + i] = kk[i];
+        csc_row[b + i] = vv[i];
+      }
   }
   if (n > 32) long_list[atomicAdd(long_cnt, 1)] = u;
   unsigned mid = __ballot_sync(0xffffffffu, n > kThreadCap && n <= 32);
@@ -253,29 +264,77 @@ k_fix_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* 
   }
 }
 
-__global__ void k_rows_long(const int* __restrict__ row_ptr, int* eperm, int* col,
-                            const int* __restrict__ col_ptr, int* ccur, int* csc_pos,
-                            int* csc_row, const int* long_list, const int* long_cnt, int* gk,
-                            int* gv) {
-  extern __shared__ int smem[];
-  int n_long = *long_cnt;
-  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
-    int row = long_list[k];
-    int b = row_ptr[row], e_ = row_ptr[row + 1];
-    block_sort(eperm + b, col + b, e_ - b, smem, smem + kLongCap, gk + b, gv + b);
-    csc_place(row, b, e_, col, col_ptr, ccur, csc_pos, csc_row, blockDim.x, threadIdx.x);
-    __syncthreads();
+// Warp-level bitonic sort in this warp's shared-memory slice (n <= kWarpCap).
+__device__ void warp_sort_smem(int* keys, int* vals, int n, int* sk, int* sv, int lane) {
+  int P = 64;
+  while (P < n) P <<= 1;
+  for (int i = lane; i < P; i += 32) {
+    sk[i] = i < n ? keys[i] : 0x7fffffff;
+    sv[i] = i < n ? vals[i] : 0;
   }
+  __syncwarp();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        int l = i ^ j;
+        if (l > i) {
+          bool up = (i & k) == 0;
+          int a = sk[i], c = sk[l];
+          if ((a > c) == up) {
+            sk[i] = c; sk[l] = a;
+            int t = sv[i]; sv[i] = sv[l]; sv[l] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  for (int i = lane; i < n; i += 32) {
+    keys[i] = sk[i];
+    vals[i] = sv[i];
+  }
+  __syncwarp();
 }
 
-__global__ void k_cols_long(const int* __restrict__ col_ptr, int* csc_pos, int* csc_row,
-                            const int* long_list, const int* long_cnt, int* gk, int* gv) {
-  extern __shared__ int smem[];
-  int n_long = *long_cnt;
+// Segments longer than 32: one warp each when n <= kWarpCap (8 per block,
+// 4 KB of shared memory per warp), else the whole block.  ROWS also places
+// the sorted row into the CSC.
+template <bool ROWS>
+__global__ void __launch_bounds__(256)
+k_sort_long(const int* __restrict__ ptr, int* keys, int* vals, const int* __restrict__ col_ptr,
+            int* ccur, int* csc_pos, int* csc_row, const int* list, const int* cnt, int* gk,
+            int* gv) {
+  __shared__ int sk[8][kWarpCap];
+  __shared__ int sv[8][kWarpCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n_long = *cnt;
+  // warp phase
+  for (int k = blockIdx.x * 8 + w; k < n_long; k += gridDim.x * 8) {
+    const int seg = list[k];
+    const int b = ptr[seg], e = ptr[seg + 1];
+    if (e - b > kWarpCap) continue;
+    warp_sort_smem(keys + b, vals + b, e - b, sk[w], sv[w], lane);
+    if (ROWS)
+      for (int p = b + lane; p < e; p += 32) {
+        int c = vals[p];
+        int w_ = col_ptr[c] + atomicAdd(&ccur[c], 1);
+        csc_pos[w_] = p;
+        csc_row[w_] = seg;
+      }
+  }
+  // block phase (rare): whole block, shared slices reused as one 32 KB buffer
   for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
-    int u = long_list[k];
-    int b = col_ptr[u], e_ = col_ptr[u + 1];
-    block_sort(csc_pos + b, csc_row + b, e_ - b, smem, smem + kLongCap, gk + b, gv + b);
+    const int seg = list[k];
+    const int b = ptr[seg], e = ptr[seg + 1];
+    if (e - b <= kWarpCap) continue;
+    __syncthreads();
+    block_sort(keys + b, vals + b, e - b, &sk[0][0], &sv[0][0], gk + b, gv + b, 8 * kWarpCap);
+    if (ROWS)
+      for (int p = b + threadIdx.x; p < e; p += blockDim.x) {
+        int c = vals[p];
+        int w_ = col_ptr[c] + atomicAdd(&ccur[c], 1);
+        csc_pos[w_] = p;
+        csc_row[w_] = seg;
+      }
   }
 }
 
@@ -348,14 +407,6 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       !d_status || num_graph_edges < 0 || (num_graph_edges > 0 && !d_edge_type))
     return HIFUSE_ERR_INVALID_ARG;
   cudaStream_t s = st(stream);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_rows_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2 * kLongCap * (int)sizeof(int));
-    cudaFuncSetAttribute(k_cols_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2 * kLongCap * (int)sizeof(int));
-    attr_done = true;
-  }
   std::vector<LayerMeta> metas(num_layers);
   LayerMeta* mv = metas.data();
   hifuse_status rc = HIFUSE_OK;
@@ -397,14 +448,14 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     exclusive_scan(w.ccnt, o.col_ptr, U_max, w.scan, s);
     int* rows_long = w.lists;
     int* cols_long = w.lists + m.rows;
-    const int smem = 2 * kLongCap * sizeof(int);
     HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 8), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
               o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
-    HF_LAUNCH(k_rows_long, 148, 1024, smem, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
+    HF_LAUNCH(k_sort_long<true>, 148, 256, 0, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
               o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv);
     HF_LAUNCH(k_fix_cols, ceil_div(U_max, 256), 256, 0, s, o.U_dev, o.col_ptr, o.csc_pos,
               o.csc_row, cols_long, w.counters + 1);   // 8 warps x 32 columns per block
-    HF_LAUNCH(k_cols_long, 148, 1024, smem, s, o.col_ptr, o.csc_pos, o.csc_row, cols_long,
+    HF_LAUNCH(k_sort_long<false>, 148, 256, 0, s, o.col_ptr, o.csc_pos, o.csc_row,
+              (const int*)nullptr, (int*)nullptr, (int*)nullptr, (int*)nullptr, cols_long,
               w.counters + 1, w.gk, w.gv);
   }
   return last_cuda();

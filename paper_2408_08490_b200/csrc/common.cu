@@ -51,7 +51,7 @@ hifuse_status make_meta(const hifuse_layer_shape* s, LayerMeta* m) {
 
 // ------------------------------------------------------------------ scan ---
 static constexpr int kScanThreads = 256;
-static constexpr int kScanItems = 16;
+static constexpr int kScanItems = 32;
 static constexpr int kScanTile = kScanThreads * kScanItems;
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -106,26 +106,36 @@ k_scan_lookback(const int* __restrict__ in, long long n, int* __restrict__ out,
   }
   int tot;
   int ex = block_excl_scan(sum, &tot);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp-parallel look-back over a window of 32 predecessors
     volatile int* st_ = status;
-    int prefix = 0;
+    const int lane = threadIdx.x;
     if (tile == 0) {
-      st_[0] = (2 << 30) | tot;
+      if (lane == 0) st_[0] = (2 << 30) | tot;
+      if (lane == 0) s_prefix = 0;
     } else {
-      st_[tile] = (1 << 30) | tot;
+      if (lane == 0) st_[tile] = (1 << 30) | tot;
       __threadfence();
-      int t = tile - 1;
+      int prefix = 0;
+      int hi = tile - 1;                       // highest predecessor not yet summed
       while (true) {
-        int w = st_[t];
+        const int t = hi - lane;
+        int w = t >= 0 ? st_[t] : (2 << 30);
         int flag = (w >> 30) & 3;
-        if (flag == 0) continue;            // predecessor not published yet
-        prefix += w & 0x3fffffff;
-        if (flag == 2) break;
-        t--;
+        if (__any_sync(0xffffffffu, flag == 0)) continue;     // someone not published yet
+        const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 32;          // nearest inclusive prefix
+        int v = (lane <= stop && t >= 0) ? (w & 0x3fffffff) : 0;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (incl) break;
+        hi -= 32;
       }
-      st_[tile] = (2 << 30) | (prefix + tot);
+      if (lane == 0) {
+        st_[tile] = (2 << 30) | (prefix + tot);
+        s_prefix = prefix;
+      }
     }
-    s_prefix = prefix;
   }
   __syncthreads();
   ex += s_prefix;

@@ -71,6 +71,7 @@ class DeviceBatch:
             gid=mb.gather_ids(feat_off).astype(np.int32),
             labels=np.ascontiguousarray(mb.labels, np.int32))
         self.B = len(mb.labels)
+        self.slot = 0          # which CSR buffer set of the Trainer this batch uses
         self.target_type = target_type
         self.h_row0 = int(self.shapes[-1].type_dst_off[target_type])
         self.device = device
@@ -146,8 +147,8 @@ class Trainer:
     def _mat(self, key, rows, cols):
         return self._buf(key, max(rows, 1) * cols)[:max(rows, 1) * cols].view(max(rows, 1), cols)
 
-    def _csr(self, l, shape):
-        key = f"csr{l}"
+    def _csr(self, l, shape, slot=0):
+        key = f"csr{slot}.{l}"
         c = self._bufs.get(key)
         need = dict(N=shape.N, rows=shape.rows, U_max=shape.U_max, S=shape.S, R=shape.R)
         if c is None or any(need[k] > c.cap[k] for k in need):
@@ -158,11 +159,21 @@ class Trainer:
             self._bufs[key] = c
         return c
 
-    def _ws(self, nbytes):
-        return self._buf("ws", (nbytes + 3) // 4 + 64)
+    def _ws(self, nbytes, key="ws"):
+        return self._buf(key, (nbytes + 3) // 4 + 64)
+
+    def build_op(self, db: DeviceBatch, edge_type):
+        """The semantic-graph build of ``db`` (A1) as a closure; CSR buffers
+        are per batch slot and the workspace is private, so it may run on a
+        side stream while another batch computes."""
+        dev, shapes = db.dev, db.shapes
+        csrs = [self._csr(l, s, db.slot) for l, s in enumerate(shapes)]
+        wsb = self._ws(max(s.build_ws for s in shapes), key="ws_build")
+        return lambda: hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"],
+                                                edge_type, wsb, self.status)
 
     # ----------------------------------------------------------------- plan
-    def plan(self, db: DeviceBatch, feat, edge_type):
+    def plan(self, db: DeviceBatch, feat, edge_type, include_build=True):
         """The step's library calls as a list of (stage name, closure).  All
         buffers are bound here, so the closures can be run eagerly or captured
         into a CUDA graph (no allocation, no host sync inside)."""
@@ -170,10 +181,9 @@ class Trainer:
         dev = db.dev
         shapes = db.shapes
         ops = []
-        csrs = [self._csr(l, s) for l, s in enumerate(shapes)]
-        wsb = self._ws(max(s.build_ws for s in shapes))
-        ops.append(("build", lambda: hf.build_semantic_graphs(
-            shapes, csrs, dev["src"], dev["dst"], dev["eid"], edge_type, wsb, self.status)))
+        csrs = [self._csr(l, s, db.slot) for l, s in enumerate(shapes)]
+        if include_build:
+            ops.append(("build", self.build_op(db, edge_type)))
         acts = []
         X, gid = feat, dev["gid"]
         for l, sh in enumerate(shapes):
@@ -269,6 +279,31 @@ class Trainer:
                 fn()
             if update and world == 1:
                 hf.sgd(self.params, self.grads, self.lr, 1.0)
+        return g, hf.kernel_launches() - n0
+
+    def capture_pipelined(self, db: DeviceBatch, db_next: DeviceBatch, feat, edge_type, side,
+                          update=True):
+        """CUDA graph of one pipelined step: the semantic-graph build of the
+        NEXT batch runs on stream ``side`` while batch ``db`` (built by the
+        previous replay) goes through forward, backward and SGD on the
+        capturing stream -- the B200 form of the paper's CPU/GPU pipeline
+        (Fig. 6) with both sides on the GPU.
+        Returns (graph, kernels launched per replay)."""
+        ops = self.plan(db, feat, edge_type, include_build=False)
+        bop = self.build_op(db_next, edge_type)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = hf.kernel_launches()
+        with torch.cuda.graph(g):
+            main = torch.cuda.current_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                bop()
+            for _, fn in ops:
+                fn()
+            if update:
+                hf.sgd(self.params, self.grads, self.lr, 1.0)
+            main.wait_stream(side)
         return g, hf.kernel_launches() - n0
 
     def capture_stages(self, db: DeviceBatch, feat, edge_type):
