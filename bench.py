@@ -231,8 +231,9 @@ def main():
     params = make_params(cfg)
     rs = np.array([r.src for r in cfg.rels], np.int32)
     rd = np.array([r.dst for r in cfg.rels], np.int32)
+    from paper_2408_08490_b200.dp import rank_batches, allreduce_grads
     nb = -(-cfg.type_counts[cfg.target_type] // cfg.batch_size)   # batches per epoch
-    ids = [rank + s * world for s in range(args.pool)]
+    ids = rank_batches(rank, world, args.pool)
     mbs = [make_batch(cfg, g, b % nb, epoch=b // nb) for b in ids]
     pool = [DeviceBatch(mb, rs, rd, foff, cfg.target_type, dev, pin=True) for mb in mbs]
     for i, db in enumerate(pool):
@@ -244,7 +245,7 @@ def main():
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
                  prec=args.prec)
     tr.load_params(params)
-    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    allreduce = (lambda t: allreduce_grads(t, world)) if world > 1 else None
     # sizing pass: every pool batch once, eagerly (buffers reach final size)
     for db in pool:
         tr.step(db, feat_d, et_d, allreduce=allreduce, world=world, update=False)
@@ -278,7 +279,7 @@ def main():
                 non_blocking=True)
         graphs[i % len(pool)][0].replay()
         if world > 1:
-            dist.all_reduce(tr.grads)
+            allreduce_grads(tr.grads, world)
             hf.sgd(tr.params, tr.grads, tr.lr, 1.0 / world)
         if e2e:
             loss_host.copy_(tr.loss, non_blocking=True)

@@ -2,12 +2,9 @@
 mini-batch HGNN layers (arXiv 2408.08490).
 
 The product is the C-ABI library ``libhifuse.so`` (include/hifuse.h); this
-package is its thin Python binding (``hifuse``) plus the training-step driver
-(``step``).  Importing the package loads the library and raises if it is
-missing: there is no CPU fallback.
+package is its thin Python binding (``hifuse``), the training-step driver
+(``step``) and the data-parallel helpers (``dp``).  The library is loaded on
+first use and every entry point raises if it is missing: there is no CPU
+fallback.
 """
-from . import hifuse
-
-hifuse.lib()
-
-__all__ = ["hifuse"]
+__all__ = ["hifuse", "step", "dp"]

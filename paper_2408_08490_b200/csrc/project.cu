@@ -9,6 +9,7 @@
 //
 // This file holds the CUDA-core fp32 path (HIFUSE_PREC_FP32) and the
 // backward; the tcgen05 TF32 forward lives in project_tc.cu.
+#include <cstdlib>
 #include "project.cuh"
 
 namespace hf {
@@ -608,8 +609,11 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   float* Wt = carve<float>(p, (long long)(m.R + m.T) * K * D);
   if (prec == HIFUSE_PREC_TF32) {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, 128, kCH);
-    rc = project_tc_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0,
-                           tile_off, Wt, s);
+    static const bool simple = getenv("HIFUSE_TC_SIMPLE") != nullptr;
+    rc = simple ? project_tc_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y,
+                                    d_R0, tile_off, Wt, s)
+                : project_tcp_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y,
+                                     d_R0, tile_off, Wt, s);
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);

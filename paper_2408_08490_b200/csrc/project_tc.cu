@@ -17,6 +17,7 @@
 // The projection is HBM-bound at K = D = 64/128 (32 flop/B), so the design
 // goal is streaming A at full bandwidth with enough CTAs per SM (64 KB smem,
 // <=128 TMEM columns each -> 3-4 CTAs/SM) rather than peak MMA rate.
+#include <cstdlib>
 #include "project.cuh"
 #include "tc_common.cuh"
 
@@ -491,6 +492,222 @@ hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int
   else if (K == 64 && D == 128) HF_WG(64, 128);
   else HF_WG(64, 64);
 #undef HF_WG
+  return HIFUSE_OK;
+}
+
+}  // namespace hf
+
+namespace hf {
+
+// ------------------------------------------------ persistent forward GEMM ----
+// One CTA per SM, warp-specialised (the canonical Blackwell structure):
+//   warps 0-3  producers: gather the tile's A rows (and B = W_g^T) with
+//              16-byte cp.async into a kFStages-deep ring of 128-B K chunks;
+//              a thread signals a chunk `full` kLag chunks later (cp.async
+//              groups retire in order), after fence.proxy.async;
+//   warp 8     one elected thread issues tcgen05.mma (M=128, N=D, K=8) per
+//              chunk into one of TWO TMEM accumulators, commits the chunk's
+//              `empty` barrier and, after a tile's last chunk, `tfull`;
+//   warps 4-7  epilogue: tcgen05.ld of the finished accumulator (warp w reads
+//              TMEM lanes 32(w%4)...) and fp32 row stores, then `tempty`.
+// Loads of tile i+1 overlap the MMAs and the epilogue of tile i.
+template <int K, int D, int kFStages, int kLag, int kCtas>
+__global__ void __launch_bounds__(288, kCtas)
+k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restrict__ rel_y_off,
+               const int* __restrict__ y_src, const int* __restrict__ gather_ids,
+               const float* __restrict__ X, const float* __restrict__ Wt, float* __restrict__ Y,
+               float* __restrict__ R0) {
+  constexpr int BM = 128, NC = K / 32;
+  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = D * 128, STAGE = A_STAGE + B_STAGE;
+  constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 0);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[kFStages], empty[kFStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  __shared__ int s_tile[HF_MAX_R + HF_MAX_T + 1], s_yoff[HF_MAX_R + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  for (int i = tid; i <= pm.R + pm.T; i += blockDim.x) s_tile[i] = tile_off[i];
+  for (int i = tid; i <= pm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  if (tid == 0) {
+    for (int q = 0; q < kFStages; q++) {
+      mbar_init(smem_u32(&full[q]), 128);
+      mbar_init(smem_u32(&empty[q]), 1);
+    }
+    for (int q = 0; q < 2; q++) {
+      mbar_init(smem_u32(&tfull[q]), 1);
+      mbar_init(smem_u32(&tempty[q]), 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 8) tmem_alloc(smem_u32(&tmem_slot), 2 * D);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int ntiles = s_tile[pm.R + pm.T];
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ producers
+    // Coalesced gathers: producer warp w owns tile rows [32w, 32w+32); one
+    // warp instruction moves 4 rows x 128 B (8 lanes x 16 B per row), so each
+    // request touches 4 full lines instead of 32 partial ones.  Lane l serves
+    // rows 32w + 4i + l/8 (i = 0..7), 16-byte piece l%8 of every K chunk.
+    // The next tile's row addresses are fetched one tile ahead.
+    const int piece = lane & 7, rsub = lane >> 3;
+    auto rows_of = [&](int t, int* g, const float** ap, uint32_t* nb) {
+      int r0, nrows;
+      tc_resolve(pm, s_tile, s_yoff, t, BM, g, &r0, &nrows);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int row = warp * 32 + i * 4 + rsub;
+        ap[i] = X;
+        nb[i] = 0;
+        if (row < nrows) {
+          ap[i] = X + tc_a_row(pm, s_yoff, y_src, gather_ids, *g, r0 + row) * K;
+          nb[i] = 16;
+        }
+      }
+    };
+    int it = 0;
+    int g = 0;
+    const float* ap[8];
+    uint32_t nb[8];
+    if ((int)blockIdx.x < ntiles) rows_of(blockIdx.x, &g, ap, nb);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int ng = 0;
+      const float* nap[8];
+      uint32_t nnb[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) { nap[i] = X; nnb[i] = 0; }
+      if (t + (int)gridDim.x < ntiles) rows_of(t + gridDim.x, &ng, nap, nnb);
+      const float* Wg = Wt + (long long)g * D * K;
+      for (int c = 0; c < NC; c++, it++) {
+        const int s = it % kFStages;
+        if (it >= kFStages) mbar_wait(smem_u32(&empty[s]), ((it / kFStages) - 1) & 1);
+        const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const int row = warp * 32 + i * 4 + rsub;
+          cp_async16(sa + sw128_off(row, piece), ap[i] + c * 32 + piece * 4, nb[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < D / 16; i++) {          // B rows: D / 4 warps / 4 rows per instr
+          const int row = warp * (D / 4) + i * 4 + rsub;
+          cp_async16(sb + sw128_off(row, piece), Wg + (long long)row * K + c * 32 + piece * 4, 16);
+        }
+        cp_async_commit();
+        if (it >= kLag) {
+          cp_async_wait<kLag>();
+          fence_proxy_async();
+          mbar_arrive(smem_u32(&full[(it - kLag) % kFStages]));
+        }
+      }
+      g = ng;
+#pragma unroll
+      for (int i = 0; i < 8; i++) { ap[i] = nap[i]; nb[i] = nnb[i]; }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async();
+    for (int j = it - kLag < 0 ? 0 : it - kLag; j < it; j++) mbar_arrive(smem_u32(&full[j % kFStages]));
+  } else if (warp < 8) {
+    // ------------------------------------------------------------- epilogue
+    const int q = warp - 4;
+    int tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      const int acc = tc & 1;
+      int g, r0, nrows;
+      tc_resolve(pm, s_tile, s_yoff, t, BM, &g, &r0, &nrows);
+      mbar_wait(smem_u32(&tfull[acc]), (tc >> 1) & 1);
+      tc_fence_after();
+      float* out = g < pm.R ? Y + (long long)s_yoff[g] * D
+                            : R0 + (long long)pm.type_dst_off[g - pm.R] * D;
+      const int row = q * 32 + lane;
+      float* orow = out + (long long)(r0 + row) * D;
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + (uint32_t)(acc * D) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+        if (row < nrows) {
+          float4* o = reinterpret_cast<float4*>(orow + c0);
+          o[0] = make_float4(v[0], v[1], v[2], v[3]);
+          o[1] = make_float4(v[4], v[5], v[6], v[7]);
+          o[2] = make_float4(v[8], v[9], v[10], v[11]);
+          o[3] = make_float4(v[12], v[13], v[14], v[15]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(&tempty[acc]));
+    }
+  } else if (lane == 0) {
+    // ------------------------------------------------------------------ MMA
+    int it = 0, tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      const int acc = tc & 1;
+      if (tc >= 2) mbar_wait(smem_u32(&tempty[acc]), ((tc >> 1) - 1) & 1);
+      tc_fence_after();
+      for (int c = 0; c < NC; c++, it++) {
+        const int s = it % kFStages;
+        mbar_wait(smem_u32(&full[s]), (it / kFStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_tf32(tmem + (uint32_t)(acc * D), sw128_desc(sa + k * 32, 16, 1024),
+                   sw128_desc(sb + k * 32, 16, 1024), IDESC, (c | k) ? 1u : 0u);
+        mma_commit(smem_u32(&empty[s]));
+      }
+      mma_commit(smem_u32(&tfull[acc]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) tmem_dealloc(tmem, 2 * D);
+}
+
+template <int K, int D, int ST>
+static constexpr int fwdp_smem() { return ST * (128 * 128 + D * 128) + 1024; }
+
+// pipeline variants (stages, lag, CTAs per SM), selectable with HIFUSE_TCP_VARIANT
+template <int K, int D, int ST, int LAG, int CT>
+static void launch_tcp(unsigned grid, const ProjMeta& pm, int* tile_off, const hifuse_csr* csr,
+                       const int* gather_ids, const float* X, const float* Wt, float* Y, float* R0,
+                       cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_proj_fwd_tcp<K, D, ST, LAG, CT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, fwdp_smem<K, D, ST>());
+    attr = true;
+  }
+  HF_LAUNCH((k_proj_fwd_tcp<K, D, ST, LAG, CT>), grid * CT, 288, (fwdp_smem<K, D, ST>()), s, pm,
+            tile_off, csr->rel_y_off, csr->y_src, gather_ids, X, Wt, Y, R0);
+}
+
+template <int K, int D>
+static void launch_tcp_variant(int v, unsigned grid, const ProjMeta& pm, int* tile_off,
+                               const hifuse_csr* csr, const int* gather_ids, const float* X,
+                               const float* Wt, float* Y, float* R0, cudaStream_t s) {
+  switch (v) {
+    case 1: launch_tcp<K, D, 6, 5, 1>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
+    case 2: launch_tcp<K, D, 3, 2, 2>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
+    case 3: launch_tcp<K, D, 3, 1, 2>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
+    default: launch_tcp<K, D, 6, 3, 1>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
+  }
+}
+
+hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
+                                 const hifuse_csr* csr, const float* X, const int* gather_ids,
+                                 const float* W_rel, const float* W_root, float* Y, float* R0,
+                                 int* tile_off, float* Wt, cudaStream_t s) {
+  static const int variant = getenv("HIFUSE_TCP_VARIANT") ? atoi(getenv("HIFUSE_TCP_VARIANT")) : 0;
+  const int G = pm.has_root ? m.R + m.T : m.R;
+  HF_LAUNCH(k_wt_transpose, ceil_div((long long)G * K * D, 256), 256, 0, s, m.R, G, K, D, W_rel,
+            W_root, Wt);
+  long long maxt = proj_max_tiles(m, 128);
+  unsigned grid = (unsigned)(maxt < 148 ? maxt : 148);
+  if (K == 128 && D == 128) launch_tcp_variant<128, 128>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
+  else if (K == 128 && D == 64) launch_tcp_variant<128, 64>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
+  else if (K == 64 && D == 128) launch_tcp_variant<64, 128>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
+  else launch_tcp_variant<64, 64>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
   return HIFUSE_OK;
 }
 

@@ -23,39 +23,7 @@ import numpy as np
 import torch
 
 from . import hifuse as hf
-
-
-def _align4(n):
-    return (n + 3) // 4 * 4
-
-
-class ParamLayout:
-    """Offsets of every parameter inside the flat buffer (16-byte aligned)."""
-
-    def __init__(self, T, R, K0, D, H, C, L, model):
-        self.entries = []
-        off = 0
-
-        def add(name, shape):
-            nonlocal off
-            n = int(np.prod(shape))
-            self.entries.append((name, off, shape))
-            off += _align4(n)
-
-        for l in range(L):
-            K = K0 if l == 0 else D
-            add(f"{l}.W_rel", (R, K, D))
-            if model == "rgcn":
-                add(f"{l}.W_root", (T, K, D))
-            add(f"{l}.bias", (T, D))
-            if model == "rgat":
-                add(f"{l}.att", (R, 2, D))
-        add("Wc", (D, C))
-        add("bc", (C,))
-        self.size = off
-
-    def views(self, flat):
-        return {name: flat[o:o + int(np.prod(s))].view(*s) for name, o, s in self.entries}
+from .dp import ParamLayout
 
 
 class DeviceBatch:
@@ -113,6 +81,7 @@ class Trainer:
 
     def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
                  prec="tf32", slope=0.2):
+        hf.lib()   # raises if libhifuse.so is missing (no CPU fallback)
         self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
         self.rel_src = np.asarray(rel_src, np.int32)
         self.rel_dst = np.asarray(rel_dst, np.int32)
