@@ -23,36 +23,48 @@ __device__ __forceinline__ float block_reduce(float v, float* sm, bool is_max) {
 }
 
 // Small SIMT GEMM: C[M,N] = op(A)[M,K] op(B)[K,N]; TA: A stored [K,M]; TB: B
-// stored [N,K].  64x64 tiles, 256 threads, 4x4 outputs per thread.
+// stored [N,K].  64x64 tiles, 256 threads, 4x4 outputs per thread, BK = 32,
+// the next K tile prefetched into registers while the current one is used.
+// gridDim.z > 1: split-K, slice z writes C + z*M*ldc (summed in fixed order).
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256)
 k_gemm_small(int M, int N, int K, const float* __restrict__ A, int lda,
              const float* __restrict__ B, int ldb, float* __restrict__ C, int ldc,
              long long a_row0, long long c_row0) {
-  __shared__ float As[16][64 + 1];
-  __shared__ float Bs[16][64 + 1];
+  constexpr int BK = 32;
+  __shared__ float As[BK][64 + 1];
+  __shared__ float Bs[BK][64 + 1];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  const int kper = (K + gridDim.z - 1) / gridDim.z;
+  const int kper = ((K + gridDim.z - 1) / gridDim.z + BK - 1) / BK * BK;
   const int kb0 = blockIdx.z * kper, kb1 = min(K, kb0 + kper);
   C += (long long)blockIdx.z * M * ldc;
   float acc[4][4] = {};
-  for (int k0 = kb0; k0 < kb1; k0 += 16) {
-    for (int i = tid; i < 16 * 64; i += 256) {
-      int kk = TA ? i / 64 : i % 16, mm = TA ? i % 64 : i / 16;
+  float ra[8], rb[8];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int i = tid + 256 * q;
+      int kk = TA ? i / 64 : i % BK, mm = TA ? i % 64 : i / BK;
       int m = m0 + mm, k = k0 + kk;
-      float v = 0.f;
-      if (m < M && k < kb1) v = TA ? A[(long long)k * lda + a_row0 + m] : A[(a_row0 + m) * lda + k];
-      As[kk][mm] = v;
-      int kb = TB ? i % 16 : i / 64, nb = TB ? i / 16 : i % 64;
+      ra[q] = (m < M && k < kb1) ? (TA ? A[(long long)k * lda + a_row0 + m] : A[(a_row0 + m) * lda + k]) : 0.f;
+      int kb = TB ? i % BK : i / 64, nb = TB ? i / BK : i % 64;
       int n = n0 + nb, k2 = k0 + kb;
-      float w = 0.f;
-      if (n < N && k2 < kb1) w = TB ? B[(long long)n * ldb + k2] : B[(long long)k2 * ldb + n];
-      Bs[kb][nb] = w;
+      rb[q] = (n < N && k2 < kb1) ? (TB ? B[(long long)n * ldb + k2] : B[(long long)k2 * ldb + n]) : 0.f;
+    }
+  };
+  if (kb0 < kb1) fetch(kb0);
+  for (int k0 = kb0; k0 < kb1; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int i = tid + 256 * q;
+      As[TA ? i / 64 : i % BK][TA ? i % 64 : i / BK] = ra[q];
+      Bs[TB ? i % BK : i / 64][TB ? i / BK : i % 64] = rb[q];
     }
     __syncthreads();
+    if (k0 + BK < kb1) fetch(k0 + BK);
 #pragma unroll
-    for (int kk = 0; kk < 16; kk++) {
+    for (int kk = 0; kk < BK; kk++) {
       float a[4], b[4];
 #pragma unroll
       for (int i = 0; i < 4; i++) a[i] = As[kk][ty + 16 * i];
@@ -163,7 +175,9 @@ extern "C" {
 
 size_t hifuse_xent_ws_bytes(int B, int D, int C) {
   (void)D;
-  long long np = (long long)kSplit * D * C > 4ll * B * D ? (long long)kSplit * D * C : 4ll * B * D;
+  long long np = (long long)kSplit * D * C;
+  if (np < 4ll * B * D) np = 4ll * B * D;
+  if (np < 4ll * B * C) np = 4ll * B * C;
   return carve_bytes((long long)B * C, 4) + carve_bytes(B, 4) + carve_bytes(np, 4);
 }
 
@@ -180,13 +194,16 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   char* p = (char*)d_ws;
   float* dlog = carve<float>(p, (long long)B * C);
   float* row_loss = carve<float>(p, B);
-  float* part = carve<float>(p, (long long)kSplit * D * C > 4ll * B * D ? (long long)kSplit * D * C
-                                                                        : 4ll * B * D);
+  long long np = (long long)kSplit * D * C;
+  if (np < 4ll * B * D) np = 4ll * B * D;
+  if (np < 4ll * B * C) np = 4ll * B * C;
+  float* part = carve<float>(p, np);
   cudaMemsetAsync(d_dH, 0, sizeof(float) * h_rows * D, s);
-  // logits = Hs Wc
-  dim3 g1(ceil_div(C, 64), ceil_div(B, 64));
-  HF_LAUNCH((k_gemm_small<false, false>), g1, 256, 0, s, B, C, D, d_H, D, d_Wc, C, dlog, C,
+  // logits = Hs Wc  (split-K 4, fixed-order sum)
+  dim3 g1(ceil_div(C, 64), ceil_div(B, 64), 4);
+  HF_LAUNCH((k_gemm_small<false, false>), g1, 256, 0, s, B, C, D, d_H, D, d_Wc, C, part, C,
             (long long)h_row0, 0ll);
+  HF_LAUNCH(k_sum_splits, ceil_div((long long)B * C, 256), 256, 0, s, B * C, 4, part, dlog);
   HF_LAUNCH(k_xent_softmax, ceil_div(B, 8), 256, 0, s, B, C, d_bc, d_labels, dlog, row_loss);
   HF_LAUNCH(k_xent_loss, 1, 256, 0, s, B, row_loss, d_loss);
   // dHs = dlog Wc^T   (Wc is [D, C]: op(B) = Wc^T stored [N = D, K = C])

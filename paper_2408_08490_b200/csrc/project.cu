@@ -645,7 +645,7 @@ size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D
   LayerMeta m;
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
   int H = heads > 0 ? heads : 1;
-  long long chunks = proj_max_tiles(m, kCH);
+  long long chunks = proj_max_tiles(m, kCH < 128 ? kCH : 128);
   size_t b = 2 * carve_bytes(m.R + m.T + 1, 4);
   b += carve_bytes(chunks * K * D, 4);                       // wgrad partials
   b += carve_bytes((long long)m.R * K * H, 4);               // v
@@ -683,7 +683,7 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   ProjMeta pm;
   make_proj_meta(m, d_W_root != nullptr, &pm);
   int H = heads > 0 ? heads : 1;
-  long long chunks = proj_max_tiles(m, kCH);
+  long long chunks = proj_max_tiles(m, kCH < 128 ? kCH : 128);
   char* p = (char*)d_ws;
   int* tile_off = carve<int>(p, m.R + m.T + 1);
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
@@ -700,9 +700,10 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
               d_att, d_ds_src, d_dY);
   }
   if (prec == HIFUSE_PREC_TF32) {
-    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCHT);
-    wgrad_tc_launch(m, pm, K, D, chunk_off, csr->rel_y_off, csr->y_src, d_gather_ids, d_X, d_dY,
-                    d_G, partial, (unsigned)proj_max_tiles(m, kCHT), s);
+    const int CH = wgrad_chunk_rows(m);
+    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, CH);
+    wgrad_tc_launch(m, pm, K, D, CH, chunk_off, csr->rel_y_off, csr->y_src, d_gather_ids, d_X,
+                    d_dY, d_G, partial, (unsigned)proj_max_tiles(m, CH), s);
   } else {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
     unsigned grid = (unsigned)chunks;

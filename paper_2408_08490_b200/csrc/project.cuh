@@ -50,9 +50,16 @@ hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot
                               const float* dY, const float* G, const float* W_rel,
                               const float* W_root, float* dX, cudaStream_t s);
 // tcgen05 TF32 wgrad partials: P[c] = sum_{rows of chunk c} X_row^T dYt_row
-// (chunks of kCHT rows per group from chunk_off).
+// (chunks of CH rows per group from chunk_off; wgrad_chunk_rows() picks CH so
+// that small layers still spread over every SM).
 static constexpr int kCHT = 1024;
-hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
+inline int wgrad_chunk_rows(const LayerMeta& m) {
+  long long rows = (long long)(m.N < m.S ? m.N : m.S) + m.dst_rows;
+  long long ch = rows / (2 * 148);
+  ch = (ch + 31) / 32 * 32;
+  return (int)(ch < 128 ? 128 : (ch > kCHT ? kCHT : ch));
+}
+hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D, int CH,
                               const int* chunk_off, const int* rel_y_off, const int* y_src,
                               const int* gather_ids, const float* X, const float* dY,
                               const float* G, float* partial, unsigned grid, cudaStream_t s);

@@ -313,7 +313,7 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
 }
 
 // ----------------------------------------------------------------- wgrad ----
-// Chunk = up to kCHT rows of one group; partial[chunk] = A^T B over the rows,
+// Chunk = up to CH rows of one group (CH adapts to the layer size, 128..1024); partial[chunk] = A^T B over the rows,
 // A = X rows (features = M, padded to 128 when K = 64), B = dYt / G rows
 // (N = D).  The reduction runs over rows, so both operands are MN-major
 // (SWIZZLE_128B_BASE32B): a stage holds 32 rows; per 32-feature block the 32
@@ -324,7 +324,7 @@ static constexpr int kWgStages = 3;
 
 template <int K, int D>
 __global__ void __launch_bounds__(128)
-k_wgrad_tc(ProjMeta pm, const int* __restrict__ chunk_off, const int* __restrict__ rel_y_off,
+k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __restrict__ rel_y_off,
            const int* __restrict__ y_src, const int* __restrict__ gather_ids,
            const float* __restrict__ X, const float* __restrict__ dY, const float* __restrict__ G,
            float* __restrict__ partial) {
@@ -336,7 +336,7 @@ k_wgrad_tc(ProjMeta pm, const int* __restrict__ chunk_off, const int* __restrict
   __shared__ __align__(8) uint64_t bars[kWgStages];
   __shared__ uint32_t tmem_slot;
   int g, r0, nrows;
-  if (!tc_resolve(pm, chunk_off, rel_y_off, blockIdx.x, kCHT, &g, &r0, &nrows)) return;
+  if (!tc_resolve(pm, chunk_off, rel_y_off, blockIdx.x, CH, &g, &r0, &nrows)) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   if (tid == 0) {
@@ -471,7 +471,7 @@ hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot
   return HIFUSE_OK;
 }
 
-hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
+hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D, int CH,
                               const int* chunk_off, const int* rel_y_off, const int* y_src,
                               const int* gather_ids, const float* X, const float* dY,
                               const float* G, float* partial, unsigned grid, cudaStream_t s) {
@@ -485,7 +485,7 @@ hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int
     attr = true;
   }
 #define HF_WG(KK, DD)                                                                          \
-  HF_LAUNCH((k_wgrad_tc<KK, DD>), grid, 128, (wgrad_smem<KK, DD>()), s, pm, chunk_off,         \
+  HF_LAUNCH((k_wgrad_tc<KK, DD>), grid, 128, (wgrad_smem<KK, DD>()), s, pm, CH, chunk_off,     \
             rel_y_off, y_src, gather_ids, X, dY, G, partial)
   if (K == 128 && D == 128) HF_WG(128, 128);
   else if (K == 128 && D == 64) HF_WG(128, 64);
@@ -698,7 +698,7 @@ hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, 
                                  const hifuse_csr* csr, const float* X, const int* gather_ids,
                                  const float* W_rel, const float* W_root, float* Y, float* R0,
                                  int* tile_off, float* Wt, cudaStream_t s) {
-  static const int variant = getenv("HIFUSE_TCP_VARIANT") ? atoi(getenv("HIFUSE_TCP_VARIANT")) : 0;
+  static const int variant = getenv("HIFUSE_TCP_VARIANT") ? atoi(getenv("HIFUSE_TCP_VARIANT")) : 2;
   const int G = pm.has_root ? m.R + m.T : m.R;
   HF_LAUNCH(k_wt_transpose, ceil_div((long long)G * K * D, 256), 256, 0, s, m.R, G, K, D, W_rel,
             W_root, Wt);
