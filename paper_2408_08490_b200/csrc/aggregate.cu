@@ -277,27 +277,54 @@ k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __res
   const int U = *U_dev;
   const int u = (blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * (32 / kLPC) + lane / kLPC;
   const int j = lane % kLPC;
-  if (u >= U) return;
-  const int b = col_ptr[u], e = col_ptr[u + 1];
-  if (e - b > kLongCol) {
-    if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
-    return;
+  if ((blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * (32 / kLPC) >= U) return;  // whole warp
+  int b = 0, e = 0;
+  bool skip = u >= U;
+  if (!skip) {
+    b = col_ptr[u];
+    e = col_ptr[u + 1];
+    if (e - b > kLongCol) {
+      if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
+      e = b;                                  // handled by k_agg_bwd_long
+      skip = true;
+    }
   }
-  const int shift = bm.shift[upper_bound_i(s_yoff, bm.R + 1, u) - 1];
+  const int shift = u < U ? bm.shift[upper_bound_i(s_yoff, bm.R + 1, u) - 1] : 0;
   float4 acc[V];
 #pragma unroll
   for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int p = b; p < e; p++) {
-    const int row = __ldg(csc_row + p);
-    float w = 1.f;
-    if (MEAN) w = 1.f / (float)(__ldg(row_ptr + row + 1) - __ldg(row_ptr + row));
-    const float4* g = G + (long long)(row + shift) * LPR + j;
-    float4 x[V];
+  // kLPC entries per round: lane j of the group fetches entry p0 + j's row
+  // and weight (one parallel round trip), then the group gathers them all.
+  // The round count is warp-uniform (shuffles need the full warp).
+  const int gbase = lane & ~(kLPC - 1);
+  const int rounds = __reduce_max_sync(0xffffffffu, (e - b + kLPC - 1) / kLPC);
+  for (int rd = 0; rd < rounds; rd++) {
+    const int p0 = b + rd * kLPC;
+    int my_row = 0;
+    float my_w = 0.f;
+    if (p0 + j < e) {
+      my_row = __ldg(csc_row + p0 + j);
+      my_w = MEAN ? 1.f / (float)(__ldg(row_ptr + my_row + 1) - __ldg(row_ptr + my_row)) : 1.f;
+    }
+    const int cnt = max(0, min(kLPC, e - p0));
+    float4 x[kLPC][V];
+    float wq[kLPC];
 #pragma unroll
-    for (int v = 0; v < V; v++) x[v] = ldg4(g + v * kLPC);
+    for (int q = 0; q < kLPC; q++) {
+      const int rq = __shfl_sync(0xffffffffu, my_row, gbase + q);
+      wq[q] = __shfl_sync(0xffffffffu, my_w, gbase + q);
+      const float4* g = G + (long long)(rq + shift) * LPR + j;
 #pragma unroll
-    for (int v = 0; v < V; v++) acc[v] = MEAN ? f4fma(w, x[v], acc[v]) : f4add(acc[v], x[v]);
+      for (int v = 0; v < V; v++)
+        x[q][v] = q < cnt ? ldg4(g + v * kLPC) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < kLPC; q++)
+#pragma unroll
+      for (int v = 0; v < V; v++)
+        acc[v] = MEAN ? f4fma(wq[q], x[q][v], acc[v]) : f4add(acc[v], x[q][v]);
   }
+  if (skip) return;
   float4* o = dY + (long long)u * LPR + j;
 #pragma unroll
   for (int v = 0; v < V; v++) o[v * kLPC] = acc[v];

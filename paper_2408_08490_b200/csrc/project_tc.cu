@@ -350,6 +350,11 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
                          base + q * STAGE + (K / 32) * BLK + i * 16),
                      "r"(0));
   }
+  // X row of every row of the chunk, resolved once up front (the dependent
+  // y_src -> gather_ids loads would otherwise stall every stage)
+  __shared__ int s_xrow[kCHT];
+  for (int i = tid; i < nrows; i += 128)
+    s_xrow[i] = (int)tc_a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + i);
   if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), D);
   tc_fence_before();
   __syncthreads();
@@ -369,7 +374,7 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
       const float* src = X;
       uint32_t nb = 0;
       if (rr < nrows) {
-        src = X + tc_a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + rr) * K + f;
+        src = X + (long long)s_xrow[rr] * K + f;
         nb = 16;
       }
       cp_async16(sa + (f >> 5) * BLK + (row >> 2) * 512 + sw128b32_off(row, (f & 31) * 4), src, nb);
@@ -524,6 +529,7 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
   __shared__ __align__(8) uint64_t full[kFStages], empty[kFStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
   __shared__ int s_tile[HF_MAX_R + HF_MAX_T + 1], s_yoff[HF_MAX_R + 1];
+  __shared__ __align__(16) float stage_ep[4 * 32 * 20];     // epilogue staging
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   for (int i = tid; i <= pm.R + pm.T; i += blockDim.x) s_tile[i] = tile_off[i];
@@ -621,19 +627,27 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
       tc_fence_after();
       float* out = g < pm.R ? Y + (long long)s_yoff[g] * D
                             : R0 + (long long)pm.type_dst_off[g - pm.R] * D;
-      const int row = q * 32 + lane;
-      float* orow = out + (long long)(r0 + row) * D;
-#pragma unroll
+      // TMEM lane = row: stage each 16-column slice of the warp's 32 rows in
+      // shared memory (80-byte row pitch: conflict-free) and write it back as
+      // 8 rows x 64 contiguous bytes per instruction (full sectors).
+      float* st = stage_ep + q * (32 * 20);
+#pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 16) {
         float v[16];
         tmem_ld16(tmem + (uint32_t)(acc * D) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-        if (row < nrows) {
-          float4* o = reinterpret_cast<float4*>(orow + c0);
-          o[0] = make_float4(v[0], v[1], v[2], v[3]);
-          o[1] = make_float4(v[4], v[5], v[6], v[7]);
-          o[2] = make_float4(v[8], v[9], v[10], v[11]);
-          o[3] = make_float4(v[12], v[13], v[14], v[15]);
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          *reinterpret_cast<float4*>(st + lane * 20 + 4 * j) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int rr = i * 8 + (lane >> 2), ch = lane & 3;
+          const int row = q * 32 + rr;
+          const float4 x = *reinterpret_cast<const float4*>(st + rr * 20 + 4 * ch);
+          if (row < nrows) *reinterpret_cast<float4*>(out + (long long)(r0 + row) * D + c0 + 4 * ch) = x;
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(smem_u32(&tempty[acc]));
