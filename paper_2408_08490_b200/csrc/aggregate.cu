@@ -260,10 +260,10 @@ k_agg_bwd_long(BwdMeta bm, const int* __restrict__ rel_y_off, const int* __restr
 // of output.  Instead kLPC lanes serve one column: a warp covers 32/kLPC
 // columns, each lane gathers D/4/kLPC float4 per entry (independent loads in
 // flight), and the kLPC lanes of a group read 16*kLPC contiguous bytes.
-static constexpr int kLPC = 4;
+static constexpr int kLPC = 8;
 
 template <int D, bool MEAN>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
 k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __restrict__ rel_y_off,
           const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
           const int* __restrict__ row_ptr, const float4* __restrict__ G, float4* __restrict__ dY,
@@ -307,22 +307,26 @@ k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __res
       my_w = MEAN ? 1.f / (float)(__ldg(row_ptr + my_row + 1) - __ldg(row_ptr + my_row)) : 1.f;
     }
     const int cnt = max(0, min(kLPC, e - p0));
-    float4 x[kLPC][V];
-    float wq[kLPC];
 #pragma unroll
-    for (int q = 0; q < kLPC; q++) {
-      const int rq = __shfl_sync(0xffffffffu, my_row, gbase + q);
-      wq[q] = __shfl_sync(0xffffffffu, my_w, gbase + q);
-      const float4* g = G + (long long)(rq + shift) * LPR + j;
+    for (int q0 = 0; q0 < kLPC; q0 += 2) {
+      float4 x[2][V];
+      float wq[2];
 #pragma unroll
-      for (int v = 0; v < V; v++)
-        x[q][v] = q < cnt ? ldg4(g + v * kLPC) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < 2; q++) {
+        const int rq = __shfl_sync(0xffffffffu, my_row, gbase + q0 + q);
+        wq[q] = __shfl_sync(0xffffffffu, my_w, gbase + q0 + q);
+        const float4* g = G + (long long)(rq + shift) * LPR + j;
+#pragma unroll
+        for (int v = 0; v < V; v++)
+          x[q][v] = q0 + q < cnt ? ldg4(g + v * kLPC) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; q++)
+#pragma unroll
+        for (int v = 0; v < V; v++)
+          acc[v] = MEAN ? f4fma(wq[q], x[q][v], acc[v]) : f4add(acc[v], x[q][v]);
+      if (__all_sync(0xffffffffu, q0 + 2 >= cnt)) break;
     }
-#pragma unroll
-    for (int q = 0; q < kLPC; q++)
-#pragma unroll
-      for (int v = 0; v < V; v++)
-        acc[v] = MEAN ? f4fma(wq[q], x[q][v], acc[v]) : f4add(acc[v], x[q][v]);
   }
   if (skip) return;
   float4* o = dY + (long long)u * LPR + j;

@@ -17,14 +17,12 @@
 //                column order, so the result is bit-exact and deterministic),
 //                then CSC placement
 //   k_fix_cols   thread per Y row: sort CSC entries by CSR position
-//   k_*_long     the same two sorts for longer segments (block-wide)
+//   k_sort_long  the same two sorts for segments longer than 32 (rank sort)
 #include <vector>
 #include "common.cuh"
 
 namespace hf {
 
-static constexpr int kLongCap = 8192;    // block bitonic in shared memory up to this
-static constexpr int kWarpCap = 512;     // warp bitonic in shared memory up to this
 
 __global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* __restrict__ dst,
                            const long long* __restrict__ eid, const int* __restrict__ edge_type,
@@ -101,71 +99,11 @@ __global__ void k_scatter(LayerMeta m, const int* __restrict__ key_e, const int*
   atomicAdd(&ccnt[c], 1);
 }
 
-// Block-wide sort of one long segment (unique keys).  Shared-memory bitonic
-// up to kLongCap, else rank sort through the scratch buffers.
-__device__ void block_sort(int* keys, int* vals, int n, int* sk, int* sv, int* gk, int* gv,
-                           int cap = kLongCap) {
-  if (n <= cap) {
-    int P = 1;
-    while (P < n) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-      sk[i] = i < n ? keys[i] : 0x7fffffff;
-      sv[i] = i < n ? vals[i] : 0;
-    }
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1)
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < P; i += blockDim.x) {
-          int l = i ^ j;
-          if (l > i) {
-            bool up = (i & k) == 0;
-            int a = sk[i], b = sk[l];
-            if ((a > b) == up) {
-              sk[i] = b; sk[l] = a;
-              int t = sv[i]; sv[i] = sv[l]; sv[l] = t;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      keys[i] = sk[i];
-      vals[i] = sv[i];
-    }
-    __syncthreads();
-    return;
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int k = keys[i], rank = 0;
-    for (int j = 0; j < n; j++) rank += keys[j] < k;
-    gk[rank] = k;
-    gv[rank] = vals[i];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    keys[i] = gk[i];
-    vals[i] = gv[i];
-  }
-  __syncthreads();
-}
-
-// Scatter one sorted CSR row into the CSC (atomic slot, fixed up by k_cols).
-__device__ __forceinline__ void csc_place(int row, int b, int e_, const int* col,
-                                          const int* col_ptr, int* ccur, int* csc_pos,
-                                          int* csc_row, int step, int first) {
-  for (int p = b + first; p < e_; p += step) {
-    int c = col[p];
-    int w = col_ptr[c] + atomicAdd(&ccur[c], 1);
-    csc_pos[w] = p;
-    csc_row[w] = row;
-  }
-}
-
 // Segment fix-up sorts (unique keys, carried values).
 //  k_fix_rows: one warp per CSR row, n <= 32 sorted in registers (shuffle
 //              bitonic), then the sorted row is placed into the CSC.
 //  k_fix_cols: one thread per CSC column, n <= kThreadCap sorted in place.
-//  Longer segments go to k_sort_long (warp-level, block-level beyond kWarpCap).
+//  Longer segments go to k_sort_long (shared-memory rank sort, warp or block).
 static constexpr int kThreadCap = 16;
 
 __device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
@@ -264,77 +202,89 @@ k_fix_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* 
   }
 }
 
-// Warp-level bitonic sort in this warp's shared-memory slice (n <= kWarpCap).
-__device__ void warp_sort_smem(int* keys, int* vals, int n, int* sk, int* sv, int lane) {
-  int P = 64;
-  while (P < n) P <<= 1;
-  for (int i = lane; i < P; i += 32) {
-    sk[i] = i < n ? keys[i] : 0x7fffffff;
-    sv[i] = i < n ? vals[i] : 0;
+// Segments longer than 32 (hub columns, long rows): rank sort in shared
+// memory -- every key's final position is the number of smaller keys (keys
+// are unique), computed with broadcast reads, no synchronisation chain.
+// n <= kWarpRank: one warp per segment (8 per block); n <= kBlockRank: the
+// whole block; longer (never seen in the workloads): rank sort in global.
+static constexpr int kWarpRank = 256;
+static constexpr int kBlockRank = 4096;
+
+template <bool ROWS>
+__device__ __forceinline__ void place_row_in_csc(int seg, int b, int e, int first, int step,
+                                                 const int* vals, const int* col_ptr, int* ccur,
+                                                 int* csc_pos, int* csc_row) {
+  if (!ROWS) return;
+  for (int p = b + first; p < e; p += step) {
+    const int c = vals[p];
+    const int w = col_ptr[c] + atomicAdd(&ccur[c], 1);
+    csc_pos[w] = p;
+    csc_row[w] = seg;
   }
-  __syncwarp();
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < P; i += 32) {
-        int l = i ^ j;
-        if (l > i) {
-          bool up = (i & k) == 0;
-          int a = sk[i], c = sk[l];
-          if ((a > c) == up) {
-            sk[i] = c; sk[l] = a;
-            int t = sv[i]; sv[i] = sv[l]; sv[l] = t;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  for (int i = lane; i < n; i += 32) {
-    keys[i] = sk[i];
-    vals[i] = sv[i];
-  }
-  __syncwarp();
 }
 
-// Segments longer than 32: one warp each when n <= kWarpCap (8 per block,
-// 4 KB of shared memory per warp), else the whole block.  ROWS also places
-// the sorted row into the CSC.
 template <bool ROWS>
 __global__ void __launch_bounds__(256)
 k_sort_long(const int* __restrict__ ptr, int* keys, int* vals, const int* __restrict__ col_ptr,
             int* ccur, int* csc_pos, int* csc_row, const int* list, const int* cnt, int* gk,
             int* gv) {
-  __shared__ int sk[8][kWarpCap];
-  __shared__ int sv[8][kWarpCap];
+  __shared__ int sk[kBlockRank], sv[kBlockRank];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int n_long = *cnt;
-  // warp phase
+  // ---- warp phase
+  int* wk = sk + w * kWarpRank;
+  int* wv = sv + w * kWarpRank;
   for (int k = blockIdx.x * 8 + w; k < n_long; k += gridDim.x * 8) {
     const int seg = list[k];
-    const int b = ptr[seg], e = ptr[seg + 1];
-    if (e - b > kWarpCap) continue;
-    warp_sort_smem(keys + b, vals + b, e - b, sk[w], sv[w], lane);
-    if (ROWS)
-      for (int p = b + lane; p < e; p += 32) {
-        int c = vals[p];
-        int w_ = col_ptr[c] + atomicAdd(&ccur[c], 1);
-        csc_pos[w_] = p;
-        csc_row[w_] = seg;
-      }
+    const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
+    if (n > kWarpRank) continue;
+    for (int i = lane; i < n; i += 32) {
+      wk[i] = keys[b + i];
+      wv[i] = vals[b + i];
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const int kk = wk[i];
+      int r = 0;
+      for (int j = 0; j < n; j++) r += wk[j] < kk;
+      keys[b + r] = kk;
+      vals[b + r] = wv[i];
+    }
+    __syncwarp();
+    place_row_in_csc<ROWS>(seg, b, e, lane, 32, vals, col_ptr, ccur, csc_pos, csc_row);
   }
-  // block phase (rare): whole block, shared slices reused as one 32 KB buffer
+  __syncthreads();
+  // ---- block phase
   for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
     const int seg = list[k];
-    const int b = ptr[seg], e = ptr[seg + 1];
-    if (e - b <= kWarpCap) continue;
-    __syncthreads();
-    block_sort(keys + b, vals + b, e - b, &sk[0][0], &sv[0][0], gk + b, gv + b, 8 * kWarpCap);
-    if (ROWS)
-      for (int p = b + threadIdx.x; p < e; p += blockDim.x) {
-        int c = vals[p];
-        int w_ = col_ptr[c] + atomicAdd(&ccur[c], 1);
-        csc_pos[w_] = p;
-        csc_row[w_] = seg;
+    const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
+    if (n <= kWarpRank) continue;
+    const int* srck = sk;
+    if (n <= kBlockRank) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sk[i] = keys[b + i];
+        sv[i] = vals[b + i];
       }
+    } else {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        gk[b + i] = keys[b + i];
+        gv[b + i] = vals[b + i];
+      }
+      srck = gk + b;
+    }
+    __syncthreads();
+    const int* srcv = n <= kBlockRank ? sv : gv + b;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int kk = srck[i];
+      int r = 0;
+      for (int j = 0; j < n; j++) r += srck[j] < kk;
+      keys[b + r] = kk;
+      vals[b + r] = srcv[i];
+    }
+    __syncthreads();
+    place_row_in_csc<ROWS>(seg, b, e, threadIdx.x, blockDim.x, vals, col_ptr, ccur, csc_pos,
+                           csc_row);
+    __syncthreads();
   }
 }
 

@@ -263,7 +263,12 @@ class Trainer:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = hf.kernel_launches()
-        with torch.cuda.graph(g):
+        # the compute chain is captured on a high-priority stream, the build on
+        # the (default-priority) side stream: the block scheduler favours the
+        # critical path and the latency-bound build fills the gaps
+        if not hasattr(self, "_hi"):
+            self._hi = torch.cuda.Stream(priority=-1)
+        with torch.cuda.graph(g, stream=self._hi):
             main = torch.cuda.current_stream()
             side.wait_stream(main)
             with torch.cuda.stream(side):
