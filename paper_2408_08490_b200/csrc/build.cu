@@ -18,6 +18,7 @@
 //                then CSC placement
 //   k_fix_cols   thread per Y row: sort CSC entries by CSR position
 //   k_sort_long  the same two sorts for segments longer than 32 (rank sort)
+#include <cstdlib>
 #include <vector>
 #include "common.cuh"
 
@@ -223,63 +224,114 @@ __device__ __forceinline__ void place_row_in_csc(int seg, int b, int e, int firs
   }
 }
 
+// Rank scatter: thread `t` of `nt` owns keys t, t+nt, ... (at most E, held in
+// registers); every key of the segment is read once per thread with 16-byte
+// shared loads (broadcast) and compared against all owned keys, so one load
+// serves 4*E comparisons.  The segment buffer is padded to a multiple of 4
+// with INT_MAX by the caller.
+template <int E>
+__device__ __forceinline__ void rank_scatter(const int* sk, const int* sv, int n, int t, int nt,
+                                             int* keys, int* vals) {
+  int kk[E], r[E];
+#pragma unroll
+  for (int q = 0; q < E; q++) {
+    const int i = t + q * nt;
+    kk[q] = i < n ? sk[i] : 0x7fffffff;
+    r[q] = 0;
+  }
+  const int n4 = (n + 3) >> 2;
+  for (int j = 0; j < n4; j++) {
+    const int4 v = reinterpret_cast<const int4*>(sk)[j];
+#pragma unroll
+    for (int q = 0; q < E; q++)
+      r[q] += (v.x < kk[q]) + (v.y < kk[q]) + (v.z < kk[q]) + (v.w < kk[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < E; q++) {
+    const int i = t + q * nt;
+    if (i < n) {
+      keys[r[q]] = kk[q];
+      vals[r[q]] = sv[i];
+    }
+  }
+}
+
+static constexpr int kSortThreads = 512;
+
 template <bool ROWS>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kSortThreads)
 k_sort_long(const int* __restrict__ ptr, int* keys, int* vals, const int* __restrict__ col_ptr,
             int* ccur, int* csc_pos, int* csc_row, const int* list, const int* cnt, int* gk,
-            int* gv) {
-  __shared__ int sk[kBlockRank], sv[kBlockRank];
+            int* gv, int dbg) {
+  constexpr int NW = kSortThreads / 32;
+  static_assert(NW * kWarpRank <= kBlockRank, "warp slices must fit the block buffer");
+  __shared__ __align__(16) int sk[kBlockRank];
+  __shared__ __align__(16) int sv[kBlockRank];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int n_long = *cnt;
-  // ---- warp phase
+  // ---- warp phase (32 < n <= kWarpRank)
   int* wk = sk + w * kWarpRank;
   int* wv = sv + w * kWarpRank;
-  for (int k = blockIdx.x * 8 + w; k < n_long; k += gridDim.x * 8) {
+  for (int k = blockIdx.x * NW + w; k < n_long; k += gridDim.x * NW) {
     const int seg = list[k];
     const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
-    if (n > kWarpRank) continue;
-    for (int i = lane; i < n; i += 32) {
-      wk[i] = keys[b + i];
-      wv[i] = vals[b + i];
+    if (n > kWarpRank || (dbg & 1)) continue;
+    for (int i = lane; i < ((n + 3) & ~3); i += 32) {
+      wk[i] = i < n ? keys[b + i] : 0x7fffffff;
+      wv[i] = i < n ? vals[b + i] : 0;
     }
     __syncwarp();
-    for (int i = lane; i < n; i += 32) {
-      const int kk = wk[i];
-      int r = 0;
-      for (int j = 0; j < n; j++) r += wk[j] < kk;
-      keys[b + r] = kk;
-      vals[b + r] = wv[i];
-    }
+    rank_scatter<kWarpRank / 32>(wk, wv, n, lane, 32, keys + b, vals + b);
     __syncwarp();
     place_row_in_csc<ROWS>(seg, b, e, lane, 32, vals, col_ptr, ccur, csc_pos, csc_row);
   }
   __syncthreads();
-  // ---- block phase
+  // ---- block phase (n > kWarpRank): one segment per block, shared memory
+  // rank sort up to kBlockRank, global-memory rank sort beyond
   for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
     const int seg = list[k];
     const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
-    if (n <= kWarpRank) continue;
-    const int* srck = sk;
+    if (n <= kWarpRank || (dbg & 2)) continue;
     if (n <= kBlockRank) {
+      // bitonic sort in shared memory, padded to a power of two
+      int P = 1;
+      while (P < n) P <<= 1;
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        sk[i] = i < n ? keys[b + i] : 0x7fffffff;
+        sv[i] = i < n ? vals[b + i] : 0;
+      }
+      __syncthreads();
+      for (int kk = 2; kk <= P; kk <<= 1)
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+            // i-th compare-exchange pair of this stage
+            const int lo = ((i / jj) * 2 * jj) + (i % jj), hi = lo + jj;
+            const bool up = (lo & kk) == 0;
+            const int a = sk[lo], c = sk[hi];
+            if ((a > c) == up) {
+              sk[lo] = c; sk[hi] = a;
+              const int t = sv[lo]; sv[lo] = sv[hi]; sv[hi] = t;
+            }
+          }
+          __syncthreads();
+        }
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        sk[i] = keys[b + i];
-        sv[i] = vals[b + i];
+        keys[b + i] = sk[i];
+        vals[b + i] = sv[i];
       }
     } else {
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         gk[b + i] = keys[b + i];
         gv[b + i] = vals[b + i];
       }
-      srck = gk + b;
-    }
-    __syncthreads();
-    const int* srcv = n <= kBlockRank ? sv : gv + b;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int kk = srck[i];
-      int r = 0;
-      for (int j = 0; j < n; j++) r += srck[j] < kk;
-      keys[b + r] = kk;
-      vals[b + r] = srcv[i];
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int kk = gk[b + i];
+        int r = 0;
+        for (int j = 0; j < n; j++) r += gk[b + j] < kk;
+        keys[b + r] = kk;
+        vals[b + r] = gv[b + i];
+      }
     }
     __syncthreads();
     place_row_in_csc<ROWS>(seg, b, e, threadIdx.x, blockDim.x, vals, col_ptr, ccur, csc_pos,
@@ -357,6 +409,7 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       !d_status || num_graph_edges < 0 || (num_graph_edges > 0 && !d_edge_type))
     return HIFUSE_ERR_INVALID_ARG;
   cudaStream_t s = st(stream);
+  static const int dbg = getenv("HIFUSE_DBG_SORT") ? atoi(getenv("HIFUSE_DBG_SORT")) : 0;
   std::vector<LayerMeta> metas(num_layers);
   LayerMeta* mv = metas.data();
   hifuse_status rc = HIFUSE_OK;
@@ -400,13 +453,13 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     int* cols_long = w.lists + m.rows;
     HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 8), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
               o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
-    HF_LAUNCH(k_sort_long<true>, 148, 256, 0, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
-              o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv);
+    HF_LAUNCH(k_sort_long<true>, 148, kSortThreads, 0, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
+              o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv, dbg);
     HF_LAUNCH(k_fix_cols, ceil_div(U_max, 256), 256, 0, s, o.U_dev, o.col_ptr, o.csc_pos,
               o.csc_row, cols_long, w.counters + 1);   // 8 warps x 32 columns per block
-    HF_LAUNCH(k_sort_long<false>, 148, 256, 0, s, o.col_ptr, o.csc_pos, o.csc_row,
+    HF_LAUNCH(k_sort_long<false>, 148, kSortThreads, 0, s, o.col_ptr, o.csc_pos, o.csc_row,
               (const int*)nullptr, (int*)nullptr, (int*)nullptr, (int*)nullptr, cols_long,
-              w.counters + 1, w.gk, w.gv);
+              w.counters + 1, w.gk, w.gv, dbg);
   }
   return last_cuda();
 }
