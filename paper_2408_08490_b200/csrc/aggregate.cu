@@ -334,6 +334,146 @@ k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __res
   for (int v = 0; v < V; v++) o[v * kLPC] = acc[v];
 }
 
+// Pre-scaled gradient rows: Gs[m] = w(m) G[g(m)] for every merged row m =
+// (r, i), w = 1 (sum) or 1/|row m| (mean); one pass over rho x D.  The CSC
+// gather then needs no relation shift and no degree lookup per entry.
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(256)
+k_scale_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, int rows,
+             const int* __restrict__ row_ptr, const float4* __restrict__ G,
+             float4* __restrict__ Gs) {
+  constexpr int LPR = D / 4;
+  __shared__ int s_roff[HF_MAX_R + 1];
+  __shared__ int s_shift[HF_MAX_R];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) {
+    s_roff[i] = rel_row_off_d[i];
+    if (i < bm.R) s_shift[i] = bm.shift[i];
+  }
+  __syncthreads();
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * LPR) return;
+  const int m = (int)(idx / LPR), c = (int)(idx % LPR);
+  const int r = upper_bound_i(s_roff, bm.R + 1, m) - 1;
+  float w = 1.f;
+  if (MEAN) {
+    const int dg = row_ptr[m + 1] - row_ptr[m];
+    w = dg > 0 ? 1.f / (float)dg : 0.f;
+  }
+  const float4 g = __ldg(G + (long long)(m + s_shift[r]) * LPR + c);
+  Gs[idx] = make_float4(w * g.x, w * g.y, w * g.z, w * g.w);
+}
+
+// Persistent CSC gather over the pre-scaled rows: 8 lanes per column, 4
+// columns per warp, grid-stride over column groups with the next group's
+// col_ptr fetched one iteration ahead.  dY[u] = sum_{p in column u} Gs[csc_row[p]].
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
+k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ col_ptr,
+            const int* __restrict__ csc_row, const float4* __restrict__ Gs,
+            float4* __restrict__ dY, int* __restrict__ long_list, int* __restrict__ long_cnt) {
+  constexpr int LPR = D / 4, LPC = 8, V = LPR / LPC, CPW = 32 / LPC;
+  const int lane = threadIdx.x & 31, j = lane % LPC, grp = lane / LPC;
+  const int gbase = lane & ~(LPC - 1);
+  const int U = *U_dev;
+  const int nw = gridDim.x * kWarpsPerBlock;
+  int cg = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  int nb = 0, ne = 0;
+  {
+    const int u = cg * CPW + grp;
+    if (u < U) { nb = __ldg(col_ptr + u); ne = __ldg(col_ptr + u + 1); }
+  }
+  for (; cg * CPW < U; cg += nw) {
+    const int u = cg * CPW + grp;
+    int b = nb, e = ne;
+    {   // prefetch the next column group's bounds
+      const int un = (cg + nw) * CPW + grp;
+      nb = ne = 0;
+      if (un < U) { nb = __ldg(col_ptr + un); ne = __ldg(col_ptr + un + 1); }
+    }
+    bool skip = u >= U;
+    if (!skip && e - b > kLongCol) {
+      if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
+      e = b;
+      skip = true;
+    }
+    float4 acc[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int rounds = __reduce_max_sync(0xffffffffu, (e - b + LPC - 1) / LPC);
+    for (int rd = 0; rd < rounds; rd++) {
+      const int p0 = b + rd * LPC;
+      const int my_row = p0 + j < e ? __ldg(csc_row + p0 + j) : -1;
+#pragma unroll
+      for (int q0 = 0; q0 < LPC; q0 += 4) {
+        float4 x[4][V];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int rq = __shfl_sync(0xffffffffu, my_row, gbase + q0 + q);
+          const float4* g = Gs + (long long)(rq < 0 ? 0 : rq) * LPR + j;
+#pragma unroll
+          for (int v = 0; v < V; v++) x[q][v] = rq >= 0 ? ldg4(g + v * LPC) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int v = 0; v < V; v++) acc[v] = f4add(acc[v], x[q][v]);
+      }
+    }
+    if (!skip) {
+      float4* o = dY + (long long)u * LPR + j;
+#pragma unroll
+      for (int v = 0; v < V; v++) o[v * LPC] = acc[v];
+    }
+  }
+}
+
+// Long columns over the pre-scaled rows (32 warps per column, fixed-order
+// combine of the warp slices).
+template <int D>
+__global__ void __launch_bounds__(1024)
+k_agg_bwd_p_long(const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
+                 const float4* __restrict__ Gs, float4* __restrict__ dY,
+                 const int* __restrict__ list, const int* __restrict__ cnt) {
+  constexpr int LPR = D / 4;
+  constexpr int NS = 32 / LPR;
+  __shared__ float4 red[32][LPR];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int sl = lane % LPR, sid = lane / LPR;
+  const int n_long = *cnt;
+  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
+    const int u = list[k];
+    const int b = col_ptr[u], e = col_ptr[u + 1];
+    const int per = (e - b + 31) / 32;
+    const int wb = min(e, b + w * per), we = min(e, wb + per);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int base = wb; base < we; base += 32) {
+      const int n = min(32, we - base);
+      const int my_row = lane < n ? __ldg(csc_row + base + lane) : 0;
+      for (int kk = 0; kk < n; kk += NS * 4) {
+        float4 x[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int idx = kk + q * NS + sid;
+          const int rr = __shfl_sync(0xffffffffu, my_row, idx < n ? idx : 0);
+          x[q] = idx < n ? ldg4(Gs + (long long)rr * LPR + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc = f4add(acc, x[q]);
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
+    if (sid == 0) red[w][sl] = acc;
+    __syncthreads();
+    if (w == 0 && lane < LPR) {
+      float4 t = red[0][lane];
+      for (int q = 1; q < 32; q++) t = f4add(t, red[q][lane]);
+      dY[(long long)u * LPR + lane] = t;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------ backward GAT, pass 1 (rows)
 // For row m=(r,i), head h, with g = G[g(m)] and alpha_p recomputed from stats:
 //   dalpha_p = <g_h, Y[col_p]_h>,  za = sum_p alpha_p dalpha_p,
@@ -584,6 +724,7 @@ size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg
   long long U_max = m.N < m.S ? m.N : m.S;
   size_t b = carve_bytes(U_max + 1, 4) + carve_bytes(2, 4);
   if (agg == HIFUSE_AGG_GAT) b += 2 * carve_bytes((long long)m.N * heads, 4);
+  else b += carve_bytes((long long)(m.rows > 0 ? m.rows : 1) * 128, 4);   // pre-scaled rows
   return b;
 }
 
@@ -638,11 +779,14 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
   } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
     if (agg == HIFUSE_AGG_MEAN && !csr->row_ptr) return HIFUSE_ERR_INVALID_ARG;
 #define HF_BWD(DD, MM)                                                                        \
-  HF_LAUNCH((k_agg_bwd<DD, MM>), gridU4, TB, 0, s, bm, (int)U_max, csr->U_dev, csr->rel_y_off,  \
-            csr->col_ptr, csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY,        \
-            long_list, long_cnt);                                                               \
-  HF_LAUNCH((k_agg_bwd_long<DD, MM>), gridL, kLongWarps * 32, 0, s, bm, csr->rel_y_off, csr->col_ptr,        \
-            csr->csc_row, csr->row_ptr, (const float4*)d_G, (float4*)d_dY, long_list, long_cnt)
+  HF_LAUNCH((k_scale_rows<DD, MM>), ceil_div((long long)m.rows * (DD / 4), 256), 256, 0, s, bm,  \
+            csr->rel_row_off, m.rows, csr->row_ptr, (const float4*)d_G, (float4*)Gs);           \
+  HF_LAUNCH((k_agg_bwd_p<DD>), 148 * 4, TB, 0, s, (int)U_max, csr->U_dev, csr->col_ptr,           \
+            csr->csc_row, (const float4*)Gs, (float4*)d_dY, long_list, long_cnt);               \
+  HF_LAUNCH((k_agg_bwd_p_long<DD>), gridL, 1024, 0, s, csr->col_ptr, csr->csc_row,                 \
+            (const float4*)Gs, (float4*)d_dY, long_list, long_cnt)
+    if (!csr->rel_row_off) return HIFUSE_ERR_INVALID_ARG;
+    float* Gs = carve<float>(p, (long long)(m.rows > 0 ? m.rows : 1) * 128);
     bool mean = agg == HIFUSE_AGG_MEAN;
     if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }
     else { if (mean) { HF_BWD(64, true); } else { HF_BWD(64, false); } }
