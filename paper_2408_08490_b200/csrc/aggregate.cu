@@ -364,8 +364,11 @@ k_scale_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, int rows,
 }
 
 // Persistent CSC gather over the pre-scaled rows: 8 lanes per column, 4
-// columns per warp, grid-stride over column groups with the next group's
-// col_ptr fetched one iteration ahead.  dY[u] = sum_{p in column u} Gs[csc_row[p]].
+// columns per warp, grid-stride over column groups.  Three-stage software
+// pipeline per iteration: col_ptr of group i+2, the first 8 csc_row entries
+// of group i+1 and the Gs rows of group i are all in flight together, so an
+// iteration costs ~one memory round trip instead of three.
+// dY[u] = sum_{p in column u} Gs[csc_row[p]].
 template <int D>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
 k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ col_ptr,
@@ -376,33 +379,43 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
   const int gbase = lane & ~(LPC - 1);
   const int U = *U_dev;
   const int nw = gridDim.x * kWarpsPerBlock;
-  int cg = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  int nb = 0, ne = 0;
-  {
+  const int cg0 = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  auto bounds = [&](int cg, int* b, int* e) {
     const int u = cg * CPW + grp;
-    if (u < U) { nb = __ldg(col_ptr + u); ne = __ldg(col_ptr + u + 1); }
-  }
-  for (; cg * CPW < U; cg += nw) {
+    *b = *e = 0;
+    if (u < U) { *b = __ldg(col_ptr + u); *e = __ldg(col_ptr + u + 1); }
+  };
+  auto first_row = [&](int b, int e) {
+    // long columns go to k_agg_bwd_p_long; their first round is not fetched
+    return (e - b <= kLongCol && b + j < e) ? __ldg(csc_row + b + j) : -1;
+  };
+  int b0, e0, b1, e1;
+  bounds(cg0, &b0, &e0);
+  bounds(cg0 + nw, &b1, &e1);
+  int row0 = first_row(b0, e0);
+  for (int cg = cg0; cg * CPW < U; cg += nw) {
+    // stage loads for the next iterations
+    int b2, e2;
+    bounds(cg + 2 * nw, &b2, &e2);
+    const int row1 = first_row(b1, e1);
     const int u = cg * CPW + grp;
-    int b = nb, e = ne;
-    {   // prefetch the next column group's bounds
-      const int un = (cg + nw) * CPW + grp;
-      nb = ne = 0;
-      if (un < U) { nb = __ldg(col_ptr + un); ne = __ldg(col_ptr + un + 1); }
-    }
     bool skip = u >= U;
-    if (!skip && e - b > kLongCol) {
+    int e = e0;
+    if (!skip && e0 - b0 > kLongCol) {
       if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
-      e = b;
+      e = b0;
       skip = true;
     }
     float4 acc[V];
 #pragma unroll
     for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int rounds = __reduce_max_sync(0xffffffffu, (e - b + LPC - 1) / LPC);
+    const int rounds = __reduce_max_sync(0xffffffffu, (e - b0 + LPC - 1) / LPC);
+    int my_row = row0;
     for (int rd = 0; rd < rounds; rd++) {
-      const int p0 = b + rd * LPC;
-      const int my_row = p0 + j < e ? __ldg(csc_row + p0 + j) : -1;
+      if (rd > 0) {
+        const int p = b0 + rd * LPC + j;
+        my_row = p < e ? __ldg(csc_row + p) : -1;
+      }
 #pragma unroll
       for (int q0 = 0; q0 < LPC; q0 += 4) {
         float4 x[4][V];
@@ -424,6 +437,8 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
 #pragma unroll
       for (int v = 0; v < V; v++) o[v * LPC] = acc[v];
     }
+    b0 = b1; e0 = e1; row0 = row1;
+    b1 = b2; e1 = e2;
   }
 }
 
