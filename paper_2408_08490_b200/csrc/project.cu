@@ -294,7 +294,23 @@ k_wgrad_partial(ProjMeta pm, const int* __restrict__ chunk_off, const int* __res
 // dW[g] = sum of group g's chunk partials, in chunk order (deterministic).
 __global__ void k_wgrad_reduce(int R, int T, int KD, const int* __restrict__ chunk_off,
                                const float4* __restrict__ partial, float4* __restrict__ dW_rel,
-                               float4* __restrict__ dW_root) {
+                               float4* __restrict__ dW_root, ProjMeta pm,
+                               const int* __restrict__ rel_y_off, int CH) {
+  // chunk table: from chunk_off (SIMT path) or rebuilt here from rel_y_off
+  __shared__ int s_co[HF_MAX_R + HF_MAX_T + 1];
+  if (!chunk_off) {
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int g = 0; g < pm.R + pm.T; g++) {
+        const int rows = g < pm.R ? rel_y_off[g + 1] - rel_y_off[g] : (pm.has_root ? pm.n_dst[g - pm.R] : 0);
+        s_co[g] = acc;
+        acc += (rows + CH - 1) / CH;
+      }
+      s_co[pm.R + pm.T] = acc;
+    }
+    __syncthreads();
+    chunk_off = s_co;
+  }
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   int KD4 = KD / 4;
   int G = dW_root ? R + T : R;
@@ -576,7 +592,6 @@ size_t hifuse_project_ws_bytes(const hifuse_layer_shape* shape, int K, int D, in
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
   size_t b = 2 * carve_bytes(m.R + m.T + 1, 4);            // tile_off, chunk_off
   b += carve_bytes((long long)m.R * K * (heads > 0 ? heads : 1), 4);   // v
-  b += carve_bytes((long long)(m.R + m.T) * K * D, 4);     // transposed weights (tf32 path)
   return b;
 }
 
@@ -606,14 +621,8 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   int* tile_off = carve<int>(p, m.R + m.T + 1);
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
   float* v = carve<float>(p, (long long)m.R * K * (heads > 0 ? heads : 1));
-  float* Wt = carve<float>(p, (long long)(m.R + m.T) * K * D);
   if (prec == HIFUSE_PREC_TF32) {
-    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, 128, kCH);
-    static const bool simple = getenv("HIFUSE_TC_SIMPLE") != nullptr;
-    rc = simple ? project_tc_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y,
-                                    d_R0, tile_off, Wt, s)
-                : project_tcp_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y,
-                                     d_R0, tile_off, Wt, s);
+    rc = project_tcp_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0, s);
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
@@ -699,9 +708,9 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
     HF_LAUNCH(k_dy_score, ceil_div(U_max, 8), 256, 0, s, m.R, D, H, csr->U_dev, csr->rel_y_off,
               d_att, d_ds_src, d_dY);
   }
+  int CH = kCH;
   if (prec == HIFUSE_PREC_TF32) {
-    const int CH = wgrad_chunk_rows(m);
-    HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, CH);
+    CH = wgrad_chunk_rows(m);
     wgrad_tc_launch(m, pm, K, D, CH, chunk_off, csr->rel_y_off, csr->y_src, d_gather_ids, d_X,
                     d_dY, d_G, partial, (unsigned)proj_max_tiles(m, CH), s);
   } else {
@@ -718,7 +727,8 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   }
   int G = d_W_root ? m.R + m.T : m.R;
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
-            chunk_off, (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root);
+            prec == HIFUSE_PREC_TF32 ? (const int*)nullptr : (const int*)chunk_off,
+            (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root, pm, csr->rel_y_off, CH);
   if (d_att) {
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, s, m.R, K, D, H, d_W_rel,
               d_att, v);

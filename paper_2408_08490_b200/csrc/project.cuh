@@ -39,11 +39,11 @@ void make_dgrad_meta(const LayerMeta& m, bool has_root, DgradMeta* dm, int bm = 
 long long proj_max_tiles(const LayerMeta& m, int step);
 
 // tcgen05 TF32 forward projection (project_tc.cu).
-// persistent warp-specialised variant of project_tc_launch (same contract)
+// tcgen05 TF32 forward projection (persistent, warp-specialised; project_tc.cu)
 hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
                                  const hifuse_csr* csr, const float* X, const int* gather_ids,
                                  const float* W_rel, const float* W_root, float* Y, float* R0,
-                                 int* tile_off, float* Wt, cudaStream_t s);
+                                 cudaStream_t s);
 // tcgen05 TF32 dgrad: dX[type s rows] = sum_terms A_term W_term^T (A = dYt rows
 // through slot_y, or G for the root term).  dm built with bm = 128.
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
@@ -63,11 +63,4 @@ hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int
                               const int* chunk_off, const int* rel_y_off, const int* y_src,
                               const int* gather_ids, const float* X, const float* dY,
                               const float* G, float* partial, unsigned grid, cudaStream_t s);
-// tile_off: 128-row tile table of the groups (k_group_table); Wt: workspace
-// for the transposed weights [(R+T)][D][K].
-hifuse_status project_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
-                                const hifuse_csr* csr, const float* X, const int* gather_ids,
-                                const float* W_rel, const float* W_root, float* Y, float* R0,
-                                int* tile_off, float* Wt, cudaStream_t s);
-
 }  // namespace hf

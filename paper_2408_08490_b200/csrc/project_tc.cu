@@ -53,145 +53,6 @@ __device__ __forceinline__ long long tc_a_row(const ProjMeta& pm, const int* rel
   return gather_ids ? (long long)gather_ids[x] : (long long)x;
 }
 
-// Wt[g][n][k] = W_g[k][n]  (groups: relations then root types)
-__global__ void k_wt_transpose(int R, int G, int K, int D, const float* __restrict__ W_rel,
-                               const float* __restrict__ W_root, float* __restrict__ Wt) {
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)G * K * D) return;
-  int g = (int)(idx / ((long long)K * D));
-  int rem = (int)(idx % ((long long)K * D));
-  int n = rem / K, k = rem % K;
-  const float* W = g < R ? W_rel + (long long)g * K * D : W_root + (long long)(g - R) * K * D;
-  Wt[idx] = W[(long long)k * D + n];
-}
-
-template <int K, int D>
-__global__ void __launch_bounds__(128)
-k_proj_fwd_tc(ProjMeta pm, const int* __restrict__ tile_off, const int* __restrict__ rel_y_off,
-              const int* __restrict__ y_src, const int* __restrict__ gather_ids,
-              const float* __restrict__ X, const float* __restrict__ Wt, float* __restrict__ Y,
-              float* __restrict__ R0) {
-  constexpr int BM = 128, NC = K / 32;
-  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = D * 128, STAGE = A_STAGE + B_STAGE;
-  constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 0);
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[2];
-  __shared__ uint32_t tmem_slot;
-  int g, r0, nrows;
-  if (!tc_resolve(pm, tile_off, rel_y_off, blockIdx.x, BM, &g, &r0, &nrows)) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t bar0 = smem_u32(&bars[0]), bar1 = smem_u32(&bars[1]);
-  if (tid == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar1, 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), D);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-
-  const float* arow = X;
-  uint32_t abytes = 0;
-  if (tid < nrows) {
-    arow = X + tc_a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + tid) * K;
-    abytes = 16;
-  }
-  const float* brow = Wt + ((long long)g * D + (tid < D ? tid : 0)) * K;
-
-  auto load = [&](int c, int s) {
-    const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
-#pragma unroll
-    for (int j = 0; j < 8; j++) cp_async16(sa + sw128_off(tid, j), arow + c * 32 + j * 4, abytes);
-    if (tid < D) {
-#pragma unroll
-      for (int j = 0; j < 8; j++) cp_async16(sb + sw128_off(tid, j), brow + c * 32 + j * 4, 16);
-    }
-    cp_async_commit();
-  };
-
-  load(0, 0);
-#pragma unroll
-  for (int c = 0; c < NC; c++) {
-    const int s = c & 1;
-    if (c + 1 < NC) {
-      if (c + 1 >= 2) mbar_wait((c + 1) & 1 ? bar1 : bar0, ((c - 1) >> 1) & 1);
-      load(c + 1, (c + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
-#pragma unroll
-      for (int k = 0; k < 4; k++)
-        mma_tf32(tmem, sw128_desc(sa + k * 32, 16, 1024), sw128_desc(sb + k * 32, 16, 1024), IDESC,
-                 (c | k) ? 1u : 0u);
-      mma_commit(s ? bar1 : bar0);
-    }
-    __syncwarp();
-  }
-  mbar_wait((NC - 1) & 1 ? bar1 : bar0, ((NC - 1) >> 1) & 1);
-  tc_fence_after();
-
-  float* out = g < pm.R ? Y + (long long)rel_y_off[g] * D
-                        : R0 + (long long)pm.type_dst_off[g - pm.R] * D;
-  const int row = warp * 32 + lane;
-  float* orow = out + (long long)(r0 + row) * D;
-#pragma unroll
-  for (int c0 = 0; c0 < D; c0 += 16) {
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-    if (row < nrows) {
-      float4* o = reinterpret_cast<float4*>(orow + c0);
-      o[0] = make_float4(v[0], v[1], v[2], v[3]);
-      o[1] = make_float4(v[4], v[5], v[6], v[7]);
-      o[2] = make_float4(v[8], v[9], v[10], v[11]);
-      o[3] = make_float4(v[12], v[13], v[14], v[15]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, D);
-}
-
-template <int K, int D>
-static constexpr int fwd_smem() {
-  return 2 * (128 * 128 + D * 128) + 1024;
-}
-
-hifuse_status project_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
-                                const hifuse_csr* csr, const float* X, const int* gather_ids,
-                                const float* W_rel, const float* W_root, float* Y, float* R0,
-                                int* tile_off, float* Wt, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_proj_fwd_tc<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<128, 128>());
-    cudaFuncSetAttribute(k_proj_fwd_tc<128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<128, 64>());
-    cudaFuncSetAttribute(k_proj_fwd_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<64, 128>());
-    cudaFuncSetAttribute(k_proj_fwd_tc<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem<64, 64>());
-    attr = true;
-  }
-  const int G = pm.has_root ? m.R + m.T : m.R;
-  HF_LAUNCH(k_wt_transpose, ceil_div((long long)G * K * D, 256), 256, 0, s, m.R, G, K, D, W_rel,
-            W_root, Wt);
-  unsigned grid = (unsigned)proj_max_tiles(m, 128);
-#define HF_TC(KK, DD)                                                                          \
-  HF_LAUNCH((k_proj_fwd_tc<KK, DD>), grid, 128, (fwd_smem<KK, DD>()), s, pm, tile_off,         \
-            csr->rel_y_off, csr->y_src, gather_ids, X, Wt, Y, R0)
-  if (K == 128 && D == 128) HF_TC(128, 128);
-  else if (K == 128 && D == 64) HF_TC(128, 64);
-  else if (K == 64 && D == 128) HF_TC(64, 128);
-  else HF_TC(64, 64);
-#undef HF_TC
-  return HIFUSE_OK;
-}
-
 }  // namespace hf
 
 namespace hf {
@@ -202,6 +63,8 @@ namespace hf {
 // columns of dYt rows gathered through slot_y (zero rows where the source has
 // no edge of that relation); B chunk: W_term[k][d0..d0+32) for every k, which
 // is already K-major (row k contiguous in d).  N = K.
+static constexpr int kDgStages = 4;
+
 template <int K, int D>
 __global__ void __launch_bounds__(128)
 k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
@@ -211,17 +74,15 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   constexpr uint32_t A_STAGE = BM * 128, B_STAGE = K * 128, STAGE = A_STAGE + B_STAGE;
   constexpr uint32_t IDESC = idesc_tf32(BM, K, 0, 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[kDgStages];
   __shared__ uint32_t tmem_slot;
   const int s_ = upper_bound_i(dm.tile_off, dm.T + 1, blockIdx.x) - 1;
   const int j0 = (blockIdx.x - dm.tile_off[s_]) * BM;
   const int nrows = min(BM, dm.n_src[s_] - j0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t bar0 = smem_u32(&bars[0]), bar1 = smem_u32(&bars[1]);
   if (tid == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar1, 1);
+    for (int q = 0; q < kDgStages; q++) mbar_init(smem_u32(&bars[q]), 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), K);
@@ -261,16 +122,21 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
     cp_async_commit();
   };
 
-  if (NC > 0) load(0, 0);
+  for (int c = 0; c < kDgStages - 1; c++) {
+    if (c < NC) load(c, c);
+    else cp_async_commit();
+  }
   for (int c = 0; c < NC; c++) {
-    const int st = c & 1;
-    if (c + 1 < NC) {
-      if (c + 1 >= 2) mbar_wait((c + 1) & 1 ? bar1 : bar0, ((c - 1) >> 1) & 1);
-      load(c + 1, (c + 1) & 1);
-      cp_async_wait<1>();
+    const int st = c % kDgStages;
+    const int nxt = c + kDgStages - 1;
+    if (nxt < NC) {
+      const int ns = nxt % kDgStages;
+      if (nxt >= kDgStages) mbar_wait(smem_u32(&bars[ns]), ((nxt / kDgStages) - 1) & 1);
+      load(nxt, ns);
     } else {
-      cp_async_wait<0>();
+      cp_async_commit();
     }
+    cp_async_wait<kDgStages - 1>();
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
@@ -280,12 +146,12 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
       for (int k = 0; k < 4; k++)
         mma_tf32(tmem, sw128_desc(sa + k * 32, 16, 1024), sw128_desc(sb + k * 32, 16, 1024), IDESC,
                  (c | k) ? 1u : 0u);
-      mma_commit(st ? bar1 : bar0);
+      mma_commit(smem_u32(&bars[st]));
     }
     __syncwarp();
   }
   if (NC > 0) {
-    mbar_wait((NC - 1) & 1 ? bar1 : bar0, ((NC - 1) >> 1) & 1);
+    mbar_wait(smem_u32(&bars[(NC - 1) % kDgStages]), ((NC - 1) / kDgStages) & 1);
     tc_fence_after();
   }
   const int row = warp * 32 + lane;
@@ -312,6 +178,9 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   if (warp == 0) tmem_dealloc(tmem, K);
 }
 
+__device__ __forceinline__ void group_table_warp(const ProjMeta& pm, const int* s_yoff, int step,
+                                                 int* s_tab, int lane);
+
 // ----------------------------------------------------------------- wgrad ----
 // Chunk = up to CH rows of one group (CH adapts to the layer size, 128..1024); partial[chunk] = A^T B over the rows,
 // A = X rows (features = M, padded to 128 when K = 64), B = dYt / G rows
@@ -335,9 +204,14 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bars[kWgStages];
   __shared__ uint32_t tmem_slot;
-  int g, r0, nrows;
-  if (!tc_resolve(pm, chunk_off, rel_y_off, blockIdx.x, CH, &g, &r0, &nrows)) return;
+  __shared__ int s_tab[HF_MAX_R + HF_MAX_T + 1], s_yo[HF_MAX_R + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i <= pm.R; i += blockDim.x) s_yo[i] = rel_y_off[i];
+  __syncthreads();
+  if (warp == 0) group_table_warp(pm, s_yo, CH, s_tab, lane);
+  __syncthreads();
+  int g, r0, nrows;
+  if (!tc_resolve(pm, s_tab, s_yo, blockIdx.x, CH, &g, &r0, &nrows)) return;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   if (tid == 0) {
     for (int q = 0; q < kWgStages; q++) mbar_init(smem_u32(&bars[q]), 1);
@@ -449,7 +323,7 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
 }
 
 template <int K, int D>
-static constexpr int dgrad_smem() { return 2 * (128 * 128 + K * 128) + 1024; }
+static constexpr int dgrad_smem() { return kDgStages * (128 * 128 + K * 128) + 1024; }
 template <int K, int D>
 static constexpr int wgrad_smem() { return kWgStages * (4 * 4096 + (D / 32) * 4096) + 1024; }
 
@@ -505,26 +379,59 @@ hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int
 namespace hf {
 
 // ------------------------------------------------ persistent forward GEMM ----
-// One CTA per SM, warp-specialised (the canonical Blackwell structure):
-//   warps 0-3  producers: gather the tile's A rows (and B = W_g^T) with
-//              16-byte cp.async into a kFStages-deep ring of 128-B K chunks;
-//              a thread signals a chunk `full` kLag chunks later (cp.async
-//              groups retire in order), after fence.proxy.async;
-//   warp 8     one elected thread issues tcgen05.mma (M=128, N=D, K=8) per
-//              chunk into one of TWO TMEM accumulators, commits the chunk's
+// Two CTAs per SM, warp-specialised (the canonical Blackwell structure):
+//   warps 0-3  producers: per 128-B K chunk, gather the tile's 128 A rows
+//              (coalesced: one warp instruction = 4 rows x 128 B) into the
+//              128B-swizzled K-major layout, and load the 32 x D slice of W_g
+//              straight from its [K][D] storage as an MN-major operand
+//              (SWIZZLE_128B_BASE32B) -- no transposed weight copy; a thread
+//              signals a stage `full` kLag chunks later (cp.async groups retire
+//              in order), after fence.proxy.async;
+//   warp 8     one elected thread issues 4 tcgen05.mma (M=128, N=D, K=8) per
+//              chunk into one of two TMEM accumulators, commits the stage's
 //              `empty` barrier and, after a tile's last chunk, `tfull`;
-//   warps 4-7  epilogue: tcgen05.ld of the finished accumulator (warp w reads
-//              TMEM lanes 32(w%4)...) and fp32 row stores, then `tempty`.
-// Loads of tile i+1 overlap the MMAs and the epilogue of tile i.
-template <int K, int D, int kFStages, int kLag, int kCtas>
-__global__ void __launch_bounds__(288, kCtas)
-k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restrict__ rel_y_off,
-               const int* __restrict__ y_src, const int* __restrict__ gather_ids,
-               const float* __restrict__ X, const float* __restrict__ Wt, float* __restrict__ Y,
-               float* __restrict__ R0) {
+//   warps 4-7  epilogue: tcgen05.ld (warp w reads TMEM lanes 32(w%4)..),
+//              16-column slices staged in shared memory and written back as
+//              8 rows x 64 contiguous bytes per instruction, then `tempty`.
+// The tile table (128-row tiles per group) is built in shared memory from
+// rel_y_off at kernel start.
+static constexpr int kFStages = 3;
+static constexpr int kLag = 2;
+static constexpr int kFwdCtas = 2;
+
+// Tiles (or chunks) of `step` rows per group -> s_tab[0..G], one warp.
+__device__ __forceinline__ void group_table_warp(const ProjMeta& pm, const int* s_yoff, int step,
+                                                 int* s_tab, int lane) {
+  const int G = pm.R + pm.T;
+  int carry = 0;
+  for (int base = 0; base < G; base += 32) {
+    const int g = base + lane;
+    int rows = 0;
+    if (g < pm.R) rows = s_yoff[g + 1] - s_yoff[g];
+    else if (g < G && pm.has_root) rows = pm.n_dst[g - pm.R];
+    const int t = (rows + step - 1) / step;
+    int inc = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += n;
+    }
+    if (g < G) s_tab[g] = carry + inc - t;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) s_tab[G] = carry;
+}
+
+template <int K, int D>
+__global__ void __launch_bounds__(288, kFwdCtas)
+k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __restrict__ y_src,
+               const int* __restrict__ gather_ids, const float* __restrict__ X,
+               const float* __restrict__ W_rel, const float* __restrict__ W_root,
+               float* __restrict__ Y, float* __restrict__ R0) {
   constexpr int BM = 128, NC = K / 32;
-  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = D * 128, STAGE = A_STAGE + B_STAGE;
-  constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 0);
+  constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
+  constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+  constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 1);      // A K-major, B MN-major
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kFStages], empty[kFStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
@@ -532,7 +439,6 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
   __shared__ __align__(16) float stage_ep[4 * 32 * 20];     // epilogue staging
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  for (int i = tid; i <= pm.R + pm.T; i += blockDim.x) s_tile[i] = tile_off[i];
   for (int i = tid; i <= pm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
   if (tid == 0) {
     for (int q = 0; q < kFStages; q++) {
@@ -545,6 +451,8 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
     }
     fence_barrier_init();
   }
+  __syncthreads();
+  if (warp == 0) group_table_warp(pm, s_yoff, BM, s_tile, lane);
   if (warp == 8) tmem_alloc(smem_u32(&tmem_slot), 2 * D);
   tc_fence_before();
   __syncthreads();
@@ -554,11 +462,9 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
 
   if (warp < 4) {
     // ------------------------------------------------------------ producers
-    // Coalesced gathers: producer warp w owns tile rows [32w, 32w+32); one
-    // warp instruction moves 4 rows x 128 B (8 lanes x 16 B per row), so each
-    // request touches 4 full lines instead of 32 partial ones.  Lane l serves
-    // rows 32w + 4i + l/8 (i = 0..7), 16-byte piece l%8 of every K chunk.
-    // The next tile's row addresses are fetched one tile ahead.
+    // producer warp w owns tile rows [32w, 32w+32); lane l serves rows
+    // 32w + 4i + l/8 (i = 0..7), 16-byte piece l%8 of every K chunk; the next
+    // tile's row addresses are fetched one tile ahead.
     const int piece = lane & 7, rsub = lane >> 3;
     auto rows_of = [&](int t, int* g, const float** ap, uint32_t* nb) {
       int r0, nrows;
@@ -578,6 +484,8 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
     int g = 0;
     const float* ap[8];
     uint32_t nb[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) { ap[i] = X; nb[i] = 0; }
     if ((int)blockIdx.x < ntiles) rows_of(blockIdx.x, &g, ap, nb);
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int ng = 0;
@@ -586,7 +494,7 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
 #pragma unroll
       for (int i = 0; i < 8; i++) { nap[i] = X; nnb[i] = 0; }
       if (t + (int)gridDim.x < ntiles) rows_of(t + gridDim.x, &ng, nap, nnb);
-      const float* Wg = Wt + (long long)g * D * K;
+      const float* Wg = g < pm.R ? W_rel + (long long)g * K * D : W_root + (long long)(g - pm.R) * K * D;
       for (int c = 0; c < NC; c++, it++) {
         const int s = it % kFStages;
         if (it >= kFStages) mbar_wait(smem_u32(&empty[s]), ((it / kFStages) - 1) & 1);
@@ -596,10 +504,13 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
           const int row = warp * 32 + i * 4 + rsub;
           cp_async16(sa + sw128_off(row, piece), ap[i] + c * 32 + piece * 4, nb[i]);
         }
+        // B: rows k = 32c .. 32c+31 of W_g, D floats each, MN-major atoms
 #pragma unroll
-        for (int i = 0; i < D / 16; i++) {          // B rows: D / 4 warps / 4 rows per instr
-          const int row = warp * (D / 4) + i * 4 + rsub;
-          cp_async16(sb + sw128_off(row, piece), Wg + (long long)row * K + c * 32 + piece * 4, 16);
+        for (int q = 0; q < 32 * D / 4 / 128; q++) {
+          const int i = tid + 128 * q;
+          const int kr = i / (D / 4), n = (i % (D / 4)) * 4;
+          cp_async16(sb + (n >> 5) * B_BLK + (kr >> 2) * 512 + sw128b32_off(kr, (n & 31) * 4),
+                     Wg + (long long)(c * 32 + kr) * D + n, 16);
         }
         cp_async_commit();
         if (it >= kLag) {
@@ -627,18 +538,15 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
       tc_fence_after();
       float* out = g < pm.R ? Y + (long long)s_yoff[g] * D
                             : R0 + (long long)pm.type_dst_off[g - pm.R] * D;
-      // TMEM lane = row: stage each 16-column slice of the warp's 32 rows in
-      // shared memory (80-byte row pitch: conflict-free) and write it back as
-      // 8 rows x 64 contiguous bytes per instruction (full sectors).
       float* st = stage_ep + q * (32 * 20);
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 16) {
         float v[16];
         tmem_ld16(tmem + (uint32_t)(acc * D) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
-        for (int j = 0; j < 4; j++)
-          *reinterpret_cast<float4*>(st + lane * 20 + 4 * j) =
-              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        for (int jj = 0; jj < 4; jj++)
+          *reinterpret_cast<float4*>(st + lane * 20 + 4 * jj) =
+              make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; i++) {
@@ -667,7 +575,7 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
 #pragma unroll
         for (int k = 0; k < 4; k++)
           mma_tf32(tmem + (uint32_t)(acc * D), sw128_desc(sa + k * 32, 16, 1024),
-                   sw128_desc(sb + k * 32, 16, 1024), IDESC, (c | k) ? 1u : 0u);
+                   sw128b32_desc(sb + k * 1024, B_BLK, 512), IDESC, (c | k) ? 1u : 0u);
         mma_commit(smem_u32(&empty[s]));
       }
       mma_commit(smem_u32(&tfull[acc]));
@@ -678,50 +586,32 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ tile_off, const int* __restr
   if (warp == 8) tmem_dealloc(tmem, 2 * D);
 }
 
-template <int K, int D, int ST>
-static constexpr int fwdp_smem() { return ST * (128 * 128 + D * 128) + 1024; }
-
-// pipeline variants (stages, lag, CTAs per SM), selectable with HIFUSE_TCP_VARIANT
-template <int K, int D, int ST, int LAG, int CT>
-static void launch_tcp(unsigned grid, const ProjMeta& pm, int* tile_off, const hifuse_csr* csr,
-                       const int* gather_ids, const float* X, const float* Wt, float* Y, float* R0,
-                       cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_proj_fwd_tcp<K, D, ST, LAG, CT>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, fwdp_smem<K, D, ST>());
-    attr = true;
-  }
-  HF_LAUNCH((k_proj_fwd_tcp<K, D, ST, LAG, CT>), grid * CT, 288, (fwdp_smem<K, D, ST>()), s, pm,
-            tile_off, csr->rel_y_off, csr->y_src, gather_ids, X, Wt, Y, R0);
-}
+template <int K, int D>
+static constexpr int fwdp_smem() { return kFStages * (128 * 128 + D * 128) + 1024; }
 
 template <int K, int D>
-static void launch_tcp_variant(int v, unsigned grid, const ProjMeta& pm, int* tile_off,
-                               const hifuse_csr* csr, const int* gather_ids, const float* X,
-                               const float* Wt, float* Y, float* R0, cudaStream_t s) {
-  switch (v) {
-    case 1: launch_tcp<K, D, 6, 5, 1>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
-    case 2: launch_tcp<K, D, 3, 2, 2>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
-    case 3: launch_tcp<K, D, 3, 1, 2>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
-    default: launch_tcp<K, D, 6, 3, 1>(grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s); break;
+static void launch_tcp(const ProjMeta& pm, const hifuse_csr* csr, const int* gather_ids,
+                       const float* X, const float* W_rel, const float* W_root, float* Y,
+                       float* R0, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_proj_fwd_tcp<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fwdp_smem<K, D>());
+    attr = true;
   }
+  HF_LAUNCH((k_proj_fwd_tcp<K, D>), 148 * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
+            csr->rel_y_off, csr->y_src, gather_ids, X, W_rel, W_root, Y, R0);
 }
 
 hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
                                  const hifuse_csr* csr, const float* X, const int* gather_ids,
                                  const float* W_rel, const float* W_root, float* Y, float* R0,
-                                 int* tile_off, float* Wt, cudaStream_t s) {
-  static const int variant = getenv("HIFUSE_TCP_VARIANT") ? atoi(getenv("HIFUSE_TCP_VARIANT")) : 2;
-  const int G = pm.has_root ? m.R + m.T : m.R;
-  HF_LAUNCH(k_wt_transpose, ceil_div((long long)G * K * D, 256), 256, 0, s, m.R, G, K, D, W_rel,
-            W_root, Wt);
-  long long maxt = proj_max_tiles(m, 128);
-  unsigned grid = (unsigned)(maxt < 148 ? maxt : 148);
-  if (K == 128 && D == 128) launch_tcp_variant<128, 128>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
-  else if (K == 128 && D == 64) launch_tcp_variant<128, 64>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
-  else if (K == 64 && D == 128) launch_tcp_variant<64, 128>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
-  else launch_tcp_variant<64, 64>(variant, grid, pm, tile_off, csr, gather_ids, X, Wt, Y, R0, s);
+                                 cudaStream_t s) {
+  (void)m;
+  if (K == 128 && D == 128) launch_tcp<128, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
+  else if (K == 128 && D == 64) launch_tcp<128, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
+  else if (K == 64 && D == 128) launch_tcp<64, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
+  else launch_tcp<64, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
   return HIFUSE_OK;
 }
 
