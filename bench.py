@@ -99,8 +99,9 @@ def layer_sizes(cfg, g, mb, rs, rd):
         r = g.edge_type[blk.edge_id]
         U = len(np.unique(r.astype(np.int64) * (1 << 32) + blk.src_local)) if blk.num_edges else 0
         rows = int(sum(int(blk.n_dst[rd[k]]) for k in range(len(rd))))
+        S = int(sum(int(blk.n_src[rs[k]]) for k in range(len(rs))))
         out.append(dict(N=blk.num_edges, rows=rows, U=U, dst=int(blk.n_dst.sum()),
-                        src=int(blk.n_src.sum())))
+                        src=int(blk.n_src.sum()), S=S))
     return out
 
 
@@ -134,7 +135,31 @@ def stage_cost(stage, l, cfg, sz):
         return 4 * D * (s["rows"] + 2 * s["dst"]), 0
     if stage == "fuse_bwd":
         return 4 * D * 3 * s["dst"], 0
+    if stage == "build":     # all layers: inputs 20 B/edge, CSR+CSC 16 B/edge, offsets, Y ids
+        b = 0
+        for q in sz:
+            b += 36 * q["N"] + 4 * (q["rows"] + 1) + 8 * q["U"] + 4 * q["S"]
+        return b, 0
     return 0, 0
+
+
+# main kernel of every library call (for the ncu traffic lookup)
+MAIN_KERNEL = {"aggregate_fwd": "k_agg_fwd", "aggregate_bwd": "k_agg_bwd_p", "project": "k_proj_fwd_tcp",
+               "project_bwd": "k_wgrad_tc", "fuse": "k_fuse", "fuse_bwd": "k_fuse_bwd_chunks",
+               "build": "k_sort_long", "xent": "k_gemm_small"}
+
+
+def ncu_traffic(kernel, layer):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` (the layer-th
+    launch in step order) from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(kernel)
+    if not v:
+        return None
+    return v[min(layer, len(v) - 1)] if isinstance(v, list) else v
 
 
 # -------------------------------------------------------------- reference ---
@@ -353,34 +378,48 @@ def main():
     pk = peaks()
     step_ms = ms / args.steps
     per_step = {k: float(np.mean([t for _, t in v])) for k, v in stage_ms.items()}
-    dom = max(per_step, key=lambda k: per_step[k])
-    name, _, layer = dom.partition(".")
-    l = int(layer) if layer else 0
-    used = [pi for pi, _ in stage_ms[dom]]
-    avg_bytes = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[0] for pi in used]))
-    avg_flops = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[1] for pi in used]))
-    t_s = per_step[dom] / 1e3
-    if name in ("project", "project_bwd") and args.prec == "fp32":
-        roof = {"bound": "alu", "achieved": avg_flops / t_s / 1e12, "peak": ALU_FP32_TFLOPS,
-                "unit": "TFLOP/s"}
-    elif name in ("project", "project_bwd"):
-        bw_time = avg_bytes / (pk["hbm"] * 1e9)
-        fl_time = avg_flops / (pk["bf16"] * TF32_OVER_BF16 * 1e12)
-        if bw_time >= fl_time:
+    pipelined = graphs is not serial_graphs
+
+    def roofline_of(stage_key):
+        name, _, layer = stage_key.partition(".")
+        l = int(layer) if layer else 0
+        used = [pi for pi, _ in stage_ms[stage_key]]
+        avg_bytes = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[0] for pi in used]))
+        avg_flops = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[1] for pi in used]))
+        t_s = per_step[stage_key] / 1e3
+        if name in ("project", "project_bwd") and args.prec == "fp32":
+            roof = {"bound": "alu", "achieved": avg_flops / t_s / 1e12, "peak": ALU_FP32_TFLOPS,
+                    "unit": "TFLOP/s"}
+        elif name in ("project", "project_bwd"):
+            bw_time = avg_bytes / (pk["hbm"] * 1e9)
+            fl_time = avg_flops / (pk["bf16"] * TF32_OVER_BF16 * 1e12)
+            if bw_time >= fl_time:
+                roof = {"bound": "hbm", "achieved": avg_bytes / t_s / 1e9, "peak": pk["hbm"],
+                        "unit": "GB/s"}
+            else:
+                roof = {"bound": "tensor", "achieved": avg_flops / t_s / 1e12,
+                        "peak": pk["bf16"] * TF32_OVER_BF16, "unit": "TFLOP/s"}
+        else:
             roof = {"bound": "hbm", "achieved": avg_bytes / t_s / 1e9, "peak": pk["hbm"],
                     "unit": "GB/s"}
-        else:
-            roof = {"bound": "tensor", "achieved": avg_flops / t_s / 1e12,
-                    "peak": pk["bf16"] * TF32_OVER_BF16, "unit": "TFLOP/s"}
-    else:
-        roof = {"bound": "hbm", "achieved": avg_bytes / t_s / 1e9, "peak": pk["hbm"],
-                "unit": "GB/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
-    roof["kernel"] = dom
-    roof["peak_source"] = pk["src"]
-    roof["algorithmic"] = {"bytes": avg_bytes, "flops": avg_flops, "us": per_step[dom] * 1e3}
-    roof["share_of_step"] = per_step[dom] / step_ms
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        bwd = name in ("aggregate_bwd", "project_bwd", "fuse_bwd")
+        tr = None if name == "build" else ncu_traffic(MAIN_KERNEL.get(name, name),
+                                                       cfg.num_layers - 1 - l if bwd else l)
+        roof["traffic"] = tr
+        roof["kernel"] = f"{stage_key} (main kernel {MAIN_KERNEL.get(name, name)})"
+        roof["peak_source"] = pk["src"]
+        roof["algorithmic"] = {"bytes": avg_bytes, "flops": avg_flops,
+                               "us": per_step[stage_key] * 1e3}
+        roof["share_of_step"] = per_step[stage_key] / step_ms
+        return roof
+
+    # the dominant call on the critical path (the build overlaps the compute
+    # stream when pipelined and is reported separately)
+    cand = [k for k in per_step if not (pipelined and k == "build")]
+    dom = max(cand, key=lambda k: per_step[k])
+    roof = roofline_of(dom)
+    build_roof = roofline_of("build") if "build" in per_step else None
     agg_gbs = {}
     for k in per_step:
         if k.startswith("aggregate_fwd"):
@@ -407,6 +446,7 @@ def main():
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "build_roofline": build_roof,
         "aggregation_hbm": agg_gbs,
         "stage_us_per_step": {k: round(v * 1e3, 2) for k, v in sorted(per_step.items())},
         "launch_mode": ("one CUDA graph per pool batch; build of batch i+1 on a side stream "
