@@ -427,31 +427,50 @@ k_dgrad(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ 
 // RGAT attention-vector partials over chunks of kCH rows of one relation:
 //   src (mode 0): P[c][h][w] = sum_u ds_src[u,h] Y[u,w]          rows = Y rows of r
 //   dst (mode 1): P[c][h][w] = sum_i ds_dst[(r,i),h] X_t(r)[i][w] rows = merged rows of r
-__global__ void __launch_bounds__(256)
+// Thread (h, w4) accumulates one float4 of the H x W outer-product sum; every
+// row is read once per block (coalesced float4 rows), 4 rows in flight.
+__global__ void __launch_bounds__(1024)
 k_att_partial(int R, int H, int W, int mode, const int* __restrict__ chunk_off,
               const int* __restrict__ row_off, const float* __restrict__ A,
               const float* __restrict__ B, ProjMeta pm, const int* __restrict__ gather_ids,
               float* __restrict__ partial) {
-  int c = blockIdx.x;
+  const int c = blockIdx.x;
   if (c >= chunk_off[R]) return;
-  int r = upper_bound_i(chunk_off, R + 1, c) - 1;
-  while (r > 0 && chunk_off[r] > c) r--;
+  const int r = upper_bound_i(chunk_off, R + 1, c) - 1;
   const int* ro = mode == 1 ? pm.rel_row_off : row_off;   // merged rows: host-known offsets
-  int first = ro[r] + (c - chunk_off[r]) * kCH;
-  int last = min(first + kCH, ro[r + 1]);
-  for (int o = threadIdx.x; o < H * W; o += blockDim.x) {
-    int h = o / W, w = o % W;
-    float s = 0.f;
-    for (int row = first; row < last; row++) {
-      long long brow = row;
-      if (mode == 1) {
-        int x = pm.type_src_off[pm.rel_dst[r]] + (row - pm.rel_row_off[r]);
-        brow = gather_ids ? (long long)gather_ids[x] : (long long)x;
-      }
-      s = fmaf(A[(long long)row * H + h], B[brow * W + w], s);
+  const int first = ro[r] + (c - chunk_off[r]) * kCH;
+  const int last = min(first + kCH, ro[r + 1]);
+  const int W4 = W / 4;
+  const int h = threadIdx.x / W4, w4 = threadIdx.x % W4;
+  if (h >= H) return;
+  auto brow = [&](int row) -> long long {
+    if (mode == 0) return row;
+    const int x = pm.type_src_off[pm.rel_dst[r]] + (row - pm.rel_row_off[r]);
+    return gather_ids ? (long long)gather_ids[x] : (long long)x;
+  };
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int row = first;
+  for (; row + 4 <= last; row += 4) {
+    float a[4];
+    float4 bv[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      a[q] = __ldg(A + (long long)(row + q) * H + h);
+      bv[q] = __ldg(reinterpret_cast<const float4*>(B + brow(row + q) * W) + w4);
     }
-    partial[((long long)c * H + h) * W + w] = s;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      acc.x = fmaf(a[q], bv[q].x, acc.x); acc.y = fmaf(a[q], bv[q].y, acc.y);
+      acc.z = fmaf(a[q], bv[q].z, acc.z); acc.w = fmaf(a[q], bv[q].w, acc.w);
+    }
   }
+  for (; row < last; row++) {
+    const float a = __ldg(A + (long long)row * H + h);
+    const float4 bv = __ldg(reinterpret_cast<const float4*>(B + brow(row) * W) + w4);
+    acc.x = fmaf(a, bv.x, acc.x); acc.y = fmaf(a, bv.y, acc.y);
+    acc.z = fmaf(a, bv.z, acc.z); acc.w = fmaf(a, bv.w, acc.w);
+  }
+  reinterpret_cast<float4*>(partial + ((long long)c * H + h) * W)[w4] = acc;
 }
 
 __global__ void k_att_chunks(int R, const int* __restrict__ row_off, ProjMeta pm,
@@ -466,40 +485,47 @@ __global__ void k_att_chunks(int R, const int* __restrict__ row_off, ProjMeta pm
   chunk_off[R] = acc;
 }
 
-// Final RGAT parameter gradients.  Per relation r, head h:
-//   datt[r,0,hc] = sum_chunks Psrc[h][hc]
-//   dv[h][k]     = sum_chunks Pdst[h][k]
-//   dW_r[k,hc]  += dv[h][k] a_dst[r,h,c]
-//   datt[r,1,hc] = sum_k W_r[k,hc] dv[h][k]
-__global__ void k_att_final(int R, int K, int D, int H, const int* __restrict__ src_chunk,
-                            const int* __restrict__ dst_chunk, const float* __restrict__ Psrc,
-                            const float* __restrict__ Pdst, const float* __restrict__ W_rel,
-                            const float* __restrict__ att, float* __restrict__ dW_rel,
-                            float* __restrict__ datt, float* __restrict__ dv_out) {
-  int r = blockIdx.x;
-  int dh = D / H;
-  extern __shared__ float dv[];   // [H][K]
-  for (int o = threadIdx.x; o < H * K; o += blockDim.x) {
-    float s = 0.f;
-    for (int c = dst_chunk[r]; c < dst_chunk[r + 1]; c++) s += Pdst[(long long)c * H * K + o];
-    dv[o] = s;
-    if (dv_out) dv_out[(long long)r * H * K + o] = s;
-  }
-  __syncthreads();
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    int h = d / dh;
-    float s = 0.f;
-    for (int c = src_chunk[r]; c < src_chunk[r + 1]; c++) s += Psrc[((long long)c * H + h) * D + d];
-    datt[(long long)r * 2 * D + d] = s;
-    float a = att[(long long)r * 2 * D + D + d];
-    float t = 0.f;
-    for (int k = 0; k < K; k++) {
-      float dvk = dv[h * K + k];
-      dW_rel[((long long)r * K + k) * D + d] += dvk * a;
-      t = fmaf(W_rel[((long long)r * K + k) * D + d], dvk, t);
-    }
-    datt[(long long)r * 2 * D + D + d] = t;
-  }
+// Final RGAT parameter gradients (three fully parallel kernels).  Per
+// relation r, head h:
+//   dv[r][h][k]  = sum_chunks Pdst[h][k]                       (k_att_dv)
+//   dW_r[k,hc]  += dv[h][k] a_dst[r,h,c]                        (k_att_dw)
+//   datt[r,0,hc] = sum_chunks Psrc[h][hc];
+//   datt[r,1,hc] = sum_k W_r[k,hc] dv[h][k]                      (k_att_da)
+__global__ void k_att_dv(int R, int K, int H, const int* __restrict__ dst_chunk,
+                         const float* __restrict__ Pdst, float* __restrict__ dv) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * H * K) return;
+  const int r = idx / (H * K), o = idx % (H * K);
+  float s = 0.f;
+  for (int c = dst_chunk[r]; c < dst_chunk[r + 1]; c++) s += Pdst[(long long)c * H * K + o];
+  dv[idx] = s;
+}
+
+__global__ void k_att_dw(int R, int K, int D, int H, const float* __restrict__ dv,
+                         const float* __restrict__ att, float* __restrict__ dW_rel) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)R * K * D) return;
+  const int d = (int)(idx % D), k = (int)((idx / D) % K), r = (int)(idx / ((long long)K * D));
+  const int h = d / (D / H);
+  dW_rel[idx] += dv[((long long)r * H + h) * K + k] * att[(long long)r * 2 * D + D + d];
+}
+
+__global__ void k_att_da(int R, int K, int D, int H, const int* __restrict__ src_chunk,
+                         const float* __restrict__ Psrc, const float* __restrict__ dv,
+                         const float* __restrict__ W_rel, float* __restrict__ datt) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * D) return;
+  const int r = idx / D, d = idx % D, h = d / (D / H);
+  float s = 0.f;
+  for (int c = src_chunk[r]; c < src_chunk[r + 1]; c++) s += Psrc[((long long)c * H + h) * D + d];
+  datt[(long long)r * 2 * D + d] = s;
+  float t[4] = {0.f, 0.f, 0.f, 0.f};
+  const float* w = W_rel + (long long)r * K * D + d;
+  const float* v = dv + ((long long)r * H + h) * K;
+  for (int k = 0; k < K; k += 4)
+#pragma unroll
+    for (int q = 0; q < 4; q++) t[q] = fmaf(w[(long long)(k + q) * D], v[k + q], t[q]);
+  datt[(long long)r * 2 * D + D + d] = (t[0] + t[1]) + (t[2] + t[3]);
 }
 
 // dX_t[i] += sum_{r: t(r)=t} sum_h ds_dst[(r,i),h] v[r][:,h]   (s_dst chain);
@@ -657,7 +683,7 @@ size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D
   long long chunks = proj_max_tiles(m, kCH < 128 ? kCH : 128);
   size_t b = 2 * carve_bytes(m.R + m.T + 1, 4);
   b += carve_bytes(chunks * K * D, 4);                       // wgrad partials
-  b += carve_bytes((long long)m.R * K * H, 4);               // v
+  b += carve_bytes((long long)m.R * K * H * 2, 4);           // v, dv
   b += 2 * carve_bytes(m.R + 1, 4);                          // att chunk tables
   long long U_max = m.N < m.S ? m.N : m.S;
   long long ach = U_max / kCH + m.rows / kCH + 2 * m.R + 2;
@@ -697,7 +723,7 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   int* tile_off = carve<int>(p, m.R + m.T + 1);
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
   float* partial = carve<float>(p, chunks * K * D);
-  float* v = carve<float>(p, (long long)m.R * K * H);
+  float* v = carve<float>(p, (long long)m.R * K * H * 2);
   int* src_chunk = carve<int>(p, m.R + 1);
   int* dst_chunk = carve<int>(p, m.R + 1);
   long long U_max = m.N < m.S ? m.N : m.S;
@@ -736,12 +762,17 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
     HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, (const int*)nullptr, pm, dst_chunk);
     unsigned gs = (unsigned)(U_max / kCH + m.R + 1);
     unsigned gdst = (unsigned)(m.rows / kCH + m.R + 1);
-    HF_LAUNCH(k_att_partial, gs, 256, 0, s, m.R, H, D, 0, src_chunk, csr->rel_y_off, d_ds_src,
-              d_Y, pm, d_gather_ids, Psrc);
-    HF_LAUNCH(k_att_partial, gdst, 256, 0, s, m.R, H, K, 1, dst_chunk, (const int*)nullptr, d_ds_dst, d_X,
-              pm, d_gather_ids, Pdst);
-    HF_LAUNCH(k_att_final, m.R, 256, H * K * sizeof(float), s, m.R, K, D, H, src_chunk, dst_chunk,
-              Psrc, Pdst, d_W_rel, d_att, d_dW_rel, d_datt, (float*)nullptr);
+    HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, s, m.R, H, D, 0, src_chunk, csr->rel_y_off,
+              d_ds_src, d_Y, pm, d_gather_ids, Psrc);
+    HF_LAUNCH(k_att_partial, gdst, H * K / 4, 0, s, m.R, H, K, 1, dst_chunk, (const int*)nullptr,
+              d_ds_dst, d_X, pm, d_gather_ids, Pdst);
+    float* dvb = v + (long long)m.R * K * H;     // dv [R][H][K] after v in the workspace
+    HF_LAUNCH(k_att_dv, ceil_div((long long)m.R * H * K, 256), 256, 0, s, m.R, K, H, dst_chunk,
+              Pdst, dvb);
+    HF_LAUNCH(k_att_dw, ceil_div((long long)m.R * K * D, 256), 256, 0, s, m.R, K, D, H, dvb, d_att,
+              d_dW_rel);
+    HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, s, m.R, K, D, H, src_chunk, Psrc,
+              dvb, d_W_rel, d_datt);
   }
   if (d_dX) {
     DgradMeta dm;
