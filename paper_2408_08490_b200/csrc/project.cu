@@ -429,17 +429,41 @@ k_dgrad(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ 
 //   dst (mode 1): P[c][h][w] = sum_i ds_dst[(r,i),h] X_t(r)[i][w] rows = merged rows of r
 // Thread (h, w4) accumulates one float4 of the H x W outer-product sum; every
 // row is read once per block (coalesced float4 rows), 4 rows in flight.
+static constexpr int kCHA = 32;    // attention-gradient chunk rows
+
+// chunk table of kCHA-row chunks per relation into shared memory (warp 0)
+__device__ __forceinline__ void att_chunk_table(int R, const int* ro, int* s_tab) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  int carry = 0;
+  for (int base = 0; base < R; base += 32) {
+    const int r = base + lane;
+    const int t = r < R ? (ro[r + 1] - ro[r] + kCHA - 1) / kCHA : 0;
+    int inc = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += n;
+    }
+    if (r < R) s_tab[r] = carry + inc - t;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) s_tab[R] = carry;
+}
+
 __global__ void __launch_bounds__(1024)
-k_att_partial(int R, int H, int W, int mode, const int* __restrict__ chunk_off,
+k_att_partial(int R, int H, int W, int mode, const int* __restrict__ unused,
               const int* __restrict__ row_off, const float* __restrict__ A,
               const float* __restrict__ B, ProjMeta pm, const int* __restrict__ gather_ids,
               float* __restrict__ partial) {
-  const int c = blockIdx.x;
-  if (c >= chunk_off[R]) return;
-  const int r = upper_bound_i(chunk_off, R + 1, c) - 1;
+  __shared__ int s_tab[HF_MAX_R + 1];
   const int* ro = mode == 1 ? pm.rel_row_off : row_off;   // merged rows: host-known offsets
-  const int first = ro[r] + (c - chunk_off[r]) * kCH;
-  const int last = min(first + kCH, ro[r + 1]);
+  att_chunk_table(R, ro, s_tab);
+  __syncthreads();
+  const int c = blockIdx.x;
+  if (c >= s_tab[R]) return;
+  const int r = upper_bound_i(s_tab, R + 1, c) - 1;
+  const int first = ro[r] + (c - s_tab[r]) * kCHA;
+  const int last = min(first + kCHA, ro[r + 1]);
   const int W4 = W / 4;
   const int h = threadIdx.x / W4, w4 = threadIdx.x % W4;
   if (h >= H) return;
@@ -450,16 +474,16 @@ k_att_partial(int R, int H, int W, int mode, const int* __restrict__ chunk_off,
   };
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   int row = first;
-  for (; row + 4 <= last; row += 4) {
-    float a[4];
-    float4 bv[4];
+  for (; row + 8 <= last; row += 8) {
+    float a[8];
+    float4 bv[8];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
+    for (int q = 0; q < 8; q++) {
       a[q] = __ldg(A + (long long)(row + q) * H + h);
       bv[q] = __ldg(reinterpret_cast<const float4*>(B + brow(row + q) * W) + w4);
     }
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
+    for (int q = 0; q < 8; q++) {
       acc.x = fmaf(a[q], bv[q].x, acc.x); acc.y = fmaf(a[q], bv[q].y, acc.y);
       acc.z = fmaf(a[q], bv[q].z, acc.z); acc.w = fmaf(a[q], bv[q].w, acc.w);
     }
@@ -491,14 +515,22 @@ __global__ void k_att_chunks(int R, const int* __restrict__ row_off, ProjMeta pm
 //   dW_r[k,hc]  += dv[h][k] a_dst[r,h,c]                        (k_att_dw)
 //   datt[r,0,hc] = sum_chunks Psrc[h][hc];
 //   datt[r,1,hc] = sum_k W_r[k,hc] dv[h][k]                      (k_att_da)
-__global__ void k_att_dv(int R, int K, int H, const int* __restrict__ dst_chunk,
-                         const float* __restrict__ Pdst, float* __restrict__ dv) {
+__global__ void k_att_dv(int R, int K, int H, ProjMeta pm, const float* __restrict__ Pdst,
+                         float* __restrict__ dv) {
+  __shared__ int s_tab[HF_MAX_R + 1];
+  att_chunk_table(R, pm.rel_row_off, s_tab);
+  __syncthreads();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= R * H * K) return;
   const int r = idx / (H * K), o = idx % (H * K);
-  float s = 0.f;
-  for (int c = dst_chunk[r]; c < dst_chunk[r + 1]; c++) s += Pdst[(long long)c * H * K + o];
-  dv[idx] = s;
+  float t[4] = {0.f, 0.f, 0.f, 0.f};
+  const int c0 = s_tab[r], c1 = s_tab[r + 1];
+  int c = c0;
+  for (; c + 4 <= c1; c += 4)
+#pragma unroll
+    for (int q = 0; q < 4; q++) t[q] += Pdst[(long long)(c + q) * H * K + o];
+  for (; c < c1; c++) t[0] += Pdst[(long long)c * H * K + o];
+  dv[idx] = (t[0] + t[1]) + (t[2] + t[3]);
 }
 
 __global__ void k_att_dw(int R, int K, int D, int H, const float* __restrict__ dv,
@@ -510,15 +542,23 @@ __global__ void k_att_dw(int R, int K, int D, int H, const float* __restrict__ d
   dW_rel[idx] += dv[((long long)r * H + h) * K + k] * att[(long long)r * 2 * D + D + d];
 }
 
-__global__ void k_att_da(int R, int K, int D, int H, const int* __restrict__ src_chunk,
+__global__ void k_att_da(int R, int K, int D, int H, const int* __restrict__ rel_y_off,
                          const float* __restrict__ Psrc, const float* __restrict__ dv,
                          const float* __restrict__ W_rel, float* __restrict__ datt) {
+  __shared__ int s_tab[HF_MAX_R + 1];
+  att_chunk_table(R, rel_y_off, s_tab);
+  __syncthreads();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= R * D) return;
   const int r = idx / D, d = idx % D, h = d / (D / H);
-  float s = 0.f;
-  for (int c = src_chunk[r]; c < src_chunk[r + 1]; c++) s += Psrc[((long long)c * H + h) * D + d];
-  datt[(long long)r * 2 * D + d] = s;
+  float u4[4] = {0.f, 0.f, 0.f, 0.f};
+  const int c0 = s_tab[r], c1 = s_tab[r + 1];
+  int c = c0;
+  for (; c + 4 <= c1; c += 4)
+#pragma unroll
+    for (int q = 0; q < 4; q++) u4[q] += Psrc[((long long)(c + q) * H + h) * D + d];
+  for (; c < c1; c++) u4[0] += Psrc[((long long)c * H + h) * D + d];
+  datt[(long long)r * 2 * D + d] = (u4[0] + u4[1]) + (u4[2] + u4[3]);
   float t[4] = {0.f, 0.f, 0.f, 0.f};
   const float* w = W_rel + (long long)r * K * D + d;
   const float* v = dv + ((long long)r * H + h) * K;
@@ -686,7 +726,7 @@ size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D
   b += carve_bytes((long long)m.R * K * H * 2, 4);           // v, dv
   b += 2 * carve_bytes(m.R + 1, 4);                          // att chunk tables
   long long U_max = m.N < m.S ? m.N : m.S;
-  long long ach = U_max / kCH + m.rows / kCH + 2 * m.R + 2;
+  long long ach = U_max / 32 + m.rows / 32 + 2 * m.R + 2;
   b += carve_bytes(ach * H * (K > D ? K : D), 4) * 2;        // att partials
   b += carve_bytes(m.R + 1, 4);                              // host row table copy
   return b;
@@ -727,7 +767,7 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   int* src_chunk = carve<int>(p, m.R + 1);
   int* dst_chunk = carve<int>(p, m.R + 1);
   long long U_max = m.N < m.S ? m.N : m.S;
-  long long ach = U_max / kCH + m.rows / kCH + 2 * m.R + 2;
+  long long ach = U_max / kCHA + m.rows / kCHA + 2 * m.R + 2;
   float* Psrc = carve<float>(p, ach * H * (K > D ? K : D));
   float* Pdst = carve<float>(p, ach * H * (K > D ? K : D));
   if (d_att) {
@@ -758,21 +798,18 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   if (d_att) {
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, s, m.R, K, D, H, d_W_rel,
               d_att, v);
-    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, csr->rel_y_off, pm, src_chunk);
-    HF_LAUNCH(k_att_chunks, 1, 32, 0, s, m.R, (const int*)nullptr, pm, dst_chunk);
-    unsigned gs = (unsigned)(U_max / kCH + m.R + 1);
-    unsigned gdst = (unsigned)(m.rows / kCH + m.R + 1);
-    HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, s, m.R, H, D, 0, src_chunk, csr->rel_y_off,
-              d_ds_src, d_Y, pm, d_gather_ids, Psrc);
-    HF_LAUNCH(k_att_partial, gdst, H * K / 4, 0, s, m.R, H, K, 1, dst_chunk, (const int*)nullptr,
-              d_ds_dst, d_X, pm, d_gather_ids, Pdst);
+    const unsigned gs = (unsigned)(U_max / kCHA + m.R + 1);
+    const unsigned gdst = (unsigned)(m.rows / kCHA + m.R + 1);
+    HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, s, m.R, H, D, 0, (const int*)nullptr,
+              csr->rel_y_off, d_ds_src, d_Y, pm, d_gather_ids, Psrc);
+    HF_LAUNCH(k_att_partial, gdst, H * K / 4, 0, s, m.R, H, K, 1, (const int*)nullptr,
+              (const int*)nullptr, d_ds_dst, d_X, pm, d_gather_ids, Pdst);
     float* dvb = v + (long long)m.R * K * H;     // dv [R][H][K] after v in the workspace
-    HF_LAUNCH(k_att_dv, ceil_div((long long)m.R * H * K, 256), 256, 0, s, m.R, K, H, dst_chunk,
-              Pdst, dvb);
+    HF_LAUNCH(k_att_dv, ceil_div((long long)m.R * H * K, 256), 256, 0, s, m.R, K, H, pm, Pdst, dvb);
     HF_LAUNCH(k_att_dw, ceil_div((long long)m.R * K * D, 256), 256, 0, s, m.R, K, D, H, dvb, d_att,
               d_dW_rel);
-    HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, s, m.R, K, D, H, src_chunk, Psrc,
-              dvb, d_W_rel, d_datt);
+    HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, s, m.R, K, D, H, csr->rel_y_off,
+              Psrc, dvb, d_W_rel, d_datt);
   }
   if (d_dX) {
     DgradMeta dm;
