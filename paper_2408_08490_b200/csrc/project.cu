@@ -175,47 +175,47 @@ __global__ void k_scores_src(int R, int D, int H, const int* __restrict__ U_dev,
   }
 }
 
-// s_dst[(r,i),h] = <X_{t(r)}[i], v[r][:,h]>, one warp per merged row.
-__global__ void k_scores_dst(ProjMeta pm, int K, int H, const int* __restrict__ gather_ids,
-                             const float* __restrict__ X, const float* __restrict__ v,
-                             float* __restrict__ s_dst) {
-  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  int lane = threadIdx.x & 31;
-  if (row >= pm.rows) return;
-  int r = upper_bound_i(pm.rel_row_off, pm.R + 1, row) - 1;
-  int t = pm.rel_dst[r];
-  int x = pm.type_src_off[t] + (row - pm.rel_row_off[r]);
-  long long xr = gather_ids ? (long long)gather_ids[x] : (long long)x;
-  float acc[HIFUSE_MAX_HEADS];
-  for (int h = 0; h < H; h++) acc[h] = 0.f;
-  for (int k = lane; k < K; k += 32) {
-    float xv = X[xr * K + k];
-    const float* vr = v + ((long long)r * K + k) * H;
-    for (int h = 0; h < H; h++) acc[h] = fmaf(xv, vr[h], acc[h]);
-  }
-  for (int h = 0; h < H; h++) {
-    float s = acc[h];
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) s_dst[(long long)row * H + h] = s;
-  }
+// s_dst[(r,i),h] = <X_{t(r)}[i], v[r][:,h]>: thread (row, h), H threads per
+// merged row share the row's X loads (broadcast); v[r] is [K][H] (coalesced).
+__global__ void __launch_bounds__(256)
+k_scores_dst(ProjMeta pm, int K, int H, const int* __restrict__ gather_ids,
+             const float* __restrict__ X, const float* __restrict__ v,
+             float* __restrict__ s_dst) {
+  const int rpb = blockDim.x / H;
+  const int row = blockIdx.x * rpb + threadIdx.x / H, h = threadIdx.x % H;
+  if (row >= pm.rows || threadIdx.x >= rpb * H) return;
+  const int r = upper_bound_i(pm.rel_row_off, pm.R + 1, row) - 1;
+  const int t = pm.rel_dst[r];
+  const int x = pm.type_src_off[t] + (row - pm.rel_row_off[r]);
+  const long long xr = gather_ids ? (long long)gather_ids[x] : (long long)x;
+  const float* xp = X + xr * K;
+  const float* vp = v + (long long)r * K * H + h;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < K; k += 4)
+#pragma unroll
+    for (int q = 0; q < 4; q++) acc[q] = fmaf(__ldg(xp + k + q), __ldg(vp + (long long)(k + q) * H), acc[q]);
+  s_dst[(long long)row * H + h] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // ------------------------------------------------------------- backward ----
-// dYt = dY + ds_src (x) a_src  (score chain), in place, one warp per Y row.
-__global__ void k_dy_score(int R, int D, int H, const int* __restrict__ U_dev,
-                           const int* __restrict__ rel_y_off, const float* __restrict__ att,
-                           const float* __restrict__ ds_src, float* __restrict__ dY) {
+// dYt = dY + ds_src (x) a_src  (score chain), in place, one thread per float4.
+__global__ void __launch_bounds__(256)
+k_dy_score(int R, int D, int H, const int* __restrict__ U_dev, const int* __restrict__ rel_y_off,
+           const float* __restrict__ att, const float* __restrict__ ds_src, float4* __restrict__ dY) {
   __shared__ int s_yoff[HF_MAX_R + 1];
   for (int i = threadIdx.x; i <= R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
   __syncthreads();
-  int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  int lane = threadIdx.x & 31;
+  const int D4 = D / 4;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int u = (int)(idx / D4), c4 = (int)(idx % D4);
   if (u >= *U_dev) return;
-  int r = upper_bound_i(s_yoff, R + 1, u) - 1;
-  const float* a = att + (long long)r * 2 * D;
-  int dh = D / H;
-  for (int c = lane; c < D; c += 32)
-    dY[(long long)u * D + c] += ds_src[(long long)u * H + c / dh] * a[c];
+  const int r = upper_bound_i(s_yoff, R + 1, u) - 1;
+  const int dh = D / H, h = (c4 * 4) / dh;
+  const float g = ds_src[(long long)u * H + h];
+  const float4 a = __ldg(reinterpret_cast<const float4*>(att + (long long)r * 2 * D) + c4);
+  float4 y = dY[idx];
+  y.x = fmaf(g, a.x, y.x); y.y = fmaf(g, a.y, y.y); y.z = fmaf(g, a.z, y.z); y.w = fmaf(g, a.w, y.w);
+  dY[idx] = y;
 }
 
 // wgrad partials: chunk c of group g: P[c][k][d] = sum_{rows} A[row][k] B[row][d]
@@ -688,7 +688,8 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
   float* v = carve<float>(p, (long long)m.R * K * (heads > 0 ? heads : 1));
   if (prec == HIFUSE_PREC_TF32) {
-    rc = project_tcp_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0, s);
+    rc = project_tcp_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0,
+                            d_att, d_s_src, heads, s);   // s_src fused in the epilogue
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
@@ -708,10 +709,11 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * heads, 256), 256, 0, s, m.R, K, D, heads,
               d_W_rel, d_att, v);
     long long U_max = m.N < m.S ? m.N : m.S;
+    if (prec != HIFUSE_PREC_TF32)
     HF_LAUNCH(k_scores_src, ceil_div(U_max, 8), 256, 0, s, m.R, D, heads, csr->U_dev,
               csr->rel_y_off, d_Y, d_att, d_s_src);
-    HF_LAUNCH(k_scores_dst, ceil_div(m.rows, 8), 256, 0, s, pm, K, heads, d_gather_ids, d_X, v,
-              d_s_dst);
+    HF_LAUNCH(k_scores_dst, ceil_div(m.rows, 256 / heads), 256, 0, s, pm, K, heads, d_gather_ids,
+              d_X, v, d_s_dst);
   }
   return last_cuda();
 }
@@ -771,8 +773,8 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   float* Psrc = carve<float>(p, ach * H * (K > D ? K : D));
   float* Pdst = carve<float>(p, ach * H * (K > D ? K : D));
   if (d_att) {
-    HF_LAUNCH(k_dy_score, ceil_div(U_max, 8), 256, 0, s, m.R, D, H, csr->U_dev, csr->rel_y_off,
-              d_att, d_ds_src, d_dY);
+    HF_LAUNCH(k_dy_score, ceil_div(U_max * (D / 4), 256), 256, 0, s, m.R, D, H, csr->U_dev,
+              csr->rel_y_off, d_att, d_ds_src, (float4*)d_dY);
   }
   int CH = kCH;
   if (prec == HIFUSE_PREC_TF32) {

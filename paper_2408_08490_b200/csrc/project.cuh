@@ -43,7 +43,7 @@ long long proj_max_tiles(const LayerMeta& m, int step);
 hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
                                  const hifuse_csr* csr, const float* X, const int* gather_ids,
                                  const float* W_rel, const float* W_root, float* Y, float* R0,
-                                 cudaStream_t s);
+                                 const float* att, float* s_src, int H, cudaStream_t s);
 // tcgen05 TF32 dgrad: dX[type s rows] = sum_terms A_term W_term^T (A = dYt rows
 // through slot_y, or G for the root term).  dm built with bm = 128.
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,

@@ -427,7 +427,8 @@ __global__ void __launch_bounds__(288, kFwdCtas)
 k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __restrict__ y_src,
                const int* __restrict__ gather_ids, const float* __restrict__ X,
                const float* __restrict__ W_rel, const float* __restrict__ W_root,
-               float* __restrict__ Y, float* __restrict__ R0) {
+               float* __restrict__ Y, float* __restrict__ R0, const float* __restrict__ att,
+               float* __restrict__ s_src, int H) {
   constexpr int BM = 128, NC = K / 32;
   constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
   constexpr uint32_t STAGE = A_STAGE + B_STAGE;
@@ -539,10 +540,43 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
       float* out = g < pm.R ? Y + (long long)s_yoff[g] * D
                             : R0 + (long long)pm.type_dst_off[g - pm.R] * D;
       float* st = stage_ep + q * (32 * 20);
+      // RGAT source scores fused here: s_src[u,h] = <Y[u, head h], a_src[r, head h]>
+      const bool scores = att != nullptr && g < pm.R;
+      const int dh = scores ? D / H : 0;
+      const float* asrc = scores ? att + (long long)g * 2 * D : nullptr;
+      float* srow = scores ? s_src + (long long)(s_yoff[g] + r0 + q * 32 + lane) * H : nullptr;
+      const bool row_ok = q * 32 + lane < nrows;
+      float sacc = 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 16) {
         float v[16];
         tmem_ld16(tmem + (uint32_t)(acc * D) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+        if (scores) {
+          float qs[4];
+#pragma unroll
+          for (int qq = 0; qq < 4; qq++) {
+            const float4 a4 = __ldg(reinterpret_cast<const float4*>(asrc + c0) + qq);
+            qs[qq] = v[4 * qq] * a4.x + v[4 * qq + 1] * a4.y + v[4 * qq + 2] * a4.z + v[4 * qq + 3] * a4.w;
+          }
+          if (row_ok) {
+            if (dh == 4) {
+#pragma unroll
+              for (int qq = 0; qq < 4; qq++) srow[c0 / 4 + qq] = qs[qq];
+            } else if (dh == 8) {
+              srow[c0 / 8] = qs[0] + qs[1];
+              srow[c0 / 8 + 1] = qs[2] + qs[3];
+            } else if (dh == 16) {
+              srow[c0 / 16] = (qs[0] + qs[1]) + (qs[2] + qs[3]);
+            }
+          }
+          if (dh >= 32) {
+            sacc += (qs[0] + qs[1]) + (qs[2] + qs[3]);
+            if ((c0 + 16) % dh == 0) {
+              if (row_ok) srow[c0 / dh] = sacc;
+              sacc = 0.f;
+            }
+          }
+        }
 #pragma unroll
         for (int jj = 0; jj < 4; jj++)
           *reinterpret_cast<float4*>(st + lane * 20 + 4 * jj) =
@@ -592,7 +626,7 @@ static constexpr int fwdp_smem() { return kFStages * (128 * 128 + D * 128) + 102
 template <int K, int D>
 static void launch_tcp(const ProjMeta& pm, const hifuse_csr* csr, const int* gather_ids,
                        const float* X, const float* W_rel, const float* W_root, float* Y,
-                       float* R0, cudaStream_t s) {
+                       float* R0, const float* att, float* s_src, int H, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_proj_fwd_tcp<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -600,18 +634,18 @@ static void launch_tcp(const ProjMeta& pm, const hifuse_csr* csr, const int* gat
     attr = true;
   }
   HF_LAUNCH((k_proj_fwd_tcp<K, D>), 148 * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
-            csr->rel_y_off, csr->y_src, gather_ids, X, W_rel, W_root, Y, R0);
+            csr->rel_y_off, csr->y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H);
 }
 
 hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
                                  const hifuse_csr* csr, const float* X, const int* gather_ids,
                                  const float* W_rel, const float* W_root, float* Y, float* R0,
-                                 cudaStream_t s) {
+                                 const float* att, float* s_src, int H, cudaStream_t s) {
   (void)m;
-  if (K == 128 && D == 128) launch_tcp<128, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
-  else if (K == 128 && D == 64) launch_tcp<128, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
-  else if (K == 64 && D == 128) launch_tcp<64, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
-  else launch_tcp<64, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, s);
+  if (K == 128 && D == 128) launch_tcp<128, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
+  else if (K == 128 && D == 64) launch_tcp<128, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
+  else if (K == 64 && D == 128) launch_tcp<64, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
+  else launch_tcp<64, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
   return HIFUSE_OK;
 }
 
