@@ -133,6 +133,14 @@ def stage_cost(stage, l, cfg, sz):
         m = s["U"] + (s["dst"] if root else 0)
         f = 2 * K * D * m * (2 if l > 0 else 1)
         return 4 * K * m + 4 * D * m + (4 * s["src"] * K if l > 0 else 0), f
+    if stage == "aggregate_features":     # aggregate-first input layer: A4 over raw X
+        return 4 * K * s["U"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
+    if stage == "project_aggregated":
+        m = s["rows"] + s["dst"]
+        return 4 * K * m + 4 * D * m + 4 * (R + T) * K * D, 2 * K * D * m
+    if stage == "project_aggregated_bwd":
+        m = s["rows"] + s["dst"]
+        return 4 * K * m + 4 * D * s["dst"] + 4 * (R + T) * K * D, 2 * K * D * m
     if stage == "fuse":
         return 4 * D * (s["rows"] + 2 * s["dst"]), 0
     if stage == "fuse_bwd":
@@ -148,7 +156,8 @@ def stage_cost(stage, l, cfg, sz):
 # main kernel of every library call (for the ncu traffic lookup)
 MAIN_KERNEL = {"aggregate_fwd": "k_agg_fwd", "aggregate_bwd": "k_agg_bwd_p", "project": "k_proj_fwd_tcp",
                "project_bwd": "k_wgrad_tc", "fuse": "k_fuse", "fuse_bwd": "k_fuse_bwd_chunks",
-               "build": "k_sort_long", "xent": "k_gemm_small"}
+               "build": "k_sort_long", "xent": "k_xent_rows", "aggregate_features": "k_agg_fwd",
+               "project_aggregated": "k_proj_fwd_tcp", "project_aggregated_bwd": "k_wgrad_tc"}
 
 
 def ncu_traffic(kernel, layer):
@@ -224,6 +233,7 @@ def config_obj(cfg, args, extra=None):
          "global_batch": cfg.batch_size * args.gpus, "fanout": list(cfg.fanout),
          "hidden": cfg.hidden, "heads": cfg.heads, "relations": cfg.num_rels,
          "parallelism": f"dp{args.gpus}", "precision": args.prec,
+         "order": getattr(args, "order", "project_first"),
          "l2": "inputs larger than L2: a pool of distinct sampled batches, per-step working "
                "set above the 126 MB L2 for mag"}
     if extra:
@@ -243,6 +253,9 @@ def main():
     ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--order", default="agg_first", choices=["project_first", "agg_first"],
+                    help="agg_first: the RGCN input layer aggregates raw features, then "
+                         "projects (exact by linearity; SURVEY §8(f) NEXT(3))")
     ap.add_argument("--pipeline", type=int, default=1,
                     help="1: overlap the next batch's semantic-graph build with this "
                          "batch's compute (side stream); 0: serial steps")
@@ -287,7 +300,7 @@ def main():
     et_d = torch.from_numpy(g.edge_type).to(dev)
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
-                 prec=args.prec)
+                 prec=args.prec, order=args.order)
     tr.load_params(params)
     allreduce = (lambda t: allreduce_grads(t, world)) if world > 1 else None
     # sizing pass: every pool batch once, eagerly (buffers reach final size)
@@ -392,6 +405,42 @@ def main():
     # restore a consistent state (stage replays repeat in-place updates)
     tr.load_params(params)
 
+    # the other layer-0 order of the same RGCN step, timed the same way (the
+    # north-star project-first path is always measured next to the faster
+    # aggregate-first one)
+    other = None
+    if cfg.model == "rgcn" and args.prec == "tf32":
+        other_order = "project_first" if tr.agg_first else "agg_first"
+        tr_main, graphs_main, serial_main = tr, graphs, serial_graphs
+        tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
+                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
+                     prec=args.prec, order=other_order)
+        tr.load_params(params)
+        for db in pool:
+            tr.step(db, feat_d, et_d, allreduce=allreduce, world=world, update=False)
+        torch.cuda.synchronize()
+        serial_graphs = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
+        graphs = serial_graphs
+        if args.pipeline:
+            graphs = [tr.capture_pipelined(db, pool[(i + 1) % len(pool)], feat_d, et_d, side,
+                                           update=(world == 1))
+                      for i, db in enumerate(pool)]
+            tr.build_op(pool[0], et_d)()
+        for i in range(args.warmup):
+            one_step(i)
+        ms_o, _, _ = timed(args.steps)
+        graphs_o = graphs
+        graphs = serial_graphs
+        for i in range(args.warmup):
+            one_step(i)
+        ms_os, _, _ = timed(args.steps)
+        other = {"order": other_order, "value": world * args.steps / (ms_o / 1e3),
+                 "ms_per_step": ms_o / args.steps, "serial_ms_per_step": ms_os / args.steps,
+                 "gpu_launches_per_step": graphs_o[0][1]}
+        del graphs_o, serial_graphs, graphs
+        tr, graphs, serial_graphs = tr_main, graphs_main, serial_main
+        tr.load_params(params)
+
     value = world * args.steps / (ms / 1e3)
     e2e_v = world * args.steps / (ms_e2e / 1e3)
     h2d = float(np.mean([pool[i % len(pool)].h2d_bytes() for i in range(args.steps)]))
@@ -407,10 +456,11 @@ def main():
         avg_bytes = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[0] for pi in used]))
         avg_flops = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[1] for pi in used]))
         t_s = per_step[stage_key] / 1e3
-        if name in ("project", "project_bwd") and args.prec == "fp32":
+        gemm = ("project", "project_bwd", "project_aggregated", "project_aggregated_bwd")
+        if name in gemm and args.prec == "fp32":
             roof = {"bound": "alu", "achieved": avg_flops / t_s / 1e12, "peak": ALU_FP32_TFLOPS,
                     "unit": "TFLOP/s"}
-        elif name in ("project", "project_bwd"):
+        elif name in gemm:
             bw_time = avg_bytes / (pk["hbm"] * 1e9)
             fl_time = avg_flops / (pk["bf16"] * TF32_OVER_BF16 * 1e12)
             if bw_time >= fl_time:
@@ -423,7 +473,7 @@ def main():
             roof = {"bound": "hbm", "achieved": avg_bytes / t_s / 1e9, "peak": pk["hbm"],
                     "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        bwd = name in ("aggregate_bwd", "project_bwd", "fuse_bwd")
+        bwd = name in ("aggregate_bwd", "project_bwd", "fuse_bwd", "project_aggregated_bwd")
         tr = None if name == "build" else ncu_traffic(MAIN_KERNEL.get(name, name),
                                                        cfg.num_layers - 1 - l if bwd else l)
         roof["traffic"] = tr
@@ -442,9 +492,9 @@ def main():
     build_roof = roofline_of("build") if "build" in per_step else None
     agg_gbs = {}
     for k in per_step:
-        if k.startswith("aggregate_fwd"):
-            ll = int(k.split(".")[1])
-            b = float(np.mean([stage_cost("aggregate_fwd", ll, cfg, sizes[pi])[0]
+        if k.startswith("aggregate_fwd") or k.startswith("aggregate_features"):
+            nm, ll = k.split(".")[0], int(k.split(".")[1])
+            b = float(np.mean([stage_cost(nm, ll, cfg, sizes[pi])[0]
                                for pi, _ in stage_ms[k]]))
             agg_gbs[k] = {"GB/s": b / (per_step[k] / 1e3) / 1e9, "us": per_step[k] * 1e3,
                           "frac_of_hbm": b / (per_step[k] / 1e3) / 1e9 / pk["hbm"]}
@@ -473,6 +523,7 @@ def main():
                         "overlaps compute of batch i" if graphs is not serial_graphs else
                         "one CUDA graph per pool batch (whole step, serial)"),
         "serial_ms_per_step": ms_serial / args.steps,
+        "other_order": other,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))

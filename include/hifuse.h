@@ -110,7 +110,9 @@ typedef struct {
  * n_src(src type of r') + j.  CSC over Y rows: col_ptr, csc_pos (CSR
  * position, ascending inside a column), csc_row (merged row of that
  * position).  Entries past the valid count are -1; col_ptr entries past U
- * equal the number of valid edges. */
+ * equal the number of valid edges.  The CSC is optional: col_ptr, csc_pos and
+ * csc_row all NULL skip the transpose (a layer whose aggregation backward is
+ * never run, e.g. the input layer of the aggregate-first RGCN). */
 typedef struct {
   int32_t *rel_row_off;  /* [R+1]      */
   int32_t *row_ptr;      /* [rows+1]   */
@@ -232,6 +234,44 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape *shape, const hifuse_c
                                  const float *d_ds_src, const float *d_ds_dst, float *d_dX,
                                  float *d_dW_rel, float *d_dW_root, float *d_datt,
                                  void *d_ws, size_t ws_bytes, hifuse_stream_t stream);
+
+/* Aggregate-first RGCN input layer.
+ * The RGCN message is linear, so Z_r = A_r (X W_r) = (A_r X) W_r exactly: the
+ * paper's stages 2-3 (projection, aggregation) may
+ * run in the other order.  For the input layer this projects rho aggregated
+ * rows instead of U compact source rows and needs no transpose SpMM.
+ *
+ * hifuse_aggregate_features_fwd: Alg. 1's merged Aggregate over the RAW
+ *   features, Xagg[(r,i)] = sum (SUM) or mean (MEAN) over the row's edges of
+ *   X[x(e)], x(e) = gather_ids[type_src_off[s(r)] + src_local(e)] (gather_ids
+ *   NULL: identity).  Xagg [rows, K]; empty rows 0.  Same kernel as A4.
+ *   Workspace: hifuse_aggregate_features_ws_bytes() (N ints).
+ * hifuse_project_aggregated: Z[(r,i)] = Xagg[(r,i)] W_r (per-relation groups
+ *   over rel_row_off), R0_t = X_t[dst prefix] W_root_t (X gathered through
+ *   gather_ids).  tcgen05 TF32 only.
+ * hifuse_project_aggregated_bwd: dW_r = sum_i Xagg[(r,i)]^T G_t(r)[i],
+ *   dW_root_t = sum_i X_t[i]^T G_t[i] (G from hifuse_semantic_fuse_bwd);
+ *   no dX (input layer).  Fixed-order chunk reduction.  Workspace:
+ *   hifuse_project_aggregated_bwd_ws_bytes(). */
+size_t hifuse_aggregate_features_ws_bytes(const hifuse_layer_shape *shape);
+hifuse_status hifuse_aggregate_features_fwd(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                            hifuse_agg agg, int K, const float *d_X,
+                                            int64_t x_rows, const int32_t *d_gather_ids,
+                                            float *d_Xagg, void *d_ws, size_t ws_bytes,
+                                            hifuse_stream_t stream);
+hifuse_status hifuse_project_aggregated(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                        hifuse_prec prec, int K, int D, const float *d_Xagg,
+                                        const float *d_X, int64_t x_rows,
+                                        const int32_t *d_gather_ids, const float *d_W_rel,
+                                        const float *d_W_root, float *d_Z, float *d_R0,
+                                        hifuse_stream_t stream);
+size_t hifuse_project_aggregated_bwd_ws_bytes(const hifuse_layer_shape *shape, int K, int D);
+hifuse_status hifuse_project_aggregated_bwd(const hifuse_layer_shape *shape,
+                                            const hifuse_csr *csr, hifuse_prec prec, int K, int D,
+                                            const float *d_Xagg, const float *d_X, int64_t x_rows,
+                                            const int32_t *d_gather_ids, const float *d_G,
+                                            float *d_dW_rel, float *d_dW_root, void *d_ws,
+                                            size_t ws_bytes, hifuse_stream_t stream);
 
 /* Training-step helpers outside the paper's four stages:
  * linear classifier + mean softmax cross-entropy on the seed rows, its

@@ -209,3 +209,38 @@ def project_bwd(shape: Shape, csr, K, D, H, X, gather_ids, W_rel, W_root, att, Y
         _p(pad(G, D)), _p(pad(ds_src, H)), _p(pad(ds_dst, H)),
         _p(dX), ctypes.c_int64(X.shape[0]), _p(dW_rel), _p(dW_root), _p(datt))
     return dict(dX=dX, dW_rel=dW_rel, dW_root=dW_root, datt=datt)
+
+
+def aggregate_features(shape: Shape, blk, edge_type, agg, K, X, gather_ids):
+    """O6a: Alg. 1 over the raw features (aggregate-first input layer)."""
+    Xagg = np.zeros((max(shape.rows, 1), K))
+    gid = None if gather_ids is None else _i32(gather_ids)
+    lib().oracle_aggregate_features(
+        *shape.head(), ctypes.c_int64(shape.N), _p(_i32(blk.src_local)), _p(_i32(blk.dst_local)),
+        _p(np.ascontiguousarray(blk.edge_id, np.int64)), _p(_i32(edge_type)),
+        ctypes.c_int64(len(edge_type)), AGG[agg], K, _p(_f64(X)), _p(gid), _p(Xagg))
+    return Xagg[:shape.rows]
+
+
+def project_aggregated(shape: Shape, K, D, Xagg, X, gather_ids, W_rel, W_root):
+    """O6b: Z[(r,i)] = Xagg[(r,i)] W_r, R0_t = X_t W_root,t."""
+    Z = np.zeros((max(shape.rows, 1), D))
+    R0 = np.zeros((max(shape.dst_rows, 1), D)) if W_root is not None else None
+    gid = None if gather_ids is None else _i32(gather_ids)
+    pad = lambda a, w: _f64(a) if len(a) else np.zeros((1, w))
+    lib().oracle_project_aggregated(
+        shape.T, shape.R, _p(shape.rel_dst), _p(shape.n_src), _p(shape.n_dst), K, D,
+        _p(pad(Xagg, K)), _p(_f64(X)), _p(gid), _p(_f64(W_rel)), _p(_f64(W_root)), _p(Z), _p(R0))
+    return dict(Z=Z[:shape.rows], R0=None if R0 is None else R0[:shape.dst_rows])
+
+
+def project_aggregated_bwd(shape: Shape, K, D, Xagg, X, gather_ids, G, root=True):
+    """O6c: adjoint of O6b for the weights (no dX: input layer)."""
+    dW_rel = np.zeros((shape.R, K, D))
+    dW_root = np.zeros((shape.T, K, D)) if root else None
+    gid = None if gather_ids is None else _i32(gather_ids)
+    pad = lambda a, w: _f64(a) if len(a) else np.zeros((1, w))
+    lib().oracle_project_aggregated_bwd(
+        shape.T, shape.R, _p(shape.rel_dst), _p(shape.n_src), _p(shape.n_dst), K, D,
+        _p(pad(Xagg, K)), _p(_f64(X)), _p(gid), _p(pad(G, D)), _p(dW_rel), _p(dW_root))
+    return dict(dW_rel=dW_rel, dW_root=dW_root)

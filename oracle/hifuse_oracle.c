@@ -571,3 +571,121 @@ void oracle_project_bwd(int T, int R, const int32_t *rel_src, const int32_t *rel
     }
     free(dyt); free(tso); free(tdo);
 }
+
+/* ------------------------------------------------------------------------ */
+/* O6. Aggregate-first RGCN input layer (DESIGN.md  */
+/* §9).  Alg. 1 applied to the RAW features, relation by        */
+/* relation: Xagg[(r,i)] = sum (mean: / |segment|) over the segment of       */
+/* X_s(r)[src e]; then the projection of P:L119 on the aggregated rows,      */
+/* Z[(r,i)] = Xagg[(r,i)] W_r, and the root term R0_t = X_t W_root,t.  By    */
+/* linearity Z equals O3(O2(X)) -- tests/test_oracle_aggfirst.py pins that.  */
+/* ------------------------------------------------------------------------ */
+void oracle_aggregate_features(int T, int R, const int32_t *rel_src, const int32_t *rel_dst,
+                               const int32_t *n_src, const int32_t *n_dst,
+                               int64_t N, const int32_t *src, const int32_t *dst,
+                               const int64_t *eid, const int32_t *edge_type, int64_t E,
+                               int agg, int K, const double *X, const int32_t *gather_ids,
+                               double *Xagg)
+{
+    int64_t *tso = (int64_t *)malloc(sizeof(int64_t) * (T + 1));
+    tso[0] = 0;
+    for (int t = 0; t < T; t++) tso[t + 1] = tso[t] + n_src[t];
+    int64_t row0 = 0;
+    for (int r = 0; r < R; r++) {
+        int64_t *ptr, *list;
+        relation_rows(R, rel_src, rel_dst, n_src, n_dst, r, N, src, dst, eid, edge_type, E, &ptr, &list);
+        for (int32_t i = 0; i < n_dst[rel_dst[r]]; i++) {
+            double *z = Xagg + (row0 + i) * K;
+            for (int k = 0; k < K; k++) z[k] = 0.0;
+            for (int64_t q = ptr[i]; q < ptr[i + 1]; q++) {
+                const double *x = xrow(X, K, gather_ids, tso, rel_src[r], src[list[q]]);
+                for (int k = 0; k < K; k++) z[k] += x[k];
+            }
+            double deg = (double)(ptr[i + 1] - ptr[i]);
+            if (agg == 1 && deg > 0)
+                for (int k = 0; k < K; k++) z[k] /= deg;
+        }
+        row0 += n_dst[rel_dst[r]];
+        free(ptr); free(list);
+    }
+    free(tso);
+}
+
+void oracle_project_aggregated(int T, int R, const int32_t *rel_dst, const int32_t *n_src,
+                               const int32_t *n_dst, int K, int D, const double *Xagg,
+                               const double *X, const int32_t *gather_ids,
+                               const double *W_rel, const double *W_root, double *Z, double *R0)
+{
+    int64_t *tso = (int64_t *)malloc(sizeof(int64_t) * (T + 1));
+    tso[0] = 0;
+    for (int t = 0; t < T; t++) tso[t + 1] = tso[t] + n_src[t];
+    int64_t row0 = 0;
+    for (int r = 0; r < R; r++) {
+        const double *W = W_rel + (int64_t)r * K * D;
+        for (int32_t i = 0; i < n_dst[rel_dst[r]]; i++) {
+            const double *x = Xagg + (row0 + i) * K;
+            double *z = Z + (row0 + i) * D;
+            for (int d = 0; d < D; d++) {
+                double s = 0.0;
+                for (int k = 0; k < K; k++) s += x[k] * W[(int64_t)k * D + d];
+                z[d] = s;
+            }
+        }
+        row0 += n_dst[rel_dst[r]];
+    }
+    if (W_root) {
+        int64_t o = 0;
+        for (int t = 0; t < T; t++) {
+            const double *W = W_root + (int64_t)t * K * D;
+            for (int32_t i = 0; i < n_dst[t]; i++) {
+                const double *x = xrow(X, K, gather_ids, tso, t, i);
+                for (int d = 0; d < D; d++) {
+                    double s = 0.0;
+                    for (int k = 0; k < K; k++) s += x[k] * W[(int64_t)k * D + d];
+                    R0[(o + i) * D + d] = s;
+                }
+            }
+            o += n_dst[t];
+        }
+    }
+    free(tso);
+}
+
+/* Adjoint: dW_r = sum_i Xagg[(r,i)]^T G_t(r)[i] (every Z row (r,i) feeds
+ * H_t(r)[i] through the fusion sum), dW_root,t = sum_i X_t[i]^T G_t[i]. */
+void oracle_project_aggregated_bwd(int T, int R, const int32_t *rel_dst, const int32_t *n_src,
+                                   const int32_t *n_dst, int K, int D, const double *Xagg,
+                                   const double *X, const int32_t *gather_ids, const double *G,
+                                   double *dW_rel, double *dW_root)
+{
+    int64_t *tso = (int64_t *)malloc(sizeof(int64_t) * (T + 1));
+    int64_t *tdo = (int64_t *)malloc(sizeof(int64_t) * (T + 1));
+    tso[0] = tdo[0] = 0;
+    for (int t = 0; t < T; t++) { tso[t + 1] = tso[t] + n_src[t]; tdo[t + 1] = tdo[t] + n_dst[t]; }
+    memset(dW_rel, 0, sizeof(double) * R * K * D);
+    int64_t row0 = 0;
+    for (int r = 0; r < R; r++) {
+        double *W = dW_rel + (int64_t)r * K * D;
+        int t = rel_dst[r];
+        for (int32_t i = 0; i < n_dst[t]; i++) {
+            const double *x = Xagg + (row0 + i) * K;
+            const double *g = G + (tdo[t] + i) * D;
+            for (int k = 0; k < K; k++)
+                for (int d = 0; d < D; d++) W[(int64_t)k * D + d] += x[k] * g[d];
+        }
+        row0 += n_dst[t];
+    }
+    if (dW_root) {
+        memset(dW_root, 0, sizeof(double) * T * K * D);
+        for (int t = 0; t < T; t++) {
+            double *W = dW_root + (int64_t)t * K * D;
+            for (int32_t i = 0; i < n_dst[t]; i++) {
+                const double *x = xrow(X, K, gather_ids, tso, t, i);
+                const double *g = G + (tdo[t] + i) * D;
+                for (int k = 0; k < K; k++)
+                    for (int d = 0; d < D; d++) W[(int64_t)k * D + d] += x[k] * g[d];
+            }
+        }
+    }
+    free(tso); free(tdo);
+}

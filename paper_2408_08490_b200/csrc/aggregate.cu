@@ -78,6 +78,32 @@ k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict
   }
 }
 
+
+// Aggregate-first input layer: CSR position p -> the global feature row of its
+// source, x = gather_ids[type_src_off[s(r)] + y_src[col[p]]] (r = relation of
+// the compact Y id col[p]), so A4's kernel can gather raw features.
+struct RelOff { int v[HF_MAX_R]; };   // type_src_off[s(r)] per relation
+
+__global__ void __launch_bounds__(256)
+k_col_to_x(int N, int R, const int* __restrict__ rel_y_off, RelOff so,
+           const int* __restrict__ col, const int* __restrict__ y_src,
+           const int* __restrict__ gather_ids, int* __restrict__ col_x) {
+  __shared__ int s_yo[HF_MAX_R + 1];
+  __shared__ int s_so[HF_MAX_R];
+  for (int i = threadIdx.x; i <= R; i += blockDim.x) {
+    s_yo[i] = rel_y_off[i];
+    if (i < R) s_so[i] = so.v[i];
+  }
+  __syncthreads();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= N) return;
+  const int c = col[p];
+  if (c < 0) { col_x[p] = 0; return; }       // tail past the valid edges: never read
+  const int r = upper_bound_i(s_yo, R + 1, c) - 1;
+  const int x = s_so[r] + y_src[c];
+  col_x[p] = gather_ids ? gather_ids[x] : x;
+}
+
 // ------------------------------------------------------------- forward GAT
 // Per head h: two passes over the row's edges (rows are short): the max of the
 // logits, then p = exp(l - max), sum p and sum p * Y.  stats = (max, sum p).
@@ -730,6 +756,46 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_a
   } else {
     return HIFUSE_ERR_INVALID_ARG;
   }
+  return last_cuda();
+}
+
+size_t hifuse_aggregate_features_ws_bytes(const hifuse_layer_shape* shape) {
+  LayerMeta m;
+  if (make_meta(shape, &m) != HIFUSE_OK) return 0;
+  return carve_bytes(m.N > 0 ? m.N : 1, 4);
+}
+
+hifuse_status hifuse_aggregate_features_fwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                            hifuse_agg agg, int K, const float* d_X,
+                                            int64_t x_rows, const int32_t* d_gather_ids,
+                                            float* d_Xagg, void* d_ws, size_t ws_bytes,
+                                            hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (agg != HIFUSE_AGG_SUM && agg != HIFUSE_AGG_MEAN) return HIFUSE_ERR_UNSUPPORTED;
+  if (K != 64 && K != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !csr->row_ptr || !csr->rel_y_off || x_rows < 0 || !d_Xagg ||
+      (m.N > 0 && (!csr->col || !csr->y_src || !d_X)))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_X) || !aligned16(d_Xagg)) return HIFUSE_ERR_ALIGNMENT;
+  if (ws_bytes < hifuse_aggregate_features_ws_bytes(shape) || !d_ws) return HIFUSE_ERR_WORKSPACE;
+  cudaStream_t s = st(stream);
+  char* p = (char*)d_ws;
+  int* col_x = carve<int>(p, m.N > 0 ? m.N : 1);
+  RelOff ro;     // by value (no host->device copy: graph-capturable)
+  for (int r = 0; r < m.R; r++) ro.v[r] = m.type_src_off[m.rel_src[r]];
+  HF_LAUNCH(k_col_to_x, ceil_div(m.N, 256), 256, 0, s, m.N, m.R, csr->rel_y_off, ro, csr->col,
+            csr->y_src, d_gather_ids, col_x);
+  unsigned grid = ceil_div((long long)m.rows, kWarpsPerBlock);
+  const int TB = kWarpsPerBlock * 32;
+  const bool mean = agg == HIFUSE_AGG_MEAN;
+#define HF_AGG(DD, MM)                                                                  \
+  HF_LAUNCH((k_agg_fwd<DD, MM>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, col_x, \
+            (const float4*)d_X, (float4*)d_Xagg)
+  if (K == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
+  else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }
+#undef HF_AGG
   return last_cuda();
 }
 

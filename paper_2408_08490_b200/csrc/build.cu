@@ -89,7 +89,8 @@ __global__ void k_scatter(LayerMeta m, const int* __restrict__ key_e, const int*
   if (e >= m.N) return;
   int nvalid = row_ptr[m.rows];
   if (e >= nvalid) {  // tail positions [nvalid, N): exactly one writer each
-    eperm[e] = -1; col[e] = -1; csc_pos[e] = -1; csc_row[e] = -1;
+    eperm[e] = -1; col[e] = -1;
+    if (csc_pos) { csc_pos[e] = -1; csc_row[e] = -1; }
   }
   int key = key_e[e];
   if (key < 0) return;
@@ -97,7 +98,7 @@ __global__ void k_scatter(LayerMeta m, const int* __restrict__ key_e, const int*
   int c = slot_y[slot_e[e]];
   eperm[pos] = e;
   col[pos] = c;
-  atomicAdd(&ccnt[c], 1);
+  if (csc_pos) atomicAdd(&ccnt[c], 1);
 }
 
 // Segment fix-up sorts (unique keys, carried values).
@@ -140,9 +141,11 @@ k_fix_rows(int rows, const int* __restrict__ row_ptr, int* eperm, int* col,
   if (lane < n) {
     eperm[b + lane] = key;
     col[b + lane] = val;
-    int w = col_ptr[val] + atomicAdd(&ccur[val], 1);
-    csc_pos[w] = b + lane;
-    csc_row[w] = row;
+    if (col_ptr) {
+      int w = col_ptr[val] + atomicAdd(&ccur[val], 1);
+      csc_pos[w] = b + lane;
+      csc_row[w] = row;
+    }
   }
 }
 
@@ -215,7 +218,7 @@ template <bool ROWS>
 __device__ __forceinline__ void place_row_in_csc(int seg, int b, int e, int first, int step,
                                                  const int* vals, const int* col_ptr, int* ccur,
                                                  int* csc_pos, int* csc_row) {
-  if (!ROWS) return;
+  if (!ROWS || !col_ptr) return;
   for (int p = b + first; p < e; p += step) {
     const int c = vals[p];
     const int w = col_ptr[c] + atomicAdd(&ccur[c], 1);
@@ -419,7 +422,8 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     const hifuse_csr& o = out[l];
     if (!o.rel_row_off || !o.row_ptr || !o.rel_y_off || !o.U_dev ||
         (mv[l].N > 0 && (!d_src_local[l] || !d_dst_local[l] || !d_edge_id[l] || !o.col ||
-                         !o.eperm || !o.y_src || !o.col_ptr || !o.csc_pos || !o.csc_row)) ||
+                         !o.eperm || !o.y_src)) ||
+        (!o.col_ptr != !o.csc_pos || !o.col_ptr != !o.csc_row) ||
         (mv[l].S > 0 && !o.slot_y))
       rc = HIFUSE_ERR_INVALID_ARG;
     else if (build_ws(mv[l], umax_of(mv[l]), nullptr, nullptr) > ws_bytes || !d_ws)
@@ -435,8 +439,13 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     long long nz = (long long)m.rows + m.S;
     cudaMemsetAsync(w.cnt, 0, sizeof(int) * (nz > 0 ? nz : 1), s);
     cudaMemsetAsync(w.cur, 0, sizeof(int) * (m.rows > 0 ? m.rows : 1), s);
-    cudaMemsetAsync(w.ccnt, 0, sizeof(int) * (U_max + 1), s);
-    cudaMemsetAsync(w.ccur, 0, sizeof(int) * (U_max + 1), s);
+    // the transpose (CSC) is optional: a layer whose aggregation backward is
+    // never run (the input layer of the aggregate-first RGCN) passes NULLs
+    const bool csc = o.col_ptr != nullptr;
+    if (csc) {
+      cudaMemsetAsync(w.ccnt, 0, sizeof(int) * (U_max + 1), s);
+      cudaMemsetAsync(w.ccur, 0, sizeof(int) * (U_max + 1), s);
+    }
     cudaMemsetAsync(w.counters, 0, sizeof(int) * 2, s);
     const int TB = 256;
     HF_LAUNCH(k_classify, ceil_div(m.N, TB), TB, 0, s, m, d_src_local[l], d_dst_local[l],
@@ -448,13 +457,14 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
               o.rel_y_off, o.y_src, o.slot_y, o.U_dev);
     HF_LAUNCH(k_scatter, ceil_div(m.N, TB), TB, 0, s, m, w.key_e, w.slot_e, o.row_ptr, o.slot_y,
               w.cur, w.ccnt, o.eperm, o.col, o.csc_pos, o.csc_row);
-    exclusive_scan(w.ccnt, o.col_ptr, U_max, w.scan, s);
+    if (csc) exclusive_scan(w.ccnt, o.col_ptr, U_max, w.scan, s);
     int* rows_long = w.lists;
     int* cols_long = w.lists + m.rows;
     HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 8), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
               o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
     HF_LAUNCH(k_sort_long<true>, 148, kSortThreads, 0, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
               o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv, dbg);
+    if (!csc) continue;
     HF_LAUNCH(k_fix_cols, ceil_div(U_max, 256), 256, 0, s, o.U_dev, o.col_ptr, o.csc_pos,
               o.csc_row, cols_long, w.counters + 1);   // 8 warps x 32 columns per block
     HF_LAUNCH(k_sort_long<false>, 148, kSortThreads, 0, s, o.col_ptr, o.csc_pos, o.csc_row,

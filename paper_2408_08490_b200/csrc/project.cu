@@ -688,8 +688,8 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
   float* v = carve<float>(p, (long long)m.R * K * (heads > 0 ? heads : 1));
   if (prec == HIFUSE_PREC_TF32) {
-    rc = project_tcp_launch(m, pm, K, D, csr, d_X, d_gather_ids, d_W_rel, d_W_root, d_Y, d_R0,
-                            d_att, d_s_src, heads, s);   // s_src fused in the epilogue
+    rc = project_tcp_launch(m, pm, K, D, csr->rel_y_off, csr->y_src, d_X, nullptr, d_gather_ids,
+                            d_W_rel, d_W_root, d_Y, d_R0, d_att, d_s_src, heads, s);   // s_src fused in the epilogue
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
@@ -833,6 +833,91 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
       HF_LAUNCH(k_dx_sdst, ceil_div((long long)m.dst_rows * K, 256), 256, 0, s, dm, m.dst_rows, K,
                 H, v, d_ds_dst, d_dX);
   }
+  return last_cuda();
+}
+
+}  // extern "C"
+
+// ------------------------------------------------ aggregate-first RGCN input --
+// SURVEY §8(f) NEXT(3), "aggregate-then-project": for the linear RGCN message
+// W_r x, Z_r = A_r (X W_r) = (A_r X) W_r exactly (linearity; PAPER.md's
+// four-stage layer P:L112-125 with stages 2 and 3 swapped), so the input
+// layer can aggregate raw features first (hifuse_aggregate_features_fwd) and
+// project rho aggregated rows instead of U compact source rows.  The layer's
+// backward needs no transpose SpMM: dW_r = Xagg_r^T G_t(r) (no dX for the
+// input features).
+static long long direct_max_chunks(const LayerMeta& m, int step) {
+  return ((long long)m.rows + m.dst_rows) / step + m.R + m.T + 1;
+}
+static int direct_chunk_rows(const LayerMeta& m) {
+  long long ch = ((long long)m.rows + m.dst_rows) / (2 * 148);
+  ch = (ch + 31) / 32 * 32;
+  return (int)(ch < 128 ? 128 : (ch > kCHT ? kCHT : ch));
+}
+
+extern "C" {
+
+hifuse_status hifuse_project_aggregated(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                        hifuse_prec prec, int K, int D, const float* d_Xagg,
+                                        const float* d_X, int64_t x_rows,
+                                        const int32_t* d_gather_ids, const float* d_W_rel,
+                                        const float* d_W_root, float* d_Z, float* d_R0,
+                                        hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!kd_ok(K, D) || prec != HIFUSE_PREC_TF32) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !csr->rel_row_off || !d_Xagg || !d_W_rel || !d_Z || x_rows < 0 ||
+      (d_W_root && (!d_R0 || !d_X)))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_Xagg) || !aligned16(d_X) || !aligned16(d_W_rel) || !aligned16(d_W_root) ||
+      !aligned16(d_Z) || !aligned16(d_R0))
+    return HIFUSE_ERR_ALIGNMENT;
+  ProjMeta pm;
+  make_proj_meta(m, d_W_root != nullptr, &pm);
+  rc = project_tcp_launch(m, pm, K, D, csr->rel_row_off, nullptr, d_X ? d_X : d_Xagg, d_Xagg,
+                          d_gather_ids, d_W_rel, d_W_root, d_Z, d_R0, nullptr, nullptr, 1,
+                          st(stream));
+  if (rc != HIFUSE_OK) return rc;
+  return last_cuda();
+}
+
+size_t hifuse_project_aggregated_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D) {
+  LayerMeta m;
+  if (make_meta(shape, &m) != HIFUSE_OK) return 0;
+  return carve_bytes(direct_max_chunks(m, 128) * K * D, 4);
+}
+
+hifuse_status hifuse_project_aggregated_bwd(const hifuse_layer_shape* shape,
+                                            const hifuse_csr* csr, hifuse_prec prec, int K, int D,
+                                            const float* d_Xagg, const float* d_X, int64_t x_rows,
+                                            const int32_t* d_gather_ids, const float* d_G,
+                                            float* d_dW_rel, float* d_dW_root, void* d_ws,
+                                            size_t ws_bytes, hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!kd_ok(K, D) || prec != HIFUSE_PREC_TF32) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !csr->rel_row_off || !d_Xagg || !d_G || !d_dW_rel || x_rows < 0 ||
+      (d_dW_root && !d_X))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_Xagg) || !aligned16(d_X) || !aligned16(d_G) || !aligned16(d_dW_rel) ||
+      !aligned16(d_dW_root))
+    return HIFUSE_ERR_ALIGNMENT;
+  if (ws_bytes < hifuse_project_aggregated_bwd_ws_bytes(shape, K, D) || !d_ws)
+    return HIFUSE_ERR_WORKSPACE;
+  cudaStream_t s = st(stream);
+  ProjMeta pm;
+  make_proj_meta(m, d_dW_root != nullptr, &pm);
+  const int CH = direct_chunk_rows(m);
+  float* partial = (float*)d_ws;
+  wgrad_tc_launch(m, pm, K, D, CH, nullptr, csr->rel_row_off, nullptr, d_gather_ids,
+                  d_X ? d_X : d_Xagg, nullptr, d_G, partial,
+                  (unsigned)direct_max_chunks(m, CH), s, d_Xagg);
+  int G = d_dW_root ? m.R + m.T : m.R;
+  HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
+            (const int*)nullptr, (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root,
+            pm, csr->rel_row_off, CH);
   return last_cuda();
 }
 

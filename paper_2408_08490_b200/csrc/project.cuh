@@ -40,10 +40,13 @@ long long proj_max_tiles(const LayerMeta& m, int step);
 
 // tcgen05 TF32 forward projection (project_tc.cu).
 // tcgen05 TF32 forward projection (persistent, warp-specialised; project_tc.cu)
+// Xm != NULL: aggregate-first input layer -- message groups read the
+// aggregated rows rel_off[r] + j of Xm (rel_off = rel_row_off) and write Z.
 hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
-                                 const hifuse_csr* csr, const float* X, const int* gather_ids,
-                                 const float* W_rel, const float* W_root, float* Y, float* R0,
-                                 const float* att, float* s_src, int H, cudaStream_t s);
+                                 const int* rel_off, const int* y_src, const float* X,
+                                 const float* Xm, const int* gather_ids, const float* W_rel,
+                                 const float* W_root, float* Y, float* R0, const float* att,
+                                 float* s_src, int H, cudaStream_t s);
 // tcgen05 TF32 dgrad: dX[type s rows] = sum_terms A_term W_term^T (A = dYt rows
 // through slot_y, or G for the root term).  dm built with bm = 128.
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
@@ -62,5 +65,6 @@ inline int wgrad_chunk_rows(const LayerMeta& m) {
 hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D, int CH,
                               const int* chunk_off, const int* rel_y_off, const int* y_src,
                               const int* gather_ids, const float* X, const float* dY,
-                              const float* G, float* partial, unsigned grid, cudaStream_t s);
+                              const float* G, float* partial, unsigned grid, cudaStream_t s,
+                              const float* Xm = nullptr);
 }  // namespace hf

@@ -44,10 +44,13 @@ __device__ __forceinline__ bool tc_resolve(const ProjMeta& pm, const int* table,
   return *nrows > 0;
 }
 
+// A row of group g, local row j.  direct (aggregate-first input): message
+// group rows are the aggregated rows rel_off[g] + j of Xm, never gathered.
 __device__ __forceinline__ long long tc_a_row(const ProjMeta& pm, const int* rel_y_off,
                                               const int* y_src, const int* gather_ids, int g,
-                                              int j) {
+                                              int j, bool direct = false) {
   int x;
+  if (g < pm.R && direct) return (long long)rel_y_off[g] + j;
   if (g < pm.R) x = pm.type_src_off[pm.rel_src[g]] + y_src[rel_y_off[g] + j];
   else x = pm.type_src_off[g - pm.R] + j;
   return gather_ids ? (long long)gather_ids[x] : (long long)x;
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(128)
 k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __restrict__ rel_y_off,
            const int* __restrict__ y_src, const int* __restrict__ gather_ids,
            const float* __restrict__ X, const float* __restrict__ dY, const float* __restrict__ G,
-           float* __restrict__ partial) {
+           float* __restrict__ partial, const float* __restrict__ Xm) {
   constexpr int MA = 128;                               // padded M (features)
   constexpr uint32_t BLK = 4096;                        // one 32-feature block of 32 rows
   constexpr uint32_t A_STAGE = (MA / 32) * BLK, B_STAGE = (D / 32) * BLK, STAGE = A_STAGE + B_STAGE;
@@ -227,14 +230,29 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
   // X row of every row of the chunk, resolved once up front (the dependent
   // y_src -> gather_ids loads would otherwise stall every stage)
   __shared__ int s_xrow[kCHT];
-  for (int i = tid; i < nrows; i += 128)
-    s_xrow[i] = (int)tc_a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + i);
+  const bool direct = Xm != nullptr;
+  for (int base = tid; base < nrows; base += 8 * 128) {    // 8 dependent chains in flight
+    int xr[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int i = base + u * 128;
+      xr[u] = i < nrows ? (int)tc_a_row(pm, rel_y_off, y_src, gather_ids, g, r0 + i, direct) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (base + u * 128 < nrows) s_xrow[base + u * 128] = xr[u];
+  }
+  const float* Ab = (direct && g < pm.R) ? Xm : X;
   if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), D);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const float* Bbase = g < pm.R ? dY + (long long)rel_y_off[g] * D
+  // B rows: dY of the relation (project-first) or, aggregate-first, the
+  // gradient G of the relation's destination type (Z_r = Xagg_r W_r feeds
+  // H_t(r) directly); root groups: G of the type
+  const float* Bbase = g < pm.R ? (direct ? G + (long long)pm.type_dst_off[pm.rel_dst[g]] * D
+                                          : dY + (long long)rel_y_off[g] * D)
                                 : G + (long long)pm.type_dst_off[g - pm.R] * D;
   const int NST = (nrows + 31) / 32;
 
@@ -245,10 +263,10 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
       const int i = tid + 128 * q;
       const int row = i / (K / 4), f = (i % (K / 4)) * 4;
       const int rr = c * 32 + row;
-      const float* src = X;
+      const float* src = Ab;
       uint32_t nb = 0;
       if (rr < nrows) {
-        src = X + (long long)s_xrow[rr] * K + f;
+        src = Ab + (long long)s_xrow[rr] * K + f;
         nb = 16;
       }
       cp_async16(sa + (f >> 5) * BLK + (row >> 2) * 512 + sw128b32_off(row, (f & 31) * 4), src, nb);
@@ -353,7 +371,8 @@ hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot
 hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D, int CH,
                               const int* chunk_off, const int* rel_y_off, const int* y_src,
                               const int* gather_ids, const float* X, const float* dY,
-                              const float* G, float* partial, unsigned grid, cudaStream_t s) {
+                              const float* G, float* partial, unsigned grid, cudaStream_t s,
+                              const float* Xm) {
   (void)m;
   static bool attr = false;
   if (!attr) {
@@ -365,7 +384,7 @@ hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int
   }
 #define HF_WG(KK, DD)                                                                          \
   HF_LAUNCH((k_wgrad_tc<KK, DD>), grid, 128, (wgrad_smem<KK, DD>()), s, pm, CH, chunk_off,     \
-            rel_y_off, y_src, gather_ids, X, dY, G, partial)
+            rel_y_off, y_src, gather_ids, X, dY, G, partial, Xm)
   if (K == 128 && D == 128) HF_WG(128, 128);
   else if (K == 128 && D == 64) HF_WG(128, 64);
   else if (K == 64 && D == 128) HF_WG(64, 128);
@@ -428,7 +447,7 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
                const int* __restrict__ gather_ids, const float* __restrict__ X,
                const float* __restrict__ W_rel, const float* __restrict__ W_root,
                float* __restrict__ Y, float* __restrict__ R0, const float* __restrict__ att,
-               float* __restrict__ s_src, int H) {
+               float* __restrict__ s_src, int H, const float* __restrict__ Xm) {
   constexpr int BM = 128, NC = K / 32;
   constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
   constexpr uint32_t STAGE = A_STAGE + B_STAGE;
@@ -476,7 +495,8 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
         ap[i] = X;
         nb[i] = 0;
         if (row < nrows) {
-          ap[i] = X + tc_a_row(pm, s_yoff, y_src, gather_ids, *g, r0 + row) * K;
+          const float* Ab = (Xm && *g < pm.R) ? Xm : X;
+          ap[i] = Ab + tc_a_row(pm, s_yoff, y_src, gather_ids, *g, r0 + row, Xm != nullptr) * K;
           nb[i] = 16;
         }
       }
@@ -624,9 +644,10 @@ template <int K, int D>
 static constexpr int fwdp_smem() { return kFStages * (128 * 128 + D * 128) + 1024; }
 
 template <int K, int D>
-static void launch_tcp(const ProjMeta& pm, const hifuse_csr* csr, const int* gather_ids,
-                       const float* X, const float* W_rel, const float* W_root, float* Y,
-                       float* R0, const float* att, float* s_src, int H, cudaStream_t s) {
+static void launch_tcp(const ProjMeta& pm, const int* rel_off, const int* y_src,
+                       const int* gather_ids, const float* X, const float* Xm,
+                       const float* W_rel, const float* W_root, float* Y, float* R0,
+                       const float* att, float* s_src, int H, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_proj_fwd_tcp<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -634,18 +655,22 @@ static void launch_tcp(const ProjMeta& pm, const hifuse_csr* csr, const int* gat
     attr = true;
   }
   HF_LAUNCH((k_proj_fwd_tcp<K, D>), 148 * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
-            csr->rel_y_off, csr->y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H);
+            rel_off, y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, Xm);
 }
 
 hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,
-                                 const hifuse_csr* csr, const float* X, const int* gather_ids,
-                                 const float* W_rel, const float* W_root, float* Y, float* R0,
-                                 const float* att, float* s_src, int H, cudaStream_t s) {
+                                 const int* rel_off, const int* y_src, const float* X,
+                                 const float* Xm, const int* gather_ids, const float* W_rel,
+                                 const float* W_root, float* Y, float* R0, const float* att,
+                                 float* s_src, int H, cudaStream_t s) {
   (void)m;
-  if (K == 128 && D == 128) launch_tcp<128, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
-  else if (K == 128 && D == 64) launch_tcp<128, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
-  else if (K == 64 && D == 128) launch_tcp<64, 128>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
-  else launch_tcp<64, 64>(pm, csr, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, s);
+#define HF_TCP(KK, DD) \
+  launch_tcp<KK, DD>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0, att, s_src, H, s)
+  if (K == 128 && D == 128) HF_TCP(128, 128);
+  else if (K == 128 && D == 64) HF_TCP(128, 64);
+  else if (K == 64 && D == 128) HF_TCP(64, 128);
+  else HF_TCP(64, 64);
+#undef HF_TCP
   return HIFUSE_OK;
 }
 

@@ -70,6 +70,13 @@ def lib():
             "hifuse_project_bwd_ws_bytes": [vp, i32, i32, i32],
             "hifuse_project_bwd": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp,
                                    vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
+            "hifuse_aggregate_features_ws_bytes": [vp],
+            "hifuse_aggregate_features_fwd": [vp, vp, i32, i32, vp, i64, vp, vp, vp, sz, vp],
+            "hifuse_project_aggregated": [vp, vp, i32, i32, i32, vp, vp, i64, vp, vp, vp, vp, vp,
+                                          vp],
+            "hifuse_project_aggregated_bwd_ws_bytes": [vp, i32, i32],
+            "hifuse_project_aggregated_bwd": [vp, vp, i32, i32, i32, vp, vp, i64, vp, vp, vp, vp,
+                                              vp, sz, vp],
             "hifuse_xent_ws_bytes": [i32, i32, i32],
             "hifuse_linear_xent": [i32, i32, i32, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp,
                                    sz, vp],
@@ -83,7 +90,8 @@ def lib():
             fn.restype = ctypes.c_int
         for name in ("hifuse_project_ws_bytes", "hifuse_fuse_bwd_ws_bytes",
                      "hifuse_aggregate_bwd_ws_bytes", "hifuse_project_bwd_ws_bytes",
-                     "hifuse_xent_ws_bytes"):
+                     "hifuse_xent_ws_bytes", "hifuse_aggregate_features_ws_bytes",
+                     "hifuse_project_aggregated_bwd_ws_bytes"):
             getattr(L, name).restype = ctypes.c_size_t
         L.hifuse_kernel_launches.restype = ctypes.c_int64
         L.hifuse_status_string.restype = ctypes.c_char_p
@@ -140,7 +148,7 @@ class Shape:
 class CsrBuffers:
     """Device buffers of one layer's build output (torch int32 tensors)."""
 
-    def __init__(self, shape: Shape, device, cap=None):
+    def __init__(self, shape: Shape, device, cap=None, csc=True):
         import torch
         cap = cap or {}
         N = max(cap.get("N", shape.N), 1)
@@ -152,7 +160,10 @@ class CsrBuffers:
         self.t = dict(rel_row_off=z(R + 1), row_ptr=z(rows + 1), col=z(N), eperm=z(N),
                       rel_y_off=z(R + 1), y_src=z(umax), col_ptr=z(umax + 1), csc_pos=z(N),
                       csc_row=z(N), slot_y=z(S), U_dev=z(1))
-        self.c = Csr(**{k: v.data_ptr() for k, v in self.t.items()})
+        if not csc:     # transpose not built (aggregate-first input layer)
+            for k in ("col_ptr", "csc_pos", "csc_row"):
+                self.t[k] = None
+        self.c = Csr(**{k: (v.data_ptr() if v is not None else None) for k, v in self.t.items()})
 
     def __getitem__(self, k):
         return self.t[k]
@@ -231,6 +242,36 @@ def project_bwd(shape, csr, K, D, heads, X, gather_ids, W_rel, W_root, att, Y, d
         _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(att), _ptr(Y), _ptr(dY), _ptr(G),
         _ptr(ds_src), _ptr(ds_dst), _ptr(dX), _ptr(dW_rel), _ptr(dW_root), _ptr(datt), _ptr(ws),
         ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def aggregate_features_ws_bytes(shape):
+    return int(lib().hifuse_aggregate_features_ws_bytes(shape.ref))
+
+
+def aggregate_features_fwd(shape, csr, agg, K, X, gather_ids, Xagg, ws, stream=None):
+    _check("hifuse_aggregate_features_fwd", lib().hifuse_aggregate_features_fwd(
+        shape.ref, csr.ref, AGG[agg], K, _ptr(X), X.shape[0], _ptr(gather_ids), _ptr(Xagg),
+        _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def project_aggregated(shape, csr, K, D, Xagg, X, gather_ids, W_rel, W_root, Z, R0, prec="tf32",
+                       stream=None):
+    _check("hifuse_project_aggregated", lib().hifuse_project_aggregated(
+        shape.ref, csr.ref, PREC[prec], K, D, _ptr(Xagg), _ptr(X),
+        0 if X is None else X.shape[0], _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(Z),
+        _ptr(R0), _stream(stream)))
+
+
+def project_aggregated_bwd_ws_bytes(shape, K, D):
+    return int(lib().hifuse_project_aggregated_bwd_ws_bytes(shape.ref, K, D))
+
+
+def project_aggregated_bwd(shape, csr, K, D, Xagg, X, gather_ids, G, dW_rel, dW_root, ws,
+                           prec="tf32", stream=None):
+    _check("hifuse_project_aggregated_bwd", lib().hifuse_project_aggregated_bwd(
+        shape.ref, csr.ref, PREC[prec], K, D, _ptr(Xagg), _ptr(X),
+        0 if X is None else X.shape[0], _ptr(gather_ids), _ptr(G), _ptr(dW_rel), _ptr(dW_root),
+        _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def xent_ws_bytes(B, D, C):

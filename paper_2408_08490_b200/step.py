@@ -80,7 +80,7 @@ class Trainer:
     """Owns parameters, gradients, activations and workspaces of the step."""
 
     def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
-                 prec="tf32", slope=0.2):
+                 prec="tf32", slope=0.2, order="project_first"):
         hf.lib()   # raises if libhifuse.so is missing (no CPU fallback)
         self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
         self.rel_src = np.asarray(rel_src, np.int32)
@@ -96,6 +96,14 @@ class Trainer:
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
         self._bufs = {}
         self.heads = H if model == "rgat" else 1
+        # "agg_first": the RGCN input layer aggregates raw features and then
+        # projects the aggregated rows (exact by linearity; SURVEY §8(f)
+        # NEXT(3)).  RGAT needs projected features for its
+        # scores, so it always projects first.
+        if order not in ("project_first", "agg_first"):
+            raise ValueError(order)
+        self.agg_first = order == "agg_first" and model == "rgcn" and prec == "tf32"
+        self.order = "agg_first" if self.agg_first else "project_first"
 
     def load_params(self, p):
         for l, lay in enumerate(p["layers"]):
@@ -123,7 +131,8 @@ class Trainer:
         if c is None or any(need[k] > c.cap[k] for k in need):
             cap = {k: int(v * 1.25) + 1 for k, v in need.items()}
             cap["R"] = shape.R
-            c = hf.CsrBuffers(shape, self.device, cap)
+            # the aggregate-first input layer never runs the transpose
+            c = hf.CsrBuffers(shape, self.device, cap, csc=not (self.agg_first and l == 0))
             c.cap = cap
             self._bufs[key] = c
         return c
@@ -167,6 +176,21 @@ class Trainer:
                      stats=self._mat(f"st{l}", sh.rows, 2 * H) if self.agg == "gat" else None,
                      H=self._mat(f"H{l}", sh.dst_rows, D),
                      wsp=self._ws(hf.project_ws_bytes(sh, K, D, H)))
+            if self.agg_first and l == 0:
+                a.update(Y=None, Xagg=self._mat("Xagg0", sh.rows, K),
+                         wsx=self._ws(hf.aggregate_features_ws_bytes(sh), key="ws_aggx"))
+                ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a:
+                            hf.aggregate_features_fwd(sh, c, self.agg, a["K"], a["X"], a["gid"],
+                                                      a["Xagg"], a["wsx"])))
+                ops.append(("project_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
+                            hf.project_aggregated(sh, c, a["K"], D, a["Xagg"], a["X"], a["gid"],
+                                                  P["W_rel"], P["W_root"], a["Z"], a["R0"],
+                                                  prec=self.prec)))
+                ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
+                    sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
+                acts.append(a)
+                X, gid = a["H"], None
+                continue
             ops.append((f"project.{l}", lambda sh=sh, c=csrs[l], a=a, P=P: hf.project(
                 sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"], P["att"], a["Y"],
                 a["R0"], a["s_src"], a["s_dst"], a["wsp"], prec=self.prec)))
@@ -187,6 +211,17 @@ class Trainer:
             sh, a = shapes[l], acts[l]
             P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
             Gr = {k: self.Gd.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
+            if self.agg_first and l == 0:
+                b = dict(dH=dH, G=self._mat(f"G{l}", sh.dst_rows, D),
+                         wsf=self._ws(hf.fuse_bwd_ws_bytes(sh, D)),
+                         wsq=self._ws(hf.project_aggregated_bwd_ws_bytes(sh, a["K"], D)))
+                ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
+                    sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
+                ops.append(("project_aggregated_bwd.0", lambda sh=sh, c=csrs[l], a=a, b=b, Gr=Gr:
+                            hf.project_aggregated_bwd(sh, c, a["K"], D, a["Xagg"], a["X"],
+                                                      a["gid"], b["G"], Gr["W_rel"],
+                                                      Gr["W_root"], b["wsq"], prec=self.prec)))
+                continue
             b = dict(dH=dH, G=self._mat(f"G{l}", sh.dst_rows, D),
                      dY=self._mat(f"dY{l}", sh.U_max, D),
                      ds_src=self._mat(f"dss{l}", sh.U_max, H) if P["att"] is not None else None,

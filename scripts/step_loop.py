@@ -15,7 +15,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="mag")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--pool", type=int, default=2)
-ap.add_argument("--prec", default="fp32")
+ap.add_argument("--prec", default="tf32")
+ap.add_argument("--order", default="agg_first")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 g = generate_graph(cfg)
@@ -27,7 +28,8 @@ dev = "cuda:0"
 pool = [DeviceBatch(make_batch(cfg, g, b % nb, epoch=b // nb), rs, rd, foff, cfg.target_type, dev)
         for b in range(a.pool)]
 tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
-             cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=0.01, prec=a.prec)
+             cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=0.01, prec=a.prec,
+             order=a.order)
 tr.load_params(make_params(cfg))
 fd = torch.from_numpy(feat).to(dev)
 et = torch.from_numpy(g.edge_type).to(dev)

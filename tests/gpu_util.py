@@ -14,11 +14,11 @@ def hf():
     return h
 
 
-def gpu_build(blk, et, rel_src, rel_dst, status=None):
+def gpu_build(blk, et, rel_src, rel_dst, status=None, csc=True):
     """Runs hifuse_build_semantic_graphs on one layer; returns (shape, csr)."""
     h = hf()
     sh = h.Shape(rel_src, rel_dst, blk.n_src, blk.n_dst, blk.num_edges)
-    csr = h.CsrBuffers(sh, DEV)
+    csr = h.CsrBuffers(sh, DEV, csc=csc)
     ws = torch.empty((sh.build_ws + 3) // 4 + 16, dtype=torch.int32, device=DEV)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=DEV)
     t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).to(DEV)
@@ -30,7 +30,7 @@ def gpu_build(blk, et, rel_src, rel_dst, status=None):
 
 def csr_host(sh, csr):
     U = int(csr["U_dev"].item())
-    g = lambda k, n: csr[k][:n].cpu().numpy()
+    g = lambda k, n: None if csr[k] is None else csr[k][:n].cpu().numpy()
     return dict(U=U, rel_row_off=g("rel_row_off", sh.R + 1), row_ptr=g("row_ptr", sh.rows + 1),
                 col=g("col", sh.N), eperm=g("eperm", sh.N), rel_y_off=g("rel_y_off", sh.R + 1),
                 y_src=g("y_src", U), col_ptr=g("col_ptr", U + 1), csc_pos=g("csc_pos", sh.N),

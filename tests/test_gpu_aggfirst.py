@@ -1,0 +1,126 @@
+"""-m gpu: the aggregate-first RGCN input layer (SURVEY.md §8(f) NEXT(3),
+DESIGN.md §9) against the oracle's O6 functions, stage by stage, and the
+whole training step against the (project-first) oracle model -- the two
+orders are equal by linearity (pinned in tests/test_oracle_aggfirst.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import random_block, random_schema
+
+from gpu_util import needs_gpu, gpu_build, csr_host, close_scaled, row_rel_l2, t, DEV, hf
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+
+
+def make_case(seed, T=None, R=None, N=None, hub=0.0, csc=True):
+    rng = np.random.default_rng(seed)
+    T = T or int(rng.integers(1, 5))
+    R = R or int(rng.integers(1, 12))
+    rs, rd = random_schema(rng, T, R)
+    n_src = rng.integers(1, 400, T)
+    n_dst = np.maximum(np.minimum(rng.integers(0, 250, T), n_src), 1)
+    N = int(rng.integers(100, 6000)) if N is None else N
+    blk, et = random_block(rng, n_src, n_dst, rs, rd, N, hub_frac=hub)
+    sh, csr, st = gpu_build(blk, et, rs, rd, csc=csc)
+    return rng, blk, et, rs, rd, sh, csr
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_build_without_transpose_is_bit_exact(seed):
+    rng, blk, et, rs, rd, sh, csr = make_case(300 + seed, hub=0.1, csc=False)
+    ch = csr_host(sh, csr)
+    ref = oracle.build(oracle.Shape.of(blk, rs, rd), blk, et)
+    assert ch["U"] == ref["U"]
+    for k in ("rel_row_off", "row_ptr", "col", "eperm", "rel_y_off", "y_src", "slot_y"):
+        assert np.array_equal(ch[k], np.asarray(ref[k])), k
+
+
+@pytest.mark.parametrize("K", [64, 128])
+@pytest.mark.parametrize("agg", ["sum", "mean"])
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_features(seed, agg, K):
+    rng, blk, et, rs, rd, sh, csr = make_case(310 + seed, hub=0.1 * (seed % 2), csc=False)
+    xr = sh.src_rows + 13
+    X = rng.standard_normal((xr, K)).astype(np.float32)
+    gid = rng.permutation(xr)[:sh.src_rows].astype(np.int32)
+    Xa = torch.full((max(sh.rows, 1), K), float("nan"), device=DEV)
+    ws = torch.empty(hf().aggregate_features_ws_bytes(sh) // 4 + 16, device=DEV)
+    hf().aggregate_features_fwd(sh, csr, agg, K, t(X), t(gid, torch.int32), Xa, ws)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.aggregate_features(osh, blk, et, agg, K, X, gid)
+    A = oracle.aggregate_features(osh, blk, et, agg, K, np.abs(X), gid)
+    close_scaled(Xa.cpu().numpy()[:sh.rows], ref, A, what=f"Xagg {agg}")
+
+
+def test_aggregate_features_integer_inputs_bit_exact():
+    rng, blk, et, rs, rd, sh, csr = make_case(333, N=5000, csc=False)
+    K = 128
+    X = rng.integers(-8, 9, (sh.src_rows, K)).astype(np.float32)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ws = torch.empty(hf().aggregate_features_ws_bytes(sh) // 4 + 16, device=DEV)
+    for agg in ("sum", "mean"):
+        Xa = torch.zeros(sh.rows, K, device=DEV)
+        hf().aggregate_features_fwd(sh, csr, agg, K, t(X), None, Xa, ws)
+        ref = oracle.aggregate_features(osh, blk, et, "sum", K, X, None)
+        if agg == "mean":     # reading C19: fp32 sum (exact here) / fp32 degree
+            deg = np.zeros(sh.rows)
+            row = 0
+            for r in range(sh.R):
+                m = et[blk.edge_id] == r
+                np.add.at(deg, row + blk.dst_local[m], 1)
+                row += int(blk.n_dst[rd[r]])
+            ref = np.where(deg[:, None] > 0, ref.astype(np.float32) /
+                           np.maximum(deg, 1)[:, None].astype(np.float32), 0)
+        assert np.array_equal(Xa.cpu().numpy(), ref.astype(np.float32)), agg
+
+
+@pytest.mark.parametrize("K,D", [(128, 128), (64, 64), (128, 64), (64, 128)])
+def test_project_aggregated_exact_on_representable_inputs(K, D):
+    """Xagg, X, W, G in {-2..2}/4: TF32-exact operands and exact fp32 sums, so
+    the tcgen05 forward and wgrad must equal the oracle bit for bit."""
+    rng, blk, et, rs, rd, sh, csr = make_case(350 + K + D, T=3, R=6, N=4000, csc=False)
+    q = lambda *s: (rng.integers(-2, 3, s) / 4).astype(np.float32)
+    Xa, X, W, Wr = q(sh.rows, K), q(sh.src_rows + 5, K), q(sh.R, K, D), q(sh.T, K, D)
+    gid = rng.permutation(sh.src_rows + 5)[:sh.src_rows].astype(np.int32)
+    Z = torch.zeros(sh.rows, D, device=DEV)
+    R0 = torch.zeros(sh.dst_rows, D, device=DEV)
+    hf().project_aggregated(sh, csr, K, D, t(Xa), t(X), t(gid, torch.int32), t(W), t(Wr), Z, R0)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.project_aggregated(osh, K, D, Xa, X, gid, W, Wr)
+    assert np.array_equal(Z.cpu().numpy(), ref["Z"].astype(np.float32))
+    assert np.array_equal(R0.cpu().numpy(), ref["R0"].astype(np.float32))
+    G = q(sh.dst_rows, D)
+    dW = torch.zeros(sh.R, K, D, device=DEV)
+    dWr = torch.zeros(sh.T, K, D, device=DEV)
+    ws = torch.empty(hf().project_aggregated_bwd_ws_bytes(sh, K, D) // 4 + 16, device=DEV)
+    hf().project_aggregated_bwd(sh, csr, K, D, t(Xa), t(X), t(gid, torch.int32), t(G), dW, dWr, ws)
+    ob = oracle.project_aggregated_bwd(osh, K, D, Xa, X, gid, G)
+    assert np.array_equal(dW.cpu().numpy(), ob["dW_rel"].astype(np.float32))
+    assert np.array_equal(dWr.cpu().numpy(), ob["dW_root"].astype(np.float32))
+
+
+@pytest.mark.parametrize("K,D", [(128, 128), (64, 64)])
+def test_project_aggregated_random(K, D):
+    rng, blk, et, rs, rd, sh, csr = make_case(370 + K, T=4, R=9, N=6000, hub=0.05, csc=False)
+    Xa = rng.standard_normal((sh.rows, K)).astype(np.float32)
+    X = rng.standard_normal((sh.src_rows, K)).astype(np.float32)
+    W = (rng.standard_normal((sh.R, K, D)) / np.sqrt(K)).astype(np.float32)
+    Wr = (rng.standard_normal((sh.T, K, D)) / np.sqrt(K)).astype(np.float32)
+    Z = torch.zeros(sh.rows, D, device=DEV)
+    R0 = torch.zeros(sh.dst_rows, D, device=DEV)
+    hf().project_aggregated(sh, csr, K, D, t(Xa), t(X), None, t(W), t(Wr), Z, R0)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.project_aggregated(osh, K, D, Xa, X, None, W, Wr)
+    row_rel_l2(Z.cpu().numpy(), ref["Z"], 2e-3, "Z")
+    row_rel_l2(R0.cpu().numpy(), ref["R0"], 2e-3, "R0")
+    G = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    dW = torch.zeros(sh.R, K, D, device=DEV)
+    dWr = torch.zeros(sh.T, K, D, device=DEV)
+    ws = torch.empty(hf().project_aggregated_bwd_ws_bytes(sh, K, D) // 4 + 16, device=DEV)
+    hf().project_aggregated_bwd(sh, csr, K, D, t(Xa), t(X), None, t(G), dW, dWr, ws)
+    ob = oracle.project_aggregated_bwd(osh, K, D, Xa, X, None, G)
+    row_rel_l2(dW.cpu().numpy().reshape(-1, D), ob["dW_rel"].reshape(-1, D), 3e-3, "dW_rel")
+    row_rel_l2(dWr.cpu().numpy().reshape(-1, D), ob["dW_root"].reshape(-1, D), 3e-3, "dW_root")

@@ -31,9 +31,12 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+@pytest.mark.parametrize("prec,order", [("fp32", "project_first"), ("tf32", "project_first"),
+                                        ("tf32", "agg_first")])
 @pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag"])
-def test_step_matches_oracle(key, prec):
+def test_step_matches_oracle(key, prec, order):
+    """agg_first (RGCN input layer aggregates raw features, then projects) is
+    checked against the same project-first oracle model: equal by linearity."""
     from paper_2408_08490_b200.step import Trainer, DeviceBatch
     cfg, g, feat, foff = setup(key)
     mb = make_batch(cfg, g, 0)
@@ -41,7 +44,10 @@ def test_step_matches_oracle(key, prec):
     rd = np.array([r.dst for r in cfg.rels], np.int32)
     params = make_params(cfg)
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
-                 cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0, prec=prec)
+                 cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0, prec=prec,
+                 order=order)
+    if order == "agg_first" and not tr.agg_first:
+        pytest.skip("aggregate-first applies to RGCN only")
     tr.load_params(params)
     db = DeviceBatch(mb, rs, rd, foff, cfg.target_type, DEV)
     feat_d = torch.from_numpy(feat).to(DEV)
