@@ -88,20 +88,33 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total) {
 // order through an atomic ticket, so every predecessor is already running).
 // status[t] = (flag << 30) | value: flag 1 = tile aggregate, 2 = inclusive
 // prefix.  Values must stay below 2^30 (counts of edges / rows / slots).
+// Tile I/O goes through shared memory: coalesced global loads/stores
+// (striped over the block), while each thread scans kScanItems consecutive
+// items read from a padded layout (index i stored at i + i/32: the 32 items
+// of a thread sit in 32 distinct banks).
+__device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
+
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_lookback(const int* __restrict__ in, long long n, int* __restrict__ out,
                 int* __restrict__ ticket, int* __restrict__ status) {
   __shared__ int s_tile, s_prefix;
+  __shared__ int sm[kScanTile + kScanTile / 32];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
   __syncthreads();
   const int tile = s_tile;
-  const long long base = (long long)tile * kScanTile + (long long)threadIdx.x * kScanItems;
+  const long long t0 = (long long)tile * kScanTile;
+  const int nt = (int)(n - t0 < kScanTile ? n - t0 : kScanTile);
+#pragma unroll
+  for (int j = 0; j < kScanItems; j++) {           // coalesced, all loads in flight
+    const int i = j * kScanThreads + threadIdx.x;
+    sm[pad32(i)] = i < nt ? in[t0 + i] : 0;
+  }
+  __syncthreads();
   int v[kScanItems];
   int sum = 0;
 #pragma unroll
   for (int j = 0; j < kScanItems; j++) {
-    long long k = base + j;
-    v[j] = k < n ? in[k] : 0;
+    v[j] = sm[pad32(threadIdx.x * kScanItems + j)];
     sum += v[j];
   }
   int tot;
@@ -125,9 +138,9 @@ k_scan_lookback(const int* __restrict__ in, long long n, int* __restrict__ out,
         if (__any_sync(0xffffffffu, flag == 0)) continue;     // someone not published yet
         const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
         const int stop = incl ? __ffs(incl) - 1 : 32;          // nearest inclusive prefix
-        int v = (lane <= stop && t >= 0) ? (w & 0x3fffffff) : 0;
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        prefix += v;
+        int v2 = (lane <= stop && t >= 0) ? (w & 0x3fffffff) : 0;
+        for (int o = 16; o; o >>= 1) v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+        prefix += v2;
         if (incl) break;
         hi -= 32;
       }
@@ -141,11 +154,16 @@ k_scan_lookback(const int* __restrict__ in, long long n, int* __restrict__ out,
   ex += s_prefix;
 #pragma unroll
   for (int j = 0; j < kScanItems; j++) {
-    long long k = base + j;
-    if (k < n) out[k] = ex;
+    sm[pad32(threadIdx.x * kScanItems + j)] = ex;
     ex += v[j];
   }
-  if ((long long)(tile + 1) * kScanTile >= n && threadIdx.x == kScanThreads - 1)
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScanItems; j++) {           // coalesced stores
+    const int i = j * kScanThreads + threadIdx.x;
+    if (i < nt) out[t0 + i] = sm[pad32(i)];
+  }
+  if (t0 + kScanTile >= n && threadIdx.x == kScanThreads - 1)
     out[n] = s_prefix + tot;
 }
 
