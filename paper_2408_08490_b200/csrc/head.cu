@@ -3,104 +3,152 @@
 // (closes the loop of PAPER.md line 156 "forward ... backward
 // ... parameter update") and the SGD update.  Deterministic fixed-order sums.
 //
-// Three kernels for the classifier (deterministic, fixed-order sums):
-//  k_head_logits  logits = Hs Wc + bc          (64x64 SIMT tiles)
+// Three kernels for the classifier:
+//  k_head_logits  logits = Hs Wc + bc
 //  k_head_softmax warp per seed row: dlog = (softmax - onehot) / B, row loss;
 //                 the last block sums the per-block losses -> mean loss
 //  k_head_grads   one grid, two jobs: dHs = dlog Wc^T and dWc = Hs^T dlog
 //                 (+ dbc = column sums of dlog), both split over K with one
 //                 partial per slice; the last slice of a tile to finish
 //                 (atomic ticket) sums the partials in slice order.
+// The three GEMMs run on the tensor cores with mma.sync m16n8k8 TF32 in the
+// 3xTF32 split (x = hi + lo, hi = tf32(x), lo = tf32(x - hi); D += lo*hi +
+// hi*lo + hi*hi), which keeps fp32-level accuracy: the head is outside the
+// paper's stages and must not add TF32 error to the fp32 step.  These GEMMs
+// are tiny (B x 128 x C); what matters is parallelism and few dependent
+// memory round trips, not the tcgen05 peak.
 #include <algorithm>
 #include "common.cuh"
 
 namespace hf {
 
-static constexpr int kBK = 32;
+static constexpr int kBK = 32;             // K slab
+static constexpr int kBM = 32, kBN = 64;   // block tile; 4 warps of 16 x 32
 
-// One 64x64 tile of C = op(A) op(B) over k in [kb0, kb1): TA: A stored [K][M]
-// (else [M][K]); TB: B stored [N][K] (else [K][N]).  256 threads, 4x4 outputs
-// each (rows ty + 16i, cols tx + 16j), the next K slab prefetched into
-// registers while the current one is used.  colsum: also sum_k B[k][n] for
-// this thread's columns (used for dbc), valid in threads with ty == 0.
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], const uint32_t (&a)[4],
+                                                const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// One kBM x kBN tile of C = op(A) op(B) over k in [kb0, kb1) on 128 threads:
+// TA: A stored [K][M] (else [M][K]); TB: B stored [N][K] (else [K][N]).  Warp w
+// owns rows 16 (w / 2) .. +16 and columns 32 (w % 2) .. +32 (4 n-tiles of 8);
+// acc[nt][4] in the mma C-fragment layout.  K slabs are staged in shared
+// memory (padded: conflict-free fragment reads), the next slab prefetched
+// into registers.  colsum != nullptr: threads 0..kBN-1 also return
+// sum_k B[k][n0 + tid] there.
 template <bool TA, bool TB>
-__device__ __forceinline__ void gemm_tile(int M, int N, const float* __restrict__ A, int lda,
-                                          const float* __restrict__ B, int ldb, int m0, int n0,
-                                          int kb0, int kb1, float (&acc)[4][4], bool colsum,
-                                          float (&bsum)[4]) {
-  __shared__ float As[kBK][64 + 1];
-  __shared__ float Bs[kBK][64 + 1];
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+__device__ __forceinline__ void mma_tile(int M, int N, const float* __restrict__ A, int lda,
+                                         const float* __restrict__ B, int ldb, int m0, int n0,
+                                         int kb0, int kb1, float (&acc)[4][4], float* colsum) {
+  __shared__ float As[kBM][kBK + 4];
+  __shared__ float Bs[kBK][kBN + 8];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (w >> 1) * 16, wn = (w & 1) * 32;
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    bsum[i] = 0.f;
+  for (int i = 0; i < 4; i++)
 #pragma unroll
     for (int j = 0; j < 4; j++) acc[i][j] = 0.f;
-  }
-  float ra[8], rb[8];
+  float cs = 0.f;
+  float ra[8], rb[16];
   auto fetch = [&](int k0) {
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const int i = tid + 256 * q;
-      const int kk = TA ? i / 64 : i % kBK, mm = TA ? i % 64 : i / kBK;
+    for (int q = 0; q < 8; q++) {                 // A slab: kBM x kBK
+      const int i = tid + 128 * q;
+      const int kk = TA ? i / kBM : i % kBK, mm = TA ? i % kBM : i / kBK;
       const int m = m0 + mm, k = k0 + kk;
       ra[q] = (m < M && k < kb1) ? (TA ? A[(long long)k * lda + m] : A[(long long)m * lda + k]) : 0.f;
-      const int kb = TB ? i % kBK : i / 64, nb = TB ? i / kBK : i % 64;
-      const int n = n0 + nb, k2 = k0 + kb;
-      rb[q] = (n < N && k2 < kb1) ? (TB ? B[(long long)n * ldb + k2] : B[(long long)k2 * ldb + n]) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; q++) {                // B slab: kBK x kBN
+      const int i = tid + 128 * q;
+      const int kk = TB ? i % kBK : i / kBN, nn = TB ? i / kBK : i % kBN;
+      const int n = n0 + nn, k = k0 + kk;
+      rb[q] = (n < N && k < kb1) ? (TB ? B[(long long)n * ldb + k] : B[(long long)k * ldb + n]) : 0.f;
     }
   };
   if (kb0 < kb1) fetch(kb0);
   for (int k0 = kb0; k0 < kb1; k0 += kBK) {
 #pragma unroll
     for (int q = 0; q < 8; q++) {
-      const int i = tid + 256 * q;
-      As[TA ? i / 64 : i % kBK][TA ? i % 64 : i / kBK] = ra[q];
-      Bs[TB ? i % kBK : i / 64][TB ? i / kBK : i % 64] = rb[q];
+      const int i = tid + 128 * q;
+      As[TA ? i % kBM : i / kBK][TA ? i / kBM : i % kBK] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int i = tid + 128 * q;
+      Bs[TB ? i % kBK : i / kBN][TB ? i / kBK : i % kBN] = rb[q];
     }
     __syncthreads();
     if (k0 + kBK < kb1) fetch(k0 + kBK);
+    if (colsum && tid < kBN) {
+#pragma unroll 8
+      for (int kk = 0; kk < kBK; kk++) cs += Bs[kk][tid];
+    }
 #pragma unroll
-    for (int kk = 0; kk < kBK; kk++) {
-      float a[4], b[4];
+    for (int ks = 0; ks < kBK; ks += 8) {
+      uint32_t ah[4], al[4];
+      const float av[4] = {As[wm + g][ks + t], As[wm + g + 8][ks + t], As[wm + g][ks + t + 4],
+                           As[wm + g + 8][ks + t + 4]};
 #pragma unroll
-      for (int i = 0; i < 4; i++) a[i] = As[kk][ty + 16 * i];
+      for (int r = 0; r < 4; r++) {
+        ah[r] = to_tf32(av[r]);
+        al[r] = to_tf32(av[r] - __uint_as_float(ah[r]));
+      }
 #pragma unroll
-      for (int j = 0; j < 4; j++) b[j] = Bs[kk][tx + 16 * j];
+      for (int nt = 0; nt < 4; nt++) {
+        const int n = wn + nt * 8 + g;
+        const float bv[2] = {Bs[ks + t][n], Bs[ks + t + 4][n]};
+        uint32_t bh[2], bl[2];
 #pragma unroll
-      for (int i = 0; i < 4; i++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-      if (colsum) {
-#pragma unroll
-        for (int j = 0; j < 4; j++) bsum[j] += b[j];
+        for (int r = 0; r < 2; r++) {
+          bh[r] = to_tf32(bv[r]);
+          bl[r] = to_tf32(bv[r] - __uint_as_float(bh[r]));
+        }
+        mma_tf32_16x8x8(acc[nt], al, bh);
+        mma_tf32_16x8x8(acc[nt], ah, bl);
+        mma_tf32_16x8x8(acc[nt], ah, bh);
       }
     }
     __syncthreads();
   }
+  if (colsum && tid < kBN) *colsum = cs;
 }
 
-__global__ void __launch_bounds__(256)
+// C-fragment coordinates of acc[nt][r], relative to the tile
+__device__ __forceinline__ int frag_row(int r) {
+  return ((threadIdx.x >> 5) >> 1) * 16 + ((threadIdx.x & 31) >> 2) + (r >= 2 ? 8 : 0);
+}
+__device__ __forceinline__ int frag_col(int nt, int r) {
+  return ((threadIdx.x >> 5) & 1) * 32 + nt * 8 + (threadIdx.x & 3) * 2 + (r & 1);
+}
+
+__global__ void __launch_bounds__(128)
 k_head_logits(int B, int D, int C, const float* __restrict__ Hs, const float* __restrict__ Wc,
               const float* __restrict__ bc, float* __restrict__ lg, int* __restrict__ tickets,
               int ntickets) {
   if (blockIdx.x == 0 && blockIdx.y == 0)   // tickets of the next two kernels
     for (int i = threadIdx.x; i < ntickets; i += blockDim.x) tickets[i] = 0;
-  float acc[4][4], bs[4];
-  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  gemm_tile<false, false>(B, C, Hs, D, Wc, C, m0, n0, 0, D, acc, false, bs);
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4];
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  mma_tile<false, false>(B, C, Hs, D, Wc, C, m0, n0, 0, D, acc, nullptr);
 #pragma unroll
-  for (int j = 0; j < 4; j++) {
-    const int n = n0 + tx + 16 * j;
-    if (n >= C) continue;
-    const float bv = __ldg(bc + n);
+  for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const int m = m0 + ty + 16 * i;
-      if (m < B) lg[(long long)m * C + n] = acc[i][j] + bv;
+    for (int r = 0; r < 4; r++) {
+      const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
+      if (m < B && n < C) lg[(long long)m * C + n] = acc[nt][r] + __ldg(bc + n);
     }
-  }
 }
 
 // 8 rows (one per warp) per block; lg is turned into dlog in place.
@@ -151,8 +199,8 @@ struct HeadGrid {
   int dw_tiles_n, dw_tiles, dw_split;       // dWc: [D, C] tiles, K = B
 };
 
-// Sum of the nz slice partials of one 64x64 tile, in slice order, by the last
-// slice block to finish.  Returns false in the other blocks.
+// True in the block that finished last among the nz slices of a tile (its
+// partials are then visible to it).
 __device__ __forceinline__ bool last_slice(int* ticket, int nz) {
   __shared__ int s_last;
   __threadfence();
@@ -163,122 +211,125 @@ __device__ __forceinline__ bool last_slice(int* ticket, int nz) {
   return s_last;
 }
 
-__global__ void __launch_bounds__(256)
+// Sum of nz slice partials (slice stride `ss`) of this thread's 16 fragment
+// outputs, two slices' loads in flight at a time, slices added in order.
+__device__ __forceinline__ void reduce_slices(const float* __restrict__ part, long long ss, int nz,
+                                              int m0, int n0, int M, int N, int ld,
+                                              float* __restrict__ out) {
+  float tsum[4][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+    for (int r = 0; r < 4; r++) tsum[nt][r] = 0.f;
+  for (int z0 = 0; z0 < nz; z0 += 2) {
+    float v[2][4][4];
+#pragma unroll
+    for (int u = 0; u < 2; u++)
+#pragma unroll
+      for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
+          v[u][nt][r] = (z0 + u < nz && m < M && n < N)
+                            ? __ldcg(part + (z0 + u) * ss + (long long)m * ld + n) : 0.f;
+        }
+#pragma unroll
+    for (int u = 0; u < 2; u++)
+#pragma unroll
+      for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+        for (int r = 0; r < 4; r++) tsum[nt][r] += v[u][nt][r];
+  }
+#pragma unroll
+  for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
+      if (m < M && n < N) out[(long long)m * ld + n] = tsum[nt][r];
+    }
+}
+
+__global__ void __launch_bounds__(128)
 k_head_grads(int B, int D, int C, HeadGrid hg, const float* __restrict__ Hs,
              const float* __restrict__ Wc, const float* __restrict__ dlog,
              float* __restrict__ part_h, float* __restrict__ part_w, float* __restrict__ part_b,
              int* __restrict__ tickets, float* __restrict__ dHs, float* __restrict__ dWc,
              float* __restrict__ dbc) {
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  float acc[4][4], bs[4];
+  float acc[4][4];
   int bid = blockIdx.x;
   const int nh = hg.dh_tiles * hg.dh_split;
   if (bid < nh) {
     // ---- dHs = dlog Wc^T: M = B, N = D, K = C; Wc stored [D][C] = [N][K]
     const int tile = bid / hg.dh_split, z = bid % hg.dh_split;
-    const int m0 = (tile / hg.dh_tiles_n) * 64, n0 = (tile % hg.dh_tiles_n) * 64;
-    const int kper = (C + hg.dh_split - 1) / hg.dh_split;
-    gemm_tile<false, true>(B, D, dlog, C, Wc, C, m0, n0, z * kper, min(C, (z + 1) * kper), acc,
-                           false, bs);
+    const int m0 = (tile / hg.dh_tiles_n) * kBM, n0 = (tile % hg.dh_tiles_n) * kBN;
+    const int kper = ((C + hg.dh_split - 1) / hg.dh_split + kBK - 1) / kBK * kBK;
+    mma_tile<false, true>(B, D, dlog, C, Wc, C, m0, n0, z * kper, min(C, (z + 1) * kper), acc,
+                          nullptr);
+    if (hg.dh_split == 1) {
+#pragma unroll
+      for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
+          if (m < B && n < D) dHs[(long long)m * D + n] = acc[nt][r];
+        }
+      return;
+    }
     float* P = part_h + (long long)z * B * D;
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-        if (m < B && n < D) P[(long long)m * D + n] = acc[i][j];
+      for (int r = 0; r < 4; r++) {
+        const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
+        if (m < B && n < D) P[(long long)m * D + n] = acc[nt][r];
       }
     if (!last_slice(&tickets[tile], hg.dh_split)) return;
-    // all slices' values of a row of 4 outputs in flight together
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const int m = m0 + ty + 16 * i;
-      float v[4][4];
-#pragma unroll
-      for (int zz = 0; zz < 4; zz++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int n = n0 + tx + 16 * j;
-          v[zz][j] = (zz < hg.dh_split && m < B && n < D)
-                         ? __ldcg(part_h + (long long)zz * B * D + (long long)m * D + n) : 0.f;
-        }
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int n = n0 + tx + 16 * j;
-        float t = v[0][j];
-#pragma unroll
-        for (int zz = 1; zz < 4; zz++) t += v[zz][j];
-        if (m < B && n < D) dHs[(long long)m * D + n] = t;
-      }
-    }
+    reduce_slices(part_h, (long long)B * D, hg.dh_split, m0, n0, B, D, D, dHs);
     return;
   }
   // ---- dWc = Hs^T dlog: M = D, N = C, K = B; Hs stored [B][D] = [K][M]
   bid -= nh;
   const int tile = bid / hg.dw_split, z = bid % hg.dw_split;
-  const int m0 = (tile / hg.dw_tiles_n) * 64, n0 = (tile % hg.dw_tiles_n) * 64;
+  const int m0 = (tile / hg.dw_tiles_n) * kBM, n0 = (tile % hg.dw_tiles_n) * kBN;
   const int kper = ((B + hg.dw_split - 1) / hg.dw_split + kBK - 1) / kBK * kBK;
   const bool bias = m0 == 0;            // the first row tile also forms dbc
-  gemm_tile<true, false>(D, C, Hs, D, dlog, C, m0, n0, z * kper, min(B, (z + 1) * kper), acc,
-                         bias, bs);
+  float cs = 0.f;
+  mma_tile<true, false>(D, C, Hs, D, dlog, C, m0, n0, z * kper, min(B, (z + 1) * kper), acc,
+                        bias ? &cs : nullptr);
   float* P = part_w + (long long)z * D * C;
 #pragma unroll
-  for (int i = 0; i < 4; i++)
+  for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-      if (m < D && n < C) P[(long long)m * C + n] = acc[i][j];
+    for (int r = 0; r < 4; r++) {
+      const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
+      if (m < D && n < C) P[(long long)m * C + n] = acc[nt][r];
     }
-  if (bias && ty == 0)
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int n = n0 + tx + 16 * j;
-      if (n < C) part_b[(long long)z * C + n] = bs[j];
-    }
+  if (bias && threadIdx.x < kBN && n0 + (int)threadIdx.x < C)
+    part_b[(long long)z * C + n0 + threadIdx.x] = cs;
   if (!last_slice(&tickets[hg.dh_tiles + tile], hg.dw_split)) return;
-  // 4 outputs x 8 slices in flight per round, summed in slice order
-  for (int i = 0; i < 4; i++) {
-    const int m = m0 + ty + 16 * i;
-    float t[4] = {0.f, 0.f, 0.f, 0.f};
+  reduce_slices(part_w, (long long)D * C, hg.dw_split, m0, n0, D, C, C, dWc);
+  if (bias && threadIdx.x < kBN && n0 + (int)threadIdx.x < C) {
+    const int n = n0 + threadIdx.x;
+    float t = 0.f;
     for (int z0 = 0; z0 < hg.dw_split; z0 += 8) {
-      float v[8][4];
+      float v[8];
 #pragma unroll
       for (int u = 0; u < 8; u++)
+        v[u] = z0 + u < hg.dw_split ? __ldcg(part_b + (long long)(z0 + u) * C + n) : 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int n = n0 + tx + 16 * j;
-          v[u][j] = (z0 + u < hg.dw_split && m < D && n < C)
-                        ? __ldcg(part_w + (long long)(z0 + u) * D * C + (long long)m * C + n) : 0.f;
-        }
-#pragma unroll
-      for (int u = 0; u < 8; u++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) t[j] += v[u][j];
+      for (int u = 0; u < 8; u++) t += v[u];
     }
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int n = n0 + tx + 16 * j;
-      if (m < D && n < C) dWc[(long long)m * C + n] = t[j];
-    }
+    dbc[n] = t;
   }
-  if (bias && ty == 0)
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int n = n0 + tx + 16 * j;
-      if (n >= C) continue;
-      float t = 0.f;
-      for (int zz = 0; zz < hg.dw_split; zz++) t += __ldcg(part_b + (long long)zz * C + n);
-      dbc[n] = t;
-    }
 }
 
 static HeadGrid head_grid(int B, int D, int C) {
   HeadGrid h;
-  h.dh_tiles_n = (int)ceil_div(D, 64);
-  h.dh_tiles = h.dh_tiles_n * (int)ceil_div(B, 64);
-  h.dh_split = (int)std::max<long long>(1, std::min<long long>(ceil_div(C, 128), 4));   // <= 4
-  h.dw_tiles_n = (int)ceil_div(C, 64);
-  h.dw_tiles = h.dw_tiles_n * (int)ceil_div(D, 64);
+  h.dh_tiles_n = (int)ceil_div(D, kBN);
+  h.dh_tiles = h.dh_tiles_n * (int)ceil_div(B, kBM);
+  h.dh_split = (int)std::max<long long>(1, std::min<long long>(ceil_div(C, 256), 4));
+  h.dw_tiles_n = (int)ceil_div(C, kBN);
+  h.dw_tiles = h.dw_tiles_n * (int)ceil_div(D, kBM);
   h.dw_split = (int)std::max<long long>(1, std::min<long long>(ceil_div(B, 128), 32));
   return h;
 }
@@ -338,11 +389,11 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   if (h_row0 + B < h_rows)
     cudaMemsetAsync(d_dH + (h_row0 + B) * D, 0, sizeof(float) * (h_rows - h_row0 - B) * D, s);
   const float* Hs = d_H + h_row0 * D;
-  HF_LAUNCH(k_head_logits, dim3(ceil_div(C, 64), ceil_div(B, 64)), 256, 0, s, B, D, C, Hs, d_Wc,
+  HF_LAUNCH(k_head_logits, dim3(ceil_div(C, kBN), ceil_div(B, kBM)), 128, 0, s, B, D, C, Hs, d_Wc,
             d_bc, dlog, tickets, ntk);
   HF_LAUNCH(k_head_softmax, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, tickets + ntk - 1,
             d_loss);
-  HF_LAUNCH(k_head_grads, h.dh_tiles * h.dh_split + h.dw_tiles * h.dw_split, 256, 0, s, B, D, C,
+  HF_LAUNCH(k_head_grads, h.dh_tiles * h.dh_split + h.dw_tiles * h.dw_split, 128, 0, s, B, D, C,
             h, Hs, d_Wc, dlog, part_h, part_w, part_b, tickets, d_dH + h_row0 * D, d_dWc, d_dbc);
   return last_cuda();
 }
