@@ -17,6 +17,7 @@
 // The projection is HBM-bound at K = D = 64/128 (32 flop/B), so the design
 // goal is streaming A at full bandwidth with enough CTAs per SM (64 KB smem,
 // <=128 TMEM columns each -> 3-4 CTAs/SM) rather than peak MMA rate.
+#include <algorithm>
 #include <cstdlib>
 #include "project.cuh"
 #include "tc_common.cuh"
@@ -61,42 +62,66 @@ __device__ __forceinline__ long long tc_a_row(const ProjMeta& pm, const int* rel
 namespace hf {
 
 // ----------------------------------------------------------------- dgrad ----
-// Tile = 128 source rows of one type s; the "K loop" runs over the terms
-// (relations out of s, then the root weight) x D/32 chunks.  A chunk: 32
-// columns of dYt rows gathered through slot_y (zero rows where the source has
-// no edge of that relation); B chunk: W_term[k][d0..d0+32) for every k, which
-// is already K-major (row k contiguous in d).  N = K.
-static constexpr int kDgStages = 4;
+// Tile = 128 source rows of one type s x KN output features (the K output
+// columns split into NS = K / KN CTAs, so a small layer still puts two CTAs
+// and twice the loads in flight on every SM); the "K loop" runs over the
+// terms (relations out of s, then the root weight) x D/32 chunks.  A chunk:
+// 32 columns of dYt rows gathered through slot_y (zero rows where the source
+// has no edge of that relation); B chunk: W_term[k][d0..d0+32) for the CTA's
+// KN features k, which is already K-major (row k contiguous in d).
+#ifndef HF_DG_STAGES
+#define HF_DG_STAGES 4
+#endif
+static constexpr int kDgStages = HF_DG_STAGES;
+static constexpr int kDgAhead = kDgStages - 2;
 
-template <int K, int D>
+template <int K, int D, int KN>
 __global__ void __launch_bounds__(128)
 k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
            const float* __restrict__ G, const float* __restrict__ W_rel,
-           const float* __restrict__ W_root, float* __restrict__ dX) {
-  constexpr int BM = 128, DC = D / 32;
-  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = K * 128, STAGE = A_STAGE + B_STAGE;
-  constexpr uint32_t IDESC = idesc_tf32(BM, K, 0, 0);
+           const float* __restrict__ W_root, float* __restrict__ dX, int max_out) {
+  constexpr int BM = 128, DC = D / 32, NS = K / KN;
+  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = KN * 128, STAGE = A_STAGE + B_STAGE;
+  constexpr uint32_t IDESC = idesc_tf32(BM, KN, 0, 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bars[kDgStages];
   __shared__ uint32_t tmem_slot;
-  const int s_ = upper_bound_i(dm.tile_off, dm.T + 1, blockIdx.x) - 1;
-  const int j0 = (blockIdx.x - dm.tile_off[s_]) * BM;
+  const int tile = blockIdx.x / NS, n0 = (blockIdx.x % NS) * KN;
+  const int s_ = upper_bound_i(dm.tile_off, dm.T + 1, tile) - 1;
+  const int j0 = (tile - dm.tile_off[s_]) * BM;
   const int nrows = min(BM, dm.n_src[s_] - j0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  int* s_arow = reinterpret_cast<int*>(smem_raw + (base - smem_u32(smem_raw)) + kDgStages * STAGE);
   if (tid == 0) {
     for (int q = 0; q < kDgStages; q++) mbar_init(smem_u32(&bars[q]), 1);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), K);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), KN < 32 ? 32 : KN);
   const int nout = dm.out_off[s_ + 1] - dm.out_off[s_];
   const int nterm = nout + (dm.has_root ? 1 : 0);
   const int NC = nterm * DC;
   const int j = j0 + tid;
+  // dYt row of every (term, tile row), fetched once up front with all loads in
+  // flight (a slot_y load inside every chunk would serialise one round trip
+  // per chunk before its cp.async could issue)
+  for (int t0 = 0; t0 < nout; t0 += 8) {
+    int v[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int term = t0 + u;
+      v[u] = (term < nout && tid < nrows)
+                 ? slot_y[dm.slot_off[dm.out_rel[dm.out_off[s_] + term]] + j] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (t0 + u < nout) s_arow[(t0 + u) * 128 + tid] = v[u];
+  }
+  (void)max_out;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
 
   auto load = [&](int c, int st) {
     const int term = c / DC, d0 = (c % DC) * 32;
@@ -108,7 +133,7 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
       W = W_root + (long long)s_ * K * D;
     } else {
       const int r = dm.out_rel[dm.out_off[s_] + term];
-      if (tid < nrows) a = slot_y[dm.slot_off[r] + j];
+      a = s_arow[term * 128 + tid];
       W = W_rel + (long long)r * K * D;
     }
     const float* A = root ? G : dY;
@@ -117,21 +142,23 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
     const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
 #pragma unroll
     for (int q = 0; q < 8; q++) cp_async16(sa + sw128_off(tid, q), arow + q * 4, abytes);
-    if (tid < K) {
-      const float* brow = W + (long long)tid * D + d0;
+    if (tid < KN) {
+      const float* brow = W + (long long)(n0 + tid) * D + d0;
 #pragma unroll
       for (int q = 0; q < 8; q++) cp_async16(sb + sw128_off(tid, q), brow + q * 4, 16);
     }
     cp_async_commit();
   };
 
-  for (int c = 0; c < kDgStages - 1; c++) {
+  // loads run kDgAhead chunks ahead; a stage is refilled two chunks after its
+  // MMA was issued, so the tensor core never stalls the load issue
+  for (int c = 0; c < kDgAhead; c++) {
     if (c < NC) load(c, c);
     else cp_async_commit();
   }
   for (int c = 0; c < NC; c++) {
     const int st = c % kDgStages;
-    const int nxt = c + kDgStages - 1;
+    const int nxt = c + kDgAhead;
     if (nxt < NC) {
       const int ns = nxt % kDgStages;
       if (nxt >= kDgStages) mbar_wait(smem_u32(&bars[ns]), ((nxt / kDgStages) - 1) & 1);
@@ -139,7 +166,7 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
     } else {
       cp_async_commit();
     }
-    cp_async_wait<kDgStages - 1>();
+    cp_async_wait<kDgAhead>();
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
@@ -158,9 +185,9 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
     tc_fence_after();
   }
   const int row = warp * 32 + lane;
-  float* orow = dX + (long long)(dm.type_src_off[s_] + j0 + row) * K;
+  float* orow = dX + (long long)(dm.type_src_off[s_] + j0 + row) * K + n0;
 #pragma unroll
-  for (int c0 = 0; c0 < K; c0 += 16) {
+  for (int c0 = 0; c0 < KN; c0 += 16) {
     float v[16];
     if (NC > 0) {
       tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
@@ -178,7 +205,7 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, K);
+  if (warp == 0) tmem_dealloc(tmem, KN < 32 ? 32 : KN);
 }
 
 __device__ __forceinline__ void group_table_warp(const ProjMeta& pm, const int* s_yoff, int step,
@@ -340,31 +367,45 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
   if (warp == 0) tmem_dealloc(tmem, D);
 }
 
-template <int K, int D>
-static constexpr int dgrad_smem() { return kDgStages * (128 * 128 + K * 128) + 1024; }
+template <int K, int D, int KN>
+static constexpr int dgrad_smem() { return kDgStages * (128 * 128 + KN * 128) + 1024; }
 template <int K, int D>
 static constexpr int wgrad_smem() { return kWgStages * (4 * 4096 + (D / 32) * 4096) + 1024; }
+
+template <int K, int D, int KN>
+static void launch_dgrad(const DgradMeta& dm, int max_out, const int* slot_y, const float* dY,
+                         const float* G, const float* W_rel, const float* W_root, float* dX,
+                         cudaStream_t s) {
+  const int smem = dgrad_smem<K, D, KN>() + max_out * 128 * 4;
+  static int attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_dgrad_tc<K, D, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = smem;
+  }
+  const unsigned grid = (unsigned)dm.tile_off[dm.T] * (K / KN);
+  HF_LAUNCH((k_dgrad_tc<K, D, KN>), grid, 128, smem, s, dm, slot_y, dY, G, W_rel, W_root, dX,
+            max_out);
+}
 
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
                               const float* dY, const float* G, const float* W_rel,
                               const float* W_root, float* dX, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dgrad_tc<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<128, 128>());
-    cudaFuncSetAttribute(k_dgrad_tc<128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<128, 64>());
-    cudaFuncSetAttribute(k_dgrad_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<64, 128>());
-    cudaFuncSetAttribute(k_dgrad_tc<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, dgrad_smem<64, 64>());
-    attr = true;
+  int max_out = 0;
+  for (int t = 0; t < dm.T; t++) max_out = std::max(max_out, dm.out_off[t + 1] - dm.out_off[t]);
+  if (max_out > 128) return HIFUSE_ERR_UNSUPPORTED;
+  // split the output features over two CTAs when that still leaves a small grid
+  const bool split = K == 128 && dm.tile_off[dm.T] < 2 * 148;
+  if (K == 128 && D == 128) {
+    if (split) launch_dgrad<128, 128, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+    else launch_dgrad<128, 128, 128>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+  } else if (K == 128 && D == 64) {
+    if (split) launch_dgrad<128, 64, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+    else launch_dgrad<128, 64, 128>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+  } else if (K == 64 && D == 128) {
+    launch_dgrad<64, 128, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+  } else {
+    launch_dgrad<64, 64, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
   }
-  unsigned grid = dm.tile_off[dm.T];
-#define HF_DG(KK, DD)                                                                        \
-  HF_LAUNCH((k_dgrad_tc<KK, DD>), grid, 128, (dgrad_smem<KK, DD>()), s, dm, slot_y, dY, G,   \
-            W_rel, W_root, dX)
-  if (K == 128 && D == 128) HF_DG(128, 128);
-  else if (K == 128 && D == 64) HF_DG(128, 64);
-  else if (K == 64 && D == 128) HF_DG(64, 128);
-  else HF_DG(64, 64);
-#undef HF_DG
   return HIFUSE_OK;
 }
 

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhifuse.so")
+# HIFUSE_LIB: an alternative build of the same library (experiments only)
+LIB_PATH = os.environ.get("HIFUSE_LIB") or os.path.join(_HERE, "libhifuse.so")
 
 AGG = {"sum": 0, "mean": 1, "gat": 2}
 ACT = {"none": 0, "relu": 1}
