@@ -302,6 +302,7 @@ def main():
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
                  prec=args.prec, order=args.order)
     tr.load_params(params)
+    tr.prepare_graph(et_d)           # relation-major edge ids -> R+1 offsets (once per graph)
     allreduce = (lambda t: allreduce_grads(t, world)) if world > 1 else None
     # sizing pass: every pool batch once, eagerly (buffers reach final size)
     for db in pool:
@@ -416,6 +417,7 @@ def main():
                      cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
                      prec=args.prec, order=other_order)
         tr.load_params(params)
+        tr.prepare_graph(et_d)
         for db in pool:
             tr.step(db, feat_d, et_d, allreduce=allreduce, world=world, update=False)
         torch.cuda.synchronize()

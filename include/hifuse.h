@@ -69,6 +69,7 @@ typedef enum {
 #define HIFUSE_ST_BAD_REL     2   /* edge_type[edge_id] not in [0, R)           */
 #define HIFUSE_ST_BAD_SRC     4   /* src_local >= n_src(src type of relation)   */
 #define HIFUSE_ST_BAD_DST     8   /* dst_local >= n_dst(dst type of relation)   */
+#define HIFUSE_ST_UNSORTED_TYPES 16 /* edge_type not relation-major (offsets unusable) */
 
 typedef enum { HIFUSE_AGG_SUM = 0, HIFUSE_AGG_MEAN = 1, HIFUSE_AGG_GAT = 2 } hifuse_agg;
 typedef enum { HIFUSE_ACT_NONE = 0, HIFUSE_ACT_RELU = 1 } hifuse_act;
@@ -137,7 +138,13 @@ hifuse_status hifuse_csr_sizes(const hifuse_layer_shape *shape, hifuse_layout la
  * producing the merged segmented CSR/CSC of each layer in `out[l]`.
  *   d_src_local[l], d_dst_local[l]: int32 [N_l] batch-local endpoint ids;
  *   d_edge_id[l]: int64 [N_l] graph-global edge ids;
- *   d_edge_type: int32 [num_graph_edges] relation of every graph edge.
+ *   d_edge_type: int32 [num_graph_edges] relation of every graph edge;
+ *   d_rel_edge_off: NULL, or int64 [R+1] with d_edge_type relation-major
+ *     (global edge ids sorted by relation): relation r owns ids
+ *     [off[r], off[r+1]).  EdgeType[EdgeID] (Alg. 2) is then
+ *     evaluated by a binary search over the R+1 offsets instead of a random
+ *     4-byte gather from the graph-sized table (same result); build the
+ *     offsets once per graph with hifuse_edge_type_offsets().
  * Workspace: d_ws of at least max_l build_ws_bytes(l).  d_status: int32 [1],
  * bits ORed (never cleared by the library).  Layers run back to back on
  * `stream`; kernel count is independent of R. */
@@ -146,9 +153,19 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape *shapes, int
                                            const int32_t *const *d_dst_local,
                                            const int64_t *const *d_edge_id,
                                            const int32_t *d_edge_type, int64_t num_graph_edges,
+                                           const int64_t *d_rel_edge_off,
                                            hifuse_layout layout, const hifuse_csr *out,
                                            void *d_ws, size_t ws_bytes, int32_t *d_status,
                                            hifuse_stream_t stream);
+
+/* One-time graph preprocessing for the build: d_rel_edge_off[r] = first edge
+ * id of relation r (lower bound of r in d_edge_type), r = 0..R, if
+ * d_edge_type is sorted ascending (relation-major ids).  If it is not sorted
+ * (or holds a relation id outside [0, R)), HIFUSE_ST_UNSORTED_TYPES is ORed
+ * into *d_status and the offsets must not be used. */
+hifuse_status hifuse_edge_type_offsets(const int32_t *d_edge_type, int64_t num_graph_edges,
+                                       int num_rels, int64_t *d_rel_edge_off, int32_t *d_status,
+                                       hifuse_stream_t stream);
 
 /* A2+A3. Feature projection (readings C3, C4, C6, C7), one
  * grouped GEMM launch over groups {relation r} u {root type t}:

@@ -27,8 +27,14 @@ namespace hf {
 
 __global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* __restrict__ dst,
                            const long long* __restrict__ eid, const int* __restrict__ edge_type,
-                           long long E, int* __restrict__ key_e, int* __restrict__ slot_e,
+                           const long long* __restrict__ rel_off, long long E,
+                           int* __restrict__ key_e, int* __restrict__ slot_e,
                            int* __restrict__ cnt, int* __restrict__ status) {
+  __shared__ long long s_off[HF_MAX_R + 1];
+  if (rel_off) {
+    for (int i = threadIdx.x; i <= m.R; i += blockDim.x) s_off[i] = rel_off[i];
+    __syncthreads();
+  }
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m.N) return;
   long long id = eid[e];
@@ -37,7 +43,18 @@ __global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* 
   if (id < 0 || id >= E) {
     bad = HIFUSE_ST_BAD_EDGE_ID;
   } else {
-    r = edge_type[id];                                   // Alg. 2
+    // Alg. 2: EdgeTypeLayer = EdgeType[EdgeID] -- a gather, or for a
+    // relation-major table the relation whose id range holds `id`
+    if (rel_off) {
+      int lo = 0, hi = m.R;                              // s_off[lo] <= id < s_off[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_off[mid] <= id) lo = mid; else hi = mid;
+      }
+      r = lo;
+    } else {
+      r = edge_type[id];
+    }
     if (r < 0 || r >= m.R) bad = HIFUSE_ST_BAD_REL;
     else if (s < 0 || s >= m.n_src[m.rel_src[r]]) bad = HIFUSE_ST_BAD_SRC;
     else if (d < 0 || d >= m.n_dst[m.rel_dst[r]]) bad = HIFUSE_ST_BAD_DST;
@@ -53,6 +70,26 @@ __global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* 
   slot_e[e] = slot;
   atomicAdd(&cnt[key], 1);
   cnt[m.rows + slot] = 1;                                // presence flag (idempotent)
+}
+
+// d_rel_edge_off[r] = lower bound of r in the (sorted) edge-type table.
+__global__ void k_et_offsets(const int* __restrict__ et, long long E, int R,
+                             long long* __restrict__ off) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > R) return;
+  long long lo = 0, hi = E;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (et[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  off[r] = r == R ? E : lo;
+}
+
+__global__ void k_et_check(const int* __restrict__ et, long long E, int R, int* __restrict__ status) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const int v = et[i];
+  if (v < 0 || v >= R || (i > 0 && et[i - 1] > v)) atomicOr(status, HIFUSE_ST_UNSORTED_TYPES);
 }
 
 // pre = exclusive scan of [row counts | slot flags]; pre[rows] = valid edges,
@@ -123,29 +160,68 @@ __device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
     }
 }
 
+// Bitonic sort of 16 (key, value) pairs held by the 16 lanes of a half warp
+// (hl = lane within the half); both halves of the warp sort independently.
+__device__ __forceinline__ void half_sort_regs(int& key, int& val, int hl) {
+#pragma unroll
+  for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      int pk = __shfl_xor_sync(0xffffffffu, key, j);
+      int pv = __shfl_xor_sync(0xffffffffu, val, j);
+      bool up = (hl & k) == 0;
+      bool lower = (hl & j) == 0;
+      bool take_min = lower == up;
+      bool swap = take_min ? (pk < key) : (pk > key);
+      if (swap) { key = pk; val = pv; }
+    }
+}
+
+__device__ __forceinline__ void place_sorted(int row, int b, int i, int key, int val,
+                                             int* eperm, int* col, const int* col_ptr, int* ccur,
+                                             int* csc_pos, int* csc_row) {
+  eperm[b + i] = key;
+  col[b + i] = val;
+  if (col_ptr) {
+    int w = col_ptr[val] + atomicAdd(&ccur[val], 1);
+    csc_pos[w] = b + i;
+    csc_row[w] = row;
+  }
+}
+
+// Two rows per warp: a row of <= 16 entries is sorted by its half warp (10
+// compare-exchange stages instead of 15 over a full warp); rows of 17..32 are
+// then sorted one after another by the whole warp; longer rows go to
+// k_sort_long.  Then the sorted row is placed into the CSC.
 __global__ void __launch_bounds__(256)
 k_fix_rows(int rows, const int* __restrict__ row_ptr, int* eperm, int* col,
            const int* __restrict__ col_ptr, int* ccur, int* csc_pos, int* csc_row, int* long_list,
            int* long_cnt) {
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const int b = row_ptr[row], e = row_ptr[row + 1], n = e - b;
-  if (n > 32) {
-    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = row;
-    return;
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 2;
+  if (row0 >= rows) return;
+  const int row = row0 + (lane >> 4);
+  int b = 0, n = 0;
+  if (row < rows) {
+    b = row_ptr[row];
+    n = row_ptr[row + 1] - b;
   }
-  int key = lane < n ? eperm[b + lane] : 0x7fffffff;
-  int val = lane < n ? col[b + lane] : 0;
-  if (n > 1) warp_sort_regs(key, val, lane);
-  if (lane < n) {
-    eperm[b + lane] = key;
-    col[b + lane] = val;
-    if (col_ptr) {
-      int w = col_ptr[val] + atomicAdd(&ccur[val], 1);
-      csc_pos[w] = b + lane;
-      csc_row[w] = row;
-    }
+  if (n > 32 && hl == 0) long_list[atomicAdd(long_cnt, 1)] = row;
+  const bool small = n <= 16;
+  int key = (small && hl < n) ? eperm[b + hl] : 0x7fffffff;
+  int val = (small && hl < n) ? col[b + hl] : 0;
+  if (__any_sync(0xffffffffu, small && n > 1)) half_sort_regs(key, val, hl);
+  if (small && hl < n) place_sorted(row, b, hl, key, val, eperm, col, col_ptr, ccur, csc_pos, csc_row);
+  unsigned mid = __ballot_sync(0xffffffffu, hl == 0 && n > 16 && n <= 32);
+  while (mid) {
+    const int src = __ffs(mid) - 1;
+    mid &= mid - 1;
+    const int bb = __shfl_sync(0xffffffffu, b, src), nn = __shfl_sync(0xffffffffu, n, src);
+    const int rr = row0 + (src >> 4);
+    int k2 = lane < nn ? eperm[bb + lane] : 0x7fffffff;
+    int v2 = lane < nn ? col[bb + lane] : 0;
+    warp_sort_regs(k2, v2, lane);
+    if (lane < nn) place_sorted(rr, bb, lane, k2, v2, eperm, col, col_ptr, ccur, csc_pos, csc_row);
   }
 }
 
@@ -404,12 +480,14 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
                                            const int32_t* const* d_dst_local,
                                            const int64_t* const* d_edge_id,
                                            const int32_t* d_edge_type, int64_t num_graph_edges,
+                                           const int64_t* d_rel_edge_off,
                                            hifuse_layout layout, const hifuse_csr* out,
                                            void* d_ws, size_t ws_bytes, int32_t* d_status,
                                            hifuse_stream_t stream) {
   if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
   if (!shapes || num_layers <= 0 || !d_src_local || !d_dst_local || !d_edge_id || !out ||
-      !d_status || num_graph_edges < 0 || (num_graph_edges > 0 && !d_edge_type))
+      !d_status || num_graph_edges < 0 ||
+      (num_graph_edges > 0 && !d_edge_type && !d_rel_edge_off))
     return HIFUSE_ERR_INVALID_ARG;
   cudaStream_t s = st(stream);
   static const int dbg = getenv("HIFUSE_DBG_SORT") ? atoi(getenv("HIFUSE_DBG_SORT")) : 0;
@@ -449,7 +527,8 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     cudaMemsetAsync(w.counters, 0, sizeof(int) * 2, s);
     const int TB = 256;
     HF_LAUNCH(k_classify, ceil_div(m.N, TB), TB, 0, s, m, d_src_local[l], d_dst_local[l],
-              (const long long*)d_edge_id[l], d_edge_type, (long long)num_graph_edges, w.key_e,
+              (const long long*)d_edge_id[l], d_edge_type, (const long long*)d_rel_edge_off,
+              (long long)num_graph_edges, w.key_e,
               w.slot_e, w.cnt, d_status);
     exclusive_scan(w.cnt, w.pre, nz, w.scan, s);
     long long fin = nz + 1 > m.R + 1 ? nz + 1 : m.R + 1;
@@ -460,7 +539,7 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     if (csc) exclusive_scan(w.ccnt, o.col_ptr, U_max, w.scan, s);
     int* rows_long = w.lists;
     int* cols_long = w.lists + m.rows;
-    HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 8), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
+    HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 16), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
               o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
     HF_LAUNCH(k_sort_long<true>, 148, kSortThreads, 0, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
               o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv, dbg);
@@ -471,6 +550,21 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
               (const int*)nullptr, (int*)nullptr, (int*)nullptr, (int*)nullptr, cols_long,
               w.counters + 1, w.gk, w.gv, dbg);
   }
+  return last_cuda();
+}
+
+hifuse_status hifuse_edge_type_offsets(const int32_t* d_edge_type, int64_t num_graph_edges,
+                                       int num_rels, int64_t* d_rel_edge_off, int32_t* d_status,
+                                       hifuse_stream_t stream) {
+  if (num_graph_edges < 0 || num_rels <= 0 || num_rels > HF_MAX_R || !d_rel_edge_off ||
+      !d_status || (num_graph_edges > 0 && !d_edge_type))
+    return HIFUSE_ERR_INVALID_ARG;
+  cudaStream_t s = st(stream);
+  if (num_graph_edges > 0)
+    HF_LAUNCH(k_et_check, ceil_div(num_graph_edges, 256), 256, 0, s, d_edge_type,
+              (long long)num_graph_edges, num_rels, d_status);
+  HF_LAUNCH(k_et_offsets, ceil_div(num_rels + 1, 64), 64, 0, s, d_edge_type,
+            (long long)num_graph_edges, num_rels, (long long*)d_rel_edge_off);
   return last_cuda();
 }
 

@@ -57,7 +57,9 @@ def lib():
                                  ctypes.c_size_t)
         sig = {
             "hifuse_csr_sizes": [vp, i32, vp, vp, vp, vp],
-            "hifuse_build_semantic_graphs": [vp, i32, vp, vp, vp, vp, i64, i32, vp, vp, sz, vp, vp],
+            "hifuse_build_semantic_graphs": [vp, i32, vp, vp, vp, vp, i64, vp, i32, vp, vp, sz, vp,
+                                             vp],
+            "hifuse_edge_type_offsets": [vp, i64, i32, vp, vp, vp],
             "hifuse_project_ws_bytes": [vp, i32, i32, i32],
             "hifuse_project": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp,
                                vp, vp, vp, sz, vp],
@@ -174,8 +176,15 @@ class CsrBuffers:
         return ctypes.byref(self.c)
 
 
+def edge_type_offsets(edge_type, num_rels, out, status, stream=None):
+    """out (int64 [R+1]) = first edge id of every relation of a relation-major
+    edge-type table; HIFUSE_ST_UNSORTED_TYPES in status if it is not one."""
+    _check("hifuse_edge_type_offsets", lib().hifuse_edge_type_offsets(
+        _ptr(edge_type), edge_type.numel(), num_rels, _ptr(out), _ptr(status), _stream(stream)))
+
+
 def build_semantic_graphs(shapes, csrs, src_local, dst_local, edge_id, edge_type, ws, status,
-                          stream=None):
+                          stream=None, rel_edge_off=None):
     n = len(shapes)
     arr_s = (ctypes.c_void_p * n)(*[t.data_ptr() for t in src_local])
     arr_d = (ctypes.c_void_p * n)(*[t.data_ptr() for t in dst_local])
@@ -183,7 +192,8 @@ def build_semantic_graphs(shapes, csrs, src_local, dst_local, edge_id, edge_type
     sh = (LayerShape * n)(*[s.c for s in shapes])
     cs = (Csr * n)(*[c.c for c in csrs])
     _check("hifuse_build_semantic_graphs", lib().hifuse_build_semantic_graphs(
-        sh, n, arr_s, arr_d, arr_e, _ptr(edge_type), edge_type.numel(), LAYOUT_COMPACT, cs,
+        sh, n, arr_s, arr_d, arr_e, _ptr(edge_type), edge_type.numel(), _ptr(rel_edge_off),
+        LAYOUT_COMPACT, cs,
         _ptr(ws), ws.numel() * ws.element_size(), _ptr(status), _stream(stream)))
 
 

@@ -140,6 +140,21 @@ class Trainer:
     def _ws(self, nbytes, key="ws"):
         return self._buf(key, (nbytes + 3) // 4 + 64)
 
+    def prepare_graph(self, edge_type):
+        """One-time per graph (synchronises): if the edge-type table is
+        relation-major, keep its R+1 offsets so that the build evaluates
+        EdgeType[EdgeID] without the random table gather (include/hifuse.h)."""
+        off = torch.empty(self.R + 1, dtype=torch.int64, device=self.device)
+        st = torch.zeros(1, dtype=torch.int32, device=self.device)
+        hf.edge_type_offsets(edge_type, self.R, off, st)
+        ok = hf.read_status(st) == 0
+        self._et_off = (edge_type.data_ptr(), off if ok else None)
+        return ok
+
+    def _et_offsets(self, edge_type):
+        c = getattr(self, "_et_off", None)
+        return c[1] if c is not None and c[0] == edge_type.data_ptr() else None
+
     def build_op(self, db: DeviceBatch, edge_type):
         """The semantic-graph build of ``db`` (A1) as a closure; CSR buffers
         are per batch slot and the workspace is private, so it may run on a
@@ -147,8 +162,9 @@ class Trainer:
         dev, shapes = db.dev, db.shapes
         csrs = [self._csr(l, s, db.slot) for l, s in enumerate(shapes)]
         wsb = self._ws(max(s.build_ws for s in shapes), key="ws_build")
+        off = self._et_offsets(edge_type)
         return lambda: hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"],
-                                                edge_type, wsb, self.status)
+                                                edge_type, wsb, self.status, rel_edge_off=off)
 
     # ----------------------------------------------------------------- plan
     def plan(self, db: DeviceBatch, feat, edge_type, include_build=True):

@@ -33,6 +33,7 @@ tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.
 tr.load_params(make_params(cfg))
 fd = torch.from_numpy(feat).to(dev)
 et = torch.from_numpy(g.edge_type).to(dev)
+tr.prepare_graph(et)
 for db in pool:
     tr.step(db, fd, et, update=False)
 torch.cuda.synchronize()

@@ -14,16 +14,24 @@ def hf():
     return h
 
 
-def gpu_build(blk, et, rel_src, rel_dst, status=None, csc=True):
-    """Runs hifuse_build_semantic_graphs on one layer; returns (shape, csr)."""
+def gpu_build(blk, et, rel_src, rel_dst, status=None, csc=True, ranged=False):
+    """Runs hifuse_build_semantic_graphs on one layer; returns (shape, csr).
+    ranged: pass the relation-major offsets of `et` instead of the table."""
     h = hf()
     sh = h.Shape(rel_src, rel_dst, blk.n_src, blk.n_dst, blk.num_edges)
     csr = h.CsrBuffers(sh, DEV, csc=csc)
     ws = torch.empty((sh.build_ws + 3) // 4 + 16, dtype=torch.int32, device=DEV)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=DEV)
     t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).to(DEV)
+    et_d = t(et, np.int32)
+    off = None
+    if ranged:
+        off = torch.empty(sh.R + 1, dtype=torch.int64, device=DEV)
+        st2 = torch.zeros(1, dtype=torch.int32, device=DEV)
+        h.edge_type_offsets(et_d, sh.R, off, st2)
+        assert h.read_status(st2) == 0, "edge types not relation-major"
     h.build_semantic_graphs([sh], [csr], [t(blk.src_local, np.int32)], [t(blk.dst_local, np.int32)],
-                            [t(blk.edge_id, np.int64)], t(et, np.int32), ws, st)
+                            [t(blk.edge_id, np.int64)], et_d, ws, st, rel_edge_off=off)
     torch.cuda.synchronize()
     return sh, csr, st
 

@@ -14,8 +14,8 @@ from gpu_util import needs_gpu, gpu_build, csr_host, assert_build_equal
 pytestmark = [pytest.mark.gpu, needs_gpu]
 
 
-def _check(blk, et, rs, rd):
-    sh, csr, st = gpu_build(blk, et, rs, rd)
+def _check(blk, et, rs, rd, ranged=False):
+    sh, csr, st = gpu_build(blk, et, rs, rd, ranged=ranged)
     ref = oracle.build(oracle.Shape.of(blk, rs, rd), blk, et)
     assert_build_equal(csr_host(sh, csr), ref)
     assert int(st.item()) == ref["status"]
@@ -73,6 +73,46 @@ def test_sampled_batches(key):
     rd = np.array([r.dst for r in cfg.rels], np.int32)
     for blk in mb.layers:
         _check(blk, g.edge_type, rs, rd)
+        _check(blk, g.edge_type, rs, rd, ranged=True)    # relation-major ids: offsets path
+
+
+def test_edge_type_offsets():
+    from gpu_util import hf, DEV
+    rng = np.random.default_rng(5)
+    R = 9
+    sizes = rng.integers(0, 50, R)
+    sizes[3] = 0                                          # an empty relation
+    et = np.repeat(np.arange(R, dtype=np.int32), sizes)
+    et_d = torch.from_numpy(et).to(DEV)
+    off = torch.empty(R + 1, dtype=torch.int64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    hf().edge_type_offsets(et_d, R, off, st)
+    assert hf().read_status(st) == 0
+    assert np.array_equal(off.cpu().numpy(), np.searchsorted(et, np.arange(R + 1), "left"))
+    et2 = et.copy()
+    et2[[0, -1]] = et2[[-1, 0]]                           # not sorted any more
+    hf().edge_type_offsets(torch.from_numpy(et2).to(DEV), R, off, st)
+    assert hf().read_status(st) & 16
+
+
+def test_random_blocks_relation_major_offsets():
+    """Random blocks whose graph-global edge ids are relation-major."""
+    for seed in range(6):
+        rng = np.random.default_rng(3000 + seed)
+        T, R = int(rng.integers(1, 5)), int(rng.integers(1, 30))
+        rs, rd = random_schema(rng, T, R)
+        n_src = rng.integers(1, 300, T)
+        n_dst = np.maximum(np.minimum(rng.integers(0, 200, T), n_src), 1)
+        blk, et = random_block(rng, n_src, n_dst, rs, rd, int(rng.integers(1, 5000)))
+        order = np.argsort(et, kind="stable")             # relabel ids relation-major
+        inv = np.empty_like(order)
+        inv[order] = np.arange(len(order))
+        blk2 = blk._replace(edge_id=inv[blk.edge_id]) if hasattr(blk, "_replace") else None
+        if blk2 is None:
+            import dataclasses
+            blk2 = dataclasses.replace(blk, edge_id=inv[blk.edge_id].astype(np.int64))
+        _check(blk2, et[order], rs, rd)
+        _check(blk2, et[order], rs, rd, ranged=True)
 
 
 def test_deterministic_across_runs():
