@@ -8,9 +8,10 @@
 //  k_head_softmax warp per seed row: dlog = (softmax - onehot) / B, row loss;
 //                 the last block sums the per-block losses -> mean loss
 //  k_head_grads   one grid, two jobs: dHs = dlog Wc^T and dWc = Hs^T dlog
-//                 (+ dbc = column sums of dlog), both split over K with one
-//                 partial per slice; the last slice of a tile to finish
-//                 (atomic ticket) sums the partials in slice order.
+//                 (+ dbc = column sums of dlog), each output tile split over
+//                 K across the 8 CTAs of a thread-block cluster whose
+//                 partials are summed in rank order through distributed
+//                 shared memory.
 // The three GEMMs run on the tensor cores with mma.sync m16n8k8 TF32 in the
 // 3xTF32 split (x = hi + lo, hi = tf32(x), lo = tf32(x - hi); D += lo*hi +
 // hi*lo + hi*hi), which keeps fp32-level accuracy: the head is outside the
@@ -18,6 +19,7 @@
 // are tiny (B x 128 x C); what matters is parallelism and few dependent
 // memory round trips, not the tcgen05 peak.
 #include <algorithm>
+#include <cooperative_groups.h>
 #include "common.cuh"
 
 namespace hf {
@@ -195,142 +197,98 @@ k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__
 }
 
 struct HeadGrid {
-  int dh_tiles_n, dh_tiles, dh_split;       // dHs: [B, D] tiles (n-major), K = C
-  int dw_tiles_n, dw_tiles, dw_split;       // dWc: [D, C] tiles, K = B
+  int dh_tiles_n, dh_tiles;       // dHs: [B, D] tiles (n-major), K = C
+  int dw_tiles_n, dw_tiles;       // dWc: [D, C] tiles, K = B
 };
 
-// True in the block that finished last among the nz slices of a tile (its
-// partials are then visible to it).
-__device__ __forceinline__ bool last_slice(int* ticket, int nz) {
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == nz - 1;
-  __syncthreads();
-  if (s_last) __threadfence();
-  return s_last;
-}
+// One thread-block cluster of kSlices CTAs per output tile: CTA rank z
+// computes the partial product over its K slice, the partials meet in
+// distributed shared memory and each rank sums 1/kSlices of the tile over the
+// ranks in rank order (deterministic; no global partials, no atomics).
+static constexpr int kSlices = 8;
 
-// Sum of nz slice partials (slice stride `ss`) of this thread's 16 fragment
-// outputs, two slices' loads in flight at a time, slices added in order.
-__device__ __forceinline__ void reduce_slices(const float* __restrict__ part, long long ss, int nz,
-                                              int m0, int n0, int M, int N, int ld,
-                                              float* __restrict__ out) {
-  float tsum[4][4];
-#pragma unroll
-  for (int nt = 0; nt < 4; nt++)
-#pragma unroll
-    for (int r = 0; r < 4; r++) tsum[nt][r] = 0.f;
-  for (int z0 = 0; z0 < nz; z0 += 2) {
-    float v[2][4][4];
-#pragma unroll
-    for (int u = 0; u < 2; u++)
-#pragma unroll
-      for (int nt = 0; nt < 4; nt++)
-#pragma unroll
-        for (int r = 0; r < 4; r++) {
-          const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
-          v[u][nt][r] = (z0 + u < nz && m < M && n < N)
-                            ? __ldcg(part + (z0 + u) * ss + (long long)m * ld + n) : 0.f;
-        }
-#pragma unroll
-    for (int u = 0; u < 2; u++)
-#pragma unroll
-      for (int nt = 0; nt < 4; nt++)
-#pragma unroll
-        for (int r = 0; r < 4; r++) tsum[nt][r] += v[u][nt][r];
-  }
-#pragma unroll
-  for (int nt = 0; nt < 4; nt++)
-#pragma unroll
-    for (int r = 0; r < 4; r++) {
-      const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
-      if (m < M && n < N) out[(long long)m * ld + n] = tsum[nt][r];
-    }
-}
-
-__global__ void __launch_bounds__(128)
+__global__ void __cluster_dims__(kSlices, 1, 1) __launch_bounds__(128)
 k_head_grads(int B, int D, int C, HeadGrid hg, const float* __restrict__ Hs,
              const float* __restrict__ Wc, const float* __restrict__ dlog,
-             float* __restrict__ part_h, float* __restrict__ part_w, float* __restrict__ part_b,
-             int* __restrict__ tickets, float* __restrict__ dHs, float* __restrict__ dWc,
-             float* __restrict__ dbc) {
+             float* __restrict__ dHs, float* __restrict__ dWc, float* __restrict__ dbc) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ float red[128 * 16];      // this CTA's partial, [thread][16 fragment values]
+  __shared__ float red_b[kBN];         // this CTA's column sums (dbc tiles)
+  const int z = (int)cluster.block_rank();
+  const int tile = blockIdx.x / kSlices;
+  const bool dh = tile < hg.dh_tiles;
+  int M, N, ld, m0, n0;
+  float* out;
   float acc[4][4];
-  int bid = blockIdx.x;
-  const int nh = hg.dh_tiles * hg.dh_split;
-  if (bid < nh) {
+  bool bias = false;
+  if (dh) {
     // ---- dHs = dlog Wc^T: M = B, N = D, K = C; Wc stored [D][C] = [N][K]
-    const int tile = bid / hg.dh_split, z = bid % hg.dh_split;
-    const int m0 = (tile / hg.dh_tiles_n) * kBM, n0 = (tile % hg.dh_tiles_n) * kBN;
-    const int kper = ((C + hg.dh_split - 1) / hg.dh_split + kBK - 1) / kBK * kBK;
+    M = B; N = D; ld = D; out = dHs;
+    m0 = (tile / hg.dh_tiles_n) * kBM;
+    n0 = (tile % hg.dh_tiles_n) * kBN;
+    const int kper = ((C + kSlices - 1) / kSlices + kBK - 1) / kBK * kBK;
     mma_tile<false, true>(B, D, dlog, C, Wc, C, m0, n0, z * kper, min(C, (z + 1) * kper), acc,
                           nullptr);
-    if (hg.dh_split == 1) {
-#pragma unroll
-      for (int nt = 0; nt < 4; nt++)
-#pragma unroll
-        for (int r = 0; r < 4; r++) {
-          const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
-          if (m < B && n < D) dHs[(long long)m * D + n] = acc[nt][r];
-        }
-      return;
-    }
-    float* P = part_h + (long long)z * B * D;
-#pragma unroll
-    for (int nt = 0; nt < 4; nt++)
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
-        if (m < B && n < D) P[(long long)m * D + n] = acc[nt][r];
-      }
-    if (!last_slice(&tickets[tile], hg.dh_split)) return;
-    reduce_slices(part_h, (long long)B * D, hg.dh_split, m0, n0, B, D, D, dHs);
-    return;
+  } else {
+    // ---- dWc = Hs^T dlog: M = D, N = C, K = B; Hs stored [B][D] = [K][M]
+    const int t2 = tile - hg.dh_tiles;
+    M = D; N = C; ld = C; out = dWc;
+    m0 = (t2 / hg.dw_tiles_n) * kBM;
+    n0 = (t2 % hg.dw_tiles_n) * kBN;
+    const int kper = ((B + kSlices - 1) / kSlices + kBK - 1) / kBK * kBK;
+    bias = m0 == 0;                    // the first row tile also forms dbc
+    float cs = 0.f;
+    mma_tile<true, false>(D, C, Hs, D, dlog, C, m0, n0, z * kper, min(B, (z + 1) * kper), acc,
+                          bias ? &cs : nullptr);
+    if (bias && threadIdx.x < kBN) red_b[threadIdx.x] = cs;
   }
-  // ---- dWc = Hs^T dlog: M = D, N = C, K = B; Hs stored [B][D] = [K][M]
-  bid -= nh;
-  const int tile = bid / hg.dw_split, z = bid % hg.dw_split;
-  const int m0 = (tile / hg.dw_tiles_n) * kBM, n0 = (tile % hg.dw_tiles_n) * kBN;
-  const int kper = ((B + hg.dw_split - 1) / hg.dw_split + kBK - 1) / kBK * kBK;
-  const bool bias = m0 == 0;            // the first row tile also forms dbc
-  float cs = 0.f;
-  mma_tile<true, false>(D, C, Hs, D, dlog, C, m0, n0, z * kper, min(B, (z + 1) * kper), acc,
-                        bias ? &cs : nullptr);
-  float* P = part_w + (long long)z * D * C;
 #pragma unroll
   for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-    for (int r = 0; r < 4; r++) {
-      const int m = m0 + frag_row(r), n = n0 + frag_col(nt, r);
-      if (m < D && n < C) P[(long long)m * C + n] = acc[nt][r];
-    }
-  if (bias && threadIdx.x < kBN && n0 + (int)threadIdx.x < C)
-    part_b[(long long)z * C + n0 + threadIdx.x] = cs;
-  if (!last_slice(&tickets[hg.dh_tiles + tile], hg.dw_split)) return;
-  reduce_slices(part_w, (long long)D * C, hg.dw_split, m0, n0, D, C, C, dWc);
-  if (bias && threadIdx.x < kBN && n0 + (int)threadIdx.x < C) {
-    const int n = n0 + threadIdx.x;
-    float t = 0.f;
-    for (int z0 = 0; z0 < hg.dw_split; z0 += 8) {
-      float v[8];
+    for (int r = 0; r < 4; r++) red[threadIdx.x * 16 + nt * 4 + r] = acc[nt][r];
+  cluster.sync();
+  // rank z reduces the fragments of threads [16 z, 16 z + 16): 256 values,
+  // two per thread, each summed over the kSlices ranks in rank order
+  {
+    const int ot = z * 16 + (threadIdx.x >> 3);        // owning thread of the fragment
+    const int q0 = (threadIdx.x & 7) * 2;              // its values q0, q0 + 1
+    float v[2][kSlices];
 #pragma unroll
-      for (int u = 0; u < 8; u++)
-        v[u] = z0 + u < hg.dw_split ? __ldcg(part_b + (long long)(z0 + u) * C + n) : 0.f;
-#pragma unroll
-      for (int u = 0; u < 8; u++) t += v[u];
+    for (int rk = 0; rk < kSlices; rk++) {
+      const float* peer = cluster.map_shared_rank(red, rk);
+      v[0][rk] = peer[ot * 16 + q0];
+      v[1][rk] = peer[ot * 16 + q0 + 1];
     }
-    dbc[n] = t;
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      float t = 0.f;
+#pragma unroll
+      for (int rk = 0; rk < kSlices; rk++) t += v[u][rk];
+      const int q = q0 + u, nt = q >> 2, r = q & 3;
+      // fragment coordinates of thread ot
+      const int w = ot >> 5, ln = ot & 31;
+      const int m = m0 + (w >> 1) * 16 + (ln >> 2) + (r >= 2 ? 8 : 0);
+      const int n = n0 + (w & 1) * 32 + nt * 8 + (ln & 3) * 2 + (r & 1);
+      if (m < M && n < N) out[(long long)m * ld + n] = t;
+    }
   }
+  if (bias && z == 0 && threadIdx.x < kBN && n0 + (int)threadIdx.x < C) {
+    float t = 0.f;
+#pragma unroll
+    for (int rk = 0; rk < kSlices; rk++) t += cluster.map_shared_rank(red_b, rk)[threadIdx.x];
+    dbc[n0 + threadIdx.x] = t;
+  }
+  cluster.sync();                      // peers' shared memory stays alive until read
 }
 
 static HeadGrid head_grid(int B, int D, int C) {
+  (void)B;
   HeadGrid h;
   h.dh_tiles_n = (int)ceil_div(D, kBN);
   h.dh_tiles = h.dh_tiles_n * (int)ceil_div(B, kBM);
-  h.dh_split = (int)std::max<long long>(1, std::min<long long>(ceil_div(C, 256), 4));
   h.dw_tiles_n = (int)ceil_div(C, kBN);
   h.dw_tiles = h.dw_tiles_n * (int)ceil_div(D, kBM);
-  h.dw_split = (int)std::max<long long>(1, std::min<long long>(ceil_div(B, 128), 32));
   return h;
 }
 
@@ -356,12 +314,7 @@ extern "C" {
 
 size_t hifuse_xent_ws_bytes(int B, int D, int C) {
   if (B <= 0 || D <= 0 || C <= 0) return 0;
-  const HeadGrid h = head_grid(B, D, C);
-  const long long nblk = ceil_div(B, 8);
-  return carve_bytes((long long)B * C, 4) + carve_bytes(nblk, 4) +
-         carve_bytes((long long)h.dh_split * B * D, 4) +
-         carve_bytes((long long)h.dw_split * D * C, 4) + carve_bytes((long long)h.dw_split * C, 4) +
-         carve_bytes(h.dh_tiles + h.dw_tiles + 1, 4);
+  return carve_bytes((long long)B * C, 4) + carve_bytes(ceil_div(B, 8), 4) + carve_bytes(1, 4);
 }
 
 hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t h_rows,
@@ -379,22 +332,17 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   char* p = (char*)d_ws;
   float* dlog = carve<float>(p, (long long)B * C);
   float* block_loss = carve<float>(p, nblk);
-  float* part_h = carve<float>(p, (long long)h.dh_split * B * D);
-  float* part_w = carve<float>(p, (long long)h.dw_split * D * C);
-  float* part_b = carve<float>(p, (long long)h.dw_split * C);
-  int* tickets = carve<int>(p, h.dh_tiles + h.dw_tiles + 1);
-  const int ntk = h.dh_tiles + h.dw_tiles + 1;       // last one: the softmax ticket
+  int* ticket = carve<int>(p, 1);
   // rows of dH outside the seeds get no gradient
   if (h_row0 > 0) cudaMemsetAsync(d_dH, 0, sizeof(float) * h_row0 * D, s);
   if (h_row0 + B < h_rows)
     cudaMemsetAsync(d_dH + (h_row0 + B) * D, 0, sizeof(float) * (h_rows - h_row0 - B) * D, s);
   const float* Hs = d_H + h_row0 * D;
   HF_LAUNCH(k_head_logits, dim3(ceil_div(C, kBN), ceil_div(B, kBM)), 128, 0, s, B, D, C, Hs, d_Wc,
-            d_bc, dlog, tickets, ntk);
-  HF_LAUNCH(k_head_softmax, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, tickets + ntk - 1,
-            d_loss);
-  HF_LAUNCH(k_head_grads, h.dh_tiles * h.dh_split + h.dw_tiles * h.dw_split, 128, 0, s, B, D, C,
-            h, Hs, d_Wc, dlog, part_h, part_w, part_b, tickets, d_dH + h_row0 * D, d_dWc, d_dbc);
+            d_bc, dlog, ticket, 1);
+  HF_LAUNCH(k_head_softmax, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket, d_loss);
+  HF_LAUNCH(k_head_grads, (h.dh_tiles + h.dw_tiles) * kSlices, 128, 0, s, B, D, C, h, Hs, d_Wc,
+            dlog, d_dH + h_row0 * D, d_dWc, d_dbc);
   return last_cuda();
 }
 
