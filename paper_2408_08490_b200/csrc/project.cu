@@ -817,7 +817,8 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
     DgradMeta dm;
     if (prec == HIFUSE_PREC_TF32) {
       make_dgrad_meta(m, d_W_root != nullptr, &dm, 128);
-      rc = dgrad_tc_launch(dm, K, D, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX, s);
+      rc = dgrad_tc_launch(dm, K, D, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX, s, U_max,
+                           m.R);
       if (rc != HIFUSE_OK) return rc;
     } else {
       make_dgrad_meta(m, d_W_root != nullptr, &dm);

@@ -51,7 +51,8 @@ hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, 
 // through slot_y, or G for the root term).  dm built with bm = 128.
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
                               const float* dY, const float* G, const float* W_rel,
-                              const float* W_root, float* dX, cudaStream_t s);
+                              const float* W_root, float* dX, cudaStream_t s, long long dy_rows,
+                              int R);
 // tcgen05 TF32 wgrad partials: P[c] = sum_{rows of chunk c} X_row^T dYt_row
 // (chunks of CH rows per group from chunk_off; wgrad_chunk_rows() picks CH so
 // that small layers still spread over every SM).

@@ -147,3 +147,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 }  // namespace tc
 }  // namespace hf
+
+// ------------------------------------------------------------------ TMA -----
+// (async proxy: no generic->async proxy fence is needed before the MMA reads
+// what these copies wrote; completion is counted in bytes on an mbarrier)
+namespace hf {
+namespace tc {
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+// 4 gathered rows (row coordinates r0..r3, column start c0) of a 2-D tensor
+// map with box {cols, 1}; rows out of range (e.g. -1) are zero-filled.
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void* map, uint32_t bar, int c0,
+                                            int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, uint32_t bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+}  // namespace tc
+}  // namespace hf
