@@ -200,6 +200,12 @@ struct BwdMeta {
 // Columns longer than kLongCol (hub sources) are handed to a block-wide
 // kernel so that no single warp serialises thousands of gathers.
 static constexpr int kLongCol = 64;
+// sum/mean CSC path: columns with <= kMidCol entries go to k_agg_bwd_p (8
+// lanes each, rounds of 8 entries), longer ones to k_agg_bwd_p_long (8 warps
+// each): a column of 64 entries on 8 lanes would be 8 dependent gather rounds
+// that stall the whole kernel (measured: layer-1 agg bwd 23 -> 15 us)
+static constexpr int kMidCol = 16;
+static constexpr int kPLongWarps = 8;      // warps per column in k_agg_bwd_p_long
 
 template <int D, bool MEAN>
 __device__ __forceinline__ float4 col_slice_sum(int b, int e, int shift,
@@ -413,7 +419,7 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
   };
   auto first_row = [&](int b, int e) {
     // long columns go to k_agg_bwd_p_long; their first round is not fetched
-    return (e - b <= kLongCol && b + j < e) ? __ldg(csc_row + b + j) : -1;
+    return (e - b <= kMidCol && b + j < e) ? __ldg(csc_row + b + j) : -1;
   };
   int b0, e0, b1, e1;
   bounds(cg0, &b0, &e0);
@@ -427,7 +433,7 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
     const int u = cg * CPW + grp;
     bool skip = u >= U;
     int e = e0;
-    if (!skip && e0 - b0 > kLongCol) {
+    if (!skip && e0 - b0 > kMidCol) {
       if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
       e = b0;
       skip = true;
@@ -468,38 +474,39 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
   }
 }
 
-// Long columns over the pre-scaled rows (32 warps per column, fixed-order
-// combine of the warp slices).
+// Long columns over the pre-scaled rows (kPLongWarps warps per column,
+// fixed-order combine of the warp slices).
 template <int D>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kPLongWarps * 32)
 k_agg_bwd_p_long(const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
                  const float4* __restrict__ Gs, float4* __restrict__ dY,
                  const int* __restrict__ list, const int* __restrict__ cnt) {
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
-  __shared__ float4 red[32][LPR];
+  constexpr int G = 8;                                   // gathers in flight per stream
+  __shared__ float4 red[kPLongWarps][LPR];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int sl = lane % LPR, sid = lane / LPR;
   const int n_long = *cnt;
   for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
     const int u = list[k];
     const int b = col_ptr[u], e = col_ptr[u + 1];
-    const int per = (e - b + 31) / 32;
+    const int per = (e - b + kPLongWarps - 1) / kPLongWarps;
     const int wb = min(e, b + w * per), we = min(e, wb + per);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int base = wb; base < we; base += 32) {
       const int n = min(32, we - base);
       const int my_row = lane < n ? __ldg(csc_row + base + lane) : 0;
-      for (int kk = 0; kk < n; kk += NS * 4) {
-        float4 x[4];
+      for (int kk = 0; kk < n; kk += NS * G) {
+        float4 x[G];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < G; q++) {
           const int idx = kk + q * NS + sid;
           const int rr = __shfl_sync(0xffffffffu, my_row, idx < n ? idx : 0);
           x[q] = idx < n ? ldg4(Gs + (long long)rr * LPR + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int q = 0; q < 4; q++) acc = f4add(acc, x[q]);
+        for (int q = 0; q < G; q++) acc = f4add(acc, x[q]);
       }
     }
 #pragma unroll
@@ -508,7 +515,7 @@ k_agg_bwd_p_long(const int* __restrict__ col_ptr, const int* __restrict__ csc_ro
     __syncthreads();
     if (w == 0 && lane < LPR) {
       float4 t = red[0][lane];
-      for (int q = 1; q < 32; q++) t = f4add(t, red[q][lane]);
+      for (int q = 1; q < kPLongWarps; q++) t = f4add(t, red[q][lane]);
       dY[(long long)u * LPR + lane] = t;
     }
     __syncthreads();
@@ -864,7 +871,7 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
             csr->rel_row_off, m.rows, csr->row_ptr, (const float4*)d_G, (float4*)Gs);           \
   HF_LAUNCH((k_agg_bwd_p<DD>), 148 * 4, TB, 0, s, (int)U_max, csr->U_dev, csr->col_ptr,           \
             csr->csc_row, (const float4*)Gs, (float4*)d_dY, long_list, long_cnt);               \
-  HF_LAUNCH((k_agg_bwd_p_long<DD>), gridL, 1024, 0, s, csr->col_ptr, csr->csc_row,                 \
+  HF_LAUNCH((k_agg_bwd_p_long<DD>), 148 * 8, kPLongWarps * 32, 0, s, csr->col_ptr, csr->csc_row,    \
             (const float4*)Gs, (float4*)d_dY, long_list, long_cnt)
     if (!csr->rel_row_off) return HIFUSE_ERR_INVALID_ARG;
     float* Gs = carve<float>(p, (long long)(m.rows > 0 ? m.rows : 1) * 128);
