@@ -49,6 +49,33 @@ hifuse_status make_meta(const hifuse_layer_shape* s, LayerMeta* m) {
   return HIFUSE_OK;
 }
 
+// ---------------------------------------------------------------- branch ---
+bool branch_begin(cudaStream_t main, Branch* b) {
+  static Branch per_dev[64];
+  static bool made[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  if (!made[dev]) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(main, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return false;                      // creating streams/events is not capture-safe
+    Branch& n = per_dev[dev];
+    if (cudaStreamCreateWithFlags(&n.side, cudaStreamNonBlocking) != cudaSuccess) return false;
+    cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming);
+    made[dev] = true;
+  }
+  *b = per_dev[dev];
+  cudaEventRecord(b->fork, main);
+  cudaStreamWaitEvent(b->side, b->fork, 0);
+  return true;
+}
+
+void branch_end(cudaStream_t main, const Branch& b) {
+  cudaEventRecord(b.join, b.side);
+  cudaStreamWaitEvent(main, b.join, 0);
+}
+
 // ------------------------------------------------------------------ scan ---
 static constexpr int kScanThreads = 256;
 static constexpr int kScanItems = 32;

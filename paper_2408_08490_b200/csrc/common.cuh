@@ -74,6 +74,19 @@ __device__ __forceinline__ int upper_bound_i(const int* a, int n, int x) {
   return lo;
 }
 
+// Fork/join of one call's independent kernels onto an auxiliary stream (per
+// device, created on first use outside graph capture): record `fork` on the
+// caller's stream, run the branch on `side`, record `join` there and make the
+// caller's stream wait for it.  Works eagerly and under CUDA-graph capture
+// (the branch becomes a parallel graph path).  Returns false (run serially)
+// before the stream exists.
+struct Branch {
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+};
+bool branch_begin(cudaStream_t main, Branch* b);
+void branch_end(cudaStream_t main, const Branch& b);
+
 // Device-wide exclusive scan of int32 counts (reduce-then-scan, 3 kernels).
 // out[0..n] receives the exclusive prefix, out[n] = total.  ws: scan_ws_ints(n).
 size_t scan_ws_ints(long long n);

@@ -776,6 +776,21 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
     HF_LAUNCH(k_dy_score, ceil_div(U_max * (D / 4), 256), 256, 0, s, m.R, D, H, csr->U_dev,
               csr->rel_y_off, d_att, d_ds_src, (float4*)d_dY);
   }
+  // dgrad (dX) is independent of the weight-gradient chain: it runs on a
+  // parallel branch (the dYt it reads is final after k_dy_score)
+  DgradMeta dm;
+  Branch br;
+  bool branched = false;
+  if (d_dX && prec == HIFUSE_PREC_TF32) {
+    make_dgrad_meta(m, d_W_root != nullptr, &dm, 128);
+    branched = branch_begin(s, &br);
+    rc = dgrad_tc_launch(dm, K, D, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX,
+                         branched ? br.side : s, U_max, m.R);
+    if (rc != HIFUSE_OK) {
+      if (branched) branch_end(s, br);
+      return rc;
+    }
+  }
   int CH = kCH;
   if (prec == HIFUSE_PREC_TF32) {
     CH = wgrad_chunk_rows(m);
@@ -813,13 +828,10 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
     HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, s, m.R, K, D, H, csr->rel_y_off,
               Psrc, dvb, d_W_rel, d_datt);
   }
+  if (branched) branch_end(s, br);       // join the dgrad branch
   if (d_dX) {
-    DgradMeta dm;
     if (prec == HIFUSE_PREC_TF32) {
-      make_dgrad_meta(m, d_W_root != nullptr, &dm, 128);
-      rc = dgrad_tc_launch(dm, K, D, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX, s, U_max,
-                           m.R);
-      if (rc != HIFUSE_OK) return rc;
+      // launched above on the parallel branch
     } else {
       make_dgrad_meta(m, d_W_root != nullptr, &dm);
       unsigned gd = dm.tile_off[m.T];
