@@ -50,22 +50,23 @@ hifuse_status make_meta(const hifuse_layer_shape* s, LayerMeta* m) {
 }
 
 // ---------------------------------------------------------------- branch ---
-bool branch_begin(cudaStream_t main, Branch* b) {
-  static Branch per_dev[64];
-  static bool made[64] = {};
+bool branch_begin(cudaStream_t main, Branch* b, int idx) {
+  static Branch per_dev[64][4];
+  static bool made[64][4] = {};
   int dev = 0;
+  if (idx < 0 || idx >= 4) return false;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
-  if (!made[dev]) {
+  if (!made[dev][idx]) {
     cudaStreamCaptureStatus cs;
     if (cudaStreamIsCapturing(main, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
       return false;                      // creating streams/events is not capture-safe
-    Branch& n = per_dev[dev];
+    Branch& n = per_dev[dev][idx];
     if (cudaStreamCreateWithFlags(&n.side, cudaStreamNonBlocking) != cudaSuccess) return false;
     cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming);
-    made[dev] = true;
+    made[dev][idx] = true;
   }
-  *b = per_dev[dev];
+  *b = per_dev[dev][idx];
   cudaEventRecord(b->fork, main);
   cudaStreamWaitEvent(b->side, b->fork, 0);
   return true;

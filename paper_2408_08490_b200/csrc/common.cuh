@@ -84,7 +84,7 @@ struct Branch {
   cudaStream_t side;
   cudaEvent_t fork, join;
 };
-bool branch_begin(cudaStream_t main, Branch* b);
+bool branch_begin(cudaStream_t main, Branch* b, int idx = 0);   // idx < 4: independent branches
 void branch_end(cudaStream_t main, const Branch& b);
 
 // Device-wide exclusive scan of int32 counts (reduce-then-scan, 3 kernels).

@@ -687,9 +687,22 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   int* tile_off = carve<int>(p, m.R + m.T + 1);
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
   float* v = carve<float>(p, (long long)m.R * K * (heads > 0 ? heads : 1));
+  // RGAT destination scores (v = W a_dst folded, s_dst = X v) only read X and
+  // W: a parallel branch next to the projection GEMM
+  Branch bs;
+  bool sbr = false;
+  if (d_att && prec == HIFUSE_PREC_TF32) {
+    sbr = branch_begin(s, &bs, 2);
+    cudaStream_t sd = sbr ? bs.side : s;
+    HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * heads, 256), 256, 0, sd, m.R, K, D, heads,
+              d_W_rel, d_att, v);
+    HF_LAUNCH(k_scores_dst, ceil_div(m.rows, 256 / heads), 256, 0, sd, pm, K, heads, d_gather_ids,
+              d_X, v, d_s_dst);
+  }
   if (prec == HIFUSE_PREC_TF32) {
     rc = project_tcp_launch(m, pm, K, D, csr->rel_y_off, csr->y_src, d_X, nullptr, d_gather_ids,
                             d_W_rel, d_W_root, d_Y, d_R0, d_att, d_s_src, heads, s);   // s_src fused in the epilogue
+    if (sbr) branch_end(s, bs);
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
     HF_LAUNCH(k_group_table, 1, 32, 0, s, pm, csr->rel_y_off, tile_off, chunk_off, kBM, kCH);
@@ -705,11 +718,10 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   } else {
     return HIFUSE_ERR_UNSUPPORTED;
   }
-  if (d_att) {
+  if (d_att && prec != HIFUSE_PREC_TF32) {
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * heads, 256), 256, 0, s, m.R, K, D, heads,
               d_W_rel, d_att, v);
     long long U_max = m.N < m.S ? m.N : m.S;
-    if (prec != HIFUSE_PREC_TF32)
     HF_LAUNCH(k_scores_src, ceil_div(U_max, 8), 256, 0, s, m.R, D, heads, csr->U_dev,
               csr->rel_y_off, d_Y, d_att, d_s_src);
     HF_LAUNCH(k_scores_dst, ceil_div(m.rows, 256 / heads), 256, 0, s, pm, K, heads, d_gather_ids,
@@ -809,24 +821,33 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
 #undef HF_WG
   }
   int G = d_W_root ? m.R + m.T : m.R;
+  // RGAT attention chain (independent of the wgrad partials until k_att_dw
+  // adds into dW_rel): a second parallel branch
+  Branch ba;
+  bool abr = false;
+  float* dvb = v + (long long)m.R * K * H;     // dv [R][H][K] after v in the workspace
+  if (d_att) {
+    abr = branch_begin(s, &ba, 1);
+    cudaStream_t sa = abr ? ba.side : s;
+    HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, sa, m.R, K, D, H, d_W_rel,
+              d_att, v);
+    const unsigned gs = (unsigned)(U_max / kCHA + m.R + 1);
+    const unsigned gdst = (unsigned)(m.rows / kCHA + m.R + 1);
+    HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, sa, m.R, H, D, 0, (const int*)nullptr,
+              csr->rel_y_off, d_ds_src, d_Y, pm, d_gather_ids, Psrc);
+    HF_LAUNCH(k_att_partial, gdst, H * K / 4, 0, sa, m.R, H, K, 1, (const int*)nullptr,
+              (const int*)nullptr, d_ds_dst, d_X, pm, d_gather_ids, Pdst);
+    HF_LAUNCH(k_att_dv, ceil_div((long long)m.R * H * K, 256), 256, 0, sa, m.R, K, H, pm, Pdst, dvb);
+    HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, sa, m.R, K, D, H, csr->rel_y_off,
+              Psrc, dvb, d_W_rel, d_datt);
+  }
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
             prec == HIFUSE_PREC_TF32 ? (const int*)nullptr : (const int*)chunk_off,
             (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root, pm, csr->rel_y_off, CH);
   if (d_att) {
-    HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, s, m.R, K, D, H, d_W_rel,
-              d_att, v);
-    const unsigned gs = (unsigned)(U_max / kCHA + m.R + 1);
-    const unsigned gdst = (unsigned)(m.rows / kCHA + m.R + 1);
-    HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, s, m.R, H, D, 0, (const int*)nullptr,
-              csr->rel_y_off, d_ds_src, d_Y, pm, d_gather_ids, Psrc);
-    HF_LAUNCH(k_att_partial, gdst, H * K / 4, 0, s, m.R, H, K, 1, (const int*)nullptr,
-              (const int*)nullptr, d_ds_dst, d_X, pm, d_gather_ids, Pdst);
-    float* dvb = v + (long long)m.R * K * H;     // dv [R][H][K] after v in the workspace
-    HF_LAUNCH(k_att_dv, ceil_div((long long)m.R * H * K, 256), 256, 0, s, m.R, K, H, pm, Pdst, dvb);
+    if (abr) branch_end(s, ba);
     HF_LAUNCH(k_att_dw, ceil_div((long long)m.R * K * D, 256), 256, 0, s, m.R, K, D, H, dvb, d_att,
               d_dW_rel);
-    HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, s, m.R, K, D, H, csr->rel_y_off,
-              Psrc, dvb, d_W_rel, d_datt);
   }
   if (branched) branch_end(s, br);       // join the dgrad branch
   if (d_dX) {
