@@ -133,6 +133,9 @@ def stage_cost(stage, l, cfg, sz):
         m = s["U"] + (s["dst"] if root else 0)
         f = 2 * K * D * m * (2 if l > 0 else 1)
         return 4 * K * m + 4 * D * m + (4 * s["src"] * K if l > 0 else 0), f
+    if stage == "xent":     # classifier head: Hs, Wc, dlog (written + read), dHs, dWc
+        C, B = cfg.num_classes, cfg.batch_size
+        return 4 * (2 * B * D + 2 * D * C + 3 * B * C), 3 * 2 * B * D * C
     if stage == "aggregate_features":     # aggregate-first input layer: A4 over raw X
         return 4 * K * s["U"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
     if stage == "project_aggregated":
@@ -156,18 +159,21 @@ def stage_cost(stage, l, cfg, sz):
 # main kernel of every library call (for the ncu traffic lookup)
 MAIN_KERNEL = {"aggregate_fwd": "k_agg_fwd", "aggregate_bwd": "k_agg_bwd_p", "project": "k_proj_fwd_tcp",
                "project_bwd": "k_wgrad_tc", "fuse": "k_fuse", "fuse_bwd": "k_fuse_bwd_chunks",
-               "build": "k_sort_long", "xent": "k_xent_rows", "aggregate_features": "k_agg_fwd",
+               "build": "k_sort_long", "xent": "k_head_grads", "aggregate_features": "k_agg_fwd",
                "project_aggregated": "k_proj_fwd_tcp", "project_aggregated_bwd": "k_wgrad_tc"}
 
 
-def ncu_traffic(kernel, layer):
+def ncu_traffic(kernel, layer, config, order):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` (the layer-th
-    launch in step order) from the committed ncu --set full capture, if any."""
+    launch in step order) from the committed ncu --set full capture of one
+    step of `config` in layer-0 `order` (profiles/traffic.json), if any."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
-    v = d.get(kernel)
+    if d.get("config") != config or d.get("order") != order:
+        return None
+    v = d.get("kernels", {}).get(kernel)
     if not v:
         return None
     return v[min(layer, len(v) - 1)] if isinstance(v, list) else v
@@ -329,14 +335,28 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    copy_stream = torch.cuda.Stream()
+    copy_done = [torch.cuda.Event() for _ in pool]
+    step_done = torch.cuda.Event()
+
     def one_step(i, e2e=False, loss_host=None):
-        db = pool[i % len(pool)]
+        P = len(pool)
         if e2e:
-            # host -> device copy of the batch the graph builds: this batch
-            # (serial) or the next one (pipelined build of batch i+1)
-            (db if graphs is serial_graphs else pool[(i + 1) % len(pool)]).to_device(
-                non_blocking=True)
+            # every step copies one batch's inputs host -> device (pinned) on a
+            # copy stream, two steps ahead of the graph that builds it, so the
+            # copy overlaps the compute of the current step; the graph waits
+            # for the copy of the batch it builds (this one if serial, the next
+            # one if pipelined).  Slots are 16 batches apart: no reuse hazard.
+            ahead = i + 2 + (0 if graphs is serial_graphs else 1)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(step_done)
+                pool[ahead % P].to_device(non_blocking=True)
+                copy_done[ahead % P].record(copy_stream)
+            built = i if graphs is serial_graphs else i + 1
+            torch.cuda.current_stream().wait_event(copy_done[built % P])
         graphs[i % len(pool)][0].replay()
+        if e2e:
+            step_done.record()
         if world > 1:
             allreduce_grads(tr.grads, world)
             hf.sgd(tr.params, tr.grads, tr.lr, 1.0 / world)
@@ -458,7 +478,7 @@ def main():
         avg_bytes = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[0] for pi in used]))
         avg_flops = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[1] for pi in used]))
         t_s = per_step[stage_key] / 1e3
-        gemm = ("project", "project_bwd", "project_aggregated", "project_aggregated_bwd")
+        gemm = ("project", "project_bwd", "project_aggregated", "project_aggregated_bwd", "xent")
         if name in gemm and args.prec == "fp32":
             roof = {"bound": "alu", "achieved": avg_flops / t_s / 1e12, "peak": ALU_FP32_TFLOPS,
                     "unit": "TFLOP/s"}
@@ -477,7 +497,8 @@ def main():
         roof["frac"] = roof["achieved"] / roof["peak"]
         bwd = name in ("aggregate_bwd", "project_bwd", "fuse_bwd", "project_aggregated_bwd")
         tr = None if name == "build" else ncu_traffic(MAIN_KERNEL.get(name, name),
-                                                       cfg.num_layers - 1 - l if bwd else l)
+                                                       cfg.num_layers - 1 - l if bwd else l,
+                                                       cfg.key, args.order)
         roof["traffic"] = tr
         roof["kernel"] = f"{stage_key} (main kernel {MAIN_KERNEL.get(name, name)})"
         roof["peak_source"] = pk["src"]
