@@ -259,6 +259,9 @@ def main():
     ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--compare", type=int, default=1,
+                    help="1: add the merged-vs-unmerged comparison arms (kernels per layer, "
+                         "per-relation launches, torch per-relation ops, cuSPARSE)")
     ap.add_argument("--order", default="agg_first", choices=["project_first", "agg_first"],
                     help="agg_first: the RGCN input layer aggregates raw features, then "
                          "projects (exact by linearity; SURVEY §8(f) NEXT(3))")
@@ -410,9 +413,12 @@ def main():
     # own graph and replayed back to back between CUDA events (the dominant
     # kernel's roofline below comes from these)
     stage_ms = {}
+    stage_kernels = {}
     reps = 5
     for pi, db in enumerate(pool[:min(len(pool), 8)]):
-        for name, g_, _ in tr.capture_stages(db, feat_d, et_d):
+        for name, g_, nk in tr.capture_stages(db, feat_d, et_d):
+            if pi == 0:
+                stage_kernels[name] = nk
             g_.replay()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
@@ -425,6 +431,16 @@ def main():
         del g_
     # restore a consistent state (stage replays repeat in-place updates)
     tr.load_params(params)
+    # merged vs unmerged per-relation arms on pool batch 0 (kernel counts per
+    # layer, same-kernel-per-relation launches, torch per-relation ops,
+    # cuSPARSE SpMM; comparison/unmerged.py)
+    unmerged = None
+    if args.compare and rank == 0:
+        from comparison.unmerged import compare_layers
+        sk = {n: (float(np.mean([t for pi, t in stage_ms[n] if pi == 0])), stage_kernels[n])
+              for n in stage_kernels}
+        unmerged = compare_layers(hf, tr, pool[0], cfg, feat_d, et_d, params, sk)
+        tr.load_params(params)
 
     # the other layer-0 order of the same RGCN step, timed the same way (the
     # north-star project-first path is always measured next to the faster
@@ -547,6 +563,7 @@ def main():
                         "one CUDA graph per pool batch (whole step, serial)"),
         "serial_ms_per_step": ms_serial / args.steps,
         "other_order": other,
+        "merged_vs_unmerged": unmerged,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))

@@ -46,6 +46,24 @@ def forward(layers, edge_type, rel_src, rel_dst, X0, gather_ids, params, agg, he
     return out
 
 
+def xent(hs, Wc, bc, labels):
+    """Linear classifier + mean softmax cross-entropy on the seed rows ``hs``
+    (fp64): returns loss, dlog = (softmax - onehot) / B, dWc, dbc, dhs."""
+    hs = np.asarray(hs, np.float64)
+    Wc = np.asarray(Wc, np.float64)
+    logits = hs @ Wc + np.asarray(bc, np.float64)
+    B = len(labels)
+    z = logits - logits.max(axis=1, keepdims=True)
+    lse = np.log(np.exp(z).sum(axis=1))
+    loss = float(np.mean(lse - z[np.arange(B), labels]))
+    p = np.exp(z)
+    p /= p.sum(axis=1, keepdims=True)
+    dlog = p.copy()
+    dlog[np.arange(B), labels] -= 1.0
+    dlog /= B
+    return dict(loss=loss, dlog=dlog, dWc=hs.T @ dlog, dbc=dlog.sum(axis=0), dhs=dlog @ Wc.T)
+
+
 def backward(fw, layers, edge_type, params, labels, agg, heads, slope=0.2):
     """Gradients of the mean cross-entropy w.r.t. every parameter."""
     logits = fw["logits"]

@@ -153,7 +153,11 @@ k_head_logits(int B, int D, int C, const float* __restrict__ Hs, const float* __
     }
 }
 
-// 8 rows (one per warp) per block; lg is turned into dlog in place.
+// 8 rows (one per warp) per block; lg is turned into dlog in place.  NV > 0:
+// the row (C <= 32 NV) is loaded once into registers with all loads in flight
+// together (the loops of the generic NV = 0 path are latency-bound: one
+// dependent L2 round trip per 32 columns per pass).
+template <int NV>
 __global__ void __launch_bounds__(256)
 k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__ lg,
                float* __restrict__ block_loss, int* __restrict__ ticket, float* __restrict__ loss) {
@@ -164,18 +168,49 @@ k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__
   float rl = 0.f;
   if (b < B) {
     float* x = lg + (long long)b * C;
-    float mx = -INFINITY;
-    for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float se = 0.f;
-    for (int c = lane; c < C; c += 32) se += expf(x[c] - mx);
-    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
     const int y = labels[b];
-    const float ly = x[y];
-    __syncwarp();
     const float inv = 1.f / (float)B;
-    for (int c = lane; c < C; c += 32) x[c] = (expf(x[c] - mx) / se - (c == y ? 1.f : 0.f)) * inv;
-    rl = logf(se) + mx - ly;
+    float mx = -INFINITY, se = 0.f, ly;
+    if constexpr (NV > 0) {
+      float v[NV];
+#pragma unroll
+      for (int q = 0; q < NV; q++) {
+        const int c = lane + 32 * q;
+        v[q] = c < C ? x[c] : -INFINITY;
+      }
+      {
+        // the label's raw logit: owner lane y % 32, register y / 32
+        float e = 0.f;
+#pragma unroll
+        for (int q = 0; q < NV; q++)
+          if (q == (y >> 5)) e = v[q];
+        ly = __shfl_sync(0xffffffffu, e, y & 31);
+      }
+#pragma unroll
+      for (int q = 0; q < NV; q++) mx = fmaxf(mx, v[q]);
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+#pragma unroll
+      for (int q = 0; q < NV; q++) {
+        v[q] = expf(v[q] - mx);          // exp(-inf) = 0 for the padding
+        se += v[q];
+      }
+      for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+#pragma unroll
+      for (int q = 0; q < NV; q++) {
+        const int c = lane + 32 * q;
+        if (c < C) x[c] = (v[q] / se - (c == y ? 1.f : 0.f)) * inv;
+      }
+      rl = logf(se) + mx - ly;
+    } else {
+      for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int c = lane; c < C; c += 32) se += expf(x[c] - mx);
+      for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      ly = x[y];
+      __syncwarp();
+      for (int c = lane; c < C; c += 32) x[c] = (expf(x[c] - mx) / se - (c == y ? 1.f : 0.f)) * inv;
+      rl = logf(se) + mx - ly;
+    }
   }
   if (lane == 0) s_l[w] = rl;
   __syncthreads();
@@ -340,7 +375,13 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   const float* Hs = d_H + h_row0 * D;
   HF_LAUNCH(k_head_logits, dim3(ceil_div(C, kBN), ceil_div(B, kBM)), 128, 0, s, B, D, C, Hs, d_Wc,
             d_bc, dlog, ticket, 1);
-  HF_LAUNCH(k_head_softmax, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket, d_loss);
+  if (C <= 128)
+    HF_LAUNCH(k_head_softmax<4>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket, d_loss);
+  else if (C <= 512)
+    HF_LAUNCH(k_head_softmax<16>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket,
+              d_loss);
+  else
+    HF_LAUNCH(k_head_softmax<0>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket, d_loss);
   HF_LAUNCH(k_head_grads, (h.dh_tiles + h.dw_tiles) * kSlices, 128, 0, s, B, D, C, h, Hs, d_Wc,
             dlog, d_dH + h_row0 * D, d_dWc, d_dbc);
   return last_cuda();

@@ -69,14 +69,15 @@ def _mirror(rels):
     return tuple(out)
 
 
-def _freebase_rels():
+def _freebase_rels(n_fwd=18):
     # 18 forward relations over distinct ordered type pairs, round-robin
     # ("round-robin over type pairs"), then 18 reverses;
-    # 1,057,688 edges split evenly over the 36 relations.
+    # 1,057,688 edges split evenly over the 36 relations.  Other n_fwd: the
+    # supplementary R-sweep, same total edge count.
     total = 1_057_688
-    per = total // 36
+    per = total // (2 * n_fwd)
     fwd = []
-    for k in range(18):
+    for k in range(n_fwd):
         s = k % 8
         t = (s + 1 + k // 8) % 8
         fwd.append(RelSpec(f"r{k}", s, t, per))
@@ -137,3 +138,19 @@ CONFIGS = {
 }
 
 CONFIG_ORDER = ("acm", "dblp", "imdb", "mag", "freebase")
+
+
+def freebase_sweep(num_rels: int, model: str = "rgat") -> WorkloadConfig:
+    """Freebase-shaped graph with ``num_rels`` relations (even: forward +
+    reverse) and the same total edge count; the supplementary R-sweep of
+    SURVEY.md §8(d) (kernels per layer vs relation count)."""
+    import dataclasses
+    if num_rels % 2:
+        raise ValueError("num_rels must be even (forward + reverse relations)")
+    base = CONFIGS["freebase"]
+    extra = {} if model == "rgat" else dict(model="rgcn", agg="mean", heads=1)
+    what = "RGAT (8 heads)" if model == "rgat" else "RGCN (mean)"
+    return dataclasses.replace(
+        base, key=f"freebase_r{num_rels}_{model}", rels=_freebase_rels(num_rels // 2),
+        description=f"Freebase-shaped R-sweep ({num_rels} relations, 8 types, feat 64), "
+                    f"2-layer {what}, batch 2048, fanout [10,10]", **extra)

@@ -294,3 +294,35 @@ def test_project_tf32_exact_on_representable_inputs(K, D):
     assert np.array_equal(dW.cpu().numpy(), ob["dW_rel"].astype(np.float32))
     assert np.array_equal(dWr.cpu().numpy(), ob["dW_root"].astype(np.float32))
     assert np.array_equal(dX.cpu().numpy(), ob["dX"].astype(np.float32))
+
+
+@pytest.mark.parametrize("B,C", [(5, 3), (128, 7), (1024, 128), (300, 129), (1024, 349),
+                                 (64, 600)])
+def test_linear_xent(B, C):
+    """Classifier head: loss, dH (seed rows; other rows zero), dWc,
+    dbc against the fp64 oracle head; register-row (C <= 512) and generic
+    softmax paths.  3xTF32 GEMMs: fp32-level error, 1e-5 of the scale."""
+    import oracle.model as om
+    rng = np.random.default_rng(B * 1000 + C)
+    D, row0, extra = 128, 17, 9
+    Hfull = rng.standard_normal((row0 + B + extra, D)).astype(np.float32)
+    Wc = (rng.standard_normal((D, C)) * 0.1).astype(np.float32)
+    bc = (rng.standard_normal(C) * 0.1).astype(np.float32)
+    lab = rng.integers(0, C, B).astype(np.int32)
+    ref = om.xent(Hfull[row0:row0 + B], Wc, bc, lab)
+    loss = torch.zeros(1, device=DEV)
+    dH = torch.full((Hfull.shape[0], D), 7.0, device=DEV)
+    dWc = torch.zeros(D, C, device=DEV)
+    dbc = torch.zeros(C, device=DEV)
+    ws = torch.empty(hf().xent_ws_bytes(B, D, C) // 4 + 64, device=DEV)
+    hf().linear_xent(B, D, C, t(Hfull), row0, torch.from_numpy(lab).to(DEV), t(Wc), t(bc), loss,
+                     dH, dWc, dbc, ws)
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref["loss"]) <= 1e-5 * max(1.0, abs(ref["loss"]))
+    dHh = dH.cpu().numpy()
+    assert not dHh[:row0].any() and not dHh[row0 + B:].any()
+    sc = np.abs(ref["dlog"]).sum(axis=1, keepdims=True) * np.abs(Wc).max() + 1e-30
+    assert np.all(np.abs(dHh[row0:row0 + B] - ref["dhs"]) <= 1e-5 * sc)
+    sw = np.abs(Hfull[row0:row0 + B]).T @ np.abs(ref["dlog"]) + 1e-30
+    assert np.all(np.abs(dWc.cpu().numpy() - ref["dWc"]) <= 1e-5 * sw)
+    assert np.all(np.abs(dbc.cpu().numpy() - ref["dbc"]) <= 1e-5 * np.abs(ref["dlog"]).sum(0) + 1e-12)
