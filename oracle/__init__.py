@@ -24,7 +24,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "hifuse_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-AGG = {"sum": 0, "mean": 1, "gat": 2}
+AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3}
 
 
 def build_lib(force: bool = False) -> str:
@@ -135,7 +135,7 @@ def aggregate_fwd(shape: Shape, blk, edge_type, csr, agg, D, H, Y, s_src=None, s
     N = shape.N
     Z = np.zeros((max(shape.rows, 1), D))
     deg = np.zeros(max(shape.rows, 1))
-    alpha = np.zeros((max(N, 1), H)) if AGG[agg] == 2 else None
+    alpha = np.zeros((max(N, 1), H)) if AGG[agg] >= 2 else None
     Yc = _f64(Y) if len(Y) else np.zeros((1, D))
     ss = _f64(s_src) if s_src is not None and len(s_src) else np.zeros((1, H))
     sd = _f64(s_dst) if s_dst is not None and len(s_dst) else np.zeros((1, H))

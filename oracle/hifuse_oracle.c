@@ -221,7 +221,8 @@ void oracle_project(int T, int R, const int32_t *rel_src, const int32_t *rel_dst
 /* SrcIndex[i]) (line 254); DstIndex appended (line 256); after the loop one */
 /* Aggregate(FeatureCat, DstIndexCat) (line 260) whose segments are the      */
 /* (relation, destination) pairs (reading C2).  agg: 0 sum, 1 mean (C1),     */
-/* 2 GAT edge-softmax within (relation, destination) (C5, C6, C8).           */
+/* 2 GAT edge-softmax within (relation, destination) (C5, C6, C8), 3 GAT     */
+/* edge-softmax across the relations of a destination (gat_xrel_fwd).        */
 /* Edges are taken from the block itself (Alg. 2 selection, line 318), the   */
 /* Y row of (r, src) from the compact layout (rel_y_off, y_src).             */
 /* ------------------------------------------------------------------------ */
@@ -276,6 +277,137 @@ static void relation_rows(int R, const int32_t *rel_src, const int32_t *rel_dst,
 
 static double leaky(double x, double slope) { return x > 0 ? x : slope * x; }
 
+/* GAT with the softmax ACROSS relations (reading
+ * C5' in DESIGN.md; the PyG RGATConv default): for destination (t, i) and
+ * head h, alpha_e = softmax over ALL in-edges of (t, i), whatever their
+ * relation, of l_e = LeakyReLU(s_src[col_e] + s_dst[(r_e, i)]); each
+ * relation's row still receives only its own edges' terms,
+ * Z[(r,i)] = sum_{e in row (r,i)} alpha_e Y[col_e], so the semantic fusion
+ * sum over r (O4) is the attention-weighted sum over all neighbours.
+ * Edge order inside the union: relation ascending, then the row's order. */
+static void gat_xrel_fwd(int T, int R, const int32_t *rel_src, const int32_t *rel_dst,
+                         const int32_t *n_src, const int32_t *n_dst,
+                         int64_t N, const int32_t *src, const int32_t *dst, const int64_t *eid,
+                         const int32_t *edge_type, int64_t E,
+                         const int32_t *rel_y_off, const int32_t *y_src,
+                         int D, int H, double slope, const double *Y, const double *s_src,
+                         const double *s_dst, const int64_t *rro, double *Z, double *deg_out,
+                         double *alpha)
+{
+    int dh = D / H;
+    int64_t **ptr = (int64_t **)malloc(sizeof(int64_t *) * R);
+    int64_t **list = (int64_t **)malloc(sizeof(int64_t *) * R);
+    for (int r = 0; r < R; r++)
+        relation_rows(R, rel_src, rel_dst, n_src, n_dst, r, N, src, dst, eid, edge_type, E,
+                      &ptr[r], &list[r]);
+    for (int t = 0; t < T; t++)
+        for (int32_t i = 0; i < n_dst[t]; i++) {
+            for (int r = 0; r < R; r++)
+                if (rel_dst[r] == t) deg_out[rro[r] + i] = (double)(ptr[r][i + 1] - ptr[r][i]);
+            for (int h = 0; h < H; h++) {
+                double m = -INFINITY, sum = 0.0;
+                for (int r = 0; r < R; r++) {
+                    if (rel_dst[r] != t) continue;
+                    for (int64_t k = ptr[r][i]; k < ptr[r][i + 1]; k++) {
+                        int32_t u = yrow_of(rel_y_off, y_src, r, src[list[r][k]]);
+                        double l = leaky(s_src[(int64_t)u * H + h] + s_dst[(rro[r] + i) * H + h], slope);
+                        if (l > m) m = l;
+                    }
+                }
+                for (int r = 0; r < R; r++) {
+                    if (rel_dst[r] != t) continue;
+                    for (int64_t k = ptr[r][i]; k < ptr[r][i + 1]; k++) {
+                        int32_t u = yrow_of(rel_y_off, y_src, r, src[list[r][k]]);
+                        sum += exp(leaky(s_src[(int64_t)u * H + h] + s_dst[(rro[r] + i) * H + h], slope) - m);
+                    }
+                }
+                for (int r = 0; r < R; r++) {
+                    if (rel_dst[r] != t) continue;
+                    double *z = Z + (rro[r] + i) * D;
+                    for (int64_t k = ptr[r][i]; k < ptr[r][i + 1]; k++) {
+                        int32_t u = yrow_of(rel_y_off, y_src, r, src[list[r][k]]);
+                        double a = exp(leaky(s_src[(int64_t)u * H + h] + s_dst[(rro[r] + i) * H + h], slope) - m) / sum;
+                        if (alpha) alpha[list[r][k] * H + h] = a;
+                        for (int c = 0; c < dh; c++) z[h * dh + c] += a * Y[(int64_t)u * D + h * dh + c];
+                    }
+                }
+            }
+        }
+    for (int r = 0; r < R; r++) { free(ptr[r]); free(list[r]); }
+    free(ptr); free(list);
+}
+
+/* Adjoint of gat_xrel_fwd.  The fusion sum gives dZ[(r,i)] = G_t[i] for every
+ * row of (t, i), so with o = sum_r Z[(r,i)] (head h):
+ *   dalpha_e = <g_h, y_e>,  dl_e = alpha_e (dalpha_e - sum_{e' in union} alpha_e' dalpha_e'). */
+static void gat_xrel_bwd(int T, int R, const int32_t *rel_src, const int32_t *rel_dst,
+                         const int32_t *n_src, const int32_t *n_dst,
+                         int64_t N, const int32_t *src, const int32_t *dst, const int64_t *eid,
+                         const int32_t *edge_type, int64_t E,
+                         const int32_t *rel_y_off, const int32_t *y_src,
+                         int D, int H, double slope, const double *Gt, const double *Y,
+                         const double *s_src, const double *s_dst, const int64_t *rro,
+                         const int64_t *tdo, double *dY, double *ds_src, double *ds_dst)
+{
+    int dh = D / H;
+    int64_t **ptr = (int64_t **)malloc(sizeof(int64_t *) * R);
+    int64_t **list = (int64_t **)malloc(sizeof(int64_t *) * R);
+    for (int r = 0; r < R; r++)
+        relation_rows(R, rel_src, rel_dst, n_src, n_dst, r, N, src, dst, eid, edge_type, E,
+                      &ptr[r], &list[r]);
+    for (int t = 0; t < T; t++)
+        for (int32_t i = 0; i < n_dst[t]; i++) {
+            const double *g = Gt + (tdo[t] + i) * D;
+            for (int h = 0; h < H; h++) {
+                double m = -INFINITY, sum = 0.0, za = 0.0;
+                for (int r = 0; r < R; r++) {
+                    if (rel_dst[r] != t) continue;
+                    for (int64_t k = ptr[r][i]; k < ptr[r][i + 1]; k++) {
+                        int32_t u = yrow_of(rel_y_off, y_src, r, src[list[r][k]]);
+                        double l = leaky(s_src[(int64_t)u * H + h] + s_dst[(rro[r] + i) * H + h], slope);
+                        if (l > m) m = l;
+                    }
+                }
+                for (int r = 0; r < R; r++) {
+                    if (rel_dst[r] != t) continue;
+                    for (int64_t k = ptr[r][i]; k < ptr[r][i + 1]; k++) {
+                        int32_t u = yrow_of(rel_y_off, y_src, r, src[list[r][k]]);
+                        sum += exp(leaky(s_src[(int64_t)u * H + h] + s_dst[(rro[r] + i) * H + h], slope) - m);
+                    }
+                }
+                for (int r = 0; r < R; r++) {
+                    if (rel_dst[r] != t) continue;
+                    for (int64_t k = ptr[r][i]; k < ptr[r][i + 1]; k++) {
+                        int32_t u = yrow_of(rel_y_off, y_src, r, src[list[r][k]]);
+                        double a = exp(leaky(s_src[(int64_t)u * H + h] + s_dst[(rro[r] + i) * H + h], slope) - m) / sum;
+                        double da = 0.0;
+                        for (int c = 0; c < dh; c++) da += g[h * dh + c] * Y[(int64_t)u * D + h * dh + c];
+                        za += a * da;
+                    }
+                }
+                for (int r = 0; r < R; r++) {
+                    if (rel_dst[r] != t) continue;
+                    int64_t row = rro[r] + i;
+                    for (int64_t k = ptr[r][i]; k < ptr[r][i + 1]; k++) {
+                        int32_t u = yrow_of(rel_y_off, y_src, r, src[list[r][k]]);
+                        double pre = s_src[(int64_t)u * H + h] + s_dst[row * H + h];
+                        double a = exp(leaky(pre, slope) - m) / sum;
+                        double da = 0.0;
+                        for (int c = 0; c < dh; c++) {
+                            da += g[h * dh + c] * Y[(int64_t)u * D + h * dh + c];
+                            dY[(int64_t)u * D + h * dh + c] += a * g[h * dh + c];
+                        }
+                        double dpre = a * (da - za) * (pre > 0 ? 1.0 : slope);
+                        ds_src[(int64_t)u * H + h] += dpre;
+                        ds_dst[row * H + h] += dpre;
+                    }
+                }
+            }
+        }
+    for (int r = 0; r < R; r++) { free(ptr[r]); free(list[r]); }
+    free(ptr); free(list);
+}
+
 void oracle_aggregate_fwd(int T, int R, const int32_t *rel_src, const int32_t *rel_dst,
                           const int32_t *n_src, const int32_t *n_dst,
                           int64_t N, const int32_t *src, const int32_t *dst, const int64_t *eid,
@@ -293,6 +425,12 @@ void oracle_aggregate_fwd(int T, int R, const int32_t *rel_src, const int32_t *r
     memset(Z, 0, sizeof(double) * rows * D);
     memset(deg_out, 0, sizeof(double) * rows);
     int dh = D / H;
+    if (agg == 3) {
+        gat_xrel_fwd(T, R, rel_src, rel_dst, n_src, n_dst, N, src, dst, eid, edge_type, E,
+                     rel_y_off, y_src, D, H, slope, Y, s_src, s_dst, rro, Z, deg_out, alpha);
+        free(rro);
+        return;
+    }
     for (int r = 0; r < R; r++) {
         /* lines 254-256: IndexSelect of the relation's sources, DstIndex kept */
         int64_t *ptr, *list;
@@ -407,8 +545,15 @@ void oracle_aggregate_bwd(int T, int R, const int32_t *rel_src, const int32_t *r
     for (int r = 0; r < R; r++) { rro[r] = rows; rows += n_dst[rel_dst[r]]; }
     rro[R] = rows;
     memset(dY, 0, sizeof(double) * U * D);
-    if (agg == 2) { memset(ds_src, 0, sizeof(double) * U * H); memset(ds_dst, 0, sizeof(double) * rows * H); }
+    if (agg >= 2) { memset(ds_src, 0, sizeof(double) * U * H); memset(ds_dst, 0, sizeof(double) * rows * H); }
     int dh = D / H;
+    if (agg == 3) {
+        gat_xrel_bwd(T, R, rel_src, rel_dst, n_src, n_dst, N, src, dst, eid, edge_type, E,
+                     rel_y_off, y_src, D, H, slope, Gt, Y, s_src, s_dst, rro, tdo, dY, ds_src,
+                     ds_dst);
+        free(rro); free(tdo);
+        return;
+    }
     for (int r = 0; r < R; r++) {
         int t = rel_dst[r];
         int64_t *ptr, *list;
