@@ -240,6 +240,7 @@ def config_obj(cfg, args, extra=None):
          "hidden": cfg.hidden, "heads": cfg.heads, "relations": cfg.num_rels,
          "parallelism": f"dp{args.gpus}", "precision": args.prec,
          "order": getattr(args, "order", "project_first"),
+         "aggregation": cfg.agg,
          "l2": "inputs larger than L2: a pool of distinct sampled batches, per-step working "
                "set above the 126 MB L2 for mag"}
     if extra:
@@ -268,8 +269,15 @@ def main():
     ap.add_argument("--pipeline", type=int, default=1,
                     help="1: overlap the next batch's semantic-graph build with this "
                          "batch's compute (side stream); 0: serial steps")
+    ap.add_argument("--gat-softmax", default="relation", choices=["relation", "across"],
+                    help="RGAT edge-softmax domain: within each (relation, destination) row "
+                         "(reading C5, default) or across all relations of a destination "
+                         "(C5', SURVEY §8(f) NEXT(2))")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if cfg.model == "rgat" and args.gat_softmax == "across":
+        import dataclasses
+        cfg = dataclasses.replace(cfg, agg="gat_xrel")
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))

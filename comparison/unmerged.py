@@ -208,6 +208,22 @@ def compare_layers(hf, tr, db, cfg, feat_d, et_d, params, stage_kernels):
         rec["merged_kernels_bwd"] = int(sum(stage_kernels[n][1] for n in bwd_names))
         rec["merged_us_fwd_bwd"] = round(sum(stage_kernels[n][0] for n in fwd_names + bwd_names)
                                          * 1e3, 2)
+        if cfg.agg == "gat_xrel":
+            # across-relation softmax: one warp per destination; the
+            # per-relation arms have no per-relation meaning here
+            a = acts[l]
+            Yr = torch.randn(max(sh.U_max, 1), D, device=dev)
+            Z = torch.empty(max(sh.rows, 1), D, device=dev)
+            stats = torch.empty(max(sh.rows, 1), 2 * H, device=dev)
+            merged = lambda: hf.aggregate_fwd_xrel(sh, csrs[l], D, H, tr.slope, Yr, a["s_src"],
+                                                   a["s_dst"], Z, stats)
+            n0 = hf.kernel_launches()
+            merged()
+            rec["agg_fwd_merged_launches"] = hf.kernel_launches() - n0
+            rec["agg_fwd_merged_us"] = round(_graph_ms(merged) * 1e3, 2)
+            out["layers"].append(rec)
+            X = acts[l]["H"][:sh.dst_rows].detach()
+            continue
         # (a) torch per-relation layer, fwd + bwd
         ti = TorchLayerInputs(db, l, et_d, X.detach(), K, D, H, cfg.model, params["layers"][l],
                               dev)

@@ -71,7 +71,10 @@ typedef enum {
 #define HIFUSE_ST_BAD_DST     8   /* dst_local >= n_dst(dst type of relation)   */
 #define HIFUSE_ST_UNSORTED_TYPES 16 /* edge_type not relation-major (offsets unusable) */
 
-typedef enum { HIFUSE_AGG_SUM = 0, HIFUSE_AGG_MEAN = 1, HIFUSE_AGG_GAT = 2 } hifuse_agg;
+/* GAT_XREL: GAT with the edge-softmax across the relations of a destination
+ * (hifuse_aggregate_fwd_xrel, reading C5'). */
+typedef enum { HIFUSE_AGG_SUM = 0, HIFUSE_AGG_MEAN = 1, HIFUSE_AGG_GAT = 2,
+               HIFUSE_AGG_GAT_XREL = 3 } hifuse_agg;
 typedef enum { HIFUSE_ACT_NONE = 0, HIFUSE_ACT_RELU = 1 } hifuse_act;
 /* Layout of the merged projected matrix Y (reading C3).  COMPACT:
  * per relation, one row per distinct source vertex of the layer, ascending.
@@ -201,6 +204,25 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr *csr, int64_t rows, hifuse_a
                                    const float *d_s_src, const float *d_s_dst, float *d_Z,
                                    float *d_stats, hifuse_stream_t stream);
 
+/* A4, GAT variant with the softmax ACROSS relations (SURVEY.md §8(f) NEXT(2),
+ * DESIGN.md reading C5'; PAPER.md is silent on the softmax domain, line 123
+ * leaves the fusion rule open).  For destination (t, i) and head h:
+ *   alpha_p = softmax over the union of rows {(r, i) : t(r) = t} of
+ *             LeakyReLU_slope(s_src[col[p],h] + s_dst[(r,i),h]),
+ *   Z[(r,i), head h] = sum_{p in row (r,i)} alpha_p Y[col[p], head h],
+ * so hifuse_semantic_fuse's sum over r is the attention-weighted sum over all
+ * neighbours.  Still ONE kernel for all relations (one warp per destination,
+ * walking its rows through the host-known rel_row_off).  d_stats [rows, 2H]
+ * holds the destination's (max, sum of exp) in every one of its rows; empty
+ * destinations give Z = 0, stats 0.  Arguments as hifuse_aggregate_fwd plus
+ * the layer shape; errors: INVALID_ARG (null buffers), UNSUPPORTED (D not
+ * 64/128, or D/H not a power of two >= 4), ALIGNMENT (Y, Z not 16-byte
+ * aligned).  The backward is hifuse_aggregate_bwd with HIFUSE_AGG_GAT_XREL. */
+hifuse_status hifuse_aggregate_fwd_xrel(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                        int D, int heads, float slope, const float *d_Y,
+                                        const float *d_s_src, const float *d_s_dst, float *d_Z,
+                                        float *d_stats, hifuse_stream_t stream);
+
 /* A5. Semantic fusion (readings C2, C4, C10):
  *   H_t[i] = act(R0_t[i] + bias_t + sum_{r: t(r)=t} Z[rel_row_off[r] + i]).
  * Z [rows, D]; R0 [sum n_dst, D] or NULL; bias [T, D] or NULL; H [sum n_dst, D]
@@ -224,6 +246,8 @@ hifuse_status hifuse_semantic_fuse_bwd(const hifuse_layer_shape *shape, int D, h
  *   GAT: pass 1 (row-major) recomputes alpha from d_stats and forms
  *        dpre = alpha (dalpha - sum alpha dalpha) LeakyReLU', ds_dst[m,h] = sum dpre;
  *        pass 2 (CSC): dY[u,head h] = sum alpha G[g(row),head h], ds_src[u,h] = sum dpre.
+ *   GAT_XREL: as GAT, but pass 1 runs per destination and sum alpha dalpha
+ *        is taken over the destination's union of rows (the fused output).
  * g(r, i) = type_dst_off[t(r)] + i maps a merged row to its row of G.  dY
  * excludes the score-chain term (hifuse_project_bwd adds it).  Workspace:
  * hifuse_aggregate_bwd_ws_bytes() (GAT: 2 N H floats). */

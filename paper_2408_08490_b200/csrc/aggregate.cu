@@ -720,6 +720,210 @@ k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
   }
 }
 
+// ------------------------------------ GAT with the softmax across relations
+// (reading C5'): the softmax of
+// destination (t, i) runs over the union of its rows (r, i), t(r) = t, i.e.
+// over all its in-edges whatever their relation; each row still receives its
+// own edges' terms, so the semantic fusion's sum over r is the attention-
+// weighted sum over all neighbours.  One warp per DESTINATION walks the rows
+// of the relations into its type (relation order): pass 1 the max, pass 2 the
+// normaliser, pass 3 each row's sum p Y / l.  stats (m, l) are written to
+// every row of the destination, so the per-row backward machinery (pass 2 over
+// the CSC) recomputes the same alpha.
+struct XrelMeta {
+  int T;
+  int type_dst_off[HF_MAX_T + 1];
+  int trel_off[HF_MAX_T + 1];     // relations into type t: trel_row[trel_off[t] .. trel_off[t+1])
+  int trel_row[HF_MAX_R];         // rel_row_off[r] of those relations, ascending r
+};
+
+__device__ __forceinline__ int xrel_type(const XrelMeta& xm, int d) {
+  int t = 0;
+  while (t + 1 < xm.T && xm.type_dst_off[t + 1] <= d) t++;
+  return t;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_fwd_gat_xrel(XrelMeta xm, int dst_rows, int H, float slope, const int* __restrict__ row_ptr,
+                   const int* __restrict__ col, const float4* __restrict__ Y,
+                   const float* __restrict__ s_src, const float* __restrict__ s_dst,
+                   float4* __restrict__ Z, float* __restrict__ stats) {
+  constexpr int LPR = D / 4;
+  constexpr int NS = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % LPR, sid = lane / LPR;
+  const int d = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (d >= dst_rows) return;
+  const int t = xrel_type(xm, d);
+  const int i = d - xm.type_dst_off[t];
+  const int q0 = xm.trel_off[t], q1 = xm.trel_off[t + 1];
+  const int dh4 = (D / H) / 4;
+  const int h = sl / dh4;
+  // pass 1: max of the logits over the union
+  float m = -INFINITY;
+  int deg = 0;
+  for (int q = q0; q < q1; q++) {
+    const long long row = (long long)xm.trel_row[q] + i;
+    const int b = row_ptr[row], e = row_ptr[row + 1];
+    deg += e - b;
+    const float sd = s_dst[row * H + h];
+    for (int p = b + sid; p < e; p += NS)
+      m = fmaxf(m, leaky(__ldg(s_src + (long long)__ldg(col + p) * H + h) + sd, slope));
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  // pass 2: normaliser
+  float l = 0.f;
+  for (int q = q0; q < q1; q++) {
+    const long long row = (long long)xm.trel_row[q] + i;
+    const int b = row_ptr[row], e = row_ptr[row + 1];
+    const float sd = s_dst[row * H + h];
+    for (int p = b + sid; p < e; p += NS)
+      l += expf(leaky(__ldg(s_src + (long long)__ldg(col + p) * H + h) + sd, slope) - m);
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if (deg == 0) { m = 0.f; l = 0.f; }
+  // pass 3: every row's share
+  for (int q = q0; q < q1; q++) {
+    const long long row = (long long)xm.trel_row[q] + i;
+    const int b = row_ptr[row], e = row_ptr[row + 1];
+    const float sd = s_dst[row * H + h];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int base = b; base < e; base += 32) {
+      const int n = min(32, e - base);
+      const int my_col = lane < n ? __ldg(col + base + lane) : 0;
+      int k = 0;
+      for (; k + NS * kUnroll <= n; k += NS * kUnroll) {
+        float4 v[kUnroll];
+        float sc[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+          int c = __shfl_sync(0xffffffffu, my_col, k + u * NS + sid);
+          v[u] = ldg4(Y + (long long)c * LPR + sl);
+          sc[u] = __ldg(s_src + (long long)c * H + h);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++)
+          acc = f4fma(expf(leaky(sc[u] + sd, slope) - m), v[u], acc);
+      }
+      for (; k < n; k += NS) {
+        int idx = k + sid;
+        int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+        if (idx < n)
+          acc = f4fma(expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - m),
+                      ldg4(Y + (long long)c * LPR + sl), acc);
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
+    if (sid == 0) {
+      if (e > b)
+        acc = make_float4(__fdiv_rn(acc.x, l), __fdiv_rn(acc.y, l), __fdiv_rn(acc.z, l),
+                          __fdiv_rn(acc.w, l));
+      Z[row * LPR + sl] = acc;
+      if (sl % dh4 == 0) {
+        stats[row * 2 * H + h] = m;
+        stats[row * 2 * H + H + h] = l;
+      }
+    }
+  }
+}
+
+// Backward pass 1, across relations: as k_agg_bwd_gat_rows, but
+// za = sum alpha dalpha runs over the destination's union of rows (the fused
+// output is the sum over them); g = G[d] is shared by all of its rows.
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_xrel_dst(XrelMeta xm, int dst_rows, int H, float slope,
+                       const int* __restrict__ row_ptr, const int* __restrict__ col,
+                       const float4* __restrict__ Y, const float* __restrict__ s_src,
+                       const float* __restrict__ s_dst, const float* __restrict__ stats,
+                       const float4* __restrict__ G, float* __restrict__ alpha,
+                       float* __restrict__ dpre, float* __restrict__ ds_dst) {
+  constexpr int LPR = D / 4;
+  constexpr int NS = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % LPR, sid = lane / LPR;
+  const int d = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (d >= dst_rows) return;
+  const int t = xrel_type(xm, d);
+  const int i = d - xm.type_dst_off[t];
+  const int q0 = xm.trel_off[t], q1 = xm.trel_off[t + 1];
+  const int dh4 = (D / H) / 4;
+  const int h = sl / dh4;
+  const bool head_lead = (sl % dh4) == 0;
+  const float4 g = ldg4(G + (long long)d * LPR + sl);
+  float za = 0.f;
+  for (int q = q0; q < q1; q++) {
+    const long long row = (long long)xm.trel_row[q] + i;
+    const int b = row_ptr[row], e = row_ptr[row + 1];
+    if (e == b) continue;
+    const float sd = s_dst[row * H + h];
+    const float mx = stats[row * 2 * H + h];
+    const float inv_l = 1.f / stats[row * 2 * H + H + h];
+    for (int base = b; base < e; base += 32) {
+      const int n = min(32, e - base);
+      const int my_col = lane < n ? __ldg(col + base + lane) : 0;
+      for (int k = 0; k < n; k += NS) {
+        int idx = k + sid;
+        int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+        float part = 0.f, a = 0.f;
+        if (idx < n) {
+          float4 y = ldg4(Y + (long long)c * LPR + sl);
+          part = g.x * y.x + g.y * y.y + g.z * y.z + g.w * y.w;
+          a = expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - mx) * inv_l;
+        }
+        for (int o = 1; o < dh4; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (idx < n) {
+          za += a * part;
+          if (head_lead) {
+            alpha[(long long)(base + idx) * H + h] = a;
+            dpre[(long long)(base + idx) * H + h] = part;   // dalpha, overwritten below
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) za += __shfl_xor_sync(0xffffffffu, za, o);
+  __syncwarp();
+  for (int q = q0; q < q1; q++) {
+    const long long row = (long long)xm.trel_row[q] + i;
+    const int b = row_ptr[row], e = row_ptr[row + 1];
+    const float sd = s_dst[row * H + h];
+    float dsd = 0.f;
+    if (head_lead) {
+      for (int p = b + sid; p < e; p += NS) {
+        int c = __ldg(col + p);
+        float pre = __ldg(s_src + (long long)c * H + h) + sd;
+        float a = alpha[(long long)p * H + h];
+        float da = dpre[(long long)p * H + h];
+        float dp = a * (da - za) * (pre > 0.f ? 1.f : slope);
+        dpre[(long long)p * H + h] = dp;
+        dsd += dp;
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) dsd += __shfl_xor_sync(0xffffffffu, dsd, o);
+    if (sid == 0 && head_lead) ds_dst[row * H + h] = dsd;
+  }
+}
+
+static void make_xrel(const LayerMeta& m, XrelMeta* xm) {
+  xm->T = m.T;
+  int q = 0;
+  for (int t = 0; t < m.T; t++) {
+    xm->type_dst_off[t] = m.type_dst_off[t];
+    xm->trel_off[t] = q;
+    for (int r = 0; r < m.R; r++)
+      if (m.rel_dst[r] == t) xm->trel_row[q++] = m.rel_row_off[r];
+  }
+  xm->type_dst_off[m.T] = m.type_dst_off[m.T];
+  xm->trel_off[m.T] = q;
+}
+
 static bool heads_ok(int D, int H) {
   if (H <= 0 || D % H) return false;
   int dh = D / H;
@@ -743,7 +947,7 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_a
   cudaStream_t s = st(stream);
   unsigned grid = ceil_div(rows, kWarpsPerBlock);
   const int TB = kWarpsPerBlock * 32;
-  if (agg == HIFUSE_AGG_GAT) {
+  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL) {
     if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
     if (rows > 0 && (!d_s_src || !d_s_dst || !d_stats)) return HIFUSE_ERR_INVALID_ARG;
     if (D == 128)
@@ -763,6 +967,33 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_a
   } else {
     return HIFUSE_ERR_INVALID_ARG;
   }
+  return last_cuda();
+}
+
+hifuse_status hifuse_aggregate_fwd_xrel(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                        int D, int heads, float slope, const float* d_Y,
+                                        const float* d_s_src, const float* d_s_dst, float* d_Z,
+                                        float* d_stats, hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!csr || !csr->row_ptr) return HIFUSE_ERR_INVALID_ARG;
+  if (D != 64 && D != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
+  if (m.rows > 0 && (!d_Z || !d_stats || !d_s_dst || (m.N > 0 && (!csr->col || !d_Y || !d_s_src))))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_Y) || !aligned16(d_Z)) return HIFUSE_ERR_ALIGNMENT;
+  XrelMeta xm;
+  make_xrel(m, &xm);
+  cudaStream_t s = st(stream);
+  unsigned grid = ceil_div(m.dst_rows, kWarpsPerBlock);
+  const int TB = kWarpsPerBlock * 32;
+  if (D == 128)
+    HF_LAUNCH(k_agg_fwd_gat_xrel<128>, grid, TB, 0, s, xm, m.dst_rows, heads, slope, csr->row_ptr,
+              csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z, d_stats);
+  else
+    HF_LAUNCH(k_agg_fwd_gat_xrel<64>, grid, TB, 0, s, xm, m.dst_rows, heads, slope, csr->row_ptr,
+              csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z, d_stats);
   return last_cuda();
 }
 
@@ -811,7 +1042,8 @@ size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
   long long U_max = m.N < m.S ? m.N : m.S;
   size_t b = carve_bytes(U_max + 1, 4) + carve_bytes(2, 4);
-  if (agg == HIFUSE_AGG_GAT) b += 2 * carve_bytes((long long)m.N * heads, 4);
+  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL)
+    b += 2 * carve_bytes((long long)m.N * heads, 4);
   else b += carve_bytes((long long)(m.rows > 0 ? m.rows : 1) * 128, 4);   // pre-scaled rows
   return b;
 }
@@ -844,7 +1076,7 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
   unsigned gridU4 = ceil_div(U_max, kWarpsPerBlock * (32 / kLPC));
   const int TB = kWarpsPerBlock * 32;
   const unsigned gridL = 296;
-  if (agg == HIFUSE_AGG_GAT) {
+  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL) {
     if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
     if (!d_Y || !d_s_src || !d_s_dst || !d_stats || !d_ds_src || !d_ds_dst || !csr->csc_pos ||
         !csr->row_ptr || !csr->col || !csr->rel_row_off)
@@ -852,10 +1084,17 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
     float* alpha = carve<float>(p, (long long)m.N * heads);
     float* dpre = carve<float>(p, (long long)m.N * heads);
     unsigned gridR = ceil_div(m.rows, kWarpsPerBlock);
+    XrelMeta xm;
+    if (agg == HIFUSE_AGG_GAT_XREL) make_xrel(m, &xm);
 #define HF_GAT(DD)                                                                             \
-  HF_LAUNCH(k_agg_bwd_gat_rows<DD>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows, \
-            heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,       \
-            d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                              \
+  if (agg == HIFUSE_AGG_GAT_XREL)                                                              \
+    HF_LAUNCH(k_agg_bwd_gat_xrel_dst<DD>, ceil_div(m.dst_rows, kWarpsPerBlock), TB, 0, s, xm, \
+              m.dst_rows, heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src,   \
+              d_s_dst, d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                    \
+  else                                                                                         \
+    HF_LAUNCH(k_agg_bwd_gat_rows<DD>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows, \
+              heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,     \
+              d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                            \
   HF_LAUNCH(k_agg_bwd_gat_cols<DD>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,   \
             csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
             (float4*)d_dY, d_ds_src, long_list, long_cnt);                                    \

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # HIFUSE_LIB: an alternative build of the same library (experiments only)
 LIB_PATH = os.environ.get("HIFUSE_LIB") or os.path.join(_HERE, "libhifuse.so")
 
-AGG = {"sum": 0, "mean": 1, "gat": 2}
+AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3}
 ACT = {"none": 0, "relu": 1}
 LAYOUT_COMPACT = 1
 PREC = {"fp32": 0, "tf32": 1}
@@ -64,6 +64,7 @@ def lib():
             "hifuse_project": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp,
                                vp, vp, vp, sz, vp],
             "hifuse_aggregate_fwd": [vp, i64, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp],
+            "hifuse_aggregate_fwd_xrel": [vp, vp, i32, i32, f32, vp, vp, vp, vp, vp, vp],
             "hifuse_semantic_fuse": [vp, i32, i32, vp, vp, vp, vp, vp],
             "hifuse_fuse_bwd_ws_bytes": [vp, i32],
             "hifuse_semantic_fuse_bwd": [vp, i32, i32, vp, vp, vp, vp, vp, sz, vp],
@@ -212,6 +213,13 @@ def project(shape, csr, K, D, heads, X, gather_ids, W_rel, W_root, att, Y, R0, s
 def aggregate_fwd(csr, rows, agg, D, heads, slope, Y, s_src, s_dst, Z, stats, stream=None):
     _check("hifuse_aggregate_fwd", lib().hifuse_aggregate_fwd(
         csr.ref, rows, AGG[agg], D, heads, slope, _ptr(Y), _ptr(s_src), _ptr(s_dst), _ptr(Z),
+        _ptr(stats), _stream(stream)))
+
+
+def aggregate_fwd_xrel(shape, csr, D, heads, slope, Y, s_src, s_dst, Z, stats, stream=None):
+    """GAT with the edge-softmax across the relations of each destination."""
+    _check("hifuse_aggregate_fwd_xrel", lib().hifuse_aggregate_fwd_xrel(
+        shape.ref, csr.ref, D, heads, slope, _ptr(Y), _ptr(s_src), _ptr(s_dst), _ptr(Z),
         _ptr(stats), _stream(stream)))
 
 

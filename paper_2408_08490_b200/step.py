@@ -189,7 +189,8 @@ class Trainer:
                      s_src=self._mat(f"ss{l}", sh.U_max, H) if P["att"] is not None else None,
                      s_dst=self._mat(f"sd{l}", sh.rows, H) if P["att"] is not None else None,
                      Z=self._mat(f"Z{l}", sh.rows, D),
-                     stats=self._mat(f"st{l}", sh.rows, 2 * H) if self.agg == "gat" else None,
+                     stats=(self._mat(f"st{l}", sh.rows, 2 * H) if self.agg.startswith("gat")
+                            else None),
                      H=self._mat(f"H{l}", sh.dst_rows, D),
                      wsp=self._ws(hf.project_ws_bytes(sh, K, D, H)))
             if self.agg_first and l == 0:
@@ -210,9 +211,14 @@ class Trainer:
             ops.append((f"project.{l}", lambda sh=sh, c=csrs[l], a=a, P=P: hf.project(
                 sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"], P["att"], a["Y"],
                 a["R0"], a["s_src"], a["s_dst"], a["wsp"], prec=self.prec)))
-            ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a: hf.aggregate_fwd(
-                c, sh.rows, self.agg, D, H, self.slope, a["Y"], a["s_src"], a["s_dst"], a["Z"],
-                a["stats"])))
+            if self.agg == "gat_xrel":     # softmax across relations (NEXT(2))
+                ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a:
+                            hf.aggregate_fwd_xrel(sh, c, D, H, self.slope, a["Y"], a["s_src"],
+                                                  a["s_dst"], a["Z"], a["stats"])))
+            else:
+                ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a: hf.aggregate_fwd(
+                    c, sh.rows, self.agg, D, H, self.slope, a["Y"], a["s_src"], a["s_dst"],
+                    a["Z"], a["stats"])))
             ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
                 sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
             acts.append(a)

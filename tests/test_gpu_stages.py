@@ -326,3 +326,82 @@ def test_linear_xent(B, C):
     sw = np.abs(Hfull[row0:row0 + B]).T @ np.abs(ref["dlog"]) + 1e-30
     assert np.all(np.abs(dWc.cpu().numpy() - ref["dWc"]) <= 1e-5 * sw)
     assert np.all(np.abs(dbc.cpu().numpy() - ref["dbc"]) <= 1e-5 * np.abs(ref["dlog"]).sum(0) + 1e-12)
+
+
+# ------------------------------------- GAT, softmax across relations (NEXT(2))
+@pytest.mark.parametrize("D,H", [(128, 8), (64, 8), (128, 1), (64, 2)])
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_fwd_gat_xrel(seed, D, H):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(130 + seed, D=D, H=H, hub=0.05,
+                                                     T=[1, 2, 4][seed], R=[3, 7, 11][seed])
+    U = ch["U"]
+    Y = rng.standard_normal((U, D)).astype(np.float32)
+    ss = (rng.standard_normal((U, H)) * 2).astype(np.float32)
+    sd = (rng.standard_normal((sh.rows, H)) * 2).astype(np.float32)
+    Z = torch.full((sh.rows, D), 9.0, device=DEV)
+    stats = torch.zeros(sh.rows, 2 * H, device=DEV)
+    n0 = hf().kernel_launches()
+    hf().aggregate_fwd_xrel(sh, csr, D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
+    assert hf().kernel_launches() - n0 == 1           # one kernel for all relations
+    ref = agg_oracle(blk, et, rs, rd, ch, "gat_xrel", D, H, Y, ss, sd)
+    A = agg_oracle(blk, et, rs, rd, ch, "gat_xrel", D, H, np.abs(Y), ss, sd)["Z"]
+    close_scaled(Z.cpu().numpy(), ref["Z"], A, what="Z gat_xrel")
+    # every row of a destination carries the destination's (max, sum): equal
+    # across its rows, and the sum >= 1 wherever the destination has edges
+    st = stats.cpu().numpy()
+    gm = _gmap_index(sh, ch)
+    deg_dst = np.zeros(sh.dst_rows)
+    np.add.at(deg_dst, gm, ref["deg"])
+    for q in range(sh.R):
+        for q2 in range(q + 1, sh.R):
+            if sh.rel_dst[q] != sh.rel_dst[q2]:
+                continue
+            a, b = ch["rel_row_off"][q], ch["rel_row_off"][q2]
+            n = sh.n_dst[sh.rel_dst[q]]
+            assert np.array_equal(st[a:a + n], st[b:b + n])
+    nz = deg_dst[gm] > 0
+    assert np.all(st[nz, H:] >= 1.0 - 1e-6)
+
+
+@pytest.mark.parametrize("D,H", [(128, 8), (64, 8)])
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_bwd_gat_xrel(seed, D, H):
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(160 + seed, D=D, H=H, hub=0.1,
+                                                     N=[800, 6000, 20000][seed], T=2, R=6)
+    U = ch["U"]
+    Y = rng.standard_normal((U, D)).astype(np.float32)
+    ss = rng.standard_normal((U, H)).astype(np.float32)
+    sd = rng.standard_normal((sh.rows, H)).astype(np.float32)
+    G = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    Z = torch.zeros(sh.rows, D, device=DEV)
+    stats = torch.zeros(sh.rows, 2 * H, device=DEV)
+    hf().aggregate_fwd_xrel(sh, csr, D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
+    dY = torch.zeros(U, D, device=DEV)
+    dss = torch.zeros(U, H, device=DEV)
+    dsd = torch.zeros(sh.rows, H, device=DEV)
+    ws = torch.empty(hf().aggregate_bwd_ws_bytes(sh, "gat_xrel", H) // 4 + 16, device=DEV)
+    hf().aggregate_bwd(sh, csr, "gat_xrel", D, H, 0.2, t(G), t(Y), t(ss), t(sd), stats, dY, dss,
+                       dsd, ws)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.aggregate_bwd(osh, blk, et, ch, "gat_xrel", D, H, G, Y, ss, sd)
+    sc_y = oracle.aggregate_bwd(osh, blk, et, ch, "gat_xrel", D, H, np.abs(G), np.abs(Y), ss, sd)
+    close_scaled(dY.cpu().numpy(), ref["dY"], sc_y["dY"], rtol=2e-5, what="dY gat_xrel")
+    # ds: absolute-sum scale of the dpre = alpha (dalpha - za) terms, za over
+    # the destination's union of rows
+    fw = oracle.aggregate_fwd(osh, blk, et, ch, "gat_xrel", D, H, Y, ss, sd)
+    nv = ch["row_ptr"][-1]
+    rows = np.repeat(np.arange(sh.rows), np.diff(ch["row_ptr"]))
+    e, u = ch["eperm"][:nv], ch["col"][:nv]
+    dest = _gmap_index(sh, ch)[rows]
+    dh = D // H
+    dabs = (np.abs(G[dest]).reshape(-1, H, dh) * np.abs(Y[u]).reshape(-1, H, dh)).sum(-1)
+    a = fw["alpha"][e]
+    za = np.zeros((sh.dst_rows, H))
+    np.add.at(za, dest, a * dabs)
+    term = a * (dabs + za[dest])
+    scale_d = np.zeros((sh.rows, H))
+    np.add.at(scale_d, rows, term)
+    scale_s = np.zeros((U, H))
+    np.add.at(scale_s, u, term)
+    close_scaled(dss.cpu().numpy(), ref["ds_src"], scale_s, rtol=2e-5, what="ds_src xrel")
+    close_scaled(dsd.cpu().numpy(), ref["ds_dst"], scale_d, rtol=2e-5, what="ds_dst xrel")

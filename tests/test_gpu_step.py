@@ -18,7 +18,11 @@ _cache = {}
 
 def setup(key):
     if key not in _cache:
-        cfg = CONFIGS[key]
+        if key.endswith("_xrel"):        # RGAT with the across-relation softmax (NEXT(2))
+            import dataclasses
+            cfg = dataclasses.replace(CONFIGS[key[:-5]], agg="gat_xrel", key=key)
+        else:
+            cfg = CONFIGS[key]
         g = generate_graph(cfg)
         feat, foff = generate_features(cfg.type_counts, cfg.feat_dim)
         _cache[key] = (cfg, g, feat, foff)
@@ -33,7 +37,8 @@ def rel_l2(a, b):
 
 @pytest.mark.parametrize("prec,order", [("fp32", "project_first"), ("tf32", "project_first"),
                                         ("tf32", "agg_first")])
-@pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag"])
+@pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag", "imdb_xrel",
+                                 "freebase_xrel"])
 def test_step_matches_oracle(key, prec, order):
     """agg_first (RGCN input layer aggregates raw features, then projects) is
     checked against the same project-first oracle model: equal by linearity."""
