@@ -6,6 +6,6 @@ This package holds no arithmetic of the method: only workload shapes
 """
 from .configs import CONFIGS, CONFIG_ORDER, SEED, WorkloadConfig, RelSpec
 from .graph import HeteroGraph, generate_graph, generate_features, glorot
-from .sampler import LayerBlock, MiniBatch, sample_batch, make_batch, epoch_seeds
+from .sampler import LayerBlock, MiniBatch, sample_batch, make_batch, epoch_seeds, batch_key
 from .blocks import random_block, random_schema, block_shape_arrays
 from .params import make_params

@@ -61,6 +61,17 @@ class HeteroGraph:
     def num_types(self):
         return len(self.counts)
 
+    def in_csc(self):
+        """Per relation r: (ptr [|V_t(r)|+1] int64, src [E_r] int32 source ids
+        within type s(r), eid [E_r] int64 global edge ids), in-edges grouped by
+        destination, stable: the graph format the GPU sampler reads (format
+        conversion only)."""
+        out = []
+        for r, (ptr, order) in enumerate(self.in_lists()):
+            out.append((ptr.astype(np.int64), self.src[r][order].astype(np.int32),
+                        self.rel_edge_off[r] + order.astype(np.int64)))
+        return out
+
     @property
     def num_rels(self):
         return len(self.src)

@@ -196,3 +196,17 @@ def make_batch(cfg: WorkloadConfig, g: HeteroGraph, batch_index: int, epoch: int
     layers = sample_batch(g, cfg.target_type, seeds, cfg.fanout, rng)
     return MiniBatch(seeds=seeds, labels=labels_of(cfg, seeds, seed), layers=layers,
                      index=batch_index)
+
+
+def batch_key(epoch: int, batch: int, seed: int = SEED) -> int:
+    """64-bit stream key of batch ``batch`` of epoch ``epoch`` for the GPU
+    sampler (splitmix64 chain of (seed, epoch, batch); a
+    batch's randomness depends only on its index, not on the rank)."""
+    M = (1 << 64) - 1
+
+    def mix(z):
+        z = (z + 0x9E3779B97F4A7C15) & M
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    return mix(mix(mix(seed) ^ epoch) ^ batch)
