@@ -329,6 +329,65 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float *d_H, int64_t 
 hifuse_status hifuse_sgd(float *d_param, const float *d_grad, int64_t n, float lr, float grad_scale,
                          hifuse_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * NEXT(1): GPU neighbour sampler.  PAPER.md Fig. 2 step (1)
+ * ("mini-batches are sampled from the original graph", line 156) and SPEC.md
+ * sample_batch: each (vertex, relation) pair of a layer's
+ * destinations contributes min(deg, fanout) of its in-edges, chosen uniformly
+ * WITHOUT replacement; message-flow block convention (reading C12): per type
+ * the layer's destinations are the first n_dst of its sources, new sources
+ * follow in ascending vertex id.  Randomness: Floyd's subset algorithm driven
+ * by a counter-based splitmix64 hash of (hop key, relation, vertex, j), so a
+ * batch is a pure function of (graph, seeds, fanout, key) -- any rank, any
+ * order.  Edge order inside a block: destination (type-major,
+ * local id), then relation ascending, then in-list position ascending.
+ * Everything runs on the device; capacities are host-known (graph-capturable);
+ * the data-dependent sizes land in hifuse_block.counts.
+ * ------------------------------------------------------------------------ */
+typedef struct {                  /* in-adjacency of the whole graph, per relation */
+  int32_t num_types, num_rels;
+  const int32_t *rel_src_type_h, *rel_dst_type_h;   /* [R] host */
+  const int64_t *type_count_h;    /* [T] host: |V_t| */
+  const int64_t *in_ptr_off_h;    /* [R] host: relation r's block of d_in_ptr starts here */
+  const int64_t *d_in_ptr;        /* device [sum_r (|V_t(r)| + 1)]: for vertex v of type
+                                   * t(r), its in-edges are positions
+                                   * [d_in_ptr[off_r + v], d_in_ptr[off_r + v + 1]) of: */
+  const int32_t *d_in_src;        /* device [E]: source vertex (id within its type)    */
+  const int64_t *d_in_eid;        /* device [E]: global edge id (EdgeType index)       */
+} hifuse_graph_csc;
+
+typedef struct {                  /* one sampled layer block (device, caller-allocated) */
+  int32_t *src_local, *dst_local; /* [edge_cap] */
+  int64_t *edge_id;               /* [edge_cap] */
+  int32_t *src_gid;               /* [src_cap] type-major source vertices (ids within type);
+                                   * the first n_dst(t) of type t are the destinations */
+  int32_t *counts;                /* [2T + 1]: n_src[T], n_dst[T], N */
+  int32_t *gather_ids;            /* [src_cap] or NULL: type_off(t) + src_gid, type_off =
+                                   * prefix of type_count_h (type-major feature store) */
+} hifuse_block;
+
+/* Host-only: per layer (outer first) the edge / source capacities the caller
+ * allocates, the workspace bytes, and the sampler state ints (2 sum_t |V_t|,
+ * zeroed once by the caller before the first call). */
+hifuse_status hifuse_sample_caps(const hifuse_graph_csc *g, int num_layers,
+                                 const int32_t *fanout_h /* [L], outer layer first */,
+                                 int64_t num_seeds, int64_t *edge_cap_h /* [L] */,
+                                 int64_t *src_cap_h /* [L] */, size_t *ws_bytes,
+                                 int64_t *state_ints);
+/* Samples num_layers blocks around d_seeds (ids within target_type) into
+ * out[L] (outer layer first).  key: 64-bit stream key of this batch (e.g. a
+ * splitmix64 of (seed, epoch, batch)); hop h uses mix(key ^ (0x1000 + h)).
+ * d_state: sampler state (see caps), stamps [stamp, stamp + L) must not have
+ * been used since it was zeroed (stamp >= 1).  d_status: HIFUSE_ST_BAD_DST is
+ * ORed for a seed out of range (it is dropped).  Errors: INVALID_ARG (null
+ * pointers, fanout < 1 or > 64, target_type out of range), WORKSPACE. */
+hifuse_status hifuse_sample_blocks(const hifuse_graph_csc *g, int num_layers,
+                                   const int32_t *fanout_h, const int32_t *d_seeds,
+                                   int64_t num_seeds, int32_t target_type, uint64_t key,
+                                   int32_t stamp, hifuse_block *out, int32_t *d_state,
+                                   void *d_ws, size_t ws_bytes, int32_t *d_status,
+                                   hifuse_stream_t stream);
+
 /* Tests / debugging: copies *d_status to *out_h and synchronises `stream`. */
 hifuse_status hifuse_read_status(const int32_t *d_status, hifuse_stream_t stream, int32_t *out_h);
 const char *hifuse_status_string(hifuse_status s);

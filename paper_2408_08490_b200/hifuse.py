@@ -43,6 +43,19 @@ class Csr(ctypes.Structure):
                  "csc_pos", "csc_row", "slot_y", "U_dev")]
 
 
+class GraphCsc(ctypes.Structure):
+    _fields_ = [("num_types", ctypes.c_int32), ("num_rels", ctypes.c_int32),
+                ("rel_src_type_h", ctypes.c_void_p), ("rel_dst_type_h", ctypes.c_void_p),
+                ("type_count_h", ctypes.c_void_p), ("in_ptr_off_h", ctypes.c_void_p),
+                ("d_in_ptr", ctypes.c_void_p), ("d_in_src", ctypes.c_void_p),
+                ("d_in_eid", ctypes.c_void_p)]
+
+
+class Block(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("src_local", "dst_local", "edge_id", "src_gid", "counts", "gather_ids")]
+
+
 _lib = None
 
 
@@ -85,6 +98,9 @@ def lib():
             "hifuse_linear_xent": [i32, i32, i32, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp,
                                    sz, vp],
             "hifuse_sgd": [vp, vp, i64, f32, f32, vp],
+            "hifuse_sample_caps": [vp, i32, vp, i64, vp, vp, vp, vp],
+            "hifuse_sample_blocks": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, i32, vp, vp, vp,
+                                     sz, vp, vp],
             "hifuse_read_status": [vp, vp, vp],
             "hifuse_kernel_launches": [],
         }
@@ -307,6 +323,30 @@ def linear_xent(B, D, C, H, h_row0, labels, Wc, bc, loss, dH, dWc, dbc, ws, stre
 def sgd(param, grad, lr, grad_scale=1.0, stream=None):
     _check("hifuse_sgd", lib().hifuse_sgd(_ptr(param), _ptr(grad), param.numel(), lr, grad_scale,
                                           _stream(stream)))
+
+
+def sample_caps(graph, fanout, num_seeds):
+    """(edge_cap[L], src_cap[L], ws_bytes, state_ints) of hifuse_sample_caps."""
+    L = len(fanout)
+    fan = np.ascontiguousarray(fanout, np.int32)
+    ec = np.zeros(L, np.int64)
+    sc = np.zeros(L, np.int64)
+    ws = ctypes.c_size_t()
+    stn = ctypes.c_int64()
+    _check("hifuse_sample_caps", lib().hifuse_sample_caps(
+        ctypes.byref(graph), L, fan.ctypes.data, int(num_seeds), ec.ctypes.data, sc.ctypes.data,
+        ctypes.byref(ws), ctypes.byref(stn)))
+    return ec, sc, ws.value, stn.value
+
+
+def sample_blocks(graph, fanout, seeds, target_type, key, stamp, blocks, state, ws, status,
+                  stream=None):
+    fan = np.ascontiguousarray(fanout, np.int32)
+    arr = (Block * len(blocks))(*blocks)
+    _check("hifuse_sample_blocks", lib().hifuse_sample_blocks(
+        ctypes.byref(graph), len(fan), fan.ctypes.data, _ptr(seeds), seeds.numel(), target_type,
+        ctypes.c_uint64(key), stamp, arr, _ptr(state), _ptr(ws), ws.numel() * ws.element_size(),
+        _ptr(status), _stream(stream)))
 
 
 def read_status(status, stream=None):
