@@ -260,6 +260,9 @@ def main():
     ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gpu-sampler", type=int, default=1,
+                    help="1: also run the training loop fed by the GPU neighbour sampler "
+                         "(NEXT(1)) and report it under gpu_sampler")
     ap.add_argument("--compare", type=int, default=1,
                     help="1: add the merged-vs-unmerged comparison arms (kernels per layer, "
                          "per-relation launches, torch per-relation ops, cuSPARSE)")
@@ -549,6 +552,11 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+    gsmp = None
+    if args.gpu_sampler and world == 1:
+        gsmp = gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev,
+                               min(args.steps, 200), max(args.warmup, 3), args.lr, args.prec,
+                               args.order)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, g, feat, foff, params, rs, rd, mbs)
@@ -572,11 +580,129 @@ def main():
         "serial_ms_per_step": ms_serial / args.steps,
         "other_order": other,
         "merged_vs_unmerged": unmerged,
+        "gpu_sampler": gsmp,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr, prec, order):
+    """NEXT(1): the GPU neighbour sampler (hifuse_sample_blocks) inside the
+    training loop.  Batch i+1 is sampled on a side stream while batch i
+    computes (the paper's Fig. 6 overlap with the sampler on the GPU too);
+    per step the host copies only the seeds and labels (pinned) and reads the
+    7-int per-layer counts; the step itself runs eagerly (its shapes change
+    every batch).  Also: the sampler's device time per batch (CUDA-graph
+    replay) and the host numpy sampler's rate for comparison."""
+    import torch
+    from paper_2408_08490_b200.sampler import GpuSampler, SampledBatch
+    from paper_2408_08490_b200.step import Trainer
+    from synth import epoch_seeds, batch_key
+    from synth.sampler import labels_of
+    B = cfg.batch_size
+    fan = list(cfg.fanout)[::-1]
+    smp = GpuSampler(g.rel_src, g.rel_dst, g.counts, g.in_csc(), fan, B, dev, nbuf=2)
+    perm = epoch_seeds(cfg, 0)
+    nb = len(perm) // B
+    host_seeds = [torch.from_numpy(perm[b * B:(b + 1) * B].astype(np.int32)).pin_memory()
+                  for b in range(nb)]
+    host_labels = [torch.from_numpy(labels_of(cfg, perm[b * B:(b + 1) * B])).pin_memory()
+                   for b in range(nb)]
+    seeds_d = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(2)]
+    labels_d = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(2)]
+    cnt_h = [torch.empty(len(fan) * (2 * cfg.num_types + 1), dtype=torch.int32).pin_memory()
+             for _ in range(2)]
+    # sampler alone: device time per batch (graph replay, fixed seeds)
+    seeds_d[0].copy_(host_seeds[0])
+    smp.sample(seeds_d[0], cfg.target_type, batch_key(0, 0), buf=0)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        smp.sample(seeds_d[0], cfg.target_type, batch_key(0, 0), buf=0)
+    gr.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(20):
+        gr.replay()
+    b.record()
+    b.synchronize()
+    smp_us = a.elapsed_time(b) / 20 * 1e3
+    del gr
+    smp.state.zero_()
+    smp.stamp = 1
+    tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
+                 cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=lr, prec=prec,
+                 order=order)
+    tr.load_params(params)
+    tr.prepare_graph(et_d)
+    side = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    ev_s = [torch.cuda.Event() for _ in range(2)]
+    ev_c = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_c:
+        e.record(main)
+    T = cfg.num_types
+
+    def launch_sample(i):
+        k = i % 2
+        with torch.cuda.stream(side):
+            side.wait_event(ev_c[k])
+            seeds_d[k].copy_(host_seeds[i % nb], non_blocking=True)
+            labels_d[k].copy_(host_labels[i % nb], non_blocking=True)
+            smp.sample(seeds_d[k], cfg.target_type, batch_key(i // nb, i % nb), side, buf=k)
+            for l, o in enumerate(smp.bufs[k][0]):
+                cnt_h[k][l * (2 * T + 1):(l + 1) * (2 * T + 1)].copy_(o["counts"],
+                                                                        non_blocking=True)
+            ev_s[k].record(side)
+
+    def run(n, start):
+        launch_sample(start)
+        launch_sample(start + 1)
+        for i in range(start, start + n):
+            k = i % 2
+            ev_s[k].synchronize()
+            c = cnt_h[k].numpy().reshape(len(fan), 2 * T + 1)
+            sb = SampledBatch(smp, list(c), labels_d[k], cfg.target_type, buf=k)
+            main.wait_event(ev_s[k])
+            tr.step(sb, feat_d, et_d)
+            ev_c[k].record(main)
+            if i + 2 < start + n:
+                launch_sample(i + 2)
+        torch.cuda.synchronize()
+
+    run(warmup, 0)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a.record()
+    run(steps, warmup + 2)
+    b.record()
+    b.synchronize()
+    wall = time.perf_counter() - t0
+    ms = a.elapsed_time(b)
+    assert hf_status_ok(smp.status) and hf_status_ok(tr.status)
+    # host numpy sampler (synth/sampler.py) for comparison
+    t0 = time.perf_counter()
+    for bi in range(2):
+        make_batch(cfg, g, bi)
+    host_rate = 2 / (time.perf_counter() - t0)
+    return {"value": steps / (ms / 1e3), "unit": "mini-batches/s",
+            "wall_mini_batches_per_s": steps / wall,
+            "sampler_us_per_batch": round(smp_us, 2),
+            "sampler_batches_per_s": 1e6 / smp_us,
+            "host_numpy_sampler_batches_per_s": host_rate,
+            "h2d_bytes_per_step": 8 * B,
+            "d2h_bytes_per_step": 4 * len(fan) * (2 * T + 1),
+            "launch_mode": "eager step (shapes change per batch), next batch sampled on a side "
+                           "stream; one counts read per batch",
+            "steps": steps}
+
+
+def hf_status_ok(st):
+    from paper_2408_08490_b200 import hifuse as hf
+    return hf.read_status(st) == 0
 
 
 def cpu_baseline(cfg, g, feat, foff, params, rs, rd, mbs):

@@ -16,9 +16,10 @@ from . import hifuse as hf
 
 class GpuSampler:
     def __init__(self, rel_src, rel_dst, type_counts, in_csc, fanout, batch_size, device,
-                 gather=True):
+                 gather=True, nbuf=1):
         """in_csc[r] = (ptr [|V_t(r)|+1], src [E_r] ids within type s(r), eid [E_r]
-        global edge ids); fanout per layer, outer first."""
+        global edge ids); fanout per layer, outer first.  nbuf output buffer
+        sets (2: sample batch i+1 while batch i computes)."""
         hf.lib()
         self.rel_src = np.ascontiguousarray(rel_src, np.int32)
         self.rel_dst = np.ascontiguousarray(rel_dst, np.int32)
@@ -48,28 +49,32 @@ class GpuSampler:
         ec, sc, wsb, stn = hf.sample_caps(self.g, self.fanout, self.B)
         self.edge_cap, self.src_cap = ec, sc
         i32 = lambda n: torch.empty(int(n), dtype=torch.int32, device=device)
-        self.out = []
-        for l in range(self.L):
-            o = dict(src=i32(ec[l]), dst=i32(ec[l]),
-                     eid=torch.empty(int(ec[l]), dtype=torch.int64, device=device),
-                     gid=i32(sc[l]), counts=i32(2 * self.T + 1),
-                     gather=i32(sc[l]) if (gather and l == 0) else None)
-            self.out.append(o)
-        self.blocks = [hf.Block(o["src"].data_ptr(), o["dst"].data_ptr(), o["eid"].data_ptr(),
-                                o["gid"].data_ptr(), o["counts"].data_ptr(),
-                                o["gather"].data_ptr() if o["gather"] is not None else None)
-                       for o in self.out]
+        self.bufs = []
+        for _ in range(nbuf):
+            outs = []
+            for l in range(self.L):
+                outs.append(dict(src=i32(ec[l]), dst=i32(ec[l]),
+                                 eid=torch.empty(int(ec[l]), dtype=torch.int64, device=device),
+                                 gid=i32(sc[l]), counts=i32(2 * self.T + 1),
+                                 gather=i32(sc[l]) if (gather and l == 0) else None))
+            blocks = [hf.Block(o["src"].data_ptr(), o["dst"].data_ptr(), o["eid"].data_ptr(),
+                               o["gid"].data_ptr(), o["counts"].data_ptr(),
+                               o["gather"].data_ptr() if o["gather"] is not None else None)
+                      for o in outs]
+            self.bufs.append((outs, blocks))
+        self.out, self.blocks = self.bufs[0]
         self.ws = torch.empty((wsb + 3) // 4 + 64, dtype=torch.int32, device=device)
         self.state = torch.zeros(int(stn), dtype=torch.int32, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.stamp = 1
 
-    def sample(self, seeds, target_type, key, stream=None):
+    def sample(self, seeds, target_type, key, stream=None, buf=0):
         """Samples the blocks of ``seeds`` (device int32, ids within the
-        target type) into this sampler's output buffers (overwritten by the
-        next call)."""
+        target type) into output buffer set ``buf`` (self.out then points at
+        it; overwritten by the next call on the same set)."""
         if seeds.numel() > self.B:
             raise ValueError("more seeds than the sampler's capacity")
+        self.out, self.blocks = self.bufs[buf]
         hf.sample_blocks(self.g, self.fanout, seeds, target_type, key, self.stamp, self.blocks,
                          self.state, self.ws, self.status, stream)
         self.stamp += self.L
@@ -77,27 +82,29 @@ class GpuSampler:
             self.state.zero_()
             self.stamp = 1
 
-    def counts(self):
+    def counts(self, buf=None):
         """Host copy of every layer's [n_src[T], n_dst[T], N] (synchronises)."""
-        return [o["counts"].cpu().numpy() for o in self.out]
+        outs = self.out if buf is None else self.bufs[buf][0]
+        return [o["counts"].cpu().numpy() for o in outs]
 
 
 class SampledBatch:
     """DeviceBatch-compatible view of the sampler's current output (valid
     until the sampler's next call)."""
 
-    def __init__(self, smp: GpuSampler, counts, labels_dev, target_type, slot=0):
+    def __init__(self, smp: GpuSampler, counts, labels_dev, target_type, slot=0, buf=None):
         T = smp.T
+        outs = smp.out if buf is None else smp.bufs[buf][0]
         self.shapes = []
         self.dev = dict(src=[], dst=[], eid=[])
         for l, c in enumerate(counts):
             n_src, n_dst, N = c[:T], c[T:2 * T], int(c[2 * T])
             self.shapes.append(hf.Shape(smp.rel_src, smp.rel_dst, n_src, n_dst, N))
-            o = smp.out[l]
+            o = outs[l]
             self.dev["src"].append(o["src"][:max(N, 1)])
             self.dev["dst"].append(o["dst"][:max(N, 1)])
             self.dev["eid"].append(o["eid"][:max(N, 1)])
-        self.dev["gid"] = smp.out[0]["gather"][:max(int(counts[0][:T].sum()), 1)]
+        self.dev["gid"] = outs[0]["gather"][:max(int(counts[0][:T].sum()), 1)]
         self.dev["labels"] = labels_dev
         self.B = int(labels_dev.numel())
         self.slot = slot
