@@ -1,0 +1,19 @@
+"""One GPU-sampler call per batch for a few mag batches (ncu target)."""
+import os
+import sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from synth import CONFIGS, generate_graph, epoch_seeds, batch_key  # noqa: E402
+from paper_2408_08490_b200.sampler import GpuSampler  # noqa: E402
+
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "mag"]
+g = generate_graph(cfg)
+smp = GpuSampler(g.rel_src, g.rel_dst, g.counts, g.in_csc(), list(cfg.fanout)[::-1],
+                 cfg.batch_size, "cuda:0")
+perm = epoch_seeds(cfg, 0)
+for b in range(3):
+    s = torch.from_numpy(perm[b * cfg.batch_size:(b + 1) * cfg.batch_size].astype(np.int32))
+    smp.sample(s.cuda(), cfg.target_type, batch_key(0, b))
+torch.cuda.synchronize()
+print([c.tolist() for c in smp.counts()])
