@@ -644,6 +644,21 @@ def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr
     for e in ev_c:
         e.record(main)
     T = cfg.num_types
+    # one CUDA graph of the sampler per output buffer; key and stamp are read
+    # from device memory (d_ctl), so the same graph serves every batch
+    ctl_h = [torch.zeros(2, dtype=torch.int64).pin_memory() for _ in range(2)]
+    ctl_d = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(2)]
+    sgraphs = []
+    with torch.cuda.stream(side):
+        for k in range(2):
+            ctl_d[k].copy_(torch.tensor([1, smp.next_stamp()], dtype=torch.int64))
+            smp.sample(seeds_d[k], cfg.target_type, 0, side, buf=k, d_ctl=ctl_d[k])
+            side.synchronize()
+            gk = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gk, stream=side):
+                smp.sample(seeds_d[k], cfg.target_type, 0, side, buf=k, d_ctl=ctl_d[k])
+            sgraphs.append(gk)
+    torch.cuda.synchronize()
 
     def launch_sample(i):
         k = i % 2
@@ -651,7 +666,11 @@ def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr
             side.wait_event(ev_c[k])
             seeds_d[k].copy_(host_seeds[i % nb], non_blocking=True)
             labels_d[k].copy_(host_labels[i % nb], non_blocking=True)
-            smp.sample(seeds_d[k], cfg.target_type, batch_key(i // nb, i % nb), side, buf=k)
+            key = batch_key(i // nb, i % nb)
+            ctl_h[k][0] = key - (1 << 64) if key >= (1 << 63) else key
+            ctl_h[k][1] = smp.next_stamp()
+            ctl_d[k].copy_(ctl_h[k], non_blocking=True)
+            sgraphs[k].replay()
             for l, o in enumerate(smp.bufs[k][0]):
                 cnt_h[k][l * (2 * T + 1):(l + 1) * (2 * T + 1)].copy_(o["counts"],
                                                                         non_blocking=True)
@@ -695,8 +714,9 @@ def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr
             "host_numpy_sampler_batches_per_s": host_rate,
             "h2d_bytes_per_step": 8 * B,
             "d2h_bytes_per_step": 4 * len(fan) * (2 * T + 1),
-            "launch_mode": "eager step (shapes change per batch), next batch sampled on a side "
-                           "stream; one counts read per batch",
+            "launch_mode": "eager step (shapes change per batch); next batch sampled on a side "
+                           "stream by a CUDA-graph replay of the sampler (key/stamp in device "
+                           "memory); one counts read per batch",
             "steps": steps}
 
 

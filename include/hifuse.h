@@ -377,6 +377,9 @@ hifuse_status hifuse_sample_caps(const hifuse_graph_csc *g, int num_layers,
 /* Samples num_layers blocks around d_seeds (ids within target_type) into
  * out[L] (outer layer first).  key: 64-bit stream key of this batch (e.g. a
  * splitmix64 of (seed, epoch, batch)); hop h uses mix(key ^ (0x1000 + h)).
+ * d_ctl: NULL, or device uint64 [2] = {key, stamp}: key and stamp are then
+ * read from device memory instead of the arguments, so one captured CUDA graph
+ * of the sampler serves every batch (write the next {key, stamp}, replay).
  * d_state: sampler state (see caps), stamps [stamp, stamp + L) must not have
  * been used since it was zeroed (stamp >= 1).  d_status: HIFUSE_ST_BAD_DST is
  * ORed for a seed out of range (it is dropped).  Errors: INVALID_ARG (null
@@ -384,7 +387,8 @@ hifuse_status hifuse_sample_caps(const hifuse_graph_csc *g, int num_layers,
 hifuse_status hifuse_sample_blocks(const hifuse_graph_csc *g, int num_layers,
                                    const int32_t *fanout_h, const int32_t *d_seeds,
                                    int64_t num_seeds, int32_t target_type, uint64_t key,
-                                   int32_t stamp, hifuse_block *out, int32_t *d_state,
+                                   const uint64_t *d_ctl, int32_t stamp, hifuse_block *out,
+                                   int32_t *d_state,
                                    void *d_ws, size_t ws_bytes, int32_t *d_status,
                                    hifuse_stream_t stream);
 

@@ -61,10 +61,12 @@ __global__ void k_smp_init(int T, int target, int B, int* __restrict__ fo) {
 
 __global__ void __launch_bounds__(256)
 k_smp_mark_dst(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ front,
-               int* __restrict__ gen, int* __restrict__ loc, int stamp, int* __restrict__ status) {
+               int* __restrict__ gen, int* __restrict__ loc, int stamp,
+               const unsigned long long* __restrict__ d_ctl, int hop, int* __restrict__ status) {
   __shared__ int fo[HF_MAX_T + 1];
   for (int i = threadIdx.x; i <= m.T; i += blockDim.x) fo[i] = fo_d[i];
   __syncthreads();
+  if (d_ctl) stamp = (int)d_ctl[1] + hop;
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= fo[m.T]) return;
   const int t = type_of(fo, m.T, d);
@@ -80,7 +82,8 @@ k_smp_mark_dst(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ 
 
 __global__ void __launch_bounds__(128)
 k_smp_pairs(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ front, int P, int f,
-            unsigned long long hk, const long long* __restrict__ in_ptr,
+            unsigned long long hk, const unsigned long long* __restrict__ d_ctl, int hop,
+            const long long* __restrict__ in_ptr,
             const int* __restrict__ in_src, const long long* __restrict__ in_eid,
             int* __restrict__ gen, unsigned* __restrict__ bitmap, int stamp,
             int* __restrict__ slot_src, long long* __restrict__ slot_eid,
@@ -88,6 +91,10 @@ k_smp_pairs(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ fro
   __shared__ int fo[HF_MAX_T + 1];
   for (int i = threadIdx.x; i <= m.T; i += blockDim.x) fo[i] = fo_d[i];
   __syncthreads();
+  if (d_ctl) {                       // key and stamp base from device memory
+    hk = mix64(d_ctl[0] ^ (0x1000ull + (unsigned long long)hop));
+    stamp = (int)d_ctl[1] + hop;
+  }
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const int d = p / m.Rmax, q = p % m.Rmax;
@@ -315,7 +322,8 @@ hifuse_status hifuse_sample_caps(const hifuse_graph_csc* g, int num_layers, cons
 hifuse_status hifuse_sample_blocks(const hifuse_graph_csc* g, int num_layers,
                                    const int32_t* fanout_h, const int32_t* d_seeds,
                                    int64_t num_seeds, int32_t target_type, uint64_t key,
-                                   int32_t stamp, hifuse_block* out, int32_t* d_state,
+                                   const uint64_t* d_ctl, int32_t stamp, hifuse_block* out,
+                                   int32_t* d_state,
                                    void* d_ws, size_t ws_bytes, int32_t* d_status,
                                    hifuse_stream_t stream) {
   SmpPlan pl;
@@ -384,9 +392,10 @@ hifuse_status hifuse_sample_blocks(const hifuse_graph_csc* g, int num_layers,
     hifuse_block& o = out[l];
     const long long D = pl.D[h], P = pl.P[h];
     cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * std::max(pl.W, 1), s);
-    HF_LAUNCH(k_smp_mark_dst, ceil_div(D, 256), 256, 0, s, m, fo, front, gen, loc, stp, d_status);
+    HF_LAUNCH(k_smp_mark_dst, ceil_div(D, 256), 256, 0, s, m, fo, front, gen, loc, stp,
+              (const unsigned long long*)d_ctl, h, d_status);
     HF_LAUNCH(k_smp_pairs, ceil_div(P, 128), 128, 0, s, m, fo, front, (int)P, f, hk,
-              (const long long*)g->d_in_ptr, g->d_in_src, (const long long*)g->d_in_eid, gen,
+              (const unsigned long long*)d_ctl, h, (const long long*)g->d_in_ptr, g->d_in_src, (const long long*)g->d_in_eid, gen,
               bitmap, stp, slot_src, slot_eid, pair_cnt);
     HF_LAUNCH(k_smp_popc, ceil_div(pl.W, 256), 256, 0, s, bitmap, pl.W, wcnt);
     exclusive_scan(wcnt, wscan, pl.W, wscan_ws, s);

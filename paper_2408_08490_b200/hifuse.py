@@ -99,8 +99,8 @@ def lib():
                                    sz, vp],
             "hifuse_sgd": [vp, vp, i64, f32, f32, vp],
             "hifuse_sample_caps": [vp, i32, vp, i64, vp, vp, vp, vp],
-            "hifuse_sample_blocks": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, i32, vp, vp, vp,
-                                     sz, vp, vp],
+            "hifuse_sample_blocks": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, vp, i32, vp, vp,
+                                     vp, sz, vp, vp],
             "hifuse_read_status": [vp, vp, vp],
             "hifuse_kernel_launches": [],
         }
@@ -131,9 +131,13 @@ def _check(fn, rc):
 
 
 def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    # the current stream of the current device, through torch's C accessors
+    # (torch.cuda.current_stream() costs ~10 us of Python per call, which
+    # dominated eager steps)
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 class Shape:
@@ -340,12 +344,12 @@ def sample_caps(graph, fanout, num_seeds):
 
 
 def sample_blocks(graph, fanout, seeds, target_type, key, stamp, blocks, state, ws, status,
-                  stream=None):
+                  stream=None, d_ctl=None):
     fan = np.ascontiguousarray(fanout, np.int32)
     arr = (Block * len(blocks))(*blocks)
     _check("hifuse_sample_blocks", lib().hifuse_sample_blocks(
         ctypes.byref(graph), len(fan), fan.ctypes.data, _ptr(seeds), seeds.numel(), target_type,
-        ctypes.c_uint64(key), stamp, arr, _ptr(state), _ptr(ws), ws.numel() * ws.element_size(),
+        ctypes.c_uint64(key), _ptr(d_ctl), stamp, arr, _ptr(state), _ptr(ws), ws.numel() * ws.element_size(),
         _ptr(status), _stream(stream)))
 
 

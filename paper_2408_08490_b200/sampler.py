@@ -68,19 +68,33 @@ class GpuSampler:
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.stamp = 1
 
-    def sample(self, seeds, target_type, key, stream=None, buf=0):
+    def sample(self, seeds, target_type, key, stream=None, buf=0, d_ctl=None):
         """Samples the blocks of ``seeds`` (device int32, ids within the
         target type) into output buffer set ``buf`` (self.out then points at
-        it; overwritten by the next call on the same set)."""
+        it; overwritten by the next call on the same set).  d_ctl: device
+        uint64 [2] {key, stamp} read by the kernels instead (graph replays;
+        the caller then advances the stamp with next_stamp())."""
         if seeds.numel() > self.B:
             raise ValueError("more seeds than the sampler's capacity")
         self.out, self.blocks = self.bufs[buf]
         hf.sample_blocks(self.g, self.fanout, seeds, target_type, key, self.stamp, self.blocks,
-                         self.state, self.ws, self.status, stream)
-        self.stamp += self.L
+                         self.state, self.ws, self.status, stream, d_ctl=d_ctl)
+        if d_ctl is None:
+            self.stamp += self.L
         if self.stamp > (1 << 30):          # stamps exhausted: reset the state
             self.state.zero_()
             self.stamp = 1
+
+    def next_stamp(self):
+        """Stamp base for the next d_ctl-driven call (resets the state when the
+        stamps run out; stream-ordered with the calls)."""
+        st = self.stamp
+        self.stamp += self.L
+        if self.stamp > (1 << 30):
+            self.state.zero_()
+            self.stamp = 1
+            st, self.stamp = 1, 1 + self.L
+        return st
 
     def counts(self, buf=None):
         """Host copy of every layer's [n_src[T], n_dst[T], N] (synchronises)."""

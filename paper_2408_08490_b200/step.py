@@ -95,6 +95,7 @@ class Trainer:
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
         self._bufs = {}
+        self._views = {}
         self.heads = H if model == "rgat" else 1
         # "agg_first": the RGCN input layer aggregates raw features and then
         # projects the aggregated rows (exact by linearity; SURVEY §8(f)
@@ -122,7 +123,13 @@ class Trainer:
         return t
 
     def _mat(self, key, rows, cols):
-        return self._buf(key, max(rows, 1) * cols)[:max(rows, 1) * cols].view(max(rows, 1), cols)
+        buf = self._buf(key, max(rows, 1) * cols)
+        vk = (key, rows, cols)
+        v = self._views.get(vk)
+        if v is None or v[0] is not buf:          # cached view (eager steps re-plan)
+            v = (buf, buf[:max(rows, 1) * cols].view(max(rows, 1), cols))
+            self._views[vk] = v
+        return v[1]
 
     def _csr(self, l, shape, slot=0):
         key = f"csr{slot}.{l}"
