@@ -175,26 +175,53 @@ __global__ void k_scores_src(int R, int D, int H, const int* __restrict__ U_dev,
   }
 }
 
-// s_dst[(r,i),h] = <X_{t(r)}[i], v[r][:,h]>: thread (row, h), H threads per
-// merged row share the row's X loads (broadcast); v[r] is [K][H] (coalesced).
+// s_dst[(r,i),h] = <X_{t(r)}[i], v[r][:,h]>: one warp per merged row; the
+// 32 lanes are (head h, K-chunk c) pairs, 32/H lanes per head, so each load
+// instruction touches only 32/H X segments and 32/H contiguous v rows
+// (v[r] is [K][H]); the chunk partials of a head meet by xor shuffles.
+// (Thread-per-(row, head) with a serial 128-long K loop was latency-bound
+// and, on its side branch, longer than the projection itself.)
+template <int K, int HMAX>
 __global__ void __launch_bounds__(256)
-k_scores_dst(ProjMeta pm, int K, int H, const int* __restrict__ gather_ids,
+k_scores_dst(ProjMeta pm, int H, const int* __restrict__ gather_ids,
              const float* __restrict__ X, const float* __restrict__ v,
              float* __restrict__ s_dst) {
-  const int rpb = blockDim.x / H;
-  const int row = blockIdx.x * rpb + threadIdx.x / H, h = threadIdx.x % H;
-  if (row >= pm.rows || threadIdx.x >= rpb * H) return;
+  (void)HMAX;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= pm.rows) return;
+  const int lph = 32 / H;                    // lanes per head (H divides 32)
+  const int h = lane / lph, c = lane % lph;
+  const int kc = K / lph;                    // features per lane
   const int r = upper_bound_i(pm.rel_row_off, pm.R + 1, row) - 1;
   const int t = pm.rel_dst[r];
   const int x = pm.type_src_off[t] + (row - pm.rel_row_off[r]);
   const long long xr = gather_ids ? (long long)gather_ids[x] : (long long)x;
-  const float* xp = X + xr * K;
-  const float* vp = v + (long long)r * K * H + h;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int k = 0; k < K; k += 4)
-#pragma unroll
-    for (int q = 0; q < 4; q++) acc[q] = fmaf(__ldg(xp + k + q), __ldg(vp + (long long)(k + q) * H), acc[q]);
-  s_dst[(long long)row * H + h] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  const float* xp = X + xr * K + c * kc;
+  const float* vp = v + ((long long)r * K + c * kc) * H + h;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  int k = 0;
+  for (; k + 4 <= kc; k += 4) {
+    a0 = fmaf(__ldg(xp + k), __ldg(vp + (k) * H), a0);
+    a1 = fmaf(__ldg(xp + k + 1), __ldg(vp + (k + 1) * H), a1);
+    a2 = fmaf(__ldg(xp + k + 2), __ldg(vp + (k + 2) * H), a2);
+    a3 = fmaf(__ldg(xp + k + 3), __ldg(vp + (k + 3) * H), a3);
+  }
+  for (; k < kc; k++) a0 = fmaf(__ldg(xp + k), __ldg(vp + k * H), a0);
+  float p = (a0 + a1) + (a2 + a3);
+  for (int o = lph >> 1; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+  if (c == 0) s_dst[(long long)row * H + h] = p;
+}
+
+static void launch_scores_dst(const ProjMeta& pm, int rows, int K, int H,
+                              const int* gather_ids, const float* X, const float* v,
+                              float* s_dst, cudaStream_t s) {
+  const unsigned grid = ceil_div(rows, 8);
+#define HF_SD(KK, HH) \
+  HF_LAUNCH((k_scores_dst<KK, HH>), grid, 256, 0, s, pm, H, gather_ids, X, v, s_dst)
+  if (K == 128) HF_SD(128, 1);
+  else HF_SD(64, 1);
+#undef HF_SD
 }
 
 // ------------------------------------------------------------- backward ----
@@ -696,8 +723,7 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
     cudaStream_t sd = sbr ? bs.side : s;
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * heads, 256), 256, 0, sd, m.R, K, D, heads,
               d_W_rel, d_att, v);
-    HF_LAUNCH(k_scores_dst, ceil_div(m.rows, 256 / heads), 256, 0, sd, pm, K, heads, d_gather_ids,
-              d_X, v, d_s_dst);
+    launch_scores_dst(pm, m.rows, K, heads, d_gather_ids, d_X, v, d_s_dst, sd);
   }
   if (prec == HIFUSE_PREC_TF32) {
     rc = project_tcp_launch(m, pm, K, D, csr->rel_y_off, csr->y_src, d_X, nullptr, d_gather_ids,
@@ -724,8 +750,7 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
     long long U_max = m.N < m.S ? m.N : m.S;
     HF_LAUNCH(k_scores_src, ceil_div(U_max, 8), 256, 0, s, m.R, D, heads, csr->U_dev,
               csr->rel_y_off, d_Y, d_att, d_s_src);
-    HF_LAUNCH(k_scores_dst, ceil_div(m.rows, 256 / heads), 256, 0, s, pm, K, heads, d_gather_ids,
-              d_X, v, d_s_dst);
+    launch_scores_dst(pm, m.rows, K, heads, d_gather_ids, d_X, v, d_s_dst, s);
   }
   return last_cuda();
 }
