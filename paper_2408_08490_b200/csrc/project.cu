@@ -852,17 +852,27 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   bool abr = false;
   float* dvb = v + (long long)m.R * K * H;     // dv [R][H][K] after v in the workspace
   if (d_att) {
+    // two parallel chains: (a) destination side: partials of ds_dst x X ->
+    // dv; (b) source side: the fold v = W a_dst (for k_dx_sdst) and the
+    // partials of ds_src x Y; (a) then waits for (b) and forms datt.
     abr = branch_begin(s, &ba, 1);
     cudaStream_t sa = abr ? ba.side : s;
-    HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, sa, m.R, K, D, H, d_W_rel,
+    Branch bb;
+    const bool bbr = abr && branch_begin(s, &bb, 3);
+    cudaStream_t sb = bbr ? bb.side : sa;
+    HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, sb, m.R, K, D, H, d_W_rel,
               d_att, v);
     const unsigned gs = (unsigned)(U_max / kCHA + m.R + 1);
     const unsigned gdst = (unsigned)(m.rows / kCHA + m.R + 1);
-    HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, sa, m.R, H, D, 0, (const int*)nullptr,
+    HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, sb, m.R, H, D, 0, (const int*)nullptr,
               csr->rel_y_off, d_ds_src, d_Y, pm, d_gather_ids, Psrc);
     HF_LAUNCH(k_att_partial, gdst, H * K / 4, 0, sa, m.R, H, K, 1, (const int*)nullptr,
               (const int*)nullptr, d_ds_dst, d_X, pm, d_gather_ids, Pdst);
     HF_LAUNCH(k_att_dv, ceil_div((long long)m.R * H * K, 256), 256, 0, sa, m.R, K, H, pm, Pdst, dvb);
+    if (bbr) {                          // (a) waits for (b)
+      cudaEventRecord(bb.join, bb.side);
+      cudaStreamWaitEvent(sa, bb.join, 0);
+    }
     HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, sa, m.R, K, D, H, csr->rel_y_off,
               Psrc, dvb, d_W_rel, d_datt);
   }
