@@ -561,7 +561,35 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
   for (int base = b; base < e; base += 32) {
     const int n = min(32, e - base);
     const int my_col = lane < n ? __ldg(col + base + lane) : 0;
-    for (int k = 0; k < n; k += NS) {
+    int k0 = 0;
+    for (; k0 + NS * kUnroll <= n; k0 += NS * kUnroll) {
+      // kUnroll edges per stream: loads first, then the dependent math
+      float4 yv[kUnroll];
+      float sv[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        const int idx = k0 + u * NS + sid;
+        const int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+        yv[u] = idx < n ? ldg4(Y + (long long)c * LPR + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+        sv[u] = idx < n ? __ldg(s_src + (long long)c * H + h) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        const int idx = k0 + u * NS + sid;
+        const float4 y = yv[u];
+        float part = g.x * y.x + g.y * y.y + g.z * y.z + g.w * y.w;
+        const float a = idx < n ? expf(leaky(sv[u] + sd, slope) - mx) * inv_l : 0.f;
+        for (int o = 1; o < dh4; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (idx < n) {
+          za += a * part;
+          if (head_lead) {
+            alpha[(long long)(base + idx) * H + h] = a;
+            dpre[(long long)(base + idx) * H + h] = part;   // dalpha, overwritten below
+          }
+        }
+      }
+    }
+    for (int k = k0; k < n; k += NS) {
       int idx = k + sid;
       int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
       float part = 0.f, a = 0.f;
@@ -601,6 +629,9 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
 }
 
 // ------------------------------------------------- backward GAT, pass 2 (CSC)
+// CSC entries in flight per stream: 4 with one stream per warp (D = 128);
+// 2 with two streams (D = 64: short columns, occupancy matters more)
+template <int D> struct ColU { static constexpr int v = D == 128 ? 4 : 2; };
 template <int D>
 __device__ __forceinline__ void gat_col_slice(int b, int e, int shift, int H,
                                               const int* __restrict__ csc_pos,
@@ -613,6 +644,7 @@ __device__ __forceinline__ void gat_col_slice(int b, int e, int shift, int H,
   constexpr int NS = 32 / LPR;
   const int sl = lane % LPR, sid = lane / LPR;
   const int h = sl / ((D / H) / 4);
+  constexpr int kColU = ColU<D>::v;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float dss = 0.f;
   for (int base = b; base < e; base += 32) {
@@ -622,7 +654,28 @@ __device__ __forceinline__ void gat_col_slice(int b, int e, int shift, int H,
       my_row = __ldg(csc_row + base + lane);
       my_pos = __ldg(csc_pos + base + lane);
     }
-    for (int k = 0; k < n; k += NS) {
+    int k = 0;
+    // kColU entries per stream in flight (a column's entries used to be
+    // one dependent L2 round trip each: the long columns set the tail)
+    for (; k + NS * kColU <= n; k += NS * kColU) {
+      float a[kColU], dp[kColU];
+      float4 g[kColU];
+#pragma unroll
+      for (int u = 0; u < kColU; u++) {
+        const int idx = k + u * NS + sid;
+        const int rr = __shfl_sync(0xffffffffu, my_row, idx);
+        const int p = __shfl_sync(0xffffffffu, my_pos, idx);
+        a[u] = __ldg(alpha + (long long)p * H + h);
+        dp[u] = __ldg(dpre + (long long)p * H + h);
+        g[u] = ldg4(G + (long long)(rr + shift) * LPR + sl);
+      }
+#pragma unroll
+      for (int u = 0; u < kColU; u++) {
+        dss += dp[u];
+        acc = f4fma(a[u], g[u], acc);
+      }
+    }
+    for (; k < n; k += NS) {
       int idx = k + sid;
       int src_lane = idx < n ? idx : 0;
       int rr = __shfl_sync(0xffffffffu, my_row, src_lane);

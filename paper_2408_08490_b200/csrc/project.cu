@@ -569,30 +569,39 @@ __global__ void k_att_dw(int R, int K, int D, int H, const float* __restrict__ d
   dW_rel[idx] += dv[((long long)r * H + h) * K + k] * att[(long long)r * 2 * D + D + d];
 }
 
-__global__ void k_att_da(int R, int K, int D, int H, const int* __restrict__ rel_y_off,
-                         const float* __restrict__ Psrc, const float* __restrict__ dv,
-                         const float* __restrict__ W_rel, float* __restrict__ datt) {
+// One block per (relation r, 32 consecutive d): lane = d (coalesced Psrc / W
+// reads), the 8 warps split the source chunks and the K loop, partials meet
+// in shared memory in warp order (deterministic).  (Thread per (r, d) left
+// R*D/128 blocks with two long serial loops on the attention critical path.)
+__global__ void __launch_bounds__(256)
+k_att_da(int R, int K, int D, int H, const int* __restrict__ rel_y_off,
+         const float* __restrict__ Psrc, const float* __restrict__ dv,
+         const float* __restrict__ W_rel, float* __restrict__ datt) {
   __shared__ int s_tab[HF_MAX_R + 1];
+  __shared__ float red[2][8][32];
   att_chunk_table(R, rel_y_off, s_tab);
   __syncthreads();
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= R * D) return;
-  const int r = idx / D, d = idx % D, h = d / (D / H);
-  float u4[4] = {0.f, 0.f, 0.f, 0.f};
-  const int c0 = s_tab[r], c1 = s_tab[r + 1];
-  int c = c0;
-  for (; c + 4 <= c1; c += 4)
+  const int tiles = D / 32;
+  const int r = blockIdx.x / tiles, d = (blockIdx.x % tiles) * 32 + (threadIdx.x & 31);
+  const int w = threadIdx.x >> 5;
+  if (r >= R) return;
+  const int h = d / (D / H);
+  float u = 0.f;
+  for (int c = s_tab[r] + w; c < s_tab[r + 1]; c += 8) u += Psrc[((long long)c * H + h) * D + d];
+  float t = 0.f;
+  const float* wp = W_rel + (long long)r * K * D + d;
+  const float* vp = dv + ((long long)r * H + h) * K;
+  for (int k = w; k < K; k += 8) t = fmaf(wp[(long long)k * D], vp[k], t);
+  red[0][w][threadIdx.x & 31] = u;
+  red[1][w][threadIdx.x & 31] = t;
+  __syncthreads();
+  if (w == 0) {
+    float a = 0.f, b2 = 0.f;
 #pragma unroll
-    for (int q = 0; q < 4; q++) u4[q] += Psrc[((long long)(c + q) * H + h) * D + d];
-  for (; c < c1; c++) u4[0] += Psrc[((long long)c * H + h) * D + d];
-  datt[(long long)r * 2 * D + d] = (u4[0] + u4[1]) + (u4[2] + u4[3]);
-  float t[4] = {0.f, 0.f, 0.f, 0.f};
-  const float* w = W_rel + (long long)r * K * D + d;
-  const float* v = dv + ((long long)r * H + h) * K;
-  for (int k = 0; k < K; k += 4)
-#pragma unroll
-    for (int q = 0; q < 4; q++) t[q] = fmaf(w[(long long)(k + q) * D], v[k + q], t[q]);
-  datt[(long long)r * 2 * D + D + d] = (t[0] + t[1]) + (t[2] + t[3]);
+    for (int q = 0; q < 8; q++) { a += red[0][q][threadIdx.x]; b2 += red[1][q][threadIdx.x]; }
+    datt[(long long)r * 2 * D + d] = a;
+    datt[(long long)r * 2 * D + D + d] = b2;
+  }
 }
 
 // dX_t[i] += sum_{r: t(r)=t} sum_h ds_dst[(r,i),h] v[r][:,h]   (s_dst chain);
@@ -873,7 +882,7 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
       cudaEventRecord(bb.join, bb.side);
       cudaStreamWaitEvent(sa, bb.join, 0);
     }
-    HF_LAUNCH(k_att_da, ceil_div((long long)m.R * D, 128), 128, 0, sa, m.R, K, D, H, csr->rel_y_off,
+    HF_LAUNCH(k_att_da, m.R * (D / 32), 256, 0, sa, m.R, K, D, H, csr->rel_y_off,
               Psrc, dvb, d_W_rel, d_datt);
   }
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
