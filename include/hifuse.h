@@ -319,13 +319,22 @@ hifuse_status hifuse_project_aggregated_bwd(const hifuse_layer_shape *shape,
  * gradients, and the SGD update p -= lr * g over a flat parameter buffer.
  *   logits = Hs Wc + bc  (Hs [B, D] rows of d_H starting at row h_row0)
  *   loss   = mean_b (logsumexp(logits_b) - logits_b[label_b])    -> d_loss [1]
- *   dH (rows h_row0.. of d_dH; all other rows zeroed), dWc [D,C], dbc [C]. */
+ *   dH (rows h_row0.. of d_dH; all other rows zeroed), dWc [D,C], dbc [C].
+ * Three kernels (logits, row softmax, gradients; 3xTF32 mma.sync, fp32-level
+ * accuracy).  d_dWc = d_dbc = NULL defers the weight gradient to hifuse_linear_xent_wgrad (same
+ * workspace), so a caller can run it on a parallel branch next to the
+ * backward of the HGNN layers. */
 size_t hifuse_xent_ws_bytes(int B, int D, int C);
 hifuse_status hifuse_linear_xent(int B, int D, int C, const float *d_H, int64_t h_rows,
                                  int64_t h_row0, const int32_t *d_labels, const float *d_Wc,
                                  const float *d_bc, float *d_loss, float *d_dH, float *d_dWc,
                                  float *d_dbc, void *d_ws, size_t ws_bytes,
                                  hifuse_stream_t stream);
+/* dWc = Hs^T dlog, dbc = column sums of dlog from the dlog a preceding
+ * hifuse_linear_xent (d_dWc = NULL) left in d_ws. */
+hifuse_status hifuse_linear_xent_wgrad(int B, int D, int C, const float *d_H, int64_t h_rows,
+                                       int64_t h_row0, float *d_dWc, float *d_dbc, void *d_ws,
+                                       size_t ws_bytes, hifuse_stream_t stream);
 hifuse_status hifuse_sgd(float *d_param, const float *d_grad, int64_t n, float lr, float grad_scale,
                          hifuse_stream_t stream);
 

@@ -358,11 +358,11 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
                                  float* d_dbc, void* d_ws, size_t ws_bytes,
                                  hifuse_stream_t stream) {
   if (B <= 0 || D <= 0 || C <= 0 || h_row0 < 0 || h_row0 + B > h_rows || !d_H || !d_labels ||
-      !d_Wc || !d_bc || !d_loss || !d_dH || !d_dWc || !d_dbc)
+      !d_Wc || !d_bc || !d_loss || !d_dH || (!d_dWc != !d_dbc))
     return HIFUSE_ERR_INVALID_ARG;
   if (ws_bytes < hifuse_xent_ws_bytes(B, D, C) || !d_ws) return HIFUSE_ERR_WORKSPACE;
   cudaStream_t s = st(stream);
-  const HeadGrid h = head_grid(B, D, C);
+  HeadGrid h = head_grid(B, D, C);
   const int nblk = (int)ceil_div(B, 8);
   char* p = (char*)d_ws;
   float* dlog = carve<float>(p, (long long)B * C);
@@ -373,17 +373,36 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   if (h_row0 + B < h_rows)
     cudaMemsetAsync(d_dH + (h_row0 + B) * D, 0, sizeof(float) * (h_rows - h_row0 - B) * D, s);
   const float* Hs = d_H + h_row0 * D;
-  HF_LAUNCH(k_head_logits, dim3(ceil_div(C, kBN), ceil_div(B, kBM)), 128, 0, s, B, D, C, Hs, d_Wc,
-            d_bc, dlog, ticket, 1);
+  HF_LAUNCH(k_head_logits, dim3(ceil_div(C, kBN), ceil_div(B, kBM)), 128, 0, s, B, D, C, Hs,
+            d_Wc, d_bc, dlog, ticket, 1);
   if (C <= 128)
-    HF_LAUNCH(k_head_softmax<4>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket, d_loss);
+    HF_LAUNCH(k_head_softmax<4>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket,
+              d_loss);
   else if (C <= 512)
     HF_LAUNCH(k_head_softmax<16>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket,
               d_loss);
   else
-    HF_LAUNCH(k_head_softmax<0>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket, d_loss);
+    HF_LAUNCH(k_head_softmax<0>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket,
+              d_loss);
+  if (!d_dWc) h.dw_tiles = 0;          // weight gradient deferred to hifuse_linear_xent_wgrad
   HF_LAUNCH(k_head_grads, (h.dh_tiles + h.dw_tiles) * kSlices, 128, 0, s, B, D, C, h, Hs, d_Wc,
             dlog, d_dH + h_row0 * D, d_dWc, d_dbc);
+  return last_cuda();
+}
+
+hifuse_status hifuse_linear_xent_wgrad(int B, int D, int C, const float* d_H, int64_t h_rows,
+                                       int64_t h_row0, float* d_dWc, float* d_dbc, void* d_ws,
+                                       size_t ws_bytes, hifuse_stream_t stream) {
+  if (B <= 0 || D <= 0 || C <= 0 || h_row0 < 0 || h_row0 + B > h_rows || !d_H || !d_dWc ||
+      !d_dbc)
+    return HIFUSE_ERR_INVALID_ARG;
+  if (ws_bytes < hifuse_xent_ws_bytes(B, D, C) || !d_ws) return HIFUSE_ERR_WORKSPACE;
+  HeadGrid h = head_grid(B, D, C);
+  h.dh_tiles = 0;
+  char* p = (char*)d_ws;
+  const float* dlog = carve<float>(p, (long long)B * C);
+  HF_LAUNCH(k_head_grads, h.dw_tiles * kSlices, 128, 0, st(stream), B, D, C, h, d_H + h_row0 * D,
+            (const float*)nullptr, dlog, (float*)nullptr, d_dWc, d_dbc);
   return last_cuda();
 }
 

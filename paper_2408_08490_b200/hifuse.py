@@ -97,6 +97,7 @@ def lib():
             "hifuse_xent_ws_bytes": [i32, i32, i32],
             "hifuse_linear_xent": [i32, i32, i32, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp,
                                    sz, vp],
+            "hifuse_linear_xent_wgrad": [i32, i32, i32, vp, i64, i64, vp, vp, vp, sz, vp],
             "hifuse_sgd": [vp, vp, i64, f32, f32, vp],
             "hifuse_sample_caps": [vp, i32, vp, i64, vp, vp, vp, vp],
             "hifuse_sample_blocks": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, vp, i32, vp, vp,
@@ -322,6 +323,12 @@ def linear_xent(B, D, C, H, h_row0, labels, Wc, bc, loss, dH, dWc, dbc, ws, stre
         B, D, C, _ptr(H), H.shape[0], h_row0, _ptr(labels), _ptr(Wc), _ptr(bc), _ptr(loss),
         _ptr(dH), _ptr(dWc), _ptr(dbc), _ptr(ws), ws.numel() * ws.element_size(),
         _stream(stream)))
+
+
+def linear_xent_wgrad(B, D, C, H, h_row0, dWc, dbc, ws, stream=None):
+    _check("hifuse_linear_xent_wgrad", lib().hifuse_linear_xent_wgrad(
+        B, D, C, _ptr(H), H.shape[0], h_row0, _ptr(dWc), _ptr(dbc), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def sgd(param, grad, lr, grad_scale=1.0, stream=None):

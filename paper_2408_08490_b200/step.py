@@ -174,10 +174,12 @@ class Trainer:
                                                 edge_type, wsb, self.status, rel_edge_off=off)
 
     # ----------------------------------------------------------------- plan
-    def plan(self, db: DeviceBatch, feat, edge_type, include_build=True):
+    def plan(self, db: DeviceBatch, feat, edge_type, include_build=True, split_head=True):
         """The step's library calls as a list of (stage name, closure).  All
         buffers are bound here, so the closures can be run eagerly or captured
-        into a CUDA graph (no allocation, no host sync inside)."""
+        into a CUDA graph (no allocation, no host sync inside).  split_head:
+        the classifier's weight gradient runs on a side stream next to the
+        layers' backward (a parallel graph branch), joined by the last op."""
         L, D, H, C = self.L, self.D, self.heads, self.C
         dev = db.dev
         shapes = db.shapes
@@ -232,10 +234,26 @@ class Trainer:
             X, gid = a["H"], None
         last = shapes[-1]
         dH = self._mat(f"dH{L - 1}", last.dst_rows, D)
-        wsx = self._ws(hf.xent_ws_bytes(db.B, D, C))
-        ops.append(("xent", lambda dH=dH: hf.linear_xent(
-            db.B, D, C, acts[-1]["H"][:last.dst_rows], db.h_row0, dev["labels"], self.P["Wc"],
-            self.P["bc"], self.loss, dH[:last.dst_rows], self.Gd["Wc"], self.Gd["bc"], wsx)))
+        wsx = self._ws(hf.xent_ws_bytes(db.B, D, C), key="ws_xent")
+        if split_head:
+            if not hasattr(self, "_head_side"):
+                self._head_side = torch.cuda.Stream(device=self.device)
+
+            def xent_op(dH=dH):
+                Hl = acts[-1]["H"][:last.dst_rows]
+                hf.linear_xent(db.B, D, C, Hl, db.h_row0, dev["labels"], self.P["Wc"],
+                               self.P["bc"], self.loss, dH[:last.dst_rows], None, None, wsx)
+                cur = torch.cuda.current_stream()
+                self._head_side.wait_stream(cur)
+                with torch.cuda.stream(self._head_side):
+                    hf.linear_xent_wgrad(db.B, D, C, Hl, db.h_row0, self.Gd["Wc"], self.Gd["bc"],
+                                         wsx)
+            ops.append(("xent", xent_op))
+        else:
+            ops.append(("xent", lambda dH=dH: hf.linear_xent(
+                db.B, D, C, acts[-1]["H"][:last.dst_rows], db.h_row0, dev["labels"],
+                self.P["Wc"], self.P["bc"], self.loss, dH[:last.dst_rows], self.Gd["Wc"],
+                self.Gd["bc"], wsx)))
         for l in range(L - 1, -1, -1):
             sh, a = shapes[l], acts[l]
             P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
@@ -270,6 +288,9 @@ class Trainer:
                                        b["ds_src"], b["ds_dst"], b["dX"], Gr["W_rel"],
                                        Gr["W_root"], Gr["att"], b["wsq"], prec=self.prec)))
             dH = b["dX"]
+        if split_head:
+            ops.append(("head_join", lambda: torch.cuda.current_stream().wait_stream(
+                self._head_side)))
         self.last = dict(acts=acts, csrs=csrs)
         return ops
 
@@ -348,7 +369,7 @@ class Trainer:
         """One CUDA graph per library call of the step (for per-stage device
         timing); returns [(name, graph, kernels)]."""
         out = []
-        ops = self.plan(db, feat, edge_type)
+        ops = self.plan(db, feat, edge_type, split_head=False)
         torch.cuda.synchronize()
         for name, fn in ops:
             g = torch.cuda.CUDAGraph()

@@ -296,12 +296,15 @@ def test_project_tf32_exact_on_representable_inputs(K, D):
     assert np.array_equal(dX.cpu().numpy(), ob["dX"].astype(np.float32))
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("B,C", [(5, 3), (128, 7), (1024, 128), (300, 129), (1024, 349),
-                                 (64, 600)])
-def test_linear_xent(B, C):
+                                 (64, 600), (2048, 7)])
+def test_linear_xent(B, C, split):
     """Classifier head: loss, dH (seed rows; other rows zero), dWc,
     dbc against the fp64 oracle head; register-row (C <= 512) and generic
-    softmax paths.  3xTF32 GEMMs: fp32-level error, 1e-5 of the scale."""
+    softmax paths; weight gradient in the same call or deferred
+    (hifuse_linear_xent_wgrad).  3xTF32 GEMMs: fp32-level error, 1e-5 of the
+    scale."""
     import oracle.model as om
     rng = np.random.default_rng(B * 1000 + C)
     D, row0, extra = 128, 17, 9
@@ -315,8 +318,14 @@ def test_linear_xent(B, C):
     dWc = torch.zeros(D, C, device=DEV)
     dbc = torch.zeros(C, device=DEV)
     ws = torch.empty(hf().xent_ws_bytes(B, D, C) // 4 + 64, device=DEV)
-    hf().linear_xent(B, D, C, t(Hfull), row0, torch.from_numpy(lab).to(DEV), t(Wc), t(bc), loss,
-                     dH, dWc, dbc, ws)
+    Hd = t(Hfull)
+    if split:      # weight gradient deferred to hifuse_linear_xent_wgrad
+        hf().linear_xent(B, D, C, Hd, row0, torch.from_numpy(lab).to(DEV), t(Wc), t(bc), loss,
+                         dH, None, None, ws)
+        hf().linear_xent_wgrad(B, D, C, Hd, row0, dWc, dbc, ws)
+    else:
+        hf().linear_xent(B, D, C, Hd, row0, torch.from_numpy(lab).to(DEV), t(Wc), t(bc), loss,
+                         dH, dWc, dbc, ws)
     torch.cuda.synchronize()
     assert abs(loss.item() - ref["loss"]) <= 1e-5 * max(1.0, abs(ref["loss"]))
     dHh = dH.cpu().numpy()
