@@ -264,7 +264,10 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape *shape, const hifuse
  *   dW_rel[r]  = sum_u X_row(u)^T dYt[u] (+ s_dst chain)   dW_root[t] = sum_i X_t[i]^T G_t[i]
  *   datt[r]    = (sum_u ds_src[u,h] Y[u,head h] | sum_i ds_dst v-chain)
  *   dX (optional, NULL for layer 0) = sum of dYt W_r^T + G W_root^T + ds_dst-chain.
- * Fixed-order chunked reductions (deterministic).  Workspace:
+ * d_dW_rel = d_dW_root = NULL (RGCN only, d_dX required): the input gradient
+ * alone; a second call with d_dX = NULL forms the weight gradients, so the
+ * caller can run it on a parallel stream while the next layer's backward
+ * proceeds.  Fixed-order chunked reductions (deterministic).  Workspace:
  * hifuse_project_bwd_ws_bytes(). */
 size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape *shape, int K, int D, int heads);
 hifuse_status hifuse_project_bwd(const hifuse_layer_shape *shape, const hifuse_csr *csr,

@@ -794,8 +794,11 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   hifuse_status rc = make_meta(shape, &m);
   if (rc != HIFUSE_OK) return rc;
   if (!kd_ok(K, D)) return HIFUSE_ERR_UNSUPPORTED;
-  if (!csr || !d_X || !d_W_rel || !d_dY || !d_dW_rel || x_rows < 0 ||
-      (d_W_root && (!d_dW_root || !d_G)))
+  // d_dW_rel == NULL: input gradient only (RGCN; the caller runs the weight
+  // gradient as a separate call, e.g. on a parallel stream)
+  const bool wgrad = d_dW_rel != nullptr;
+  if (!csr || !d_X || !d_W_rel || !d_dY || x_rows < 0 || (!wgrad && (!d_dX || d_att)) ||
+      (d_W_root && (!d_G || (wgrad && !d_dW_root))))
     return HIFUSE_ERR_INVALID_ARG;
   if (d_att && (!heads_ok2(D, heads) || !d_ds_src || !d_ds_dst || !d_datt || !d_Y))
     return HIFUSE_ERR_INVALID_ARG;
@@ -825,6 +828,24 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   // dgrad (dX) is independent of the weight-gradient chain: it runs on a
   // parallel branch (the dYt it reads is final after k_dy_score)
   DgradMeta dm;
+  if (!wgrad) {
+    if (prec == HIFUSE_PREC_TF32) {
+      make_dgrad_meta(m, d_W_root != nullptr, &dm, 128);
+      rc = dgrad_tc_launch(dm, K, D, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX, s, U_max,
+                           m.R);
+      return rc != HIFUSE_OK ? rc : last_cuda();
+    }
+    make_dgrad_meta(m, d_W_root != nullptr, &dm);
+    unsigned gd = dm.tile_off[m.T];
+#define HF_DG(KK, DD)                                                                         \
+  HF_LAUNCH((k_dgrad<KK, DD>), gd, 256, 0, s, dm, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX)
+    if (K == 128 && D == 128) HF_DG(128, 128);
+    else if (K == 128 && D == 64) HF_DG(128, 64);
+    else if (K == 64 && D == 128) HF_DG(64, 128);
+    else HF_DG(64, 64);
+#undef HF_DG
+    return last_cuda();
+  }
   Branch br;
   bool branched = false;
   if (d_dX && prec == HIFUSE_PREC_TF32) {

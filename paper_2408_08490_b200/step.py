@@ -282,11 +282,30 @@ class Trainer:
             ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b: hf.aggregate_bwd(
                 sh, c, self.agg, D, H, self.slope, b["G"], a["Y"], a["s_src"], a["s_dst"],
                 a["stats"], b["dY"], b["ds_src"], b["ds_dst"], b["wsa"])))
-            ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
+            if split_head and P["att"] is None and b["dX"] is not None:
+                # RGCN inner layer: the input gradient (next on the critical
+                # path) on the main stream; the weight gradients on the side
+                # stream, overlapping the outer layer's backward (own workspace)
+                b["wsw"] = self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H), key=f"ws_wg{l}")
+
+                def pbwd(sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr):
+                    hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
+                                   P["W_root"], None, a["Y"], b["dY"], b["G"], None, None,
+                                   b["dX"], None, None, None, b["wsq"], prec=self.prec)
+                    cur = torch.cuda.current_stream()
+                    self._head_side.wait_stream(cur)
+                    with torch.cuda.stream(self._head_side):
                         hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
-                                       P["W_root"], P["att"], a["Y"], b["dY"], b["G"],
-                                       b["ds_src"], b["ds_dst"], b["dX"], Gr["W_rel"],
-                                       Gr["W_root"], Gr["att"], b["wsq"], prec=self.prec)))
+                                       P["W_root"], None, a["Y"], b["dY"], b["G"], None, None,
+                                       None, Gr["W_rel"], Gr["W_root"], None, b["wsw"],
+                                       prec=self.prec)
+                ops.append((f"project_bwd.{l}", pbwd))
+            else:
+                ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
+                            hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
+                                           P["W_root"], P["att"], a["Y"], b["dY"], b["G"],
+                                           b["ds_src"], b["ds_dst"], b["dX"], Gr["W_rel"],
+                                           Gr["W_root"], Gr["att"], b["wsq"], prec=self.prec)))
             dH = b["dX"]
         if split_head:
             ops.append(("head_join", lambda: torch.cuda.current_stream().wait_stream(
