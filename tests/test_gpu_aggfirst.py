@@ -53,6 +53,13 @@ def test_aggregate_features(seed, agg, K):
     ref = oracle.aggregate_features(osh, blk, et, agg, K, X, gid)
     A = oracle.aggregate_features(osh, blk, et, agg, K, np.abs(X), gid)
     close_scaled(Xa.cpu().numpy()[:sh.rows], ref, A, what=f"Xagg {agg}")
+    # the split form (feature rows formed with the build, then the
+    # aggregation) is the same computation: bit-identical
+    colx = torch.empty(max(sh.N, 1), dtype=torch.int32, device=DEV)
+    Xb = torch.full_like(Xa, float("nan"))
+    hf().feature_cols(sh, csr, t(gid, torch.int32), colx)
+    hf().aggregate_features_cols(sh, csr, agg, K, t(X), colx, Xb)
+    assert torch.equal(Xa[:sh.rows], Xb[:sh.rows])
 
 
 def test_aggregate_features_integer_inputs_bit_exact():
