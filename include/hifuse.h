@@ -303,6 +303,19 @@ hifuse_status hifuse_aggregate_features_fwd(const hifuse_layer_shape *shape, con
                                             int64_t x_rows, const int32_t *d_gather_ids,
                                             float *d_Xagg, void *d_ws, size_t ws_bytes,
                                             hifuse_stream_t stream);
+/* The two halves of hifuse_aggregate_features_fwd, so the first can run with
+ * the semantic-graph build (off the critical path):
+ *   hifuse_feature_cols: d_col_x [N] = the feature-store row x(e) of every
+ *     CSR position (gather_ids NULL: identity);
+ *   hifuse_aggregate_features_cols: the aggregation over X rows d_col_x. */
+hifuse_status hifuse_feature_cols(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                  const int32_t *d_gather_ids, int32_t *d_col_x,
+                                  hifuse_stream_t stream);
+hifuse_status hifuse_aggregate_features_cols(const hifuse_layer_shape *shape,
+                                             const hifuse_csr *csr, hifuse_agg agg, int K,
+                                             const float *d_X, int64_t x_rows,
+                                             const int32_t *d_col_x, float *d_Xagg,
+                                             hifuse_stream_t stream);
 hifuse_status hifuse_project_aggregated(const hifuse_layer_shape *shape, const hifuse_csr *csr,
                                         hifuse_prec prec, int K, int D, const float *d_Xagg,
                                         const float *d_X, int64_t x_rows,

@@ -1090,6 +1090,47 @@ hifuse_status hifuse_aggregate_features_fwd(const hifuse_layer_shape* shape, con
   return last_cuda();
 }
 
+hifuse_status hifuse_feature_cols(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                  const int32_t* d_gather_ids, int32_t* d_col_x,
+                                  hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!csr || !csr->rel_y_off || !d_col_x || (m.N > 0 && (!csr->col || !csr->y_src)))
+    return HIFUSE_ERR_INVALID_ARG;
+  RelOff ro;
+  for (int r = 0; r < m.R; r++) ro.v[r] = m.type_src_off[m.rel_src[r]];
+  HF_LAUNCH(k_col_to_x, ceil_div(m.N, 256), 256, 0, st(stream), m.N, m.R, csr->rel_y_off, ro,
+            csr->col, csr->y_src, d_gather_ids, d_col_x);
+  return last_cuda();
+}
+
+hifuse_status hifuse_aggregate_features_cols(const hifuse_layer_shape* shape,
+                                             const hifuse_csr* csr, hifuse_agg agg, int K,
+                                             const float* d_X, int64_t x_rows,
+                                             const int32_t* d_col_x, float* d_Xagg,
+                                             hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (agg != HIFUSE_AGG_SUM && agg != HIFUSE_AGG_MEAN) return HIFUSE_ERR_UNSUPPORTED;
+  if (K != 64 && K != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !csr->row_ptr || x_rows < 0 || !d_Xagg || (m.N > 0 && (!d_col_x || !d_X)))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_X) || !aligned16(d_Xagg)) return HIFUSE_ERR_ALIGNMENT;
+  cudaStream_t s = st(stream);
+  unsigned grid = ceil_div((long long)m.rows, kWarpsPerBlock);
+  const int TB = kWarpsPerBlock * 32;
+  const bool mean = agg == HIFUSE_AGG_MEAN;
+#define HF_AGG(DD, MM)                                                                  \
+  HF_LAUNCH((k_agg_fwd<DD, MM>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, d_col_x, \
+            (const float4*)d_X, (float4*)d_Xagg)
+  if (K == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
+  else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }
+#undef HF_AGG
+  return last_cuda();
+}
+
 size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg agg, int heads) {
   LayerMeta m;
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;

@@ -89,6 +89,8 @@ def lib():
                                    vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
             "hifuse_aggregate_features_ws_bytes": [vp],
             "hifuse_aggregate_features_fwd": [vp, vp, i32, i32, vp, i64, vp, vp, vp, sz, vp],
+            "hifuse_feature_cols": [vp, vp, vp, vp, vp],
+            "hifuse_aggregate_features_cols": [vp, vp, i32, i32, vp, i64, vp, vp, vp],
             "hifuse_project_aggregated": [vp, vp, i32, i32, i32, vp, vp, i64, vp, vp, vp, vp, vp,
                                           vp],
             "hifuse_project_aggregated_bwd_ws_bytes": [vp, i32, i32],
@@ -292,6 +294,17 @@ def aggregate_features_fwd(shape, csr, agg, K, X, gather_ids, Xagg, ws, stream=N
     _check("hifuse_aggregate_features_fwd", lib().hifuse_aggregate_features_fwd(
         shape.ref, csr.ref, AGG[agg], K, _ptr(X), X.shape[0], _ptr(gather_ids), _ptr(Xagg),
         _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def feature_cols(shape, csr, gather_ids, col_x, stream=None):
+    _check("hifuse_feature_cols", lib().hifuse_feature_cols(
+        shape.ref, csr.ref, _ptr(gather_ids), _ptr(col_x), _stream(stream)))
+
+
+def aggregate_features_cols(shape, csr, agg, K, X, col_x, Xagg, stream=None):
+    _check("hifuse_aggregate_features_cols", lib().hifuse_aggregate_features_cols(
+        shape.ref, csr.ref, AGG[agg], K, _ptr(X), X.shape[0], _ptr(col_x), _ptr(Xagg),
+        _stream(stream)))
 
 
 def project_aggregated(shape, csr, K, D, Xagg, X, gather_ids, W_rel, W_root, Z, R0, prec="tf32",

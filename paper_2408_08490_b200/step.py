@@ -170,8 +170,19 @@ class Trainer:
         csrs = [self._csr(l, s, db.slot) for l, s in enumerate(shapes)]
         wsb = self._ws(max(s.build_ws for s in shapes), key="ws_build")
         off = self._et_offsets(edge_type)
-        return lambda: hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"],
-                                                edge_type, wsb, self.status, rel_edge_off=off)
+        if not self.agg_first:
+            return lambda: hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"],
+                                                    dev["eid"], edge_type, wsb, self.status,
+                                                    rel_edge_off=off)
+        # aggregate-first input layer: the feature-store row of every CSR
+        # position is formed with the build (off the critical path)
+        colx = self._buf(f"colx{db.slot}", max(shapes[0].N, 1), torch.int32)
+
+        def op():
+            hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"], edge_type,
+                                     wsb, self.status, rel_edge_off=off)
+            hf.feature_cols(shapes[0], csrs[0], dev["gid"], colx)
+        return op
 
     # ----------------------------------------------------------------- plan
     def plan(self, db: DeviceBatch, feat, edge_type, include_build=True, split_head=True):
@@ -203,11 +214,12 @@ class Trainer:
                      H=self._mat(f"H{l}", sh.dst_rows, D),
                      wsp=self._ws(hf.project_ws_bytes(sh, K, D, H)))
             if self.agg_first and l == 0:
-                a.update(Y=None, Xagg=self._mat("Xagg0", sh.rows, K),
-                         wsx=self._ws(hf.aggregate_features_ws_bytes(sh), key="ws_aggx"))
-                ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a:
-                            hf.aggregate_features_fwd(sh, c, self.agg, a["K"], a["X"], a["gid"],
-                                                      a["Xagg"], a["wsx"])))
+                a.update(Y=None, Xagg=self._mat("Xagg0", sh.rows, K))
+                # colx: written by this batch's build op (hifuse_feature_cols)
+                colx = self._buf(f"colx{db.slot}", max(sh.N, 1), torch.int32)
+                ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a, colx=colx:
+                            hf.aggregate_features_cols(sh, c, self.agg, a["K"], a["X"], colx,
+                                                       a["Xagg"])))
                 ops.append(("project_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
                             hf.project_aggregated(sh, c, a["K"], D, a["Xagg"], a["X"], a["gid"],
                                                   P["W_rel"], P["W_root"], a["Z"], a["R0"],

@@ -258,6 +258,20 @@ def test_project_fwd_bwd(K, D, H, att, prec):
     row_rel_l2(dX.cpu().numpy(), ob["dX"], wt, "dX")
     if att:
         row_rel_l2(datt.cpu().numpy().reshape(-1, D), ob["datt"].reshape(-1, D), wt, "datt")
+    if not att:
+        # split form (input gradient alone, then weights alone with dX = NULL,
+        # the Trainer's side-stream schedule): bit-identical to the combined call
+        dX2 = torch.zeros_like(dX)
+        dW2 = torch.zeros_like(dW)
+        dWr2 = torch.zeros_like(dWr) if dWr is not None else None
+        wsc = torch.empty_like(wsb)
+        hf().project_bwd(sh, csr, K, D, H, t(Xl), None, t(W), tn(Wr), None, t(Yl), t(dYn), t(Gn),
+                         None, None, dX2, None, None, None, wsb, prec=prec)
+        hf().project_bwd(sh, csr, K, D, H, t(Xl), None, t(W), tn(Wr), None, t(Yl), t(dYn), t(Gn),
+                         None, None, None, dW2, dWr2, None, wsc, prec=prec)
+        assert torch.equal(dX2, dX) and torch.equal(dW2, dW)
+        if dWr is not None:
+            assert torch.equal(dWr2, dWr)
 
 
 @pytest.mark.parametrize("K,D", [(128, 128), (64, 64), (128, 64), (64, 128)])
