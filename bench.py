@@ -131,11 +131,19 @@ def stage_cost(stage, l, cfg, sz):
         return 4 * K * m + 4 * D * m + 4 * (R + T) * K * D, 2 * K * D * m
     if stage == "project_bwd":
         m = s["U"] + (s["dst"] if root else 0)
+        if cfg.model == "rgcn" and l > 0:     # input gradient only (weights: project_wgrad)
+            return 4 * D * m + 4 * s["src"] * K + 4 * (R + T) * K * D, 2 * K * D * m
         f = 2 * K * D * m * (2 if l > 0 else 1)
         return 4 * K * m + 4 * D * m + (4 * s["src"] * K if l > 0 else 0), f
-    if stage == "xent":     # classifier head: Hs, Wc, dlog (written + read), dHs, dWc
+    if stage == "project_wgrad":
+        m = s["U"] + (s["dst"] if root else 0)
+        return 4 * K * m + 4 * D * m, 2 * K * D * m
+    if stage == "xent_wgrad":
         C, B = cfg.num_classes, cfg.batch_size
-        return 4 * (2 * B * D + 2 * D * C + 3 * B * C), 3 * 2 * B * D * C
+        return 4 * (B * D + D * C + B * C), 2 * B * D * C
+    if stage == "xent":     # classifier head: Hs, Wc (twice), dlog (written + read), dHs
+        C, B = cfg.num_classes, cfg.batch_size
+        return 4 * (2 * B * D + 2 * D * C + 2 * B * C), 2 * 2 * B * D * C
     if stage == "aggregate_features":     # aggregate-first input layer: A4 over raw X
         return 4 * K * s["U"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
     if stage == "project_aggregated":
@@ -158,6 +166,7 @@ def stage_cost(stage, l, cfg, sz):
 
 # main kernel of every library call (for the ncu traffic lookup)
 MAIN_KERNEL = {"aggregate_fwd": "k_agg_fwd", "aggregate_bwd": "k_agg_bwd_p", "project": "k_proj_fwd_tcp",
+               "project_wgrad": "k_wgrad_tc", "xent_wgrad": "k_head_grads",
                "project_bwd": "k_wgrad_tc", "fuse": "k_fuse", "fuse_bwd": "k_fuse_bwd_chunks",
                "build": "k_sort_long", "xent": "k_head_grads", "aggregate_features": "k_agg_fwd",
                "project_aggregated": "k_proj_fwd_tcp", "project_aggregated_bwd": "k_wgrad_tc"}
@@ -509,7 +518,8 @@ def main():
         avg_bytes = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[0] for pi in used]))
         avg_flops = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[1] for pi in used]))
         t_s = per_step[stage_key] / 1e3
-        gemm = ("project", "project_bwd", "project_aggregated", "project_aggregated_bwd", "xent")
+        gemm = ("project", "project_bwd", "project_aggregated", "project_aggregated_bwd", "xent",
+                "project_wgrad", "xent_wgrad")
         if name in gemm and args.prec == "fp32":
             roof = {"bound": "alu", "achieved": avg_flops / t_s / 1e12, "peak": ALU_FP32_TFLOPS,
                     "unit": "TFLOP/s"}
@@ -526,12 +536,16 @@ def main():
             roof = {"bound": "hbm", "achieved": avg_bytes / t_s / 1e9, "peak": pk["hbm"],
                     "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        bwd = name in ("aggregate_bwd", "project_bwd", "fuse_bwd", "project_aggregated_bwd")
-        tr = None if name == "build" else ncu_traffic(MAIN_KERNEL.get(name, name),
+        bwd = name in ("aggregate_bwd", "project_bwd", "fuse_bwd", "project_aggregated_bwd",
+                       "project_wgrad")
+        mk = MAIN_KERNEL.get(name, name)
+        if name == "project_bwd" and cfg.model == "rgcn":
+            mk = "k_dgrad_tc"                 # input gradient only (weights: project_wgrad)
+        tr = None if name == "build" else ncu_traffic(mk,
                                                        cfg.num_layers - 1 - l if bwd else l,
                                                        cfg.key, args.order)
         roof["traffic"] = tr
-        roof["kernel"] = f"{stage_key} (main kernel {MAIN_KERNEL.get(name, name)})"
+        roof["kernel"] = f"{stage_key} (main kernel {mk})"
         roof["peak_source"] = pk["src"]
         roof["algorithmic"] = {"bytes": avg_bytes, "flops": avg_flops,
                                "us": per_step[stage_key] * 1e3}
@@ -540,7 +554,9 @@ def main():
 
     # the dominant call on the critical path (the build overlaps the compute
     # stream when pipelined and is reported separately)
-    cand = [k for k in per_step if not (pipelined and k == "build")]
+    side = ("xent_wgrad", "project_wgrad")      # side-stream calls: off the critical path
+    cand = [k for k in per_step if not (pipelined and k == "build")
+            and not k.startswith(side)]
     dom = max(cand, key=lambda k: per_step[k])
     roof = roofline_of(dom)
     build_roof = roofline_of("build") if "build" in per_step else None
@@ -661,6 +677,7 @@ def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr
     sgraphs = []
     with torch.cuda.stream(side):
         for k in range(2):
+            seeds_d[k].copy_(host_seeds[0])          # valid seeds for the warm-up call
             ctl_d[k].copy_(torch.tensor([1, smp.next_stamp()], dtype=torch.int64))
             smp.sample(seeds_d[k], cfg.target_type, 0, side, buf=k, d_ctl=ctl_d[k])
             side.synchronize()
@@ -669,6 +686,8 @@ def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr
                 smp.sample(seeds_d[k], cfg.target_type, 0, side, buf=k, d_ctl=ctl_d[k])
             sgraphs.append(gk)
     torch.cuda.synchronize()
+    smp.status.zero_()
+    tr.status.zero_()
 
     def launch_sample(i):
         k = i % 2

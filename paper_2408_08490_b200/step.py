@@ -247,25 +247,27 @@ class Trainer:
         last = shapes[-1]
         dH = self._mat(f"dH{L - 1}", last.dst_rows, D)
         wsx = self._ws(hf.xent_ws_bytes(db.B, D, C), key="ws_xent")
-        if split_head:
-            if not hasattr(self, "_head_side"):
-                self._head_side = torch.cuda.Stream(device=self.device)
+        if not hasattr(self, "_head_side"):
+            self._head_side = torch.cuda.Stream(device=self.device)
 
-            def xent_op(dH=dH):
-                Hl = acts[-1]["H"][:last.dst_rows]
-                hf.linear_xent(db.B, D, C, Hl, db.h_row0, dev["labels"], self.P["Wc"],
-                               self.P["bc"], self.loss, dH[:last.dst_rows], None, None, wsx)
-                cur = torch.cuda.current_stream()
-                self._head_side.wait_stream(cur)
+        def side_op(fn):
+            """Weight-gradient calls: on the side stream when split_head (a
+            parallel graph branch, joined by the last op), else in line."""
+            if not split_head:
+                return fn
+
+            def run():
+                self._head_side.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(self._head_side):
-                    hf.linear_xent_wgrad(db.B, D, C, Hl, db.h_row0, self.Gd["Wc"], self.Gd["bc"],
-                                         wsx)
-            ops.append(("xent", xent_op))
-        else:
-            ops.append(("xent", lambda dH=dH: hf.linear_xent(
-                db.B, D, C, acts[-1]["H"][:last.dst_rows], db.h_row0, dev["labels"],
-                self.P["Wc"], self.P["bc"], self.loss, dH[:last.dst_rows], self.Gd["Wc"],
-                self.Gd["bc"], wsx)))
+                    fn()
+            return run
+
+        Hl = acts[-1]["H"][:last.dst_rows]
+        ops.append(("xent", lambda dH=dH: hf.linear_xent(
+            db.B, D, C, Hl, db.h_row0, dev["labels"], self.P["Wc"], self.P["bc"], self.loss,
+            dH[:last.dst_rows], None, None, wsx)))
+        ops.append(("xent_wgrad", side_op(lambda: hf.linear_xent_wgrad(
+            db.B, D, C, Hl, db.h_row0, self.Gd["Wc"], self.Gd["bc"], wsx))))
         for l in range(L - 1, -1, -1):
             sh, a = shapes[l], acts[l]
             P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
@@ -294,24 +296,21 @@ class Trainer:
             ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b: hf.aggregate_bwd(
                 sh, c, self.agg, D, H, self.slope, b["G"], a["Y"], a["s_src"], a["s_dst"],
                 a["stats"], b["dY"], b["ds_src"], b["ds_dst"], b["wsa"])))
-            if split_head and P["att"] is None and b["dX"] is not None:
+            if P["att"] is None and b["dX"] is not None:
                 # RGCN inner layer: the input gradient (next on the critical
-                # path) on the main stream; the weight gradients on the side
-                # stream, overlapping the outer layer's backward (own workspace)
+                # path) and the weight gradients as two calls, the second on
+                # the side stream overlapping the outer layer's backward
                 b["wsw"] = self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H), key=f"ws_wg{l}")
-
-                def pbwd(sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr):
+                ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P:
+                            hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
+                                           P["W_root"], None, a["Y"], b["dY"], b["G"], None,
+                                           None, b["dX"], None, None, None, b["wsq"],
+                                           prec=self.prec)))
+                ops.append((f"project_wgrad.{l}", side_op(
+                    lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
                     hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
-                                   P["W_root"], None, a["Y"], b["dY"], b["G"], None, None,
-                                   b["dX"], None, None, None, b["wsq"], prec=self.prec)
-                    cur = torch.cuda.current_stream()
-                    self._head_side.wait_stream(cur)
-                    with torch.cuda.stream(self._head_side):
-                        hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
-                                       P["W_root"], None, a["Y"], b["dY"], b["G"], None, None,
-                                       None, Gr["W_rel"], Gr["W_root"], None, b["wsw"],
-                                       prec=self.prec)
-                ops.append((f"project_bwd.{l}", pbwd))
+                                   P["W_root"], None, a["Y"], b["dY"], b["G"], None, None, None,
+                                   Gr["W_rel"], Gr["W_root"], None, b["wsw"], prec=self.prec))))
             else:
                 ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
                             hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
