@@ -696,6 +696,69 @@ __device__ __forceinline__ void gat_col_slice(int b, int e, int shift, int H,
   *dss_out = dss;
 }
 
+// D = 64: one column per HALF warp (16 lanes x float4 = one row), so the two
+// halves walk two short columns independently (the one-column-per-warp form
+// split every column's 1-2 entries over two streams and left the warp count
+// at U).  Entries are summed in CSC order, as in gat_col_slice.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_cols_half(BwdMeta bm, int H, const int* __restrict__ U_dev,
+                        const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
+                        const int* __restrict__ csc_pos, const int* __restrict__ csc_row,
+                        const float* __restrict__ alpha, const float* __restrict__ dpre,
+                        const float4* __restrict__ G, float4* __restrict__ dY,
+                        float* __restrict__ ds_src, int* __restrict__ long_list,
+                        int* __restrict__ long_cnt) {
+  constexpr int LPR = 16;                       // D = 64
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  const unsigned mask = 0xffffu << (16 * half);
+  const int u = (blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * 2 + half;
+  if (u >= *U_dev) return;
+  const int b = col_ptr[u], e = col_ptr[u + 1];
+  if (e - b > kLongCol) {
+    if (hl == 0) long_list[atomicAdd(long_cnt, 1)] = u;
+    return;
+  }
+  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
+  const int shift = bm.shift[r];
+  const int dh4 = (64 / H) / 4;
+  const int h = hl / dh4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float dss = 0.f;
+  for (int base = b; base < e; base += 16) {
+    const int n = min(16, e - base);
+    int my_row = 0, my_pos = 0;
+    if (hl < n) {
+      my_row = __ldg(csc_row + base + hl);
+      my_pos = __ldg(csc_pos + base + hl);
+    }
+    int k = 0;
+    for (; k + 2 <= n; k += 2) {               // two entries in flight
+      const int rr0 = __shfl_sync(mask, my_row, k, 16), p0 = __shfl_sync(mask, my_pos, k, 16);
+      const int rr1 = __shfl_sync(mask, my_row, k + 1, 16);
+      const int p1 = __shfl_sync(mask, my_pos, k + 1, 16);
+      const float a0 = __ldg(alpha + (long long)p0 * H + h), d0 = __ldg(dpre + (long long)p0 * H + h);
+      const float a1 = __ldg(alpha + (long long)p1 * H + h), d1 = __ldg(dpre + (long long)p1 * H + h);
+      const float4 g0 = ldg4(G + (long long)(rr0 + shift) * LPR + hl);
+      const float4 g1 = ldg4(G + (long long)(rr1 + shift) * LPR + hl);
+      dss += d0;
+      acc = f4fma(a0, g0, acc);
+      dss += d1;
+      acc = f4fma(a1, g1, acc);
+    }
+    if (k < n) {
+      const int rr = __shfl_sync(mask, my_row, k, 16), p = __shfl_sync(mask, my_pos, k, 16);
+      dss += __ldg(dpre + (long long)p * H + h);
+      acc = f4fma(__ldg(alpha + (long long)p * H + h), ldg4(G + (long long)(rr + shift) * LPR + hl),
+                  acc);
+    }
+  }
+  dY[(long long)u * LPR + hl] = acc;
+  if (hl % dh4 == 0) ds_src[(long long)u * H + hl / dh4] = dss;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
@@ -1189,9 +1252,14 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
     HF_LAUNCH(k_agg_bwd_gat_rows<DD>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows, \
               heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,     \
               d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                            \
-  HF_LAUNCH(k_agg_bwd_gat_cols<DD>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off,   \
-            csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
-            (float4*)d_dY, d_ds_src, long_list, long_cnt);                                    \
+  if (DD == 64)                                                                                \
+    HF_LAUNCH(k_agg_bwd_gat_cols_half, ceil_div(U_max, kWarpsPerBlock * 2), TB, 0, s, bm, heads, \
+              csr->U_dev, csr->rel_y_off, csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre,\
+              (const float4*)d_G, (float4*)d_dY, d_ds_src, long_list, long_cnt);               \
+  else                                                                                         \
+    HF_LAUNCH(k_agg_bwd_gat_cols<DD>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off, \
+              csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,      \
+              (float4*)d_dY, d_ds_src, long_list, long_cnt);                                  \
   HF_LAUNCH(k_agg_bwd_gat_cols_long<DD>, gridL, kLongWarps * 32, 0, s, bm, heads, csr->rel_y_off,          \
             csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
             (float4*)d_dY, d_ds_src, long_list, long_cnt)
