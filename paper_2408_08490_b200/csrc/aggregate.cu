@@ -189,6 +189,74 @@ k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_pt
   }
 }
 
+// D = 64: one merged row per HALF warp (16 lanes x float4 = one Y row); the
+// two halves process two rows independently (rows are short: ~3-10 edges).
+// Same two passes as k_agg_fwd_gat; edges summed in row order.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_fwd_gat_half(long long rows, int H, float slope, const int* __restrict__ row_ptr,
+                   const int* __restrict__ col, const float4* __restrict__ Y,
+                   const float* __restrict__ s_src, const float* __restrict__ s_dst,
+                   float4* __restrict__ Z, float* __restrict__ stats) {
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  const unsigned mask = 0xffffu << (16 * half);
+  const long long row = ((long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * 2 + half;
+  if (row >= rows) return;
+  const int dh4 = (64 / H) / 4;
+  const int h = hl / dh4;
+  const int b = row_ptr[row], e = row_ptr[row + 1];
+  const float sd = s_dst[row * H + h];
+  float m = -INFINITY;
+  for (int base = b; base < e; base += 16) {
+    const int n = min(16, e - base);
+    const int my_col = hl < n ? __ldg(col + base + hl) : 0;
+    for (int k = 0; k < n; k++) {
+      const int c = __shfl_sync(mask, my_col, k, 16);
+      m = fmaxf(m, leaky(__ldg(s_src + (long long)c * H + h) + sd, slope));
+    }
+  }
+  float l = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = b; base < e; base += 16) {
+    const int n = min(16, e - base);
+    const int my_col = hl < n ? __ldg(col + base + hl) : 0;
+    int k = 0;
+    for (; k + 4 <= n; k += 4) {
+      float4 v[4];
+      float sc[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int c = __shfl_sync(mask, my_col, k + u, 16);
+        v[u] = ldg4(Y + (long long)c * 16 + hl);
+        sc[u] = __ldg(s_src + (long long)c * H + h);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const float p = expf(leaky(sc[u] + sd, slope) - m);
+        l += p;
+        acc = f4fma(p, v[u], acc);
+      }
+    }
+    for (; k < n; k++) {
+      const int c = __shfl_sync(mask, my_col, k, 16);
+      const float p = expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - m);
+      l += p;
+      acc = f4fma(p, ldg4(Y + (long long)c * 16 + hl), acc);
+    }
+  }
+  if (e > b) {
+    acc = make_float4(__fdiv_rn(acc.x, l), __fdiv_rn(acc.y, l), __fdiv_rn(acc.z, l),
+                      __fdiv_rn(acc.w, l));
+  } else {
+    m = 0.f;
+    l = 0.f;
+  }
+  Z[row * 16 + hl] = acc;
+  if (hl % dh4 == 0) {
+    stats[row * 2 * H + h] = m;
+    stats[row * 2 * H + H + h] = l;
+  }
+}
+
 // ---------------------------------------------------- backward SUM/MEAN (CSC)
 // dY[u] = sum_{q in column u} w(row_q) G[row_q + shift(r(u))]; all rows of a
 // column belong to Y row u's relation r(u), found once per warp.
@@ -1070,8 +1138,9 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_a
       HF_LAUNCH(k_agg_fwd_gat<128>, grid, TB, 0, s, (long long)rows, heads, slope, csr->row_ptr,
                 csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z, d_stats);
     else
-      HF_LAUNCH(k_agg_fwd_gat<64>, grid, TB, 0, s, (long long)rows, heads, slope, csr->row_ptr,
-                csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z, d_stats);
+      HF_LAUNCH(k_agg_fwd_gat_half, ceil_div(rows, kWarpsPerBlock * 2), TB, 0, s, (long long)rows,
+                heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,
+                (float4*)d_Z, d_stats);
   } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
     bool mean = agg == HIFUSE_AGG_MEAN;
 #define HF_AGG(DD, MM)                                                                   \
