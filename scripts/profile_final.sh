@@ -4,7 +4,7 @@
 # activity), traffic.json, warm launch lists, bench lines of all configs,
 # the reference arm, and the GPU sampler launch list.
 set -x
-OUT=gpurun_out/prof_r1c
+OUT=gpurun_out/${PROF_OUT:-prof_r1c}
 mkdir -p $OUT
 for c in mag imdb; do
   ncu --set full --import-source on --clock-control none -o /tmp/step_$c \
