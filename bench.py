@@ -391,15 +391,29 @@ def main():
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
+        # events also at 10 chunk boundaries (same stream, no sync): the
+        # spread of the per-step time over the run (SURVEY §8(d) protocol)
+        nchunk = 10 if K >= 10 else 1
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(nchunk - 1)]
+        bounds = [K * (c + 1) // nchunk for c in range(nchunk - 1)]
         t0 = time.time()
         a.record()
         for i in range(K):
             one_step(i, e2e, loss_host)
+            if i + 1 in bounds:
+                marks[bounds.index(i + 1)].record()
         b.record()
         b.synchronize()
         t1 = time.time()
         barrier()
         ms = a.elapsed_time(b)
+        evs = [a] + marks + [b]
+        cuts = [0] + bounds + [K]
+        chunks = [evs[c].elapsed_time(evs[c + 1]) / (cuts[c + 1] - cuts[c])
+                  for c in range(len(evs) - 1)]
+        timed.spread = {"chunks": nchunk, "min_ms_per_step": min(chunks),
+                        "median_ms_per_step": float(np.median(chunks)),
+                        "max_ms_per_step": max(chunks)}
         if world > 1:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -411,6 +425,7 @@ def main():
     clocks = ClockSampler(local % ngpu)
     time.sleep(0.25)
     ms, t0, t1 = timed(args.steps)
+    spread = dict(timed.spread)
     launches = sum(graphs[i % len(pool)][1] for i in range(args.steps)) + \
         (args.steps if world > 1 else 0)
     clk = clocks.summary(t0, t1)
@@ -602,6 +617,7 @@ def main():
                         "overlaps compute of batch i" if graphs is not serial_graphs else
                         "one CUDA graph per pool batch (whole step, serial)"),
         "serial_ms_per_step": ms_serial / args.steps,
+        "spread": spread,
         "other_order": other,
         "merged_vs_unmerged": unmerged,
         "gpu_sampler": gsmp,
