@@ -696,6 +696,83 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
   if (sid == 0 && head_lead) ds_dst[row * H + h] = dsd;
 }
 
+// D = 64: pass 1 with one merged row per HALF warp (rows are short; the
+// warp-per-row form split each row over two streams).  Same arithmetic as
+// k_agg_bwd_gat_rows, edges in row order.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_rows_half(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long rows, int H,
+                        float slope, const int* __restrict__ row_ptr,
+                        const int* __restrict__ col, const float4* __restrict__ Y,
+                        const float* __restrict__ s_src, const float* __restrict__ s_dst,
+                        const float* __restrict__ stats, const float4* __restrict__ G,
+                        float* __restrict__ alpha, float* __restrict__ dpre,
+                        float* __restrict__ ds_dst) {
+  __shared__ int s_roff[HF_MAX_R + 1];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_roff[i] = rel_row_off_d[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  const unsigned mask = 0xffffu << (16 * half);
+  const long long row = ((long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * 2 + half;
+  if (row >= rows) return;
+  const int dh4 = (64 / H) / 4;
+  const int h = hl / dh4;
+  const bool head_lead = (hl % dh4) == 0;
+  const int b = row_ptr[row], e = row_ptr[row + 1];
+  if (e == b) {
+    if (head_lead) ds_dst[row * H + h] = 0.f;
+    return;
+  }
+  const int r = upper_bound_i(s_roff, bm.R + 1, (int)row) - 1;
+  const float4 g = ldg4(G + (row + bm.shift[r]) * 16 + hl);
+  const float sd = s_dst[row * H + h];
+  const float mx = stats[row * 2 * H + h];
+  const float inv_l = 1.f / stats[row * 2 * H + H + h];
+  float za = 0.f;
+  for (int base = b; base < e; base += 16) {
+    const int n = min(16, e - base);
+    const int my_col = hl < n ? __ldg(col + base + hl) : 0;
+    for (int k0 = 0; k0 < n; k0 += 4) {
+      float4 yv[4];
+      float sv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int idx = k0 + u;
+        const int c = __shfl_sync(mask, my_col, idx < n ? idx : 0, 16);
+        yv[u] = idx < n ? ldg4(Y + (long long)c * 16 + hl) : make_float4(0.f, 0.f, 0.f, 0.f);
+        sv[u] = idx < n ? __ldg(s_src + (long long)c * H + h) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int idx = k0 + u;
+        float part = g.x * yv[u].x + g.y * yv[u].y + g.z * yv[u].z + g.w * yv[u].w;
+        for (int o = 1; o < dh4; o <<= 1) part += __shfl_xor_sync(mask, part, o, 16);
+        if (idx < n) {
+          const float a = expf(leaky(sv[u] + sd, slope) - mx) * inv_l;
+          za += a * part;
+          if (head_lead) {
+            alpha[(long long)(base + idx) * H + h] = a;
+            dpre[(long long)(base + idx) * H + h] = part;   // dalpha, overwritten below
+          }
+        }
+      }
+    }
+  }
+  __syncwarp(mask);
+  float dsd = 0.f;
+  if (head_lead) {
+    for (int p = b; p < e; p++) {
+      const int c = __ldg(col + p);
+      const float pre = __ldg(s_src + (long long)c * H + h) + sd;
+      const float a = alpha[(long long)p * H + h];
+      const float da = dpre[(long long)p * H + h];
+      const float dp = a * (da - za) * (pre > 0.f ? 1.f : slope);
+      dpre[(long long)p * H + h] = dp;
+      dsd += dp;
+    }
+    ds_dst[row * H + h] = dsd;
+  }
+}
+
 // ------------------------------------------------- backward GAT, pass 2 (CSC)
 // CSC entries in flight per stream: 4 with one stream per warp (D = 128);
 // 2 with two streams (D = 64: short columns, occupancy matters more)
@@ -1317,6 +1394,11 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
     HF_LAUNCH(k_agg_bwd_gat_xrel_dst<DD>, ceil_div(m.dst_rows, kWarpsPerBlock), TB, 0, s, xm, \
               m.dst_rows, heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src,   \
               d_s_dst, d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                    \
+  else if (DD == 64)                                                                           \
+    HF_LAUNCH(k_agg_bwd_gat_rows_half, ceil_div(m.rows, kWarpsPerBlock * 2), TB, 0, s, bm,      \
+              csr->rel_row_off, (long long)m.rows, heads, slope, csr->row_ptr, csr->col,        \
+              (const float4*)d_Y, d_s_src, d_s_dst, d_stats, (const float4*)d_G, alpha, dpre,   \
+              d_ds_dst);                                                                       \
   else                                                                                         \
     HF_LAUNCH(k_agg_bwd_gat_rows<DD>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows, \
               heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,     \
