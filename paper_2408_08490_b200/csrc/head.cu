@@ -231,6 +231,80 @@ k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__
   }
 }
 
+// Few classes (C <= 32, the RGCN/RGAT configs except ogbn-mag): the whole
+// critical part of the head in ONE kernel, one warp per seed row:
+//   lane c < C: logit_c = bc_c + <Hs_b, Wc[:, c]> (Hs row broadcast by shuffles,
+//   Wc is a few KB and stays in L1) -> softmax / cross-entropy across the lanes
+//   -> dlog (global, for hifuse_linear_xent_wgrad) -> dHs_b[k] = sum_c dlog_c
+//   Wc[k, c] (lane k + 32 j).  Exact fp32; replaces three latency-bound
+//   launches.  Block = 8 rows; the last block sums the per-block losses.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_head_small(int B, int C, const float* __restrict__ Hs, const float* __restrict__ Wc,
+             const float* __restrict__ bc, const int* __restrict__ labels,
+             float* __restrict__ dlog, float* __restrict__ dHs, float* __restrict__ block_loss,
+             int* __restrict__ ticket, float* __restrict__ loss) {
+  constexpr int KPL = D / 32;              // features per lane
+  __shared__ float s_l[8];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * 8 + w;
+  float rl = 0.f;
+  if (b < B) {
+    float hv[KPL];
+#pragma unroll
+    for (int j = 0; j < KPL; j++) hv[j] = Hs[(long long)b * D + j * 32 + lane];
+    const bool act = lane < C;
+    float z = act ? __ldg(bc + lane) : -INFINITY;
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < KPL; j++)
+#pragma unroll 8
+      for (int q = 0; q < 32; q++) {
+        const float x = __shfl_sync(0xffffffffu, hv[j], q);
+        if (act) acc = fmaf(x, __ldg(Wc + (long long)(j * 32 + q) * C + lane), acc);
+      }
+    if (act) z += acc;
+    float mx = z;
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float ex = act ? expf(z - mx) : 0.f;
+    float se = ex;
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int y = labels[b];
+    const float zy = __shfl_sync(0xffffffffu, z, y);
+    const float g = act ? (ex / se - (lane == y ? 1.f : 0.f)) / (float)B : 0.f;
+    if (act) dlog[(long long)b * C + lane] = g;
+    rl = logf(se) + mx - zy;
+#pragma unroll
+    for (int j = 0; j < KPL; j++) {
+      const int k = j * 32 + lane;
+      float d = 0.f;
+      for (int c = 0; c < C; c++)
+        d = fmaf(__shfl_sync(0xffffffffu, g, c), __ldg(Wc + (long long)k * C + c), d);
+      dHs[(long long)b * D + k] = d;
+    }
+  }
+  if (lane == 0) s_l[w] = rl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int q = 0; q < 8; q++) t += s_l[q];
+    block_loss[blockIdx.x] = t;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < 32) {
+    __threadfence();
+    float t = 0.f;
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += 32) t += __ldcg(block_loss + q);
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) loss[0] = t / (float)B;
+  }
+}
+
+__global__ void k_zero_int(int* p) { *p = 0; }
+
 struct HeadGrid {
   int dh_tiles_n, dh_tiles;       // dHs: [B, D] tiles (n-major), K = C
   int dw_tiles_n, dw_tiles;       // dWc: [D, C] tiles, K = B
@@ -373,6 +447,21 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   if (h_row0 + B < h_rows)
     cudaMemsetAsync(d_dH + (h_row0 + B) * D, 0, sizeof(float) * (h_rows - h_row0 - B) * D, s);
   const float* Hs = d_H + h_row0 * D;
+  if (C <= 32 && (D == 128 || D == 64)) {
+    HF_LAUNCH(k_zero_int, 1, 1, 0, s, ticket);
+    if (D == 128)
+      HF_LAUNCH(k_head_small<128>, nblk, 256, 0, s, B, C, Hs, d_Wc, d_bc, d_labels, dlog,
+                d_dH + h_row0 * D, block_loss, ticket, d_loss);
+    else
+      HF_LAUNCH(k_head_small<64>, nblk, 256, 0, s, B, C, Hs, d_Wc, d_bc, d_labels, dlog,
+                d_dH + h_row0 * D, block_loss, ticket, d_loss);
+    h.dh_tiles = 0;                    // dHs done
+    if (!d_dWc) h.dw_tiles = 0;
+    if (h.dw_tiles)
+      HF_LAUNCH(k_head_grads, h.dw_tiles * kSlices, 128, 0, s, B, D, C, h, Hs, d_Wc, dlog,
+                d_dH + h_row0 * D, d_dWc, d_dbc);
+    return last_cuda();
+  }
   HF_LAUNCH(k_head_logits, dim3(ceil_div(C, kBN), ceil_div(B, kBM)), 128, 0, s, B, D, C, Hs,
             d_Wc, d_bc, dlog, ticket, 1);
   if (C <= 128)
