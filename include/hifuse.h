@@ -259,6 +259,19 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape *shape, const hifuse
                                    float *d_ds_src, float *d_ds_dst, void *d_ws, size_t ws_bytes,
                                    hifuse_stream_t stream);
 
+/* RGAT, score chain folded into the CSC pass: as hifuse_aggregate_bwd (GAT or
+ * GAT_XREL) but d_dY receives dYt = dY + ds_src (x) att[r, 0] directly (the
+ * term hifuse_project_bwd would otherwise add in place, same fp32 fma), so
+ * the projection backward must then be hifuse_project_bwd_scored.  d_att
+ * [R, 2, D] (16-byte aligned); INVALID_ARG for SUM/MEAN or NULL d_att. */
+hifuse_status hifuse_aggregate_bwd_scored(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                          hifuse_agg agg, int D, int heads, float slope,
+                                          const float *d_G, const float *d_Y,
+                                          const float *d_s_src, const float *d_s_dst,
+                                          const float *d_stats, const float *d_att, float *d_dY,
+                                          float *d_ds_src, float *d_ds_dst, void *d_ws,
+                                          size_t ws_bytes, hifuse_stream_t stream);
+
 /* A6c. Projection backward, the adjoint of hifuse_project:
  *   dYt = dY + ds_src (x) att[r,0]             (score chain, RGAT; d_dY updated in place)
  *   dW_rel[r]  = sum_u X_row(u)^T dYt[u] (+ s_dst chain)   dW_root[t] = sum_i X_t[i]^T G_t[i]
@@ -353,6 +366,20 @@ hifuse_status hifuse_linear_xent_wgrad(int B, int D, int C, const float *d_H, in
                                        size_t ws_bytes, hifuse_stream_t stream);
 hifuse_status hifuse_sgd(float *d_param, const float *d_grad, int64_t n, float lr, float grad_scale,
                          hifuse_stream_t stream);
+
+/* hifuse_project_bwd for a d_dY that already holds dYt (produced by
+ * hifuse_aggregate_bwd_scored): identical except that the in-place score-chain
+ * update of d_dY is skipped.  d_att required. */
+hifuse_status hifuse_project_bwd_scored(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                        hifuse_layout layout, hifuse_prec prec, int K, int D,
+                                        int heads, const float *d_X, int64_t x_rows,
+                                        const int32_t *d_gather_ids, const float *d_W_rel,
+                                        const float *d_W_root, const float *d_att,
+                                        const float *d_Y, float *d_dY, const float *d_G,
+                                        const float *d_ds_src, const float *d_ds_dst,
+                                        float *d_dX, float *d_dW_rel, float *d_dW_root,
+                                        float *d_datt, void *d_ws, size_t ws_bytes,
+                                        hifuse_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * NEXT(1): GPU neighbour sampler.  PAPER.md Fig. 2 step (1)

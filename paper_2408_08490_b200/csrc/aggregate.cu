@@ -30,6 +30,11 @@ __device__ __forceinline__ float4 f4shfl_xor(float4 v, int o) {
   return make_float4(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o),
                      __shfl_xor_sync(0xffffffffu, v.z, o), __shfl_xor_sync(0xffffffffu, v.w, o));
 }
+// y + s * a elementwise as fmaf(s, a, y): the score-chain term of dYt
+// (k_dy_score's arithmetic, bit for bit)
+__device__ __forceinline__ float4 f4fma_into(float s, float4 a, float4 y) {
+  return make_float4(fmaf(s, a.x, y.x), fmaf(s, a.y, y.y), fmaf(s, a.z, y.z), fmaf(s, a.w, y.w));
+}
 __device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? x : slope * x; }
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
@@ -852,7 +857,7 @@ k_agg_bwd_gat_cols_half(BwdMeta bm, int H, const int* __restrict__ U_dev,
                         const float* __restrict__ alpha, const float* __restrict__ dpre,
                         const float4* __restrict__ G, float4* __restrict__ dY,
                         float* __restrict__ ds_src, int* __restrict__ long_list,
-                        int* __restrict__ long_cnt) {
+                        int* __restrict__ long_cnt, const float* __restrict__ att) {
   constexpr int LPR = 16;                       // D = 64
   __shared__ int s_yoff[HF_MAX_R + 1];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
@@ -900,6 +905,7 @@ k_agg_bwd_gat_cols_half(BwdMeta bm, int H, const int* __restrict__ U_dev,
                   acc);
     }
   }
+  if (att) acc = f4fma_into(dss, ldg4(reinterpret_cast<const float4*>(att + (long long)r * 2 * 64) + hl), acc);
   dY[(long long)u * LPR + hl] = acc;
   if (hl % dh4 == 0) ds_src[(long long)u * H + hl / dh4] = dss;
 }
@@ -912,7 +918,7 @@ k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
                    const float* __restrict__ alpha, const float* __restrict__ dpre,
                    const float4* __restrict__ G, float4* __restrict__ dY,
                    float* __restrict__ ds_src, int* __restrict__ long_list,
-                   int* __restrict__ long_cnt) {
+                   int* __restrict__ long_cnt, const float* __restrict__ att) {
   constexpr int LPR = D / 4;
   __shared__ int s_yoff[HF_MAX_R + 1];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
@@ -931,6 +937,7 @@ k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
   gat_col_slice<D>(b, e, bm.shift[r], H, csc_pos, csc_row, alpha, dpre, G, lane, &acc, &dss);
   const int dh4 = (D / H) / 4;
   if (lane < LPR) {
+    if (att) acc = f4fma_into(dss, ldg4(reinterpret_cast<const float4*>(att + (long long)r * 2 * D) + lane), acc);
     dY[(long long)u * LPR + lane] = acc;
     if (lane % dh4 == 0) ds_src[(long long)u * H + lane / dh4] = dss;
   }
@@ -943,7 +950,8 @@ k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
                         const int* __restrict__ csc_row, const float* __restrict__ alpha,
                         const float* __restrict__ dpre, const float4* __restrict__ G,
                         float4* __restrict__ dY, float* __restrict__ ds_src,
-                        const int* __restrict__ list, const int* __restrict__ cnt) {
+                        const int* __restrict__ list, const int* __restrict__ cnt,
+                        const float* __restrict__ att) {
   constexpr int LPR = D / 4;
   __shared__ int s_yoff[HF_MAX_R + 1];
   __shared__ float4 red[kLongWarps][LPR];
@@ -974,6 +982,7 @@ k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
         t = f4add(t, red[q][lane]);
         ts += reds[q][lane];
       }
+      if (att) t = f4fma_into(ts, ldg4(reinterpret_cast<const float4*>(att + (long long)r * 2 * D) + lane), t);
       dY[(long long)u * LPR + lane] = t;
       if (lane % dh4 == 0) ds_src[(long long)u * H + lane / dh4] = ts;
     }
@@ -1351,12 +1360,13 @@ size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg
   return b;
 }
 
-hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
-                                   hifuse_agg agg, int D, int heads, float slope,
-                                   const float* d_G, const float* d_Y, const float* d_s_src,
-                                   const float* d_s_dst, const float* d_stats, float* d_dY,
-                                   float* d_ds_src, float* d_ds_dst, void* d_ws, size_t ws_bytes,
-                                   hifuse_stream_t stream) {
+static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                        hifuse_agg agg, int D, int heads, float slope,
+                                        const float* d_G, const float* d_Y, const float* d_s_src,
+                                        const float* d_s_dst, const float* d_stats,
+                                        const float* d_att, float* d_dY, float* d_ds_src,
+                                        float* d_ds_dst, void* d_ws, size_t ws_bytes,
+                                        hifuse_stream_t stream) {
   LayerMeta m;
   hifuse_status rc = make_meta(shape, &m);
   if (rc != HIFUSE_OK) return rc;
@@ -1406,14 +1416,14 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
   if (DD == 64)                                                                                \
     HF_LAUNCH(k_agg_bwd_gat_cols_half, ceil_div(U_max, kWarpsPerBlock * 2), TB, 0, s, bm, heads, \
               csr->U_dev, csr->rel_y_off, csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre,\
-              (const float4*)d_G, (float4*)d_dY, d_ds_src, long_list, long_cnt);               \
+              (const float4*)d_G, (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att);        \
   else                                                                                         \
     HF_LAUNCH(k_agg_bwd_gat_cols<DD>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off, \
               csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,      \
-              (float4*)d_dY, d_ds_src, long_list, long_cnt);                                  \
+              (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att);                           \
   HF_LAUNCH(k_agg_bwd_gat_cols_long<DD>, gridL, kLongWarps * 32, 0, s, bm, heads, csr->rel_y_off,          \
             csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
-            (float4*)d_dY, d_ds_src, long_list, long_cnt)
+            (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att)
     if (D == 128) { HF_GAT(128); } else { HF_GAT(64); }
 #undef HF_GAT
   } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
@@ -1435,6 +1445,30 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse
     return HIFUSE_ERR_INVALID_ARG;
   }
   return last_cuda();
+}
+
+hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                   hifuse_agg agg, int D, int heads, float slope,
+                                   const float* d_G, const float* d_Y, const float* d_s_src,
+                                   const float* d_s_dst, const float* d_stats, float* d_dY,
+                                   float* d_ds_src, float* d_ds_dst, void* d_ws, size_t ws_bytes,
+                                   hifuse_stream_t stream) {
+  return aggregate_bwd_impl(shape, csr, agg, D, heads, slope, d_G, d_Y, d_s_src, d_s_dst, d_stats,
+                            nullptr, d_dY, d_ds_src, d_ds_dst, d_ws, ws_bytes, stream);
+}
+
+hifuse_status hifuse_aggregate_bwd_scored(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                          hifuse_agg agg, int D, int heads, float slope,
+                                          const float* d_G, const float* d_Y,
+                                          const float* d_s_src, const float* d_s_dst,
+                                          const float* d_stats, const float* d_att, float* d_dY,
+                                          float* d_ds_src, float* d_ds_dst, void* d_ws,
+                                          size_t ws_bytes, hifuse_stream_t stream) {
+  if ((agg != HIFUSE_AGG_GAT && agg != HIFUSE_AGG_GAT_XREL) || !d_att)
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_att)) return HIFUSE_ERR_ALIGNMENT;
+  return aggregate_bwd_impl(shape, csr, agg, D, heads, slope, d_G, d_Y, d_s_src, d_s_dst, d_stats,
+                            d_att, d_dY, d_ds_src, d_ds_dst, d_ws, ws_bytes, stream);
 }
 
 }  // extern "C"

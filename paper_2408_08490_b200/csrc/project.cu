@@ -780,14 +780,16 @@ size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D
   return b;
 }
 
-hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
-                                 hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
-                                 const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
-                                 const float* d_W_rel, const float* d_W_root, const float* d_att,
-                                 const float* d_Y, float* d_dY, const float* d_G,
-                                 const float* d_ds_src, const float* d_ds_dst, float* d_dX,
-                                 float* d_dW_rel, float* d_dW_root, float* d_datt, void* d_ws,
-                                 size_t ws_bytes, hifuse_stream_t stream) {
+static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                      hifuse_layout layout, hifuse_prec prec, int K, int D,
+                                      int heads, const float* d_X, int64_t x_rows,
+                                      const int32_t* d_gather_ids, const float* d_W_rel,
+                                      const float* d_W_root, const float* d_att,
+                                      const float* d_Y, float* d_dY, const float* d_G,
+                                      const float* d_ds_src, const float* d_ds_dst, float* d_dX,
+                                      float* d_dW_rel, float* d_dW_root, float* d_datt,
+                                      void* d_ws, size_t ws_bytes, hifuse_stream_t stream,
+                                      bool scored) {
   if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
   if (prec != HIFUSE_PREC_FP32 && prec != HIFUSE_PREC_TF32) return HIFUSE_ERR_UNSUPPORTED;
   LayerMeta m;
@@ -821,7 +823,7 @@ hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_c
   long long ach = U_max / kCHA + m.rows / kCHA + 2 * m.R + 2;
   float* Psrc = carve<float>(p, ach * H * (K > D ? K : D));
   float* Pdst = carve<float>(p, ach * H * (K > D ? K : D));
-  if (d_att) {
+  if (d_att && !scored) {      // scored: dY already holds dYt (hifuse_aggregate_bwd_scored)
     HF_LAUNCH(k_dy_score, ceil_div(U_max * (D / 4), 256), 256, 0, s, m.R, D, H, csr->U_dev,
               csr->rel_y_off, d_att, d_ds_src, (float4*)d_dY);
   }
@@ -1019,6 +1021,35 @@ hifuse_status hifuse_project_aggregated_bwd(const hifuse_layer_shape* shape,
             (const int*)nullptr, (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root,
             pm, csr->rel_row_off, CH);
   return last_cuda();
+}
+
+hifuse_status hifuse_project_bwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                 hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
+                                 const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
+                                 const float* d_W_rel, const float* d_W_root, const float* d_att,
+                                 const float* d_Y, float* d_dY, const float* d_G,
+                                 const float* d_ds_src, const float* d_ds_dst, float* d_dX,
+                                 float* d_dW_rel, float* d_dW_root, float* d_datt, void* d_ws,
+                                 size_t ws_bytes, hifuse_stream_t stream) {
+  return project_bwd_impl(shape, csr, layout, prec, K, D, heads, d_X, x_rows, d_gather_ids,
+                          d_W_rel, d_W_root, d_att, d_Y, d_dY, d_G, d_ds_src, d_ds_dst, d_dX,
+                          d_dW_rel, d_dW_root, d_datt, d_ws, ws_bytes, stream, false);
+}
+
+hifuse_status hifuse_project_bwd_scored(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                        hifuse_layout layout, hifuse_prec prec, int K, int D,
+                                        int heads, const float* d_X, int64_t x_rows,
+                                        const int32_t* d_gather_ids, const float* d_W_rel,
+                                        const float* d_W_root, const float* d_att,
+                                        const float* d_Y, float* d_dY, const float* d_G,
+                                        const float* d_ds_src, const float* d_ds_dst,
+                                        float* d_dX, float* d_dW_rel, float* d_dW_root,
+                                        float* d_datt, void* d_ws, size_t ws_bytes,
+                                        hifuse_stream_t stream) {
+  if (!d_att) return HIFUSE_ERR_INVALID_ARG;
+  return project_bwd_impl(shape, csr, layout, prec, K, D, heads, d_X, x_rows, d_gather_ids,
+                          d_W_rel, d_W_root, d_att, d_Y, d_dY, d_G, d_ds_src, d_ds_dst, d_dX,
+                          d_dW_rel, d_dW_root, d_datt, d_ws, ws_bytes, stream, true);
 }
 
 }  // extern "C"

@@ -84,6 +84,10 @@ def lib():
             "hifuse_aggregate_bwd_ws_bytes": [vp, i32, i32],
             "hifuse_aggregate_bwd": [vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp,
                                      vp, sz, vp],
+            "hifuse_aggregate_bwd_scored": [vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp,
+                                            vp, vp, vp, sz, vp],
+            "hifuse_project_bwd_scored": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp,
+                                          vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
             "hifuse_project_bwd_ws_bytes": [vp, i32, i32, i32],
             "hifuse_project_bwd": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp,
                                    vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
@@ -273,6 +277,14 @@ def aggregate_bwd(shape, csr, agg, D, heads, slope, G, Y, s_src, s_dst, stats, d
         0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)))
 
 
+def aggregate_bwd_scored(shape, csr, agg, D, heads, slope, G, Y, s_src, s_dst, stats, att, dY,
+                         ds_src, ds_dst, ws, stream=None):
+    _check("hifuse_aggregate_bwd_scored", lib().hifuse_aggregate_bwd_scored(
+        shape.ref, csr.ref, AGG[agg], D, heads, slope, _ptr(G), _ptr(Y), _ptr(s_src), _ptr(s_dst),
+        _ptr(stats), _ptr(att), _ptr(dY), _ptr(ds_src), _ptr(ds_dst), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
+
+
 def project_bwd_ws_bytes(shape, K, D, heads):
     return int(lib().hifuse_project_bwd_ws_bytes(shape.ref, K, D, heads))
 
@@ -280,6 +292,15 @@ def project_bwd_ws_bytes(shape, K, D, heads):
 def project_bwd(shape, csr, K, D, heads, X, gather_ids, W_rel, W_root, att, Y, dY, G, ds_src,
                 ds_dst, dX, dW_rel, dW_root, datt, ws, prec="fp32", stream=None):
     _check("hifuse_project_bwd", lib().hifuse_project_bwd(
+        shape.ref, csr.ref, LAYOUT_COMPACT, PREC[prec], K, D, heads, _ptr(X), X.shape[0],
+        _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(att), _ptr(Y), _ptr(dY), _ptr(G),
+        _ptr(ds_src), _ptr(ds_dst), _ptr(dX), _ptr(dW_rel), _ptr(dW_root), _ptr(datt), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def project_bwd_scored(shape, csr, K, D, heads, X, gather_ids, W_rel, W_root, att, Y, dY, G,
+                       ds_src, ds_dst, dX, dW_rel, dW_root, datt, ws, prec="fp32", stream=None):
+    _check("hifuse_project_bwd_scored", lib().hifuse_project_bwd_scored(
         shape.ref, csr.ref, LAYOUT_COMPACT, PREC[prec], K, D, heads, _ptr(X), X.shape[0],
         _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(att), _ptr(Y), _ptr(dY), _ptr(G),
         _ptr(ds_src), _ptr(ds_dst), _ptr(dX), _ptr(dW_rel), _ptr(dW_root), _ptr(datt), _ptr(ws),

@@ -293,9 +293,17 @@ class Trainer:
                      wsq=self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H)))
             ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
                 sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
-            ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b: hf.aggregate_bwd(
-                sh, c, self.agg, D, H, self.slope, b["G"], a["Y"], a["s_src"], a["s_dst"],
-                a["stats"], b["dY"], b["ds_src"], b["ds_dst"], b["wsa"])))
+            if P["att"] is not None:   # RGAT: score chain folded into the CSC pass
+                ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P:
+                            hf.aggregate_bwd_scored(sh, c, self.agg, D, H, self.slope, b["G"],
+                                                    a["Y"], a["s_src"], a["s_dst"], a["stats"],
+                                                    P["att"], b["dY"], b["ds_src"], b["ds_dst"],
+                                                    b["wsa"])))
+            else:
+                ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b:
+                            hf.aggregate_bwd(sh, c, self.agg, D, H, self.slope, b["G"], a["Y"],
+                                             a["s_src"], a["s_dst"], a["stats"], b["dY"],
+                                             b["ds_src"], b["ds_dst"], b["wsa"])))
             if P["att"] is None and b["dX"] is not None:
                 # RGCN inner layer: the input gradient (next on the critical
                 # path) and the weight gradients as two calls, the second on
@@ -312,11 +320,13 @@ class Trainer:
                                    P["W_root"], None, a["Y"], b["dY"], b["G"], None, None, None,
                                    Gr["W_rel"], Gr["W_root"], None, b["wsw"], prec=self.prec))))
             else:
-                ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
-                            hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
-                                           P["W_root"], P["att"], a["Y"], b["dY"], b["G"],
-                                           b["ds_src"], b["ds_dst"], b["dX"], Gr["W_rel"],
-                                           Gr["W_root"], Gr["att"], b["wsq"], prec=self.prec)))
+                pb = hf.project_bwd_scored if P["att"] is not None else hf.project_bwd
+                ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr,
+                            pb=pb:
+                            pb(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"],
+                               P["att"], a["Y"], b["dY"], b["G"], b["ds_src"], b["ds_dst"],
+                               b["dX"], Gr["W_rel"], Gr["W_root"], Gr["att"], b["wsq"],
+                               prec=self.prec)))
             dH = b["dX"]
         if split_head:
             ops.append(("head_join", lambda: torch.cuda.current_stream().wait_stream(

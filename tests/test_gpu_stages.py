@@ -170,6 +170,20 @@ def test_aggregate_bwd_gat(seed, D, H):
     np.add.at(scale_s, u, term)
     close_scaled(dss.cpu().numpy(), ref["ds_src"], scale_s, rtol=2e-5, what="ds_src")
     close_scaled(dsd.cpu().numpy(), ref["ds_dst"], scale_d, rtol=2e-5, what="ds_dst")
+    # score chain folded into the CSC pass (hifuse_aggregate_bwd_scored):
+    # dYt = dY + ds_src (x) att[r, 0] in the same fp32 fma as k_dy_score
+    att = torch.from_numpy(rng.standard_normal((sh.R, 2, D)).astype(np.float32)).to(DEV)
+    dY2 = torch.zeros_like(dY)
+    dss2 = torch.zeros_like(dss)
+    dsd2 = torch.zeros_like(dsd)
+    hf().aggregate_bwd_scored(sh, csr, "gat", D, H, 0.2, t(G), t(Y), t(ss), t(sd), stats, att,
+                              dY2, dss2, dsd2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(dss2, dss) and torch.equal(dsd2, dsd)
+    rel = np.repeat(np.arange(sh.R), np.diff(ch["rel_y_off"]))
+    a_src = att[torch.from_numpy(rel).to(DEV), 0]                       # [U, D]
+    want = torch.addcmul(dY, dss.repeat_interleave(D // H, dim=1), a_src)
+    torch.testing.assert_close(dY2, want, rtol=1e-6, atol=1e-6)
 
 
 def _gmap_index(sh, ch):
