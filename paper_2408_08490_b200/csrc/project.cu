@@ -780,6 +780,22 @@ size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D
   return b;
 }
 
+// One event per device ordering k_dx_sdst (dgrad branch) after the fold of
+// W a_dst (source-side attention branch); created outside graph capture.
+static cudaEvent_t fold_event(cudaStream_t s) {
+  static cudaEvent_t ev[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!ev[dev]) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return nullptr;
+    if (cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+  }
+  return ev[dev];
+}
+
 static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hifuse_csr* csr,
                                       hifuse_layout layout, hifuse_prec prec, int K, int D,
                                       int heads, const float* d_X, int64_t x_rows,
@@ -850,6 +866,7 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
   }
   Branch br;
   bool branched = false;
+  bool dx_sdst_done = false;
   if (d_dX && prec == HIFUSE_PREC_TF32) {
     make_dgrad_meta(m, d_W_root != nullptr, &dm, 128);
     branched = branch_begin(s, &br);
@@ -894,6 +911,19 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
     cudaStream_t sb = bbr ? bb.side : sa;
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, sb, m.R, K, D, H, d_W_rel,
               d_att, v);
+    // the s_dst chain's dX term needs only the fold and the dgrad: it runs on
+    // the dgrad branch as soon as both are done (not after both attention
+    // chains and k_att_dw)
+    if (d_dX && branched && prec == HIFUSE_PREC_TF32) {
+      cudaEvent_t ev = fold_event(s);
+      if (ev) {
+        cudaEventRecord(ev, sb);
+        cudaStreamWaitEvent(br.side, ev, 0);
+        HF_LAUNCH(k_dx_sdst, ceil_div((long long)m.dst_rows * K, 256), 256, 0, br.side, dm,
+                  m.dst_rows, K, H, v, d_ds_dst, d_dX);
+        dx_sdst_done = true;
+      }
+    }
     const unsigned gs = (unsigned)(U_max / kCHA + m.R + 1);
     const unsigned gdst = (unsigned)(m.rows / kCHA + m.R + 1);
     HF_LAUNCH(k_att_partial, gs, H * D / 4, 0, sb, m.R, H, D, 0, (const int*)nullptr,
@@ -931,7 +961,7 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
       else HF_DG(64, 64);
 #undef HF_DG
     }
-    if (d_att)
+    if (d_att && !dx_sdst_done)
       HF_LAUNCH(k_dx_sdst, ceil_div((long long)m.dst_rows * K, 256), 256, 0, s, dm, m.dst_rows, K,
                 H, v, d_ds_dst, d_dX);
   }
