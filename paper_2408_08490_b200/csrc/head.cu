@@ -238,7 +238,7 @@ k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__
 //   -> dlog (global, for hifuse_linear_xent_wgrad) -> dHs_b[k] = sum_c dlog_c
 //   Wc[k, c] (lane k + 32 j).  Exact fp32; replaces three latency-bound
 //   launches.  Block = 8 rows; the last block sums the per-block losses.
-template <int D>
+template <int D, int CMAX>
 __global__ void __launch_bounds__(256)
 k_head_small(int B, int C, const float* __restrict__ Hs, const float* __restrict__ Wc,
              const float* __restrict__ bc, const int* __restrict__ labels,
@@ -255,15 +255,27 @@ k_head_small(int B, int C, const float* __restrict__ Hs, const float* __restrict
 #pragma unroll
     for (int j = 0; j < KPL; j++) hv[j] = Hs[(long long)b * D + j * 32 + lane];
     const bool act = lane < C;
-    float z = act ? __ldg(bc + lane) : -INFINITY;
+    // lane owns features k = lane + 32 j: partial logits of every class over
+    // its features, then one butterfly sum per class (no serial K chain)
+    float pc[CMAX];
+#pragma unroll
+    for (int c = 0; c < CMAX; c++) pc[c] = 0.f;
+#pragma unroll
+    for (int j = 0; j < KPL; j++) {
+      const float* wr = Wc + (long long)(j * 32 + lane) * C;
+#pragma unroll
+      for (int c = 0; c < CMAX; c++)
+        if (c < C) pc[c] = fmaf(hv[j], __ldg(wr + c), pc[c]);
+    }
     float acc = 0.f;
 #pragma unroll
-    for (int j = 0; j < KPL; j++)
-#pragma unroll 8
-      for (int q = 0; q < 32; q++) {
-        const float x = __shfl_sync(0xffffffffu, hv[j], q);
-        if (act) acc = fmaf(x, __ldg(Wc + (long long)(j * 32 + q) * C + lane), acc);
-      }
+    for (int c = 0; c < CMAX; c++) {
+      if (c >= C) break;
+      float v = pc[c];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == c) acc = v;
+    }
+    float z = act ? __ldg(bc + lane) : -INFINITY;
     if (act) z += acc;
     float mx = z;
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -449,12 +461,12 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
   const float* Hs = d_H + h_row0 * D;
   if (C <= 32 && (D == 128 || D == 64)) {
     HF_LAUNCH(k_zero_int, 1, 1, 0, s, ticket);
-    if (D == 128)
-      HF_LAUNCH(k_head_small<128>, nblk, 256, 0, s, B, C, Hs, d_Wc, d_bc, d_labels, dlog,
-                d_dH + h_row0 * D, block_loss, ticket, d_loss);
-    else
-      HF_LAUNCH(k_head_small<64>, nblk, 256, 0, s, B, C, Hs, d_Wc, d_bc, d_labels, dlog,
-                d_dH + h_row0 * D, block_loss, ticket, d_loss);
+#define HF_SMALL(DD, CC)                                                                      \
+  HF_LAUNCH((k_head_small<DD, CC>), nblk, 256, 0, s, B, C, Hs, d_Wc, d_bc, d_labels, dlog,      \
+            d_dH + h_row0 * D, block_loss, ticket, d_loss)
+    if (D == 128) { if (C <= 8) HF_SMALL(128, 8); else HF_SMALL(128, 32); }
+    else { if (C <= 8) HF_SMALL(64, 8); else HF_SMALL(64, 32); }
+#undef HF_SMALL
     h.dh_tiles = 0;                    // dHs done
     if (!d_dWc) h.dw_tiles = 0;
     if (h.dw_tiles)
