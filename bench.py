@@ -100,9 +100,14 @@ def layer_sizes(cfg, g, mb, rs, rd):
     for blk in mb.layers:
         r = g.edge_type[blk.edge_id]
         U = len(np.unique(r.astype(np.int64) * (1 << 32) + blk.src_local)) if blk.num_edges else 0
+        # distinct source VERTICES read by the layer (a vertex that is a
+        # source of several relations is one feature row): the compulsory
+        # read of an aggregation over raw features
+        st = rs[r].astype(np.int64)
+        F = len(np.unique(st * (1 << 32) + blk.src_local)) if blk.num_edges else 0
         rows = int(sum(int(blk.n_dst[rd[k]]) for k in range(len(rd))))
         S = int(sum(int(blk.n_src[rs[k]]) for k in range(len(rs))))
-        out.append(dict(N=blk.num_edges, rows=rows, U=U, dst=int(blk.n_dst.sum()),
+        out.append(dict(N=blk.num_edges, rows=rows, U=U, F=F, dst=int(blk.n_dst.sum()),
                         src=int(blk.n_src.sum()), S=S))
     return out
 
@@ -145,7 +150,7 @@ def stage_cost(stage, l, cfg, sz):
         C, B = cfg.num_classes, cfg.batch_size
         return 4 * (2 * B * D + 2 * D * C + 2 * B * C), 2 * 2 * B * D * C
     if stage == "aggregate_features":     # aggregate-first input layer: A4 over raw X
-        return 4 * K * s["U"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
+        return 4 * K * s["F"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
     if stage == "project_aggregated":
         m = s["rows"] + s["dst"]
         return 4 * K * m + 4 * D * m + 4 * (R + T) * K * D, 2 * K * D * m
@@ -204,7 +209,7 @@ def run_reference(args, cfg):
     rs = np.array([r.src for r in cfg.rels], np.int32)
     rd = np.array([r.dst for r in cfg.rels], np.int32)
     budget_s = 150.0                                   # whole timed + warm-up run
-    est_full = {"mag": 5.5, "freebase": 2.0}.get(cfg.key, 0.5)   # s per full batch (1 core)
+    est_full = {"mag": 1.5, "freebase": 0.6}.get(cfg.key, 0.2)   # s per full batch (all cores)
     frac = min(1.0, budget_s / max(1, args.steps + args.warmup) / est_full)
     seeds = max(16, int(cfg.batch_size * frac))
     frac = seeds / cfg.batch_size
@@ -213,13 +218,12 @@ def run_reference(args, cfg):
     pool = [make_batch(scfg, g, b % nb, epoch=b // nb) for b in range(max(1, min(4, args.steps + args.warmup)))]
 
     def one(mb):
-        gid = mb.gather_ids(foff)
-        fw = om.forward(mb.layers, g.edge_type, rs, rd, feat[gid].astype(np.float64),
-                        np.arange(len(gid), dtype=np.int32), params, cfg.agg, cfg.heads,
-                        labels=mb.labels, target_type=cfg.target_type)
-        om.backward(fw, mb.layers, g.edge_type, params, mb.labels, cfg.agg, cfg.heads)
+        _oracle_step(om, cfg, g, feat, foff, params, rs, rd, mb)
 
-    with threadpool_limits(1):
+    import oracle
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    with threadpool_limits(cores):
         for i in range(args.warmup):
             one(pool[i % len(pool)])
         t0 = time.perf_counter()
@@ -228,7 +232,8 @@ def run_reference(args, cfg):
         dt = time.perf_counter() - t0
     v = frac * args.steps / dt
     sample = (f"{args.steps} {cfg.key} mini-batches of {seeds} seeds (= {frac:.3f} of a "
-              f"{cfg.batch_size}-seed batch each), fwd+bwd, plain-C fp64 oracle, 1 thread")
+              f"{cfg.batch_size}-seed batch each), fwd+bwd, plain-C fp64 oracle, {cores} OpenMP "
+              f"threads ({cpu_model()})")
     conf = config_obj(cfg, args)
     conf["precision"] = "fp64 (oracle)"
     line = {"impl": "reference", "metric": "mini-batches/sec", "value": v,
@@ -236,8 +241,8 @@ def run_reference(args, cfg):
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": conf,
-            "cpu_baseline": {"value": v, "unit": "mini-batches/s", "cores": 1, "kind": "oracle",
-                             "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "mini-batches/s", "cores": cores,
+                             "kind": "oracle", "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "mini-batches/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -257,6 +262,149 @@ def config_obj(cfg, args, extra=None):
     return d
 
 
+
+# ----------------------------------------------------------- timed loop -----
+def build_graphs(tr, pool, feat_d, et_d, side, world, pipeline, allreduce=None):
+    """The graphs bench.py replays (tests/test_gpu_pipeline.py replays the same
+    ones against eager steps).  A sizing pass runs every pool batch once
+    eagerly (buffers reach their final size, update=False), then one CUDA
+    graph per pool batch is captured: `serial` (build + step of batch i) and,
+    when pipelined, `graphs` (step of batch i while a side stream builds batch
+    i+1, Trainer.capture_pipelined).  The SGD is inside the graph for N = 1;
+    for N > 1 it follows the eager all-reduce."""
+    import torch
+    from paper_2408_08490_b200 import hifuse as hf
+    for i, db in enumerate(pool):
+        db.slot = i                      # private CSR buffers per pool batch
+    for db in pool:
+        tr.step(db, feat_d, et_d, allreduce=allreduce, world=world, update=False)
+    torch.cuda.synchronize()
+    if hf.read_status(tr.status) != 0:
+        raise RuntimeError("device reported invalid edges in the batch pool")
+    serial = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
+    graphs = serial
+    if pipeline:
+        graphs = [tr.capture_pipelined(db, pool[(i + 1) % len(pool)], feat_d, et_d, side,
+                                       update=(world == 1))
+                  for i, db in enumerate(pool)]
+    return {"serial": serial, "graphs": graphs, "pipelined": bool(pipeline)}
+
+
+def prime_pipeline(tr, gset, pool, et_d):
+    """Pipelined graphs compute a batch built by the previous replay: build
+    batch 0 before the first one."""
+    import torch
+    if gset["pipelined"]:
+        tr.build_op(pool[0], et_d)()
+        torch.cuda.synchronize()
+
+
+class StepRunner:
+    """Replays the pool's graphs step by step; `timed` brackets K steps with a
+    barrier + synchronize and CUDA events (max over ranks)."""
+
+    def __init__(self, tr, gset, pool, world, dev):
+        import torch
+        self.tr, self.gset, self.pool, self.world, self.dev = tr, gset, pool, world, dev
+        self.use("pipelined" if gset["pipelined"] else "serial")
+        self.copy_stream = torch.cuda.Stream()
+        self.copy_done = [torch.cuda.Event() for _ in pool]
+        self.step_done = torch.cuda.Event()
+
+    def use(self, mode):
+        self.mode = mode
+        self.graphs = self.gset["graphs"] if mode == "pipelined" else self.gset["serial"]
+
+    def one_step(self, i, e2e=False, loss_host=None):
+        import torch
+        from paper_2408_08490_b200 import hifuse as hf
+        P, tr = len(self.pool), self.tr
+        pipelined = self.mode == "pipelined"
+        if e2e:
+            # every step copies one batch's inputs host -> device (pinned) on a
+            # copy stream, ahead of the graph that builds it, so the copy
+            # overlaps the compute of the current step; the graph waits for the
+            # copy of the batch it builds (this one if serial, the next one if
+            # pipelined).  The copied slot was last used by the previous step
+            # (waited for through step_done), so P >= 4 has no reuse hazard.
+            assert P >= 4
+            ahead = i + 2 + (1 if pipelined else 0)
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(self.step_done)
+                self.pool[ahead % P].to_device(non_blocking=True)
+                self.copy_done[ahead % P].record(self.copy_stream)
+            built = i + 1 if pipelined else i
+            torch.cuda.current_stream().wait_event(self.copy_done[built % P])
+        self.graphs[i % P][0].replay()
+        if e2e:
+            self.step_done.record()
+        if self.world > 1:
+            from paper_2408_08490_b200.dp import allreduce_grads
+            allreduce_grads(tr.grads, self.world)
+            hf.sgd(tr.params, tr.grads, tr.lr, 1.0 / self.world)
+        if e2e:
+            loss_host.copy_(tr.loss, non_blocking=True)
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(self, K, e2e=False):
+        """(ms for K steps max over ranks, t0, t1, spread over 10 chunks)."""
+        import torch
+        import torch.distributed as dist
+        loss_host = torch.empty(1, dtype=torch.float32).pin_memory() if e2e else None
+        self.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        # events also at 10 chunk boundaries (same stream, no sync): the
+        # spread of the per-step time over the run (SURVEY §8(d) protocol)
+        nchunk = 10 if K >= 10 else 1
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(nchunk - 1)]
+        bounds = [K * (c + 1) // nchunk for c in range(nchunk - 1)]
+        t0 = time.time()
+        a.record()
+        for i in range(K):
+            self.one_step(i, e2e, loss_host)
+            if i + 1 in bounds:
+                marks[bounds.index(i + 1)].record()
+        b.record()
+        b.synchronize()
+        t1 = time.time()
+        self.barrier()
+        ms = a.elapsed_time(b)
+        evs = [a] + marks + [b]
+        cuts = [0] + bounds + [K]
+        chunks = [evs[c].elapsed_time(evs[c + 1]) / (cuts[c + 1] - cuts[c])
+                  for c in range(len(evs) - 1)]
+        spread = {"chunks": nchunk, "min_ms_per_step": min(chunks),
+                  "median_ms_per_step": float(np.median(chunks)),
+                  "max_ms_per_step": max(chunks)}
+        if self.world > 1:
+            t = torch.tensor([ms], device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, t0, t1, spread
+
+    def run_e2e_losses(self, steps, et_d):
+        """Test hook: the e2e loop from a cold start (the first batches copied,
+        batch 0 built), returning the loss read back after every step."""
+        import torch
+        for j in range(min(len(self.pool), 3)):
+            self.pool[j].to_device()
+        torch.cuda.synchronize()
+        prime_pipeline(self.tr, self.gset, self.pool, et_d)
+        loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+        out = []
+        for i in range(steps):
+            self.one_step(i, True, loss_host)
+            torch.cuda.synchronize()
+            out.append(float(loss_host.item()))
+        return out
+
 # ------------------------------------------------------------------- main ---
 def main():
     ap = argparse.ArgumentParser()
@@ -266,6 +414,8 @@ def main():
     ap.add_argument("--config", default="mag", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="hifuse", choices=["hifuse", "reference"])
     ap.add_argument("--pool", type=int, default=16)
+    ap.add_argument("--repeats", type=int, default=5,
+                    help="the K-step timed region is repeated this many times; value = median")
     ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -333,117 +483,48 @@ def main():
     tr.load_params(params)
     tr.prepare_graph(et_d)           # relation-major edge ids -> R+1 offsets (once per graph)
     allreduce = (lambda t: allreduce_grads(t, world)) if world > 1 else None
-    # sizing pass: every pool batch once, eagerly (buffers reach final size)
-    for db in pool:
-        tr.step(db, feat_d, et_d, allreduce=allreduce, world=world, update=False)
-    torch.cuda.synchronize()
-    if hf.read_status(tr.status) != 0:
-        raise RuntimeError("device reported invalid edges in the batch pool")
     # one CUDA graph per pool batch: the whole step is replayed without host
     # launch overhead (all sizes are host-known, nothing syncs inside).
     # Pipelined (default, N = 1): graph i computes batch i while a side stream
     # builds the semantic graphs of batch i+1 (Fig. 6 pipeline).
-    serial_graphs = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
-    graphs = serial_graphs
     side = torch.cuda.Stream()
-    if args.pipeline:
-        graphs = [tr.capture_pipelined(db, pool[(i + 1) % len(pool)], feat_d, et_d, side,
-                                       update=(world == 1))
-                  for i, db in enumerate(pool)]
-        tr.build_op(pool[0], et_d)()       # batch 0's CSR for the first replay
-        torch.cuda.synchronize()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    copy_stream = torch.cuda.Stream()
-    copy_done = [torch.cuda.Event() for _ in pool]
-    step_done = torch.cuda.Event()
-
-    def one_step(i, e2e=False, loss_host=None):
-        P = len(pool)
-        if e2e:
-            # every step copies one batch's inputs host -> device (pinned) on a
-            # copy stream, two steps ahead of the graph that builds it, so the
-            # copy overlaps the compute of the current step; the graph waits
-            # for the copy of the batch it builds (this one if serial, the next
-            # one if pipelined).  Slots are 16 batches apart: no reuse hazard.
-            ahead = i + 2 + (0 if graphs is serial_graphs else 1)
-            with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(step_done)
-                pool[ahead % P].to_device(non_blocking=True)
-                copy_done[ahead % P].record(copy_stream)
-            built = i if graphs is serial_graphs else i + 1
-            torch.cuda.current_stream().wait_event(copy_done[built % P])
-        graphs[i % len(pool)][0].replay()
-        if e2e:
-            step_done.record()
-        if world > 1:
-            allreduce_grads(tr.grads, world)
-            hf.sgd(tr.params, tr.grads, tr.lr, 1.0 / world)
-        if e2e:
-            loss_host.copy_(tr.loss, non_blocking=True)
-
-    def timed(K, e2e=False):
-        loss_host = torch.empty(1, dtype=torch.float32).pin_memory() if e2e else None
-        barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        # events also at 10 chunk boundaries (same stream, no sync): the
-        # spread of the per-step time over the run (SURVEY §8(d) protocol)
-        nchunk = 10 if K >= 10 else 1
-        marks = [torch.cuda.Event(enable_timing=True) for _ in range(nchunk - 1)]
-        bounds = [K * (c + 1) // nchunk for c in range(nchunk - 1)]
-        t0 = time.time()
-        a.record()
-        for i in range(K):
-            one_step(i, e2e, loss_host)
-            if i + 1 in bounds:
-                marks[bounds.index(i + 1)].record()
-        b.record()
-        b.synchronize()
-        t1 = time.time()
-        barrier()
-        ms = a.elapsed_time(b)
-        evs = [a] + marks + [b]
-        cuts = [0] + bounds + [K]
-        chunks = [evs[c].elapsed_time(evs[c + 1]) / (cuts[c + 1] - cuts[c])
-                  for c in range(len(evs) - 1)]
-        timed.spread = {"chunks": nchunk, "min_ms_per_step": min(chunks),
-                        "median_ms_per_step": float(np.median(chunks)),
-                        "max_ms_per_step": max(chunks)}
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, t0, t1
+    gset = build_graphs(tr, pool, feat_d, et_d, side, world, bool(args.pipeline), allreduce)
+    prime_pipeline(tr, gset, pool, et_d)
+    runner = StepRunner(tr, gset, pool, world, dev)
 
     for i in range(args.warmup):
-        one_step(i)
+        runner.one_step(i)
     clocks = ClockSampler(local % ngpu)
     time.sleep(0.25)
-    ms, t0, t1 = timed(args.steps)
-    spread = dict(timed.spread)
-    launches = sum(graphs[i % len(pool)][1] for i in range(args.steps)) + \
+    # the K-step timed region, repeated (median reported; PAPER.md line 388:
+    # ten runs, outliers discarded)
+    reps = []
+    for _ in range(max(1, args.repeats)):
+        reps.append(runner.timed(args.steps))
+    ms_all = [r[0] for r in reps]
+    ms = float(np.median(ms_all))
+    t0, t1 = reps[0][1], reps[-1][2]
+    spread = dict(reps[int(np.argsort(ms_all)[len(ms_all) // 2])][3])
+    spread["repeats"] = len(ms_all)
+    spread["repeat_ms_per_step"] = {"median": ms / args.steps, "min": min(ms_all) / args.steps,
+                                    "max": max(ms_all) / args.steps}
+    launches = sum(runner.graphs[i % len(pool)][1] for i in range(args.steps)) + \
         (args.steps if world > 1 else 0)
     clk = clocks.summary(t0, t1)
     # the same steps without the build/compute overlap (every graph builds
     # its own batch first), for reference
-    graphs_pipe = graphs
-    graphs = serial_graphs
+    runner.use("serial")
     for i in range(args.warmup):
-        one_step(i)
-    ms_serial, _, _ = timed(args.steps)
-    graphs = graphs_pipe
-    if graphs is not serial_graphs:
-        tr.build_op(pool[0], et_d)()
+        runner.one_step(i)
+    ms_serial = runner.timed(args.steps)[0]
+    runner.use("pipelined" if gset["pipelined"] else "serial")
+    prime_pipeline(tr, gset, pool, et_d)
     # end-to-end through the public API with host (pinned) buffers
     for i in range(args.warmup):
-        one_step(i, True, torch.empty(1).pin_memory())
-    ms_e2e, _, _ = timed(args.steps, e2e=True)
+        runner.one_step(i, True, torch.empty(1).pin_memory())
+    ms_e2e = runner.timed(args.steps, e2e=True)[0]
     clocks.stop()
+    graphs, serial_graphs = runner.graphs, gset["serial"]
     # per-stage device time: every library call of the step captured as its
     # own graph and replayed back to back between CUDA events (the dominant
     # kernel's roofline below comes from these)
@@ -487,35 +568,27 @@ def main():
     other = None
     if cfg.model == "rgcn" and args.prec == "tf32":
         other_order = "project_first" if tr.agg_first else "agg_first"
-        tr_main, graphs_main, serial_main = tr, graphs, serial_graphs
-        tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
-                     cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
-                     prec=args.prec, order=other_order)
-        tr.load_params(params)
-        tr.prepare_graph(et_d)
-        for db in pool:
-            tr.step(db, feat_d, et_d, allreduce=allreduce, world=world, update=False)
-        torch.cuda.synchronize()
-        serial_graphs = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
-        graphs = serial_graphs
-        if args.pipeline:
-            graphs = [tr.capture_pipelined(db, pool[(i + 1) % len(pool)], feat_d, et_d, side,
-                                           update=(world == 1))
-                      for i, db in enumerate(pool)]
-            tr.build_op(pool[0], et_d)()
+        tr_o = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
+                       cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
+                       prec=args.prec, order=other_order)
+        tr_o.load_params(params)
+        tr_o.prepare_graph(et_d)
+        gset_o = build_graphs(tr_o, pool, feat_d, et_d, side, world, bool(args.pipeline),
+                              allreduce)
+        prime_pipeline(tr_o, gset_o, pool, et_d)
+        run_o = StepRunner(tr_o, gset_o, pool, world, dev)
         for i in range(args.warmup):
-            one_step(i)
-        ms_o, _, _ = timed(args.steps)
-        graphs_o = graphs
-        graphs = serial_graphs
+            run_o.one_step(i)
+        ms_o = float(np.median([run_o.timed(args.steps)[0] for _ in range(max(1, args.repeats))]))
+        run_o.use("serial")
         for i in range(args.warmup):
-            one_step(i)
-        ms_os, _, _ = timed(args.steps)
+            run_o.one_step(i)
+        ms_os = run_o.timed(args.steps)[0]
         other = {"order": other_order, "value": world * args.steps / (ms_o / 1e3),
                  "ms_per_step": ms_o / args.steps, "serial_ms_per_step": ms_os / args.steps,
-                 "gpu_launches_per_step": graphs_o[0][1]}
-        del graphs_o, serial_graphs, graphs
-        tr, graphs, serial_graphs = tr_main, graphs_main, serial_main
+                 "gpu_launches_per_step": gset_o["graphs"][0][1]}
+        del run_o, gset_o, tr_o
+        torch.cuda.synchronize()
         tr.load_params(params)
 
     value = world * args.steps / (ms / 1e3)
@@ -554,6 +627,11 @@ def main():
         bwd = name in ("aggregate_bwd", "project_bwd", "fuse_bwd", "project_aggregated_bwd",
                        "project_wgrad")
         mk = MAIN_KERNEL.get(name, name)
+        if name == "aggregate_bwd" and cfg.agg.startswith("gat"):
+            mk = "k_agg_bwd_gat_cols_half" if cfg.hidden == 64 else "k_agg_bwd_gat_cols"
+        if name == "aggregate_fwd" and cfg.agg.startswith("gat"):
+            mk = ("k_agg_fwd_gat_xrel" if cfg.agg == "gat_xrel" else
+                  "k_agg_fwd_gat_half" if cfg.hidden == 64 else "k_agg_fwd_gat")
         if name == "project_bwd" and cfg.model == "rgcn":
             mk = "k_dgrad_tc"                 # input gradient only (weights: project_wgrad)
         tr = None if name == "build" else ncu_traffic(mk,
@@ -771,22 +849,46 @@ def hf_status_ok(st):
     return hf.read_status(st) == 0
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_step(om, cfg, g, feat, foff, params, rs, rd, mb):
+    gid = mb.gather_ids(foff)
+    fw = om.forward(mb.layers, g.edge_type, rs, rd, feat[gid].astype(np.float64),
+                    np.arange(len(gid), dtype=np.int32), params, cfg.agg, cfg.heads,
+                    labels=mb.labels, target_type=cfg.target_type)
+    om.backward(fw, mb.layers, g.edge_type, params, mb.labels, cfg.agg, cfg.heads)
+
+
 def cpu_baseline(cfg, g, feat, foff, params, rs, rd, mbs):
-    """The oracle, as it stands, on a bounded sample of the same workload."""
+    """The oracle, as it stands, on a bounded sample of the same workload: at
+    all of the host's cores (its OpenMP loops; the reported value) and at 1
+    thread."""
+    import oracle
     import oracle.model as om
     from threadpoolctl import threadpool_limits
     n = 2 if cfg.key == "mag" else 8
-    with threadpool_limits(1):
-        t0 = time.perf_counter()
-        for mb in mbs[:n]:
-            gid = mb.gather_ids(foff)
-            fw = om.forward(mb.layers, g.edge_type, rs, rd, feat[gid].astype(np.float64),
-                            np.arange(len(gid), dtype=np.int32), params, cfg.agg, cfg.heads,
-                            labels=mb.labels, target_type=cfg.target_type)
-            om.backward(fw, mb.layers, g.edge_type, params, mb.labels, cfg.agg, cfg.heads)
-        dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "mini-batches/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} {cfg.key} mini-batches (fwd+bwd, plain-C fp64 oracle, 1 thread)"}
+    cores = os.cpu_count() or 1
+    res = {}
+    for threads in (cores, 1):
+        oracle.set_threads(threads)
+        with threadpool_limits(threads):
+            t0 = time.perf_counter()
+            for mb in mbs[:n]:
+                _oracle_step(om, cfg, g, feat, foff, params, rs, rd, mb)
+            res[threads] = n / (time.perf_counter() - t0)
+    oracle.set_threads(1)
+    return {"value": res[cores], "unit": "mini-batches/s", "cores": cores, "kind": "oracle",
+            "value_1_thread": res[1], "cpu_model": cpu_model(),
+            "sample": f"{n} {cfg.key} mini-batches (fwd+bwd, plain-C fp64 oracle, {cores} "
+                      f"OpenMP threads = the host's cores; value_1_thread at 1 thread)"}
 
 
 if __name__ == "__main__":

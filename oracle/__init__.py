@@ -29,7 +29,7 @@ AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3}
 
 def build_lib(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC",
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-fopenmp", "-shared", "-fPIC",
                                "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
@@ -42,7 +42,18 @@ def lib():
     if _lib is None:
         _lib = ctypes.CDLL(build_lib())
         _lib.oracle_build.restype = ctypes.c_int
+        _lib.oracle_set_threads(1)
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's parallel loops (results are bit-identical
+    for any count: single writer per output, serial summation order)."""
+    lib().oracle_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())
 
 
 def _p(a):

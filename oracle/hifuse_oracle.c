@@ -12,11 +12,39 @@
  *
  * Pins: tests/test_oracle_*.py (brute-force dense adjacency, library special
  * cases, hand examples from SPEC.md, finite differences, adjoint identities).
+ *
+ * Threads (OpenMP, oracle_set_threads; default 1): only loops whose
+ * iterations write disjoint outputs run in parallel, and every output element
+ * is accumulated in the same order as the serial loop, so results are
+ * bit-identical for any thread count (tests/test_oracle_threads.py).
  */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <stdio.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* number of OpenMP threads of the parallel loops below (1: serial) */
+void oracle_set_threads(int n)
+{
+#ifdef _OPENMP
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
+#endif
+}
+
+int oracle_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
 
 #define ST_BAD_EDGE_ID 1   /* edge_id >= E_graph or < 0            */
 #define ST_BAD_REL     2   /* edge_type[edge_id] not in [0, R)     */
@@ -161,6 +189,7 @@ void oracle_project(int T, int R, const int32_t *rel_src, const int32_t *rel_dst
     /* Y[(r,j)] = X_{s(r)}[j] . W_r */
     for (int r = 0; r < R; r++) {
         const double *W = W_rel + (int64_t)r * K * D;
+        #pragma omp parallel for schedule(static)
         for (int32_t u = rel_y_off[r]; u < rel_y_off[r + 1]; u++) {
             const double *x = xrow(X, K, gather_ids, tso, rel_src[r], y_src[u]);
             double *y = Y + (int64_t)u * D;
@@ -181,6 +210,7 @@ void oracle_project(int T, int R, const int32_t *rel_src, const int32_t *rel_dst
     if (W_root) {
         for (int t = 0; t < T; t++) {
             const double *W = W_root + (int64_t)t * K * D;
+            #pragma omp parallel for schedule(static)
             for (int32_t i = 0; i < n_dst[t]; i++) {
                 const double *x = xrow(X, K, gather_ids, tso, t, i);
                 double *o = R0 + (tdo[t] + i) * (int64_t)D;
@@ -192,25 +222,31 @@ void oracle_project(int T, int R, const int32_t *rel_src, const int32_t *rel_dst
     }
     /* s_dst[(r,i),h] = <(X_{t(r)}[i] W_r)[head h], a_dst^{r,h}>  (reading C7) */
     if (att) {
-        int64_t row = 0;
-        double *hv = (double *)malloc(sizeof(double) * D);
+        int64_t row0 = 0;
         for (int r = 0; r < R; r++) {
             const double *W = W_rel + (int64_t)r * K * D;
             const double *a_dst = att + (int64_t)r * 2 * D + D;
             int t = rel_dst[r];
-            for (int32_t i = 0; i < n_dst[t]; i++, row++) {
-                const double *x = xrow(X, K, gather_ids, tso, t, i);
-                for (int d = 0; d < D; d++) hv[d] = 0.0;
-                for (int k = 0; k < K; k++)
-                    for (int d = 0; d < D; d++) hv[d] += x[k] * W[(int64_t)k * D + d];
-                for (int h = 0; h < H; h++) {
-                    double s = 0.0;
-                    for (int c = 0; c < dh; c++) s += hv[h * dh + c] * a_dst[h * dh + c];
-                    s_dst[row * H + h] = s;
+            #pragma omp parallel
+            {
+                double *hv = (double *)malloc(sizeof(double) * D);
+                #pragma omp for schedule(static)
+                for (int32_t i = 0; i < n_dst[t]; i++) {
+                    int64_t row = row0 + i;
+                    const double *x = xrow(X, K, gather_ids, tso, t, i);
+                    for (int d = 0; d < D; d++) hv[d] = 0.0;
+                    for (int k = 0; k < K; k++)
+                        for (int d = 0; d < D; d++) hv[d] += x[k] * W[(int64_t)k * D + d];
+                    for (int h = 0; h < H; h++) {
+                        double s = 0.0;
+                        for (int c = 0; c < dh; c++) s += hv[h * dh + c] * a_dst[h * dh + c];
+                        s_dst[row * H + h] = s;
+                    }
                 }
+                free(hv);
             }
+            row0 += n_dst[t];
         }
-        free(hv);
     }
     free(tso); free(tdo);
 }
@@ -233,7 +269,11 @@ static int32_t yrow_of(const int32_t *rel_y_off, const int32_t *y_src, int r, in
         int32_t mid = lo + (hi - lo) / 2;
         if (y_src[mid] < j) lo = mid + 1; else hi = mid;
     }
-    return (lo < rel_y_off[r + 1] && y_src[lo] == j) ? lo : -1;
+    if (lo < rel_y_off[r + 1] && y_src[lo] == j) return lo;
+    /* a valid edge whose source is missing from y_src: the caller passed an
+     * inconsistent (rel_y_off, y_src); fail loudly, never index Y[-1] */
+    fprintf(stderr, "oracle: yrow_of: source %d of relation %d not in y_src\n", (int)j, r);
+    abort();
 }
 
 static int valid_edge(int R, const int32_t *rel_src, const int32_t *rel_dst,
@@ -638,83 +678,129 @@ void oracle_project_bwd(int T, int R, const int32_t *rel_src, const int32_t *rel
     if (dW_root) memset(dW_root, 0, sizeof(double) * T * K * D);
     if (datt) memset(datt, 0, sizeof(double) * R * 2 * D);
     if (dX) memset(dX, 0, sizeof(double) * x_rows * K);
-    double *dyt = (double *)malloc(sizeof(double) * D);
     for (int r = 0; r < R; r++) {
         const double *W = W_rel + (int64_t)r * K * D;
         double *dW = dW_rel + (int64_t)r * K * D;
         const double *a_src = att ? att + (int64_t)r * 2 * D : NULL;
-        for (int32_t u = rel_y_off[r]; u < rel_y_off[r + 1]; u++) {
-            int64_t xr = tso[rel_src[r]] + y_src[u];
-            if (gather_ids) xr = gather_ids[xr];
-            const double *x = X + xr * K;
-            for (int d = 0; d < D; d++) dyt[d] = dY[(int64_t)u * D + d];
+        int32_t u0 = rel_y_off[r], nu = rel_y_off[r + 1] - rel_y_off[r];
+        /* dYt[u] = dY[u] + ds_src[u,h] a_src^{r,h} (the s_src term of O2) */
+        double *dyt = (double *)malloc(sizeof(double) * D * (nu > 0 ? nu : 1));
+        for (int32_t q = 0; q < nu; q++) {
+            int32_t u = u0 + q;
+            for (int d = 0; d < D; d++) dyt[(int64_t)q * D + d] = dY[(int64_t)u * D + d];
             if (att)
                 for (int h = 0; h < H; h++)
                     for (int c = 0; c < dh; c++) {
-                        dyt[h * dh + c] += ds_src[(int64_t)u * H + h] * a_src[h * dh + c];
+                        dyt[(int64_t)q * D + h * dh + c] += ds_src[(int64_t)u * H + h] * a_src[h * dh + c];
                         datt[(int64_t)r * 2 * D + h * dh + c] += ds_src[(int64_t)u * H + h] * Y[(int64_t)u * D + h * dh + c];
                     }
-            for (int k = 0; k < K; k++)
-                for (int d = 0; d < D; d++) dW[(int64_t)k * D + d] += x[k] * dyt[d];
-            if (dX)
+        }
+        /* dW_r[k,:] = sum_u X[src u, k] dYt[u]  (u ascending, row k per thread) */
+        #pragma omp parallel for schedule(static)
+        for (int k = 0; k < K; k++)
+            for (int32_t q = 0; q < nu; q++) {
+                int64_t xr = tso[rel_src[r]] + y_src[u0 + q];
+                if (gather_ids) xr = gather_ids[xr];
+                double xk = X[xr * K + k];
+                for (int d = 0; d < D; d++) dW[(int64_t)k * D + d] += xk * dyt[(int64_t)q * D + d];
+            }
+        /* dX[src u] += dYt[u] W_r^T  (distinct sources within relation r) */
+        if (dX) {
+            #pragma omp parallel for schedule(static)
+            for (int32_t q = 0; q < nu; q++) {
+                int64_t xr = tso[rel_src[r]] + y_src[u0 + q];
+                if (gather_ids) xr = gather_ids[xr];
                 for (int k = 0; k < K; k++) {
                     double acc = 0.0;
-                    for (int d = 0; d < D; d++) acc += dyt[d] * W[(int64_t)k * D + d];
+                    for (int d = 0; d < D; d++) acc += dyt[(int64_t)q * D + d] * W[(int64_t)k * D + d];
                     dX[xr * K + k] += acc;
                 }
+            }
         }
+        free(dyt);
     }
     if (W_root) {
         for (int t = 0; t < T; t++) {
             const double *W = W_root + (int64_t)t * K * D;
             double *dW = dW_root + (int64_t)t * K * D;
-            for (int32_t i = 0; i < n_dst[t]; i++) {
-                int64_t xr = tso[t] + i;
-                if (gather_ids) xr = gather_ids[xr];
-                const double *x = X + xr * K;
-                const double *g = G + (tdo[t] + i) * D;
-                for (int k = 0; k < K; k++)
-                    for (int d = 0; d < D; d++) dW[(int64_t)k * D + d] += x[k] * g[d];
-                if (dX)
+            /* dW_root,t[k,:] = sum_i X_t[i, k] G_t[i] */
+            #pragma omp parallel for schedule(static)
+            for (int k = 0; k < K; k++)
+                for (int32_t i = 0; i < n_dst[t]; i++) {
+                    int64_t xr = tso[t] + i;
+                    if (gather_ids) xr = gather_ids[xr];
+                    const double *g = G + (tdo[t] + i) * D;
+                    double xk = X[xr * K + k];
+                    for (int d = 0; d < D; d++) dW[(int64_t)k * D + d] += xk * g[d];
+                }
+            if (dX) {
+                #pragma omp parallel for schedule(static)
+                for (int32_t i = 0; i < n_dst[t]; i++) {
+                    int64_t xr = tso[t] + i;
+                    if (gather_ids) xr = gather_ids[xr];
+                    const double *g = G + (tdo[t] + i) * D;
                     for (int k = 0; k < K; k++) {
                         double acc = 0.0;
                         for (int d = 0; d < D; d++) acc += g[d] * W[(int64_t)k * D + d];
                         dX[xr * K + k] += acc;
                     }
+                }
             }
         }
     }
     if (att) {
-        int64_t row = 0;
-        double *hv = (double *)malloc(sizeof(double) * D);
+        int64_t row0 = 0;
         for (int r = 0; r < R; r++) {
             const double *W = W_rel + (int64_t)r * K * D;
             double *dW = dW_rel + (int64_t)r * K * D;
             const double *a_dst = att + (int64_t)r * 2 * D + D;
             int t = rel_dst[r];
-            for (int32_t i = 0; i < n_dst[t]; i++, row++) {
+            int32_t nt = n_dst[t];
+            /* s_dst = sum_c (x W_r)[hc] a_dst[hc]  =>  d/d(xW)[hc] = ds_dst[h] a_dst[hc];
+             * gd[i, d] = ds_dst[(r,i), h(d)] a_dst[d] */
+            double *gd = (double *)malloc(sizeof(double) * D * (nt > 0 ? nt : 1));
+            for (int32_t i = 0; i < nt; i++)
+                for (int h = 0; h < H; h++)
+                    for (int c = 0; c < dh; c++)
+                        gd[(int64_t)i * D + h * dh + c] = ds_dst[(row0 + i) * H + h] * a_dst[h * dh + c];
+            /* datt_dst[d] += ds_dst[h(d)] (x W_r)[d], i ascending */
+            double *hv = (double *)malloc(sizeof(double) * D);
+            for (int32_t i = 0; i < nt; i++) {
                 int64_t xr = tso[t] + i;
                 if (gather_ids) xr = gather_ids[xr];
                 const double *x = X + xr * K;
-                /* s_dst = sum_c (x W_r)[hc] a_dst[hc]  =>  d/d(xW)[hc] = ds_dst[h] a_dst[hc] */
                 for (int d = 0; d < D; d++) hv[d] = 0.0;
                 for (int k = 0; k < K; k++)
                     for (int d = 0; d < D; d++) hv[d] += x[k] * W[(int64_t)k * D + d];
-                for (int h = 0; h < H; h++) {
-                    double g = ds_dst[row * H + h];
-                    for (int c = 0; c < dh; c++) {
-                        int d = h * dh + c;
-                        datt[(int64_t)r * 2 * D + D + d] += g * hv[d];
-                        for (int k = 0; k < K; k++) dW[(int64_t)k * D + d] += x[k] * g * a_dst[d];
-                        if (dX)
-                            for (int k = 0; k < K; k++) dX[xr * K + k] += g * a_dst[d] * W[(int64_t)k * D + d];
-                    }
+                for (int h = 0; h < H; h++)
+                    for (int c = 0; c < dh; c++)
+                        datt[(int64_t)r * 2 * D + D + h * dh + c] += ds_dst[(row0 + i) * H + h] * hv[h * dh + c];
+            }
+            free(hv);
+            /* dW_r[k, d] += x_i[k] gd[i, d], i ascending */
+            #pragma omp parallel for schedule(static)
+            for (int k = 0; k < K; k++)
+                for (int32_t i = 0; i < nt; i++) {
+                    int64_t xr = tso[t] + i;
+                    if (gather_ids) xr = gather_ids[xr];
+                    double xk = X[xr * K + k];
+                    for (int d = 0; d < D; d++) dW[(int64_t)k * D + d] += xk * gd[(int64_t)i * D + d];
+                }
+            if (dX) {
+                #pragma omp parallel for schedule(static)
+                for (int32_t i = 0; i < nt; i++) {
+                    int64_t xr = tso[t] + i;
+                    if (gather_ids) xr = gather_ids[xr];
+                    for (int k = 0; k < K; k++)
+                        for (int d = 0; d < D; d++)
+                            dX[xr * K + k] += gd[(int64_t)i * D + d] * W[(int64_t)k * D + d];
                 }
             }
+            free(gd);
+            row0 += nt;
         }
-        free(hv);
     }
-    free(dyt); free(tso); free(tdo);
+    free(tso); free(tdo);
 }
 
 /* ------------------------------------------------------------------------ */
