@@ -25,8 +25,13 @@
  *
  * Conventions:
  *  - Pointers named d_* are device memory; *_h are host memory.  The caller
- *    owns every buffer, including workspace; the library never allocates on
- *    the hot path and keeps no global state except cached device attributes.
+ *    owns every buffer, including workspace; the library never allocates
+ *    device memory.  Its only state: cached device attributes (SM count,
+ *    per-kernel shared-memory opt-in) and, per (device, caller stream), the
+ *    auxiliary streams + events that fork a call's independent kernels into
+ *    parallel branches (see hifuse_stream_attach).  Calls on different
+ *    streams share none of it; calls on one stream must come from one host
+ *    thread at a time (as stream order already requires).
  *  - Every call is asynchronous and stream-ordered on `stream`; no call
  *    synchronises the device (except hifuse_read_status, for tests).  All
  *    sizes a launch needs are host-known from hifuse_layer_shape, so a whole
@@ -70,6 +75,7 @@ typedef enum {
 #define HIFUSE_ST_BAD_SRC     4   /* src_local >= n_src(src type of relation)   */
 #define HIFUSE_ST_BAD_DST     8   /* dst_local >= n_dst(dst type of relation)   */
 #define HIFUSE_ST_UNSORTED_TYPES 16 /* edge_type not relation-major (offsets unusable) */
+#define HIFUSE_ST_BAD_LABEL   32  /* class label outside [0, C) (hifuse_linear_xent) */
 
 /* GAT_XREL: GAT with the edge-softmax across the relations of a destination
  * (hifuse_aggregate_fwd_xrel, reading C5'). */
@@ -148,9 +154,10 @@ hifuse_status hifuse_csr_sizes(const hifuse_layer_shape *shape, hifuse_layout la
  *     evaluated by a binary search over the R+1 offsets instead of a random
  *     4-byte gather from the graph-sized table (same result); build the
  *     offsets once per graph with hifuse_edge_type_offsets().
- * Workspace: d_ws of at least max_l build_ws_bytes(l).  d_status: int32 [1],
- * bits ORed (never cleared by the library).  Layers run back to back on
- * `stream`; kernel count is independent of R. */
+ * Workspace: d_ws of at least sum_l build_ws_bytes(l) (the layers are built
+ * together); no initial contents required.  d_status: int32 [1], bits ORed
+ * (never cleared by the library).  Launches: one memset + five kernels for
+ * up to 4 layers (build.cu), independent of R and of the layer count. */
 hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape *shapes, int num_layers,
                                            const int32_t *const *d_src_local,
                                            const int32_t *const *d_dst_local,
@@ -357,9 +364,11 @@ size_t hifuse_xent_ws_bytes(int B, int D, int C);
 hifuse_status hifuse_linear_xent(int B, int D, int C, const float *d_H, int64_t h_rows,
                                  int64_t h_row0, const int32_t *d_labels, const float *d_Wc,
                                  const float *d_bc, float *d_loss, float *d_dH, float *d_dWc,
-                                 float *d_dbc, void *d_ws, size_t ws_bytes,
+                                 float *d_dbc, void *d_ws, size_t ws_bytes, int32_t *d_status,
                                  hifuse_stream_t stream);
-/* dWc = Hs^T dlog, dbc = column sums of dlog from the dlog a preceding
+/* d_status (nullable): a label outside [0, C) ORs HIFUSE_ST_BAD_LABEL; that
+ * row contributes no loss and no gradient (the loss is still divided by B).
+ * dWc = Hs^T dlog, dbc = column sums of dlog from the dlog a preceding
  * hifuse_linear_xent (d_dWc = NULL) left in d_ws. */
 hifuse_status hifuse_linear_xent_wgrad(int B, int D, int C, const float *d_H, int64_t h_rows,
                                        int64_t h_row0, float *d_dWc, float *d_dbc, void *d_ws,
@@ -443,6 +452,22 @@ hifuse_status hifuse_sample_blocks(const hifuse_graph_csc *g, int num_layers,
                                    int32_t *d_state,
                                    void *d_ws, size_t ws_bytes, int32_t *d_status,
                                    hifuse_stream_t stream);
+
+/* Per-stream fork/join resources (common.cu).  A call that runs independent
+ * kernels concurrently (the dgrad || wgrad of hifuse_project_bwd, the two
+ * RGAT attention chains, the RGAT destination scores || the projection)
+ * forks them onto auxiliary streams owned by the caller's stream `stream`
+ * (created on first use; under CUDA-graph capture the fork becomes a parallel
+ * graph branch).  hifuse_stream_attach creates them ahead of time -- call it
+ * outside capture for every stream that will later be captured;
+ * HIFUSE_ERR_INVALID_ARG if `stream` is capturing.  hifuse_stream_release
+ * destroys them (synchronises the auxiliary streams; the caller guarantees no
+ * call on `stream` is in flight or later replayed from a graph).  If the
+ * resources cannot be created, branches run serially on `stream`.  No
+ * arithmetic; PAPER.md has no counterpart (a B200 scheduling detail, DESIGN
+ * §9 "Backward off the critical path"). */
+hifuse_status hifuse_stream_attach(hifuse_stream_t stream);
+hifuse_status hifuse_stream_release(hifuse_stream_t stream);
 
 /* Tests / debugging: copies *d_status to *out_h and synchronises `stream`. */
 hifuse_status hifuse_read_status(const int32_t *d_status, hifuse_stream_t stream, int32_t *out_h);

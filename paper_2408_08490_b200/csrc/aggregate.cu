@@ -439,15 +439,55 @@ k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __res
   for (int v = 0; v < V; v++) o[v * kLPC] = acc[v];
 }
 
-// Pre-scaled gradient rows: Gs[m] = w(m) G[g(m)] for every merged row m =
-// (r, i), w = 1 (sum) or 1/|row m| (mean); one pass over rho x D.  The CSC
-// gather then needs no relation shift and no degree lookup per entry.
+// Transpose SpMM of the sum / mean aggregation (the adjoint of Alg. 1):
+//   dY[u] = sum_{p in CSC column u} w(m_p) G[g(m_p)],  m_p = csc_row[p],
+// g(m) = m + shift[r(m)] the type-major G row of merged row m = (r, i), w = 1
+// (sum) or 1 / |row m| (mean, reading C19: the product w*g is rounded, then
+// summed, as an fp32 multiply followed by an add).  No pre-scaled copy of G:
+// the lane that loads csc_row[p] resolves (g(m), w) -- relation by binary
+// search over rel_row_off in shared memory, degree from row_ptr -- and
+// broadcasts them to the 8 lanes that gather the row.
+struct EntryRW {
+  int g;       // G row (-1: none)
+  float w;
+};
+
+template <bool MEAN>
+__device__ __forceinline__ EntryRW entry_rw(int m, const int* s_roff, const int* s_shift, int R,
+                                            const int* __restrict__ row_ptr) {
+  EntryRW e{-1, 0.f};
+  if (m < 0) return e;
+  int lo = 0, hi = R;                        // s_roff[lo] <= m < s_roff[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_roff[mid] <= m) lo = mid; else hi = mid;
+  }
+  e.g = m + s_shift[lo];
+  e.w = 1.f;
+  if (MEAN) {
+    const int dg = __ldg(row_ptr + m + 1) - __ldg(row_ptr + m);
+    e.w = 1.f / (float)dg;                   // dg >= 1: m holds the entry
+  }
+  return e;
+}
+
+__device__ __forceinline__ float4 f4mul_add(float w, float4 x, float4 a, bool mean) {
+  if (!mean) return f4add(a, x);
+  return make_float4(__fadd_rn(a.x, __fmul_rn(w, x.x)), __fadd_rn(a.y, __fmul_rn(w, x.y)),
+                     __fadd_rn(a.z, __fmul_rn(w, x.z)), __fadd_rn(a.w, __fmul_rn(w, x.w)));
+}
+
+// Persistent CSC gather: 8 lanes per column, 4 columns per warp, grid-stride
+// over column groups.  Software pipeline per iteration: col_ptr of group i+2,
+// the first 8 (g, w) entries of group i+1 and the G rows of group i are in
+// flight together.
 template <int D, bool MEAN>
-__global__ void __launch_bounds__(256)
-k_scale_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, int rows,
-             const int* __restrict__ row_ptr, const float4* __restrict__ G,
-             float4* __restrict__ Gs) {
-  constexpr int LPR = D / 4;
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
+k_agg_bwd_p(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __restrict__ row_ptr,
+            int U_max, const int* __restrict__ U_dev, const int* __restrict__ col_ptr,
+            const int* __restrict__ csc_row, const float4* __restrict__ G,
+            float4* __restrict__ dY, int* __restrict__ long_list, int* __restrict__ long_cnt) {
+  constexpr int LPR = D / 4, LPC = 8, V = LPR / LPC, CPW = 32 / LPC;
   __shared__ int s_roff[HF_MAX_R + 1];
   __shared__ int s_shift[HF_MAX_R];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) {
@@ -455,31 +495,6 @@ k_scale_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, int rows,
     if (i < bm.R) s_shift[i] = bm.shift[i];
   }
   __syncthreads();
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)rows * LPR) return;
-  const int m = (int)(idx / LPR), c = (int)(idx % LPR);
-  const int r = upper_bound_i(s_roff, bm.R + 1, m) - 1;
-  float w = 1.f;
-  if (MEAN) {
-    const int dg = row_ptr[m + 1] - row_ptr[m];
-    w = dg > 0 ? 1.f / (float)dg : 0.f;
-  }
-  const float4 g = __ldg(G + (long long)(m + s_shift[r]) * LPR + c);
-  Gs[idx] = make_float4(w * g.x, w * g.y, w * g.z, w * g.w);
-}
-
-// Persistent CSC gather over the pre-scaled rows: 8 lanes per column, 4
-// columns per warp, grid-stride over column groups.  Three-stage software
-// pipeline per iteration: col_ptr of group i+2, the first 8 csc_row entries
-// of group i+1 and the Gs rows of group i are all in flight together, so an
-// iteration costs ~one memory round trip instead of three.
-// dY[u] = sum_{p in column u} Gs[csc_row[p]].
-template <int D>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
-k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ col_ptr,
-            const int* __restrict__ csc_row, const float4* __restrict__ Gs,
-            float4* __restrict__ dY, int* __restrict__ long_list, int* __restrict__ long_cnt) {
-  constexpr int LPR = D / 4, LPC = 8, V = LPR / LPC, CPW = 32 / LPC;
   const int lane = threadIdx.x & 31, j = lane % LPC, grp = lane / LPC;
   const int gbase = lane & ~(LPC - 1);
   const int U = *U_dev;
@@ -499,7 +514,6 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
   bounds(cg0 + nw, &b1, &e1);
   int row0 = first_row(b0, e0);
   for (int cg = cg0; cg * CPW < U; cg += nw) {
-    // stage loads for the next iterations
     int b2, e2;
     bounds(cg + 2 * nw, &b2, &e2);
     const int row1 = first_row(b1, e1);
@@ -521,20 +535,25 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
         const int p = b0 + rd * LPC + j;
         my_row = p < e ? __ldg(csc_row + p) : -1;
       }
+      const EntryRW me = entry_rw<MEAN>(my_row, s_roff, s_shift, bm.R, row_ptr);
 #pragma unroll
       for (int q0 = 0; q0 < LPC; q0 += 4) {
         float4 x[4][V];
+        float wq[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-          const int rq = __shfl_sync(0xffffffffu, my_row, gbase + q0 + q);
-          const float4* g = Gs + (long long)(rq < 0 ? 0 : rq) * LPR + j;
+          const int gq = __shfl_sync(0xffffffffu, me.g, gbase + q0 + q);
+          wq[q] = __shfl_sync(0xffffffffu, me.w, gbase + q0 + q);
+          const float4* g = G + (long long)(gq < 0 ? 0 : gq) * LPR + j;
 #pragma unroll
-          for (int v = 0; v < V; v++) x[q][v] = rq >= 0 ? ldg4(g + v * LPC) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int v = 0; v < V; v++)
+            x[q][v] = gq >= 0 ? ldg4(g + v * LPC) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gq < 0) wq[q] = 0.f;
         }
 #pragma unroll
         for (int q = 0; q < 4; q++)
 #pragma unroll
-          for (int v = 0; v < V; v++) acc[v] = f4add(acc[v], x[q][v]);
+          for (int v = 0; v < V; v++) acc[v] = f4mul_add(wq[q], x[q][v], acc[v], MEAN);
       }
     }
     if (!skip) {
@@ -547,17 +566,26 @@ k_agg_bwd_p(int U_max, const int* __restrict__ U_dev, const int* __restrict__ co
   }
 }
 
-// Long columns over the pre-scaled rows (kPLongWarps warps per column,
-// fixed-order combine of the warp slices).
-template <int D>
+// Long columns (kPLongWarps warps per column, fixed-order combine of the
+// warp slices).
+template <int D, bool MEAN>
 __global__ void __launch_bounds__(kPLongWarps * 32)
-k_agg_bwd_p_long(const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
-                 const float4* __restrict__ Gs, float4* __restrict__ dY,
-                 const int* __restrict__ list, const int* __restrict__ cnt) {
+k_agg_bwd_p_long(BwdMeta bm, const int* __restrict__ rel_row_off_d,
+                 const int* __restrict__ row_ptr, const int* __restrict__ col_ptr,
+                 const int* __restrict__ csc_row, const float4* __restrict__ G,
+                 float4* __restrict__ dY, const int* __restrict__ list,
+                 const int* __restrict__ cnt) {
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
-  constexpr int G = 8;                                   // gathers in flight per stream
+  constexpr int GF = 8;                                   // gathers in flight per stream
   __shared__ float4 red[kPLongWarps][LPR];
+  __shared__ int s_roff[HF_MAX_R + 1];
+  __shared__ int s_shift[HF_MAX_R];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) {
+    s_roff[i] = rel_row_off_d[i];
+    if (i < bm.R) s_shift[i] = bm.shift[i];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int sl = lane % LPR, sid = lane / LPR;
   const int n_long = *cnt;
@@ -569,17 +597,20 @@ k_agg_bwd_p_long(const int* __restrict__ col_ptr, const int* __restrict__ csc_ro
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int base = wb; base < we; base += 32) {
       const int n = min(32, we - base);
-      const int my_row = lane < n ? __ldg(csc_row + base + lane) : 0;
-      for (int kk = 0; kk < n; kk += NS * G) {
-        float4 x[G];
+      const EntryRW me = entry_rw<MEAN>(lane < n ? __ldg(csc_row + base + lane) : -1, s_roff,
+                                        s_shift, bm.R, row_ptr);
+      for (int kk = 0; kk < n; kk += NS * GF) {
+        float4 x[GF];
+        float wq[GF];
 #pragma unroll
-        for (int q = 0; q < G; q++) {
+        for (int q = 0; q < GF; q++) {
           const int idx = kk + q * NS + sid;
-          const int rr = __shfl_sync(0xffffffffu, my_row, idx < n ? idx : 0);
-          x[q] = idx < n ? ldg4(Gs + (long long)rr * LPR + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const int gq = __shfl_sync(0xffffffffu, me.g, idx < n ? idx : 0);
+          wq[q] = idx < n ? __shfl_sync(0xffffffffu, me.w, idx < n ? idx : 0) : 0.f;
+          x[q] = idx < n ? ldg4(G + (long long)gq * LPR + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int q = 0; q < G; q++) acc = f4add(acc, x[q]);
+        for (int q = 0; q < GF; q++) acc = f4mul_add(wq[q], x[q], acc, MEAN);
       }
     }
 #pragma unroll
@@ -1356,7 +1387,6 @@ size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg
   size_t b = carve_bytes(U_max + 1, 4) + carve_bytes(2, 4);
   if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL)
     b += 2 * carve_bytes((long long)m.N * heads, 4);
-  else b += carve_bytes((long long)(m.rows > 0 ? m.rows : 1) * 128, 4);   // pre-scaled rows
   return b;
 }
 
@@ -1376,6 +1406,19 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   if (!aligned16(d_G) || !aligned16(d_dY)) return HIFUSE_ERR_ALIGNMENT;
   if (ws_bytes < hifuse_aggregate_bwd_ws_bytes(shape, agg, heads) || !d_ws)
     return HIFUSE_ERR_WORKSPACE;
+  // every host-side check before the first enqueue (an invalid call launches nothing)
+  const bool gat = agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL;
+  if (gat) {
+    if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
+    if (!d_Y || !d_s_src || !d_s_dst || !d_stats || !d_ds_src || !d_ds_dst || !csr->csc_pos ||
+        !csr->row_ptr || !csr->col || !csr->rel_row_off)
+      return HIFUSE_ERR_INVALID_ARG;
+  } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
+    if ((agg == HIFUSE_AGG_MEAN && !csr->row_ptr) || !csr->rel_row_off)
+      return HIFUSE_ERR_INVALID_ARG;
+  } else {
+    return HIFUSE_ERR_INVALID_ARG;
+  }
   cudaStream_t s = st(stream);
   BwdMeta bm;
   bm.R = m.R;
@@ -1389,11 +1432,7 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   unsigned gridU4 = ceil_div(U_max, kWarpsPerBlock * (32 / kLPC));
   const int TB = kWarpsPerBlock * 32;
   const unsigned gridL = 296;
-  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL) {
-    if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
-    if (!d_Y || !d_s_src || !d_s_dst || !d_stats || !d_ds_src || !d_ds_dst || !csr->csc_pos ||
-        !csr->row_ptr || !csr->col || !csr->rel_row_off)
-      return HIFUSE_ERR_INVALID_ARG;
+  if (gat) {
     float* alpha = carve<float>(p, (long long)m.N * heads);
     float* dpre = carve<float>(p, (long long)m.N * heads);
     unsigned gridR = ceil_div(m.rows, kWarpsPerBlock);
@@ -1426,23 +1465,18 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
             (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att)
     if (D == 128) { HF_GAT(128); } else { HF_GAT(64); }
 #undef HF_GAT
-  } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
-    if (agg == HIFUSE_AGG_MEAN && !csr->row_ptr) return HIFUSE_ERR_INVALID_ARG;
+  } else {
 #define HF_BWD(DD, MM)                                                                        \
-  HF_LAUNCH((k_scale_rows<DD, MM>), ceil_div((long long)m.rows * (DD / 4), 256), 256, 0, s, bm,  \
-            csr->rel_row_off, m.rows, csr->row_ptr, (const float4*)d_G, (float4*)Gs);           \
-  HF_LAUNCH((k_agg_bwd_p<DD>), 148 * 4, TB, 0, s, (int)U_max, csr->U_dev, csr->col_ptr,           \
-            csr->csc_row, (const float4*)Gs, (float4*)d_dY, long_list, long_cnt);               \
-  HF_LAUNCH((k_agg_bwd_p_long<DD>), 148 * 8, kPLongWarps * 32, 0, s, csr->col_ptr, csr->csc_row,    \
-            (const float4*)Gs, (float4*)d_dY, long_list, long_cnt)
-    if (!csr->rel_row_off) return HIFUSE_ERR_INVALID_ARG;
-    float* Gs = carve<float>(p, (long long)(m.rows > 0 ? m.rows : 1) * 128);
+  HF_LAUNCH((k_agg_bwd_p<DD, MM>), sm_count() * 4, TB, 0, s, bm, csr->rel_row_off, csr->row_ptr, \
+            (int)U_max, csr->U_dev, csr->col_ptr, csr->csc_row, (const float4*)d_G,             \
+            (float4*)d_dY, long_list, long_cnt);                                                \
+  HF_LAUNCH((k_agg_bwd_p_long<DD, MM>), sm_count() * 8, kPLongWarps * 32, 0, s, bm,               \
+            csr->rel_row_off, csr->row_ptr, csr->col_ptr, csr->csc_row, (const float4*)d_G,     \
+            (float4*)d_dY, long_list, long_cnt)
     bool mean = agg == HIFUSE_AGG_MEAN;
     if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }
     else { if (mean) { HF_BWD(64, true); } else { HF_BWD(64, false); } }
 #undef HF_BWD
-  } else {
-    return HIFUSE_ERR_INVALID_ARG;
   }
   return last_cuda();
 }

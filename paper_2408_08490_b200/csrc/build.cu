@@ -1,149 +1,125 @@
 // build.cu -- A1: semantic graph build (Alg. 2) as a
-// merged segmented CSR + CSC, on the GPU, with a kernel count independent of
-// the number of relations R.
+// merged segmented CSR + CSC for EVERY layer of a step in six launches (one
+// memset + five kernels), independent of the number of relations R and of
+// the number of layers.
 //
 // Alg. 2 runs, per layer, 1 gather (line 316) + R compares (318) + R
 // index-selects (319): 2R+1 short kernels that the paper offloads to the CPU
-// (lines 299-336).  Here the relation of each edge only decides a KEY,
+// (lines 299-336; "numerous and short", line 174).  Here the relation of an
+// edge only decides a KEY,
 //   key(e) = rel_row_off[r(e)] + dst(e)      (merged row, relation-major),
-// and one counting sort by key performs every relation's selection at once:
-//   k_classify   EdgeTypeLayer gather + validation + row histogram + source
-//                presence flags per (relation, source) slot
-//   scan         row_ptr and the compact Y-row numbering (one scan over both)
-//   k_finish     rel_y_off, y_src, slot_y, U
-//   k_scatter    unstable atomic placement into rows + column histogram
-//   scan         col_ptr
-//   k_fix_rows   warp per row: sort by original column (restores Alg. 2's
-//                column order, so the result is bit-exact and deterministic),
-//                then CSC placement
-//   k_fix_cols   thread per Y row: sort CSC entries by CSR position
-//   k_sort_long  the same two sorts for segments longer than 32 (rank sort)
-#include <cstdlib>
+// and one counting sort by key performs every relation's selection at once.
+// Every kernel covers all layers of the call (a flattened (layer, tile) grid):
+//   memset      per-layer counters (one contiguous zone)
+//   k_classify  EdgeTypeLayer (gather, or binary search of relation-major
+//               edge-id ranges) + validation; row histogram whose atomic
+//               return is the edge's arrival rank in its row (warp-aggregated:
+//               one atomic per distinct row of a warp); per (relation,
+//               source) slot the number of edges
+//   k_scan      segmented decoupled-look-back scan of the row counts and of
+//               the slot (presence, count) pairs: row_ptr, rel_row_off,
+//               slot_y, y_src, rel_y_off, U -- and col_ptr, because Y rows are
+//               numbered in slot order, so the CSC column of Y row slot_y[s]
+//               starts at the exclusive prefix of the slot counts at s
+//   k_scatter   pos = row_ptr[key] + rank: eperm, col (unsorted inside rows)
+//   k_rows      warp per 32 consecutive rows: their CSR span staged in shared
+//               memory, every row sorted by original column (restores Alg.
+//               2's order: bit-exact and deterministic), then placed into the
+//               CSC (one atomic slot per entry); longer rows by the block
+//   k_cols      warp per 32 consecutive CSC columns: each sorted by CSR
+//               position (lane per column <= 16 entries, warp bitonic <= 32),
+//               hub columns by a warp (rank) / the block (bitonic) in smem
+// The kernels are short with many blocks, so on the pipelined step (build of
+// batch i+1 on a low-priority side stream) they interleave with the compute
+// of batch i at block granularity.  (A single persistent kernel with
+// ticket-ordered phases was measured and dropped: resident for the whole
+// build, it starved the compute stream -- DESIGN.md §8.)
+#include <algorithm>
+#include <cstring>
 #include <vector>
 #include "common.cuh"
 
 namespace hf {
 
+namespace {
 
-__global__ void k_classify(LayerMeta m, const int* __restrict__ src, const int* __restrict__ dst,
-                           const long long* __restrict__ eid, const int* __restrict__ edge_type,
-                           const long long* __restrict__ rel_off, long long E,
-                           int* __restrict__ key_e, int* __restrict__ slot_e,
-                           int* __restrict__ cnt, int* __restrict__ status) {
-  __shared__ long long s_off[HF_MAX_R + 1];
-  if (rel_off) {
-    for (int i = threadIdx.x; i <= m.R; i += blockDim.x) s_off[i] = rel_off[i];
-    __syncthreads();
-  }
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m.N) return;
-  long long id = eid[e];
-  int bad = 0, r = -1;
-  int s = src[e], d = dst[e];
-  if (id < 0 || id >= E) {
-    bad = HIFUSE_ST_BAD_EDGE_ID;
-  } else {
-    // Alg. 2: EdgeTypeLayer = EdgeType[EdgeID] -- a gather, or for a
-    // relation-major table the relation whose id range holds `id`
-    if (rel_off) {
-      int lo = 0, hi = m.R;                              // s_off[lo] <= id < s_off[hi]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_off[mid] <= id) lo = mid; else hi = mid;
-      }
-      r = lo;
-    } else {
-      r = edge_type[id];
-    }
-    if (r < 0 || r >= m.R) bad = HIFUSE_ST_BAD_REL;
-    else if (s < 0 || s >= m.n_src[m.rel_src[r]]) bad = HIFUSE_ST_BAD_SRC;
-    else if (d < 0 || d >= m.n_dst[m.rel_dst[r]]) bad = HIFUSE_ST_BAD_DST;
-  }
-  if (bad) {
-    atomicOr(status, bad);
-    key_e[e] = -1;
-    return;
-  }
-  int key = m.rel_row_off[r] + d;                        // lines 318-319, all r at once
-  int slot = m.slot_off[r] + s;
-  key_e[e] = key;
-  slot_e[e] = slot;
-  atomicAdd(&cnt[key], 1);
-  cnt[m.rows + slot] = 1;                                // presence flag (idempotent)
+constexpr int kBT = 256;               // threads per block
+constexpr int kNW = kBT / 32;
+constexpr int kEdgeTile = 2048;        // edges per classify / scatter block
+constexpr int kEPT = kEdgeTile / kBT;  // edges per thread
+constexpr int kScanPer = 16;           // scan elements per thread
+constexpr int kScanTile = kBT * kScanPer;
+constexpr int kSegRows = 32;           // rows / columns per warp in k_rows / k_cols
+constexpr int kSegTile = kNW * kSegRows;
+constexpr int kSpan = 1024;            // CSR/CSC entries a warp stages in smem
+constexpr int kMaxL = 4;               // layers per launch set (more: further sets)
+constexpr int kWarpRank = 256;
+constexpr int kBlockRank = 4096;
+constexpr int kLongRowBlocks = 16;     // k_rows blocks for rows > 32 (not in workloads)
+constexpr size_t kSmem = (size_t)kNW * kSpan * 2 * sizeof(int);   // 64 KB
+static_assert(kBlockRank * 2 * sizeof(int) <= kSmem, "block rank sort buffer");
+static_assert(2 * (kScanTile + kScanTile / 32) * sizeof(int) + 128 <= kSmem, "scan buffer");
+
+enum Kern { K_CLASSIFY, K_SCAN, K_SCATTER, K_ROWS, K_COLS, kKerns };
+
+struct BLayer {
+  int R, N, rows, S, U_max, csc;
+  int t_rows, t_slots;                 // scan tiles per segment
+  int key_base[HF_MAX_R + 1];          // rel_row_off
+  int slot_base[HF_MAX_R + 1];         // slot_off
+  int src_lim[HF_MAX_R];               // n_src of the source type of r
+  int dst_lim[HF_MAX_R];               // n_dst of the destination type of r
+  const int* src;
+  const int* dst;
+  const long long* eid;
+  // outputs
+  int *o_rel_row_off, *row_ptr, *col, *eperm, *o_rel_y_off, *y_src, *col_ptr, *csc_pos,
+      *csc_row, *slot_y, *U_dev;
+  // workspace: zero zone
+  int *cnt, *ccur;                     // cnt = [row counts | slot counts]
+  int* lcnt;                           // [0] long rows, [1] long columns
+  unsigned long long* sst;             // scan tile status [t_rows | t_slots]
+  // workspace: scratch
+  int *key_e, *slot_e, *rank_e, *gk, *gv, *long_rows, *long_cols;
+  int rows_reg, cols_reg;              // regular (non-long) blocks of k_rows / k_cols
+  int cols_xtra;                       // extra k_cols blocks for hub columns
+};
+
+struct BPlan {
+  int L;
+  int blk_off[kKerns][kMaxL + 1];      // block ranges of the layers in each kernel
+  long long E;
+  const int* edge_type;
+  const long long* rel_off;
+  int* status;
+};
+
+struct BuildParams {
+  BPlan p;
+  BLayer lay[kMaxL];
+};
+
+// (layer, tile) of this block in kernel k
+__device__ __forceinline__ int layer_of(const BPlan& P, int k, int* j) {
+  const int b = blockIdx.x;
+  int l = 0;
+  while (l + 1 < P.L && b >= P.blk_off[k][l + 1]) l++;
+  *j = b - P.blk_off[k][l];
+  return l;
 }
 
-// d_rel_edge_off[r] = lower bound of r in the (sorted) edge-type table.
-__global__ void k_et_offsets(const int* __restrict__ et, long long E, int R,
-                             long long* __restrict__ off) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r > R) return;
-  long long lo = 0, hi = E;
-  while (lo < hi) {
-    const long long mid = (lo + hi) >> 1;
-    if (et[mid] < r) lo = mid + 1; else hi = mid;
-  }
-  off[r] = r == R ? E : lo;
+// ------------------------------------------------------------ primitives --
+// Look-back polls use relaxed loads (an acquire load per poll compiles to an
+// L1 invalidation that stalls every block on the SM); the tile statuses are
+// themselves the data.
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
-
-__global__ void k_et_check(const int* __restrict__ et, long long E, int R, int* __restrict__ status) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= E) return;
-  const int v = et[i];
-  if (v < 0 || v >= R || (i > 0 && et[i - 1] > v)) atomicOr(status, HIFUSE_ST_UNSORTED_TYPES);
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-
-// pre = exclusive scan of [row counts | slot flags]; pre[rows] = valid edges,
-// pre[rows + S] - pre[rows] = U.
-__global__ void k_finish(LayerMeta m, const int* __restrict__ cnt, const int* __restrict__ pre,
-                         int* __restrict__ row_ptr, int* __restrict__ rel_row_off,
-                         int* __restrict__ rel_y_off, int* __restrict__ y_src,
-                         int* __restrict__ slot_y, int* __restrict__ U_dev) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int nvalid = pre[m.rows];
-  if (i <= m.rows) row_ptr[i] = pre[i];
-  if (i < m.S) {
-    int u = -1;
-    if (cnt[m.rows + i]) {
-      u = pre[m.rows + i] - nvalid;
-      int r = upper_bound_i(m.slot_off, m.R + 1, i) - 1;
-      y_src[u] = i - m.slot_off[r];
-    }
-    slot_y[i] = u;
-  }
-  if (i <= m.R) {
-    rel_row_off[i] = m.rel_row_off[i];
-    rel_y_off[i] = pre[m.rows + m.slot_off[i]] - nvalid;
-  }
-  if (i == 0) U_dev[0] = pre[m.rows + m.S] - nvalid;
-}
-
-__global__ void k_scatter(LayerMeta m, const int* __restrict__ key_e, const int* __restrict__ slot_e,
-                          const int* __restrict__ row_ptr, const int* __restrict__ slot_y,
-                          int* __restrict__ cur, int* __restrict__ ccnt, int* __restrict__ eperm,
-                          int* __restrict__ col, int* __restrict__ csc_pos,
-                          int* __restrict__ csc_row) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m.N) return;
-  int nvalid = row_ptr[m.rows];
-  if (e >= nvalid) {  // tail positions [nvalid, N): exactly one writer each
-    eperm[e] = -1; col[e] = -1;
-    if (csc_pos) { csc_pos[e] = -1; csc_row[e] = -1; }
-  }
-  int key = key_e[e];
-  if (key < 0) return;
-  int pos = row_ptr[key] + atomicAdd(&cur[key], 1);
-  int c = slot_y[slot_e[e]];
-  eperm[pos] = e;
-  col[pos] = c;
-  if (csc_pos) atomicAdd(&ccnt[c], 1);
-}
-
-// Segment fix-up sorts (unique keys, carried values).
-//  k_fix_rows: one warp per CSR row, n <= 32 sorted in registers (shuffle
-//              bitonic), then the sorted row is placed into the CSC.
-//  k_fix_cols: one thread per CSC column, n <= kThreadCap sorted in place.
-//  Longer segments go to k_sort_long (shared-memory rank sort, warp or block).
-static constexpr int kThreadCap = 16;
 
 __device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
 #pragma unroll
@@ -154,14 +130,12 @@ __device__ __forceinline__ void warp_sort_regs(int& key, int& val, int lane) {
       int pv = __shfl_xor_sync(0xffffffffu, val, j);
       bool up = (lane & k) == 0;
       bool lower = (lane & j) == 0;
-      bool take_min = lower == up;
-      bool swap = take_min ? (pk < key) : (pk > key);
+      bool swap = (lower == up) ? (pk < key) : (pk > key);
       if (swap) { key = pk; val = pv; }
     }
 }
 
-// Bitonic sort of 16 (key, value) pairs held by the 16 lanes of a half warp
-// (hl = lane within the half); both halves of the warp sort independently.
+// bitonic sort of the 16 (key, value) pairs of each half warp (hl = lane & 15)
 __device__ __forceinline__ void half_sort_regs(int& key, int& val, int hl) {
 #pragma unroll
   for (int k = 2; k <= 16; k <<= 1)
@@ -171,143 +145,14 @@ __device__ __forceinline__ void half_sort_regs(int& key, int& val, int hl) {
       int pv = __shfl_xor_sync(0xffffffffu, val, j);
       bool up = (hl & k) == 0;
       bool lower = (hl & j) == 0;
-      bool take_min = lower == up;
-      bool swap = take_min ? (pk < key) : (pk > key);
+      bool swap = (lower == up) ? (pk < key) : (pk > key);
       if (swap) { key = pk; val = pv; }
     }
 }
 
-__device__ __forceinline__ void place_sorted(int row, int b, int i, int key, int val,
-                                             int* eperm, int* col, const int* col_ptr, int* ccur,
-                                             int* csc_pos, int* csc_row) {
-  eperm[b + i] = key;
-  col[b + i] = val;
-  if (col_ptr) {
-    int w = col_ptr[val] + atomicAdd(&ccur[val], 1);
-    csc_pos[w] = b + i;
-    csc_row[w] = row;
-  }
-}
-
-// Two rows per warp: a row of <= 16 entries is sorted by its half warp (10
-// compare-exchange stages instead of 15 over a full warp); rows of 17..32 are
-// then sorted one after another by the whole warp; longer rows go to
-// k_sort_long.  Then the sorted row is placed into the CSC.
-__global__ void __launch_bounds__(256)
-k_fix_rows(int rows, const int* __restrict__ row_ptr, int* eperm, int* col,
-           const int* __restrict__ col_ptr, int* ccur, int* csc_pos, int* csc_row, int* long_list,
-           int* long_cnt) {
-  const int lane = threadIdx.x & 31, hl = lane & 15;
-  const int row0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 2;
-  if (row0 >= rows) return;
-  const int row = row0 + (lane >> 4);
-  int b = 0, n = 0;
-  if (row < rows) {
-    b = row_ptr[row];
-    n = row_ptr[row + 1] - b;
-  }
-  if (n > 32 && hl == 0) long_list[atomicAdd(long_cnt, 1)] = row;
-  const bool small = n <= 16;
-  int key = (small && hl < n) ? eperm[b + hl] : 0x7fffffff;
-  int val = (small && hl < n) ? col[b + hl] : 0;
-  if (__any_sync(0xffffffffu, small && n > 1)) half_sort_regs(key, val, hl);
-  if (small && hl < n) place_sorted(row, b, hl, key, val, eperm, col, col_ptr, ccur, csc_pos, csc_row);
-  unsigned mid = __ballot_sync(0xffffffffu, hl == 0 && n > 16 && n <= 32);
-  while (mid) {
-    const int src = __ffs(mid) - 1;
-    mid &= mid - 1;
-    const int bb = __shfl_sync(0xffffffffu, b, src), nn = __shfl_sync(0xffffffffu, n, src);
-    const int rr = row0 + (src >> 4);
-    int k2 = lane < nn ? eperm[bb + lane] : 0x7fffffff;
-    int v2 = lane < nn ? col[bb + lane] : 0;
-    warp_sort_regs(k2, v2, lane);
-    if (lane < nn) place_sorted(rr, bb, lane, k2, v2, eperm, col, col_ptr, ccur, csc_pos, csc_row);
-  }
-}
-
-// One warp per 32 consecutive CSC columns: lane l sorts column 32w+l in place
-// when it has <= kThreadCap entries; columns of (kThreadCap, 32] are sorted by
-// the whole warp in registers, one after another; longer ones go to the
-// block-wide kernel.
-__global__ void __launch_bounds__(256)
-k_fix_cols(const int* __restrict__ U_dev, const int* __restrict__ col_ptr, int* csc_pos,
-           int* csc_row, int* long_list, int* long_cnt) {
-  const int lane = threadIdx.x & 31;
-  const int U = *U_dev;
-  const int u0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
-  if (u0 >= U) return;
-  const int u = u0 + lane;
-  int b = 0, n = 0;
-  if (u < U) {
-    b = col_ptr[u];
-    n = col_ptr[u + 1] - b;
-  }
-  if (n > 1 && n <= kThreadCap) {
-    // registers + odd-even transposition network (compile-time indices, no
-    // dependent global-memory round trips)
-    int kk[kThreadCap], vv[kThreadCap];
-#pragma unroll
-    for (int i = 0; i < kThreadCap; i++) {
-      kk[i] = i < n ? csc_pos[b + i] : 0x7fffffff;
-      vv[i] = i < n ? csc_row[b + i] : 0;
-    }
-#pragma unroll
-    for (int ph = 0; ph < kThreadCap; ph++)
-#pragma unroll
-      for (int i = ph & 1; i + 1 < kThreadCap; i += 2)
-        if (kk[i] > kk[i + 1]) {
-          int t = kk[i]; kk[i] = kk[i + 1]; kk[i + 1] = t;
-          t = vv[i]; vv[i] = vv[i + 1]; vv[i + 1] = t;
-        }
-#pragma unroll
-    for (int i = 0; i < kThreadCap; i++)
-      if (i < n) {
-        csc_pos[b + i] = kk[i];
-        csc_row[b + i] = vv[i];
-      }
-  }
-  if (n > 32) long_list[atomicAdd(long_cnt, 1)] = u;
-  unsigned mid = __ballot_sync(0xffffffffu, n > kThreadCap && n <= 32);
-  while (mid) {
-    const int src = __ffs(mid) - 1;
-    mid &= mid - 1;
-    const int bb = __shfl_sync(0xffffffffu, b, src), nn = __shfl_sync(0xffffffffu, n, src);
-    int key = lane < nn ? csc_pos[bb + lane] : 0x7fffffff;
-    int val = lane < nn ? csc_row[bb + lane] : 0;
-    warp_sort_regs(key, val, lane);
-    if (lane < nn) {
-      csc_pos[bb + lane] = key;
-      csc_row[bb + lane] = val;
-    }
-  }
-}
-
-// Segments longer than 32 (hub columns, long rows): rank sort in shared
-// memory -- every key's final position is the number of smaller keys (keys
-// are unique), computed with broadcast reads, no synchronisation chain.
-// n <= kWarpRank: one warp per segment (8 per block); n <= kBlockRank: the
-// whole block; longer (never seen in the workloads): rank sort in global.
-static constexpr int kWarpRank = 256;
-static constexpr int kBlockRank = 4096;
-
-template <bool ROWS>
-__device__ __forceinline__ void place_row_in_csc(int seg, int b, int e, int first, int step,
-                                                 const int* vals, const int* col_ptr, int* ccur,
-                                                 int* csc_pos, int* csc_row) {
-  if (!ROWS || !col_ptr) return;
-  for (int p = b + first; p < e; p += step) {
-    const int c = vals[p];
-    const int w = col_ptr[c] + atomicAdd(&ccur[c], 1);
-    csc_pos[w] = p;
-    csc_row[w] = seg;
-  }
-}
-
-// Rank scatter: thread `t` of `nt` owns keys t, t+nt, ... (at most E, held in
-// registers); every key of the segment is read once per thread with 16-byte
-// shared loads (broadcast) and compared against all owned keys, so one load
-// serves 4*E comparisons.  The segment buffer is padded to a multiple of 4
-// with INT_MAX by the caller.
+// Rank sort of n unique keys (+ values) held in shared memory (sk, sv, padded
+// with INT_MAX to a multiple of 4): thread t of nt owns keys t, t+nt, ...;
+// every key's final position is the number of smaller keys.
 template <int E>
 __device__ __forceinline__ void rank_scatter(const int* sk, const int* sv, int n, int t, int nt,
                                              int* keys, int* vals) {
@@ -335,127 +180,698 @@ __device__ __forceinline__ void rank_scatter(const int* sk, const int* sv, int n
   }
 }
 
-static constexpr int kSortThreads = 512;
-
-template <bool ROWS>
-__global__ void __launch_bounds__(kSortThreads)
-k_sort_long(const int* __restrict__ ptr, int* keys, int* vals, const int* __restrict__ col_ptr,
-            int* ccur, int* csc_pos, int* csc_row, const int* list, const int* cnt, int* gk,
-            int* gv, int dbg) {
-  constexpr int NW = kSortThreads / 32;
-  static_assert(NW * kWarpRank <= kBlockRank, "warp slices must fit the block buffer");
-  __shared__ __align__(16) int sk[kBlockRank];
-  __shared__ __align__(16) int sv[kBlockRank];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int n_long = *cnt;
-  // ---- warp phase (32 < n <= kWarpRank)
-  int* wk = sk + w * kWarpRank;
-  int* wv = sv + w * kWarpRank;
-  for (int k = blockIdx.x * NW + w; k < n_long; k += gridDim.x * NW) {
-    const int seg = list[k];
-    const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
-    if (n > kWarpRank || (dbg & 1)) continue;
-    for (int i = lane; i < ((n + 3) & ~3); i += 32) {
-      wk[i] = i < n ? keys[b + i] : 0x7fffffff;
-      wv[i] = i < n ? vals[b + i] : 0;
+// Copies n entries of two int arrays into shared memory, 8 loads per thread
+// in flight before the stores; [n, pad) is filled with (INT_MAX, 0).
+__device__ __forceinline__ void stage2(const int* __restrict__ ka, const int* __restrict__ va,
+                                       int n, int pad, int* sk, int* sv, int t, int nt) {
+  constexpr int B = 8;
+  for (int i0 = 0; i0 < pad; i0 += B * nt) {
+    int kk[B], vv[B];
+#pragma unroll
+    for (int q = 0; q < B; q++) {
+      const int i = i0 + q * nt + t;
+      kk[q] = i < n ? ka[i] : 0x7fffffff;
+      vv[q] = i < n ? va[i] : 0;
     }
-    __syncwarp();
-    rank_scatter<kWarpRank / 32>(wk, wv, n, lane, 32, keys + b, vals + b);
-    __syncwarp();
-    place_row_in_csc<ROWS>(seg, b, e, lane, 32, vals, col_ptr, ccur, csc_pos, csc_row);
+#pragma unroll
+    for (int q = 0; q < B; q++) {
+      const int i = i0 + q * nt + t;
+      if (i < pad) {
+        sk[i] = kk[q];
+        sv[i] = vv[q];
+      }
+    }
+  }
+}
+
+// CSC placement of CSR position p (row `row`, Y row c)
+__device__ __forceinline__ void place_entry(const BLayer& L, int row, int p, int c) {
+  const int w = L.col_ptr[c] + atomicAdd(L.ccur + c, 1);
+  L.csc_pos[w] = p;
+  L.csc_row[w] = row;
+}
+
+// Block-wide sort of one segment [b, e) of (keys, vals): rank sort in shared
+// memory (<= kBlockRank entries), a global rank sort beyond (never seen in
+// the workloads).  sm: >= 2 kBlockRank ints.  Ends with __syncthreads.
+__device__ void block_sort_segment(int* keys, int* vals, int b, int e, int* sm, int* gk,
+                                   int* gv) {
+  const int n = e - b;
+  int* sk = sm;
+  int* sv = sm + kBlockRank;
+  if (n <= kBlockRank) {
+    // bitonic sort in shared memory, padded to a power of two (n log^2 n;
+    // a rank sort is n^2 -- 30 us for a 1757-entry hub column of ogbn-mag)
+    int P2 = 1;
+    while (P2 < n) P2 <<= 1;
+    stage2(keys + b, vals + b, n, P2, sk, sv, threadIdx.x, kBT);
+    __syncthreads();
+    for (int kk = 2; kk <= P2; kk <<= 1)
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < P2 / 2; i += kBT) {
+          const int lo = ((i / jj) * 2 * jj) + (i % jj), hi = lo + jj;
+          const bool up = (lo & kk) == 0;
+          const int x = sk[lo], y = sk[hi];
+          if ((x > y) == up) {
+            sk[lo] = y; sk[hi] = x;
+            const int tv = sv[lo]; sv[lo] = sv[hi]; sv[hi] = tv;
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < n; i += kBT) {
+      keys[b + i] = sk[i];
+      vals[b + i] = sv[i];
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += kBT) {
+      gk[b + i] = keys[b + i];
+      gv[b + i] = vals[b + i];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kBT) {
+      const int kk = gk[b + i];
+      int r = 0;
+      for (int q = 0; q < n; q++) r += gk[b + q] < kk;
+      keys[b + r] = kk;
+      vals[b + r] = gv[b + i];
+    }
   }
   __syncthreads();
-  // ---- block phase (n > kWarpRank): one segment per block, shared memory
-  // rank sort up to kBlockRank, global-memory rank sort beyond
-  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
-    const int seg = list[k];
-    const int b = ptr[seg], e = ptr[seg + 1], n = e - b;
-    if (n <= kWarpRank || (dbg & 2)) continue;
-    if (n <= kBlockRank) {
-      // bitonic sort in shared memory, padded to a power of two
-      int P = 1;
-      while (P < n) P <<= 1;
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        sk[i] = i < n ? keys[b + i] : 0x7fffffff;
-        sv[i] = i < n ? vals[b + i] : 0;
-      }
-      __syncthreads();
-      for (int kk = 2; kk <= P; kk <<= 1)
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-          for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
-            // i-th compare-exchange pair of this stage
-            const int lo = ((i / jj) * 2 * jj) + (i % jj), hi = lo + jj;
-            const bool up = (lo & kk) == 0;
-            const int a = sk[lo], c = sk[hi];
-            if ((a > c) == up) {
-              sk[lo] = c; sk[hi] = a;
-              const int t = sv[lo]; sv[lo] = sv[hi]; sv[hi] = t;
-            }
-          }
-          __syncthreads();
-        }
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        keys[b + i] = sk[i];
-        vals[b + i] = sv[i];
-      }
+}
+
+// ------------------------------------------------------------- k_classify --
+struct RelSmem {
+  long long off[HF_MAX_R + 1];         // relation-major edge-id ranges
+  int key_base[HF_MAX_R + 1], slot_base[HF_MAX_R + 1], src_lim[HF_MAX_R], dst_lim[HF_MAX_R];
+};
+
+__global__ void __launch_bounds__(kBT)
+k_classify(const __grid_constant__ BuildParams bp) {
+  __shared__ RelSmem rs;
+  const BPlan& P = bp.p;
+  int j;
+  const BLayer& L = bp.lay[layer_of(P, K_CLASSIFY, &j)];
+  // per-relation tables in shared memory (divergent relation ids would
+  // serialise constant-bank reads of the kernel parameters)
+  for (int i = threadIdx.x; i <= L.R; i += kBT) {
+    if (P.rel_off) rs.off[i] = P.rel_off[i];
+    rs.key_base[i] = L.key_base[i];
+    rs.slot_base[i] = L.slot_base[i];
+    if (i < L.R) {
+      rs.src_lim[i] = L.src_lim[i];
+      rs.dst_lim[i] = L.dst_lim[i];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int e0 = j * kEdgeTile;
+  long long id[kEPT];
+  int sv[kEPT], dv[kEPT], key[kEPT], slot[kEPT];
+  // all loads of the thread in flight together
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    const int e = e0 + q * kBT + threadIdx.x;
+    const bool in = e < L.N;
+    id[q] = in ? L.eid[e] : -2;
+    sv[q] = in ? L.src[e] : 0;
+    dv[q] = in ? L.dst[e] : 0;
+  }
+  int bad_any = 0;
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    key[q] = -1;
+    slot[q] = -1;
+    if (id[q] == -2) continue;                     // past the tile
+    int bad = 0, r = -1;
+    if (id[q] < 0 || id[q] >= P.E) {
+      bad = HIFUSE_ST_BAD_EDGE_ID;
     } else {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        gk[b + i] = keys[b + i];
-        gv[b + i] = vals[b + i];
+      // Alg. 2: EdgeTypeLayer = EdgeType[EdgeID] -- a gather, or for
+      // a relation-major table the relation whose id range holds `id`
+      if (P.rel_off) {
+        int lo = 0, hi = L.R;                       // off[lo] <= id < off[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (rs.off[mid] <= id[q]) lo = mid; else hi = mid;
+        }
+        r = lo;
+      } else {
+        r = P.edge_type[id[q]];
       }
+      if (r < 0 || r >= L.R) bad = HIFUSE_ST_BAD_REL;
+      else if (sv[q] < 0 || sv[q] >= rs.src_lim[r]) bad = HIFUSE_ST_BAD_SRC;
+      else if (dv[q] < 0 || dv[q] >= rs.dst_lim[r]) bad = HIFUSE_ST_BAD_DST;
+    }
+    if (bad) {
+      bad_any |= bad;
+      key[q] = -3;                                 // dropped edge
+      continue;
+    }
+    key[q] = rs.key_base[r] + dv[q];               // lines 318-319, every r at once
+    slot[q] = L.rows + rs.slot_base[r] + sv[q];    // index into cnt
+  }
+  if (bad_any) atomicOr(P.status, bad_any);
+  // Warp-aggregated atomics: sampled blocks list the edges of a destination
+  // (and often of a source) together, so lanes of a warp often share a row
+  // or slot -- one atomic per distinct address and warp.  Row: the atomic's
+  // return is the arrival rank (lane order inside the warp).
+  unsigned prow[kEPT], pslot[kEPT];
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    prow[q] = __match_any_sync(0xffffffffu, key[q] >= 0 ? key[q] : -1 - lane);
+    pslot[q] = __match_any_sync(0xffffffffu, key[q] >= 0 ? slot[q] : -1 - lane);
+  }
+  int base[kEPT];
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    const bool lead_r = key[q] >= 0 && lane == __ffs(prow[q]) - 1;
+    const bool lead_s = key[q] >= 0 && lane == __ffs(pslot[q]) - 1;
+    base[q] = lead_r ? atomicAdd(L.cnt + key[q], __popc(prow[q])) : 0;
+    if (lead_s) atomicAdd(L.cnt + slot[q], __popc(pslot[q]));
+  }
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    const int b = __shfl_sync(0xffffffffu, base[q], __ffs(prow[q]) - 1);
+    const int e = e0 + q * kBT + threadIdx.x;
+    if (key[q] == -1) continue;
+    L.key_e[e] = key[q] >= 0 ? key[q] : -1;
+    if (key[q] >= 0) {
+      L.slot_e[e] = slot[q] - L.rows;
+      L.rank_e[e] = b + __popc(prow[q] & ((1u << lane) - 1u));
+    }
+  }
+}
+
+// ----------------------------------------------------------------- k_scan --
+// Segmented exclusive scan, decoupled look-back over the tiles of a segment.
+// Rows segment: the row counts.  Slots segment: (presence, count) pairs of
+// the (relation, source) slots -- presence numbers the Y rows (slot_y,
+// y_src, rel_y_off, U), the counts give col_ptr.  Tile status (u64):
+// flag << 62 | a << 31 | b, flag 1 aggregate, 2 inclusive prefix; a, b < 2^31.
+constexpr unsigned long long kValMask = (1ull << 31) - 1;
+
+__device__ __forceinline__ unsigned long long pack(int flag, long long a, long long b) {
+  return ((unsigned long long)flag << 62) | ((unsigned long long)a << 31) | (unsigned long long)b;
+}
+
+__global__ void __launch_bounds__(kBT)
+k_scan(const __grid_constant__ BuildParams bp) {
+  extern __shared__ __align__(16) int sm[];
+  int jj;
+  const BLayer& L = bp.lay[layer_of(bp.p, K_SCAN, &jj)];
+  const bool rows_seg = jj < L.t_rows;
+  const int j = rows_seg ? jj : jj - L.t_rows;
+  const int* a = rows_seg ? L.cnt : L.cnt + L.rows;
+  const int len = rows_seg ? L.rows : L.S;
+  unsigned long long* st = rows_seg ? L.sst : L.sst + L.t_rows;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int base = j * kScanTile;
+  const int n = max(0, min(kScanTile, len - base));
+  int* buf = sm;                                    // counts, then count prefixes
+  int* fbuf = sm + kScanTile + kScanTile / 32;      // flag prefixes (slots)
+  __shared__ int wsum[2 * kNW];
+  __shared__ long long s_pre[2];
+  auto pad = [](int i) { return i + (i >> 5); };
+  // coalesced load, 16 per thread in flight
+  {
+    int v[kScanPer];
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      const int i = k * kBT + t;
+      v[k] = i < n ? a[base + i] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) buf[pad(k * kBT + t)] = v[k];
+  }
+  __syncthreads();
+  int c[kScanPer];
+  int csum = 0, fsum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; k++) {
+    c[k] = buf[pad(t * kScanPer + k)];
+    csum += c[k];
+    fsum += c[k] > 0;
+  }
+  // block exclusive scan of the per-thread (count, flag) sums
+  int ci = csum, fi = fsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y1 = __shfl_up_sync(0xffffffffu, ci, o);
+    const int y2 = __shfl_up_sync(0xffffffffu, fi, o);
+    if (lane >= o) { ci += y1; fi += y2; }
+  }
+  if (lane == 31) { wsum[w] = ci; wsum[kNW + w] = fi; }
+  __syncthreads();
+  if (w == 0) {
+    int x1 = lane < kNW ? wsum[lane] : 0, x2 = lane < kNW ? wsum[kNW + lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y1 = __shfl_up_sync(0xffffffffu, x1, o);
+      const int y2 = __shfl_up_sync(0xffffffffu, x2, o);
+      if (lane >= o) { x1 += y1; x2 += y2; }
+    }
+    if (lane < kNW) { wsum[lane] = x1; wsum[kNW + lane] = x2; }
+  }
+  __syncthreads();
+  const int cex = (w ? wsum[w - 1] : 0) + ci - csum;
+  const int fex = (w ? wsum[kNW + w - 1] : 0) + fi - fsum;
+  const long long cagg = wsum[kNW - 1], fagg = wsum[2 * kNW - 1];
+  // look-back (warp 0)
+  if (w == 0) {
+    long long ce = 0, fe = 0;
+    if (j == 0) {
+      if (lane == 0) st_release64(st, pack(2, fagg, cagg));
+    } else {
+      if (lane == 0) st_release64(st + j, pack(1, fagg, cagg));
+      int k = j - 1;
+      for (;;) {
+        const int idx = k - lane;
+        unsigned long long sv;
+        for (int ns = 32;; ns = min(ns * 2, 256)) {
+          sv = idx >= 0 ? ld_relaxed64(st + idx) : pack(2, 0, 0);
+          if (__all_sync(0xffffffffu, (sv >> 62) != 0)) break;
+          __nanosleep(ns);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 31;
+        long long va = lane <= stop ? (long long)((sv >> 31) & kValMask) : 0;
+        long long vb = lane <= stop ? (long long)(sv & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          va += __shfl_xor_sync(0xffffffffu, va, o);
+          vb += __shfl_xor_sync(0xffffffffu, vb, o);
+        }
+        fe += va;
+        ce += vb;
+        if (incl) break;
+        k -= 32;
+      }
+      if (lane == 0) st_release64(st + j, pack(2, fe + fagg, ce + cagg));
+    }
+    if (lane == 0) { s_pre[0] = ce; s_pre[1] = fe; }
+  }
+  __syncthreads();
+  const long long cpre = s_pre[0], fpre = s_pre[1];
+  const bool last_tile = base + kScanTile >= len;
+  long long crun = cpre + cex, frun = fpre + fex;
+  if (rows_seg) {
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      buf[pad(t * kScanPer + k)] = (int)crun;
+      crun += c[k];
+      // rows longer than 32: sorted by k_rows' extra blocks
+      if (c[k] > 32) L.long_rows[atomicAdd(L.lcnt + 0, 1)] = base + t * kScanPer + k;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      const int i = k * kBT + t;
+      if (i < n) L.row_ptr[base + i] = buf[pad(i)];
+    }
+    if (last_tile && t == 0) L.row_ptr[len] = (int)(cpre + cagg);
+    if (j == 0)
+      for (int r = t; r <= L.R; r += kBT) L.o_rel_row_off[r] = L.key_base[r];
+    return;
+  }
+  // slots: Y row numbering (presence prefix) and column starts (count prefix)
+  {
+    const int i0 = base + t * kScanPer;
+    int r = 0;
+    {
+      int lo = 0, hi = L.R;                            // slot_base[lo] <= i0 < slot_base[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (L.slot_base[mid] <= i0) lo = mid; else hi = mid;
+      }
+      r = lo;
+    }
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      const int i = i0 + k;
+      if (i < len && c[k] > 0) {
+        while (r + 1 < L.R && L.slot_base[r + 1] <= i) r++;
+        L.y_src[frun] = i - L.slot_base[r];
+        if (L.csc) {
+          L.col_ptr[frun] = (int)crun;
+          // hub columns (> 32 entries): sorted by k_cols' extra blocks
+          if (c[k] > 32) L.long_cols[atomicAdd(L.lcnt + 1, 1)] = (int)frun;
+        }
+      }
+      // encoded: prefix if present, -1 - prefix if absent
+      fbuf[pad(t * kScanPer + k)] = c[k] > 0 ? (int)frun : -1 - (int)frun;
+      frun += c[k] > 0;
+      crun += c[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanPer; k++) {
+    const int i = k * kBT + t;
+    if (i < n) {
+      const int f = fbuf[pad(i)];
+      L.slot_y[base + i] = f >= 0 ? f : -1;
+    }
+  }
+  // rel_y_off[r] = number of present slots before slot_base[r]
+  for (int r = t; r <= L.R; r += kBT) {
+    const int q = L.slot_base[r];
+    if (q >= base && q < base + n) {
+      const int f = fbuf[pad(q - base)];
+      L.o_rel_y_off[r] = f >= 0 ? f : -1 - f;
+    } else if (q >= len && last_tile) {
+      L.o_rel_y_off[r] = (int)(fpre + fagg);
+    }
+  }
+  if (last_tile && t == 0) {
+    L.U_dev[0] = (int)(fpre + fagg);
+    if (L.csc) L.col_ptr[fpre + fagg] = (int)(cpre + cagg);    // col_ptr[U] = valid edges
+  }
+}
+
+// -------------------------------------------------------------- k_scatter --
+__global__ void __launch_bounds__(kBT)
+k_scatter(const __grid_constant__ BuildParams bp) {
+  int j;
+  const BLayer& L = bp.lay[layer_of(bp.p, K_SCATTER, &j)];
+  const int nvalid = L.row_ptr[L.rows];
+  const int e0 = j * kEdgeTile;
+  int key[kEPT], slot[kEPT], rank[kEPT], pos[kEPT], c[kEPT];
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    const int e = e0 + q * kBT + threadIdx.x;
+    key[q] = e < L.N ? L.key_e[e] : -1;
+    slot[q] = key[q] >= 0 ? L.slot_e[e] : 0;
+    rank[q] = key[q] >= 0 ? L.rank_e[e] : 0;
+  }
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    pos[q] = key[q] >= 0 ? L.row_ptr[key[q]] + rank[q] : 0;
+    c[q] = key[q] >= 0 ? L.slot_y[slot[q]] : 0;
+  }
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    const int e = e0 + q * kBT + threadIdx.x;
+    if (e < L.N && e >= nvalid) {      // tail positions [nvalid, N): one writer each
+      L.eperm[e] = -1;
+      L.col[e] = -1;
+      if (L.csc) { L.csc_pos[e] = -1; L.csc_row[e] = -1; }
+    }
+    if (key[q] < 0) continue;
+    L.eperm[pos[q]] = e;
+    L.col[pos[q]] = c[q];
+  }
+}
+
+// ----------------------------------------------------------------- k_rows --
+// Warp per 32 consecutive merged rows.  Their CSR span [row_ptr[r0],
+// row_ptr[r0+32]) is contiguous: staged in shared memory, every row <= 32
+// sorted by original column in registers (half warp per row <= 16, whole warp
+// <= 32) and written back; the span is then placed into the CSC with its
+// atomic slot requests batched (8 per lane in flight).  Rows longer than 32
+// go to a block-local list, sorted and placed by the whole block at the end.
+__device__ __forceinline__ void row_sorted(const BLayer& L, bool staged, int* sk, int* sv,
+                                           int span_b, int b, int i, int key, int val) {
+  L.eperm[b + i] = key;
+  L.col[b + i] = val;
+  if (staged) {
+    sk[b - span_b + i] = key;
+    sv[b - span_b + i] = val;
+  }
+}
+
+__global__ void __launch_bounds__(kBT)
+k_rows(const __grid_constant__ BuildParams bp) {
+  extern __shared__ __align__(16) int sm[];
+  int j;
+  const BLayer& L = bp.lay[layer_of(bp.p, K_ROWS, &j)];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (j >= L.rows_reg) {
+    // rows longer than 32 (listed by k_scan; not produced by fanout <= 32
+    // sampling): one block per row
+    const int nl = L.lcnt[0];
+    for (int k = j - L.rows_reg; k < nl; k += kLongRowBlocks) {
+      const int row = L.long_rows[k];
+      const int b = L.row_ptr[row], e = L.row_ptr[row + 1];
+      block_sort_segment(L.eperm, L.col, b, e, sm, L.gk, L.gv);
+      if (L.csc)
+        for (int p = b + threadIdx.x; p < e; p += kBT) place_entry(L, row, p, L.col[p]);
       __syncthreads();
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int kk = gk[b + i];
-        int r = 0;
-        for (int j = 0; j < n; j++) r += gk[b + j] < kk;
-        keys[b + r] = kk;
-        vals[b + r] = gv[b + i];
+    }
+    return;
+  }
+  const int r0 = (j * kNW + w) * kSegRows;
+  if (r0 < L.rows) {
+    const int nr = min(kSegRows, L.rows - r0);
+    int* sk = sm + w * 2 * kSpan;
+    int* sv = sk + kSpan;
+    const int rb = L.row_ptr[r0 + min(lane, nr)];                 // start of row r0+lane
+    const int re = L.row_ptr[r0 + min(lane + 1, nr)];             // its end
+    const int n = lane < nr ? re - rb : 0;
+    const int span_b = __shfl_sync(0xffffffffu, rb, 0);
+    const int span_e = __shfl_sync(0xffffffffu, re, nr - 1);
+    const int span = span_e - span_b;
+    const bool staged = span <= kSpan;
+    if (staged) {
+      stage2(L.eperm + span_b, L.col + span_b, span, span, sk, sv, lane, 32);
+      __syncwarp();
+    }
+    // rows of <= 16 entries: two per iteration (one per half warp)
+    const int hl = lane & 15, half = lane >> 4;
+    for (int q = 0; q < nr; q += 2) {
+      const int row = q + half;
+      const int src = row < nr ? row : 0;
+      const int b = __shfl_sync(0xffffffffu, rb, src);
+      const int nn = __shfl_sync(0xffffffffu, n, src);
+      const bool mine = row < nr && nn <= 16;
+      int key = 0x7fffffff, val = 0;
+      if (mine && hl < nn) {
+        key = staged ? sk[b - span_b + hl] : L.eperm[b + hl];
+        val = staged ? sv[b - span_b + hl] : L.col[b + hl];
+      }
+      if (__any_sync(0xffffffffu, mine && nn > 1)) half_sort_regs(key, val, hl);
+      __syncwarp();
+      if (mine && hl < nn) row_sorted(L, staged, sk, sv, span_b, b, hl, key, val);
+    }
+    // rows of 17..32 entries: whole warp, one after another
+    unsigned mid = __ballot_sync(0xffffffffu, lane < nr && n > 16 && n <= 32);
+    while (mid) {
+      const int src = __ffs(mid) - 1;
+      mid &= mid - 1;
+      const int b = __shfl_sync(0xffffffffu, rb, src), nn = __shfl_sync(0xffffffffu, n, src);
+      int key = 0x7fffffff, val = 0;
+      if (lane < nn) {
+        key = staged ? sk[b - span_b + lane] : L.eperm[b + lane];
+        val = staged ? sv[b - span_b + lane] : L.col[b + lane];
+      }
+      warp_sort_regs(key, val, lane);
+      __syncwarp();
+      if (lane < nn) row_sorted(L, staged, sk, sv, span_b, b, lane, key, val);
+    }
+    __syncwarp();
+    if (L.csc) {
+      // CSC placement of the span's rows of <= 32 entries
+      constexpr int kB = 8;
+      for (int i0 = 0; i0 < span; i0 += 32 * kB) {
+        int c[kB], row[kB], ws[kB], cp[kB];
+#pragma unroll
+        for (int k = 0; k < kB; k++) {
+          const int i = i0 + k * 32 + lane;
+          const int ic = min(i, span - 1);
+          // row of entry ic: the last row of the group whose start is <= ic
+          // (an empty row shares its start with the next row, which is later)
+          int lo = 0;
+#pragma unroll
+          for (int stp = 16; stp; stp >>= 1) {
+            const int cand = lo + stp;
+            const int bs = __shfl_sync(0xffffffffu, rb, cand < nr ? cand : 0);
+            if (cand < nr && bs - span_b <= ic) lo = cand;
+          }
+          const int nlo = __shfl_sync(0xffffffffu, n, lo);
+          row[k] = lo;
+          c[k] = (i < span && nlo <= 32) ? (staged ? sv[i] : L.col[span_b + i]) : -1;
+        }
+        // slot requests: warp-aggregated (a hub source appears in many of the
+        // warp's 32 rows), all of the batch in flight together
+        unsigned pc[kB];
+#pragma unroll
+        for (int k = 0; k < kB; k++) pc[k] = __match_any_sync(0xffffffffu, c[k] >= 0 ? c[k] : -1 - lane);
+#pragma unroll
+        for (int k = 0; k < kB; k++) {
+          const bool lead = c[k] >= 0 && lane == __ffs(pc[k]) - 1;
+          ws[k] = lead ? atomicAdd(L.ccur + c[k], __popc(pc[k])) : 0;
+          cp[k] = c[k] >= 0 ? L.col_ptr[c[k]] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < kB; k++)
+          ws[k] = __shfl_sync(0xffffffffu, ws[k], __ffs(pc[k]) - 1) +
+                  __popc(pc[k] & ((1u << lane) - 1u));
+#pragma unroll
+        for (int k = 0; k < kB; k++)
+          if (c[k] >= 0) {
+            const int w2 = cp[k] + ws[k];
+            L.csc_pos[w2] = span_b + i0 + k * 32 + lane;
+            L.csc_row[w2] = r0 + row[k];
+          }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- k_cols --
+// Warp per 32 consecutive CSC columns (Y rows < U): lane per column for
+// <= 16 entries (insertion sort in shared memory), whole warp for 17..32;
+// longer (hub) columns: warp rank sort in shared memory for <= kWarpRank,
+// block rank sort beyond.  Blocks past U write the col_ptr tail (= valid
+// edges).
+__global__ void __launch_bounds__(kBT)
+k_cols(const __grid_constant__ BuildParams bp) {
+  extern __shared__ __align__(16) int sm[];
+  constexpr int kThreadCap = 16;
+  int j;
+  const BLayer& L = bp.lay[layer_of(bp.p, K_COLS, &j)];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (j >= L.cols_reg) {
+    // hub columns (> 32 entries, listed by k_scan), spread over the extra
+    // blocks: <= kWarpRank entries by one warp (rank sort), longer by the
+    // whole block (bitonic)
+    const int xb = j - L.cols_reg;
+    const int n_extra = L.cols_xtra;
+    const int nl = L.lcnt[1];
+    {
+      int* sk = sm + w * 2 * kWarpRank;
+      int* sv = sk + kWarpRank;
+      for (int k = xb * kNW + w; k < nl; k += n_extra * kNW) {
+        const int u = L.long_cols[k];
+        const int b = L.col_ptr[u], e = L.col_ptr[u + 1], n = e - b;
+        if (n > kWarpRank) continue;
+        stage2(L.csc_pos + b, L.csc_row + b, n, (n + 3) & ~3, sk, sv, lane, 32);
+        __syncwarp();
+        rank_scatter<kWarpRank / 32>(sk, sv, n, lane, 32, L.csc_pos + b, L.csc_row + b);
+        __syncwarp();
       }
     }
     __syncthreads();
-    place_row_in_csc<ROWS>(seg, b, e, threadIdx.x, blockDim.x, vals, col_ptr, ccur, csc_pos,
-                           csc_row);
-    __syncthreads();
+    for (int k = xb; k < nl; k += n_extra) {
+      const int u = L.long_cols[k];
+      const int b = L.col_ptr[u], e = L.col_ptr[u + 1];
+      if (e - b <= kWarpRank) continue;
+      block_sort_segment(L.csc_pos, L.csc_row, b, e, sm, L.gk, L.gv);
+    }
+    return;
+  }
+  const int U = *L.U_dev;
+  if ((j + 1) * kSegTile > U) {                   // col_ptr tail (U, U_max] of this tile
+    const int nvalid = L.row_ptr[L.rows];
+    const int hi = min((j + 1) * kSegTile - 1, L.U_max);
+    for (int u = max(j * kSegTile, U + 1) + threadIdx.x; u <= hi; u += kBT) L.col_ptr[u] = nvalid;
+    if (j * kSegTile >= U) return;
+  }
+  const int u0 = (j * kNW + w) * kSegRows;
+  if (u0 < U) {
+    const int nu = min(kSegRows, U - u0);
+    int* sk = sm + w * 2 * kSpan;
+    int* sv = sk + kSpan;
+    const int cb = L.col_ptr[u0 + min(lane, nu)];
+    const int ce = L.col_ptr[u0 + min(lane + 1, nu)];
+    const int n = lane < nu ? ce - cb : 0;
+    const int span_b = __shfl_sync(0xffffffffu, cb, 0);
+    const int span_e = __shfl_sync(0xffffffffu, ce, nu - 1);
+    const int span = span_e - span_b;
+    // stage the span unless hub columns make it long (then read from global)
+    const bool staged = span <= kSpan;
+    if (staged) {
+      stage2(L.csc_pos + span_b, L.csc_row + span_b, span, span, sk, sv, lane, 32);
+      __syncwarp();
+    }
+    if (n > 1 && n <= kThreadCap) {
+      // insertion sort of the lane's column in shared memory (columns hold
+      // ~2 entries on average: a fixed 16-element network wasted most work).
+      // Unstaged span: the lane copies its column to a private 16-slot area.
+      int* ks = staged ? sk + (cb - span_b) : sk + lane * kThreadCap;
+      int* vs = staged ? sv + (cb - span_b) : sv + lane * kThreadCap;
+      if (!staged)
+        for (int i = 0; i < n; i++) {
+          ks[i] = L.csc_pos[cb + i];
+          vs[i] = L.csc_row[cb + i];
+        }
+      for (int i = 1; i < n; i++) {
+        const int k0 = ks[i], v0 = vs[i];
+        int q = i - 1;
+        while (q >= 0 && ks[q] > k0) {
+          ks[q + 1] = ks[q];
+          vs[q + 1] = vs[q];
+          q--;
+        }
+        ks[q + 1] = k0;
+        vs[q + 1] = v0;
+      }
+      for (int i = 0; i < n; i++) {
+        L.csc_pos[cb + i] = ks[i];
+        L.csc_row[cb + i] = vs[i];
+      }
+    }
+    __syncwarp();
+    unsigned mid = __ballot_sync(0xffffffffu, n > kThreadCap && n <= 32);
+    while (mid) {
+      const int src = __ffs(mid) - 1;
+      mid &= mid - 1;
+      const int b = __shfl_sync(0xffffffffu, cb, src), nn = __shfl_sync(0xffffffffu, n, src);
+      int key = 0x7fffffff, val = 0;
+      if (lane < nn) {
+        key = staged ? sk[b - span_b + lane] : L.csc_pos[b + lane];
+        val = staged ? sv[b - span_b + lane] : L.csc_row[b + lane];
+      }
+      warp_sort_regs(key, val, lane);
+      if (lane < nn) {
+        L.csc_pos[b + lane] = key;
+        L.csc_row[b + lane] = val;
+      }
+    }
   }
 }
 
-struct BuildWs {
-  int *cnt, *pre, *key_e, *slot_e, *cur, *ccnt, *ccur, *scan, *lists, *counters, *gk, *gv;
+// ------------------------------------------------------------- host side --
+long long umax_of(const LayerMeta& m) { return m.N < m.S ? m.N : m.S; }
+int tiles(long long n, long long per) { return (int)std::max<long long>(1, (n + per - 1) / per); }
+
+// Per-layer workspace: zero zone (cnt [rows + S], ccur [U_max + 1], scan tile
+// statuses) and scratch.  The zero zones of all layers of a call are laid
+// out first and contiguously (one memset), the scratch after them.
+struct LayerWs {
+  long long zero_bytes, scratch_bytes;
 };
 
-static size_t build_ws(const LayerMeta& m, long long U_max, char* base, BuildWs* w) {
-  long long nz = (long long)m.rows + m.S;
-  long long sc = (long long)scan_ws_ints(nz > U_max ? nz : U_max);
-  size_t b = 0;
-  b += carve_bytes(nz, 4);              // cnt
-  b += carve_bytes(nz + 1, 4);          // pre
-  b += carve_bytes(m.N, 4) * 2;         // key_e, slot_e
-  b += carve_bytes(m.rows, 4);          // cur
-  b += carve_bytes(U_max + 1, 4) * 2;   // ccnt, ccur
-  b += carve_bytes(sc, 4);              // scan
-  b += carve_bytes((long long)m.rows + U_max, 4);  // long lists
-  b += carve_bytes(2, 4);               // counters
-  b += carve_bytes(m.N, 4) * 2;         // gk, gv
-  if (base && w) {
-    char* p = base;
-    w->cnt = carve<int>(p, nz);
-    w->pre = carve<int>(p, nz + 1);
-    w->key_e = carve<int>(p, m.N);
-    w->slot_e = carve<int>(p, m.N);
-    w->cur = carve<int>(p, m.rows);
-    w->ccnt = carve<int>(p, U_max + 1);
-    w->ccur = carve<int>(p, U_max + 1);
-    w->scan = carve<int>(p, sc);
-    w->lists = carve<int>(p, (long long)m.rows + U_max);
-    w->counters = carve<int>(p, 2);
-    w->gk = carve<int>(p, m.N);
-    w->gv = carve<int>(p, m.N);
-  }
-  return b;
+LayerWs layer_ws_sizes(const LayerMeta& m, bool csc) {
+  const long long U_max = umax_of(m);
+  LayerWs s;
+  s.zero_bytes = carve_bytes((long long)m.rows + m.S, 4) +
+                 (csc ? carve_bytes(U_max + 1, 4) : 0) + carve_bytes(2, 4) +
+                 carve_bytes(2ll * (tiles(m.rows, kScanTile) + tiles(m.S, kScanTile)), 4);
+  s.scratch_bytes = carve_bytes(m.N, 4) * 5 +              // key_e slot_e rank_e gk gv
+                    carve_bytes(m.rows, 4) + carve_bytes(U_max, 4);   // long lists
+  return s;
 }
 
-static long long umax_of(const LayerMeta& m) { return m.N < m.S ? m.N : m.S; }
+void carve_layer(const LayerMeta& m, bool csc, char*& zp, char*& sp, BLayer* L) {
+  const long long U_max = umax_of(m);
+  L->t_rows = tiles(m.rows, kScanTile);
+  L->t_slots = tiles(m.S, kScanTile);
+  L->cnt = carve<int>(zp, (long long)m.rows + m.S);
+  L->ccur = csc ? carve<int>(zp, U_max + 1) : nullptr;
+  L->lcnt = carve<int>(zp, 2);
+  L->sst = reinterpret_cast<unsigned long long*>(
+      carve<int>(zp, 2ll * (L->t_rows + L->t_slots)));
+  L->key_e = carve<int>(sp, m.N);
+  L->slot_e = carve<int>(sp, m.N);
+  L->rank_e = carve<int>(sp, m.N);
+  L->gk = carve<int>(sp, m.N);
+  L->gv = carve<int>(sp, m.N);
+  L->long_rows = carve<int>(sp, m.rows);
+  L->long_cols = carve<int>(sp, U_max);
+}
 
+}  // namespace
 }  // namespace hf
 
 using namespace hf;
@@ -471,7 +887,10 @@ hifuse_status hifuse_csr_sizes(const hifuse_layer_shape* shape, hifuse_layout la
   if (rows) *rows = m.rows;
   if (U_max) *U_max = umax_of(m);
   if (S) *S = m.S;
-  if (ws_bytes) *ws_bytes = build_ws(m, umax_of(m), nullptr, nullptr);
+  if (ws_bytes) {
+    const LayerWs w = layer_ws_sizes(m, true);
+    *ws_bytes = (size_t)(w.zero_bytes + w.scratch_bytes);
+  }
   return HIFUSE_OK;
 }
 
@@ -490,72 +909,132 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       (num_graph_edges > 0 && !d_edge_type && !d_rel_edge_off))
     return HIFUSE_ERR_INVALID_ARG;
   cudaStream_t s = st(stream);
-  static const int dbg = getenv("HIFUSE_DBG_SORT") ? atoi(getenv("HIFUSE_DBG_SORT")) : 0;
   std::vector<LayerMeta> metas(num_layers);
-  LayerMeta* mv = metas.data();
-  hifuse_status rc = HIFUSE_OK;
-  for (int l = 0; l < num_layers && rc == HIFUSE_OK; l++) {
-    rc = make_meta(&shapes[l], &mv[l]);
-    if (rc != HIFUSE_OK) break;
+  for (int l = 0; l < num_layers; l++) {
+    hifuse_status rc = make_meta(&shapes[l], &metas[l]);
+    if (rc != HIFUSE_OK) return rc;
+    const LayerMeta& m = metas[l];
     const hifuse_csr& o = out[l];
     if (!o.rel_row_off || !o.row_ptr || !o.rel_y_off || !o.U_dev ||
-        (mv[l].N > 0 && (!d_src_local[l] || !d_dst_local[l] || !d_edge_id[l] || !o.col ||
-                         !o.eperm || !o.y_src)) ||
-        (!o.col_ptr != !o.csc_pos || !o.col_ptr != !o.csc_row) ||
-        (mv[l].S > 0 && !o.slot_y))
-      rc = HIFUSE_ERR_INVALID_ARG;
-    else if (build_ws(mv[l], umax_of(mv[l]), nullptr, nullptr) > ws_bytes || !d_ws)
-      rc = HIFUSE_ERR_WORKSPACE;
+        (m.N > 0 && (!d_src_local[l] || !d_dst_local[l] || !d_edge_id[l] || !o.col ||
+                     !o.eperm || !o.y_src)) ||
+        (!o.col_ptr != !o.csc_pos || !o.col_ptr != !o.csc_row) || (m.S > 0 && !o.slot_y))
+      return HIFUSE_ERR_INVALID_ARG;
+    if (m.N >= (1 << 30) || m.S >= (1 << 30)) return HIFUSE_ERR_UNSUPPORTED;   // status packing
   }
-  if (rc != HIFUSE_OK) return rc;
-  for (int l = 0; l < num_layers; l++) {
-    const LayerMeta& m = mv[l];
-    const hifuse_csr& o = out[l];
-    long long U_max = umax_of(m);
-    BuildWs w;
-    build_ws(m, U_max, (char*)d_ws, &w);
-    long long nz = (long long)m.rows + m.S;
-    cudaMemsetAsync(w.cnt, 0, sizeof(int) * (nz > 0 ? nz : 1), s);
-    cudaMemsetAsync(w.cur, 0, sizeof(int) * (m.rows > 0 ? m.rows : 1), s);
-    // the transpose (CSC) is optional: a layer whose aggregation backward is
-    // never run (the input layer of the aggregate-first RGCN) passes NULLs
-    const bool csc = o.col_ptr != nullptr;
-    if (csc) {
-      cudaMemsetAsync(w.ccnt, 0, sizeof(int) * (U_max + 1), s);
-      cudaMemsetAsync(w.ccur, 0, sizeof(int) * (U_max + 1), s);
+  // the layer sets of kMaxL layers run in order, each from the start of d_ws
+  size_t need = 0;
+  for (int l0 = 0; l0 < num_layers; l0 += kMaxL) {
+    size_t set = 0;
+    for (int l = l0; l < std::min(num_layers, l0 + kMaxL); l++) {
+      const LayerWs w = layer_ws_sizes(metas[l], out[l].col_ptr != nullptr);
+      set += w.zero_bytes + w.scratch_bytes;
     }
-    cudaMemsetAsync(w.counters, 0, sizeof(int) * 2, s);
-    const int TB = 256;
-    HF_LAUNCH(k_classify, ceil_div(m.N, TB), TB, 0, s, m, d_src_local[l], d_dst_local[l],
-              (const long long*)d_edge_id[l], d_edge_type, (const long long*)d_rel_edge_off,
-              (long long)num_graph_edges, w.key_e,
-              w.slot_e, w.cnt, d_status);
-    exclusive_scan(w.cnt, w.pre, nz, w.scan, s);
-    long long fin = nz + 1 > m.R + 1 ? nz + 1 : m.R + 1;
-    HF_LAUNCH(k_finish, ceil_div(fin, TB), TB, 0, s, m, w.cnt, w.pre, o.row_ptr, o.rel_row_off,
-              o.rel_y_off, o.y_src, o.slot_y, o.U_dev);
-    HF_LAUNCH(k_scatter, ceil_div(m.N, TB), TB, 0, s, m, w.key_e, w.slot_e, o.row_ptr, o.slot_y,
-              w.cur, w.ccnt, o.eperm, o.col, o.csc_pos, o.csc_row);
-    if (csc) exclusive_scan(w.ccnt, o.col_ptr, U_max, w.scan, s);
-    int* rows_long = w.lists;
-    int* cols_long = w.lists + m.rows;
-    HF_LAUNCH(k_fix_rows, ceil_div(m.rows, 16), 256, 0, s, m.rows, o.row_ptr, o.eperm, o.col,
-              o.col_ptr, w.ccur, o.csc_pos, o.csc_row, rows_long, w.counters);
-    HF_LAUNCH(k_sort_long<true>, 148, kSortThreads, 0, s, o.row_ptr, o.eperm, o.col, o.col_ptr, w.ccur,
-              o.csc_pos, o.csc_row, rows_long, w.counters, w.gk, w.gv, dbg);
-    if (!csc) continue;
-    HF_LAUNCH(k_fix_cols, ceil_div(U_max, 256), 256, 0, s, o.U_dev, o.col_ptr, o.csc_pos,
-              o.csc_row, cols_long, w.counters + 1);   // 8 warps x 32 columns per block
-    HF_LAUNCH(k_sort_long<false>, 148, kSortThreads, 0, s, o.col_ptr, o.csc_pos, o.csc_row,
-              (const int*)nullptr, (int*)nullptr, (int*)nullptr, (int*)nullptr, cols_long,
-              w.counters + 1, w.gk, w.gv, dbg);
+    need = std::max(need, set);
+  }
+  if (!d_ws || need > ws_bytes) return HIFUSE_ERR_WORKSPACE;
+  set_max_smem((const void*)k_scan, (int)kSmem);
+  set_max_smem((const void*)k_rows, (int)kSmem);
+  set_max_smem((const void*)k_cols, (int)kSmem);
+  for (int l0 = 0; l0 < num_layers; l0 += kMaxL) {
+    const int nl = std::min(kMaxL, num_layers - l0);
+    BuildParams bp;
+    memset(&bp, 0, sizeof(bp));
+    BPlan& P = bp.p;
+    P.L = nl;
+    P.E = num_graph_edges;
+    P.edge_type = d_edge_type;
+    P.rel_off = (const long long*)d_rel_edge_off;
+    P.status = d_status;
+    long long zero_total = 0;
+    for (int q = 0; q < nl; q++)
+      zero_total += layer_ws_sizes(metas[l0 + q], out[l0 + q].col_ptr != nullptr).zero_bytes;
+    char* zp = (char*)d_ws;
+    char* sp = (char*)d_ws + zero_total;
+    int blocks[kKerns][kMaxL] = {};
+    for (int q = 0; q < nl; q++) {
+      const LayerMeta& m = metas[l0 + q];
+      const hifuse_csr& o = out[l0 + q];
+      BLayer& L = bp.lay[q];
+      const bool csc = o.col_ptr != nullptr;
+      carve_layer(m, csc, zp, sp, &L);
+      L.R = m.R; L.N = m.N; L.rows = m.rows; L.S = m.S;
+      L.U_max = (int)umax_of(m);
+      L.csc = csc;
+      for (int r = 0; r <= m.R; r++) {
+        L.key_base[r] = m.rel_row_off[r];
+        L.slot_base[r] = m.slot_off[r];
+      }
+      for (int r = 0; r < m.R; r++) {
+        L.src_lim[r] = m.n_src[m.rel_src[r]];
+        L.dst_lim[r] = m.n_dst[m.rel_dst[r]];
+      }
+      L.src = d_src_local[l0 + q];
+      L.dst = d_dst_local[l0 + q];
+      L.eid = (const long long*)d_edge_id[l0 + q];
+      L.o_rel_row_off = o.rel_row_off; L.row_ptr = o.row_ptr; L.col = o.col; L.eperm = o.eperm;
+      L.o_rel_y_off = o.rel_y_off; L.y_src = o.y_src; L.col_ptr = o.col_ptr;
+      L.csc_pos = o.csc_pos; L.csc_row = o.csc_row; L.slot_y = o.slot_y; L.U_dev = o.U_dev;
+      const int et = m.N > 0 ? tiles(m.N, kEdgeTile) : 0;
+      blocks[K_CLASSIFY][q] = et;
+      blocks[K_SCAN][q] = L.t_rows + L.t_slots;
+      blocks[K_SCATTER][q] = et;
+      L.rows_reg = m.rows > 0 ? tiles(m.rows, kSegTile) : 0;
+      L.cols_reg = csc ? tiles((long long)L.U_max + 1, kSegTile) : 0;
+      L.cols_xtra = csc && m.N > 0 ? 2 * sm_count() : 0;
+      blocks[K_ROWS][q] = L.rows_reg + (m.rows > 0 ? kLongRowBlocks : 0);
+      blocks[K_COLS][q] = L.cols_reg + L.cols_xtra;
+    }
+    int total[kKerns];
+    for (int k = 0; k < kKerns; k++) {
+      int acc = 0;
+      for (int q = 0; q <= kMaxL; q++) {
+        P.blk_off[k][q] = acc;
+        if (q < nl) acc += blocks[k][q];
+      }
+      total[k] = acc;
+    }
+    cudaMemsetAsync(d_ws, 0, (size_t)zero_total, s);
+    HF_LAUNCH(k_classify, total[K_CLASSIFY], kBT, 0, s, bp);
+    HF_LAUNCH(k_scan, total[K_SCAN], kBT, kSmem, s, bp);
+    HF_LAUNCH(k_scatter, total[K_SCATTER], kBT, 0, s, bp);
+    HF_LAUNCH(k_rows, total[K_ROWS], kBT, kSmem, s, bp);
+    HF_LAUNCH(k_cols, total[K_COLS], kBT, kSmem, s, bp);
   }
   return last_cuda();
 }
 
-hifuse_status hifuse_edge_type_offsets(const int32_t* d_edge_type, int64_t num_graph_edges,
-                                       int num_rels, int64_t* d_rel_edge_off, int32_t* d_status,
-                                       hifuse_stream_t stream) {
+}  // extern "C"
+
+// ------------------------------------------------- edge-type preprocessing --
+namespace hf {
+namespace {
+// d_rel_edge_off[r] = lower bound of r in the (sorted) edge-type table.
+__global__ void k_et_offsets(const int* __restrict__ et, long long E, int R,
+                             long long* __restrict__ off) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > R) return;
+  long long lo = 0, hi = E;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (et[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  off[r] = r == R ? E : lo;
+}
+
+__global__ void k_et_check(const int* __restrict__ et, long long E, int R, int* __restrict__ status) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const int v = et[i];
+  if (v < 0 || v >= R || (i > 0 && et[i - 1] > v)) atomicOr(status, HIFUSE_ST_UNSORTED_TYPES);
+}
+}  // namespace
+}  // namespace hf
+
+extern "C" hifuse_status hifuse_edge_type_offsets(const int32_t* d_edge_type,
+                                                  int64_t num_graph_edges, int num_rels,
+                                                  int64_t* d_rel_edge_off, int32_t* d_status,
+                                                  hifuse_stream_t stream) {
   if (num_graph_edges < 0 || num_rels <= 0 || num_rels > HF_MAX_R || !d_rel_edge_off ||
       !d_status || (num_graph_edges > 0 && !d_edge_type))
     return HIFUSE_ERR_INVALID_ARG;
@@ -567,5 +1046,3 @@ hifuse_status hifuse_edge_type_offsets(const int32_t* d_edge_type, int64_t num_g
             (long long)num_graph_edges, num_rels, (long long*)d_rel_edge_off);
   return last_cuda();
 }
-
-}  // extern "C"

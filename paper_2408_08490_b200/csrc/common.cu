@@ -1,6 +1,10 @@
 // common.cu -- layer metadata, device-wide scan, status helpers.
 #include "common.cuh"
 
+#include <map>
+#include <mutex>
+#include <set>
+
 namespace hf {
 
 std::atomic<int64_t> g_launches{0};
@@ -49,24 +53,63 @@ hifuse_status make_meta(const hifuse_layer_shape* s, LayerMeta* m) {
   return HIFUSE_OK;
 }
 
-// ---------------------------------------------------------------- branch ---
-bool branch_begin(cudaStream_t main, Branch* b, int idx) {
-  static Branch per_dev[64][4];
-  static bool made[64][4] = {};
-  int dev = 0;
-  if (idx < 0 || idx >= 4) return false;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
-  if (!made[dev][idx]) {
-    cudaStreamCaptureStatus cs;
-    if (cudaStreamIsCapturing(main, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-      return false;                      // creating streams/events is not capture-safe
-    Branch& n = per_dev[dev][idx];
-    if (cudaStreamCreateWithFlags(&n.side, cudaStreamNonBlocking) != cudaSuccess) return false;
-    cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming);
-    made[dev][idx] = true;
+// ------------------------------------------------------- per-stream state ---
+// Fork/join resources (auxiliary streams + events) are owned per (device,
+// caller stream): calls issued on different streams (or from different host
+// threads, one stream each) never share an event or a side stream, so there
+// is no hidden cross-stream dependency and no record/wait race.  The map is
+// mutex-protected; entries are created on first use or by
+// hifuse_stream_attach (outside graph capture), and freed by
+// hifuse_stream_release.
+namespace {
+struct StreamKey {
+  int dev;
+  cudaStream_t s;
+  bool operator<(const StreamKey& o) const { return dev != o.dev ? dev < o.dev : s < o.s; }
+};
+std::mutex g_mu;
+std::map<StreamKey, StreamCtx*> g_ctx;
+std::map<std::pair<int, const void*>, int> g_smem;
+int g_sm[64] = {};
+}  // namespace
+
+static StreamCtx* make_ctx() {
+  StreamCtx* c = new StreamCtx();
+  for (int i = 0; i < kBranches; i++) {
+    Branch& n = c->br[i];
+    if (cudaStreamCreateWithFlags(&n.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      c->ok = false;
+      return c;
+    }
   }
-  *b = per_dev[dev][idx];
+  if (cudaEventCreateWithFlags(&c->fold, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    c->ok = false;
+    return c;
+  }
+  c->ok = true;
+  return c;
+}
+
+StreamCtx* stream_ctx(cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_ctx.find(StreamKey{dev, s});
+  if (it != g_ctx.end()) return it->second->ok ? it->second : nullptr;
+  StreamCtx* c = make_ctx();
+  g_ctx[StreamKey{dev, s}] = c;
+  return c->ok ? c : nullptr;
+}
+
+bool branch_begin(cudaStream_t main, Branch* b, int idx) {
+  if (idx < 0 || idx >= kBranches) return false;
+  StreamCtx* c = stream_ctx(main);
+  if (!c) return false;                  // run the branch serially on `main`
+  *b = c->br[idx];
   cudaEventRecord(b->fork, main);
   cudaStreamWaitEvent(b->side, b->fork, 0);
   return true;
@@ -75,6 +118,31 @@ bool branch_begin(cudaStream_t main, Branch* b, int idx) {
 void branch_end(cudaStream_t main, const Branch& b) {
   cudaEventRecord(b.join, b.side);
   cudaStreamWaitEvent(main, b.join, 0);
+}
+
+void set_max_smem(const void* kernel, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  int& cur = g_smem[{dev, kernel}];
+  if (bytes <= cur) return;
+  // raised to the largest request seen so far on this device
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+      cudaSuccess)
+    cur = bytes;
+  else
+    cudaGetLastError();
+}
+
+int sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int v = __atomic_load_n(&g_sm[dev], __ATOMIC_RELAXED);
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+    v = 148;
+  __atomic_store_n(&g_sm[dev], v, __ATOMIC_RELAXED);
+  return v;
 }
 
 // ------------------------------------------------------------------ scan ---
@@ -234,5 +302,41 @@ hifuse_status hifuse_read_status(const int32_t* d_status, hifuse_stream_t stream
 }
 
 int64_t hifuse_kernel_launches(void) { return hf::g_launches.load(); }
+
+}  // extern "C"
+
+extern "C" {
+
+hifuse_status hifuse_stream_attach(hifuse_stream_t stream) {
+  cudaStreamCaptureStatus cs;
+  cudaStream_t s = hf::st(stream);
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) return HIFUSE_ERR_CUDA;
+  if (cs != cudaStreamCaptureStatusNone) return HIFUSE_ERR_INVALID_ARG;
+  return hf::stream_ctx(s) ? HIFUSE_OK : HIFUSE_ERR_CUDA;
+}
+
+hifuse_status hifuse_stream_release(hifuse_stream_t stream) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HIFUSE_ERR_CUDA;
+  hf::StreamCtx* c = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(hf::g_mu);
+    auto it = hf::g_ctx.find(hf::StreamKey{dev, hf::st(stream)});
+    if (it == hf::g_ctx.end()) return HIFUSE_OK;
+    c = it->second;
+    hf::g_ctx.erase(it);
+  }
+  if (c->ok) {
+    for (int i = 0; i < hf::kBranches; i++) {
+      cudaStreamSynchronize(c->br[i].side);
+      cudaStreamDestroy(c->br[i].side);
+      cudaEventDestroy(c->br[i].fork);
+      cudaEventDestroy(c->br[i].join);
+    }
+    cudaEventDestroy(c->fold);
+  }
+  delete c;
+  return HIFUSE_OK;
+}
 
 }  // extern "C"

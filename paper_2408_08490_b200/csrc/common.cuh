@@ -74,18 +74,31 @@ __device__ __forceinline__ int upper_bound_i(const int* a, int n, int x) {
   return lo;
 }
 
-// Fork/join of one call's independent kernels onto an auxiliary stream (per
-// device, created on first use outside graph capture): record `fork` on the
-// caller's stream, run the branch on `side`, record `join` there and make the
-// caller's stream wait for it.  Works eagerly and under CUDA-graph capture
-// (the branch becomes a parallel graph path).  Returns false (run serially)
-// before the stream exists.
+// Fork/join of one call's independent kernels onto an auxiliary stream:
+// record `fork` on the caller's stream, run the branch on `side`, record
+// `join` there and make the caller's stream wait for it.  Works eagerly and
+// under CUDA-graph capture (the branch becomes a parallel graph path).  The
+// side streams and events belong to the caller's stream (StreamCtx, one per
+// (device, caller stream)); returns false (run serially) if they cannot be
+// created.
 struct Branch {
   cudaStream_t side;
   cudaEvent_t fork, join;
 };
-bool branch_begin(cudaStream_t main, Branch* b, int idx = 0);   // idx < 4: independent branches
+constexpr int kBranches = 4;
+struct StreamCtx {
+  Branch br[kBranches];
+  cudaEvent_t fold;     // orders the RGAT dX term after the W a_dst fold (project.cu)
+  bool ok;
+};
+StreamCtx* stream_ctx(cudaStream_t s);   // nullptr if the resources cannot be created
+bool branch_begin(cudaStream_t main, Branch* b, int idx = 0);   // idx < kBranches
 void branch_end(cudaStream_t main, const Branch& b);
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize once per (device, kernel).
+void set_max_smem(const void* kernel, int bytes);
+// Multiprocessor count of the current device (cached device attribute).
+int sm_count();
 
 // Device-wide exclusive scan of int32 counts (reduce-then-scan, 3 kernels).
 // out[0..n] receives the exclusive prefix, out[n] = total.  ws: scan_ws_ints(n).

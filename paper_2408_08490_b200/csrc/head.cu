@@ -160,7 +160,8 @@ k_head_logits(int B, int D, int C, const float* __restrict__ Hs, const float* __
 template <int NV>
 __global__ void __launch_bounds__(256)
 k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__ lg,
-               float* __restrict__ block_loss, int* __restrict__ ticket, float* __restrict__ loss) {
+               float* __restrict__ block_loss, int* __restrict__ ticket, float* __restrict__ loss,
+               int* __restrict__ status) {
   __shared__ float s_l[8];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -168,8 +169,13 @@ k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__
   float rl = 0.f;
   if (b < B) {
     float* x = lg + (long long)b * C;
-    const int y = labels[b];
-    const float inv = 1.f / (float)B;
+    // a label outside [0, C) drops the row (no loss term, zero gradient) and
+    // sets HIFUSE_ST_BAD_LABEL; it is never used as an index
+    const int y0 = labels[b];
+    const bool ok = (unsigned)y0 < (unsigned)C;
+    const int y = ok ? y0 : 0;
+    if (!ok && lane == 0 && status) atomicOr(status, HIFUSE_ST_BAD_LABEL);
+    const float inv = ok ? 1.f / (float)B : 0.f;
     float mx = -INFINITY, se = 0.f, ly;
     if constexpr (NV > 0) {
       float v[NV];
@@ -200,7 +206,7 @@ k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__
         const int c = lane + 32 * q;
         if (c < C) x[c] = (v[q] / se - (c == y ? 1.f : 0.f)) * inv;
       }
-      rl = logf(se) + mx - ly;
+      rl = ok ? logf(se) + mx - ly : 0.f;
     } else {
       for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
       for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -209,7 +215,7 @@ k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__
       ly = x[y];
       __syncwarp();
       for (int c = lane; c < C; c += 32) x[c] = (expf(x[c] - mx) / se - (c == y ? 1.f : 0.f)) * inv;
-      rl = logf(se) + mx - ly;
+      rl = ok ? logf(se) + mx - ly : 0.f;
     }
   }
   if (lane == 0) s_l[w] = rl;
@@ -243,7 +249,7 @@ __global__ void __launch_bounds__(256)
 k_head_small(int B, int C, const float* __restrict__ Hs, const float* __restrict__ Wc,
              const float* __restrict__ bc, const int* __restrict__ labels,
              float* __restrict__ dlog, float* __restrict__ dHs, float* __restrict__ block_loss,
-             int* __restrict__ ticket, float* __restrict__ loss) {
+             int* __restrict__ ticket, float* __restrict__ loss, int* __restrict__ status) {
   constexpr int KPL = D / 32;              // features per lane
   __shared__ float s_l[8];
   __shared__ int s_last;
@@ -282,11 +288,15 @@ k_head_small(int B, int C, const float* __restrict__ Hs, const float* __restrict
     const float ex = act ? expf(z - mx) : 0.f;
     float se = ex;
     for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-    const int y = labels[b];
+    // a label outside [0, C) drops the row (HIFUSE_ST_BAD_LABEL)
+    const int y0 = labels[b];
+    const bool ok = (unsigned)y0 < (unsigned)C;
+    const int y = ok ? y0 : 0;
+    if (!ok && lane == 0 && status) atomicOr(status, HIFUSE_ST_BAD_LABEL);
     const float zy = __shfl_sync(0xffffffffu, z, y);
-    const float g = act ? (ex / se - (lane == y ? 1.f : 0.f)) / (float)B : 0.f;
+    const float g = act && ok ? (ex / se - (lane == y ? 1.f : 0.f)) / (float)B : 0.f;
     if (act) dlog[(long long)b * C + lane] = g;
-    rl = logf(se) + mx - zy;
+    rl = ok ? logf(se) + mx - zy : 0.f;
 #pragma unroll
     for (int j = 0; j < KPL; j++) {
       const int k = j * 32 + lane;
@@ -441,7 +451,7 @@ size_t hifuse_xent_ws_bytes(int B, int D, int C) {
 hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t h_rows,
                                  int64_t h_row0, const int32_t* d_labels, const float* d_Wc,
                                  const float* d_bc, float* d_loss, float* d_dH, float* d_dWc,
-                                 float* d_dbc, void* d_ws, size_t ws_bytes,
+                                 float* d_dbc, void* d_ws, size_t ws_bytes, int32_t* d_status,
                                  hifuse_stream_t stream) {
   if (B <= 0 || D <= 0 || C <= 0 || h_row0 < 0 || h_row0 + B > h_rows || !d_H || !d_labels ||
       !d_Wc || !d_bc || !d_loss || !d_dH || (!d_dWc != !d_dbc))
@@ -463,7 +473,7 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
     HF_LAUNCH(k_zero_int, 1, 1, 0, s, ticket);
 #define HF_SMALL(DD, CC)                                                                      \
   HF_LAUNCH((k_head_small<DD, CC>), nblk, 256, 0, s, B, C, Hs, d_Wc, d_bc, d_labels, dlog,      \
-            d_dH + h_row0 * D, block_loss, ticket, d_loss)
+            d_dH + h_row0 * D, block_loss, ticket, d_loss, d_status)
     if (D == 128) { if (C <= 8) HF_SMALL(128, 8); else HF_SMALL(128, 32); }
     else { if (C <= 8) HF_SMALL(64, 8); else HF_SMALL(64, 32); }
 #undef HF_SMALL
@@ -478,13 +488,13 @@ hifuse_status hifuse_linear_xent(int B, int D, int C, const float* d_H, int64_t 
             d_Wc, d_bc, dlog, ticket, 1);
   if (C <= 128)
     HF_LAUNCH(k_head_softmax<4>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket,
-              d_loss);
+              d_loss, d_status);
   else if (C <= 512)
     HF_LAUNCH(k_head_softmax<16>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket,
-              d_loss);
+              d_loss, d_status);
   else
     HF_LAUNCH(k_head_softmax<0>, nblk, 256, 0, s, B, C, d_labels, dlog, block_loss, ticket,
-              d_loss);
+              d_loss, d_status);
   if (!d_dWc) h.dw_tiles = 0;          // weight gradient deferred to hifuse_linear_xent_wgrad
   HF_LAUNCH(k_head_grads, (h.dh_tiles + h.dw_tiles) * kSlices, 128, 0, s, B, D, C, h, Hs, d_Wc,
             dlog, d_dH + h_row0 * D, d_dWc, d_dbc);

@@ -780,20 +780,11 @@ size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D
   return b;
 }
 
-// One event per device ordering k_dx_sdst (dgrad branch) after the fold of
-// W a_dst (source-side attention branch); created outside graph capture.
+// The event ordering k_dx_sdst (dgrad branch) after the fold of W a_dst
+// (source-side attention branch): owned by the caller's stream.
 static cudaEvent_t fold_event(cudaStream_t s) {
-  static cudaEvent_t ev[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!ev[dev]) {
-    cudaStreamCaptureStatus cs;
-    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-      return nullptr;
-    if (cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming) != cudaSuccess)
-      return nullptr;
-  }
-  return ev[dev];
+  StreamCtx* c = stream_ctx(s);
+  return c ? c->fold : nullptr;
 }
 
 static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hifuse_csr* csr,
@@ -982,7 +973,7 @@ static long long direct_max_chunks(const LayerMeta& m, int step) {
   return ((long long)m.rows + m.dst_rows) / step + m.R + m.T + 1;
 }
 static int direct_chunk_rows(const LayerMeta& m) {
-  long long ch = ((long long)m.rows + m.dst_rows) / (2 * 148);
+  long long ch = ((long long)m.rows + m.dst_rows) / (2 * sm_count());
   ch = (ch + 31) / 32 * 32;
   return (int)(ch < 128 ? 128 : (ch > kCHT ? kCHT : ch));
 }

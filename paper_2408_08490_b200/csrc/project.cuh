@@ -59,7 +59,7 @@ hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot
 static constexpr int kCHT = 1024;
 inline int wgrad_chunk_rows(const LayerMeta& m) {
   long long rows = (long long)(m.N < m.S ? m.N : m.S) + m.dst_rows;
-  long long ch = rows / (2 * 148);
+  long long ch = rows / (2 * sm_count());
   ch = (ch + 31) / 32 * 32;
   return (int)(ch < 128 ? 128 : (ch > kCHT ? kCHT : ch));
 }

@@ -21,7 +21,6 @@
 #include <cstdlib>
 #include "project.cuh"
 #include "tc_common.cuh"
-#include "tma.cuh"
 
 namespace hf {
 
@@ -223,134 +222,6 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   if (warp == 0) tmem_dealloc(tmem, KN < 32 ? 32 : KN);
 }
 
-// TMA variant of the dgrad (the default): one thread streams each chunk with
-// 32 tile::gather4 copies (4 dYt rows of 128 B each, absent rows = -1 are
-// zero-filled by the TMA unit) plus one 3-D tile copy of the KN x 32 slice of
-// W_term, all completing on the stage's mbarrier by byte count; everything is
-// in the async proxy, so there is no proxy fence and no thread waits for its
-// own copies.  One thread issues the MMAs; four warps run the epilogue.
-template <int K, int D, int KN>
-__global__ void __launch_bounds__(192)
-k_dgrad_tma(DgradMeta dm, const __grid_constant__ CUtensorMap map_dy,
-            const __grid_constant__ CUtensorMap map_g, const __grid_constant__ CUtensorMap map_wr,
-            const __grid_constant__ CUtensorMap map_wt, const int* __restrict__ slot_y,
-            float* __restrict__ dX) {
-  constexpr int BM = 128, DC = D / 32, NS = K / KN;
-  constexpr uint32_t A_STAGE = BM * 128, B_STAGE = KN * 128, STAGE = A_STAGE + B_STAGE;
-  constexpr uint32_t IDESC = idesc_tf32(BM, KN, 0, 0);
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[kDgStages], empty[kDgStages], done;
-  __shared__ uint32_t tmem_slot;
-  const int tile = blockIdx.x / NS, n0 = (blockIdx.x % NS) * KN;
-  const int s_ = upper_bound_i(dm.tile_off, dm.T + 1, tile) - 1;
-  const int j0 = (tile - dm.tile_off[s_]) * BM;
-  const int nrows = min(BM, dm.n_src[s_] - j0);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  int* s_arow = reinterpret_cast<int*>(smem_raw + (base - smem_u32(smem_raw)) + kDgStages * STAGE);
-  if (tid == 0) {
-    for (int q = 0; q < kDgStages; q++) {
-      mbar_init(smem_u32(&full[q]), 1);
-      mbar_init(smem_u32(&empty[q]), 1);
-    }
-    mbar_init(smem_u32(&done), 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), KN < 32 ? 32 : KN);
-  const int nout = dm.out_off[s_ + 1] - dm.out_off[s_];
-  const int nterm = nout + (dm.has_root ? 1 : 0);
-  const int NC = nterm * DC;
-  // dYt row of every (term, tile row) (-1: absent -> zero-filled by the TMA)
-  if (tid < BM) {
-    const int j = j0 + tid;
-    for (int t0 = 0; t0 < nout; t0 += 8) {
-      int v[8];
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        const int term = t0 + u;
-        v[u] = (term < nout && tid < nrows)
-                   ? slot_y[dm.slot_off[dm.out_rel[dm.out_off[s_] + term]] + j] : -1;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; u++)
-        if (t0 + u < nout) s_arow[(t0 + u) * BM + tid] = v[u];
-    }
-    if (dm.has_root)      // root term: rows of G (the destination prefix of type s)
-      s_arow[nout * BM + tid] = (tid < nrows && j < dm.n_dst[s_]) ? dm.type_dst_off[s_] + j : -1;
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-
-  if (warp == 4) {
-    if (lane == 0) {
-      // --------------------------------------------------------- producer
-      for (int c = 0; c < NC; c++) {
-        const int st = c % kDgStages;
-        if (c >= kDgStages) mbar_wait(smem_u32(&empty[st]), ((c / kDgStages) - 1) & 1);
-        const int term = c / DC, d0 = (c % DC) * 32;
-        const bool root = term == nout;
-        const uint32_t bar = smem_u32(&full[st]);
-        const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
-        mbar_arrive_expect_tx(bar, STAGE);
-        const void* amap = root ? (const void*)&map_g : (const void*)&map_dy;
-        const int* ids = s_arow + term * BM;
-#pragma unroll 4
-        for (int g = 0; g < BM / 4; g++)
-          tma_gather4(sa + g * 512, amap, bar, d0, ids[4 * g], ids[4 * g + 1], ids[4 * g + 2],
-                      ids[4 * g + 3]);
-        if (root) tma_load_3d(sb, &map_wt, bar, d0, n0, s_);
-        else tma_load_3d(sb, &map_wr, bar, d0, n0, dm.out_rel[dm.out_off[s_] + term]);
-      }
-    }
-  } else if (warp == 5) {
-    if (lane == 0) {
-      // -------------------------------------------------------------- MMA
-      for (int c = 0; c < NC; c++) {
-        const int st = c % kDgStages;
-        mbar_wait(smem_u32(&full[st]), (c / kDgStages) & 1);
-        tc_fence_after();
-        const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-          mma_tf32(tmem, sw128_desc(sa + k * 32, 16, 1024), sw128_desc(sb + k * 32, 16, 1024),
-                   IDESC, (c | k) ? 1u : 0u);
-        mma_commit(smem_u32(&empty[st]));
-      }
-      mma_commit(smem_u32(&done));
-    }
-  } else {
-    // ------------------------------------------------------------- epilogue
-    if (NC > 0) {
-      mbar_wait(smem_u32(&done), 0);
-      tc_fence_after();
-    }
-    const int row = warp * 32 + lane;
-    float* orow = dX + (long long)(dm.type_src_off[s_] + j0 + row) * K + n0;
-#pragma unroll
-    for (int c0 = 0; c0 < KN; c0 += 16) {
-      float v[16];
-      if (NC > 0) {
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; q++) v[q] = 0.f;
-      }
-      if (row < nrows) {
-        float4* o = reinterpret_cast<float4*>(orow + c0);
-        o[0] = make_float4(v[0], v[1], v[2], v[3]);
-        o[1] = make_float4(v[4], v[5], v[6], v[7]);
-        o[2] = make_float4(v[8], v[9], v[10], v[11]);
-        o[3] = make_float4(v[12], v[13], v[14], v[15]);
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, KN < 32 ? 32 : KN);
-}
-
 __device__ __forceinline__ void group_table_warp(const ProjMeta& pm, const int* s_yoff, int step,
                                                  int* s_tab, int lane);
 
@@ -520,35 +391,10 @@ static void launch_dgrad(const DgradMeta& dm, int max_out, const int* slot_y, co
                          const float* G, const float* W_rel, const float* W_root, float* dX,
                          cudaStream_t s) {
   const int smem = dgrad_smem<K, D, KN>() + max_out * 128 * 4;
-  static int attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_dgrad_tc<K, D, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = smem;
-  }
+  set_max_smem((const void*)k_dgrad_tc<K, D, KN>, smem);
   const unsigned grid = (unsigned)dm.tile_off[dm.T] * (K / KN);
   HF_LAUNCH((k_dgrad_tc<K, D, KN>), grid, 160, smem, s, dm, slot_y, dY, G, W_rel, W_root, dX,
             max_out);
-}
-
-template <int K, int D, int KN>
-static bool launch_dgrad_tma(const DgradMeta& dm, int max_out, long long dy_rows, int R,
-                             const int* slot_y, const float* dY, const float* G,
-                             const float* W_rel, const float* W_root, float* dX, cudaStream_t s) {
-  CUtensorMap my, mg, mwr, mwt;
-  const long long g_rows = dm.type_dst_off[dm.T];
-  if (!tma_map_rows(&my, dY, dy_rows > 0 ? dy_rows : 1, D, 32)) return false;
-  if (!tma_map_rows(&mg, G ? G : dY, G && g_rows > 0 ? g_rows : 1, D, 32)) return false;
-  if (!tma_map_3d(&mwr, W_rel, R, K, D, 32, KN)) return false;
-  if (!tma_map_3d(&mwt, W_root ? W_root : W_rel, W_root ? dm.T : R, K, D, 32, KN)) return false;
-  const int smem = dgrad_smem<K, D, KN>() + (max_out + 1) * 128 * 4;
-  static int attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_dgrad_tma<K, D, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = smem;
-  }
-  const unsigned grid = (unsigned)dm.tile_off[dm.T] * (K / KN);
-  HF_LAUNCH((k_dgrad_tma<K, D, KN>), grid, 192, smem, s, dm, my, mg, mwr, mwt, slot_y, dX);
-  return true;
 }
 
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
@@ -558,18 +404,6 @@ hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot
   int max_out = 0;
   for (int t = 0; t < dm.T; t++) max_out = std::max(max_out, dm.out_off[t + 1] - dm.out_off[t]);
   if (max_out > 128) return HIFUSE_ERR_UNSUPPORTED;
-  // TMA gather4 variant: opt-in (HIFUSE_DGRAD_TMA=1).  Measured on mag layer 1:
-  // 34 us vs 22 us for the cp.async producer warps (one thread issuing 32
-  // gather4 per chunk is bound by the TMA unit's per-request rate).
-  static const bool use_tma = getenv("HIFUSE_DGRAD_TMA") != nullptr;
-  if (use_tma && dy_rows > 0) {
-    bool ok;
-    if (K == 128 && D == 128) ok = launch_dgrad_tma<128, 128, 128>(dm, max_out, dy_rows, R, slot_y, dY, G, W_rel, W_root, dX, s);
-    else if (K == 128 && D == 64) ok = launch_dgrad_tma<128, 64, 128>(dm, max_out, dy_rows, R, slot_y, dY, G, W_rel, W_root, dX, s);
-    else if (K == 64 && D == 128) ok = launch_dgrad_tma<64, 128, 64>(dm, max_out, dy_rows, R, slot_y, dY, G, W_rel, W_root, dX, s);
-    else ok = launch_dgrad_tma<64, 64, 64>(dm, max_out, dy_rows, R, slot_y, dY, G, W_rel, W_root, dX, s);
-    if (ok) return HIFUSE_OK;
-  }
   // split the output features over two CTAs when that still leaves a small grid
   const bool split = false;   // measured: no gain from splitting the output features
   if (K == 128 && D == 128) {
@@ -592,13 +426,11 @@ hifuse_status wgrad_tc_launch(const LayerMeta& m, const ProjMeta& pm, int K, int
                               const float* G, float* partial, unsigned grid, cudaStream_t s,
                               const float* Xm) {
   (void)m;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_wgrad_tc<128, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<128, 128>());
-    cudaFuncSetAttribute(k_wgrad_tc<128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<128, 64>());
-    cudaFuncSetAttribute(k_wgrad_tc<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<64, 128>());
-    cudaFuncSetAttribute(k_wgrad_tc<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgrad_smem<64, 64>());
-    attr = true;
+  {
+    set_max_smem((const void*)k_wgrad_tc<128, 128>, wgrad_smem<128, 128>());
+    set_max_smem((const void*)k_wgrad_tc<128, 64>, wgrad_smem<128, 64>());
+    set_max_smem((const void*)k_wgrad_tc<64, 128>, wgrad_smem<64, 128>());
+    set_max_smem((const void*)k_wgrad_tc<64, 64>, wgrad_smem<64, 64>());
   }
 #define HF_WG(KK, DD)                                                                          \
   HF_LAUNCH((k_wgrad_tc<KK, DD>), grid, 128, (wgrad_smem<KK, DD>()), s, pm, CH, chunk_off,     \
@@ -866,13 +698,8 @@ static void launch_tcp(const ProjMeta& pm, const int* rel_off, const int* y_src,
                        const int* gather_ids, const float* X, const float* Xm,
                        const float* W_rel, const float* W_root, float* Y, float* R0,
                        const float* att, float* s_src, int H, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_proj_fwd_tcp<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         fwdp_smem<K, D>());
-    attr = true;
-  }
-  HF_LAUNCH((k_proj_fwd_tcp<K, D>), 148 * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
+  set_max_smem((const void*)k_proj_fwd_tcp<K, D>, fwdp_smem<K, D>());
+  HF_LAUNCH((k_proj_fwd_tcp<K, D>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
             rel_off, y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, Xm);
 }
 

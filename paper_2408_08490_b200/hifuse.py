@@ -13,8 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# HIFUSE_LIB: an alternative build of the same library (experiments only)
-LIB_PATH = os.environ.get("HIFUSE_LIB") or os.path.join(_HERE, "libhifuse.so")
+LIB_PATH = os.path.join(_HERE, "libhifuse.so")
 
 AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3}
 ACT = {"none": 0, "relu": 1}
@@ -102,13 +101,15 @@ def lib():
                                               vp, sz, vp],
             "hifuse_xent_ws_bytes": [i32, i32, i32],
             "hifuse_linear_xent": [i32, i32, i32, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp,
-                                   sz, vp],
+                                   sz, vp, vp],
             "hifuse_linear_xent_wgrad": [i32, i32, i32, vp, i64, i64, vp, vp, vp, sz, vp],
             "hifuse_sgd": [vp, vp, i64, f32, f32, vp],
             "hifuse_sample_caps": [vp, i32, vp, i64, vp, vp, vp, vp],
             "hifuse_sample_blocks": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, vp, i32, vp, vp,
                                      vp, sz, vp, vp],
             "hifuse_read_status": [vp, vp, vp],
+            "hifuse_stream_attach": [vp],
+            "hifuse_stream_release": [vp],
             "hifuse_kernel_launches": [],
         }
         for name, args in sig.items():
@@ -352,11 +353,12 @@ def xent_ws_bytes(B, D, C):
     return int(lib().hifuse_xent_ws_bytes(B, D, C))
 
 
-def linear_xent(B, D, C, H, h_row0, labels, Wc, bc, loss, dH, dWc, dbc, ws, stream=None):
+def linear_xent(B, D, C, H, h_row0, labels, Wc, bc, loss, dH, dWc, dbc, ws, status=None,
+                stream=None):
     _check("hifuse_linear_xent", lib().hifuse_linear_xent(
         B, D, C, _ptr(H), H.shape[0], h_row0, _ptr(labels), _ptr(Wc), _ptr(bc), _ptr(loss),
         _ptr(dH), _ptr(dWc), _ptr(dbc), _ptr(ws), ws.numel() * ws.element_size(),
-        _stream(stream)))
+        _ptr(status), _stream(stream)))
 
 
 def linear_xent_wgrad(B, D, C, H, h_row0, dWc, dbc, ws, stream=None):
@@ -403,3 +405,13 @@ def read_status(status, stream=None):
 
 def kernel_launches():
     return int(lib().hifuse_kernel_launches())
+
+
+def stream_attach(stream=None):
+    """hifuse_stream_attach: create the fork/join resources of `stream` (a
+    torch.cuda.Stream; default: the current stream) outside graph capture."""
+    _check("hifuse_stream_attach", lib().hifuse_stream_attach(_stream(stream)))
+
+
+def stream_release(stream=None):
+    _check("hifuse_stream_release", lib().hifuse_stream_release(_stream(stream)))

@@ -105,6 +105,16 @@ class Trainer:
             raise ValueError(order)
         self.agg_first = order == "agg_first" and model == "rgcn" and prec == "tf32"
         self.order = "agg_first" if self.agg_first else "project_first"
+        # capture streams: `_hi` (high priority) for the pipelined graphs,
+        # `_cap` for the serial / per-stage graphs; the library's fork/join
+        # resources of every stream that runs steps are created here, outside
+        # graph capture (hifuse_stream_attach)
+        self._hi = torch.cuda.Stream(device=device, priority=-1)
+        self._cap = torch.cuda.Stream(device=device)
+        self._head_side = torch.cuda.Stream(device=device)
+        with torch.cuda.device(device):
+            for s in (torch.cuda.current_stream(device), self._hi, self._cap, self._head_side):
+                hf.stream_attach(s)
 
     def load_params(self, p):
         for l, lay in enumerate(p["layers"]):
@@ -168,7 +178,7 @@ class Trainer:
         side stream while another batch computes."""
         dev, shapes = db.dev, db.shapes
         csrs = [self._csr(l, s, db.slot) for l, s in enumerate(shapes)]
-        wsb = self._ws(max(s.build_ws for s in shapes), key="ws_build")
+        wsb = self._ws(sum(s.build_ws for s in shapes), key="ws_build")   # layers built together
         off = self._et_offsets(edge_type)
         if not self.agg_first:
             return lambda: hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"],
@@ -247,8 +257,6 @@ class Trainer:
         last = shapes[-1]
         dH = self._mat(f"dH{L - 1}", last.dst_rows, D)
         wsx = self._ws(hf.xent_ws_bytes(db.B, D, C), key="ws_xent")
-        if not hasattr(self, "_head_side"):
-            self._head_side = torch.cuda.Stream(device=self.device)
 
         def side_op(fn):
             """Weight-gradient calls: on the side stream when split_head (a
@@ -265,7 +273,7 @@ class Trainer:
         Hl = acts[-1]["H"][:last.dst_rows]
         ops.append(("xent", lambda dH=dH: hf.linear_xent(
             db.B, D, C, Hl, db.h_row0, dev["labels"], self.P["Wc"], self.P["bc"], self.loss,
-            dH[:last.dst_rows], None, None, wsx)))
+            dH[:last.dst_rows], None, None, wsx, status=self.status)))
         ops.append(("xent_wgrad", side_op(lambda: hf.linear_xent_wgrad(
             db.B, D, C, Hl, db.h_row0, self.Gd["Wc"], self.Gd["bc"], wsx))))
         for l in range(L - 1, -1, -1):
@@ -368,7 +376,7 @@ class Trainer:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = hf.kernel_launches()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g, stream=self._cap):
             for _, fn in ops:
                 fn()
             if update and world == 1:
@@ -391,8 +399,6 @@ class Trainer:
         # the compute chain is captured on a high-priority stream, the build on
         # the (default-priority) side stream: the block scheduler favours the
         # critical path and the latency-bound build fills the gaps
-        if not hasattr(self, "_hi"):
-            self._hi = torch.cuda.Stream(priority=-1)
         with torch.cuda.graph(g, stream=self._hi):
             main = torch.cuda.current_stream()
             side.wait_stream(main)
@@ -414,7 +420,7 @@ class Trainer:
         for name, fn in ops:
             g = torch.cuda.CUDAGraph()
             n0 = hf.kernel_launches()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=self._cap):
                 fn()
             out.append((name, g, hf.kernel_launches() - n0))
         return out

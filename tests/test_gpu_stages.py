@@ -128,6 +128,24 @@ def test_aggregate_bwd(seed, agg, D):
     close_scaled(dY.cpu().numpy()[:U], ref["dY"], A, what="dY")
 
 
+@pytest.mark.parametrize("D", [64, 128])
+def test_aggregate_bwd_integer_inputs_bit_exact(D):
+    """Transpose SpMM with integer-valued G: every partial sum is exact in
+    fp32, so sum is bit-exact in any order; mean (reading C19: w = 1/deg
+    rounded, w*g rounded, then summed) equals the oracle evaluated with the
+    same fp32 products (hub columns included: the long-column kernel)."""
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(91, D=D, N=12000, hub=0.15)
+    U = ch["U"]
+    G = rng.integers(-8, 9, (sh.dst_rows, D)).astype(np.float32)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ws = torch.empty(hf().aggregate_bwd_ws_bytes(sh, "sum", 1) // 4 + 16, device=DEV)
+    dY = torch.zeros(max(sh.U_max, 1), D, device=DEV)
+    hf().aggregate_bwd(sh, csr, "sum", D, 1, 0.2, t(G), None, None, None, None, dY, None, None, ws)
+    ref = oracle.aggregate_bwd(osh, blk, et, ch, "sum", D, 1, G, np.zeros((U, D)))
+    assert np.array_equal(dY.cpu().numpy()[:U], ref["dY"])
+    assert (np.diff(ch["col_ptr"]) > 16).any()          # long columns exercised
+
+
 @pytest.mark.parametrize("D,H", [(128, 8), (64, 8)])
 @pytest.mark.parametrize("seed", range(3))
 def test_aggregate_bwd_gat(seed, D, H):
@@ -374,6 +392,37 @@ def test_linear_xent(B, C, split):
     assert np.all(np.abs(dWc.cpu().numpy() - ref["dWc"]) <= 1e-5 * sw)
     assert np.all(np.abs(dbc.cpu().numpy() - ref["dbc"]) <= 1e-5 * np.abs(ref["dlog"]).sum(0) + 1e-12)
 
+
+
+@pytest.mark.parametrize("B,C", [(64, 7), (300, 349), (64, 600)])
+def test_linear_xent_bad_labels(B, C):
+    """Labels outside [0, C) (negative, == C, >= 32 for the small-C kernel)
+    set HIFUSE_ST_BAD_LABEL and drop their rows: the loss is the oracle's sum
+    over the valid rows divided by B, their dH rows are zero."""
+    import oracle.model as om
+    rng = np.random.default_rng(B + C)
+    D = 128
+    Hs = rng.standard_normal((B, D)).astype(np.float32)
+    Wc = (rng.standard_normal((D, C)) * 0.1).astype(np.float32)
+    bc = (rng.standard_normal(C) * 0.1).astype(np.float32)
+    lab = rng.integers(0, C, B).astype(np.int32)
+    bad = np.array([1, 5, B - 1])
+    lab[bad] = [-1, C, C + 40]
+    good = np.setdiff1d(np.arange(B), bad)
+    ref = om.xent(Hs[good], Wc, bc, lab[good])
+    loss = torch.zeros(1, device=DEV)
+    dH = torch.full((B, D), 7.0, device=DEV)
+    ws = torch.empty(hf().xent_ws_bytes(B, D, C) // 4 + 64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    hf().linear_xent(B, D, C, t(Hs), 0, torch.from_numpy(lab).to(DEV), t(Wc), t(bc), loss, dH,
+                     None, None, ws, status=st)
+    torch.cuda.synchronize()
+    assert hf().read_status(st) == 32            # HIFUSE_ST_BAD_LABEL
+    want = ref["loss"] * len(good) / B
+    assert abs(loss.item() - want) <= 1e-5 * max(1.0, abs(want))
+    dHh = dH.cpu().numpy()
+    assert not dHh[bad].any()
+    assert np.isfinite(dHh).all()
 
 # ------------------------------------- GAT, softmax across relations (NEXT(2))
 @pytest.mark.parametrize("D,H", [(128, 8), (64, 8), (128, 1), (64, 2)])
