@@ -24,7 +24,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "hifuse_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3}
+AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3, "gat_mul": 4}
 
 
 def build_lib(force: bool = False) -> str:
@@ -161,14 +161,42 @@ def aggregate_fwd(shape: Shape, blk, edge_type, csr, agg, D, H, Y, s_src=None, s
                 alpha=None if alpha is None else alpha[:N])
 
 
-def fuse(shape: Shape, D, act, Z, R0, bias):
-    """O4: H_t[i] = act(R0_t[i] + b_t + sum_{r: t(r)=t} Z[(r,i)])."""
+def fuse(shape: Shape, D, act, Z, R0, bias, beta=None):
+    """O4: H_t[i] = act(R0_t[i] + b_t + sum_{r: t(r)=t} beta_r Z[(r,i)]) (beta = 1
+    unless HAN semantic-attention weights are given, O4')."""
     Hout = np.zeros((max(shape.dst_rows, 1), D))
     Zc = _f64(Z) if len(Z) else np.zeros((1, D))
     R0c = None if R0 is None else (_f64(R0) if len(R0) else np.zeros((1, D)))
     lib().oracle_fuse(shape.T, shape.R, _p(shape.rel_dst), _p(shape.n_dst), D, int(act),
-                      _p(Zc), _p(R0c), _p(_f64(bias)), _p(Hout))
+                      _p(Zc), _p(R0c), _p(_f64(bias)), _p(_f64(beta)), _p(Hout))
     return Hout[:shape.dst_rows]
+
+
+def sem_att(shape: Shape, D, Z, Ws, bs, q):
+    """O4': HAN semantic attention; returns (w [R], beta [R])."""
+    A = len(q)
+    w = np.zeros(shape.R)
+    beta = np.zeros(shape.R)
+    Zc = _f64(Z) if len(Z) else np.zeros((1, D))
+    lib().oracle_sem_att(shape.T, shape.R, _p(shape.rel_dst), _p(shape.n_dst), D, A, _p(Zc),
+                         _p(_f64(Ws)), _p(_f64(bs)), _p(_f64(q)), _p(w), _p(beta))
+    return w, beta
+
+
+def sem_att_bwd(shape: Shape, D, Z, Ws, bs, q, beta, G):
+    """O5a': adjoint of O4' + the beta-weighted sum; returns dZ [rows, D] (per
+    merged row), dWs [D, A], dbs [A], dq [A]."""
+    A = len(q)
+    dZ = np.zeros((max(shape.rows, 1), D))
+    dWs = np.zeros((D, A))
+    dbs = np.zeros(A)
+    dq = np.zeros(A)
+    Zc = _f64(Z) if len(Z) else np.zeros((1, D))
+    Gc = _f64(G) if len(G) else np.zeros((1, D))
+    lib().oracle_sem_att_bwd(shape.T, shape.R, _p(shape.rel_dst), _p(shape.n_dst), D, A, _p(Zc),
+                             _p(_f64(Ws)), _p(_f64(bs)), _p(_f64(q)), _p(_f64(beta)), _p(Gc),
+                             _p(dZ), _p(dWs), _p(dbs), _p(dq))
+    return dict(dZ=dZ[:shape.rows], dWs=dWs, dbs=dbs, dq=dq)
 
 
 def fuse_bwd(shape: Shape, D, act, dH, Hv):
@@ -182,8 +210,10 @@ def fuse_bwd(shape: Shape, D, act, dH, Hv):
 
 
 def aggregate_bwd(shape: Shape, blk, edge_type, csr, agg, D, H, G, Y, s_src=None, s_dst=None,
-                  slope=0.2):
-    """O5b: adjoint of O3. Returns dY [U,D], ds_src [U,H], ds_dst [rows,H]."""
+                  slope=0.2, g_rows=False):
+    """O5b: adjoint of O3. Returns dY [U,D], ds_src [U,H], ds_dst [rows,H].
+    G: type-major [dst_rows, D] (dZ[(r,i)] = G_t[i]), or with g_rows the
+    per-merged-row gradient dZ [rows, D] (HAN fusion)."""
     U = csr["U"]
     dY = np.zeros((max(U, 1), D))
     ds_src = np.zeros((max(U, 1), H))
@@ -197,7 +227,7 @@ def aggregate_bwd(shape: Shape, blk, edge_type, csr, agg, D, H, G, Y, s_src=None
         _p(np.ascontiguousarray(blk.edge_id, np.int64)), _p(_i32(edge_type)),
         ctypes.c_int64(len(edge_type)), _p(csr["rel_y_off"]),
         _p(_i32(csr["y_src"]) if U else np.zeros(1, np.int32)), ctypes.c_int64(U),
-        AGG[agg], D, H, ctypes.c_double(slope), _p(Gc), _p(Yc), _p(ss), _p(sd),
+        AGG[agg], D, H, ctypes.c_double(slope), int(bool(g_rows)), _p(Gc), _p(Yc), _p(ss), _p(sd),
         _p(dY), _p(ds_src), _p(ds_dst))
     return dict(dY=dY[:U], ds_src=ds_src[:U], ds_dst=ds_dst[:shape.rows])
 

@@ -317,6 +317,26 @@ static void relation_rows(int R, const int32_t *rel_src, const int32_t *rel_dst,
 
 static double leaky(double x, double slope) { return x > 0 ? x : slope * x; }
 
+/* Attention logit of an edge from its source score ss and destination score
+ * sd: agg 2/3 additive GAT (reading C6) LeakyReLU(ss + sd); agg 4
+ * multiplicative (reading C23, RGAT's multiplicative logit q_i . k_j with one
+ * query / key unit per head [ext]) ss * sd.  dl_dss / dl_dsd: its partial
+ * derivatives (LeakyReLU'(0) = slope, C8). */
+static double att_logit(int agg, double ss, double sd, double slope)
+{
+    return agg == 4 ? ss * sd : leaky(ss + sd, slope);
+}
+static double dlogit_dss(int agg, double ss, double sd, double slope)
+{
+    (void)ss;
+    return agg == 4 ? sd : ((ss + sd) > 0 ? 1.0 : slope);
+}
+static double dlogit_dsd(int agg, double ss, double sd, double slope)
+{
+    (void)sd;
+    return agg == 4 ? ss : ((ss + sd) > 0 ? 1.0 : slope);
+}
+
 /* GAT with the softmax ACROSS relations (reading
  * C5' in DESIGN.md; the PyG RGATConv default): for destination (t, i) and
  * head h, alpha_e = softmax over ALL in-edges of (t, i), whatever their
@@ -480,7 +500,7 @@ void oracle_aggregate_fwd(int T, int R, const int32_t *rel_src, const int32_t *r
             double deg = (double)(ptr[i + 1] - ptr[i]);
             deg_out[row] = deg;
             double *z = Z + row * D;
-            if (agg != 2) {
+            if (agg != 2 && agg != 4) {
                 /* line 260: Aggregate = segment sum (mean: / |segment|, C1) */
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     const double *y = Y + (int64_t)yrow_of(rel_y_off, y_src, r, src[list[k]]) * D;
@@ -490,22 +510,23 @@ void oracle_aggregate_fwd(int T, int R, const int32_t *rel_src, const int32_t *r
                     for (int d = 0; d < D; d++) z[d] /= deg;
                 continue;
             }
-            /* GAT (C5, C6, C8): per head, softmax over the segment of
-             * l_e = LeakyReLU(s_src[col_e] + s_dst[row]), then sum alpha_e Y[col_e] */
+            /* GAT (C5, C6, C8; agg 4: multiplicative logit, C23): per head,
+             * softmax over the segment of l_e = LeakyReLU(s_src[col_e] +
+             * s_dst[row]) (agg 4: s_src[col_e] s_dst[row]), then sum alpha_e Y[col_e] */
             for (int h = 0; h < H; h++) {
                 double m = -INFINITY, sum = 0.0;
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
-                    double l = leaky(s_src[(int64_t)u * H + h] + s_dst[row * H + h], slope);
+                    double l = att_logit(agg, s_src[(int64_t)u * H + h], s_dst[row * H + h], slope);
                     if (l > m) m = l;
                 }
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
-                    sum += exp(leaky(s_src[(int64_t)u * H + h] + s_dst[row * H + h], slope) - m);
+                    sum += exp(att_logit(agg, s_src[(int64_t)u * H + h], s_dst[row * H + h], slope) - m);
                 }
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
-                    double a = exp(leaky(s_src[(int64_t)u * H + h] + s_dst[row * H + h], slope) - m) / sum;
+                    double a = exp(att_logit(agg, s_src[(int64_t)u * H + h], s_dst[row * H + h], slope) - m) / sum;
                     if (alpha) alpha[list[k] * H + h] = a;
                     for (int c = 0; c < dh; c++) z[h * dh + c] += a * Y[(int64_t)u * D + h * dh + c];
                 }
@@ -522,7 +543,8 @@ void oracle_aggregate_fwd(int T, int R, const int32_t *rel_src, const int32_t *r
 /* Z[(r,i)]); act: 0 none, 1 ReLU.                                           */
 /* ------------------------------------------------------------------------ */
 void oracle_fuse(int T, int R, const int32_t *rel_dst, const int32_t *n_dst, int D, int act,
-                 const double *Z, const double *R0, const double *bias, double *Hout)
+                 const double *Z, const double *R0, const double *bias, const double *beta,
+                 double *Hout)
 {
     int64_t *tdo = (int64_t *)malloc(sizeof(int64_t) * (T + 1));
     tdo[0] = 0;
@@ -535,13 +557,117 @@ void oracle_fuse(int T, int R, const int32_t *rel_dst, const int32_t *n_dst, int
                 if (bias) v += bias[(int64_t)t * D + d];
                 int64_t row = 0;
                 for (int r = 0; r < R; r++) {
-                    if (rel_dst[r] == t) v += Z[(row + i) * D + d];
+                    /* beta: HAN semantic-attention weights (O4'), NULL: 1 */
+                    if (rel_dst[r] == t) v += (beta ? beta[r] : 1.0) * Z[(row + i) * D + d];
                     row += n_dst[rel_dst[r]];
                 }
                 if (act == 1 && v < 0) v = 0;
                 Hout[(tdo[t] + i) * D + d] = v;
             }
     free(tdo);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O4'. HAN semantic-attention fusion (P:L123 leaves */
+/* the fusion rule open: "combining the results"; reading C22, HAN's          */
+/* semantic-level attention [ext]).  Per relation r into type t:              */
+/*   w_r    = (1/n_t) sum_{i<n_t} q . tanh(Ws^T Z[(r,i)] + bs)                */
+/*   beta_r = exp(w_r) / sum_{r': t(r')=t} exp(w_r')                          */
+/* and O4 fuses with weights: H_t[i] = act(R0 + b + sum_r beta_r Z[(r,i)]).   */
+/* Ws [D,A], bs [A], q [A].  A type without destinations gets w = 0.          */
+/* ------------------------------------------------------------------------ */
+void oracle_sem_att(int T, int R, const int32_t *rel_dst, const int32_t *n_dst, int D, int A,
+                    const double *Z, const double *Ws, const double *bs, const double *q,
+                    double *w, double *beta)
+{
+    double *a = (double *)malloc(sizeof(double) * A);
+    int64_t row = 0;
+    for (int r = 0; r < R; r++) {
+        int32_t nt = n_dst[rel_dst[r]];
+        double acc = 0.0;
+        for (int32_t i = 0; i < nt; i++, row++) {
+            const double *z = Z + row * D;
+            for (int c = 0; c < A; c++) {
+                double v = bs[c];
+                for (int d = 0; d < D; d++) v += z[d] * Ws[(int64_t)d * A + c];
+                a[c] = v;
+            }
+            double s = 0.0;
+            for (int c = 0; c < A; c++) s += q[c] * tanh(a[c]);
+            acc += s;
+        }
+        w[r] = nt > 0 ? acc / nt : 0.0;
+    }
+    for (int t = 0; t < T; t++) {
+        double m = -INFINITY, sum = 0.0;
+        for (int r = 0; r < R; r++) if (rel_dst[r] == t && w[r] > m) m = w[r];
+        for (int r = 0; r < R; r++) if (rel_dst[r] == t) sum += exp(w[r] - m);
+        for (int r = 0; r < R; r++) if (rel_dst[r] == t) beta[r] = exp(w[r] - m) / sum;
+    }
+    free(a);
+}
+
+/* O5a'. Adjoint of O4' + the weighted sum of O4, given G = dL/d(pre-       */
+/* activation fused value) (type-major, from O5a):                           */
+/*   dbeta_r = sum_i <G_t[i], Z[(r,i)]>                                       */
+/*   dw_r    = beta_r (dbeta_r - sum_{r': t(r')=t} beta_r' dbeta_r')          */
+/*   g_a     = (dw_r / n_t) q (.) (1 - tanh^2(a)),  a = Ws^T Z[(r,i)] + bs    */
+/*   dZ[(r,i)] = beta_r G_t[i] + Ws g_a                                       */
+/*   dWs += Z[(r,i)] (x) g_a;  dbs += g_a;  dq += (dw_r / n_t) tanh(a)         */
+void oracle_sem_att_bwd(int T, int R, const int32_t *rel_dst, const int32_t *n_dst, int D, int A,
+                        const double *Z, const double *Ws, const double *bs, const double *q,
+                        const double *beta, const double *G,
+                        double *dZ, double *dWs, double *dbs, double *dq)
+{
+    int64_t *tdo = (int64_t *)malloc(sizeof(int64_t) * (T + 1));
+    tdo[0] = 0;
+    for (int t = 0; t < T; t++) tdo[t + 1] = tdo[t] + n_dst[t];
+    double *dbeta = (double *)calloc(R, sizeof(double));
+    double *dw = (double *)calloc(R, sizeof(double));
+    double *a = (double *)malloc(sizeof(double) * A);
+    double *ga = (double *)malloc(sizeof(double) * A);
+    memset(dWs, 0, sizeof(double) * D * A);
+    memset(dbs, 0, sizeof(double) * A);
+    memset(dq, 0, sizeof(double) * A);
+    int64_t row = 0;
+    for (int r = 0; r < R; r++) {
+        int t = rel_dst[r];
+        for (int32_t i = 0; i < n_dst[t]; i++, row++)
+            for (int d = 0; d < D; d++) dbeta[r] += G[(tdo[t] + i) * D + d] * Z[row * D + d];
+    }
+    for (int r = 0; r < R; r++) {
+        double s = 0.0;
+        for (int r2 = 0; r2 < R; r2++) if (rel_dst[r2] == rel_dst[r]) s += beta[r2] * dbeta[r2];
+        dw[r] = beta[r] * (dbeta[r] - s);
+    }
+    row = 0;
+    for (int r = 0; r < R; r++) {
+        int t = rel_dst[r];
+        int32_t nt = n_dst[t];
+        for (int32_t i = 0; i < nt; i++, row++) {
+            const double *z = Z + row * D;
+            for (int c = 0; c < A; c++) {
+                double v = bs[c];
+                for (int d = 0; d < D; d++) v += z[d] * Ws[(int64_t)d * A + c];
+                a[c] = v;
+            }
+            for (int c = 0; c < A; c++) {
+                double th = tanh(a[c]);
+                ga[c] = dw[r] / nt * q[c] * (1.0 - th * th);
+                dbs[c] += ga[c];
+                dq[c] += dw[r] / nt * th;
+            }
+            for (int d = 0; d < D; d++) {
+                double v = beta[r] * G[(tdo[t] + i) * D + d];
+                for (int c = 0; c < A; c++) {
+                    v += Ws[(int64_t)d * A + c] * ga[c];
+                    dWs[(int64_t)d * A + c] += z[d] * ga[c];
+                }
+                dZ[row * D + d] = v;
+            }
+        }
+    }
+    free(dbeta); free(dw); free(a); free(ga); free(tdo);
 }
 
 /* O5a. Fusion backward: G = dH * act'(H) (ReLU' = 1[H > 0]), which is also   */
@@ -573,7 +699,7 @@ void oracle_aggregate_bwd(int T, int R, const int32_t *rel_src, const int32_t *r
                           int64_t N, const int32_t *src, const int32_t *dst, const int64_t *eid,
                           const int32_t *edge_type, int64_t E,
                           const int32_t *rel_y_off, const int32_t *y_src, int64_t U,
-                          int agg, int D, int H, double slope,
+                          int agg, int D, int H, double slope, int g_rows,
                           const double *Gt, const double *Y, const double *s_src, const double *s_dst,
                           double *dY, double *ds_src, double *ds_dst)
 {
@@ -586,6 +712,7 @@ void oracle_aggregate_bwd(int T, int R, const int32_t *rel_src, const int32_t *r
     rro[R] = rows;
     memset(dY, 0, sizeof(double) * U * D);
     if (agg >= 2) { memset(ds_src, 0, sizeof(double) * U * H); memset(ds_dst, 0, sizeof(double) * rows * H); }
+    if (g_rows && agg == 3) { free(rro); free(tdo); abort(); }   /* not defined for xrel */
     int dh = D / H;
     if (agg == 3) {
         gat_xrel_bwd(T, R, rel_src, rel_dst, n_src, n_dst, N, src, dst, eid, edge_type, E,
@@ -600,9 +727,11 @@ void oracle_aggregate_bwd(int T, int R, const int32_t *rel_src, const int32_t *r
         relation_rows(R, rel_src, rel_dst, n_src, n_dst, r, N, src, dst, eid, edge_type, E, &ptr, &list);
         for (int32_t i = 0; i < n_dst[t]; i++) {
             int64_t row = rro[r] + i;
-            const double *g = Gt + (tdo[t] + i) * D;     /* dZ[(r,i)] = G_t[i] */
+            /* dZ[(r,i)] = G_t[i] (plain fusion), or a per-row gradient
+             * (g_rows: HAN semantic attention, O4') */
+            const double *g = g_rows ? Gt + row * D : Gt + (tdo[t] + i) * D;
             double deg = (double)(ptr[i + 1] - ptr[i]);
-            if (agg != 2) {
+            if (agg != 2 && agg != 4) {
                 double w = agg == 1 ? 1.0 / deg : 1.0;
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
@@ -615,34 +744,34 @@ void oracle_aggregate_bwd(int T, int R, const int32_t *rel_src, const int32_t *r
                 double m = -INFINITY, sum = 0.0, za = 0.0;
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
-                    double l = leaky(s_src[(int64_t)u * H + h] + s_dst[row * H + h], slope);
+                    double l = att_logit(agg, s_src[(int64_t)u * H + h], s_dst[row * H + h], slope);
                     if (l > m) m = l;
                 }
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
-                    sum += exp(leaky(s_src[(int64_t)u * H + h] + s_dst[row * H + h], slope) - m);
+                    sum += exp(att_logit(agg, s_src[(int64_t)u * H + h], s_dst[row * H + h], slope) - m);
                 }
                 /* z_h = sum_e alpha_e y_e  =>  dalpha_e = <g_h, y_e>;
                  * softmax: dl_e = alpha_e (dalpha_e - sum_e' alpha_e' dalpha_e') */
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
-                    double a = exp(leaky(s_src[(int64_t)u * H + h] + s_dst[row * H + h], slope) - m) / sum;
+                    double a = exp(att_logit(agg, s_src[(int64_t)u * H + h], s_dst[row * H + h], slope) - m) / sum;
                     double da = 0.0;
                     for (int c = 0; c < dh; c++) da += g[h * dh + c] * Y[(int64_t)u * D + h * dh + c];
                     za += a * da;
                 }
                 for (int64_t k = ptr[i]; k < ptr[i + 1]; k++) {
                     int32_t u = yrow_of(rel_y_off, y_src, r, src[list[k]]);
-                    double pre = s_src[(int64_t)u * H + h] + s_dst[row * H + h];
-                    double a = exp(leaky(pre, slope) - m) / sum;
+                    double ss = s_src[(int64_t)u * H + h], sd = s_dst[row * H + h];
+                    double a = exp(att_logit(agg, ss, sd, slope) - m) / sum;
                     double da = 0.0;
                     for (int c = 0; c < dh; c++) {
                         da += g[h * dh + c] * Y[(int64_t)u * D + h * dh + c];
                         dY[(int64_t)u * D + h * dh + c] += a * g[h * dh + c];
                     }
-                    double dpre = a * (da - za) * (pre > 0 ? 1.0 : slope);   /* LeakyReLU'(0) = slope (C8) */
-                    ds_src[(int64_t)u * H + h] += dpre;
-                    ds_dst[row * H + h] += dpre;
+                    double dl = a * (da - za);
+                    ds_src[(int64_t)u * H + h] += dl * dlogit_dss(agg, ss, sd, slope);
+                    ds_dst[row * H + h] += dl * dlogit_dsd(agg, ss, sd, slope);
                 }
             }
         }

@@ -11,7 +11,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import Shape, build, project, aggregate_fwd, fuse, fuse_bwd, aggregate_bwd, project_bwd
+from . import (Shape, build, project, aggregate_fwd, fuse, fuse_bwd, aggregate_bwd, project_bwd,
+               sem_att, sem_att_bwd)
 
 
 def forward(layers, edge_type, rel_src, rel_dst, X0, gather_ids, params, agg, heads,
@@ -31,8 +32,13 @@ def forward(layers, edge_type, rel_src, rel_dst, X0, gather_ids, params, agg, he
         ag = aggregate_fwd(sh, blk, edge_type, csr, agg, D, heads, pr["Y"], pr["s_src"],
                            pr["s_dst"], slope)
         act = 1 if l < L - 1 else 0
-        Hh = fuse(sh, D, act, ag["Z"], pr["R0"] if p["W_root"] is not None else None, p["bias"])
-        cache.append(dict(shape=sh, csr=csr, X=X, gid=gid, proj=pr, agg=ag, H=Hh, act=act, D=D, K=K))
+        beta = None
+        if p.get("sem_W") is not None:      # HAN semantic-attention fusion (O4')
+            _, beta = sem_att(sh, D, ag["Z"], p["sem_W"], p["sem_b"], p["sem_q"])
+        Hh = fuse(sh, D, act, ag["Z"], pr["R0"] if p["W_root"] is not None else None, p["bias"],
+                  beta=beta)
+        cache.append(dict(shape=sh, csr=csr, X=X, gid=gid, proj=pr, agg=ag, H=Hh, act=act, D=D, K=K,
+                          beta=beta))
         X, gid = Hh, None
     sh = cache[-1]["shape"]
     t0 = int(sh.n_dst[:target_type].sum())
@@ -83,12 +89,20 @@ def backward(fw, layers, edge_type, params, labels, agg, heads, slope=0.2):
         pl = params["layers"][l]
         sh, D, K = c["shape"], c["D"], c["K"]
         G, dbias = fuse_bwd(sh, D, c["act"], dH, c["H"])
-        ab = aggregate_bwd(sh, layers[l], edge_type, c["csr"], agg, D, heads, G, c["proj"]["Y"],
-                           c["proj"]["s_src"], c["proj"]["s_dst"], slope)
+        sem = None
+        Gz, g_rows = G, False
+        if c["beta"] is not None:
+            sem = sem_att_bwd(sh, D, c["agg"]["Z"], pl["sem_W"], pl["sem_b"], pl["sem_q"],
+                              c["beta"], G)
+            Gz, g_rows = sem["dZ"], True
+        ab = aggregate_bwd(sh, layers[l], edge_type, c["csr"], agg, D, heads, Gz, c["proj"]["Y"],
+                           c["proj"]["s_src"], c["proj"]["s_dst"], slope, g_rows=g_rows)
         pb = project_bwd(sh, c["csr"], K, D, heads, c["X"], c["gid"], pl["W_rel"], pl["W_root"],
                          pl["att"], c["proj"]["Y"], ab["dY"], G, ab["ds_src"], ab["ds_dst"],
                          need_dX=l > 0)
         grads["layers"][l] = dict(W_rel=pb["dW_rel"], W_root=pb["dW_root"], bias=dbias,
                                   att=pb["datt"])
+        if sem is not None:
+            grads["layers"][l].update(sem_W=sem["dWs"], sem_b=sem["dbs"], sem_q=sem["dq"])
         dH = pb["dX"]
     return grads
