@@ -151,6 +151,9 @@ def stage_cost(stage, l, cfg, sz):
         return 4 * (2 * B * D + 2 * D * C + 2 * B * C), 2 * 2 * B * D * C
     if stage == "aggregate_features":     # aggregate-first input layer: A4 over raw X
         return 4 * K * s["F"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
+    if stage == "project_fuse_aggregated":     # Xagg + X dst rows in, H out (+ weights)
+        m = s["rows"] + s["dst"]
+        return 4 * K * m + 4 * D * s["dst"] + 4 * (R + T) * K * D + 4 * T * D, 2 * K * D * m
     if stage == "project_aggregated":
         m = s["rows"] + s["dst"]
         return 4 * K * m + 4 * D * m + 4 * (R + T) * K * D, 2 * K * D * m
@@ -174,7 +177,8 @@ MAIN_KERNEL = {"aggregate_fwd": "k_agg_fwd", "aggregate_bwd": "k_agg_bwd_p", "pr
                "project_wgrad": "k_wgrad_tc", "xent_wgrad": "k_head_grads",
                "project_bwd": "k_wgrad_tc", "fuse": "k_fuse", "fuse_bwd": "k_fuse_bwd_chunks",
                "build": "k_sort_long", "xent": "k_head_grads", "aggregate_features": "k_agg_fwd",
-               "project_aggregated": "k_proj_fwd_tcp", "project_aggregated_bwd": "k_wgrad_tc"}
+               "project_aggregated": "k_proj_fwd_tcp", "project_aggregated_bwd": "k_wgrad_tc",
+               "project_fuse_aggregated": "k_fuse_gemm_tcp"}
 
 
 def ncu_traffic(kernel, layer, config, order):
@@ -255,6 +259,7 @@ def config_obj(cfg, args, extra=None):
          "parallelism": f"dp{args.gpus}", "precision": args.prec,
          "order": getattr(args, "order", "project_first"),
          "aggregation": cfg.agg,
+         "fusion": getattr(args, "fusion", "sum"),
          "l2": "inputs larger than L2: a pool of distinct sampled batches, per-step working "
                "set above the 126 MB L2 for mag"}
     if extra:
@@ -264,7 +269,7 @@ def config_obj(cfg, args, extra=None):
 
 
 # ----------------------------------------------------------- timed loop -----
-def build_graphs(tr, pool, feat_d, et_d, side, world, pipeline, allreduce=None):
+def build_graphs(tr, pool, feat_d, et_d, side, world, pipeline, allreduce=None, capture=True):
     """The graphs bench.py replays (tests/test_gpu_pipeline.py replays the same
     ones against eager steps).  A sizing pass runs every pool batch once
     eagerly (buffers reach their final size, update=False), then one CUDA
@@ -281,13 +286,18 @@ def build_graphs(tr, pool, feat_d, et_d, side, world, pipeline, allreduce=None):
     torch.cuda.synchronize()
     if hf.read_status(tr.status) != 0:
         raise RuntimeError("device reported invalid edges in the batch pool")
+    if not capture:        # a collective that cannot be captured (gloo): eager steps
+        return {"serial": None, "graphs": None, "pipelined": False, "eager": True,
+                "feat": feat_d, "et": et_d}
+    # with set_dp (N > 1, NCCL) the bucketed all-reduces and the SGD are inside
+    # the graphs
     serial = [tr.capture(db, feat_d, et_d, update=True, world=world) for db in pool]
     graphs = serial
     if pipeline:
         graphs = [tr.capture_pipelined(db, pool[(i + 1) % len(pool)], feat_d, et_d, side,
-                                       update=(world == 1))
+                                       update=(world == 1 or tr.world > 1))
                   for i, db in enumerate(pool)]
-    return {"serial": serial, "graphs": graphs, "pipelined": bool(pipeline)}
+    return {"serial": serial, "graphs": graphs, "pipelined": bool(pipeline), "eager": False}
 
 
 def prime_pipeline(tr, gset, pool, et_d):
@@ -312,7 +322,7 @@ class StepRunner:
         self.step_done = torch.cuda.Event()
 
     def use(self, mode):
-        self.mode = mode
+        self.mode = mode if not self.gset.get("eager") else "eager"
         self.graphs = self.gset["graphs"] if mode == "pipelined" else self.gset["serial"]
 
     def one_step(self, i, e2e=False, loss_host=None):
@@ -335,10 +345,13 @@ class StepRunner:
                 self.copy_done[ahead % P].record(self.copy_stream)
             built = i + 1 if pipelined else i
             torch.cuda.current_stream().wait_event(self.copy_done[built % P])
-        self.graphs[i % P][0].replay()
+        if self.gset.get("eager"):
+            tr.step(self.pool[i % P], self.gset["feat"], self.gset["et"])
+        else:
+            self.graphs[i % P][0].replay()
         if e2e:
             self.step_done.record()
-        if self.world > 1:
+        if self.world > 1 and tr.world == 1:      # (legacy: flat all-reduce after the graph)
             from paper_2408_08490_b200.dp import allreduce_grads
             allreduce_grads(tr.grads, self.world)
             hf.sgd(tr.params, tr.grads, tr.lr, 1.0 / self.world)
@@ -435,11 +448,22 @@ def main():
                     help="RGAT edge-softmax domain: within each (relation, destination) row "
                          "(reading C5, default) or across all relations of a destination "
                          "(C5', SURVEY §8(f) NEXT(2))")
+    ap.add_argument("--fusion", default="sum", choices=["sum", "han"],
+                    help="semantic fusion: plain sum over relations (reading C2/C4, default) or "
+                         "HAN semantic attention (C22, NEXT(2))")
+    ap.add_argument("--gat-logit", default="add", choices=["add", "mul"],
+                    help="RGAT attention logit: additive LeakyReLU(s_src + s_dst) (reading C6, "
+                         "default) or multiplicative s_src * s_dst (C23, NEXT(2))")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if cfg.model == "rgat" and args.gat_softmax == "across":
         import dataclasses
         cfg = dataclasses.replace(cfg, agg="gat_xrel")
+    if cfg.model == "rgat" and args.gat_logit == "mul":
+        import dataclasses
+        if args.gat_softmax == "across":
+            raise SystemExit("multiplicative attention is defined with the within-relation softmax")
+        cfg = dataclasses.replace(cfg, agg="gat_mul")
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -464,7 +488,7 @@ def main():
 
     g = generate_graph(cfg)
     feat, foff = generate_features(cfg.type_counts, cfg.feat_dim)
-    params = make_params(cfg)
+    params = make_params(cfg, fusion=args.fusion)
     rs = np.array([r.src for r in cfg.rels], np.int32)
     rd = np.array([r.dst for r in cfg.rels], np.int32)
     from paper_2408_08490_b200.dp import rank_batches, allreduce_grads
@@ -479,16 +503,23 @@ def main():
     et_d = torch.from_numpy(g.edge_type).to(dev)
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
-                 prec=args.prec, order=args.order)
+                 prec=args.prec, order=args.order, fusion=args.fusion)
     tr.load_params(params)
     tr.prepare_graph(et_d)           # relation-major edge ids -> R+1 offsets (once per graph)
-    allreduce = (lambda t: allreduce_grads(t, world)) if world > 1 else None
+    # N > 1: per-layer bucketed all-reduce on a comm stream inside the step
+    # (Trainer.set_dp), captured in the CUDA graphs with NCCL; a gloo run
+    # (functional check) replays eager steps
+    backend = os.environ.get("HIFUSE_DIST_BACKEND", "nccl") if world > 1 else None
+    allreduce = None
+    if world > 1:
+        tr.set_dp(world)
     # one CUDA graph per pool batch: the whole step is replayed without host
     # launch overhead (all sizes are host-known, nothing syncs inside).
     # Pipelined (default, N = 1): graph i computes batch i while a side stream
     # builds the semantic graphs of batch i+1 (Fig. 6 pipeline).
     side = torch.cuda.Stream()
-    gset = build_graphs(tr, pool, feat_d, et_d, side, world, bool(args.pipeline), allreduce)
+    gset = build_graphs(tr, pool, feat_d, et_d, side, world, bool(args.pipeline), allreduce,
+                        capture=backend != "gloo")
     prime_pipeline(tr, gset, pool, et_d)
     runner = StepRunner(tr, gset, pool, world, dev)
 
@@ -508,8 +539,13 @@ def main():
     spread["repeats"] = len(ms_all)
     spread["repeat_ms_per_step"] = {"median": ms / args.steps, "min": min(ms_all) / args.steps,
                                     "max": max(ms_all) / args.steps}
-    launches = sum(runner.graphs[i % len(pool)][1] for i in range(args.steps)) + \
-        (args.steps if world > 1 else 0)
+    if runner.graphs is not None:
+        launches = sum(runner.graphs[i % len(pool)][1] for i in range(args.steps))
+    else:                                   # eager steps (gloo): count one step's launches
+        n0 = hf.kernel_launches()
+        tr.step(pool[0], feat_d, et_d, update=False)
+        torch.cuda.synchronize()
+        launches = (hf.kernel_launches() - n0) * args.steps
     clk = clocks.summary(t0, t1)
     # the same steps without the build/compute overlap (every graph builds
     # its own batch first), for reference
@@ -566,15 +602,17 @@ def main():
     # north-star project-first path is always measured next to the faster
     # aggregate-first one)
     other = None
-    if cfg.model == "rgcn" and args.prec == "tf32":
+    if cfg.model == "rgcn" and args.prec == "tf32" and args.fusion == "sum":
         other_order = "project_first" if tr.agg_first else "agg_first"
         tr_o = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                        cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
-                       prec=args.prec, order=other_order)
+                       prec=args.prec, order=other_order, fusion=args.fusion)
         tr_o.load_params(params)
         tr_o.prepare_graph(et_d)
+        if world > 1:
+            tr_o.set_dp(world)
         gset_o = build_graphs(tr_o, pool, feat_d, et_d, side, world, bool(args.pipeline),
-                              allreduce)
+                              allreduce, capture=backend != "gloo")
         prime_pipeline(tr_o, gset_o, pool, et_d)
         run_o = StepRunner(tr_o, gset_o, pool, world, dev)
         for i in range(args.warmup):
@@ -586,7 +624,7 @@ def main():
         ms_os = run_o.timed(args.steps)[0]
         other = {"order": other_order, "value": world * args.steps / (ms_o / 1e3),
                  "ms_per_step": ms_o / args.steps, "serial_ms_per_step": ms_os / args.steps,
-                 "gpu_launches_per_step": gset_o["graphs"][0][1]}
+                 "gpu_launches_per_step": gset_o["graphs"][0][1] if gset_o["graphs"] else None}
         del run_o, gset_o, tr_o
         torch.cuda.synchronize()
         tr.load_params(params)
@@ -607,6 +645,7 @@ def main():
         avg_flops = float(np.mean([stage_cost(name, l, cfg, sizes[pi])[1] for pi in used]))
         t_s = per_step[stage_key] / 1e3
         gemm = ("project", "project_bwd", "project_aggregated", "project_aggregated_bwd", "xent",
+                "project_fuse_aggregated",
                 "project_wgrad", "xent_wgrad")
         if name in gemm and args.prec == "fp32":
             roof = {"bound": "alu", "achieved": avg_flops / t_s / 1e12, "peak": ALU_FP32_TFLOPS,
@@ -671,7 +710,7 @@ def main():
         try:
             gsmp = gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev,
                                    min(args.steps, 200), max(args.warmup, 3), args.lr, args.prec,
-                                   args.order)
+                                   args.order, args.fusion)
         except Exception as e:      # noqa: BLE001
             gsmp = {"error": f"{type(e).__name__}: {e}"[:300]}
     cpu = None
@@ -706,7 +745,8 @@ def main():
         dist.destroy_process_group()
 
 
-def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr, prec, order):
+def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr, prec, order,
+                    fusion="sum"):
     """NEXT(1): the GPU neighbour sampler (hifuse_sample_blocks) inside the
     training loop.  Batch i+1 is sampled on a side stream while batch i
     computes (the paper's Fig. 6 overlap with the sampler on the GPU too);
@@ -754,7 +794,7 @@ def gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev, steps, warmup, lr
     # side stream below
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=lr, prec=prec,
-                 order=order)
+                 order=order, fusion=fusion)
     tr.load_params(params)
     tr.prepare_graph(et_d)
     side = torch.cuda.Stream()

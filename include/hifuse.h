@@ -80,7 +80,11 @@ typedef enum {
 /* GAT_XREL: GAT with the edge-softmax across the relations of a destination
  * (hifuse_aggregate_fwd_xrel, reading C5'). */
 typedef enum { HIFUSE_AGG_SUM = 0, HIFUSE_AGG_MEAN = 1, HIFUSE_AGG_GAT = 2,
-               HIFUSE_AGG_GAT_XREL = 3 } hifuse_agg;
+               HIFUSE_AGG_GAT_XREL = 3,
+               /* multiplicative attention (reading C23):
+                * logit s_src[col] * s_dst[row] per head instead of
+                * LeakyReLU(s_src[col] + s_dst[row]); softmax within the row */
+               HIFUSE_AGG_GAT_MUL = 4 } hifuse_agg;
 typedef enum { HIFUSE_ACT_NONE = 0, HIFUSE_ACT_RELU = 1 } hifuse_act;
 /* Layout of the merged projected matrix Y (reading C3).  COMPACT:
  * per relation, one row per distinct source vertex of the layer, ascending.
@@ -248,6 +252,38 @@ hifuse_status hifuse_semantic_fuse_bwd(const hifuse_layer_shape *shape, int D, h
                                        float *d_dbias, void *d_ws, size_t ws_bytes,
                                        hifuse_stream_t stream);
 
+/* A5' / A6a'. HAN semantic-attention fusion (PAPER.md
+ * line 123 leaves the fusion rule open; reading C22, HAN's semantic-level
+ * attention [ext]).  Per relation r into type t, over the batch's n_t
+ * destinations:
+ *   w_r    = (1/n_t) sum_i q . tanh(Ws^T Z[rel_row_off[r] + i] + bs)
+ *   beta_r = exp(w_r) / sum_{r': t(r')=t} exp(w_r')
+ *   H_t[i] = act(R0_t[i] + bias_t + sum_r beta_r Z[rel_row_off[r] + i]).
+ * d_Ws [D, A] row-major, d_bs [A], d_q [A]; A == D (64 or 128).  Outputs
+ * d_beta [R] (kept for the backward), d_w [R] (nullable), d_H.  Workspace:
+ * hifuse_sem_att_ws_bytes() (the same buffer serves the backward).
+ * Backward: G = dH act'(H) (= dR0), dbias, and the per-merged-row gradient
+ *   dZ[(r,i)] = beta_r G_t[i] + Ws (c_r q (.) (1 - tanh^2(a))),
+ *   c_r = beta_r (dbeta_r - sum_{r'|t} beta_r' dbeta_r') / n_t,
+ *   dbeta_r = sum_i <G_t[i], Z[(r,i)]>,  a = Ws^T Z[(r,i)] + bs,
+ * plus dWs, dbs, dq (fixed-order reductions); dZ feeds
+ * hifuse_aggregate_bwd_rows. */
+size_t hifuse_sem_att_ws_bytes(const hifuse_layer_shape *shape, int D, int A);
+hifuse_status hifuse_semantic_fuse_att(const hifuse_layer_shape *shape, int D, int A,
+                                       hifuse_act act, const float *d_Z, const float *d_R0,
+                                       const float *d_bias, const float *d_Ws,
+                                       const float *d_bs, const float *d_q, float *d_beta,
+                                       float *d_w, float *d_H, void *d_ws, size_t ws_bytes,
+                                       hifuse_stream_t stream);
+hifuse_status hifuse_semantic_fuse_att_bwd(const hifuse_layer_shape *shape, int D, int A,
+                                           hifuse_act act, const float *d_dH, const float *d_H,
+                                           const float *d_Z, const float *d_Ws,
+                                           const float *d_bs, const float *d_q,
+                                           const float *d_beta, float *d_G, float *d_dZ,
+                                           float *d_dbias, float *d_dWs, float *d_dbs,
+                                           float *d_dq, void *d_ws, size_t ws_bytes,
+                                           hifuse_stream_t stream);
+
 /* A6b. Aggregation backward: the transpose gather over the CSC.
  *   SUM/MEAN: dY[u] = sum_{q in col u} w(row_q) G[g(row_q)],  w = 1 or 1/|row|
  *   GAT: pass 1 (row-major) recomputes alpha from d_stats and forms
@@ -265,6 +301,20 @@ hifuse_status hifuse_aggregate_bwd(const hifuse_layer_shape *shape, const hifuse
                                    const float *d_s_dst, const float *d_stats, float *d_dY,
                                    float *d_ds_src, float *d_ds_dst, void *d_ws, size_t ws_bytes,
                                    hifuse_stream_t stream);
+
+/* Aggregation backward for a PER-MERGED-ROW gradient d_dZ [rows, D] (dL/dZ,
+ * e.g. after HAN semantic-attention fusion, where the relations of a type get
+ * different gradients: hifuse_semantic_fuse_att_bwd) instead of the
+ * type-major G of hifuse_aggregate_bwd; otherwise identical.  d_att: NULL,
+ * or (GAT kinds) the score chain is folded in as in
+ * hifuse_aggregate_bwd_scored.  UNSUPPORTED for GAT_XREL. */
+hifuse_status hifuse_aggregate_bwd_rows(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                        hifuse_agg agg, int D, int heads, float slope,
+                                        const float *d_dZ, const float *d_Y,
+                                        const float *d_s_src, const float *d_s_dst,
+                                        const float *d_stats, const float *d_att, float *d_dY,
+                                        float *d_ds_src, float *d_ds_dst, void *d_ws,
+                                        size_t ws_bytes, hifuse_stream_t stream);
 
 /* RGAT, score chain folded into the CSC pass: as hifuse_aggregate_bwd (GAT or
  * GAT_XREL) but d_dY receives dYt = dY + ds_src (x) att[r, 0] directly (the
@@ -323,6 +373,24 @@ hifuse_status hifuse_aggregate_features_fwd(const hifuse_layer_shape *shape, con
                                             int64_t x_rows, const int32_t *d_gather_ids,
                                             float *d_Xagg, void *d_ws, size_t ws_bytes,
                                             hifuse_stream_t stream);
+/* NEXT(3) fused fusion GEMM of the aggregate-first RGCN input layer (SURVEY.md
+ * §8(f) row 3): hifuse_project_aggregated and
+ * hifuse_semantic_fuse as ONE tcgen05 TF32 GEMM per destination type,
+ *   H_t[i] = act([X_t[i] | Xagg[rel_row_off[r1] + i] | ...] . [W_root,t; W_r1; ...] + b_t),
+ * K = (1 + R_in(t)) K_in (relations r into t in ascending id; the root term
+ * when d_W_root != NULL, reading X through d_gather_ids like
+ * hifuse_project_aggregated), bias and activation in the epilogue; writes H
+ * [sum_t n_dst(t), D] directly (no Z / R0).  Same values as the two calls up
+ * to the fp32 summation order.  The backward is unchanged
+ * (hifuse_semantic_fuse_bwd + hifuse_project_aggregated_bwd). */
+hifuse_status hifuse_project_fuse_aggregated(const hifuse_layer_shape *shape,
+                                            const hifuse_csr *csr, hifuse_prec prec, int K, int D,
+                                            hifuse_act act, const float *d_Xagg,
+                                            const float *d_X, int64_t x_rows,
+                                            const int32_t *d_gather_ids, const float *d_W_rel,
+                                            const float *d_W_root, const float *d_bias,
+                                            float *d_H, hifuse_stream_t stream);
+
 /* The two halves of hifuse_aggregate_features_fwd, so the first can run with
  * the semantic-graph build (off the critical path):
  *   hifuse_feature_cols: d_col_x [N] = the feature-store row x(e) of every
@@ -468,6 +536,27 @@ hifuse_status hifuse_sample_blocks(const hifuse_graph_csc *g, int num_layers,
  * §9 "Backward off the critical path"). */
 hifuse_status hifuse_stream_attach(hifuse_stream_t stream);
 hifuse_status hifuse_stream_release(hifuse_stream_t stream);
+
+/* NEXT(4) feature-sharded data parallelism (PAPER.md
+ * line 219 "a large heterogeneous graph can be partitioned into several
+ * subgraphs", line 404).  Rank k keeps rows [bounds[k], bounds[k+1]) of the
+ * type-major feature store; before A2 a batch's layer-0 rows are fetched from
+ * their owners with one all-to-all of ids and one of rows (shard.py).
+ * hifuse_shard_plan: stable counting sort of d_ids [n] (global rows) by owner:
+ *   d_counts [W] per-owner counts, d_order [n] batch positions grouped by
+ *   owner (batch order inside an owner); W <= 64, d_bounds int64 [W+1]
+ *   ascending.  Ids outside [bounds[0], bounds[W]) set HIFUSE_ST_BAD_EDGE_ID
+ *   and are left out.
+ * hifuse_gather_words: dst[i] = src[idx[i] - base] for rows of `words`
+ *   4-byte words (16-byte vectors when words % 4 == 0 and both aligned).
+ * hifuse_scatter_words: dst[idx[i]] = src[i] (rows of `words` words). */
+hifuse_status hifuse_shard_plan(const int32_t *d_ids, int64_t n, const int64_t *d_bounds, int W,
+                                int32_t *d_counts, int32_t *d_order, int32_t *d_status,
+                                hifuse_stream_t stream);
+hifuse_status hifuse_gather_words(const void *d_src, const int32_t *d_idx, int64_t n, int words,
+                                  int64_t base, void *d_dst, hifuse_stream_t stream);
+hifuse_status hifuse_scatter_words(const void *d_src, const int32_t *d_idx, int64_t n, int words,
+                                   void *d_dst, hifuse_stream_t stream);
 
 /* Tests / debugging: copies *d_status to *out_h and synchronises `stream`. */
 hifuse_status hifuse_read_status(const int32_t *d_status, hifuse_stream_t stream, int32_t *out_h);

@@ -36,6 +36,21 @@ __device__ __forceinline__ float4 f4fma_into(float s, float4 a, float4 y) {
   return make_float4(fmaf(s, a.x, y.x), fmaf(s, a.y, y.y), fmaf(s, a.z, y.z), fmaf(s, a.w, y.w));
 }
 __device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? x : slope * x; }
+// Attention logit of an edge from its source score ss and destination score
+// sd: additive GAT (reading C6) LeakyReLU(ss + sd), or multiplicative (MUL,
+// reading C23: one query / key unit per head) ss * sd; and its partials.
+template <bool MUL>
+__device__ __forceinline__ float att_logit(float ss, float sd, float slope) {
+  return MUL ? __fmul_rn(ss, sd) : leaky(ss + sd, slope);   // rounded product: no fma contraction
+}
+template <bool MUL>
+__device__ __forceinline__ float dlogit_dss(float ss, float sd, float slope) {
+  return MUL ? sd : ((ss + sd) > 0.f ? 1.f : slope);
+}
+template <bool MUL>
+__device__ __forceinline__ float dlogit_dsd(float ss, float sd, float slope) {
+  return MUL ? ss : ((ss + sd) > 0.f ? 1.f : slope);
+}
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
 // ------------------------------------------------------------ forward SUM/MEAN
@@ -112,7 +127,7 @@ k_col_to_x(int N, int R, const int* __restrict__ rel_y_off, RelOff so,
 // ------------------------------------------------------------- forward GAT
 // Per head h: two passes over the row's edges (rows are short): the max of the
 // logits, then p = exp(l - max), sum p and sum p * Y.  stats = (max, sum p).
-template <int D>
+template <int D, bool MUL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_ptr,
               const int* __restrict__ col, const float4* __restrict__ Y,
@@ -135,7 +150,7 @@ k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_pt
     for (int k = 0; k < n; k += NS) {
       int idx = k + sid;
       int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
-      if (idx < n) m = fmaxf(m, leaky(__ldg(s_src + (long long)c * H + h) + sd, slope));
+      if (idx < n) m = fmaxf(m, att_logit<MUL>(__ldg(s_src + (long long)c * H + h), sd, slope));
     }
   }
   // all streams agree on the max
@@ -158,7 +173,7 @@ k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_pt
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) {
-        float p = expf(leaky(sc[u] + sd, slope) - m);
+        float p = expf(att_logit<MUL>(sc[u], sd, slope) - m);
         l += p;
         acc = f4fma(p, v[u], acc);
       }
@@ -167,7 +182,7 @@ k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_pt
       int idx = k + sid;
       int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
       if (idx < n) {
-        float p = expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - m);
+        float p = expf(att_logit<MUL>(__ldg(s_src + (long long)c * H + h), sd, slope) - m);
         l += p;
         acc = f4fma(p, ldg4(Y + (long long)c * LPR + sl), acc);
       }
@@ -197,6 +212,7 @@ k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_pt
 // D = 64: one merged row per HALF warp (16 lanes x float4 = one Y row); the
 // two halves process two rows independently (rows are short: ~3-10 edges).
 // Same two passes as k_agg_fwd_gat; edges summed in row order.
+template <bool MUL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_fwd_gat_half(long long rows, int H, float slope, const int* __restrict__ row_ptr,
                    const int* __restrict__ col, const float4* __restrict__ Y,
@@ -216,7 +232,7 @@ k_agg_fwd_gat_half(long long rows, int H, float slope, const int* __restrict__ r
     const int my_col = hl < n ? __ldg(col + base + hl) : 0;
     for (int k = 0; k < n; k++) {
       const int c = __shfl_sync(mask, my_col, k, 16);
-      m = fmaxf(m, leaky(__ldg(s_src + (long long)c * H + h) + sd, slope));
+      m = fmaxf(m, att_logit<MUL>(__ldg(s_src + (long long)c * H + h), sd, slope));
     }
   }
   float l = 0.f;
@@ -236,14 +252,14 @@ k_agg_fwd_gat_half(long long rows, int H, float slope, const int* __restrict__ r
       }
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        const float p = expf(leaky(sc[u] + sd, slope) - m);
+        const float p = expf(att_logit<MUL>(sc[u], sd, slope) - m);
         l += p;
         acc = f4fma(p, v[u], acc);
       }
     }
     for (; k < n; k++) {
       const int c = __shfl_sync(mask, my_col, k, 16);
-      const float p = expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - m);
+      const float p = expf(att_logit<MUL>(__ldg(s_src + (long long)c * H + h), sd, slope) - m);
       l += p;
       acc = f4fma(p, ldg4(Y + (long long)c * 16 + hl), acc);
     }
@@ -606,7 +622,8 @@ k_agg_bwd_p_long(BwdMeta bm, const int* __restrict__ rel_row_off_d,
         for (int q = 0; q < GF; q++) {
           const int idx = kk + q * NS + sid;
           const int gq = __shfl_sync(0xffffffffu, me.g, idx < n ? idx : 0);
-          wq[q] = idx < n ? __shfl_sync(0xffffffffu, me.w, idx < n ? idx : 0) : 0.f;
+          const float wv = __shfl_sync(0xffffffffu, me.w, idx < n ? idx : 0);   // all lanes
+          wq[q] = idx < n ? wv : 0.f;
           x[q] = idx < n ? ldg4(G + (long long)gq * LPR + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
@@ -631,7 +648,7 @@ k_agg_bwd_p_long(BwdMeta bm, const int* __restrict__ rel_row_off_d,
 //   dalpha_p = <g_h, Y[col_p]_h>,  za = sum_p alpha_p dalpha_p,
 //   dpre_p   = alpha_p (dalpha_p - za) LeakyReLU'(pre_p),  ds_dst[m,h] = sum_p dpre_p.
 // alpha and dpre are stored per CSR position for pass 2.
-template <int D>
+template <int D, bool MUL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long rows, int H,
                    float slope, const int* __restrict__ row_ptr, const int* __restrict__ col,
@@ -682,7 +699,7 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
         const int idx = k0 + u * NS + sid;
         const float4 y = yv[u];
         float part = g.x * y.x + g.y * y.y + g.z * y.z + g.w * y.w;
-        const float a = idx < n ? expf(leaky(sv[u] + sd, slope) - mx) * inv_l : 0.f;
+        const float a = idx < n ? expf(att_logit<MUL>(sv[u], sd, slope) - mx) * inv_l : 0.f;
         for (int o = 1; o < dh4; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         if (idx < n) {
           za += a * part;
@@ -700,7 +717,7 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
       if (idx < n) {
         float4 y = ldg4(Y + (long long)c * LPR + sl);
         part = g.x * y.x + g.y * y.y + g.z * y.z + g.w * y.w;
-        a = expf(leaky(__ldg(s_src + (long long)c * H + h) + sd, slope) - mx) * inv_l;
+        a = expf(att_logit<MUL>(__ldg(s_src + (long long)c * H + h), sd, slope) - mx) * inv_l;
       }
       for (int o = 1; o < dh4; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       if (idx < n) {
@@ -719,12 +736,13 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
   if (head_lead) {
     for (int p = b + sid; p < e; p += NS) {
       int c = __ldg(col + p);
-      float pre = __ldg(s_src + (long long)c * H + h) + sd;
+      const float ss = __ldg(s_src + (long long)c * H + h);
       float a = alpha[(long long)p * H + h];
       float da = dpre[(long long)p * H + h];
-      float dp = a * (da - za) * (pre > 0.f ? 1.f : slope);
-      dpre[(long long)p * H + h] = dp;
-      dsd += dp;
+      const float dl = a * (da - za);
+      // dpre keeps the source-side partial (pass 2 sums it into ds_src)
+      dpre[(long long)p * H + h] = dl * dlogit_dss<MUL>(ss, sd, slope);
+      dsd += dl * dlogit_dsd<MUL>(ss, sd, slope);
     }
   }
 #pragma unroll
@@ -735,6 +753,7 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
 // D = 64: pass 1 with one merged row per HALF warp (rows are short; the
 // warp-per-row form split each row over two streams).  Same arithmetic as
 // k_agg_bwd_gat_rows, edges in row order.
+template <bool MUL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_bwd_gat_rows_half(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long rows, int H,
                         float slope, const int* __restrict__ row_ptr,
@@ -783,7 +802,7 @@ k_agg_bwd_gat_rows_half(BwdMeta bm, const int* __restrict__ rel_row_off_d, long 
         float part = g.x * yv[u].x + g.y * yv[u].y + g.z * yv[u].z + g.w * yv[u].w;
         for (int o = 1; o < dh4; o <<= 1) part += __shfl_xor_sync(mask, part, o, 16);
         if (idx < n) {
-          const float a = expf(leaky(sv[u] + sd, slope) - mx) * inv_l;
+          const float a = expf(att_logit<MUL>(sv[u], sd, slope) - mx) * inv_l;
           za += a * part;
           if (head_lead) {
             alpha[(long long)(base + idx) * H + h] = a;
@@ -798,12 +817,12 @@ k_agg_bwd_gat_rows_half(BwdMeta bm, const int* __restrict__ rel_row_off_d, long 
   if (head_lead) {
     for (int p = b; p < e; p++) {
       const int c = __ldg(col + p);
-      const float pre = __ldg(s_src + (long long)c * H + h) + sd;
+      const float ss = __ldg(s_src + (long long)c * H + h);
       const float a = alpha[(long long)p * H + h];
       const float da = dpre[(long long)p * H + h];
-      const float dp = a * (da - za) * (pre > 0.f ? 1.f : slope);
-      dpre[(long long)p * H + h] = dp;
-      dsd += dp;
+      const float dl = a * (da - za);
+      dpre[(long long)p * H + h] = dl * dlogit_dss<MUL>(ss, sd, slope);
+      dsd += dl * dlogit_dsd<MUL>(ss, sd, slope);
     }
     ds_dst[row * H + h] = dsd;
   }
@@ -1248,16 +1267,20 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_a
   cudaStream_t s = st(stream);
   unsigned grid = ceil_div(rows, kWarpsPerBlock);
   const int TB = kWarpsPerBlock * 32;
-  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL) {
+  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL || agg == HIFUSE_AGG_GAT_MUL) {
     if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
     if (rows > 0 && (!d_s_src || !d_s_dst || !d_stats)) return HIFUSE_ERR_INVALID_ARG;
-    if (D == 128)
-      HF_LAUNCH(k_agg_fwd_gat<128>, grid, TB, 0, s, (long long)rows, heads, slope, csr->row_ptr,
-                csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z, d_stats);
-    else
-      HF_LAUNCH(k_agg_fwd_gat_half, ceil_div(rows, kWarpsPerBlock * 2), TB, 0, s, (long long)rows,
-                heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,
-                (float4*)d_Z, d_stats);
+#define HF_GATF(MM)                                                                             \
+  if (D == 128)                                                                                 \
+    HF_LAUNCH((k_agg_fwd_gat<128, MM>), grid, TB, 0, s, (long long)rows, heads, slope,          \
+              csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst, (float4*)d_Z,       \
+              d_stats);                                                                         \
+  else                                                                                          \
+    HF_LAUNCH(k_agg_fwd_gat_half<MM>, ceil_div(rows, kWarpsPerBlock * 2), TB, 0, s,             \
+              (long long)rows, heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y,        \
+              d_s_src, d_s_dst, (float4*)d_Z, d_stats)
+    if (agg == HIFUSE_AGG_GAT_MUL) { HF_GATF(true); } else { HF_GATF(false); }
+#undef HF_GATF
   } else if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {
     bool mean = agg == HIFUSE_AGG_MEAN;
 #define HF_AGG(DD, MM)                                                                   \
@@ -1385,7 +1408,7 @@ size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
   long long U_max = m.N < m.S ? m.N : m.S;
   size_t b = carve_bytes(U_max + 1, 4) + carve_bytes(2, 4);
-  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL)
+  if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL || agg == HIFUSE_AGG_GAT_MUL)
     b += 2 * carve_bytes((long long)m.N * heads, 4);
   return b;
 }
@@ -1396,7 +1419,7 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
                                         const float* d_s_dst, const float* d_stats,
                                         const float* d_att, float* d_dY, float* d_ds_src,
                                         float* d_ds_dst, void* d_ws, size_t ws_bytes,
-                                        hifuse_stream_t stream) {
+                                        hifuse_stream_t stream, bool row_grad = false) {
   LayerMeta m;
   hifuse_status rc = make_meta(shape, &m);
   if (rc != HIFUSE_OK) return rc;
@@ -1407,7 +1430,9 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   if (ws_bytes < hifuse_aggregate_bwd_ws_bytes(shape, agg, heads) || !d_ws)
     return HIFUSE_ERR_WORKSPACE;
   // every host-side check before the first enqueue (an invalid call launches nothing)
-  const bool gat = agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL;
+  const bool gat = agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL ||
+                   agg == HIFUSE_AGG_GAT_MUL;
+  if (row_grad && agg == HIFUSE_AGG_GAT_XREL) return HIFUSE_ERR_UNSUPPORTED;
   if (gat) {
     if (!heads_ok(D, heads)) return HIFUSE_ERR_UNSUPPORTED;
     if (!d_Y || !d_s_src || !d_s_dst || !d_stats || !d_ds_src || !d_ds_dst || !csr->csc_pos ||
@@ -1422,7 +1447,10 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   cudaStream_t s = st(stream);
   BwdMeta bm;
   bm.R = m.R;
-  for (int r = 0; r < m.R; r++) bm.shift[r] = m.type_dst_off[m.rel_dst[r]] - m.rel_row_off[r];
+  // G row of merged row m: m + shift[r(m)] (type-major G), or m itself for a
+  // per-merged-row gradient (row_grad: HAN fusion, hifuse_aggregate_bwd_rows)
+  for (int r = 0; r < m.R; r++)
+    bm.shift[r] = row_grad ? 0 : m.type_dst_off[m.rel_dst[r]] - m.rel_row_off[r];
   long long U_max = m.N < m.S ? m.N : m.S;
   char* p = (char*)d_ws;
   int* long_list = carve<int>(p, U_max + 1);
@@ -1438,18 +1466,19 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
     unsigned gridR = ceil_div(m.rows, kWarpsPerBlock);
     XrelMeta xm;
     if (agg == HIFUSE_AGG_GAT_XREL) make_xrel(m, &xm);
-#define HF_GAT(DD)                                                                             \
+#define HF_GAT(DD, MM)                                                                         \
   if (agg == HIFUSE_AGG_GAT_XREL)                                                              \
     HF_LAUNCH(k_agg_bwd_gat_xrel_dst<DD>, ceil_div(m.dst_rows, kWarpsPerBlock), TB, 0, s, xm, \
               m.dst_rows, heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src,   \
               d_s_dst, d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                    \
   else if (DD == 64)                                                                           \
-    HF_LAUNCH(k_agg_bwd_gat_rows_half, ceil_div(m.rows, kWarpsPerBlock * 2), TB, 0, s, bm,      \
+    HF_LAUNCH(k_agg_bwd_gat_rows_half<MM>, ceil_div(m.rows, kWarpsPerBlock * 2), TB, 0, s, bm,  \
               csr->rel_row_off, (long long)m.rows, heads, slope, csr->row_ptr, csr->col,        \
               (const float4*)d_Y, d_s_src, d_s_dst, d_stats, (const float4*)d_G, alpha, dpre,   \
               d_ds_dst);                                                                       \
   else                                                                                         \
-    HF_LAUNCH(k_agg_bwd_gat_rows<DD>, gridR, TB, 0, s, bm, csr->rel_row_off, (long long)m.rows, \
+    HF_LAUNCH((k_agg_bwd_gat_rows<DD, MM>), gridR, TB, 0, s, bm, csr->rel_row_off,              \
+              (long long)m.rows,                                                              \
               heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,     \
               d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                            \
   if (DD == 64)                                                                                \
@@ -1463,7 +1492,9 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   HF_LAUNCH(k_agg_bwd_gat_cols_long<DD>, gridL, kLongWarps * 32, 0, s, bm, heads, csr->rel_y_off,          \
             csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
             (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att)
-    if (D == 128) { HF_GAT(128); } else { HF_GAT(64); }
+    const bool mul = agg == HIFUSE_AGG_GAT_MUL;
+    if (D == 128) { if (mul) { HF_GAT(128, true); } else { HF_GAT(128, false); } }
+    else { if (mul) { HF_GAT(64, true); } else { HF_GAT(64, false); } }
 #undef HF_GAT
   } else {
 #define HF_BWD(DD, MM)                                                                        \
@@ -1498,11 +1529,26 @@ hifuse_status hifuse_aggregate_bwd_scored(const hifuse_layer_shape* shape, const
                                           const float* d_stats, const float* d_att, float* d_dY,
                                           float* d_ds_src, float* d_ds_dst, void* d_ws,
                                           size_t ws_bytes, hifuse_stream_t stream) {
-  if ((agg != HIFUSE_AGG_GAT && agg != HIFUSE_AGG_GAT_XREL) || !d_att)
+  if ((agg != HIFUSE_AGG_GAT && agg != HIFUSE_AGG_GAT_XREL && agg != HIFUSE_AGG_GAT_MUL) ||
+      !d_att)
     return HIFUSE_ERR_INVALID_ARG;
   if (!aligned16(d_att)) return HIFUSE_ERR_ALIGNMENT;
   return aggregate_bwd_impl(shape, csr, agg, D, heads, slope, d_G, d_Y, d_s_src, d_s_dst, d_stats,
                             d_att, d_dY, d_ds_src, d_ds_dst, d_ws, ws_bytes, stream);
+}
+
+hifuse_status hifuse_aggregate_bwd_rows(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                        hifuse_agg agg, int D, int heads, float slope,
+                                        const float* d_dZ, const float* d_Y,
+                                        const float* d_s_src, const float* d_s_dst,
+                                        const float* d_stats, const float* d_att, float* d_dY,
+                                        float* d_ds_src, float* d_ds_dst, void* d_ws,
+                                        size_t ws_bytes, hifuse_stream_t stream) {
+  if (d_att && (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN)) return HIFUSE_ERR_INVALID_ARG;
+  if (d_att && !aligned16(d_att)) return HIFUSE_ERR_ALIGNMENT;
+  return aggregate_bwd_impl(shape, csr, agg, D, heads, slope, d_dZ, d_Y, d_s_src, d_s_dst,
+                            d_stats, d_att, d_dY, d_ds_src, d_ds_dst, d_ws, ws_bytes, stream,
+                            true);
 }
 
 }  // extern "C"

@@ -1005,6 +1005,30 @@ hifuse_status hifuse_project_aggregated(const hifuse_layer_shape* shape, const h
   return last_cuda();
 }
 
+hifuse_status hifuse_project_fuse_aggregated(const hifuse_layer_shape* shape,
+                                            const hifuse_csr* csr, hifuse_prec prec, int K, int D,
+                                            hifuse_act act, const float* d_Xagg,
+                                            const float* d_X, int64_t x_rows,
+                                            const int32_t* d_gather_ids, const float* d_W_rel,
+                                            const float* d_W_root, const float* d_bias,
+                                            float* d_H, hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (!kd_ok(K, D) || prec != HIFUSE_PREC_TF32) return HIFUSE_ERR_UNSUPPORTED;
+  if (act != HIFUSE_ACT_RELU && act != HIFUSE_ACT_NONE) return HIFUSE_ERR_INVALID_ARG;
+  if (!csr || !csr->rel_row_off || !d_W_rel || (m.dst_rows > 0 && !d_H) || x_rows < 0 ||
+      (m.rows > 0 && !d_Xagg) || (d_W_root && !d_X))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_Xagg) || !aligned16(d_X) || !aligned16(d_W_rel) || !aligned16(d_W_root) ||
+      !aligned16(d_bias) || !aligned16(d_H))
+    return HIFUSE_ERR_ALIGNMENT;
+  rc = fuse_gemm_launch(m, d_W_root != nullptr, K, D, act == HIFUSE_ACT_RELU, d_gather_ids, d_X,
+                        d_Xagg, d_W_rel, d_W_root, d_bias, d_H, st(stream));
+  if (rc != HIFUSE_OK) return rc;
+  return last_cuda();
+}
+
 size_t hifuse_project_aggregated_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D) {
   LayerMeta m;
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;

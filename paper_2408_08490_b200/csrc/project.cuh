@@ -47,6 +47,12 @@ hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, 
                                  const float* Xm, const int* gather_ids, const float* W_rel,
                                  const float* W_root, float* Y, float* R0, const float* att,
                                  float* s_src, int H, cudaStream_t s);
+// tcgen05 TF32 fused fusion GEMM of the aggregate-first input layer (NEXT(3)):
+// H_t = act([X_t | Xagg_r...] [W_root,t; W_r...] + b_t), one launch.
+hifuse_status fuse_gemm_launch(const LayerMeta& m, bool has_root, int K, int D, bool relu,
+                               const int* gid, const float* X, const float* Xm,
+                               const float* W_rel, const float* W_root, const float* bias,
+                               float* H, cudaStream_t s);
 // tcgen05 TF32 dgrad: dX[type s rows] = sum_terms A_term W_term^T (A = dYt rows
 // through slot_y, or G for the root term).  dm built with bm = 128.
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,

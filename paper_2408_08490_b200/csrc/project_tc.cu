@@ -690,6 +690,207 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
   if (warp == 8) tmem_dealloc(tmem, 2 * D);
 }
 
+// ------------------------------------------- fused fusion GEMM (NEXT(3)) ----
+// Aggregate-first RGCN input layer, projection + semantic fusion as ONE
+// tcgen05 GEMM per destination type (PAPER.md lines
+// 265-268, merging for memory efficiency and fewer kernels):
+//   H_t[i] = act( [X_t[i] | Xagg_{r1}[i] | Xagg_{r2}[i] | ...]
+//                 . [W_root,t ; W_r1 ; W_r2 ; ...] + b_t ),  r_j: t(r_j) = t,
+// i.e. K = (1 + R_in(t)) * K_in, accumulated in one TMEM tile, bias and ReLU
+// in the epilogue, H written once: no Z [rho, D] / R0 write and re-read, no
+// separate fusion kernel.  Same warp specialisation, swizzles and stages as
+// k_proj_fwd_tcp; the A rows of a K segment come from the feature store
+// (root segment, through gather_ids) or from the aggregated rows
+// Xagg[rel_row_off[r] + i]; the B chunks from W_root[t] / W_rel[r].
+struct FuseGemmMeta {
+  int T, R, has_root;
+  int tile_off[HF_MAX_T + 1];      // 128-row tiles of each destination type
+  int n_dst[HF_MAX_T];
+  int type_src_off[HF_MAX_T + 1];
+  int type_dst_off[HF_MAX_T + 1];
+  int in_off[HF_MAX_T + 1];        // relations into type t: in_rel[in_off[t] .. in_off[t+1])
+  int in_rel[HF_MAX_R];
+  int rel_row_off[HF_MAX_R + 1];
+};
+
+template <int K, int D, bool RELU>
+__global__ void __launch_bounds__(288, kFwdCtas)
+k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float* __restrict__ X,
+                const float* __restrict__ Xm, const float* __restrict__ W_rel,
+                const float* __restrict__ W_root, const float* __restrict__ bias,
+                float* __restrict__ H) {
+  constexpr int BM = 128, NCS = K / 32;                      // chunks per K segment
+  constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
+  constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+  constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 1);      // A K-major, B MN-major
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[kFStages], empty[kFStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(16) float stage_ep[4 * 32 * 20];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  if (tid == 0) {
+    for (int q = 0; q < kFStages; q++) {
+      mbar_init(smem_u32(&full[q]), 128);
+      mbar_init(smem_u32(&empty[q]), 1);
+    }
+    for (int q = 0; q < 2; q++) {
+      mbar_init(smem_u32(&tfull[q]), 1);
+      mbar_init(smem_u32(&tempty[q]), 128);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 8) tmem_alloc(smem_u32(&tmem_slot), 2 * D);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int ntiles = fm.tile_off[fm.T];
+  // tile -> (type, first row, rows, K segments)
+  auto resolve = [&](int t, int* ty, int* r0, int* nrows, int* nseg) {
+    int lo = 0, hi = fm.T;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (fm.tile_off[mid] <= t) lo = mid; else hi = mid;
+    }
+    *ty = lo;
+    *r0 = (t - fm.tile_off[lo]) * BM;
+    *nrows = min(BM, fm.n_dst[lo] - *r0);
+    *nseg = fm.has_root + fm.in_off[lo + 1] - fm.in_off[lo];
+  };
+  if (warp < 4) {
+    // ------------------------------------------------------------ producers
+    const int piece = lane & 7, rsub = lane >> 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int ty, r0, nrows, nseg;
+      resolve(t, &ty, &r0, &nrows, &nseg);
+      for (int sg = 0; sg < nseg; sg++) {
+        // segment sg: root (sg == 0 with a root term) or relation in_rel[...]
+        const bool root = fm.has_root && sg == 0;
+        const int r = root ? -1 : fm.in_rel[fm.in_off[ty] + sg - fm.has_root];
+        const float* Wg = root ? W_root + (long long)ty * K * D : W_rel + (long long)r * K * D;
+        const float* ap[8];
+        uint32_t nb[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const int row = warp * 32 + i * 4 + rsub;
+          ap[i] = Xm;
+          nb[i] = 0;
+          if (row < nrows) {
+            if (root) {
+              const int x = fm.type_src_off[ty] + r0 + row;     // destinations: source prefix
+              ap[i] = X + (long long)(gather_ids ? gather_ids[x] : x) * K;
+            } else {
+              ap[i] = Xm + (long long)(fm.rel_row_off[r] + r0 + row) * K;
+            }
+            nb[i] = 16;
+          }
+        }
+        for (int c = 0; c < NCS; c++, it++) {
+          const int s = it % kFStages;
+          if (it >= kFStages) mbar_wait(smem_u32(&empty[s]), ((it / kFStages) - 1) & 1);
+          const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+          for (int i = 0; i < 8; i++) {
+            const int row = warp * 32 + i * 4 + rsub;
+            cp_async16(sa + sw128_off(row, piece), ap[i] + c * 32 + piece * 4, nb[i]);
+          }
+#pragma unroll
+          for (int q = 0; q < 32 * D / 4 / 128; q++) {
+            const int i = tid + 128 * q;
+            const int kr = i / (D / 4), n = (i % (D / 4)) * 4;
+            cp_async16(sb + (n >> 5) * B_BLK + (kr >> 2) * 512 + sw128b32_off(kr, (n & 31) * 4),
+                       Wg + (long long)(c * 32 + kr) * D + n, 16);
+          }
+          cp_async_commit();
+          if (it >= kLag) {
+            cp_async_wait<kLag>();
+            fence_proxy_async();
+            mbar_arrive(smem_u32(&full[(it - kLag) % kFStages]));
+          }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async();
+    for (int j = it - kLag < 0 ? 0 : it - kLag; j < it; j++) mbar_arrive(smem_u32(&full[j % kFStages]));
+  } else if (warp < 8) {
+    // ------------------------------------------------------------- epilogue
+    const int q = warp - 4;
+    int tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      const int acc = tc & 1;
+      int ty, r0, nrows, nseg;
+      resolve(t, &ty, &r0, &nrows, &nseg);
+      mbar_wait(smem_u32(&tfull[acc]), (tc >> 1) & 1);
+      tc_fence_after();
+      float* out = H + (long long)(fm.type_dst_off[ty] + r0) * D;
+      const float* bt = bias ? bias + (long long)ty * D : nullptr;
+      float* st = stage_ep + q * (32 * 20);
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + (uint32_t)(acc * D) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+        if (nseg == 0) {
+#pragma unroll
+          for (int jj = 0; jj < 16; jj++) v[jj] = 0.f;    // no term at all: act(b)
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          float4 b4 = bt ? __ldg(reinterpret_cast<const float4*>(bt + c0) + jj)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 o4 = make_float4(v[4 * jj] + b4.x, v[4 * jj + 1] + b4.y, v[4 * jj + 2] + b4.z,
+                                  v[4 * jj + 3] + b4.w);
+          if (RELU) {
+            o4.x = fmaxf(o4.x, 0.f); o4.y = fmaxf(o4.y, 0.f);
+            o4.z = fmaxf(o4.z, 0.f); o4.w = fmaxf(o4.w, 0.f);
+          }
+          *reinterpret_cast<float4*>(st + lane * 20 + 4 * jj) = o4;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int rr = i * 8 + (lane >> 2), ch = lane & 3;
+          const int row = q * 32 + rr;
+          const float4 x = *reinterpret_cast<const float4*>(st + rr * 20 + 4 * ch);
+          if (row < nrows) *reinterpret_cast<float4*>(out + (long long)row * D + c0 + 4 * ch) = x;
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(&tempty[acc]));
+    }
+  } else if (lane == 0) {
+    // ------------------------------------------------------------------ MMA
+    int it = 0, tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      const int acc = tc & 1;
+      int ty, r0, nrows, nseg;
+      resolve(t, &ty, &r0, &nrows, &nseg);
+      if (tc >= 2) mbar_wait(smem_u32(&tempty[acc]), ((tc >> 1) - 1) & 1);
+      tc_fence_after();
+      const int nc = nseg * NCS;
+      for (int c = 0; c < nc; c++, it++) {
+        const int s = it % kFStages;
+        mbar_wait(smem_u32(&full[s]), (it / kFStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          mma_tf32(tmem + (uint32_t)(acc * D), sw128_desc(sa + k * 32, 16, 1024),
+                   sw128b32_desc(sb + k * 1024, B_BLK, 512), IDESC, (c | k) ? 1u : 0u);
+        mma_commit(smem_u32(&empty[s]));
+      }
+      mma_commit(smem_u32(&tfull[acc]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) tmem_dealloc(tmem, 2 * D);
+}
+
 template <int K, int D>
 static constexpr int fwdp_smem() { return kFStages * (128 * 128 + D * 128) + 1024; }
 
@@ -701,6 +902,51 @@ static void launch_tcp(const ProjMeta& pm, const int* rel_off, const int* y_src,
   set_max_smem((const void*)k_proj_fwd_tcp<K, D>, fwdp_smem<K, D>());
   HF_LAUNCH((k_proj_fwd_tcp<K, D>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
             rel_off, y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, Xm);
+}
+
+template <int K, int D, bool RELU>
+static void launch_fuse_gemm(const FuseGemmMeta& fm, const int* gid, const float* X,
+                             const float* Xm, const float* W_rel, const float* W_root,
+                             const float* bias, float* H, cudaStream_t s) {
+  set_max_smem(reinterpret_cast<const void*>(&k_fuse_gemm_tcp<K, D, RELU>), fwdp_smem<K, D>());
+  HF_LAUNCH((k_fuse_gemm_tcp<K, D, RELU>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s, fm,
+            gid, X, Xm, W_rel, W_root, bias, H);
+}
+
+hifuse_status fuse_gemm_launch(const LayerMeta& m, bool has_root, int K, int D, bool relu,
+                               const int* gid, const float* X, const float* Xm,
+                               const float* W_rel, const float* W_root, const float* bias,
+                               float* H, cudaStream_t s) {
+  FuseGemmMeta fm;
+  fm.T = m.T;
+  fm.R = m.R;
+  fm.has_root = has_root ? 1 : 0;
+  int tiles = 0, k = 0;
+  for (int t = 0; t < m.T; t++) {
+    fm.tile_off[t] = tiles;
+    tiles += (m.n_dst[t] + 127) / 128;
+    fm.n_dst[t] = m.n_dst[t];
+    fm.in_off[t] = k;
+    for (int r = 0; r < m.R; r++)
+      if (m.rel_dst[r] == t) fm.in_rel[k++] = r;
+  }
+  fm.tile_off[m.T] = tiles;
+  fm.in_off[m.T] = k;
+  for (int t = 0; t <= m.T; t++) {
+    fm.type_src_off[t] = m.type_src_off[t];
+    fm.type_dst_off[t] = m.type_dst_off[t];
+  }
+  for (int r = 0; r <= m.R; r++) fm.rel_row_off[r] = m.rel_row_off[r];
+  if (tiles == 0) return HIFUSE_OK;
+#define HF_FG(KK, DD)                                                                          \
+  if (relu) launch_fuse_gemm<KK, DD, true>(fm, gid, X, Xm, W_rel, W_root, bias, H, s);         \
+  else launch_fuse_gemm<KK, DD, false>(fm, gid, X, Xm, W_rel, W_root, bias, H, s)
+  if (K == 128 && D == 128) { HF_FG(128, 128); }
+  else if (K == 128 && D == 64) { HF_FG(128, 64); }
+  else if (K == 64 && D == 128) { HF_FG(64, 128); }
+  else { HF_FG(64, 64); }
+#undef HF_FG
+  return HIFUSE_OK;
 }
 
 hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, int D,

@@ -18,7 +18,7 @@ def _align4(n):
 class ParamLayout:
     """Offsets of every parameter inside the flat buffer (16-byte aligned)."""
 
-    def __init__(self, T, R, K0, D, H, C, L, model):
+    def __init__(self, T, R, K0, D, H, C, L, model, fusion="sum"):
         self.entries = []
         off = 0
 
@@ -36,9 +36,25 @@ class ParamLayout:
             add(f"{l}.bias", (T, D))
             if model == "rgat":
                 add(f"{l}.att", (R, 2, D))
+            if fusion == "han":          # HAN semantic attention (A = D)
+                add(f"{l}.sem_W", (D, D))
+                add(f"{l}.sem_b", (D,))
+                add(f"{l}.sem_q", (D,))
         add("Wc", (D, C))
         add("bc", (C,))
         self.size = off
+
+    def buckets(self, L):
+        """Contiguous [lo, hi) ranges of the flat buffer: one per HGNN layer
+        (its W_rel, W_root, bias, att, sem_* entries) and one for the classifier
+        (Wc, bc), keyed "layer{l}" / "head"."""
+        out = {}
+        for name, o, shp in self.entries:
+            key = f"layer{name.split('.')[0]}" if "." in name else "head"
+            n = _align4(int(np.prod(shp)))
+            lo, hi = out.get(key, (o, o))
+            out[key] = (min(lo, o), max(hi, o + n))
+        return out
 
     def views(self, flat):
         return {name: flat[o:o + int(np.prod(s))].view(*s) for name, o, s in self.entries}

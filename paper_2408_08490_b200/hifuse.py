@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhifuse.so")
 
-AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3}
+AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3, "gat_mul": 4}
 ACT = {"none": 0, "relu": 1}
 LAYOUT_COMPACT = 1
 PREC = {"fp32": 0, "tf32": 1}
@@ -85,6 +85,8 @@ def lib():
                                      vp, sz, vp],
             "hifuse_aggregate_bwd_scored": [vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp,
                                             vp, vp, vp, sz, vp],
+            "hifuse_aggregate_bwd_rows": [vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp,
+                                          vp, vp, vp, sz, vp],
             "hifuse_project_bwd_scored": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp,
                                           vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
             "hifuse_project_bwd_ws_bytes": [vp, i32, i32, i32],
@@ -108,6 +110,16 @@ def lib():
             "hifuse_sample_blocks": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, vp, i32, vp, vp,
                                      vp, sz, vp, vp],
             "hifuse_read_status": [vp, vp, vp],
+            "hifuse_sem_att_ws_bytes": [vp, i32, i32],
+            "hifuse_project_fuse_aggregated": [vp, vp, i32, i32, i32, i32, vp, vp, i64, vp, vp, vp,
+                                               vp, vp, vp],
+            "hifuse_shard_plan": [vp, i64, vp, i32, vp, vp, vp, vp],
+            "hifuse_gather_words": [vp, vp, i64, i32, i64, vp, vp],
+            "hifuse_scatter_words": [vp, vp, i64, i32, vp, vp],
+            "hifuse_semantic_fuse_att": [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                         vp, sz, vp],
+            "hifuse_semantic_fuse_att_bwd": [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             vp, vp, vp, vp, vp, vp, sz, vp],
             "hifuse_stream_attach": [vp],
             "hifuse_stream_release": [vp],
             "hifuse_kernel_launches": [],
@@ -119,7 +131,7 @@ def lib():
         for name in ("hifuse_project_ws_bytes", "hifuse_fuse_bwd_ws_bytes",
                      "hifuse_aggregate_bwd_ws_bytes", "hifuse_project_bwd_ws_bytes",
                      "hifuse_xent_ws_bytes", "hifuse_aggregate_features_ws_bytes",
-                     "hifuse_project_aggregated_bwd_ws_bytes"):
+                     "hifuse_project_aggregated_bwd_ws_bytes", "hifuse_sem_att_ws_bytes"):
             getattr(L, name).restype = ctypes.c_size_t
         L.hifuse_kernel_launches.restype = ctypes.c_int64
         L.hifuse_status_string.restype = ctypes.c_char_p
@@ -286,6 +298,34 @@ def aggregate_bwd_scored(shape, csr, agg, D, heads, slope, G, Y, s_src, s_dst, s
         ws.numel() * ws.element_size(), _stream(stream)))
 
 
+def aggregate_bwd_rows(shape, csr, agg, D, heads, slope, dZ, Y, s_src, s_dst, stats, att, dY,
+                       ds_src, ds_dst, ws, stream=None):
+    """hifuse_aggregate_bwd_rows: per-merged-row gradient dZ [rows, D]."""
+    _check("hifuse_aggregate_bwd_rows", lib().hifuse_aggregate_bwd_rows(
+        shape.ref, csr.ref, AGG[agg], D, heads, slope, _ptr(dZ), _ptr(Y), _ptr(s_src),
+        _ptr(s_dst), _ptr(stats), _ptr(att), _ptr(dY), _ptr(ds_src), _ptr(ds_dst), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def sem_att_ws_bytes(shape, D, A):
+    return int(lib().hifuse_sem_att_ws_bytes(shape.ref, D, A))
+
+
+def semantic_fuse_att(shape, D, A, act, Z, R0, bias, Ws, bs, q, beta, w, H, ws, stream=None):
+    """hifuse_semantic_fuse_att: HAN semantic-attention fusion (NEXT(2))."""
+    _check("hifuse_semantic_fuse_att", lib().hifuse_semantic_fuse_att(
+        shape.ref, D, A, ACT[act], _ptr(Z), _ptr(R0), _ptr(bias), _ptr(Ws), _ptr(bs), _ptr(q),
+        _ptr(beta), _ptr(w), _ptr(H), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def semantic_fuse_att_bwd(shape, D, A, act, dH, H, Z, Ws, bs, q, beta, G, dZ, dbias, dWs, dbs,
+                          dq, ws, stream=None):
+    _check("hifuse_semantic_fuse_att_bwd", lib().hifuse_semantic_fuse_att_bwd(
+        shape.ref, D, A, ACT[act], _ptr(dH), _ptr(H), _ptr(Z), _ptr(Ws), _ptr(bs), _ptr(q),
+        _ptr(beta), _ptr(G), _ptr(dZ), _ptr(dbias), _ptr(dWs), _ptr(dbs), _ptr(dq), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
+
+
 def project_bwd_ws_bytes(shape, K, D, heads):
     return int(lib().hifuse_project_bwd_ws_bytes(shape.ref, K, D, heads))
 
@@ -415,3 +455,29 @@ def stream_attach(stream=None):
 
 def stream_release(stream=None):
     _check("hifuse_stream_release", lib().hifuse_stream_release(_stream(stream)))
+
+
+def shard_plan(ids, n, bounds, W, counts, order, status, stream=None):
+    """hifuse_shard_plan (NEXT(4)): ids grouped by owner rank."""
+    _check("hifuse_shard_plan", lib().hifuse_shard_plan(
+        _ptr(ids), n, _ptr(bounds), W, _ptr(counts), _ptr(order), _ptr(status), _stream(stream)))
+
+
+def gather_words(src, idx, n, words, base, dst, stream=None):
+    _check("hifuse_gather_words", lib().hifuse_gather_words(
+        _ptr(src), _ptr(idx), n, words, base, _ptr(dst), _stream(stream)))
+
+
+def scatter_words(src, idx, n, words, dst, stream=None):
+    _check("hifuse_scatter_words", lib().hifuse_scatter_words(
+        _ptr(src), _ptr(idx), n, words, _ptr(dst), _stream(stream)))
+
+
+def project_fuse_aggregated(shape, csr, K, D, act, Xagg, X, gather_ids, W_rel, W_root, bias, H,
+                            prec="tf32", stream=None):
+    """hifuse_project_fuse_aggregated: the aggregate-first layer's projection
+    and fusion as one GEMM per destination type (NEXT(3))."""
+    _check("hifuse_project_fuse_aggregated", lib().hifuse_project_fuse_aggregated(
+        shape.ref, csr.ref, PREC[prec], K, D, ACT[act], _ptr(Xagg), _ptr(X),
+        X.shape[0] if X is not None else 0, _ptr(gather_ids), _ptr(W_rel), _ptr(W_root),
+        _ptr(bias), _ptr(H), _stream(stream)))

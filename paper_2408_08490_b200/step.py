@@ -80,20 +80,24 @@ class Trainer:
     """Owns parameters, gradients, activations and workspaces of the step."""
 
     def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
-                 prec="tf32", slope=0.2, order="project_first"):
+                 prec="tf32", slope=0.2, order="project_first", fusion="sum", fuse_gemm=True):
         hf.lib()   # raises if libhifuse.so is missing (no CPU fallback)
         self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
         self.rel_src = np.asarray(rel_src, np.int32)
         self.rel_dst = np.asarray(rel_dst, np.int32)
         self.model, self.agg, self.device, self.lr, self.prec, self.slope = (
             model, agg, device, lr, prec, slope)
-        self.layout = ParamLayout(T, R, K0, D, H, C, L, model)
+        if fusion not in ("sum", "han"):
+            raise ValueError(fusion)
+        self.fusion = fusion       # "han": HAN semantic-attention fusion (NEXT(2), reading C22)
+        self.layout = ParamLayout(T, R, K0, D, H, C, L, model, fusion)
         self.params = torch.zeros(self.layout.size, dtype=torch.float32, device=device)
         self.grads = torch.zeros_like(self.params)
         self.P = self.layout.views(self.params)
         self.Gd = self.layout.views(self.grads)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
+        self.world, self.dp_group, self._comm = 1, None, None
         self._bufs = {}
         self._views = {}
         self.heads = H if model == "rgat" else 1
@@ -103,8 +107,13 @@ class Trainer:
         # scores, so it always projects first.
         if order not in ("project_first", "agg_first"):
             raise ValueError(order)
-        self.agg_first = order == "agg_first" and model == "rgcn" and prec == "tf32"
+        # (HAN fusion gives every relation its own gradient: project-first only)
+        self.agg_first = (order == "agg_first" and model == "rgcn" and prec == "tf32" and
+                          fusion == "sum")
         self.order = "agg_first" if self.agg_first else "project_first"
+        # aggregate-first input layer: projection + fusion as one GEMM per
+        # destination type (hifuse_project_fuse_aggregated, NEXT(3))
+        self.fuse_gemm = bool(fuse_gemm) and self.agg_first
         # capture streams: `_hi` (high priority) for the pipelined graphs,
         # `_cap` for the serial / per-stage graphs; the library's fork/join
         # resources of every stream that runs steps are created here, outside
@@ -118,11 +127,42 @@ class Trainer:
 
     def load_params(self, p):
         for l, lay in enumerate(p["layers"]):
-            for k in ("W_rel", "W_root", "bias", "att"):
+            for k in ("W_rel", "W_root", "bias", "att", "sem_W", "sem_b", "sem_q"):
                 if lay.get(k) is not None and f"{l}.{k}" in self.P:
                     self.P[f"{l}.{k}"].copy_(torch.from_numpy(np.asarray(lay[k], np.float32)))
         self.P["Wc"].copy_(torch.from_numpy(np.asarray(p["Wc"], np.float32)))
         self.P["bc"].copy_(torch.from_numpy(np.asarray(p["bc"], np.float32)))
+
+    # ------------------------------------------------------ data parallelism
+    def set_dp(self, world, group=None):
+        """Data parallelism over independent mini-batches:
+        the weight gradients are summed over `world` ranks with one all-reduce
+        per bucket (one bucket per HGNN layer + the classifier), each issued on
+        a communication stream as soon as its layer's backward has produced
+        them, overlapping the backward of the layers below; the SGD applies the
+        1/world factor.  With NCCL the all-reduces are capturable, so a whole
+        DP step (compute + collectives + update) is one CUDA graph."""
+        self.world = int(world)
+        self.dp_group = group
+        self._comm = torch.cuda.Stream(device=self.device) if self.world > 1 else None
+        self._bk = self.layout.buckets(self.L)
+
+    def _allreduce_op(self, key):
+        """Op: the comm stream waits for everything issued so far (main and
+        weight-gradient side stream) and all-reduces bucket `key`."""
+        import torch.distributed as dist
+        lo, hi = self._bk[key]
+
+        def run():
+            main = torch.cuda.current_stream()
+            self._comm.wait_stream(main)
+            self._comm.wait_stream(self._head_side)
+            with torch.cuda.stream(self._comm):
+                dist.all_reduce(self.grads[lo:hi], group=self.dp_group)
+        return run
+
+    def _dp_join(self):
+        torch.cuda.current_stream().wait_stream(self._comm)
 
     # -------------------------------------------------------------- buffers
     def _buf(self, key, n, dtype=torch.float32):
@@ -230,12 +270,19 @@ class Trainer:
                 ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a, colx=colx:
                             hf.aggregate_features_cols(sh, c, self.agg, a["K"], a["X"], colx,
                                                        a["Xagg"])))
-                ops.append(("project_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
-                            hf.project_aggregated(sh, c, a["K"], D, a["Xagg"], a["X"], a["gid"],
-                                                  P["W_rel"], P["W_root"], a["Z"], a["R0"],
-                                                  prec=self.prec)))
-                ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
-                    sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
+                if self.fuse_gemm:
+                    ops.append(("project_fuse_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
+                                hf.project_fuse_aggregated(sh, c, a["K"], D, a["act"], a["Xagg"],
+                                                           a["X"], a["gid"], P["W_rel"],
+                                                           P["W_root"], P["bias"], a["H"],
+                                                           prec=self.prec)))
+                else:
+                    ops.append(("project_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
+                                hf.project_aggregated(sh, c, a["K"], D, a["Xagg"], a["X"],
+                                                      a["gid"], P["W_rel"], P["W_root"], a["Z"],
+                                                      a["R0"], prec=self.prec)))
+                    ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
+                        sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
                 acts.append(a)
                 X, gid = a["H"], None
                 continue
@@ -250,8 +297,16 @@ class Trainer:
                 ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a: hf.aggregate_fwd(
                     c, sh.rows, self.agg, D, H, self.slope, a["Y"], a["s_src"], a["s_dst"],
                     a["Z"], a["stats"])))
-            ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
-                sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
+            if self.fusion == "han":
+                a["beta"] = self._buf(f"beta{l}", max(sh.R, 1))
+                a["wss"] = self._ws(hf.sem_att_ws_bytes(sh, D, D), key=f"ws_sem{l}")
+                ops.append((f"fuse.{l}", lambda sh=sh, a=a, l=l: hf.semantic_fuse_att(
+                    sh, D, D, a["act"], a["Z"], a["R0"], self.P[f"{l}.bias"],
+                    self.P[f"{l}.sem_W"], self.P[f"{l}.sem_b"], self.P[f"{l}.sem_q"], a["beta"],
+                    None, a["H"], a["wss"])))
+            else:
+                ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
+                    sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
             acts.append(a)
             X, gid = a["H"], None
         last = shapes[-1]
@@ -276,6 +331,8 @@ class Trainer:
             dH[:last.dst_rows], None, None, wsx, status=self.status)))
         ops.append(("xent_wgrad", side_op(lambda: hf.linear_xent_wgrad(
             db.B, D, C, Hl, db.h_row0, self.Gd["Wc"], self.Gd["bc"], wsx))))
+        if self.world > 1:
+            ops.append(("allreduce.head", self._allreduce_op("head")))
         for l in range(L - 1, -1, -1):
             sh, a = shapes[l], acts[l]
             P = {k: self.P.get(f"{l}.{k}") for k in ("W_rel", "W_root", "bias", "att")}
@@ -290,6 +347,8 @@ class Trainer:
                             hf.project_aggregated_bwd(sh, c, a["K"], D, a["Xagg"], a["X"],
                                                       a["gid"], b["G"], Gr["W_rel"],
                                                       Gr["W_root"], b["wsq"], prec=self.prec)))
+                if self.world > 1:
+                    ops.append((f"allreduce.{l}", self._allreduce_op(f"layer{l}")))
                 continue
             b = dict(dH=dH, G=self._mat(f"G{l}", sh.dst_rows, D),
                      dY=self._mat(f"dY{l}", sh.U_max, D),
@@ -299,9 +358,25 @@ class Trainer:
                      wsf=self._ws(hf.fuse_bwd_ws_bytes(sh, D)),
                      wsa=self._ws(hf.aggregate_bwd_ws_bytes(sh, self.agg, H)),
                      wsq=self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H)))
-            ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
-                sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
-            if P["att"] is not None:   # RGAT: score chain folded into the CSC pass
+            if self.fusion == "han":
+                # HAN: per-merged-row gradient dZ, then the row-gradient adjoint
+                b["dZ"] = self._mat(f"dZ{l}", sh.rows, D)
+                ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, l=l: hf.semantic_fuse_att_bwd(
+                    sh, D, D, a["act"], b["dH"], a["H"], a["Z"], self.P[f"{l}.sem_W"],
+                    self.P[f"{l}.sem_b"], self.P[f"{l}.sem_q"], a["beta"], b["G"], b["dZ"],
+                    self.Gd[f"{l}.bias"], self.Gd[f"{l}.sem_W"], self.Gd[f"{l}.sem_b"],
+                    self.Gd[f"{l}.sem_q"], a["wss"])))
+                ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P:
+                            hf.aggregate_bwd_rows(sh, c, self.agg, D, H, self.slope, b["dZ"],
+                                                  a["Y"], a["s_src"], a["s_dst"], a["stats"],
+                                                  P["att"], b["dY"], b["ds_src"], b["ds_dst"],
+                                                  b["wsa"])))
+            else:
+                ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
+                    sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
+            if self.fusion == "han":
+                pass                   # aggregation adjoint queued above
+            elif P["att"] is not None:   # RGAT: score chain folded into the CSC pass
                 ops.append((f"aggregate_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P:
                             hf.aggregate_bwd_scored(sh, c, self.agg, D, H, self.slope, b["G"],
                                                     a["Y"], a["s_src"], a["s_dst"], a["stats"],
@@ -336,6 +411,10 @@ class Trainer:
                                b["dX"], Gr["W_rel"], Gr["W_root"], Gr["att"], b["wsq"],
                                prec=self.prec)))
             dH = b["dX"]
+            if self.world > 1:
+                ops.append((f"allreduce.{l}", self._allreduce_op(f"layer{l}")))
+        if self.world > 1:
+            ops.append(("allreduce_join", self._dp_join))
         if split_head:
             ops.append(("head_join", lambda: torch.cuda.current_stream().wait_stream(
                 self._head_side)))
@@ -363,6 +442,8 @@ class Trainer:
             timed(name, fn)
         if allreduce is not None:
             timed("allreduce", lambda: allreduce(self.grads))
+        if self.world > 1:
+            world = self.world               # bucketed all-reduce ran inside the plan
         if update:
             timed("sgd", lambda: hf.sgd(self.params, self.grads, self.lr, 1.0 / world))
         return self.loss
@@ -379,8 +460,9 @@ class Trainer:
         with torch.cuda.graph(g, stream=self._cap):
             for _, fn in ops:
                 fn()
-            if update and world == 1:
-                hf.sgd(self.params, self.grads, self.lr, 1.0)
+            if update and (world == 1 or self.world > 1):
+                # (bucketed in-graph all-reduce when set_dp was called: NCCL)
+                hf.sgd(self.params, self.grads, self.lr, 1.0 / max(self.world, 1))
         return g, hf.kernel_launches() - n0
 
     def capture_pipelined(self, db: DeviceBatch, db_next: DeviceBatch, feat, edge_type, side,
@@ -407,7 +489,7 @@ class Trainer:
             for _, fn in ops:
                 fn()
             if update:
-                hf.sgd(self.params, self.grads, self.lr, 1.0)
+                hf.sgd(self.params, self.grads, self.lr, 1.0 / max(self.world, 1))
             main.wait_stream(side)
         return g, hf.kernel_launches() - n0
 
@@ -415,7 +497,8 @@ class Trainer:
         """One CUDA graph per library call of the step (for per-stage device
         timing); returns [(name, graph, kernels)]."""
         out = []
-        ops = self.plan(db, feat, edge_type, split_head=False)
+        ops = [(n, f) for n, f in self.plan(db, feat, edge_type, split_head=False)
+               if not n.startswith("allreduce")]          # library calls only
         torch.cuda.synchronize()
         for name, fn in ops:
             g = torch.cuda.CUDAGraph()

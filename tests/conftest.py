@@ -18,3 +18,16 @@ def oracle_lib():
     import oracle
     oracle.build_lib()
     return oracle
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _oracle_threads():
+    """The oracle's OpenMP loops are bit-identical at any thread count
+    (tests/test_oracle_threads.py): use the host's cores for the big -m gpu
+    references."""
+    try:
+        import oracle
+        oracle.set_threads(os.cpu_count() or 1)
+    except Exception:      # noqa: BLE001  (no compiler: the oracle tests report it)
+        pass
+    yield

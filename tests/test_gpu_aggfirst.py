@@ -131,3 +131,38 @@ def test_project_aggregated_random(K, D):
     ob = oracle.project_aggregated_bwd(osh, K, D, Xa, X, None, G)
     row_rel_l2(dW.cpu().numpy().reshape(-1, D), ob["dW_rel"].reshape(-1, D), 3e-3, "dW_rel")
     row_rel_l2(dWr.cpu().numpy().reshape(-1, D), ob["dW_root"].reshape(-1, D), 3e-3, "dW_root")
+
+
+@pytest.mark.parametrize("K,D", [(128, 128), (64, 64), (128, 64)])
+@pytest.mark.parametrize("act", ["relu", "none"])
+def test_project_fuse_aggregated(K, D, act):
+    """NEXT(3) fused fusion GEMM: one tcgen05 GEMM per destination type with
+    K = (1 + R_in) K_in equals the oracle's O6 projection + O4 fusion: bit-
+    exact on TF32-representable inputs (every partial sum exact in fp32), and
+    within the TF32 row tolerance on random inputs; identical (same
+    rounding class) to the two-call path's H within the same tolerance."""
+    rng, blk, et, rs, rd, sh, csr = make_case(340 + K + D, T=3, R=7, N=6000, csc=False)
+    osh = oracle.Shape.of(blk, rs, rd)
+    a = 1 if act == "relu" else 0
+    for exact in (True, False):
+        if exact:
+            mk = lambda *shape: (rng.integers(-2, 3, shape) / 4).astype(np.float32)
+        else:
+            mk = lambda *shape: (rng.standard_normal(shape) / np.sqrt(K)).astype(np.float32)
+        Xagg = mk(sh.rows, K)
+        X = mk(sh.src_rows + 7, K)
+        gid = rng.permutation(sh.src_rows + 7)[:sh.src_rows].astype(np.int32)
+        W = mk(sh.R, K, D)
+        Wr = mk(sh.T, K, D)
+        b = mk(sh.T, D)
+        H = torch.full((sh.dst_rows, D), float("nan"), device=DEV)
+        hf().project_fuse_aggregated(sh, csr, K, D, act, t(Xagg), t(X), t(gid, torch.int32),
+                                     t(W), t(Wr), t(b), H)
+        torch.cuda.synchronize()
+        pr = oracle.project_aggregated(osh, K, D, Xagg, X, gid, W, Wr)
+        ref = oracle.fuse(osh, D, a, pr["Z"], pr["R0"], b)
+        got = H.cpu().numpy()
+        if exact:
+            assert np.array_equal(got, ref.astype(np.float32))
+        else:
+            row_rel_l2(got, ref, 2e-3, what="H fused")

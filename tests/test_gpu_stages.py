@@ -67,9 +67,11 @@ def test_aggregate_integer_inputs_bit_exact(D):
         assert np.array_equal(Z.cpu().numpy(), exp), agg
 
 
+@pytest.mark.parametrize("agg", ["gat", "gat_mul"])
 @pytest.mark.parametrize("D,H", [(128, 8), (64, 8), (128, 1), (64, 2)])
 @pytest.mark.parametrize("seed", range(3))
-def test_aggregate_fwd_gat(seed, D, H):
+def test_aggregate_fwd_gat(seed, D, H, agg):
+    """gat_mul: multiplicative logit s_src * s_dst (NEXT(2), reading C23)."""
     rng, blk, et, rs, rd, sh, csr, ch = make_case(30 + seed, D=D, H=H, hub=0.05)
     U = ch["U"]
     Y = rng.standard_normal((U, D)).astype(np.float32)
@@ -77,10 +79,10 @@ def test_aggregate_fwd_gat(seed, D, H):
     sd = (rng.standard_normal((sh.rows, H)) * 2).astype(np.float32)
     Z = torch.zeros(sh.rows, D, device=DEV)
     stats = torch.zeros(sh.rows, 2 * H, device=DEV)
-    hf().aggregate_fwd(csr, sh.rows, "gat", D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
-    ref = agg_oracle(blk, et, rs, rd, ch, "gat", D, H, Y, ss, sd)
-    A = agg_oracle(blk, et, rs, rd, ch, "gat", D, H, np.abs(Y), ss, sd)["Z"]
-    close_scaled(Z.cpu().numpy(), ref["Z"], A, what="Z gat")
+    hf().aggregate_fwd(csr, sh.rows, agg, D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
+    ref = agg_oracle(blk, et, rs, rd, ch, agg, D, H, Y, ss, sd)
+    A = agg_oracle(blk, et, rs, rd, ch, agg, D, H, np.abs(Y), ss, sd)["Z"]
+    close_scaled(Z.cpu().numpy(), ref["Z"], A, what=f"Z {agg}")
     # stats reproduce sum of alpha = 1: l = sum exp(l_e - m)
     st = stats.cpu().numpy()
     nz = ref["deg"] > 0
@@ -146,9 +148,10 @@ def test_aggregate_bwd_integer_inputs_bit_exact(D):
     assert (np.diff(ch["col_ptr"]) > 16).any()          # long columns exercised
 
 
+@pytest.mark.parametrize("agg", ["gat", "gat_mul"])
 @pytest.mark.parametrize("D,H", [(128, 8), (64, 8)])
 @pytest.mark.parametrize("seed", range(3))
-def test_aggregate_bwd_gat(seed, D, H):
+def test_aggregate_bwd_gat(seed, D, H, agg):
     rng, blk, et, rs, rd, sh, csr, ch = make_case(60 + seed, D=D, H=H, hub=0.1,
                                                      N=[800, 6000, 20000][seed])
     U = ch["U"]
@@ -158,21 +161,21 @@ def test_aggregate_bwd_gat(seed, D, H):
     G = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
     Z = torch.zeros(sh.rows, D, device=DEV)
     stats = torch.zeros(sh.rows, 2 * H, device=DEV)
-    hf().aggregate_fwd(csr, sh.rows, "gat", D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
+    hf().aggregate_fwd(csr, sh.rows, agg, D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
     dY = torch.zeros(U, D, device=DEV)
     dss = torch.zeros(U, H, device=DEV)
     dsd = torch.zeros(sh.rows, H, device=DEV)
-    ws = torch.empty(hf().aggregate_bwd_ws_bytes(sh, "gat", H) // 4 + 16, device=DEV)
-    hf().aggregate_bwd(sh, csr, "gat", D, H, 0.2, t(G), t(Y), t(ss), t(sd), stats, dY, dss, dsd,
+    ws = torch.empty(hf().aggregate_bwd_ws_bytes(sh, agg, H) // 4 + 16, device=DEV)
+    hf().aggregate_bwd(sh, csr, agg, D, H, 0.2, t(G), t(Y), t(ss), t(sd), stats, dY, dss, dsd,
                        ws)
     osh = oracle.Shape.of(blk, rs, rd)
-    ref = oracle.aggregate_bwd(osh, blk, et, ch, "gat", D, H, G, Y, ss, sd)
+    ref = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, H, G, Y, ss, sd)
     # scale: magnitude of the per-element sums (|G| |Y| bound), row-wise
-    sc_y = oracle.aggregate_bwd(osh, blk, et, ch, "gat", D, H, np.abs(G), np.abs(Y), ss, sd)
+    sc_y = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, H, np.abs(G), np.abs(Y), ss, sd)
     close_scaled(dY.cpu().numpy(), ref["dY"], sc_y["dY"], what="dY gat")
     # ds: absolute-sum scale of dpre = alpha (dalpha - za) terms
-    fw = oracle.aggregate_fwd(osh, blk, et, ch, "gat", D, H, Y, ss, sd)
-    scale_s, scale_d = gat_ds_scales(sh, ch, fw, G, Y, D, H)
+    fw = oracle.aggregate_fwd(osh, blk, et, ch, agg, D, H, Y, ss, sd)
+    scale_s, scale_d = gat_ds_scales(sh, ch, fw, G, Y, D, H, agg, ss, sd)
     close_scaled(dss.cpu().numpy(), ref["ds_src"], scale_s, what="ds_src")
     close_scaled(dsd.cpu().numpy(), ref["ds_dst"], scale_d, what="ds_dst")
     # score chain folded into the CSC pass (hifuse_aggregate_bwd_scored):
@@ -181,7 +184,7 @@ def test_aggregate_bwd_gat(seed, D, H):
     dY2 = torch.zeros_like(dY)
     dss2 = torch.zeros_like(dss)
     dsd2 = torch.zeros_like(dsd)
-    hf().aggregate_bwd_scored(sh, csr, "gat", D, H, 0.2, t(G), t(Y), t(ss), t(sd), stats, att,
+    hf().aggregate_bwd_scored(sh, csr, agg, D, H, 0.2, t(G), t(Y), t(ss), t(sd), stats, att,
                               dY2, dss2, dsd2, ws)
     torch.cuda.synchronize()
     assert torch.equal(dss2, dss) and torch.equal(dsd2, dsd)
@@ -191,7 +194,7 @@ def test_aggregate_bwd_gat(seed, D, H):
     torch.testing.assert_close(dY2, want, rtol=1e-6, atol=1e-6)
 
 
-def gat_ds_scales(sh, ch, fw, G, Y, D, H):
+def gat_ds_scales(sh, ch, fw, G, Y, D, H, agg="gat", ss=None, sd=None):
     """Absolute-sum scales of the GAT score gradients: per
     edge and head, dpre = alpha (dalpha - sum_row alpha dalpha) with dalpha =
     <G_row, Y_col>; the scale sums alpha (|dalpha|_abs + sum alpha |dalpha|_abs)
@@ -207,10 +210,13 @@ def gat_ds_scales(sh, ch, fw, G, Y, D, H):
     za = np.zeros((sh.rows, H))
     np.add.at(za, rows, a * dabs)
     term = a * (dabs + za[rows])
+    # multiplicative logit: ds_src = sum dl s_dst, ds_dst = sum dl s_src
+    tsrc = term * np.abs(sd[rows]) if agg == "gat_mul" else term
+    tdst = term * np.abs(ss[u]) if agg == "gat_mul" else term
     scale_d = np.zeros((sh.rows, H))
-    np.add.at(scale_d, rows, term)
+    np.add.at(scale_d, rows, tdst)
     scale_s = np.zeros((U, H))
-    np.add.at(scale_s, u, term)
+    np.add.at(scale_s, u, tsrc)
     return scale_s, scale_d
 
 
@@ -501,3 +507,101 @@ def test_aggregate_bwd_gat_xrel(seed, D, H):
     np.add.at(scale_s, u, term)
     close_scaled(dss.cpu().numpy(), ref["ds_src"], scale_s, what="ds_src xrel")
     close_scaled(dsd.cpu().numpy(), ref["ds_dst"], scale_d, what="ds_dst xrel")
+
+
+@pytest.mark.parametrize("agg,H", [("mean", 1), ("sum", 1), ("gat", 8), ("gat_mul", 8)])
+def test_aggregate_bwd_rows_matches_type_major(agg, H):
+    """hifuse_aggregate_bwd_rows (per-merged-row gradient, HAN fusion) fed
+    with G_t[i] on every row (r, i) computes exactly what hifuse_aggregate_bwd
+    computes from the type-major G (bit-identical), and matches the oracle's
+    g_rows path for a genuinely per-row gradient."""
+    from test_oracle_backward import gmap
+    D = 128
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(95, D=D, H=H, N=9000, hub=0.1)
+    U = ch["U"]
+    Y = rng.standard_normal((U, D)).astype(np.float32)
+    ss = rng.standard_normal((U, H)).astype(np.float32)
+    sd = rng.standard_normal((sh.rows, H)).astype(np.float32)
+    G = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    gat = agg.startswith("gat")
+    stats = torch.zeros(sh.rows, 2 * H, device=DEV) if gat else None
+    if gat:
+        Z = torch.zeros(sh.rows, D, device=DEV)
+        hf().aggregate_fwd(csr, sh.rows, agg, D, H, 0.2, t(Y), t(ss), t(sd), Z, stats)
+    ws = torch.empty(hf().aggregate_bwd_ws_bytes(sh, agg, H) // 4 + 16, device=DEV)
+    outs = []
+    for rows_mode in (False, True):
+        dY = torch.zeros(max(U, 1), D, device=DEV)
+        dss = torch.zeros(max(U, 1), H, device=DEV) if gat else None
+        dsd = torch.zeros(sh.rows, H, device=DEV) if gat else None
+        args = (t(Y), t(ss) if gat else None, t(sd) if gat else None, stats)
+        if rows_mode:
+            hf().aggregate_bwd_rows(sh, csr, agg, D, H, 0.2, t(gmap(sh, ch, G).astype(np.float32)),
+                                    *args, None, dY, dss, dsd, ws)
+        else:
+            hf().aggregate_bwd(sh, csr, agg, D, H, 0.2, t(G), *args, dY, dss, dsd, ws)
+        outs.append([x for x in (dY, dss, dsd) if x is not None])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    # a per-row gradient that differs between the relations of a type
+    dZ = rng.standard_normal((sh.rows, D)).astype(np.float32)
+    dY = torch.zeros(max(U, 1), D, device=DEV)
+    dss = torch.zeros(max(U, 1), H, device=DEV) if gat else None
+    dsd = torch.zeros(sh.rows, H, device=DEV) if gat else None
+    hf().aggregate_bwd_rows(sh, csr, agg, D, H, 0.2, t(dZ), t(Y), t(ss) if gat else None,
+                            t(sd) if gat else None, stats, None, dY, dss, dsd, ws)
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, H, dZ, Y, ss, sd, g_rows=True)
+    sc = oracle.aggregate_bwd(osh, blk, et, ch, agg, D, H, np.abs(dZ), np.abs(Y), ss, sd,
+                              g_rows=True)
+    close_scaled(dY.cpu().numpy()[:U], ref["dY"], sc["dY"], what=f"dY rows {agg}")
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("act", ["relu", "none"])
+def test_semantic_fuse_att(D, act):
+    """HAN semantic-attention fusion (NEXT(2), reading C22), stage-isolated:
+    beta and H against the oracle's O4' + O4 on the GPU's own Z; the backward
+    (G, per-row dZ, dbias, dWs, dbs, dq) against O5a + O5a'."""
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(97, D=D, N=5000, T=3, R=7)
+    osh = oracle.Shape.of(blk, rs, rd)
+    Z = rng.standard_normal((sh.rows, D)).astype(np.float32)
+    R0 = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    bias = (rng.standard_normal((sh.T, D)) * 0.1).astype(np.float32)
+    Ws = (rng.standard_normal((D, D)) / np.sqrt(D)).astype(np.float32)
+    bs = (rng.standard_normal(D) * 0.1).astype(np.float32)
+    q = (rng.standard_normal(D) / np.sqrt(D)).astype(np.float32)
+    beta = torch.zeros(sh.R, device=DEV)
+    w = torch.zeros(sh.R, device=DEV)
+    Hd = torch.zeros(sh.dst_rows, D, device=DEV)
+    ws = torch.empty(hf().sem_att_ws_bytes(sh, D, D) // 4 + 64, device=DEV)
+    hf().semantic_fuse_att(sh, D, D, act, t(Z), t(R0), t(bias), t(Ws), t(bs), t(q), beta, w, Hd,
+                           ws)
+    w_ref, beta_ref = oracle.sem_att(osh, D, Z, Ws, bs, q)
+    np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(beta.cpu().numpy(), beta_ref, rtol=1e-5, atol=1e-7)
+    a = 1 if act == "relu" else 0
+    H_ref = oracle.fuse(osh, D, a, Z, R0, bias, beta=beta_ref)
+    A = oracle.fuse(osh, D, 0, np.abs(Z), np.abs(R0), np.abs(bias), beta=beta_ref)
+    close_scaled(Hd.cpu().numpy(), H_ref, A, rtol=2e-5, what="H han")
+    # backward
+    dH = rng.standard_normal((sh.dst_rows, D)).astype(np.float32)
+    G = torch.zeros(sh.dst_rows, D, device=DEV)
+    dZ = torch.zeros(sh.rows, D, device=DEV)
+    dbias = torch.zeros(sh.T, D, device=DEV)
+    dWs = torch.zeros(D, D, device=DEV)
+    dbs = torch.zeros(D, device=DEV)
+    dq = torch.zeros(D, device=DEV)
+    hf().semantic_fuse_att_bwd(sh, D, D, act, t(dH), Hd, t(Z), t(Ws), t(bs), t(q), beta, G, dZ,
+                               dbias, dWs, dbs, dq, ws)
+    G_ref, db_ref = oracle.fuse_bwd(osh, D, a, dH, Hd.cpu().numpy())
+    assert np.array_equal(G.cpu().numpy(), G_ref.astype(np.float32))
+    sem = oracle.sem_att_bwd(osh, D, Z, Ws, bs, q, beta.cpu().numpy().astype(np.float64), G_ref)
+
+    def rl2(g, r):
+        return np.linalg.norm(np.asarray(g, np.float64) - r) / max(np.linalg.norm(r), 1e-30)
+    assert rl2(dZ.cpu().numpy(), sem["dZ"]) < 1e-5
+    assert rl2(dbias.cpu().numpy(), db_ref) < 1e-6
+    for name, got, ref in (("dWs", dWs, sem["dWs"]), ("dbs", dbs, sem["dbs"]),
+                           ("dq", dq, sem["dq"])):
+        assert rl2(got.cpu().numpy(), ref) < 5e-5, name

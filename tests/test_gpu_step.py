@@ -21,6 +21,11 @@ def setup(key):
         if key.endswith("_xrel"):        # RGAT with the across-relation softmax (NEXT(2))
             import dataclasses
             cfg = dataclasses.replace(CONFIGS[key[:-5]], agg="gat_xrel", key=key)
+        elif key.endswith("_mul"):       # RGAT with multiplicative attention (NEXT(2))
+            import dataclasses
+            cfg = dataclasses.replace(CONFIGS[key[:-4]], agg="gat_mul", key=key)
+        elif key.endswith("_han"):       # HAN semantic-attention fusion (NEXT(2))
+            cfg = CONFIGS[key[:-4]]
         else:
             cfg = CONFIGS[key]
         g = generate_graph(cfg)
@@ -38,7 +43,8 @@ def rel_l2(a, b):
 @pytest.mark.parametrize("prec,order", [("fp32", "project_first"), ("tf32", "project_first"),
                                         ("tf32", "agg_first")])
 @pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag", "imdb_xrel",
-                                 "freebase_xrel"])
+                                 "freebase_xrel", "imdb_mul", "freebase_mul", "imdb_han",
+                                 "dblp_han", "freebase_han"])
 def test_step_matches_oracle(key, prec, order):
     """agg_first (RGCN input layer aggregates raw features, then projects) is
     checked against the same project-first oracle model: equal by linearity."""
@@ -47,10 +53,11 @@ def test_step_matches_oracle(key, prec, order):
     mb = make_batch(cfg, g, 0)
     rs = np.array([r.src for r in cfg.rels], np.int32)
     rd = np.array([r.dst for r in cfg.rels], np.int32)
-    params = make_params(cfg)
+    fusion = "han" if key.endswith("_han") else "sum"
+    params = make_params(cfg, fusion=fusion)
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0, prec=prec,
-                 order=order)
+                 order=order, fusion=fusion)
     if order == "agg_first" and not tr.agg_first:
         pytest.skip("aggregate-first applies to RGCN only")
     tr.load_params(params)
@@ -76,8 +83,8 @@ def test_step_matches_oracle(key, prec, order):
     assert abs(float(loss.item()) - fw["loss"]) <= ltol * max(1.0, abs(fw["loss"]))
     checks = [("Wc", gr["Wc"]), ("bc", gr["bc"])]
     for l in range(cfg.num_layers):
-        for k in ("W_rel", "W_root", "bias", "att"):
-            if gr["layers"][l][k] is not None and f"{l}.{k}" in tr.Gd:
+        for k in ("W_rel", "W_root", "bias", "att", "sem_W", "sem_b", "sem_q"):
+            if gr["layers"][l].get(k) is not None and f"{l}.{k}" in tr.Gd:
                 checks.append((f"{l}.{k}", gr["layers"][l][k]))
     for name, ref in checks:
         err = rel_l2(tr.Gd[name].cpu().numpy(), ref)
