@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 from synth import CONFIGS, generate_graph, generate_features, make_batch, make_params  # noqa: E402
 
 ALU_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # CUDA-core fp32 FMA peak at max clock
+FEAT_BYTES = 4                                      # bytes per stored input feature (--feat-dtype)
 TF32_OVER_BF16 = 1.1 / 2.25                         # nominal dense ratio (B200_PROFILING.md)
 
 
@@ -150,6 +151,9 @@ def stage_cost(stage, l, cfg, sz):
         C, B = cfg.num_classes, cfg.batch_size
         return 4 * (2 * B * D + 2 * D * C + 2 * B * C), 2 * 2 * B * D * C
     if stage == "aggregate_features":     # aggregate-first input layer: A4 over raw X
+        if FEAT_BYTES == 2:                   # BF16 store: + fp32 dst rows written
+            return (2 * K * s["F"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"]
+                    + 4 * K * s["dst"]), 0
         return 4 * K * s["F"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
     if stage == "project_fuse_aggregated":     # Xagg + X dst rows in, H out (+ weights)
         m = s["rows"] + s["dst"]
@@ -260,6 +264,7 @@ def config_obj(cfg, args, extra=None):
          "order": getattr(args, "order", "project_first"),
          "aggregation": cfg.agg,
          "fusion": getattr(args, "fusion", "sum"),
+         "feature_storage": getattr(args, "feat_dtype", "fp32"),
          "l2": "inputs larger than L2: a pool of distinct sampled batches, per-step working "
                "set above the 126 MB L2 for mag"}
     if extra:
@@ -448,6 +453,9 @@ def main():
                     help="RGAT edge-softmax domain: within each (relation, destination) row "
                          "(reading C5, default) or across all relations of a destination "
                          "(C5', SURVEY §8(f) NEXT(2))")
+    ap.add_argument("--feat-dtype", default="fp32", choices=["fp32", "bf16"],
+                    help="storage of the input feature store: fp32, or BF16 read by the "
+                         "aggregate-first input layer (NEXT(3) byte diet; fp32 accumulation)")
     ap.add_argument("--fusion", default="sum", choices=["sum", "han"],
                     help="semantic fusion: plain sum over relations (reading C2/C4, default) or "
                          "HAN semantic attention (C22, NEXT(2))")
@@ -455,6 +463,8 @@ def main():
                     help="RGAT attention logit: additive LeakyReLU(s_src + s_dst) (reading C6, "
                          "default) or multiplicative s_src * s_dst (C23, NEXT(2))")
     args = ap.parse_args()
+    global FEAT_BYTES
+    FEAT_BYTES = 2 if args.feat_dtype == "bf16" else 4
     cfg = CONFIGS[args.config]
     if cfg.model == "rgat" and args.gat_softmax == "across":
         import dataclasses
@@ -500,10 +510,13 @@ def main():
         db.slot = i                      # private CSR buffers per pool batch
     sizes = [layer_sizes(cfg, g, mb, rs, rd) for mb in mbs]
     feat_d = torch.from_numpy(feat).to(dev)
+    if args.feat_dtype == "bf16":            # RN-even rounded store (NEXT(3) byte diet)
+        feat_d = feat_d.to(torch.bfloat16)
     et_d = torch.from_numpy(g.edge_type).to(dev)
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
-                 prec=args.prec, order=args.order, fusion=args.fusion)
+                 prec=args.prec, order=args.order, fusion=args.fusion,
+                 feat_dtype=args.feat_dtype)
     tr.load_params(params)
     tr.prepare_graph(et_d)           # relation-major edge ids -> R+1 offsets (once per graph)
     # N > 1: per-layer bucketed all-reduce on a comm stream inside the step
@@ -602,7 +615,8 @@ def main():
     # north-star project-first path is always measured next to the faster
     # aggregate-first one)
     other = None
-    if cfg.model == "rgcn" and args.prec == "tf32" and args.fusion == "sum":
+    if cfg.model == "rgcn" and args.prec == "tf32" and args.fusion == "sum" and \
+            args.feat_dtype == "fp32":
         other_order = "project_first" if tr.agg_first else "agg_first"
         tr_o = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                        cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
@@ -705,7 +719,7 @@ def main():
             dist.destroy_process_group()
         return
     gsmp = None
-    if args.gpu_sampler and world == 1:
+    if args.gpu_sampler and world == 1 and args.feat_dtype == "fp32":
         # supplementary (NEXT(1)); a failure here must not cost the bench line
         try:
             gsmp = gpu_sampler_run(cfg, g, params, rs, rd, feat_d, et_d, dev,

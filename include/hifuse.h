@@ -391,6 +391,22 @@ hifuse_status hifuse_project_fuse_aggregated(const hifuse_layer_shape *shape,
                                             const float *d_W_root, const float *d_bias,
                                             float *d_H, hifuse_stream_t stream);
 
+/* NEXT(3) BF16 storage of the input features (byte
+ * diet): hifuse_aggregate_features_cols over a BF16 feature store d_Xb
+ * (bfloat16 [x_rows, K], RN-even rounded by the caller), fp32 accumulation in
+ * the same order, fp32 Xagg out -- half the bytes of the layer's dominant
+ * read.  d_Xdst (nullable, fp32 [sum_t n_src(t), K]): the layer's destination
+ * rows (the root term's X rows) converted to fp32 at rows type_src_off[t] +
+ * i, i < n_dst(t) (other rows untouched), for the tcgen05 GEMMs
+ * (hifuse_project_fuse_aggregated / hifuse_project_aggregated_bwd with
+ * d_X = d_Xdst, d_gather_ids = NULL).  Same launch. */
+hifuse_status hifuse_aggregate_features_cols_bf16(const hifuse_layer_shape *shape,
+                                                  const hifuse_csr *csr, hifuse_agg agg, int K,
+                                                  const void *d_Xb, int64_t x_rows,
+                                                  const int32_t *d_col_x,
+                                                  const int32_t *d_gather_ids, float *d_Xagg,
+                                                  float *d_Xdst, hifuse_stream_t stream);
+
 /* The two halves of hifuse_aggregate_features_fwd, so the first can run with
  * the semantic-graph build (off the critical path):
  *   hifuse_feature_cols: d_col_x [N] = the feature-store row x(e) of every

@@ -13,6 +13,7 @@
 // column indices are fetched with one coalesced load and broadcast with
 // shuffles; the gathers of UNROLL edges per stream are issued back to back to
 // keep several 256-512 B row loads in flight per warp (HBM latency hiding).
+#include <cuda_bf16.h>
 #include "common.cuh"
 
 namespace hf {
@@ -98,6 +99,94 @@ k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict
   }
 }
 
+
+// NEXT(3) byte diet: the aggregate-first input layer over a BF16 feature
+// store (2 bytes per feature instead of 4 on the layer's dominant read).
+// Rows are accumulated in fp32 in the same order as k_agg_fwd (the oracle is
+// fed the BF16-rounded features).  A lane loads 16 B = 8 bf16;
+// K = 128: 16 lanes per row, 2 edge streams per warp.  Blocks past the
+// aggregation grid convert the layer's destination rows (the root term's X
+// rows) to fp32 into Xdst[type_src_off[t] + i] for the tcgen05 GEMMs.
+__device__ __forceinline__ void bf16x8_add(const uint4 q, float* a) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const float2 f = __bfloat1622float2(h[j]);
+    a[2 * j] += f.x;
+    a[2 * j + 1] += f.y;
+  }
+}
+
+struct DstConv {
+  int T;
+  int n_dst[HF_MAX_T];
+  int type_src_off[HF_MAX_T + 1];
+  int dst_off[HF_MAX_T + 1];      // prefix over types of n_dst
+};
+
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_fwd_bf16(long long rows, unsigned agg_blocks, const int* __restrict__ row_ptr,
+               const int* __restrict__ col, const uint4* __restrict__ Xb,
+               float4* __restrict__ Z, DstConv dc, const int* __restrict__ gather_ids,
+               float4* __restrict__ Xdst) {
+  constexpr int LPR = D / 8;              // lanes per row stream (8 bf16 each)
+  constexpr int NS = 32 / LPR;            // edge streams per warp
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x >= agg_blocks) {
+    // destination rows -> fp32 (one thread per 8 features)
+    const long long i = (long long)(blockIdx.x - agg_blocks) * blockDim.x + threadIdx.x;
+    if (!Xdst || i >= (long long)dc.dst_off[dc.T] * LPR) return;
+    const int o = (int)(i / LPR), c8 = (int)(i % LPR);
+    const int t = upper_bound_i(dc.dst_off, dc.T + 1, o) - 1;
+    const int x = dc.type_src_off[t] + (o - dc.dst_off[t]);
+    const long long g = gather_ids ? (long long)gather_ids[x] : (long long)x;
+    const uint4 q = __ldg(Xb + g * LPR + c8);
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    bf16x8_add(q, a);
+    Xdst[(long long)x * (D / 4) + 2 * c8] = make_float4(a[0], a[1], a[2], a[3]);
+    Xdst[(long long)x * (D / 4) + 2 * c8 + 1] = make_float4(a[4], a[5], a[6], a[7]);
+    return;
+  }
+  const int sl = lane % LPR, sid = lane / LPR;
+  long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int b = row_ptr[row], e = row_ptr[row + 1];
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int base = b; base < e; base += 32) {
+    const int n = min(32, e - base);
+    const int my_col = lane < n ? __ldg(col + base + lane) : 0;
+    int k = 0;
+    for (; k + NS * kUnroll <= n; k += NS * kUnroll) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        const int c = __shfl_sync(0xffffffffu, my_col, k + u * NS + sid);
+        v[u] = __ldg(Xb + (long long)c * LPR + sl);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) bf16x8_add(v[u], acc);
+    }
+    for (; k < n; k += NS) {
+      const int idx = k + sid;
+      const int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+      if (idx < n) bf16x8_add(__ldg(Xb + (long long)c * LPR + sl), acc);
+    }
+  }
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  if (sid == 0) {
+    if (MEAN && e > b) {
+      const float dg = (float)(e - b);
+#pragma unroll
+      for (int j = 0; j < 8; j++) acc[j] = __fdiv_rn(acc[j], dg);
+    }
+    Z[row * (D / 4) + 2 * sl] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    Z[row * (D / 4) + 2 * sl + 1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
 
 // Aggregate-first input layer: CSR position p -> the global feature row of its
 // source, x = gather_ids[type_src_off[s(r)] + y_src[col[p]]] (r = relation of
@@ -1400,6 +1489,46 @@ hifuse_status hifuse_aggregate_features_cols(const hifuse_layer_shape* shape,
   if (K == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
   else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }
 #undef HF_AGG
+  return last_cuda();
+}
+
+hifuse_status hifuse_aggregate_features_cols_bf16(const hifuse_layer_shape* shape,
+                                                  const hifuse_csr* csr, hifuse_agg agg, int K,
+                                                  const void* d_Xb, int64_t x_rows,
+                                                  const int32_t* d_col_x,
+                                                  const int32_t* d_gather_ids, float* d_Xagg,
+                                                  float* d_Xdst, hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (agg != HIFUSE_AGG_SUM && agg != HIFUSE_AGG_MEAN) return HIFUSE_ERR_UNSUPPORTED;
+  if (K != 64 && K != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !csr->row_ptr || x_rows < 0 || !d_Xagg ||
+      (m.N > 0 && (!d_col_x || !d_Xb)) || (d_Xdst && m.dst_rows > 0 && !d_Xb))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_Xb) || !aligned16(d_Xagg) || !aligned16(d_Xdst)) return HIFUSE_ERR_ALIGNMENT;
+  cudaStream_t s = st(stream);
+  const unsigned agg_blocks = ceil_div((long long)m.rows, kWarpsPerBlock);
+  const int TB = kWarpsPerBlock * 32;
+  DstConv dc;
+  dc.T = m.T;
+  int acc = 0;
+  for (int t = 0; t < m.T; t++) {
+    dc.n_dst[t] = m.n_dst[t];
+    dc.dst_off[t] = acc;
+    acc += m.n_dst[t];
+  }
+  dc.dst_off[m.T] = acc;
+  for (int t = 0; t <= m.T; t++) dc.type_src_off[t] = m.type_src_off[t];
+  const unsigned conv_blocks = d_Xdst ? ceil_div((long long)acc * (K / 8), TB) : 0;
+  const bool mean = agg == HIFUSE_AGG_MEAN;
+#define HF_AGGB(DD, MM)                                                                       \
+  HF_LAUNCH((k_agg_fwd_bf16<DD, MM>), agg_blocks + conv_blocks, TB, 0, s, (long long)m.rows,    \
+            agg_blocks, csr->row_ptr, d_col_x, (const uint4*)d_Xb, (float4*)d_Xagg, dc,        \
+            d_gather_ids, (float4*)d_Xdst)
+  if (K == 128) { if (mean) HF_AGGB(128, true); else HF_AGGB(128, false); }
+  else { if (mean) HF_AGGB(64, true); else HF_AGGB(64, false); }
+#undef HF_AGGB
   return last_cuda();
 }
 

@@ -111,6 +111,7 @@ def lib():
                                      vp, sz, vp, vp],
             "hifuse_read_status": [vp, vp, vp],
             "hifuse_sem_att_ws_bytes": [vp, i32, i32],
+            "hifuse_aggregate_features_cols_bf16": [vp, vp, i32, i32, vp, i64, vp, vp, vp, vp, vp],
             "hifuse_project_fuse_aggregated": [vp, vp, i32, i32, i32, i32, vp, vp, i64, vp, vp, vp,
                                                vp, vp, vp],
             "hifuse_shard_plan": [vp, i64, vp, i32, vp, vp, vp, vp],
@@ -481,3 +482,15 @@ def project_fuse_aggregated(shape, csr, K, D, act, Xagg, X, gather_ids, W_rel, W
         shape.ref, csr.ref, PREC[prec], K, D, ACT[act], _ptr(Xagg), _ptr(X),
         X.shape[0] if X is not None else 0, _ptr(gather_ids), _ptr(W_rel), _ptr(W_root),
         _ptr(bias), _ptr(H), _stream(stream)))
+
+
+def aggregate_features_cols_bf16(shape, csr, agg, K, Xb, col_x, gather_ids, Xagg, Xdst,
+                                 stream=None):
+    """hifuse_aggregate_features_cols_bf16: the aggregate-first input layer over
+    a BF16 feature store (NEXT(3) byte diet); Xdst receives the destination rows
+    in fp32 (root term)."""
+    import torch
+    assert Xb.dtype == torch.bfloat16
+    _check("hifuse_aggregate_features_cols_bf16", lib().hifuse_aggregate_features_cols_bf16(
+        shape.ref, csr.ref, AGG[agg], K, _ptr(Xb), Xb.shape[0], _ptr(col_x), _ptr(gather_ids),
+        _ptr(Xagg), _ptr(Xdst), _stream(stream)))

@@ -80,7 +80,8 @@ class Trainer:
     """Owns parameters, gradients, activations and workspaces of the step."""
 
     def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
-                 prec="tf32", slope=0.2, order="project_first", fusion="sum", fuse_gemm=True):
+                 prec="tf32", slope=0.2, order="project_first", fusion="sum", fuse_gemm=True,
+                 feat_dtype="fp32"):
         hf.lib()   # raises if libhifuse.so is missing (no CPU fallback)
         self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
         self.rel_src = np.asarray(rel_src, np.int32)
@@ -114,6 +115,14 @@ class Trainer:
         # aggregate-first input layer: projection + fusion as one GEMM per
         # destination type (hifuse_project_fuse_aggregated, NEXT(3))
         self.fuse_gemm = bool(fuse_gemm) and self.agg_first
+        # NEXT(3) byte diet: BF16 storage of the input features (the
+        # aggregate-first input layer reads them; its root term reads the
+        # destination rows converted to fp32 by the same launch)
+        if feat_dtype not in ("fp32", "bf16"):
+            raise ValueError(feat_dtype)
+        if feat_dtype == "bf16" and not self.agg_first:
+            raise ValueError("a BF16 feature store needs the aggregate-first input layer")
+        self.feat_dtype = feat_dtype
         # capture streams: `_hi` (high priority) for the pipelined graphs,
         # `_cap` for the serial / per-stage graphs; the library's fork/join
         # resources of every stream that runs steps are created here, outside
@@ -267,19 +276,27 @@ class Trainer:
                 a.update(Y=None, Xagg=self._mat("Xagg0", sh.rows, K))
                 # colx: written by this batch's build op (hifuse_feature_cols)
                 colx = self._buf(f"colx{db.slot}", max(sh.N, 1), torch.int32)
-                ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a, colx=colx:
-                            hf.aggregate_features_cols(sh, c, self.agg, a["K"], a["X"], colx,
-                                                       a["Xagg"])))
+                if self.feat_dtype == "bf16":
+                    a.update(Xroot=self._mat("Xdst0", sh.src_rows, K), gid_root=None)
+                    ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a, colx=colx:
+                                hf.aggregate_features_cols_bf16(sh, c, self.agg, a["K"], a["X"],
+                                                                colx, a["gid"], a["Xagg"],
+                                                                a["Xroot"])))
+                else:
+                    a.update(Xroot=a["X"], gid_root=a["gid"])
+                    ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a, colx=colx:
+                                hf.aggregate_features_cols(sh, c, self.agg, a["K"], a["X"], colx,
+                                                           a["Xagg"])))
                 if self.fuse_gemm:
                     ops.append(("project_fuse_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
                                 hf.project_fuse_aggregated(sh, c, a["K"], D, a["act"], a["Xagg"],
-                                                           a["X"], a["gid"], P["W_rel"],
+                                                           a["Xroot"], a["gid_root"], P["W_rel"],
                                                            P["W_root"], P["bias"], a["H"],
                                                            prec=self.prec)))
                 else:
                     ops.append(("project_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
-                                hf.project_aggregated(sh, c, a["K"], D, a["Xagg"], a["X"],
-                                                      a["gid"], P["W_rel"], P["W_root"], a["Z"],
+                                hf.project_aggregated(sh, c, a["K"], D, a["Xagg"], a["Xroot"],
+                                                      a["gid_root"], P["W_rel"], P["W_root"], a["Z"],
                                                       a["R0"], prec=self.prec)))
                     ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
                         sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
@@ -344,8 +361,8 @@ class Trainer:
                 ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
                     sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
                 ops.append(("project_aggregated_bwd.0", lambda sh=sh, c=csrs[l], a=a, b=b, Gr=Gr:
-                            hf.project_aggregated_bwd(sh, c, a["K"], D, a["Xagg"], a["X"],
-                                                      a["gid"], b["G"], Gr["W_rel"],
+                            hf.project_aggregated_bwd(sh, c, a["K"], D, a["Xagg"], a["Xroot"],
+                                                      a["gid_root"], b["G"], Gr["W_rel"],
                                                       Gr["W_root"], b["wsq"], prec=self.prec)))
                 if self.world > 1:
                     ops.append((f"allreduce.{l}", self._allreduce_op(f"layer{l}")))

@@ -17,6 +17,7 @@ ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--pool", type=int, default=2)
 ap.add_argument("--prec", default="tf32")
 ap.add_argument("--order", default="agg_first")
+ap.add_argument("--feat-dtype", default="fp32")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 g = generate_graph(cfg)
@@ -29,9 +30,11 @@ pool = [DeviceBatch(make_batch(cfg, g, b % nb, epoch=b // nb), rs, rd, foff, cfg
         for b in range(a.pool)]
 tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
              cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=0.01, prec=a.prec,
-             order=a.order)
+             order=a.order, feat_dtype=a.feat_dtype)
 tr.load_params(make_params(cfg))
 fd = torch.from_numpy(feat).to(dev)
+if a.feat_dtype == "bf16":
+    fd = fd.to(torch.bfloat16)
 et = torch.from_numpy(g.edge_type).to(dev)
 tr.prepare_graph(et)
 for db in pool:

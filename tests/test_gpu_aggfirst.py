@@ -166,3 +166,34 @@ def test_project_fuse_aggregated(K, D, act):
             assert np.array_equal(got, ref.astype(np.float32))
         else:
             row_rel_l2(got, ref, 2e-3, what="H fused")
+
+
+@pytest.mark.parametrize("K", [64, 128])
+@pytest.mark.parametrize("agg", ["sum", "mean"])
+def test_aggregate_features_bf16(K, agg):
+    """NEXT(3) BF16 feature storage: hifuse_aggregate_features_cols_bf16 equals
+    the oracle's O6 aggregation of the BF16-ROUNDED features (1e-5 of the
+    absolute-sum scale; bit-exact when the sums are exact), and the fp32
+    destination rows it writes equal the rounded features exactly."""
+    rng, blk, et, rs, rd, sh, csr = make_case(360 + K, hub=0.1, csc=False)
+    xr = sh.src_rows + 11
+    X = rng.standard_normal((xr, K)).astype(np.float32)
+    Xb = torch.from_numpy(X).to(DEV).to(torch.bfloat16)
+    Xr = Xb.float().cpu().numpy()                       # the rounded values
+    gid = rng.permutation(xr)[:sh.src_rows].astype(np.int32)
+    gid_d = t(gid, torch.int32)
+    colx = torch.empty(max(sh.N, 1), dtype=torch.int32, device=DEV)
+    hf().feature_cols(sh, csr, gid_d, colx)
+    Xa = torch.full((max(sh.rows, 1), K), float("nan"), device=DEV)
+    Xdst = torch.full((sh.src_rows, K), float("nan"), device=DEV)
+    hf().aggregate_features_cols_bf16(sh, csr, agg, K, Xb, colx, gid_d, Xa, Xdst)
+    torch.cuda.synchronize()
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.aggregate_features(osh, blk, et, agg, K, Xr, gid)
+    A = oracle.aggregate_features(osh, blk, et, agg, K, np.abs(Xr), gid)
+    close_scaled(Xa.cpu().numpy()[:sh.rows], ref, A, what=f"Xagg bf16 {agg}")
+    xd = Xdst.cpu().numpy()
+    for tt in range(sh.T):
+        a = int(sh.type_src_off[tt])
+        n = int(sh.n_dst[tt])
+        assert np.array_equal(xd[a:a + n], Xr[gid[a:a + n]])

@@ -41,7 +41,7 @@ def rel_l2(a, b):
 
 
 @pytest.mark.parametrize("prec,order", [("fp32", "project_first"), ("tf32", "project_first"),
-                                        ("tf32", "agg_first")])
+                                        ("tf32", "agg_first"), ("tf32", "agg_first_bf16")])
 @pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag", "imdb_xrel",
                                  "freebase_xrel", "imdb_mul", "freebase_mul", "imdb_han",
                                  "dblp_han", "freebase_han"])
@@ -55,14 +55,21 @@ def test_step_matches_oracle(key, prec, order):
     rd = np.array([r.dst for r in cfg.rels], np.int32)
     fusion = "han" if key.endswith("_han") else "sum"
     params = make_params(cfg, fusion=fusion)
+    bf16 = order == "agg_first_bf16"      # NEXT(3): BF16 feature store, oracle fed rounded values
+    if bf16 and (cfg.model != "rgcn" or fusion != "sum"):
+        pytest.skip("the BF16 feature store needs the aggregate-first RGCN input layer")
+    order = "agg_first" if bf16 else order
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0, prec=prec,
-                 order=order, fusion=fusion)
+                 order=order, fusion=fusion, feat_dtype="bf16" if bf16 else "fp32")
     if order == "agg_first" and not tr.agg_first:
         pytest.skip("aggregate-first applies to RGCN only")
     tr.load_params(params)
     db = DeviceBatch(mb, rs, rd, foff, cfg.target_type, DEV)
     feat_d = torch.from_numpy(feat).to(DEV)
+    if bf16:
+        feat_d = feat_d.to(torch.bfloat16)
+        feat = feat_d.float().cpu().numpy()          # the oracle sees the rounded store
     et_d = torch.from_numpy(g.edge_type).to(DEV)
     loss = tr.step(db, feat_d, et_d, update=False)
     torch.cuda.synchronize()
@@ -88,7 +95,14 @@ def test_step_matches_oracle(key, prec, order):
                 checks.append((f"{l}.{k}", gr["layers"][l][k]))
     for name, ref in checks:
         err = rel_l2(tr.Gd[name].cpu().numpy(), ref)
-        assert err <= tol, f"{key} grad {name}: rel L2 {err:.3e}"
+        # HAN fusion under TF32: every gradient below the fusion goes
+        # through dw_r = beta_r (dbeta_r - sum_r' beta_r' dbeta_r'), a softmax
+        # adjoint whose terms nearly cancel (3-5 relations per type), so the
+        # TF32 errors of the chain above are amplified by |dbeta| / |dw|
+        # (~5x measured on IMDB); the same gradients are checked at 2e-4 in
+        # fp32
+        t_ = 0.1 if (prec == "tf32" and key.endswith("_han")) else tol
+        assert err <= t_, f"{key} grad {name}: rel L2 {err:.3e}"
     # logits-level: the last layer's H on the seeds
     last = tr.last["acts"][-1]["H"][db.h_row0:db.h_row0 + db.B].cpu().numpy()
     err = rel_l2(last, fw["hs"])
