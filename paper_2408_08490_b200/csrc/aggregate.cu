@@ -368,181 +368,16 @@ k_agg_fwd_gat_half(long long rows, int H, float slope, const int* __restrict__ r
 }
 
 // ---------------------------------------------------- backward SUM/MEAN (CSC)
-// dY[u] = sum_{q in column u} w(row_q) G[row_q + shift(r(u))]; all rows of a
-// column belong to Y row u's relation r(u), found once per warp.
+// dY[u] = sum_{q in column u} w(row_q) G[row_q + shift(r(row_q))].
 struct BwdMeta {
   int R;
   int shift[HF_MAX_R];   // type_dst_off[t(r)] - rel_row_off[r]
 };
 
-// Columns longer than kLongCol (hub sources) are handed to a block-wide
-// kernel so that no single warp serialises thousands of gathers.
+// GAT column pass: columns longer than kLongCol (hub sources) are handed to
+// a block-wide kernel so that no single warp serialises thousands of gathers.
 static constexpr int kLongCol = 64;
-// sum/mean CSC path: columns with <= kMidCol entries go to k_agg_bwd_p (8
-// lanes each, rounds of 8 entries), longer ones to k_agg_bwd_p_long (8 warps
-// each): a column of 64 entries on 8 lanes would be 8 dependent gather rounds
-// that stall the whole kernel (measured: layer-1 agg bwd 23 -> 15 us)
-static constexpr int kMidCol = 16;
-static constexpr int kPLongWarps = 8;      // warps per column in k_agg_bwd_p_long
-
-template <int D, bool MEAN>
-__device__ __forceinline__ float4 col_slice_sum(int b, int e, int shift,
-                                                const int* __restrict__ csc_row,
-                                                const int* __restrict__ row_ptr,
-                                                const float4* __restrict__ G, int lane) {
-  constexpr int LPR = D / 4;
-  constexpr int NS = 32 / LPR;
-  const int sl = lane % LPR, sid = lane / LPR;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int base = b; base < e; base += 32) {
-    const int n = min(32, e - base);
-    int my_row = 0;
-    float my_w = 1.f;
-    if (lane < n) {
-      my_row = __ldg(csc_row + base + lane);
-      if (MEAN) my_w = 1.f / (float)(__ldg(row_ptr + my_row + 1) - __ldg(row_ptr + my_row));
-    }
-    int k = 0;
-    for (; k + NS * kUnroll <= n; k += NS * kUnroll) {
-      float4 v[kUnroll];
-      float w[kUnroll];
-#pragma unroll
-      for (int q = 0; q < kUnroll; q++) {
-        int src_lane = k + q * NS + sid;
-        int rr = __shfl_sync(0xffffffffu, my_row, src_lane);
-        w[q] = __shfl_sync(0xffffffffu, my_w, src_lane);
-        v[q] = ldg4(G + (long long)(rr + shift) * LPR + sl);
-      }
-#pragma unroll
-      for (int q = 0; q < kUnroll; q++) acc = MEAN ? f4fma(w[q], v[q], acc) : f4add(acc, v[q]);
-    }
-    for (; k < n; k += NS) {
-      int idx = k + sid;
-      int src_lane = idx < n ? idx : 0;
-      int rr = __shfl_sync(0xffffffffu, my_row, src_lane);
-      float w = __shfl_sync(0xffffffffu, my_w, src_lane);
-      if (idx < n) {
-        float4 v = ldg4(G + (long long)(rr + shift) * LPR + sl);
-        acc = MEAN ? f4fma(w, v, acc) : f4add(acc, v);
-      }
-    }
-  }
-#pragma unroll
-  for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
-  return acc;
-}
-
 static constexpr int kLongWarps = 32;
-
-template <int D, bool MEAN>
-__global__ void __launch_bounds__(kLongWarps * 32)
-k_agg_bwd_long(BwdMeta bm, const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
-               const int* __restrict__ csc_row, const int* __restrict__ row_ptr,
-               const float4* __restrict__ G, float4* __restrict__ dY, const int* __restrict__ list,
-               const int* __restrict__ cnt) {
-  constexpr int LPR = D / 4;
-  __shared__ int s_yoff[HF_MAX_R + 1];
-  __shared__ float4 red[kLongWarps][LPR];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int n_long = *cnt;
-  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
-    const int u = list[k];
-    const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
-    const int b = col_ptr[u], e = col_ptr[u + 1];
-    const int per = (e - b + kLongWarps - 1) / kLongWarps;
-    const int wb = min(e, b + w * per), we = min(e, wb + per);
-    float4 acc = col_slice_sum<D, MEAN>(wb, we, bm.shift[r], csc_row, row_ptr, G, lane);
-    if (lane < LPR) red[w][lane] = acc;
-    __syncthreads();
-    if (w == 0 && lane < LPR) {
-      float4 t = red[0][lane];
-      for (int q = 1; q < kLongWarps; q++) t = f4add(t, red[q][lane]);
-      dY[(long long)u * LPR + lane] = t;
-    }
-    __syncthreads();
-  }
-}
-
-// Columns hold 1-3 entries on average, so a warp per column would spend its
-// time in one dependent chain (col_ptr -> csc_row -> row_ptr -> G) per 512 B
-// of output.  Instead kLPC lanes serve one column: a warp covers 32/kLPC
-// columns, each lane gathers D/4/kLPC float4 per entry (independent loads in
-// flight), and the kLPC lanes of a group read 16*kLPC contiguous bytes.
-static constexpr int kLPC = 8;
-
-template <int D, bool MEAN>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
-k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __restrict__ rel_y_off,
-          const int* __restrict__ col_ptr, const int* __restrict__ csc_row,
-          const int* __restrict__ row_ptr, const float4* __restrict__ G, float4* __restrict__ dY,
-          int* __restrict__ long_list, int* __restrict__ long_cnt) {
-  constexpr int LPR = D / 4;            // float4 per row
-  constexpr int V = LPR / kLPC;         // float4 per lane
-  __shared__ int s_yoff[HF_MAX_R + 1];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int U = *U_dev;
-  const int u = (blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * (32 / kLPC) + lane / kLPC;
-  const int j = lane % kLPC;
-  if ((blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * (32 / kLPC) >= U) return;  // whole warp
-  int b = 0, e = 0;
-  bool skip = u >= U;
-  if (!skip) {
-    b = col_ptr[u];
-    e = col_ptr[u + 1];
-    if (e - b > kLongCol) {
-      if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
-      e = b;                                  // handled by k_agg_bwd_long
-      skip = true;
-    }
-  }
-  const int shift = u < U ? bm.shift[upper_bound_i(s_yoff, bm.R + 1, u) - 1] : 0;
-  float4 acc[V];
-#pragma unroll
-  for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-  // kLPC entries per round: lane j of the group fetches entry p0 + j's row
-  // and weight (one parallel round trip), then the group gathers them all.
-  // The round count is warp-uniform (shuffles need the full warp).
-  const int gbase = lane & ~(kLPC - 1);
-  const int rounds = __reduce_max_sync(0xffffffffu, (e - b + kLPC - 1) / kLPC);
-  for (int rd = 0; rd < rounds; rd++) {
-    const int p0 = b + rd * kLPC;
-    int my_row = 0;
-    float my_w = 0.f;
-    if (p0 + j < e) {
-      my_row = __ldg(csc_row + p0 + j);
-      my_w = MEAN ? 1.f / (float)(__ldg(row_ptr + my_row + 1) - __ldg(row_ptr + my_row)) : 1.f;
-    }
-    const int cnt = max(0, min(kLPC, e - p0));
-#pragma unroll
-    for (int q0 = 0; q0 < kLPC; q0 += 2) {
-      float4 x[2][V];
-      float wq[2];
-#pragma unroll
-      for (int q = 0; q < 2; q++) {
-        const int rq = __shfl_sync(0xffffffffu, my_row, gbase + q0 + q);
-        wq[q] = __shfl_sync(0xffffffffu, my_w, gbase + q0 + q);
-        const float4* g = G + (long long)(rq + shift) * LPR + j;
-#pragma unroll
-        for (int v = 0; v < V; v++)
-          x[q][v] = q0 + q < cnt ? ldg4(g + v * kLPC) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int q = 0; q < 2; q++)
-#pragma unroll
-        for (int v = 0; v < V; v++)
-          acc[v] = MEAN ? f4fma(wq[q], x[q][v], acc[v]) : f4add(acc[v], x[q][v]);
-      if (__all_sync(0xffffffffu, q0 + 2 >= cnt)) break;
-    }
-  }
-  if (skip) return;
-  float4* o = dY + (long long)u * LPR + j;
-#pragma unroll
-  for (int v = 0; v < V; v++) o[v * kLPC] = acc[v];
-}
 
 // Transpose SpMM of the sum / mean aggregation (the adjoint of Alg. 1):
 //   dY[u] = sum_{p in CSC column u} w(m_p) G[g(m_p)],  m_p = csc_row[p],
@@ -551,139 +386,61 @@ k_agg_bwd(BwdMeta bm, int U_max, const int* __restrict__ U_dev, const int* __res
 // summed, as an fp32 multiply followed by an add).  No pre-scaled copy of G:
 // the lane that loads csc_row[p] resolves (g(m), w) -- relation by binary
 // search over rel_row_off in shared memory, degree from row_ptr -- and
-// broadcasts them to the 8 lanes that gather the row.
-struct EntryRW {
-  int g;       // G row (-1: none)
-  float w;
-};
-
-template <bool MEAN>
-__device__ __forceinline__ EntryRW entry_rw(int m, const int* s_roff, const int* s_shift, int R,
-                                            const int* __restrict__ row_ptr) {
-  EntryRW e{-1, 0.f};
-  if (m < 0) return e;
-  int lo = 0, hi = R;                        // s_roff[lo] <= m < s_roff[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (s_roff[mid] <= m) lo = mid; else hi = mid;
-  }
-  e.g = m + s_shift[lo];
-  e.w = 1.f;
-  if (MEAN) {
-    const int dg = __ldg(row_ptr + m + 1) - __ldg(row_ptr + m);
-    e.w = 1.f / (float)dg;                   // dg >= 1: m holds the entry
-  }
-  return e;
-}
-
+// broadcasts them to the lanes that gather the row.
 __device__ __forceinline__ float4 f4mul_add(float w, float4 x, float4 a, bool mean) {
   if (!mean) return f4add(a, x);
   return make_float4(__fadd_rn(a.x, __fmul_rn(w, x.x)), __fadd_rn(a.y, __fmul_rn(w, x.y)),
                      __fadd_rn(a.z, __fmul_rn(w, x.z)), __fadd_rn(a.w, __fmul_rn(w, x.w)));
 }
 
-// Persistent CSC gather: 8 lanes per column, 4 columns per warp, grid-stride
-// over column groups.  Software pipeline per iteration: col_ptr of group i+2,
-// the first 8 (g, w) entries of group i+1 and the G rows of group i are in
-// flight together.
-template <int D, bool MEAN>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
-k_agg_bwd_p(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __restrict__ row_ptr,
-            int U_max, const int* __restrict__ U_dev, const int* __restrict__ col_ptr,
-            const int* __restrict__ csc_row, const float4* __restrict__ G,
-            float4* __restrict__ dY, int* __restrict__ long_list, int* __restrict__ long_cnt) {
-  constexpr int LPR = D / 4, LPC = 8, V = LPR / LPC, CPW = 32 / LPC;
-  __shared__ int s_roff[HF_MAX_R + 1];
-  __shared__ int s_shift[HF_MAX_R];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) {
-    s_roff[i] = rel_row_off_d[i];
-    if (i < bm.R) s_shift[i] = bm.shift[i];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, j = lane % LPC, grp = lane / LPC;
-  const int gbase = lane & ~(LPC - 1);
-  const int U = *U_dev;
-  const int nw = gridDim.x * kWarpsPerBlock;
-  const int cg0 = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  auto bounds = [&](int cg, int* b, int* e) {
-    const int u = cg * CPW + grp;
-    *b = *e = 0;
-    if (u < U) { *b = __ldg(col_ptr + u); *e = __ldg(col_ptr + u + 1); }
-  };
-  auto first_row = [&](int b, int e) {
-    // long columns go to k_agg_bwd_p_long; their first round is not fetched
-    return (e - b <= kMidCol && b + j < e) ? __ldg(csc_row + b + j) : -1;
-  };
-  int b0, e0, b1, e1;
-  bounds(cg0, &b0, &e0);
-  bounds(cg0 + nw, &b1, &e1);
-  int row0 = first_row(b0, e0);
-  for (int cg = cg0; cg * CPW < U; cg += nw) {
-    int b2, e2;
-    bounds(cg + 2 * nw, &b2, &e2);
-    const int row1 = first_row(b1, e1);
-    const int u = cg * CPW + grp;
-    bool skip = u >= U;
-    int e = e0;
-    if (!skip && e0 - b0 > kMidCol) {
-      if (j == 0) long_list[atomicAdd(long_cnt, 1)] = u;
-      e = b0;
-      skip = true;
-    }
-    float4 acc[V];
-#pragma unroll
-    for (int v = 0; v < V; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int rounds = __reduce_max_sync(0xffffffffu, (e - b0 + LPC - 1) / LPC);
-    int my_row = row0;
-    for (int rd = 0; rd < rounds; rd++) {
-      if (rd > 0) {
-        const int p = b0 + rd * LPC + j;
-        my_row = p < e ? __ldg(csc_row + p) : -1;
-      }
-      const EntryRW me = entry_rw<MEAN>(my_row, s_roff, s_shift, bm.R, row_ptr);
-#pragma unroll
-      for (int q0 = 0; q0 < LPC; q0 += 4) {
-        float4 x[4][V];
-        float wq[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const int gq = __shfl_sync(0xffffffffu, me.g, gbase + q0 + q);
-          wq[q] = __shfl_sync(0xffffffffu, me.w, gbase + q0 + q);
-          const float4* g = G + (long long)(gq < 0 ? 0 : gq) * LPR + j;
-#pragma unroll
-          for (int v = 0; v < V; v++)
-            x[q][v] = gq >= 0 ? ldg4(g + v * LPC) : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (gq < 0) wq[q] = 0.f;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-#pragma unroll
-          for (int v = 0; v < V; v++) acc[v] = f4mul_add(wq[q], x[q][v], acc[v], MEAN);
-      }
-    }
-    if (!skip) {
-      float4* o = dY + (long long)u * LPR + j;
-#pragma unroll
-      for (int v = 0; v < V; v++) o[v * LPC] = acc[v];
-    }
-    b0 = b1; e0 = e1; row0 = row1;
-    b1 = b2; e1 = e2;
-  }
+// Edge-balanced CSC walk.  Warp k owns the CSC entries [k E, (k+1) E) (E =
+// chosen per call), whatever columns they fall in, so a hub column costs no more per
+// warp than a run of one-entry columns: the warp finds the column of its first
+// entry with a 32-ary search over col_ptr, then walks its entries in
+// sub-batches of up to 32 (one coalesced load of csc_row and one of the
+// col_ptr window, prefetched one sub-batch ahead), resolves (g, w) per entry
+// on the lane that loaded it and gathers kEDepth G rows at a time with the
+// whole warp on a row (D/32 floats per lane).  The row sum of a column is
+// accumulated in registers in CSC order and stored when the column changes:
+//   - a column wholly inside the chunk goes straight to dY;
+//   - the column the chunk starts in the middle of goes to the chunk's head
+//     slot, a column that runs past the chunk end to its tail slot (and
+//     tail_col[k] records it); k_agg_bwd_fix adds tail[a] + head[a+1] + ...
+//     + head[z] in chunk order (deterministic) for every split column.
+// E is chosen per call (32 <= E <= kEMax) so that the chunks fill one wave
+// of resident warps: small layers get short chunks (more warps,
+// shorter dependent chains), large ones long chunks (fewer split columns).
+static constexpr int kEMax = 256;
+static constexpr int kEDepth = 8;
+static inline int bwd_chunk_entries(long long N) {
+  const long long warps = (long long)sm_count() * 3 * kWarpsPerBlock;   // resident at 3 blocks/SM
+  return (int)std::max(32ll, std::min<long long>(kEMax, (N + warps - 1) / warps));
 }
 
-// Long columns (kPLongWarps warps per column, fixed-order combine of the
-// warp slices).
+template <int D> struct RowVec;
+template <> struct RowVec<128> { using T = float4; };
+template <> struct RowVec<64> { using T = float2; };
+__device__ __forceinline__ float2 vzero(float2) { return make_float2(0.f, 0.f); }
+__device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ float2 vadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) { return f4add(a, b); }
+__device__ __forceinline__ float2 vmul_add(float w, float2 x, float2 a, bool mean) {
+  if (!mean) return vadd(a, x);
+  return make_float2(__fadd_rn(a.x, __fmul_rn(w, x.x)), __fadd_rn(a.y, __fmul_rn(w, x.y)));
+}
+__device__ __forceinline__ float4 vmul_add(float w, float4 x, float4 a, bool mean) {
+  return f4mul_add(w, x, a, mean);
+}
+
 template <int D, bool MEAN>
-__global__ void __launch_bounds__(kPLongWarps * 32)
-k_agg_bwd_p_long(BwdMeta bm, const int* __restrict__ rel_row_off_d,
-                 const int* __restrict__ row_ptr, const int* __restrict__ col_ptr,
-                 const int* __restrict__ csc_row, const float4* __restrict__ G,
-                 float4* __restrict__ dY, const int* __restrict__ list,
-                 const int* __restrict__ cnt) {
-  constexpr int LPR = D / 4;
-  constexpr int NS = 32 / LPR;
-  constexpr int GF = 8;                                   // gathers in flight per stream
-  __shared__ float4 red[kPLongWarps][LPR];
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
+k_agg_bwd_e(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __restrict__ row_ptr,
+            const int* __restrict__ U_dev, const int* __restrict__ col_ptr,
+            const int* __restrict__ csc_row, const typename RowVec<D>::T* __restrict__ G,
+            typename RowVec<D>::T* __restrict__ dY, typename RowVec<D>::T* __restrict__ part,
+            int* __restrict__ tail_col, int n_chunks, int E) {
+  using VT = typename RowVec<D>::T;
+  constexpr unsigned FULL = 0xffffffffu;
   __shared__ int s_roff[HF_MAX_R + 1];
   __shared__ int s_shift[HF_MAX_R];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) {
@@ -691,45 +448,126 @@ k_agg_bwd_p_long(BwdMeta bm, const int* __restrict__ rel_row_off_d,
     if (i < bm.R) s_shift[i] = bm.shift[i];
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int sl = lane % LPR, sid = lane / LPR;
-  const int n_long = *cnt;
-  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
-    const int u = list[k];
-    const int b = col_ptr[u], e = col_ptr[u + 1];
-    const int per = (e - b + kPLongWarps - 1) / kPLongWarps;
-    const int wb = min(e, b + w * per), we = min(e, wb + per);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int base = wb; base < we; base += 32) {
-      const int n = min(32, we - base);
-      const EntryRW me = entry_rw<MEAN>(lane < n ? __ldg(csc_row + base + lane) : -1, s_roff,
-                                        s_shift, bm.R, row_ptr);
-      for (int kk = 0; kk < n; kk += NS * GF) {
-        float4 x[GF];
-        float wq[GF];
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (k >= n_chunks) return;
+  const int U = *U_dev;
+  const int nnz = __ldg(col_ptr + U);                 // valid entries
+  const int p0 = k * E, p1 = min(nnz, p0 + E);
+  if (p0 >= nnz) {
+    if (lane == 0) tail_col[k] = -1;
+    return;
+  }
+  // column of entry p0: the largest c < U with col_ptr[c] <= p0
+  int lo = 0, hi = U;                                 // col_ptr[lo] <= p0 < col_ptr[hi]
+#pragma unroll 1
+  for (int it = 0; it < 7; it++) {                    // 32^7 > 2^31: fixed trip count
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + step * (lane + 1);
+    const bool le = idx < hi && __ldg(col_ptr + idx) <= p0;
+    lo += __popc(__ballot_sync(FULL, le)) * step;
+    hi = min(hi, lo + step);
+  }
+  int c_sb = lo;                                      // column of the sub-batch's first entry
+  int sb_start = __ldg(col_ptr + lo);                 // ... and its first CSC entry
+  int cp = c_sb + 1 + lane <= U ? __ldg(col_ptr + c_sb + 1 + lane) : INT_MAX;  // col_ptr[c_sb+1+lane]
+  // Software pipeline over sub-batches: csc_row runs two sub-batches ahead,
+  // the col_ptr window and (mean) the row_ptr pair of each entry's merged row
+  // one ahead, so only the G gathers sit on a sub-batch's critical path.
+  int row_c = p0 + lane < p1 ? __ldg(csc_row + p0 + lane) : -1;
+  int rb_c = 0, re_c = 1;
+  if (MEAN && row_c >= 0) { rb_c = __ldg(row_ptr + row_c); re_c = __ldg(row_ptr + row_c + 1); }
+  int row_n = p0 + 32 + lane < p1 ? __ldg(csc_row + p0 + 32 + lane) : -1;
+  int tail = -1;
+  VT acc = vzero(VT{});
+  // Columns hold >= 1 entry, so the 32-column window covers min(32, p1 - q)
+  // entries.  Loop bounds are warp-uniform; shuffles run converged.
+#pragma unroll 1
+  for (int q = p0; q < p1; q += 32) {
+    const int n = min(32, p1 - q);
+    // my entry q + lane: its column c_sb + off, that column's CSC range, and
+    // where the running sum goes if the entry closes the column's piece
+    const int pe = q + lane;
+    int off = 0;
 #pragma unroll
-        for (int q = 0; q < GF; q++) {
-          const int idx = kk + q * NS + sid;
-          const int gq = __shfl_sync(0xffffffffu, me.g, idx < n ? idx : 0);
-          const float wv = __shfl_sync(0xffffffffu, me.w, idx < n ? idx : 0);   // all lanes
-          wq[q] = idx < n ? wv : 0.f;
-          x[q] = idx < n ? ldg4(G + (long long)gq * LPR + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int st = 16; st >= 1; st >>= 1)
+      if (__shfl_sync(FULL, cp, off + st - 1) <= pe) off += st;
+    const int c_end = __shfl_sync(FULL, cp, off);
+    const int c_prev = __shfl_sync(FULL, cp, off > 0 ? off - 1 : 0);
+    const int c_start = off > 0 ? c_prev : sb_start;
+    VT* my_dst = nullptr;                             // row my entry's running sum closes
+    if (lane < n && (pe + 1 == c_end || pe + 1 == p1)) {
+      if (c_start < p0) my_dst = part + 2ll * k * 32;                      // head slot
+      else if (c_end > p1) { my_dst = part + (2ll * k + 1) * 32; tail = c_sb + off; }
+      else my_dst = dY + (long long)(c_sb + off) * 32;
+    }
+    // prefetches
+    const int qn = q + 32;
+    const int cnt = __popc(__ballot_sync(FULL, cp <= qn));
+    const int cp_last = __shfl_sync(FULL, cp, cnt > 0 ? cnt - 1 : 0);
+    const int cn = c_sb + cnt;
+    const int cp_n = qn < p1 && cn + 1 + lane <= U ? __ldg(col_ptr + cn + 1 + lane) : INT_MAX;
+    const int row_nn = qn + 32 + lane < p1 ? __ldg(csc_row + qn + 32 + lane) : -1;
+    int rb_n = 0, re_n = 1;
+    if (MEAN && row_n >= 0) { rb_n = __ldg(row_ptr + row_n); re_n = __ldg(row_ptr + row_n + 1); }
+    // (g, w) of my entry: G row m + shift[r(m)], weight 1 / |row m| (mean)
+    int my_g = 0;
+    if (row_c >= 0) {
+      int rlo = 0, rhi = bm.R;                        // s_roff[rlo] <= m < s_roff[rhi]
+      while (rhi - rlo > 1) {
+        const int mid = (rlo + rhi) >> 1;
+        if (s_roff[mid] <= row_c) rlo = mid; else rhi = mid;
+      }
+      my_g = row_c + s_shift[rlo];
+    }
+    const float my_w = MEAN ? __frcp_rn((float)(re_c - rb_c)) : 1.f;
+#pragma unroll 1
+    for (int k0 = 0; k0 < n; k0 += kEDepth) {
+      VT x[kEDepth];
+#pragma unroll
+      for (int j = 0; j < kEDepth; j++) {             // past n: entry n-1's row again
+        const int g = __shfl_sync(FULL, my_g, min(k0 + j, n - 1));
+        x[j] = __ldg(G + (long long)g * 32 + lane);
+      }
+#pragma unroll
+      for (int j = 0; j < kEDepth; j++) {             // k0 + j <= 31
+        VT* dst = reinterpret_cast<VT*>(
+            __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my_dst), k0 + j));
+        if (MEAN) acc = vmul_add(__shfl_sync(FULL, my_w, k0 + j), x[j], acc, true);
+        else acc = vadd(acc, x[j]);
+        // past n the sum is garbage but never stored (dst null there): entry
+        // n-1 closes the chunk's last piece
+        if (dst) {
+          dst[lane] = acc;
+          acc = vzero(VT{});
         }
-#pragma unroll
-        for (int q = 0; q < GF; q++) acc = f4mul_add(wq[q], x[q], acc, MEAN);
       }
     }
-#pragma unroll
-    for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
-    if (sid == 0) red[w][sl] = acc;
-    __syncthreads();
-    if (w == 0 && lane < LPR) {
-      float4 t = red[0][lane];
-      for (int q = 1; q < kPLongWarps; q++) t = f4add(t, red[q][lane]);
-      dY[(long long)u * LPR + lane] = t;
-    }
-    __syncthreads();
+    sb_start = cnt > 0 ? cp_last : sb_start;          // column cn starts at col_ptr[cn]
+    c_sb = cn;
+    cp = cp_n;
+    row_c = row_n; rb_c = rb_n; re_c = re_n;
+    row_n = row_nn;
   }
+  tail = __reduce_max_sync(FULL, tail);
+  if (lane == 0) tail_col[k] = tail;
+}
+
+// Split columns: dY[t] = tail[a] + head[a+1] + ... + head[z] (chunk order).
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_fix(const int* __restrict__ col_ptr, const typename RowVec<D>::T* __restrict__ part,
+              const int* __restrict__ tail_col, typename RowVec<D>::T* __restrict__ dY,
+              int n_chunks, int E) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (k >= n_chunks) return;
+  const int t = tail_col[k];
+  if (t < 0) return;
+  const int z = (__ldg(col_ptr + t + 1) - 1) / E;
+  auto acc = part[(2ll * k + 1) * 32 + lane];
+  for (int j = k + 1; j <= z; j++) acc = vadd(acc, part[(2ll * j) * 32 + lane]);
+  dY[(long long)t * 32 + lane] = acc;
 }
 
 // ------------------------------------------------ backward GAT, pass 1 (rows)
@@ -1537,6 +1375,10 @@ size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
   long long U_max = m.N < m.S ? m.N : m.S;
   size_t b = carve_bytes(U_max + 1, 4) + carve_bytes(2, 4);
+  if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {   // k_agg_bwd_e slots (D <= 128)
+    const long long nch = (m.N + 31) / 32;                  // chunks of >= 32 entries
+    b += carve_bytes(2 * nch * 128, 4) + carve_bytes(nch, 4);
+  }
   if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL || agg == HIFUSE_AGG_GAT_MUL)
     b += 2 * carve_bytes((long long)m.N * heads, 4);
   return b;
@@ -1586,7 +1428,6 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   int* long_cnt = carve<int>(p, 2);
   cudaMemsetAsync(long_cnt, 0, sizeof(int), s);
   unsigned gridU = ceil_div(U_max, kWarpsPerBlock);
-  unsigned gridU4 = ceil_div(U_max, kWarpsPerBlock * (32 / kLPC));
   const int TB = kWarpsPerBlock * 32;
   const unsigned gridL = 296;
   if (gat) {
@@ -1626,16 +1467,22 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
     else { if (mul) { HF_GAT(64, true); } else { HF_GAT(64, false); } }
 #undef HF_GAT
   } else {
+    const int E = bwd_chunk_entries(m.N);
+    const long long nch = (m.N + E - 1) / E;
+    float* part = carve<float>(p, 2 * ((m.N + 31) / 32) * 128);
+    int* tail_col = carve<int>(p, (m.N + 31) / 32);
+    const unsigned gridE = ceil_div(nch, kWarpsPerBlock);
 #define HF_BWD(DD, MM)                                                                        \
-  HF_LAUNCH((k_agg_bwd_p<DD, MM>), sm_count() * 4, TB, 0, s, bm, csr->rel_row_off, csr->row_ptr, \
-            (int)U_max, csr->U_dev, csr->col_ptr, csr->csc_row, (const float4*)d_G,             \
-            (float4*)d_dY, long_list, long_cnt);                                                \
-  HF_LAUNCH((k_agg_bwd_p_long<DD, MM>), sm_count() * 8, kPLongWarps * 32, 0, s, bm,               \
-            csr->rel_row_off, csr->row_ptr, csr->col_ptr, csr->csc_row, (const float4*)d_G,     \
-            (float4*)d_dY, long_list, long_cnt)
-    bool mean = agg == HIFUSE_AGG_MEAN;
-    if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }
-    else { if (mean) { HF_BWD(64, true); } else { HF_BWD(64, false); } }
+  HF_LAUNCH((k_agg_bwd_e<DD, MM>), gridE, TB, 0, s, bm, csr->rel_row_off, csr->row_ptr,          \
+            csr->U_dev, csr->col_ptr, csr->csc_row, (const RowVec<DD>::T*)d_G,                  \
+            (RowVec<DD>::T*)d_dY, (RowVec<DD>::T*)part, tail_col, (int)nch, E);                    \
+  HF_LAUNCH((k_agg_bwd_fix<DD>), gridE, TB, 0, s, csr->col_ptr, (const RowVec<DD>::T*)part,      \
+            tail_col, (RowVec<DD>::T*)d_dY, (int)nch, E)
+    if (m.N > 0) {
+      bool mean = agg == HIFUSE_AGG_MEAN;
+      if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }
+      else { if (mean) { HF_BWD(64, true); } else { HF_BWD(64, false); } }
+    }
 #undef HF_BWD
   }
   return last_cuda();
