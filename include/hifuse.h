@@ -123,9 +123,11 @@ typedef struct {
  * slot_y[slot(r, j)] = Y row of (r, j) or -1, slot(r, j) = sum_{r'<r}
  * n_src(src type of r') + j.  CSC over Y rows: col_ptr, csc_pos (CSR
  * position, ascending inside a column), csc_row (merged row of that
- * position).  Entries past the valid count are -1; col_ptr entries past U
- * equal the number of valid edges.  The CSC is optional: col_ptr, csc_pos and
- * csc_row all NULL skip the transpose (a layer whose aggregation backward is
+ * position), csc_col (the column, i.e. Y row, of the entry: the edge-balanced
+ * transpose SpMM reads it instead of searching col_ptr).  Entries past the
+ * valid count are -1; col_ptr entries past U equal the number of valid edges.
+ * The CSC is optional: col_ptr, csc_pos, csc_row and csc_col all NULL skip
+ * the transpose (a layer whose aggregation backward is
  * never run, e.g. the input layer of the aggregate-first RGCN). */
 typedef struct {
   int32_t *rel_row_off;  /* [R+1]      */
@@ -137,6 +139,7 @@ typedef struct {
   int32_t *col_ptr;      /* [U_max+1]  */
   int32_t *csc_pos;      /* [N]        */
   int32_t *csc_row;      /* [N]        */
+  int32_t *csc_col;      /* [N]        */
   int32_t *slot_y;       /* [S]        */
   int32_t *U_dev;        /* [1]        */
 } hifuse_csr;

@@ -120,6 +120,12 @@ def build(shape: Shape, blk, edge_type):
     out["status"] = int(st)
     out["y_src"] = out["y_src"][:out["U"]]
     out["col_ptr"] = out["col_ptr"][:out["U"] + 1]
+    # csc_col[p] = the column u with col_ptr[u] <= p < col_ptr[u+1]; -1 past
+    # the valid entries (the definition, written out)
+    cc = np.full(N, -1, np.int32)
+    for u in range(out["U"]):
+        cc[out["col_ptr"][u]:out["col_ptr"][u + 1]] = u
+    out["csc_col"] = cc
     out["slot_y"] = out["slot_y"][:shape.S]
     return out
 

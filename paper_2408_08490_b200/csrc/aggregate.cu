@@ -374,11 +374,6 @@ struct BwdMeta {
   int shift[HF_MAX_R];   // type_dst_off[t(r)] - rel_row_off[r]
 };
 
-// GAT column pass: columns longer than kLongCol (hub sources) are handed to
-// a block-wide kernel so that no single warp serialises thousands of gathers.
-static constexpr int kLongCol = 64;
-static constexpr int kLongWarps = 32;
-
 // Transpose SpMM of the sum / mean aggregation (the adjoint of Alg. 1):
 //   dY[u] = sum_{p in CSC column u} w(m_p) G[g(m_p)],  m_p = csc_row[p],
 // g(m) = m + shift[r(m)] the type-major G row of merged row m = (r, i), w = 1
@@ -393,28 +388,34 @@ __device__ __forceinline__ float4 f4mul_add(float w, float4 x, float4 a, bool me
                      __fadd_rn(a.z, __fmul_rn(w, x.z)), __fadd_rn(a.w, __fmul_rn(w, x.w)));
 }
 
-// Edge-balanced CSC walk.  Warp k owns the CSC entries [k E, (k+1) E) (E =
-// chosen per call), whatever columns they fall in, so a hub column costs no more per
-// warp than a run of one-entry columns: the warp finds the column of its first
-// entry with a 32-ary search over col_ptr, then walks its entries in
-// sub-batches of up to 32 (one coalesced load of csc_row and one of the
-// col_ptr window, prefetched one sub-batch ahead), resolves (g, w) per entry
-// on the lane that loaded it and gathers kEDepth G rows at a time with the
-// whole warp on a row (D/32 floats per lane).  The row sum of a column is
-// accumulated in registers in CSC order and stored when the column changes:
-//   - a column wholly inside the chunk goes straight to dY;
-//   - the column the chunk starts in the middle of goes to the chunk's head
-//     slot, a column that runs past the chunk end to its tail slot (and
-//     tail_col[k] records it); k_agg_bwd_fix adds tail[a] + head[a+1] + ...
-//     + head[z] in chunk order (deterministic) for every split column.
-// E is chosen per call (32 <= E <= kEMax) so that the chunks fill one wave
-// of resident warps: small layers get short chunks (more warps,
-// shorter dependent chains), large ones long chunks (fewer split columns).
-static constexpr int kEMax = 256;
+// Edge-balanced CSC walk.  Warp k owns the CSC entries [k E, (k+1) E) (E
+// chosen per call), whatever columns they fall in, so a hub column costs no
+// more per warp than a run of one-entry columns.  The build's csc_col gives
+// every entry's column directly (no search over col_ptr): the warp walks its
+// entries in sub-batches of 32 (coalesced loads of csc_col / csc_row, two
+// sub-batches ahead; the mean's row_ptr pair one ahead), the lane of an entry
+// resolves (g, w) and whether the entry closes its column's piece, and the
+// whole warp gathers kEDepth G rows at a time (D/32 floats per lane), summing
+// a column's rows in registers in CSC order.  A closed piece goes
+//   - to dY when the column lies inside the chunk,
+//   - to the chunk's head slot when the column began before the chunk
+//     (head_col[k] records it), to its tail slot when it runs past the end
+//     (tail_col[k]); the fix-up kernel adds tail[a] + head[a+1] + ... in chunk
+//     order (deterministic).
+// E is chosen per call (kEMin <= E <= kEMax) so that the chunks fill one
+// wave of resident warps: small layers get short chunks (more warps, shorter
+// dependent chains), large ones long chunks (fewer split columns).  Either
+// way the chunk count is at most max(resident warps, N / kEMax) + 1, which
+// sizes the partial slots of the workspace.
+static constexpr int kEMin = 8, kEMax = 256;
 static constexpr int kEDepth = 8;
+static inline long long bwd_resident_warps() { return (long long)sm_count() * 3 * kWarpsPerBlock; }
 static inline int bwd_chunk_entries(long long N) {
-  const long long warps = (long long)sm_count() * 3 * kWarpsPerBlock;   // resident at 3 blocks/SM
-  return (int)std::max(32ll, std::min<long long>(kEMax, (N + warps - 1) / warps));
+  const long long warps = bwd_resident_warps();          // resident at 3 blocks/SM
+  return (int)std::max<long long>(kEMin, std::min<long long>(kEMax, (N + warps - 1) / warps));
+}
+static inline long long bwd_max_chunks(long long N) {
+  return std::max(bwd_resident_warps(), (N + kEMax - 1) / kEMax) + 1;
 }
 
 template <int D> struct RowVec;
@@ -431,13 +432,43 @@ __device__ __forceinline__ float2 vmul_add(float w, float2 x, float2 a, bool mea
 __device__ __forceinline__ float4 vmul_add(float w, float4 x, float4 a, bool mean) {
   return f4mul_add(w, x, a, mean);
 }
+__device__ __forceinline__ float2 vfma(float s, float2 y, float2 a) {
+  return make_float2(fmaf(s, y.x, a.x), fmaf(s, y.y, a.y));
+}
+__device__ __forceinline__ float4 vfma(float s, float4 y, float4 a) { return f4fma(s, y, a); }
+template <int D>
+__device__ __forceinline__ typename RowVec<D>::T ldg_row(const float* p, int lane) {
+  return __ldg(reinterpret_cast<const typename RowVec<D>::T*>(p) + lane);
+}
+
+// The chunk [p0, pend) and the columns of the entries just before and after it.
+struct ChunkCtx {
+  int p0, pend, prev_col, after_col;
+};
+// Column of the entry after mine (lane 31: first of the next sub-batch).
+__device__ __forceinline__ int next_col(const ChunkCtx& cx, int q, int lane, int col_c,
+                                        int col_n) {
+  const int nx0 = __shfl_sync(0xffffffffu, col_n, 0);
+  const int dn = __shfl_down_sync(0xffffffffu, col_c, 1);
+  if (q + lane + 1 == cx.pend) return cx.after_col;
+  return lane == 31 ? nx0 : dn;
+}
+// G row of merged row m: m + shift[r(m)], r by binary search of rel_row_off
+__device__ __forceinline__ int g_row(int m, const int* s_roff, const int* s_shift, int R) {
+  int lo = 0, hi = R;                                 // s_roff[lo] <= m < s_roff[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_roff[mid] <= m) lo = mid; else hi = mid;
+  }
+  return m + s_shift[lo];
+}
 
 template <int D, bool MEAN>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
 k_agg_bwd_e(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __restrict__ row_ptr,
-            const int* __restrict__ U_dev, const int* __restrict__ col_ptr,
-            const int* __restrict__ csc_row, const typename RowVec<D>::T* __restrict__ G,
-            typename RowVec<D>::T* __restrict__ dY, typename RowVec<D>::T* __restrict__ part,
+            long long N, const int* __restrict__ csc_col, const int* __restrict__ csc_row,
+            const typename RowVec<D>::T* __restrict__ G, typename RowVec<D>::T* __restrict__ dY,
+            typename RowVec<D>::T* __restrict__ part, int* __restrict__ head_col,
             int* __restrict__ tail_col, int n_chunks, int E) {
   using VT = typename RowVec<D>::T;
   constexpr unsigned FULL = 0xffffffffu;
@@ -451,75 +482,41 @@ k_agg_bwd_e(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __rest
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (k >= n_chunks) return;
-  const int U = *U_dev;
-  const int nnz = __ldg(col_ptr + U);                 // valid entries
-  const int p0 = k * E, p1 = min(nnz, p0 + E);
-  if (p0 >= nnz) {
-    if (lane == 0) tail_col[k] = -1;
-    return;
-  }
-  // column of entry p0: the largest c < U with col_ptr[c] <= p0
-  int lo = 0, hi = U;                                 // col_ptr[lo] <= p0 < col_ptr[hi]
-#pragma unroll 1
-  for (int it = 0; it < 7; it++) {                    // 32^7 > 2^31: fixed trip count
-    const int step = (hi - lo + 31) >> 5;
-    const int idx = lo + step * (lane + 1);
-    const bool le = idx < hi && __ldg(col_ptr + idx) <= p0;
-    lo += __popc(__ballot_sync(FULL, le)) * step;
-    hi = min(hi, lo + step);
-  }
-  int c_sb = lo;                                      // column of the sub-batch's first entry
-  int sb_start = __ldg(col_ptr + lo);                 // ... and its first CSC entry
-  int cp = c_sb + 1 + lane <= U ? __ldg(col_ptr + c_sb + 1 + lane) : INT_MAX;  // col_ptr[c_sb+1+lane]
-  // Software pipeline over sub-batches: csc_row runs two sub-batches ahead,
-  // the col_ptr window and (mean) the row_ptr pair of each entry's merged row
-  // one ahead, so only the G gathers sit on a sub-batch's critical path.
-  int row_c = p0 + lane < p1 ? __ldg(csc_row + p0 + lane) : -1;
+  ChunkCtx cx;
+  cx.p0 = k * E;
+  cx.pend = (int)min(N, (long long)cx.p0 + E);
+  cx.prev_col = cx.p0 > 0 ? __ldg(csc_col + cx.p0 - 1) : -1;
+  cx.after_col = cx.pend < N ? __ldg(csc_col + cx.pend) : -1;
+  const int p0 = cx.p0, pend = cx.pend;
+  // software pipeline: csc_col / csc_row two sub-batches ahead, row_ptr one
+  int col_c = p0 + lane < pend ? __ldg(csc_col + p0 + lane) : -1;
+  int row_c = p0 + lane < pend ? __ldg(csc_row + p0 + lane) : -1;
   int rb_c = 0, re_c = 1;
   if (MEAN && row_c >= 0) { rb_c = __ldg(row_ptr + row_c); re_c = __ldg(row_ptr + row_c + 1); }
-  int row_n = p0 + 32 + lane < p1 ? __ldg(csc_row + p0 + 32 + lane) : -1;
+  int col_n = p0 + 32 + lane < pend ? __ldg(csc_col + p0 + 32 + lane) : -1;
+  int row_n = p0 + 32 + lane < pend ? __ldg(csc_row + p0 + 32 + lane) : -1;
+  const int c0 = __shfl_sync(FULL, col_c, 0);
+  if (lane == 0) head_col[k] = c0 >= 0 && c0 == cx.prev_col ? c0 : -1;
   int tail = -1;
   VT acc = vzero(VT{});
-  // Columns hold >= 1 entry, so the 32-column window covers min(32, p1 - q)
-  // entries.  Loop bounds are warp-uniform; shuffles run converged.
 #pragma unroll 1
-  for (int q = p0; q < p1; q += 32) {
-    const int n = min(32, p1 - q);
-    // my entry q + lane: its column c_sb + off, that column's CSC range, and
-    // where the running sum goes if the entry closes the column's piece
-    const int pe = q + lane;
-    int off = 0;
-#pragma unroll
-    for (int st = 16; st >= 1; st >>= 1)
-      if (__shfl_sync(FULL, cp, off + st - 1) <= pe) off += st;
-    const int c_end = __shfl_sync(FULL, cp, off);
-    const int c_prev = __shfl_sync(FULL, cp, off > 0 ? off - 1 : 0);
-    const int c_start = off > 0 ? c_prev : sb_start;
-    VT* my_dst = nullptr;                             // row my entry's running sum closes
-    if (lane < n && (pe + 1 == c_end || pe + 1 == p1)) {
-      if (c_start < p0) my_dst = part + 2ll * k * 32;                      // head slot
-      else if (c_end > p1) { my_dst = part + (2ll * k + 1) * 32; tail = c_sb + off; }
-      else my_dst = dY + (long long)(c_sb + off) * 32;
+  for (int q = p0; q < pend; q += 32) {
+    const int n = __popc(__ballot_sync(FULL, col_c >= 0));      // valid entries: a prefix
+    if (n == 0) break;
+    const int nx = next_col(cx, q, lane, col_c, col_n);
+    VT* my_dst = nullptr;
+    if (col_c >= 0 && (nx != col_c || q + lane + 1 == pend)) {  // my entry closes a piece
+      if (col_c == cx.prev_col) my_dst = part + 2ll * k * 32;             // head slot
+      else if (nx == col_c) { my_dst = part + (2ll * k + 1) * 32; tail = col_c; }  // tail
+      else my_dst = dY + (long long)col_c * 32;
     }
-    // prefetches
     const int qn = q + 32;
-    const int cnt = __popc(__ballot_sync(FULL, cp <= qn));
-    const int cp_last = __shfl_sync(FULL, cp, cnt > 0 ? cnt - 1 : 0);
-    const int cn = c_sb + cnt;
-    const int cp_n = qn < p1 && cn + 1 + lane <= U ? __ldg(col_ptr + cn + 1 + lane) : INT_MAX;
-    const int row_nn = qn + 32 + lane < p1 ? __ldg(csc_row + qn + 32 + lane) : -1;
+    const int col_nn = qn + 32 + lane < pend ? __ldg(csc_col + qn + 32 + lane) : -1;
+    const int row_nn = qn + 32 + lane < pend ? __ldg(csc_row + qn + 32 + lane) : -1;
     int rb_n = 0, re_n = 1;
     if (MEAN && row_n >= 0) { rb_n = __ldg(row_ptr + row_n); re_n = __ldg(row_ptr + row_n + 1); }
     // (g, w) of my entry: G row m + shift[r(m)], weight 1 / |row m| (mean)
-    int my_g = 0;
-    if (row_c >= 0) {
-      int rlo = 0, rhi = bm.R;                        // s_roff[rlo] <= m < s_roff[rhi]
-      while (rhi - rlo > 1) {
-        const int mid = (rlo + rhi) >> 1;
-        if (s_roff[mid] <= row_c) rlo = mid; else rhi = mid;
-      }
-      my_g = row_c + s_shift[rlo];
-    }
+    const int my_g = row_c >= 0 ? g_row(row_c, s_roff, s_shift, bm.R) : 0;
     const float my_w = MEAN ? __frcp_rn((float)(re_c - rb_c)) : 1.f;
 #pragma unroll 1
     for (int k0 = 0; k0 < n; k0 += kEDepth) {
@@ -535,39 +532,192 @@ k_agg_bwd_e(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __rest
             __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my_dst), k0 + j));
         if (MEAN) acc = vmul_add(__shfl_sync(FULL, my_w, k0 + j), x[j], acc, true);
         else acc = vadd(acc, x[j]);
-        // past n the sum is garbage but never stored (dst null there): entry
-        // n-1 closes the chunk's last piece
+        // past n the sum is garbage but never stored (dst null there): the
+        // last valid entry closes its piece
         if (dst) {
           dst[lane] = acc;
           acc = vzero(VT{});
         }
       }
     }
-    sb_start = cnt > 0 ? cp_last : sb_start;          // column cn starts at col_ptr[cn]
-    c_sb = cn;
-    cp = cp_n;
-    row_c = row_n; rb_c = rb_n; re_c = re_n;
-    row_n = row_nn;
+    col_c = col_n; row_c = row_n; rb_c = rb_n; re_c = re_n;
+    col_n = col_nn; row_n = row_nn;
   }
   tail = __reduce_max_sync(FULL, tail);
   if (lane == 0) tail_col[k] = tail;
 }
 
-// Split columns: dY[t] = tail[a] + head[a+1] + ... + head[z] (chunk order).
+// Split columns: dY[t] = tail[k] + head[k+1] + ... (chunk order).
 template <int D>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_agg_bwd_fix(const int* __restrict__ col_ptr, const typename RowVec<D>::T* __restrict__ part,
+k_agg_bwd_fix(const typename RowVec<D>::T* __restrict__ part, const int* __restrict__ head_col,
               const int* __restrict__ tail_col, typename RowVec<D>::T* __restrict__ dY,
-              int n_chunks, int E) {
+              int n_chunks) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (k >= n_chunks) return;
   const int t = tail_col[k];
   if (t < 0) return;
-  const int z = (__ldg(col_ptr + t + 1) - 1) / E;
   auto acc = part[(2ll * k + 1) * 32 + lane];
-  for (int j = k + 1; j <= z; j++) acc = vadd(acc, part[(2ll * j) * 32 + lane]);
+  for (int j = k + 1; j < n_chunks && head_col[j] == t; j++)
+    acc = vadd(acc, part[(2ll * j) * 32 + lane]);
   dY[(long long)t * 32 + lane] = acc;
+}
+
+// GAT pass 2 (CSC), edge-balanced like k_agg_bwd_e: per CSC entry p of column u
+// (CSR position pos = csc_pos[p], merged row m = csc_row[p]) and head h,
+//   dY[u]_h += alpha[pos, h] G[g(m)]_h     (fmaf, CSC order)
+//   ds_src[u, h] += dpre[pos, h]
+// and at the column's end dY[u] += ds_src[u] a_src(r(u)) (the scored form,
+// att != NULL).  A lane holds D/32 features of one head; its alpha / dpre
+// loads hit the same word as the other lanes of the head.  Split columns:
+// (acc, dss) pieces in head / tail slots, k_agg_bwd_gat_fix adds them in
+// chunk order and applies the a_src term.
+static constexpr int kGatDss = 32;        // dss words per slot (H <= D/4 <= 32)
+__device__ __forceinline__ int rel_of_y(int u, const int* s_yoff, int R) {
+  int lo = 0, hi = R;                                 // s_yoff[lo] <= u < s_yoff[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_yoff[mid] <= u) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
+k_agg_bwd_gat_e(BwdMeta bm, int H, const int* __restrict__ rel_row_off_d,
+                const int* __restrict__ rel_y_off, long long N, const int* __restrict__ csc_col,
+                const int* __restrict__ csc_pos, const int* __restrict__ csc_row,
+                const float* __restrict__ alpha, const float* __restrict__ dpre,
+                const float* __restrict__ Gf, float* __restrict__ dYf, float* __restrict__ ds_src,
+                typename RowVec<D>::T* __restrict__ part, float* __restrict__ part_dss,
+                int* __restrict__ head_col, int* __restrict__ tail_col, int n_chunks, int E,
+                const float* __restrict__ att) {
+  using VT = typename RowVec<D>::T;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int VEC = D / 32;
+  constexpr int kNone = -1, kHead = -2, kTail = -3;
+  __shared__ int s_roff[HF_MAX_R + 1];
+  __shared__ int s_yoff[HF_MAX_R + 1];
+  __shared__ int s_shift[HF_MAX_R];
+  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) {
+    s_roff[i] = rel_row_off_d[i];
+    s_yoff[i] = rel_y_off[i];
+    if (i < bm.R) s_shift[i] = bm.shift[i];
+  }
+  __syncthreads();
+  const VT* G = reinterpret_cast<const VT*>(Gf);
+  VT* dY = reinterpret_cast<VT*>(dYf);
+  const int lane = threadIdx.x & 31;
+  const int dh = D / H;
+  const int h = lane * VEC / dh;
+  const bool head_lead = (lane * VEC) % dh == 0;
+  const int k = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (k >= n_chunks) return;
+  ChunkCtx cx;
+  cx.p0 = k * E;
+  cx.pend = (int)min(N, (long long)cx.p0 + E);
+  cx.prev_col = cx.p0 > 0 ? __ldg(csc_col + cx.p0 - 1) : -1;
+  cx.after_col = cx.pend < N ? __ldg(csc_col + cx.pend) : -1;
+  const int p0 = cx.p0, pend = cx.pend;
+  int col_c = p0 + lane < pend ? __ldg(csc_col + p0 + lane) : -1;
+  int row_c = p0 + lane < pend ? __ldg(csc_row + p0 + lane) : -1;
+  int pos_c = p0 + lane < pend ? __ldg(csc_pos + p0 + lane) : 0;
+  int col_n = p0 + 32 + lane < pend ? __ldg(csc_col + p0 + 32 + lane) : -1;
+  const int c0 = __shfl_sync(FULL, col_c, 0);
+  if (lane == 0) head_col[k] = c0 >= 0 && c0 == cx.prev_col ? c0 : -1;
+  int tail = -1;
+  VT acc = vzero(VT{});
+  float dss = 0.f;
+#pragma unroll 1
+  for (int q = p0; q < pend; q += 32) {
+    const int n = __popc(__ballot_sync(FULL, col_c >= 0));
+    if (n == 0) break;
+    const int nx = next_col(cx, q, lane, col_c, col_n);
+    int tgt = kNone;
+    if (col_c >= 0 && (nx != col_c || q + lane + 1 == pend)) {
+      if (col_c == cx.prev_col) tgt = kHead;
+      else if (nx == col_c) { tgt = kTail; tail = col_c; }
+      else tgt = col_c;
+    }
+    const int qn = q + 32;
+    const int col_nn = qn + 32 + lane < pend ? __ldg(csc_col + qn + 32 + lane) : -1;
+    const int row_n = qn + lane < pend ? __ldg(csc_row + qn + lane) : -1;
+    const int pos_n = qn + lane < pend ? __ldg(csc_pos + qn + lane) : 0;
+    const int my_g = row_c >= 0 ? g_row(row_c, s_roff, s_shift, bm.R) : 0;
+#pragma unroll 1
+    for (int k0 = 0; k0 < n; k0 += kEDepth) {
+      VT x[kEDepth];
+      float a[kEDepth], d[kEDepth];
+#pragma unroll
+      for (int j = 0; j < kEDepth; j++) {             // past n: entry n-1 again
+        const int src = min(k0 + j, n - 1);
+        const int g = __shfl_sync(FULL, my_g, src);
+        const int ps = __shfl_sync(FULL, pos_c, src);
+        x[j] = __ldg(G + (long long)g * 32 + lane);
+        a[j] = __ldg(alpha + (long long)ps * H + h);
+        d[j] = __ldg(dpre + (long long)ps * H + h);
+      }
+#pragma unroll
+      for (int j = 0; j < kEDepth; j++) {             // k0 + j <= 31
+        const int t = __shfl_sync(FULL, tgt, k0 + j);
+        acc = vfma(a[j], x[j], acc);
+        dss += d[j];
+        if (t != kNone) {                             // warp-uniform
+          if (t >= 0) {
+            if (att)
+              acc = vfma(dss, ldg_row<D>(att + (long long)rel_of_y(t, s_yoff, bm.R) * 2 * D, lane),
+                         acc);
+            dY[(long long)t * 32 + lane] = acc;
+            if (head_lead) ds_src[(long long)t * H + h] = dss;
+          } else {
+            const long long sl = 2ll * k + (t == kTail);
+            part[sl * 32 + lane] = acc;
+            if (head_lead) part_dss[sl * kGatDss + h] = dss;
+          }
+          acc = vzero(VT{});
+          dss = 0.f;
+        }
+      }
+    }
+    col_c = col_n; row_c = row_n; pos_c = pos_n;
+    col_n = col_nn;
+  }
+  tail = __reduce_max_sync(FULL, tail);
+  if (lane == 0) tail_col[k] = tail;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_bwd_gat_fix(int R, int H, const int* __restrict__ rel_y_off,
+                  const typename RowVec<D>::T* __restrict__ part,
+                  const float* __restrict__ part_dss, const int* __restrict__ head_col,
+                  const int* __restrict__ tail_col, float* __restrict__ dYf,
+                  float* __restrict__ ds_src, int n_chunks, const float* __restrict__ att) {
+  using VT = typename RowVec<D>::T;
+  constexpr int VEC = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (k >= n_chunks) return;
+  const int t = tail_col[k];
+  if (t < 0) return;
+  const int dh = D / H, h = lane * VEC / dh;
+  VT acc = part[(2ll * k + 1) * 32 + lane];
+  float dss = part_dss[(2ll * k + 1) * kGatDss + h];
+  for (int j = k + 1; j < n_chunks && head_col[j] == t; j++) {
+    acc = vadd(acc, part[(2ll * j) * 32 + lane]);
+    dss += part_dss[(2ll * j) * kGatDss + h];
+  }
+  if (att) {
+    int lo = 0, hi = R;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(rel_y_off + mid) <= t) lo = mid; else hi = mid;
+    }
+    acc = vfma(dss, ldg_row<D>(att + (long long)lo * 2 * D, lane), acc);
+  }
+  reinterpret_cast<VT*>(dYf)[(long long)t * 32 + lane] = acc;
+  if ((lane * VEC) % dh == 0) ds_src[(long long)t * H + h] = dss;
 }
 
 // ------------------------------------------------ backward GAT, pass 1 (rows)
@@ -752,218 +902,6 @@ k_agg_bwd_gat_rows_half(BwdMeta bm, const int* __restrict__ rel_row_off_d, long 
       dsd += dl * dlogit_dsd<MUL>(ss, sd, slope);
     }
     ds_dst[row * H + h] = dsd;
-  }
-}
-
-// ------------------------------------------------- backward GAT, pass 2 (CSC)
-// CSC entries in flight per stream: 4 with one stream per warp (D = 128);
-// 2 with two streams (D = 64: short columns, occupancy matters more)
-template <int D> struct ColU { static constexpr int v = D == 128 ? 4 : 2; };
-template <int D>
-__device__ __forceinline__ void gat_col_slice(int b, int e, int shift, int H,
-                                              const int* __restrict__ csc_pos,
-                                              const int* __restrict__ csc_row,
-                                              const float* __restrict__ alpha,
-                                              const float* __restrict__ dpre,
-                                              const float4* __restrict__ G, int lane,
-                                              float4* acc_out, float* dss_out) {
-  constexpr int LPR = D / 4;
-  constexpr int NS = 32 / LPR;
-  const int sl = lane % LPR, sid = lane / LPR;
-  const int h = sl / ((D / H) / 4);
-  constexpr int kColU = ColU<D>::v;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float dss = 0.f;
-  for (int base = b; base < e; base += 32) {
-    const int n = min(32, e - base);
-    int my_row = 0, my_pos = 0;
-    if (lane < n) {
-      my_row = __ldg(csc_row + base + lane);
-      my_pos = __ldg(csc_pos + base + lane);
-    }
-    int k = 0;
-    // kColU entries per stream in flight (a column's entries used to be
-    // one dependent L2 round trip each: the long columns set the tail)
-    for (; k + NS * kColU <= n; k += NS * kColU) {
-      float a[kColU], dp[kColU];
-      float4 g[kColU];
-#pragma unroll
-      for (int u = 0; u < kColU; u++) {
-        const int idx = k + u * NS + sid;
-        const int rr = __shfl_sync(0xffffffffu, my_row, idx);
-        const int p = __shfl_sync(0xffffffffu, my_pos, idx);
-        a[u] = __ldg(alpha + (long long)p * H + h);
-        dp[u] = __ldg(dpre + (long long)p * H + h);
-        g[u] = ldg4(G + (long long)(rr + shift) * LPR + sl);
-      }
-#pragma unroll
-      for (int u = 0; u < kColU; u++) {
-        dss += dp[u];
-        acc = f4fma(a[u], g[u], acc);
-      }
-    }
-    for (; k < n; k += NS) {
-      int idx = k + sid;
-      int src_lane = idx < n ? idx : 0;
-      int rr = __shfl_sync(0xffffffffu, my_row, src_lane);
-      int p = __shfl_sync(0xffffffffu, my_pos, src_lane);
-      if (idx < n) {
-        float a = __ldg(alpha + (long long)p * H + h);
-        dss += __ldg(dpre + (long long)p * H + h);
-        acc = f4fma(a, ldg4(G + (long long)(rr + shift) * LPR + sl), acc);
-      }
-    }
-  }
-#pragma unroll
-  for (int o = LPR; o < 32; o <<= 1) {
-    acc = f4add(acc, f4shfl_xor(acc, o));
-    dss += __shfl_xor_sync(0xffffffffu, dss, o);
-  }
-  *acc_out = acc;
-  *dss_out = dss;
-}
-
-// D = 64: one column per HALF warp (16 lanes x float4 = one row), so the two
-// halves walk two short columns independently (the one-column-per-warp form
-// split every column's 1-2 entries over two streams and left the warp count
-// at U).  Entries are summed in CSC order, as in gat_col_slice.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_agg_bwd_gat_cols_half(BwdMeta bm, int H, const int* __restrict__ U_dev,
-                        const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
-                        const int* __restrict__ csc_pos, const int* __restrict__ csc_row,
-                        const float* __restrict__ alpha, const float* __restrict__ dpre,
-                        const float4* __restrict__ G, float4* __restrict__ dY,
-                        float* __restrict__ ds_src, int* __restrict__ long_list,
-                        int* __restrict__ long_cnt, const float* __restrict__ att) {
-  constexpr int LPR = 16;                       // D = 64
-  __shared__ int s_yoff[HF_MAX_R + 1];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
-  const unsigned mask = 0xffffu << (16 * half);
-  const int u = (blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * 2 + half;
-  if (u >= *U_dev) return;
-  const int b = col_ptr[u], e = col_ptr[u + 1];
-  if (e - b > kLongCol) {
-    if (hl == 0) long_list[atomicAdd(long_cnt, 1)] = u;
-    return;
-  }
-  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
-  const int shift = bm.shift[r];
-  const int dh4 = (64 / H) / 4;
-  const int h = hl / dh4;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float dss = 0.f;
-  for (int base = b; base < e; base += 16) {
-    const int n = min(16, e - base);
-    int my_row = 0, my_pos = 0;
-    if (hl < n) {
-      my_row = __ldg(csc_row + base + hl);
-      my_pos = __ldg(csc_pos + base + hl);
-    }
-    int k = 0;
-    for (; k + 2 <= n; k += 2) {               // two entries in flight
-      const int rr0 = __shfl_sync(mask, my_row, k, 16), p0 = __shfl_sync(mask, my_pos, k, 16);
-      const int rr1 = __shfl_sync(mask, my_row, k + 1, 16);
-      const int p1 = __shfl_sync(mask, my_pos, k + 1, 16);
-      const float a0 = __ldg(alpha + (long long)p0 * H + h), d0 = __ldg(dpre + (long long)p0 * H + h);
-      const float a1 = __ldg(alpha + (long long)p1 * H + h), d1 = __ldg(dpre + (long long)p1 * H + h);
-      const float4 g0 = ldg4(G + (long long)(rr0 + shift) * LPR + hl);
-      const float4 g1 = ldg4(G + (long long)(rr1 + shift) * LPR + hl);
-      dss += d0;
-      acc = f4fma(a0, g0, acc);
-      dss += d1;
-      acc = f4fma(a1, g1, acc);
-    }
-    if (k < n) {
-      const int rr = __shfl_sync(mask, my_row, k, 16), p = __shfl_sync(mask, my_pos, k, 16);
-      dss += __ldg(dpre + (long long)p * H + h);
-      acc = f4fma(__ldg(alpha + (long long)p * H + h), ldg4(G + (long long)(rr + shift) * LPR + hl),
-                  acc);
-    }
-  }
-  if (att) acc = f4fma_into(dss, ldg4(reinterpret_cast<const float4*>(att + (long long)r * 2 * 64) + hl), acc);
-  dY[(long long)u * LPR + hl] = acc;
-  if (hl % dh4 == 0) ds_src[(long long)u * H + hl / dh4] = dss;
-}
-
-template <int D>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_agg_bwd_gat_cols(BwdMeta bm, int H, const int* __restrict__ U_dev,
-                   const int* __restrict__ rel_y_off, const int* __restrict__ col_ptr,
-                   const int* __restrict__ csc_pos, const int* __restrict__ csc_row,
-                   const float* __restrict__ alpha, const float* __restrict__ dpre,
-                   const float4* __restrict__ G, float4* __restrict__ dY,
-                   float* __restrict__ ds_src, int* __restrict__ long_list,
-                   int* __restrict__ long_cnt, const float* __restrict__ att) {
-  constexpr int LPR = D / 4;
-  __shared__ int s_yoff[HF_MAX_R + 1];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  int u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (u >= *U_dev) return;
-  const int b = col_ptr[u], e = col_ptr[u + 1];
-  if (e - b > kLongCol) {
-    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = u;
-    return;
-  }
-  const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
-  float4 acc;
-  float dss;
-  gat_col_slice<D>(b, e, bm.shift[r], H, csc_pos, csc_row, alpha, dpre, G, lane, &acc, &dss);
-  const int dh4 = (D / H) / 4;
-  if (lane < LPR) {
-    if (att) acc = f4fma_into(dss, ldg4(reinterpret_cast<const float4*>(att + (long long)r * 2 * D) + lane), acc);
-    dY[(long long)u * LPR + lane] = acc;
-    if (lane % dh4 == 0) ds_src[(long long)u * H + lane / dh4] = dss;
-  }
-}
-
-template <int D>
-__global__ void __launch_bounds__(kLongWarps * 32)
-k_agg_bwd_gat_cols_long(BwdMeta bm, int H, const int* __restrict__ rel_y_off,
-                        const int* __restrict__ col_ptr, const int* __restrict__ csc_pos,
-                        const int* __restrict__ csc_row, const float* __restrict__ alpha,
-                        const float* __restrict__ dpre, const float4* __restrict__ G,
-                        float4* __restrict__ dY, float* __restrict__ ds_src,
-                        const int* __restrict__ list, const int* __restrict__ cnt,
-                        const float* __restrict__ att) {
-  constexpr int LPR = D / 4;
-  __shared__ int s_yoff[HF_MAX_R + 1];
-  __shared__ float4 red[kLongWarps][LPR];
-  __shared__ float reds[kLongWarps][LPR];
-  for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int dh4 = (D / H) / 4;
-  const int n_long = *cnt;
-  for (int k = blockIdx.x; k < n_long; k += gridDim.x) {
-    const int u = list[k];
-    const int r = upper_bound_i(s_yoff, bm.R + 1, u) - 1;
-    const int b = col_ptr[u], e = col_ptr[u + 1];
-    const int per = (e - b + kLongWarps - 1) / kLongWarps;
-    const int wb = min(e, b + w * per), we = min(e, wb + per);
-    float4 acc;
-    float dss;
-    gat_col_slice<D>(wb, we, bm.shift[r], H, csc_pos, csc_row, alpha, dpre, G, lane, &acc, &dss);
-    if (lane < LPR) {
-      red[w][lane] = acc;
-      reds[w][lane] = dss;
-    }
-    __syncthreads();
-    if (w == 0 && lane < LPR) {
-      float4 t = red[0][lane];
-      float ts = reds[0][lane];
-      for (int q = 1; q < kLongWarps; q++) {
-        t = f4add(t, red[q][lane]);
-        ts += reds[q][lane];
-      }
-      if (att) t = f4fma_into(ts, ldg4(reinterpret_cast<const float4*>(att + (long long)r * 2 * D) + lane), t);
-      dY[(long long)u * LPR + lane] = t;
-      if (lane % dh4 == 0) ds_src[(long long)u * H + lane / dh4] = ts;
-    }
-    __syncthreads();
   }
 }
 
@@ -1373,14 +1311,12 @@ hifuse_status hifuse_aggregate_features_cols_bf16(const hifuse_layer_shape* shap
 size_t hifuse_aggregate_bwd_ws_bytes(const hifuse_layer_shape* shape, hifuse_agg agg, int heads) {
   LayerMeta m;
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
-  long long U_max = m.N < m.S ? m.N : m.S;
-  size_t b = carve_bytes(U_max + 1, 4) + carve_bytes(2, 4);
-  if (agg == HIFUSE_AGG_SUM || agg == HIFUSE_AGG_MEAN) {   // k_agg_bwd_e slots (D <= 128)
-    const long long nch = (m.N + 31) / 32;                  // chunks of >= 32 entries
-    b += carve_bytes(2 * nch * 128, 4) + carve_bytes(nch, 4);
-  }
+  // edge-balanced CSC pass: two partial slots (D <= 128 floats) per chunk,
+  // the chunk's head and tail columns
+  const long long nch = bwd_max_chunks(m.N);
+  size_t b = carve_bytes(2 * nch * 128, 4) + 2 * carve_bytes(nch, 4);
   if (agg == HIFUSE_AGG_GAT || agg == HIFUSE_AGG_GAT_XREL || agg == HIFUSE_AGG_GAT_MUL)
-    b += 2 * carve_bytes((long long)m.N * heads, 4);
+    b += carve_bytes(2 * nch * kGatDss, 4) + 2 * carve_bytes((long long)m.N * heads, 4);
   return b;
 }
 
@@ -1394,7 +1330,8 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   LayerMeta m;
   hifuse_status rc = make_meta(shape, &m);
   if (rc != HIFUSE_OK) return rc;
-  if (!csr || !csr->col_ptr || !csr->csc_row || !csr->U_dev || !csr->rel_y_off || !d_dY || !d_G)
+  if (!csr || !csr->col_ptr || !csr->csc_row || !csr->csc_col || !csr->U_dev || !csr->rel_y_off ||
+      !d_dY || !d_G)
     return HIFUSE_ERR_INVALID_ARG;
   if (D != 64 && D != 128) return HIFUSE_ERR_UNSUPPORTED;
   if (!aligned16(d_G) || !aligned16(d_dY)) return HIFUSE_ERR_ALIGNMENT;
@@ -1422,15 +1359,17 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
   // per-merged-row gradient (row_grad: HAN fusion, hifuse_aggregate_bwd_rows)
   for (int r = 0; r < m.R; r++)
     bm.shift[r] = row_grad ? 0 : m.type_dst_off[m.rel_dst[r]] - m.rel_row_off[r];
-  long long U_max = m.N < m.S ? m.N : m.S;
   char* p = (char*)d_ws;
-  int* long_list = carve<int>(p, U_max + 1);
-  int* long_cnt = carve<int>(p, 2);
-  cudaMemsetAsync(long_cnt, 0, sizeof(int), s);
-  unsigned gridU = ceil_div(U_max, kWarpsPerBlock);
   const int TB = kWarpsPerBlock * 32;
-  const unsigned gridL = 296;
+  // edge-balanced CSC pass: chunks of E entries, two partial slots per chunk
+  const int E = bwd_chunk_entries(m.N);
+  const long long nch = (m.N + E - 1) / E, nch_max = bwd_max_chunks(m.N);
+  const unsigned gridE = ceil_div(nch, kWarpsPerBlock);
+  float* part = carve<float>(p, 2 * nch_max * 128);
+  int* head_col = carve<int>(p, nch_max);
+  int* tail_col = carve<int>(p, nch_max);
   if (gat) {
+    float* part_dss = carve<float>(p, 2 * nch_max * kGatDss);
     float* alpha = carve<float>(p, (long long)m.N * heads);
     float* dpre = carve<float>(p, (long long)m.N * heads);
     unsigned gridR = ceil_div(m.rows, kWarpsPerBlock);
@@ -1451,38 +1390,26 @@ static hifuse_status aggregate_bwd_impl(const hifuse_layer_shape* shape, const h
               (long long)m.rows,                                                              \
               heads, slope, csr->row_ptr, csr->col, (const float4*)d_Y, d_s_src, d_s_dst,     \
               d_stats, (const float4*)d_G, alpha, dpre, d_ds_dst);                            \
-  if (DD == 64)                                                                                \
-    HF_LAUNCH(k_agg_bwd_gat_cols_half, ceil_div(U_max, kWarpsPerBlock * 2), TB, 0, s, bm, heads, \
-              csr->U_dev, csr->rel_y_off, csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre,\
-              (const float4*)d_G, (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att);        \
-  else                                                                                         \
-    HF_LAUNCH(k_agg_bwd_gat_cols<DD>, gridU, TB, 0, s, bm, heads, csr->U_dev, csr->rel_y_off, \
-              csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,      \
-              (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att);                           \
-  HF_LAUNCH(k_agg_bwd_gat_cols_long<DD>, gridL, kLongWarps * 32, 0, s, bm, heads, csr->rel_y_off,          \
-            csr->col_ptr, csr->csc_pos, csr->csc_row, alpha, dpre, (const float4*)d_G,        \
-            (float4*)d_dY, d_ds_src, long_list, long_cnt, d_att)
+  HF_LAUNCH(k_agg_bwd_gat_e<DD>, gridE, TB, 0, s, bm, heads, csr->rel_row_off, csr->rel_y_off,    \
+            (long long)m.N, csr->csc_col, csr->csc_pos, csr->csc_row, alpha, dpre, d_G, d_dY,   \
+            d_ds_src, (RowVec<DD>::T*)part, part_dss, head_col, tail_col, (int)nch, E, d_att);  \
+  HF_LAUNCH(k_agg_bwd_gat_fix<DD>, gridE, TB, 0, s, m.R, heads, csr->rel_y_off,                   \
+            (const RowVec<DD>::T*)part, part_dss, head_col, tail_col, d_dY, d_ds_src, (int)nch, \
+            d_att)
     const bool mul = agg == HIFUSE_AGG_GAT_MUL;
     if (D == 128) { if (mul) { HF_GAT(128, true); } else { HF_GAT(128, false); } }
     else { if (mul) { HF_GAT(64, true); } else { HF_GAT(64, false); } }
 #undef HF_GAT
   } else {
-    const int E = bwd_chunk_entries(m.N);
-    const long long nch = (m.N + E - 1) / E;
-    float* part = carve<float>(p, 2 * ((m.N + 31) / 32) * 128);
-    int* tail_col = carve<int>(p, (m.N + 31) / 32);
-    const unsigned gridE = ceil_div(nch, kWarpsPerBlock);
 #define HF_BWD(DD, MM)                                                                        \
   HF_LAUNCH((k_agg_bwd_e<DD, MM>), gridE, TB, 0, s, bm, csr->rel_row_off, csr->row_ptr,          \
-            csr->U_dev, csr->col_ptr, csr->csc_row, (const RowVec<DD>::T*)d_G,                  \
-            (RowVec<DD>::T*)d_dY, (RowVec<DD>::T*)part, tail_col, (int)nch, E);                    \
-  HF_LAUNCH((k_agg_bwd_fix<DD>), gridE, TB, 0, s, csr->col_ptr, (const RowVec<DD>::T*)part,      \
-            tail_col, (RowVec<DD>::T*)d_dY, (int)nch, E)
-    if (m.N > 0) {
-      bool mean = agg == HIFUSE_AGG_MEAN;
-      if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }
-      else { if (mean) { HF_BWD(64, true); } else { HF_BWD(64, false); } }
-    }
+            (long long)m.N, csr->csc_col, csr->csc_row, (const RowVec<DD>::T*)d_G,              \
+            (RowVec<DD>::T*)d_dY, (RowVec<DD>::T*)part, head_col, tail_col, (int)nch, E);       \
+  HF_LAUNCH((k_agg_bwd_fix<DD>), gridE, TB, 0, s, (const RowVec<DD>::T*)part, head_col,          \
+            tail_col, (RowVec<DD>::T*)d_dY, (int)nch)
+    bool mean = agg == HIFUSE_AGG_MEAN;
+    if (D == 128) { if (mean) { HF_BWD(128, true); } else { HF_BWD(128, false); } }
+    else { if (mean) { HF_BWD(64, true); } else { HF_BWD(64, false); } }
 #undef HF_BWD
   }
   return last_cuda();

@@ -74,7 +74,7 @@ struct BLayer {
   const long long* eid;
   // outputs
   int *o_rel_row_off, *row_ptr, *col, *eperm, *o_rel_y_off, *y_src, *col_ptr, *csc_pos,
-      *csc_row, *slot_y, *U_dev;
+      *csc_row, *csc_col, *slot_y, *U_dev;
   // workspace: zero zone
   int *cnt, *ccur;                     // cnt = [row counts | slot counts]
   int* lcnt;                           // [0] long rows, [1] long columns
@@ -209,6 +209,7 @@ __device__ __forceinline__ void place_entry(const BLayer& L, int row, int p, int
   const int w = L.col_ptr[c] + atomicAdd(L.ccur + c, 1);
   L.csc_pos[w] = p;
   L.csc_row[w] = row;
+  L.csc_col[w] = c;
 }
 
 // Block-wide sort of one segment [b, e) of (keys, vals): rank sort in shared
@@ -575,7 +576,7 @@ k_scatter(const __grid_constant__ BuildParams bp) {
     if (e < L.N && e >= nvalid) {      // tail positions [nvalid, N): one writer each
       L.eperm[e] = -1;
       L.col[e] = -1;
-      if (L.csc) { L.csc_pos[e] = -1; L.csc_row[e] = -1; }
+      if (L.csc) { L.csc_pos[e] = -1; L.csc_row[e] = -1; L.csc_col[e] = -1; }
     }
     if (key[q] < 0) continue;
     L.eperm[pos[q]] = e;
@@ -712,6 +713,7 @@ k_rows(const __grid_constant__ BuildParams bp) {
             const int w2 = cp[k] + ws[k];
             L.csc_pos[w2] = span_b + i0 + k * 32 + lane;
             L.csc_row[w2] = r0 + row[k];
+            L.csc_col[w2] = c[k];
           }
       }
     }
@@ -918,7 +920,7 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     if (!o.rel_row_off || !o.row_ptr || !o.rel_y_off || !o.U_dev ||
         (m.N > 0 && (!d_src_local[l] || !d_dst_local[l] || !d_edge_id[l] || !o.col ||
                      !o.eperm || !o.y_src)) ||
-        (!o.col_ptr != !o.csc_pos || !o.col_ptr != !o.csc_row) || (m.S > 0 && !o.slot_y))
+        (!o.col_ptr != !o.csc_pos || !o.col_ptr != !o.csc_row || !o.col_ptr != !o.csc_col) || (m.S > 0 && !o.slot_y))
       return HIFUSE_ERR_INVALID_ARG;
     if (m.N >= (1 << 30) || m.S >= (1 << 30)) return HIFUSE_ERR_UNSUPPORTED;   // status packing
   }
@@ -974,7 +976,7 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       L.eid = (const long long*)d_edge_id[l0 + q];
       L.o_rel_row_off = o.rel_row_off; L.row_ptr = o.row_ptr; L.col = o.col; L.eperm = o.eperm;
       L.o_rel_y_off = o.rel_y_off; L.y_src = o.y_src; L.col_ptr = o.col_ptr;
-      L.csc_pos = o.csc_pos; L.csc_row = o.csc_row; L.slot_y = o.slot_y; L.U_dev = o.U_dev;
+      L.csc_pos = o.csc_pos; L.csc_row = o.csc_row; L.csc_col = o.csc_col; L.slot_y = o.slot_y; L.U_dev = o.U_dev;
       const int et = m.N > 0 ? tiles(m.N, kEdgeTile) : 0;
       blocks[K_CLASSIFY][q] = et;
       blocks[K_SCAN][q] = L.t_rows + L.t_slots;

@@ -39,7 +39,7 @@ class LayerShape(ctypes.Structure):
 class Csr(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("rel_row_off", "row_ptr", "col", "eperm", "rel_y_off", "y_src", "col_ptr",
-                 "csc_pos", "csc_row", "slot_y", "U_dev")]
+                 "csc_pos", "csc_row", "csc_col", "slot_y", "U_dev")]
 
 
 class GraphCsc(ctypes.Structure):
@@ -204,9 +204,9 @@ class CsrBuffers:
         z = lambda n: torch.empty(n, dtype=torch.int32, device=device)
         self.t = dict(rel_row_off=z(R + 1), row_ptr=z(rows + 1), col=z(N), eperm=z(N),
                       rel_y_off=z(R + 1), y_src=z(umax), col_ptr=z(umax + 1), csc_pos=z(N),
-                      csc_row=z(N), slot_y=z(S), U_dev=z(1))
+                      csc_row=z(N), csc_col=z(N), slot_y=z(S), U_dev=z(1))
         if not csc:     # transpose not built (aggregate-first input layer)
-            for k in ("col_ptr", "csc_pos", "csc_row"):
+            for k in ("col_ptr", "csc_pos", "csc_row", "csc_col"):
                 self.t[k] = None
         self.c = Csr(**{k: (v.data_ptr() if v is not None else None) for k, v in self.t.items()})
 

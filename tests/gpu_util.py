@@ -42,13 +42,13 @@ def csr_host(sh, csr):
     return dict(U=U, rel_row_off=g("rel_row_off", sh.R + 1), row_ptr=g("row_ptr", sh.rows + 1),
                 col=g("col", sh.N), eperm=g("eperm", sh.N), rel_y_off=g("rel_y_off", sh.R + 1),
                 y_src=g("y_src", U), col_ptr=g("col_ptr", U + 1), csc_pos=g("csc_pos", sh.N),
-                csc_row=g("csc_row", sh.N), slot_y=g("slot_y", sh.S))
+                csc_row=g("csc_row", sh.N), csc_col=g("csc_col", sh.N), slot_y=g("slot_y", sh.S))
 
 
 def assert_build_equal(gpu, ref):
     assert gpu["U"] == ref["U"]
     for k in ("rel_row_off", "row_ptr", "col", "eperm", "rel_y_off", "y_src", "col_ptr",
-              "csc_pos", "csc_row", "slot_y"):
+              "csc_pos", "csc_row", "csc_col", "slot_y"):
         assert np.array_equal(gpu[k], np.asarray(ref[k])), k
 
 

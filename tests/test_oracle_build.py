@@ -91,6 +91,10 @@ def test_build_matches_bruteforce(seed):
     # csc_row is the merged row of each CSC entry
     row_of = np.repeat(np.arange(sh.rows), np.diff(c["row_ptr"]))
     assert np.array_equal(c["csc_row"], row_of[c["csc_pos"]])
+    # csc_col is the Y row of each CSC entry: the CSR column of its position
+    nv = int(c["col_ptr"][-1])
+    assert np.array_equal(c["csc_col"][:nv], c["col"][c["csc_pos"][:nv]])
+    assert (c["csc_col"][nv:] == -1).all()
     # partition invariant: multiset of (src, dst, relation) preserved
     r = et[blk.edge_id]
     got = sorted(zip(blk.src_local[c["eperm"]].tolist(), blk.dst_local[c["eperm"]].tolist(),
