@@ -177,10 +177,10 @@ def stage_cost(stage, l, cfg, sz):
 
 
 # main kernel of every library call (for the ncu traffic lookup)
-MAIN_KERNEL = {"aggregate_fwd": "k_agg_fwd", "aggregate_bwd": "k_agg_bwd_p", "project": "k_proj_fwd_tcp",
+MAIN_KERNEL = {"aggregate_fwd": "k_agg_fwd", "aggregate_bwd": "k_agg_bwd_e", "project": "k_proj_fwd_tcp",
                "project_wgrad": "k_wgrad_tc", "xent_wgrad": "k_head_grads",
                "project_bwd": "k_wgrad_tc", "fuse": "k_fuse", "fuse_bwd": "k_fuse_bwd_chunks",
-               "build": "k_sort_long", "xent": "k_head_grads", "aggregate_features": "k_agg_fwd",
+               "build": "k_rows", "xent": "k_head_grads", "aggregate_features": "k_agg_fwd",
                "project_aggregated": "k_proj_fwd_tcp", "project_aggregated_bwd": "k_wgrad_tc",
                "project_fuse_aggregated": "k_fuse_gemm_tcp"}
 
@@ -681,7 +681,7 @@ def main():
                        "project_wgrad")
         mk = MAIN_KERNEL.get(name, name)
         if name == "aggregate_bwd" and cfg.agg.startswith("gat"):
-            mk = "k_agg_bwd_gat_cols_half" if cfg.hidden == 64 else "k_agg_bwd_gat_cols"
+            mk = "k_agg_bwd_gat_e"
         if name == "aggregate_fwd" and cfg.agg.startswith("gat"):
             mk = ("k_agg_fwd_gat_xrel" if cfg.agg == "gat_xrel" else
                   "k_agg_fwd_gat_half" if cfg.hidden == 64 else "k_agg_fwd_gat")

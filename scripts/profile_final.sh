@@ -7,7 +7,7 @@ set -x
 OUT=gpurun_out/${PROF_OUT:-prof_r1c}
 mkdir -p $OUT
 for c in mag imdb; do
-  ncu --set full --import-source on --clock-control none -o /tmp/step_$c \
+  ncu -f --set full --import-source on --clock-control none -o /tmp/step_$c \
       python scripts/step_loop.py --config $c --steps 1 --pool 1 > $OUT/ncu_full_$c.log 2>&1
   ncu -i /tmp/step_$c.ncu-rep --page raw --csv > $OUT/step_full_$c.all.csv 2>/dev/null
   python scripts/ncu_table.py $OUT/step_full_$c.all.csv > $OUT/ncu_table_$c.md 2>&1

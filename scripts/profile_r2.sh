@@ -8,7 +8,7 @@ OUT=gpurun_out/${PROF_OUT:-prof_r2}
 mkdir -p $OUT
 for spec in "mag fp32" "mag bf16" "imdb fp32"; do
   set -- $spec
-  ncu --set full --import-source on --clock-control none -o /tmp/step_$1_$2 \
+  ncu -f --set full --import-source on --clock-control none -o /tmp/step_$1_$2 \
       python scripts/step_loop.py --config $1 --steps 1 --pool 1 --feat-dtype $2 --order $( [ $1 = imdb ] && echo project_first || echo agg_first ) > $OUT/ncu_full_$1_$2.log 2>&1
   ncu -i /tmp/step_$1_$2.ncu-rep --page raw --csv > $OUT/step_full_$1_$2.all.csv 2>/dev/null
   python scripts/ncu_table.py $OUT/step_full_$1_$2.all.csv > $OUT/ncu_table_$1_$2.md 2>&1

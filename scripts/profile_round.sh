@@ -7,7 +7,7 @@
 set -x
 OUT=gpurun_out/prof_${1:-r1}
 mkdir -p $OUT
-ncu --set full --import-source on --clock-control none -o /tmp/step_full \
+ncu -f --set full --import-source on --clock-control none -o /tmp/step_full \
     python scripts/step_loop.py --config mag --steps 1 --pool 1 > $OUT/ncu_full.log 2>&1
 ncu -i /tmp/step_full.ncu-rep --page raw --csv \
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct,launch__grid_size \

@@ -1,11 +1,11 @@
 #!/bin/bash
 # Profiling pass after the sampler / xent / xrel additions (writes gpurun_out/prof_r1b):
-#  ncu --set full of one mag step (traffic.json), launch lists of the step and
+#  ncu -f --set full of one mag step (traffic.json), launch lists of the step and
 #  of the GPU sampler, eager-step host profile, bench lines for all configs.
 set -x
 OUT=gpurun_out/prof_r1b
 mkdir -p $OUT
-ncu --set full --import-source on --clock-control none -o /tmp/step_full \
+ncu -f --set full --import-source on --clock-control none -o /tmp/step_full \
     python scripts/step_loop.py --config mag --steps 1 --pool 1 > $OUT/ncu_full.log 2>&1
 ncu -i /tmp/step_full.ncu-rep --page raw --csv \
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct,launch__grid_size \
