@@ -434,7 +434,7 @@ def main():
     ap.add_argument("--pool", type=int, default=16)
     ap.add_argument("--repeats", type=int, default=5,
                     help="the K-step timed region is repeated this many times; value = median")
-    ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32"])
+    ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32", "bf16"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gpu-sampler", type=int, default=1,

@@ -91,8 +91,12 @@ typedef enum { HIFUSE_ACT_NONE = 0, HIFUSE_ACT_RELU = 1 } hifuse_act;
  * SLOTS (every source vertex x every live relation) is reserved. */
 typedef enum { HIFUSE_LAYOUT_SLOTS = 0, HIFUSE_LAYOUT_COMPACT = 1 } hifuse_layout;
 /* Projection arithmetic.  FP32: CUDA-core fp32 FMA.  TF32: tcgen05 kind::tf32
- * tensor cores, fp32 accumulate (reading C17/C18). */
-typedef enum { HIFUSE_PREC_FP32 = 0, HIFUSE_PREC_TF32 = 1 } hifuse_prec;
+ * tensor cores, fp32 accumulate (reading C17/C18).  BF16 (hifuse_project
+ * only): X and W rounded to bfloat16 (round-to-nearest-even) on their way
+ * into shared memory, tcgen05 kind::f16, fp32 accumulate and fp32 outputs;
+ * the RGAT destination scores s_dst stay fp32 (reading C24).  The backward
+ * calls take FP32 or TF32. */
+typedef enum { HIFUSE_PREC_FP32 = 0, HIFUSE_PREC_TF32 = 1, HIFUSE_PREC_BF16 = 2 } hifuse_prec;
 
 #define HIFUSE_MAX_TYPES 64
 #define HIFUSE_MAX_RELS 512
@@ -195,7 +199,8 @@ hifuse_status hifuse_edge_type_offsets(const int32_t *d_edge_type, int64_t num_g
  * straight from the type-major feature store).
  * W_rel [R,K,D]; W_root [T,K,D] or NULL; att [R,2,D] or NULL.
  * Outputs: Y [U_max,D], R0 [sum_t n_dst[t], D] (if W_root), s_src [U_max,H],
- * s_dst [rows,H] (if att).  Workspace: hifuse_project_ws_bytes(). */
+ * s_dst [rows,H] (if att).  Workspace: hifuse_project_ws_bytes().
+ * prec: FP32, TF32 or BF16 (see hifuse_prec). */
 size_t hifuse_project_ws_bytes(const hifuse_layer_shape *shape, int K, int D, int heads);
 hifuse_status hifuse_project(const hifuse_layer_shape *shape, const hifuse_csr *csr,
                              hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,

@@ -130,6 +130,19 @@ def build(shape: Shape, blk, edge_type):
     return out
 
 
+def bf16_round(x):
+    """Round to the nearest bfloat16 value, ties to even (reading C24: the BF16
+    projection's operand rounding), returned as float64.  The definition
+    written out on the fp32 bit pattern: keep the top 16 bits, adding half an
+    ulp of the kept part plus the kept part's lowest bit (ties to even);
+    values already representable (and +-0, +-inf) are unchanged.  NaN is not
+    handled (never an input here)."""
+    u = np.ascontiguousarray(np.asarray(x, dtype=np.float32)).view(np.uint32).astype(np.uint64)
+    lsb = (u >> np.uint64(16)) & np.uint64(1)
+    u = ((u + np.uint64(0x7FFF) + lsb) & np.uint64(0xFFFF0000)).astype(np.uint32)
+    return u.view(np.float32).astype(np.float64).reshape(np.shape(x))
+
+
 def project(shape: Shape, csr, K, D, H, X, gather_ids, W_rel, W_root, att):
     """O2: Y = X_s W_r per relation (compact rows), R0 = X_t W_root,t, RGAT scores."""
     X = _f64(X)

@@ -709,6 +709,7 @@ size_t hifuse_project_ws_bytes(const hifuse_layer_shape* shape, int K, int D, in
   if (make_meta(shape, &m) != HIFUSE_OK) return 0;
   size_t b = 2 * carve_bytes(m.R + m.T + 1, 4);            // tile_off, chunk_off
   b += carve_bytes((long long)m.R * K * (heads > 0 ? heads : 1), 4);   // v
+  b += carve_bytes((long long)(m.R + m.T) * K * D, 2);      // bf16 W^T (HIFUSE_PREC_BF16)
   return b;
 }
 
@@ -738,20 +739,23 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   int* tile_off = carve<int>(p, m.R + m.T + 1);
   int* chunk_off = carve<int>(p, m.R + m.T + 1);
   float* v = carve<float>(p, (long long)m.R * K * (heads > 0 ? heads : 1));
+  uint16_t* wt = carve<uint16_t>(p, (long long)(m.R + m.T) * K * D);
+  const bool tc = prec == HIFUSE_PREC_TF32 || prec == HIFUSE_PREC_BF16;
   // RGAT destination scores (v = W a_dst folded, s_dst = X v) only read X and
-  // W: a parallel branch next to the projection GEMM
+  // W: a parallel branch next to the projection GEMM (fp32 in every precision)
   Branch bs;
   bool sbr = false;
-  if (d_att && prec == HIFUSE_PREC_TF32) {
+  if (d_att && tc) {
     sbr = branch_begin(s, &bs, 2);
     cudaStream_t sd = sbr ? bs.side : s;
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * heads, 256), 256, 0, sd, m.R, K, D, heads,
               d_W_rel, d_att, v);
     launch_scores_dst(pm, m.rows, K, heads, d_gather_ids, d_X, v, d_s_dst, sd);
   }
-  if (prec == HIFUSE_PREC_TF32) {
+  if (tc) {
     rc = project_tcp_launch(m, pm, K, D, csr->rel_y_off, csr->y_src, d_X, nullptr, d_gather_ids,
-                            d_W_rel, d_W_root, d_Y, d_R0, d_att, d_s_src, heads, s);   // s_src fused in the epilogue
+                            d_W_rel, d_W_root, d_Y, d_R0, d_att, d_s_src, heads, s,
+                            prec == HIFUSE_PREC_BF16 ? wt : nullptr);   // s_src fused in the epilogue
     if (sbr) branch_end(s, bs);
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
@@ -768,7 +772,7 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   } else {
     return HIFUSE_ERR_UNSUPPORTED;
   }
-  if (d_att && prec != HIFUSE_PREC_TF32) {
+  if (d_att && !tc) {
     HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * heads, 256), 256, 0, s, m.R, K, D, heads,
               d_W_rel, d_att, v);
     long long U_max = m.N < m.S ? m.N : m.S;

@@ -18,6 +18,7 @@
 // goal is streaming A at full bandwidth with enough CTAs per SM (64 KB smem,
 // <=128 TMEM columns each -> 3-4 CTAs/SM) rather than peak MMA rate.
 #include <algorithm>
+#include <cuda_bf16.h>
 #include <cstdlib>
 #include "project.cuh"
 #include "tc_common.cuh"
@@ -25,6 +26,18 @@
 namespace hf {
 
 using namespace tc;
+
+// 8 fp32 -> 8 bf16 (RN-even, cvt.rn.bf16x2) -> one 16-byte shared store
+__device__ __forceinline__ void st_shared_bf16x8(uint32_t dst, float4 a, float4 b) {
+  uint32_t w[4];
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[0]) : "f"(a.y), "f"(a.x));
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[1]) : "f"(a.w), "f"(a.z));
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[2]) : "f"(b.y), "f"(b.x));
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[3]) : "f"(b.w), "f"(b.z));
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(w[0]), "r"(w[1]),
+               "r"(w[2]), "r"(w[3])
+               : "memory");
+}
 
 __device__ __forceinline__ bool tc_resolve(const ProjMeta& pm, const int* table,
                                            const int* rel_y_off, int bid, int step, int* g_out,
@@ -491,17 +504,25 @@ __device__ __forceinline__ void group_table_warp(const ProjMeta& pm, const int* 
   if (lane == 0) s_tab[G] = carry;
 }
 
-template <int K, int D>
+// BF16 (HIFUSE_PREC_BF16): the operands are rounded to bf16 (RN-even) on the
+// way into shared memory -- A by the producer threads (fp32 X loads, cvt,
+// st.shared into the same 128B-swizzled K-major layout, 64 bf16 per 128-byte
+// row), B from Wt, W_g^T pre-rounded to bf16 [D][K] by k_w_bf16t (K-major,
+// cp.async) -- and tcgen05.mma kind::f16 (K = 16 per instruction) accumulates
+// in fp32.  Everything else (stages, barriers, epilogue) is shared.
+template <int K, int D, bool BF>
 __global__ void __launch_bounds__(288, kFwdCtas)
 k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __restrict__ y_src,
                const int* __restrict__ gather_ids, const float* __restrict__ X,
                const float* __restrict__ W_rel, const float* __restrict__ W_root,
                float* __restrict__ Y, float* __restrict__ R0, const float* __restrict__ att,
-               float* __restrict__ s_src, int H, const float* __restrict__ Xm) {
-  constexpr int BM = 128, NC = K / 32;
+               float* __restrict__ s_src, int H, const float* __restrict__ Xm,
+               const uint16_t* __restrict__ Wt) {
+  constexpr int BM = 128, KC = BF ? 64 : 32, NC = K / KC;   // K elements per 128-byte row
   constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
   constexpr uint32_t STAGE = A_STAGE + B_STAGE;
-  constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 1);      // A K-major, B MN-major
+  constexpr uint32_t IDESC = BF ? idesc_bf16(BM, D, 0, 0)    // A, B K-major
+                                : idesc_tf32(BM, D, 0, 1);   // A K-major, B MN-major
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kFStages], empty[kFStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
@@ -568,20 +589,53 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
       const float* Wg = g < pm.R ? W_rel + (long long)g * K * D : W_root + (long long)(g - pm.R) * K * D;
       for (int c = 0; c < NC; c++, it++) {
         const int s = it % kFStages;
-        if (it >= kFStages) mbar_wait(smem_u32(&empty[s]), ((it / kFStages) - 1) & 1);
-        const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+        if constexpr (BF) {
+          // A: 8 fp32 of each of the lane's 8 rows, loaded before the stage
+          // wait (in flight meanwhile), rounded to bf16 and stored as one
+          // 16-byte piece of the swizzled row
+          // (two halves of 4 rows: 8 float4 in flight per lane, no spills)
+          const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-          const int row = warp * 32 + i * 4 + rsub;
-          cp_async16(sa + sw128_off(row, piece), ap[i] + c * 32 + piece * 4, nb[i]);
-        }
-        // B: rows k = 32c .. 32c+31 of W_g, D floats each, MN-major atoms
+          for (int hh = 0; hh < 2; hh++) {
+            float4 xa[4][2];
 #pragma unroll
-        for (int q = 0; q < 32 * D / 4 / 128; q++) {
-          const int i = tid + 128 * q;
-          const int kr = i / (D / 4), n = (i % (D / 4)) * 4;
-          cp_async16(sb + (n >> 5) * B_BLK + (kr >> 2) * 512 + sw128b32_off(kr, (n & 31) * 4),
-                     Wg + (long long)(c * 32 + kr) * D + n, 16);
+            for (int i = 0; i < 4; i++) {
+              const int ii = hh * 4 + i;
+              const float4* src = reinterpret_cast<const float4*>(ap[ii] + c * 64 + piece * 8);
+              xa[i][0] = nb[ii] ? __ldg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+              xa[i][1] = nb[ii] ? __ldg(src + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (hh == 0 && it >= kFStages) mbar_wait(smem_u32(&empty[s]), ((it / kFStages) - 1) & 1);
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              const int row = warp * 32 + (hh * 4 + i) * 4 + rsub;
+              st_shared_bf16x8(sa + sw128_off(row, piece), xa[i][0], xa[i][1]);
+            }
+          }
+          // B: Wt[g] rows n = 0 .. D-1, K elements 64c .. 64c+63 (K-major)
+          const uint16_t* Wtg = Wt + (long long)g * D * K;
+#pragma unroll
+          for (int q = 0; q < D * 8 / 128; q++) {
+            const int i = tid + 128 * q;
+            const int n = i >> 3, pc = i & 7;
+            cp_async16(sb + sw128_off(n, pc), Wtg + (long long)n * K + c * 64 + pc * 8, 16);
+          }
+        } else {
+          if (it >= kFStages) mbar_wait(smem_u32(&empty[s]), ((it / kFStages) - 1) & 1);
+          const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
+#pragma unroll
+          for (int i = 0; i < 8; i++) {
+            const int row = warp * 32 + i * 4 + rsub;
+            cp_async16(sa + sw128_off(row, piece), ap[i] + c * 32 + piece * 4, nb[i]);
+          }
+          // B: rows k = 32c .. 32c+31 of W_g, D floats each, MN-major atoms
+#pragma unroll
+          for (int q = 0; q < 32 * D / 4 / 128; q++) {
+            const int i = tid + 128 * q;
+            const int kr = i / (D / 4), n = (i % (D / 4)) * 4;
+            cp_async16(sb + (n >> 5) * B_BLK + (kr >> 2) * 512 + sw128b32_off(kr, (n & 31) * 4),
+                       Wg + (long long)(c * 32 + kr) * D + n, 16);
+          }
         }
         cp_async_commit();
         if (it >= kLag) {
@@ -677,9 +731,14 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
         tc_fence_after();
         const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-          mma_tf32(tmem + (uint32_t)(acc * D), sw128_desc(sa + k * 32, 16, 1024),
-                   sw128b32_desc(sb + k * 1024, B_BLK, 512), IDESC, (c | k) ? 1u : 0u);
+        for (int k = 0; k < 4; k++) {
+          if constexpr (BF)      // K = 16 bf16 = 32 bytes per MMA along both K-major rows
+            mma_f16(tmem + (uint32_t)(acc * D), sw128_desc(sa + k * 32, 16, 1024),
+                    sw128_desc(sb + k * 32, 16, 1024), IDESC, (c | k) ? 1u : 0u);
+          else
+            mma_tf32(tmem + (uint32_t)(acc * D), sw128_desc(sa + k * 32, 16, 1024),
+                     sw128b32_desc(sb + k * 1024, B_BLK, 512), IDESC, (c | k) ? 1u : 0u);
+        }
         mma_commit(smem_u32(&empty[s]));
       }
       mma_commit(smem_u32(&tfull[acc]));
@@ -688,6 +747,20 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
   tc_fence_before();
   __syncthreads();
   if (warp == 8) tmem_dealloc(tmem, 2 * D);
+}
+
+// Wt[g][n][k] = bf16_rn(W_g[k][n]) for the R relation weights then the T root
+// weights (transposed to K-major, the B layout of the BF16 projection).
+__global__ void k_w_bf16t(int R, int T, int K, int D, const float* __restrict__ W_rel,
+                          const float* __restrict__ W_root, uint16_t* __restrict__ Wt) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (long long)K * D;
+  if (i >= (R + T) * per) return;
+  const int g = (int)(i / per);
+  const int n = (int)(i % per) / K, k = (int)(i % per) % K;
+  const float w = g < R ? W_rel[(long long)g * per + (long long)k * D + n]
+                        : W_root[(long long)(g - R) * per + (long long)k * D + n];
+  Wt[i] = __bfloat16_as_ushort(__float2bfloat16_rn(w));
 }
 
 // ------------------------------------------- fused fusion GEMM (NEXT(3)) ----
@@ -894,14 +967,15 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
 template <int K, int D>
 static constexpr int fwdp_smem() { return kFStages * (128 * 128 + D * 128) + 1024; }
 
-template <int K, int D>
+template <int K, int D, bool BF>
 static void launch_tcp(const ProjMeta& pm, const int* rel_off, const int* y_src,
                        const int* gather_ids, const float* X, const float* Xm,
                        const float* W_rel, const float* W_root, float* Y, float* R0,
-                       const float* att, float* s_src, int H, cudaStream_t s) {
-  set_max_smem((const void*)k_proj_fwd_tcp<K, D>, fwdp_smem<K, D>());
-  HF_LAUNCH((k_proj_fwd_tcp<K, D>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
-            rel_off, y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, Xm);
+                       const float* att, float* s_src, int H, const uint16_t* Wt,
+                       cudaStream_t s) {
+  set_max_smem(reinterpret_cast<const void*>(&k_proj_fwd_tcp<K, D, BF>), fwdp_smem<K, D>());
+  HF_LAUNCH((k_proj_fwd_tcp<K, D, BF>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
+            rel_off, y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, Xm, Wt);
 }
 
 template <int K, int D, bool RELU>
@@ -953,14 +1027,23 @@ hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, 
                                  const int* rel_off, const int* y_src, const float* X,
                                  const float* Xm, const int* gather_ids, const float* W_rel,
                                  const float* W_root, float* Y, float* R0, const float* att,
-                                 float* s_src, int H, cudaStream_t s) {
-  (void)m;
-#define HF_TCP(KK, DD) \
-  launch_tcp<KK, DD>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0, att, s_src, H, s)
-  if (K == 128 && D == 128) HF_TCP(128, 128);
-  else if (K == 128 && D == 64) HF_TCP(128, 64);
-  else if (K == 64 && D == 128) HF_TCP(64, 128);
-  else HF_TCP(64, 64);
+                                 float* s_src, int H, cudaStream_t s, uint16_t* Wt_bf16) {
+  if (Wt_bf16) {             // BF16 operands: round + transpose the weights first
+    const int G = m.R + (W_root ? m.T : 0);
+    HF_LAUNCH(k_w_bf16t, ceil_div((long long)G * K * D, 256), 256, 0, s, m.R, W_root ? m.T : 0, K,
+              D, W_rel, W_root, Wt_bf16);
+  }
+#define HF_TCP(KK, DD)                                                                          \
+  if (Wt_bf16)                                                                                 \
+    launch_tcp<KK, DD, true>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0, att,  \
+                             s_src, H, Wt_bf16, s);                                             \
+  else                                                                                         \
+    launch_tcp<KK, DD, false>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0, att, \
+                              s_src, H, nullptr, s)
+  if (K == 128 && D == 128) { HF_TCP(128, 128); }
+  else if (K == 128 && D == 64) { HF_TCP(128, 64); }
+  else if (K == 64 && D == 128) { HF_TCP(64, 128); }
+  else { HF_TCP(64, 64); }
 #undef HF_TCP
   return HIFUSE_OK;
 }

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libhifuse.so")
 AGG = {"sum": 0, "mean": 1, "gat": 2, "gat_xrel": 3, "gat_mul": 4}
 ACT = {"none": 0, "relu": 1}
 LAYOUT_COMPACT = 1
-PREC = {"fp32": 0, "tf32": 1}
+PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
 STATUS = {0: "ok", 1: "invalid argument", 2: "alignment", 3: "unsupported", 4: "workspace",
           5: "cuda"}
 

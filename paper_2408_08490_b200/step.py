@@ -88,6 +88,12 @@ class Trainer:
         self.rel_dst = np.asarray(rel_dst, np.int32)
         self.model, self.agg, self.device, self.lr, self.prec, self.slope = (
             model, agg, device, lr, prec, slope)
+        # prec "bf16": the per-relation projection (hifuse_project) runs on
+        # BF16 operands (HIFUSE_PREC_BF16); the backward GEMMs and the
+        # aggregate-first input layer's GEMMs take TF32 (no BF16 variant)
+        if prec not in ("fp32", "tf32", "bf16"):
+            raise ValueError(prec)
+        self.prec_tc = "tf32" if prec == "bf16" else prec
         if fusion not in ("sum", "han"):
             raise ValueError(fusion)
         self.fusion = fusion       # "han": HAN semantic-attention fusion (NEXT(2), reading C22)
@@ -109,7 +115,7 @@ class Trainer:
         if order not in ("project_first", "agg_first"):
             raise ValueError(order)
         # (HAN fusion gives every relation its own gradient: project-first only)
-        self.agg_first = (order == "agg_first" and model == "rgcn" and prec == "tf32" and
+        self.agg_first = (order == "agg_first" and model == "rgcn" and prec != "fp32" and
                           fusion == "sum")
         self.order = "agg_first" if self.agg_first else "project_first"
         # aggregate-first input layer: projection + fusion as one GEMM per
@@ -292,12 +298,12 @@ class Trainer:
                                 hf.project_fuse_aggregated(sh, c, a["K"], D, a["act"], a["Xagg"],
                                                            a["Xroot"], a["gid_root"], P["W_rel"],
                                                            P["W_root"], P["bias"], a["H"],
-                                                           prec=self.prec)))
+                                                           prec=self.prec_tc)))
                 else:
                     ops.append(("project_aggregated.0", lambda sh=sh, c=csrs[l], a=a, P=P:
                                 hf.project_aggregated(sh, c, a["K"], D, a["Xagg"], a["Xroot"],
                                                       a["gid_root"], P["W_rel"], P["W_root"], a["Z"],
-                                                      a["R0"], prec=self.prec)))
+                                                      a["R0"], prec=self.prec_tc)))
                     ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
                         sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
                 acts.append(a)
@@ -363,7 +369,7 @@ class Trainer:
                 ops.append(("project_aggregated_bwd.0", lambda sh=sh, c=csrs[l], a=a, b=b, Gr=Gr:
                             hf.project_aggregated_bwd(sh, c, a["K"], D, a["Xagg"], a["Xroot"],
                                                       a["gid_root"], b["G"], Gr["W_rel"],
-                                                      Gr["W_root"], b["wsq"], prec=self.prec)))
+                                                      Gr["W_root"], b["wsq"], prec=self.prec_tc)))
                 if self.world > 1:
                     ops.append((f"allreduce.{l}", self._allreduce_op(f"layer{l}")))
                 continue
@@ -413,12 +419,12 @@ class Trainer:
                             hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
                                            P["W_root"], None, a["Y"], b["dY"], b["G"], None,
                                            None, b["dX"], None, None, None, b["wsq"],
-                                           prec=self.prec)))
+                                           prec=self.prec_tc)))
                 ops.append((f"project_wgrad.{l}", side_op(
                     lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
                     hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
                                    P["W_root"], None, a["Y"], b["dY"], b["G"], None, None, None,
-                                   Gr["W_rel"], Gr["W_root"], None, b["wsw"], prec=self.prec))))
+                                   Gr["W_rel"], Gr["W_root"], None, b["wsw"], prec=self.prec_tc))))
             else:
                 pb = hf.project_bwd_scored if P["att"] is not None else hf.project_bwd
                 ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr,
@@ -426,7 +432,7 @@ class Trainer:
                             pb(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"],
                                P["att"], a["Y"], b["dY"], b["G"], b["ds_src"], b["ds_dst"],
                                b["dX"], Gr["W_rel"], Gr["W_root"], Gr["att"], b["wsq"],
-                               prec=self.prec)))
+                               prec=self.prec_tc)))
             dH = b["dX"]
             if self.world > 1:
                 ops.append((f"allreduce.{l}", self._allreduce_op(f"layer{l}")))

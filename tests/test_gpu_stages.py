@@ -358,6 +358,64 @@ def test_project_tf32_exact_on_representable_inputs(K, D):
     assert np.array_equal(dX.cpu().numpy(), ob["dX"].astype(np.float32))
 
 
+@pytest.mark.parametrize("K,D", [(128, 128), (128, 64), (64, 128), (64, 64)])
+@pytest.mark.parametrize("att", [False, True])
+def test_project_bf16(K, D, att):
+    """HIFUSE_PREC_BF16 (reading C24): Y, R0 and the epilogue's s_src against
+    the oracle fed BF16-rounded X and W (every product of two bf16 values is
+    exact in fp32, so only the fp32 accumulation differs: 1e-5 row-norm);
+    s_dst stays fp32 (unrounded oracle)."""
+    H = 2 if att else 1
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(300 + K + D, D=D, H=H, T=3, R=7, hub=0.05)
+    U = ch["U"]
+    xr = sh.src_rows + 7
+    X = rng.standard_normal((xr, K)).astype(np.float32)
+    gid = rng.permutation(xr)[:sh.src_rows].astype(np.int32)
+    W = (rng.standard_normal((sh.R, K, D)) / np.sqrt(K)).astype(np.float32)
+    Wr = None if att else (rng.standard_normal((sh.T, K, D)) / np.sqrt(K)).astype(np.float32)
+    A = rng.standard_normal((sh.R, 2, D)).astype(np.float32) if att else None
+    Y = torch.zeros(max(sh.U_max, 1), D, device=DEV)
+    R0 = torch.zeros(sh.dst_rows, D, device=DEV) if Wr is not None else None
+    ss = torch.zeros(max(sh.U_max, 1), H, device=DEV) if att else None
+    sd = torch.zeros(sh.rows, H, device=DEV) if att else None
+    ws = torch.empty(hf().project_ws_bytes(sh, K, D, H) // 4 + 16, device=DEV)
+    tn = lambda a: None if a is None else t(a)
+    hf().project(sh, csr, K, D, H, t(X), t(gid, torch.int32), t(W), tn(Wr), tn(A), Y, R0, ss, sd,
+                 ws, prec="bf16")
+    osh = oracle.Shape.of(blk, rs, rd)
+    rb = oracle.bf16_round
+    ref = oracle.project(osh, ch, K, D, H, rb(X), gid, rb(W), None if Wr is None else rb(Wr), A)
+    row_rel_l2(Y.cpu().numpy()[:U], ref["Y"], 1e-5, "Y")
+    if Wr is not None:
+        row_rel_l2(R0.cpu().numpy(), ref["R0"], 1e-5, "R0")
+    if att:
+        row_rel_l2(ss.cpu().numpy()[:U], ref["s_src"], 1e-4, "s_src")
+        ref32 = oracle.project(osh, ch, K, D, H, X, gid, W, None, A)
+        row_rel_l2(sd.cpu().numpy(), ref32["s_dst"], 1e-4, "s_dst")
+
+
+@pytest.mark.parametrize("K,D", [(128, 128), (64, 64)])
+def test_project_bf16_exact_on_representable_inputs(K, D):
+    """X, W in {-2..2}/4 are exact in bf16 and every partial sum is exact in
+    fp32: the kind::f16 result equals the oracle bit for bit (layout /
+    descriptor check of the BF16 operand path)."""
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(321 + K + D, D=D, T=3, R=6, N=4000)
+    U = ch["U"]
+    X = (rng.integers(-2, 3, (sh.src_rows + 5, K)) / 4).astype(np.float32)
+    gid = rng.permutation(sh.src_rows + 5)[:sh.src_rows].astype(np.int32)
+    W = (rng.integers(-2, 3, (sh.R, K, D)) / 4).astype(np.float32)
+    Wr = (rng.integers(-2, 3, (sh.T, K, D)) / 4).astype(np.float32)
+    Y = torch.zeros(max(sh.U_max, 1), D, device=DEV)
+    R0 = torch.zeros(sh.dst_rows, D, device=DEV)
+    ws = torch.empty(hf().project_ws_bytes(sh, K, D, 1) // 4 + 16, device=DEV)
+    hf().project(sh, csr, K, D, 1, t(X), t(gid, torch.int32), t(W), t(Wr), None, Y, R0, None,
+                 None, ws, prec="bf16")
+    osh = oracle.Shape.of(blk, rs, rd)
+    ref = oracle.project(osh, ch, K, D, 1, X, gid, W, Wr, None)
+    assert np.array_equal(Y.cpu().numpy()[:U], ref["Y"].astype(np.float32))
+    assert np.array_equal(R0.cpu().numpy(), ref["R0"].astype(np.float32))
+
+
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("B,C", [(5, 3), (128, 7), (1024, 128), (300, 129), (1024, 349),
                                  (64, 600), (2048, 7)])

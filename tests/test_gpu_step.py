@@ -41,7 +41,8 @@ def rel_l2(a, b):
 
 
 @pytest.mark.parametrize("prec,order", [("fp32", "project_first"), ("tf32", "project_first"),
-                                        ("tf32", "agg_first"), ("tf32", "agg_first_bf16")])
+                                        ("tf32", "agg_first"), ("tf32", "agg_first_bf16"),
+                                        ("bf16", "project_first")])
 @pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag", "imdb_xrel",
                                  "freebase_xrel", "imdb_mul", "freebase_mul", "imdb_han",
                                  "dblp_han", "freebase_han"])
@@ -59,6 +60,9 @@ def test_step_matches_oracle(key, prec, order):
     if bf16 and (cfg.model != "rgcn" or fusion != "sum"):
         pytest.skip("the BF16 feature store needs the aggregate-first RGCN input layer")
     order = "agg_first" if bf16 else order
+    if prec == "bf16" and fusion == "han":
+        pytest.skip("HAN's semantic-attention adjoint amplifies the BF16 operand error past "
+                    "any useful bound (DESIGN.md §5); HAN is checked in fp32 and tf32")
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, DEV, lr=0.0, prec=prec,
                  order=order, fusion=fusion, feat_dtype="bf16" if bf16 else "fp32")
@@ -87,6 +91,12 @@ def test_step_matches_oracle(key, prec, order):
     # 5 u x 4 (conditioning) = 2e-2 there; the GEMM kernels themselves are
     # pinned bit-exact on TF32-representable inputs (test_gpu_stages).
     ltol, tol, htol = (1e-5, 2e-4, 1e-5) if prec == "fp32" else (2e-3, 2e-2, 5e-3)
+    if prec == "bf16":
+        # BF16 projection operands against the unrounded fp64 oracle: u = 2^-8
+        # per operand rounding (~u on H and the loss, the weight
+        # gradients behind two BF16 forward GEMMs and the TF32 backward chain
+        # ~10 u)
+        ltol, tol, htol = 1e-2, 5e-2, 2e-2
     assert abs(float(loss.item()) - fw["loss"]) <= ltol * max(1.0, abs(fw["loss"]))
     checks = [("Wc", gr["Wc"]), ("bc", gr["bc"])]
     for l in range(cfg.num_layers):
@@ -101,7 +111,7 @@ def test_step_matches_oracle(key, prec, order):
         # TF32 errors of the chain above are amplified by |dbeta| / |dw|
         # (~5x measured on IMDB); the same gradients are checked at 2e-4 in
         # fp32
-        t_ = 0.1 if (prec == "tf32" and key.endswith("_han")) else tol
+        t_ = 0.1 if (prec != "fp32" and key.endswith("_han")) else tol
         assert err <= t_, f"{key} grad {name}: rel L2 {err:.3e}"
     # logits-level: the last layer's H on the seeds
     last = tr.last["acts"][-1]["H"][db.h_row0:db.h_row0 + db.B].cpu().numpy()
