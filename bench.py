@@ -265,6 +265,7 @@ def config_obj(cfg, args, extra=None):
          "aggregation": cfg.agg,
          "fusion": getattr(args, "fusion", "sum"),
          "feature_storage": getattr(args, "feat_dtype", "fp32"),
+         "y_storage": getattr(args, "y_dtype", "fp32"),
          "l2": "inputs larger than L2: a pool of distinct sampled batches, per-step working "
                "set above the 126 MB L2 for mag"}
     if extra:
@@ -456,6 +457,9 @@ def main():
     ap.add_argument("--feat-dtype", default="fp32", choices=["fp32", "bf16"],
                     help="storage of the input feature store: fp32, or BF16 read by the "
                          "aggregate-first input layer (NEXT(3) byte diet; fp32 accumulation)")
+    ap.add_argument("--y-dtype", default="fp32", choices=["fp32", "bf16"],
+                    help="storage of the projected Y of the RGCN project-first layers: fp32, "
+                         "or BF16 (NEXT(3) byte diet, reading C25; fp32 accumulation)")
     ap.add_argument("--fusion", default="sum", choices=["sum", "han"],
                     help="semantic fusion: plain sum over relations (reading C2/C4, default) or "
                          "HAN semantic attention (C22, NEXT(2))")
@@ -516,7 +520,7 @@ def main():
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
                  prec=args.prec, order=args.order, fusion=args.fusion,
-                 feat_dtype=args.feat_dtype)
+                 feat_dtype=args.feat_dtype, y_dtype=args.y_dtype)
     tr.load_params(params)
     tr.prepare_graph(et_d)           # relation-major edge ids -> R+1 offsets (once per graph)
     # N > 1: per-layer bucketed all-reduce on a comm stream inside the step

@@ -202,6 +202,18 @@ hifuse_status hifuse_edge_type_offsets(const int32_t *d_edge_type, int64_t num_g
  * s_dst [rows,H] (if att).  Workspace: hifuse_project_ws_bytes().
  * prec: FP32, TF32 or BF16 (see hifuse_prec). */
 size_t hifuse_project_ws_bytes(const hifuse_layer_shape *shape, int K, int D, int heads);
+/* hifuse_project for RGCN (no attention) with Y stored as bfloat16 (RN-even
+ * rounding of the fp32 accumulator; SURVEY §8(f) NEXT(3) "BF16 storage of Y",
+ * reading C25): d_Yb [U_max, D] bf16, 16-byte aligned; R0 fp32.  prec TF32
+ * or BF16 (tcgen05 paths); FP32 -> HIFUSE_ERR_UNSUPPORTED.  The aggregation
+ * then reads Y through hifuse_aggregate_features_cols_bf16 with d_col_x =
+ * csr->col (Z[(r,i)] = sum_p w_p Y[col[p]]).  Workspace as hifuse_project. */
+hifuse_status hifuse_project_y16(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                 hifuse_layout layout, hifuse_prec prec, int K, int D,
+                                 const float *d_X, int64_t x_rows, const int32_t *d_gather_ids,
+                                 const float *d_W_rel, const float *d_W_root, uint16_t *d_Yb,
+                                 float *d_R0, void *d_ws, size_t ws_bytes,
+                                 hifuse_stream_t stream);
 hifuse_status hifuse_project(const hifuse_layer_shape *shape, const hifuse_csr *csr,
                              hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
                              const float *d_X, int64_t x_rows, const int32_t *d_gather_ids,

@@ -713,24 +713,28 @@ size_t hifuse_project_ws_bytes(const hifuse_layer_shape* shape, int K, int D, in
   return b;
 }
 
-hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* csr,
-                             hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
-                             const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
-                             const float* d_W_rel, const float* d_W_root, const float* d_att,
-                             float* d_Y, float* d_R0, float* d_s_src, float* d_s_dst, void* d_ws,
-                             size_t ws_bytes, hifuse_stream_t stream) {
+static hifuse_status project_impl(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                  hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
+                                  const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
+                                  const float* d_W_rel, const float* d_W_root, const float* d_att,
+                                  float* d_Y, uint16_t* d_Yb, float* d_R0, float* d_s_src,
+                                  float* d_s_dst, void* d_ws, size_t ws_bytes,
+                                  hifuse_stream_t stream) {
   if (layout != HIFUSE_LAYOUT_COMPACT) return HIFUSE_ERR_UNSUPPORTED;
   LayerMeta m;
   hifuse_status rc = make_meta(shape, &m);
   if (rc != HIFUSE_OK) return rc;
   if (!kd_ok(K, D)) return HIFUSE_ERR_UNSUPPORTED;
-  if (!csr || !csr->rel_y_off || !csr->y_src || !csr->U_dev || !d_X || !d_W_rel || !d_Y ||
-      x_rows < 0 || (d_W_root && !d_R0))
+  if (!csr || !csr->rel_y_off || !csr->y_src || !csr->U_dev || !d_X || !d_W_rel ||
+      (!d_Y && !d_Yb) || x_rows < 0 || (d_W_root && !d_R0))
     return HIFUSE_ERR_INVALID_ARG;
   if (d_att && (!heads_ok2(D, heads) || !d_s_src || !d_s_dst)) return HIFUSE_ERR_INVALID_ARG;
   if (!aligned16(d_X) || !aligned16(d_W_rel) || !aligned16(d_W_root) || !aligned16(d_Y) ||
-      !aligned16(d_R0))
+      !aligned16(d_Yb) || !aligned16(d_R0))
     return HIFUSE_ERR_ALIGNMENT;
+  // bf16 Y: the tcgen05 path without RGAT scores (RGCN)
+  if (d_Yb && (d_att || (prec != HIFUSE_PREC_TF32 && prec != HIFUSE_PREC_BF16)))
+    return HIFUSE_ERR_UNSUPPORTED;
   if (ws_bytes < hifuse_project_ws_bytes(shape, K, D, heads) || !d_ws) return HIFUSE_ERR_WORKSPACE;
   cudaStream_t s = st(stream);
   ProjMeta pm;
@@ -755,7 +759,7 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
   if (tc) {
     rc = project_tcp_launch(m, pm, K, D, csr->rel_y_off, csr->y_src, d_X, nullptr, d_gather_ids,
                             d_W_rel, d_W_root, d_Y, d_R0, d_att, d_s_src, heads, s,
-                            prec == HIFUSE_PREC_BF16 ? wt : nullptr);   // s_src fused in the epilogue
+                            prec == HIFUSE_PREC_BF16 ? wt : nullptr, d_Yb);   // s_src fused in the epilogue
     if (sbr) branch_end(s, bs);
     if (rc != HIFUSE_OK) return rc;
   } else if (prec == HIFUSE_PREC_FP32) {
@@ -781,6 +785,30 @@ hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* 
     launch_scores_dst(pm, m.rows, K, heads, d_gather_ids, d_X, v, d_s_dst, s);
   }
   return last_cuda();
+}
+
+hifuse_status hifuse_project(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                             hifuse_layout layout, hifuse_prec prec, int K, int D, int heads,
+                             const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
+                             const float* d_W_rel, const float* d_W_root, const float* d_att,
+                             float* d_Y, float* d_R0, float* d_s_src, float* d_s_dst, void* d_ws,
+                             size_t ws_bytes, hifuse_stream_t stream) {
+  if (!d_Y) return HIFUSE_ERR_INVALID_ARG;
+  return project_impl(shape, csr, layout, prec, K, D, heads, d_X, x_rows, d_gather_ids, d_W_rel,
+                      d_W_root, d_att, d_Y, nullptr, d_R0, d_s_src, d_s_dst, d_ws, ws_bytes,
+                      stream);
+}
+
+hifuse_status hifuse_project_y16(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                 hifuse_layout layout, hifuse_prec prec, int K, int D,
+                                 const float* d_X, int64_t x_rows, const int32_t* d_gather_ids,
+                                 const float* d_W_rel, const float* d_W_root, uint16_t* d_Yb,
+                                 float* d_R0, void* d_ws, size_t ws_bytes,
+                                 hifuse_stream_t stream) {
+  if (!d_Yb) return HIFUSE_ERR_INVALID_ARG;
+  return project_impl(shape, csr, layout, prec, K, D, 1, d_X, x_rows, d_gather_ids, d_W_rel,
+                      d_W_root, nullptr, nullptr, d_Yb, d_R0, nullptr, nullptr, d_ws, ws_bytes,
+                      stream);
 }
 
 size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape* shape, int K, int D, int heads) {

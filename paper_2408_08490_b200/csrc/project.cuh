@@ -47,7 +47,8 @@ hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, 
                                  const float* Xm, const int* gather_ids, const float* W_rel,
                                  const float* W_root, float* Y, float* R0, const float* att,
                                  float* s_src, int H, cudaStream_t s,
-                                 uint16_t* Wt_bf16 = nullptr);   // non-NULL: BF16 operands
+                                 uint16_t* Wt_bf16 = nullptr,    // non-NULL: BF16 operands
+                                 uint16_t* Yb = nullptr);        // non-NULL: Y stored bf16
 // tcgen05 TF32 fused fusion GEMM of the aggregate-first input layer (NEXT(3)):
 // H_t = act([X_t | Xagg_r...] [W_root,t; W_r...] + b_t), one launch.
 hifuse_status fuse_gemm_launch(const LayerMeta& m, bool has_root, int K, int D, bool relu,

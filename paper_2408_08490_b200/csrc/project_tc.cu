@@ -510,14 +510,17 @@ __device__ __forceinline__ void group_table_warp(const ProjMeta& pm, const int* 
 // row), B from Wt, W_g^T pre-rounded to bf16 [D][K] by k_w_bf16t (K-major,
 // cp.async) -- and tcgen05.mma kind::f16 (K = 16 per instruction) accumulates
 // in fp32.  Everything else (stages, barriers, epilogue) is shared.
-template <int K, int D, bool BF>
+// YB: the relation groups' rows (Y) are stored as bf16 (RN-even) into Yb
+// (NEXT(3) byte diet: half the Y write and half the aggregation's gather);
+// the root rows R0 stay fp32.
+template <int K, int D, bool BF, bool YB>
 __global__ void __launch_bounds__(288, kFwdCtas)
 k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __restrict__ y_src,
                const int* __restrict__ gather_ids, const float* __restrict__ X,
                const float* __restrict__ W_rel, const float* __restrict__ W_root,
                float* __restrict__ Y, float* __restrict__ R0, const float* __restrict__ att,
                float* __restrict__ s_src, int H, const float* __restrict__ Xm,
-               const uint16_t* __restrict__ Wt) {
+               const uint16_t* __restrict__ Wt, uint16_t* __restrict__ Yb) {
   constexpr int BM = 128, KC = BF ? 64 : 32, NC = K / KC;   // K elements per 128-byte row
   constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
   constexpr uint32_t STAGE = A_STAGE + B_STAGE;
@@ -711,7 +714,16 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
           const int rr = i * 8 + (lane >> 2), ch = lane & 3;
           const int row = q * 32 + rr;
           const float4 x = *reinterpret_cast<const float4*>(st + rr * 20 + 4 * ch);
-          if (row < nrows) *reinterpret_cast<float4*>(out + (long long)(r0 + row) * D + c0 + 4 * ch) = x;
+          if (YB && g < pm.R) {
+            if (row < nrows) {
+              uint2 w;
+              asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w.x) : "f"(x.y), "f"(x.x));
+              asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w.y) : "f"(x.w), "f"(x.z));
+              *reinterpret_cast<uint2*>(Yb + (long long)(s_yoff[g] + r0 + row) * D + c0 + 4 * ch) = w;
+            }
+          } else if (row < nrows) {
+            *reinterpret_cast<float4*>(out + (long long)(r0 + row) * D + c0 + 4 * ch) = x;
+          }
         }
         __syncwarp();
       }
@@ -967,15 +979,15 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
 template <int K, int D>
 static constexpr int fwdp_smem() { return kFStages * (128 * 128 + D * 128) + 1024; }
 
-template <int K, int D, bool BF>
+template <int K, int D, bool BF, bool YB>
 static void launch_tcp(const ProjMeta& pm, const int* rel_off, const int* y_src,
                        const int* gather_ids, const float* X, const float* Xm,
                        const float* W_rel, const float* W_root, float* Y, float* R0,
                        const float* att, float* s_src, int H, const uint16_t* Wt,
-                       cudaStream_t s) {
-  set_max_smem(reinterpret_cast<const void*>(&k_proj_fwd_tcp<K, D, BF>), fwdp_smem<K, D>());
-  HF_LAUNCH((k_proj_fwd_tcp<K, D, BF>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s, pm,
-            rel_off, y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, Xm, Wt);
+                       uint16_t* Yb, cudaStream_t s) {
+  set_max_smem(reinterpret_cast<const void*>(&k_proj_fwd_tcp<K, D, BF, YB>), fwdp_smem<K, D>());
+  HF_LAUNCH((k_proj_fwd_tcp<K, D, BF, YB>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s,
+            pm, rel_off, y_src, gather_ids, X, W_rel, W_root, Y, R0, att, s_src, H, Xm, Wt, Yb);
 }
 
 template <int K, int D, bool RELU>
@@ -1027,24 +1039,28 @@ hifuse_status project_tcp_launch(const LayerMeta& m, const ProjMeta& pm, int K, 
                                  const int* rel_off, const int* y_src, const float* X,
                                  const float* Xm, const int* gather_ids, const float* W_rel,
                                  const float* W_root, float* Y, float* R0, const float* att,
-                                 float* s_src, int H, cudaStream_t s, uint16_t* Wt_bf16) {
+                                 float* s_src, int H, cudaStream_t s, uint16_t* Wt_bf16,
+                                 uint16_t* Yb) {
   if (Wt_bf16) {             // BF16 operands: round + transpose the weights first
     const int G = m.R + (W_root ? m.T : 0);
     HF_LAUNCH(k_w_bf16t, ceil_div((long long)G * K * D, 256), 256, 0, s, m.R, W_root ? m.T : 0, K,
               D, W_rel, W_root, Wt_bf16);
   }
-#define HF_TCP(KK, DD)                                                                          \
+#define HF_TCP2(KK, DD, YBB)                                                                    \
   if (Wt_bf16)                                                                                 \
-    launch_tcp<KK, DD, true>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0, att,  \
-                             s_src, H, Wt_bf16, s);                                             \
+    launch_tcp<KK, DD, true, YBB>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0,  \
+                                  att, s_src, H, Wt_bf16, Yb, s);                               \
   else                                                                                         \
-    launch_tcp<KK, DD, false>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0, att, \
-                              s_src, H, nullptr, s)
+    launch_tcp<KK, DD, false, YBB>(pm, rel_off, y_src, gather_ids, X, Xm, W_rel, W_root, Y, R0, \
+                                   att, s_src, H, nullptr, Yb, s)
+#define HF_TCP(KK, DD)                                                                          \
+  if (Yb) { HF_TCP2(KK, DD, true); } else { HF_TCP2(KK, DD, false); }
   if (K == 128 && D == 128) { HF_TCP(128, 128); }
   else if (K == 128 && D == 64) { HF_TCP(128, 64); }
   else if (K == 64 && D == 128) { HF_TCP(64, 128); }
   else { HF_TCP(64, 64); }
 #undef HF_TCP
+#undef HF_TCP2
   return HIFUSE_OK;
 }
 

@@ -75,6 +75,8 @@ def lib():
             "hifuse_project_ws_bytes": [vp, i32, i32, i32],
             "hifuse_project": [vp, vp, i32, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp,
                                vp, vp, vp, sz, vp],
+            "hifuse_project_y16": [vp, vp, i32, i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp, sz,
+                                   vp],
             "hifuse_aggregate_fwd": [vp, i64, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp],
             "hifuse_aggregate_fwd_xrel": [vp, vp, i32, i32, f32, vp, vp, vp, vp, vp, vp],
             "hifuse_semantic_fuse": [vp, i32, i32, vp, vp, vp, vp, vp],
@@ -249,6 +251,17 @@ def project(shape, csr, K, D, heads, X, gather_ids, W_rel, W_root, att, Y, R0, s
         shape.ref, csr.ref, LAYOUT_COMPACT, PREC[prec], K, D, heads, _ptr(X), X.shape[0],
         _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(att), _ptr(Y), _ptr(R0), _ptr(s_src),
         _ptr(s_dst), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def project_y16(shape, csr, K, D, X, gather_ids, W_rel, W_root, Yb, R0, ws, prec="tf32",
+                stream=None):
+    """hifuse_project_y16: RGCN projection with Y stored as bfloat16 (NEXT(3))."""
+    import torch
+    assert Yb.dtype == torch.bfloat16
+    _check("hifuse_project_y16", lib().hifuse_project_y16(
+        shape.ref, csr.ref, LAYOUT_COMPACT, PREC[prec], K, D, _ptr(X), X.shape[0],
+        _ptr(gather_ids), _ptr(W_rel), _ptr(W_root), _ptr(Yb), _ptr(R0), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def aggregate_fwd(csr, rows, agg, D, heads, slope, Y, s_src, s_dst, Z, stats, stream=None):

@@ -81,7 +81,7 @@ class Trainer:
 
     def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
                  prec="tf32", slope=0.2, order="project_first", fusion="sum", fuse_gemm=True,
-                 feat_dtype="fp32"):
+                 feat_dtype="fp32", y_dtype="fp32"):
         hf.lib()   # raises if libhifuse.so is missing (no CPU fallback)
         self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
         self.rel_src = np.asarray(rel_src, np.int32)
@@ -129,6 +129,13 @@ class Trainer:
         if feat_dtype == "bf16" and not self.agg_first:
             raise ValueError("a BF16 feature store needs the aggregate-first input layer")
         self.feat_dtype = feat_dtype
+        # NEXT(3) byte diet: BF16 storage of Y (RGCN project-first layers; the
+        # aggregation reads it through the BF16 gather kernel, reading C25)
+        if y_dtype not in ("fp32", "bf16"):
+            raise ValueError(y_dtype)
+        if y_dtype == "bf16" and (model != "rgcn" or prec == "fp32" or fusion != "sum"):
+            raise ValueError("BF16 Y needs the RGCN tcgen05 projection (tf32 / bf16)")
+        self.y_dtype = y_dtype
         # capture streams: `_hi` (high priority) for the pipelined graphs,
         # `_cap` for the serial / per-stage graphs; the library's fork/join
         # resources of every stream that runs steps are created here, outside
@@ -309,10 +316,22 @@ class Trainer:
                 acts.append(a)
                 X, gid = a["H"], None
                 continue
-            ops.append((f"project.{l}", lambda sh=sh, c=csrs[l], a=a, P=P: hf.project(
-                sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"], P["att"], a["Y"],
-                a["R0"], a["s_src"], a["s_dst"], a["wsp"], prec=self.prec)))
-            if self.agg == "gat_xrel":     # softmax across relations (NEXT(2))
+            if self.y_dtype == "bf16":
+                yb = self._buf(f"Yb{l}", max(sh.U_max, 1) * D, torch.bfloat16)
+                a["Yb"] = yb[:max(sh.U_max, 1) * D].view(max(sh.U_max, 1), D)
+                ops.append((f"project.{l}", lambda sh=sh, c=csrs[l], a=a, P=P: hf.project_y16(
+                    sh, c, a["K"], D, a["X"], a["gid"], P["W_rel"], P["W_root"], a["Yb"],
+                    a["R0"], a["wsp"], prec=self.prec)))
+                ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a:
+                            hf.aggregate_features_cols_bf16(sh, c, self.agg, D, a["Yb"], c["col"],
+                                                            None, a["Z"], None)))
+            else:
+                ops.append((f"project.{l}", lambda sh=sh, c=csrs[l], a=a, P=P: hf.project(
+                    sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"], P["W_root"], P["att"],
+                    a["Y"], a["R0"], a["s_src"], a["s_dst"], a["wsp"], prec=self.prec)))
+            if self.y_dtype == "bf16":
+                pass
+            elif self.agg == "gat_xrel":     # softmax across relations (NEXT(2))
                 ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a:
                             hf.aggregate_fwd_xrel(sh, c, D, H, self.slope, a["Y"], a["s_src"],
                                                   a["s_dst"], a["Z"], a["stats"])))

@@ -416,6 +416,48 @@ def test_project_bf16_exact_on_representable_inputs(K, D):
     assert np.array_equal(R0.cpu().numpy(), ref["R0"].astype(np.float32))
 
 
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("K,D", [(128, 128), (64, 64), (128, 64)])
+def test_project_y16_and_bf16_aggregation(K, D, prec):
+    """NEXT(3) BF16 storage of Y (reading C25): on {-2..2}/4 inputs the fp32
+    accumulator is exact, so Yb must be the RN-even bf16 rounding of the fp64
+    oracle's Y bit for bit; on random inputs Yb within TF32 + half a bf16 ulp
+    (row-norm 5e-3).  The aggregation over Yb (the BF16 gather kernel with
+    col_x = csr.col) against the oracle's aggregation of the same rounded Y at
+    1e-5 of the absolute-sum scale (sum and mean)."""
+    rng, blk, et, rs, rd, sh, csr, ch = make_case(350 + K + D, D=D, T=3, R=6, N=5000, hub=0.1)
+    U = ch["U"]
+    osh = oracle.Shape.of(blk, rs, rd)
+    ws = torch.empty(hf().project_ws_bytes(sh, K, D, 1) // 4 + 16, device=DEV)
+    for exact in (True, False):
+        if exact:
+            X = (rng.integers(-2, 3, (sh.src_rows, K)) / 4).astype(np.float32)
+            W = (rng.integers(-2, 3, (sh.R, K, D)) / 4).astype(np.float32)
+            Wr = (rng.integers(-2, 3, (sh.T, K, D)) / 4).astype(np.float32)
+        else:
+            X = rng.standard_normal((sh.src_rows, K)).astype(np.float32)
+            W = (rng.standard_normal((sh.R, K, D)) / np.sqrt(K)).astype(np.float32)
+            Wr = (rng.standard_normal((sh.T, K, D)) / np.sqrt(K)).astype(np.float32)
+        Yb = torch.zeros(max(sh.U_max, 1), D, device=DEV, dtype=torch.bfloat16)
+        R0 = torch.zeros(sh.dst_rows, D, device=DEV)
+        hf().project_y16(sh, csr, K, D, t(X), None, t(W), t(Wr), Yb, R0, ws, prec=prec)
+        rb = oracle.bf16_round if prec == "bf16" else (lambda a: a)
+        ref = oracle.project(osh, ch, K, D, 1, rb(X), None, rb(W), rb(Wr), None)
+        got = Yb.float().cpu().numpy()[:U]
+        if exact:
+            assert np.array_equal(got, oracle.bf16_round(ref["Y"]).astype(np.float32))
+        else:
+            row_rel_l2(got, ref["Y"], 5e-3, "Yb")
+        for agg in ("sum", "mean"):
+            Z = torch.zeros(sh.rows, D, device=DEV)
+            hf().aggregate_features_cols_bf16(sh, csr, agg, D, Yb, csr["col"], None, Z, None)
+            Yr = np.zeros((max(U, 1), D))
+            Yr[:U] = got
+            zr = oracle.aggregate_fwd(osh, blk, et, ch, agg, D, 1, Yr)["Z"]
+            za = oracle.aggregate_fwd(osh, blk, et, ch, agg, D, 1, np.abs(Yr))["Z"]
+            close_scaled(Z.cpu().numpy(), zr, za, 1e-5, f"Z {agg}")
+
+
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("B,C", [(5, 3), (128, 7), (1024, 128), (300, 129), (1024, 349),
                                  (64, 600), (2048, 7)])
