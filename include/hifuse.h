@@ -76,6 +76,7 @@ typedef enum {
 #define HIFUSE_ST_BAD_DST     8   /* dst_local >= n_dst(dst type of relation)   */
 #define HIFUSE_ST_UNSORTED_TYPES 16 /* edge_type not relation-major (offsets unusable) */
 #define HIFUSE_ST_BAD_LABEL   32  /* class label outside [0, C) (hifuse_linear_xent) */
+#define HIFUSE_ST_OVERFLOW    64  /* padded sampler: a block exceeded its capacities  */
 
 /* GAT_XREL: GAT with the edge-softmax across the relations of a destination
  * (hifuse_aggregate_fwd_xrel, reading C5'). */
@@ -157,7 +158,9 @@ hifuse_status hifuse_csr_sizes(const hifuse_layer_shape *shape, hifuse_layout la
  * 310-324: EdgeTypeLayer = EdgeType[EdgeID], per-relation compare + select),
  * producing the merged segmented CSR/CSC of each layer in `out[l]`.
  *   d_src_local[l], d_dst_local[l]: int32 [N_l] batch-local endpoint ids;
- *   d_edge_id[l]: int64 [N_l] graph-global edge ids;
+ *   d_edge_id[l]: int64 [N_l] graph-global edge ids; -1 marks a NULL edge
+ *     (capacity padding, e.g. the tail of a padded GPU-sampled block): it is
+ *     dropped like an invalid edge but sets no status bit;
  *   d_edge_type: int32 [num_graph_edges] relation of every graph edge;
  *   d_rel_edge_off: NULL, or int64 [R+1] with d_edge_type relation-major
  *     (global edge ids sorted by relation): relation r owns ids
@@ -556,6 +559,34 @@ hifuse_status hifuse_sample_blocks(const hifuse_graph_csc *g, int num_layers,
                                    int32_t *d_state,
                                    void *d_ws, size_t ws_bytes, int32_t *d_status,
                                    hifuse_stream_t stream);
+
+/* Padded (capacity) layout of the same sampler, so that ONE captured CUDA
+ * graph of sampler + build + training step serves every batch (the step's
+ * host shapes become the capacities; Fig. 6, with
+ * sampling inside the pipelined loop).  src_cap_h [L*T] (outer layer first,
+ * row l): sources of type t in layer l occupy slots [off_l(t), off_l(t) +
+ * src_cap_h[l*T+t]) of src_gid / gather_ids, off_l = prefix of the row; the
+ * layer's destinations (layer l+1's padded sources, or the seeds) are the
+ * first slots of each type, so src_cap_h[l*T+t] >= src_cap_h[(l+1)*T+t].
+ * Slots past the sampled sources hold src_gid -1 (gather id: the type's
+ * first feature row); padded destinations (src_gid -1) are not sampled.
+ * Edge positions [N, edge_pad_h[l]) hold null edges (edge_id -1, ids 0),
+ * which the build drops silently.  counts: n_src[t] = padded destinations +
+ * sampled new sources, n_dst[t] = padded destinations, N = sampled edges; a
+ * block past its capacities ORs HIFUSE_ST_OVERFLOW into d_status (its layout
+ * is then invalid: the caller re-samples it in the compact layout).  Output
+ * buffers as for hifuse_sample_blocks (worst-case capacities).  Errors:
+ * INVALID_ARG also for capacities that break the rules above or exceed the
+ * worst-case capacities of hifuse_sample_caps. */
+hifuse_status hifuse_sample_blocks_padded(const hifuse_graph_csc *g, int num_layers,
+                                          const int32_t *fanout_h, const int32_t *d_seeds,
+                                          int64_t num_seeds, int32_t target_type, uint64_t key,
+                                          const uint64_t *d_ctl, int32_t stamp,
+                                          const int64_t *src_cap_h /* [L*T] */,
+                                          const int64_t *edge_pad_h /* [L] */,
+                                          hifuse_block *out, int32_t *d_state, void *d_ws,
+                                          size_t ws_bytes, int32_t *d_status,
+                                          hifuse_stream_t stream);
 
 /* Per-stream fork/join resources (common.cu).  A call that runs independent
  * kernels concurrently (the dgrad || wgrad of hifuse_project_bwd, the two

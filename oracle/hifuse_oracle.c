@@ -65,6 +65,8 @@ int oracle_max_threads(void)
  * reading C3); col[p] is the Y row of the edge at CSR position p; the CSC
  * lists, per Y row, the CSR positions that read it, ascending.
  * Invalid edges (status bits) are dropped; unused tails are set to -1.
+ * Edge id -1 is a null edge (capacity padding, reading C26): it is
+ * dropped without a status bit.
  */
 int oracle_build(int T, int R, const int32_t *rel_src, const int32_t *rel_dst,
                  const int32_t *n_src, const int32_t *n_dst,
@@ -80,6 +82,7 @@ int oracle_build(int T, int R, const int32_t *rel_src, const int32_t *rel_dst,
     int32_t *etl = (int32_t *)malloc(sizeof(int32_t) * (N > 0 ? N : 1));
     for (int64_t e = 0; e < N; e++) {
         etl[e] = -1;
+        if (eid[e] == -1) continue;        /* null (padding) edge: dropped, no status (C26) */
         if (eid[e] < 0 || eid[e] >= E) { status |= ST_BAD_EDGE_ID; continue; }
         int32_t r = edge_type[eid[e]];
         if (r < 0 || r >= R) { status |= ST_BAD_REL; continue; }

@@ -59,6 +59,7 @@ template <int D, bool MEAN>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict__ col,
           const float4* __restrict__ Y, float4* __restrict__ Z) {
+  HF_PDL_ENTRY();
   constexpr int LPR = D / 4;              // lanes per row stream
   constexpr int NS = 32 / LPR;            // edge streams per warp
   const int lane = threadIdx.x & 31;
@@ -130,6 +131,7 @@ k_agg_fwd_bf16(long long rows, unsigned agg_blocks, const int* __restrict__ row_
                const int* __restrict__ col, const uint4* __restrict__ Xb,
                float4* __restrict__ Z, DstConv dc, const int* __restrict__ gather_ids,
                float4* __restrict__ Xdst) {
+  HF_PDL_ENTRY();
   constexpr int LPR = D / 8;              // lanes per row stream (8 bf16 each)
   constexpr int NS = 32 / LPR;            // edge streams per warp
   const int lane = threadIdx.x & 31;
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(256)
 k_col_to_x(int N, int R, const int* __restrict__ rel_y_off, RelOff so,
            const int* __restrict__ col, const int* __restrict__ y_src,
            const int* __restrict__ gather_ids, int* __restrict__ col_x) {
+  HF_PDL_ENTRY();
   __shared__ int s_yo[HF_MAX_R + 1];
   __shared__ int s_so[HF_MAX_R];
   for (int i = threadIdx.x; i <= R; i += blockDim.x) {
@@ -222,6 +225,7 @@ k_agg_fwd_gat(long long rows, int H, float slope, const int* __restrict__ row_pt
               const int* __restrict__ col, const float4* __restrict__ Y,
               const float* __restrict__ s_src, const float* __restrict__ s_dst,
               float4* __restrict__ Z, float* __restrict__ stats) {
+  HF_PDL_ENTRY();
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
   const int lane = threadIdx.x & 31;
@@ -307,6 +311,7 @@ k_agg_fwd_gat_half(long long rows, int H, float slope, const int* __restrict__ r
                    const int* __restrict__ col, const float4* __restrict__ Y,
                    const float* __restrict__ s_src, const float* __restrict__ s_dst,
                    float4* __restrict__ Z, float* __restrict__ stats) {
+  HF_PDL_ENTRY();
   const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
   const unsigned mask = 0xffffu << (16 * half);
   const long long row = ((long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * 2 + half;
@@ -470,6 +475,7 @@ k_agg_bwd_e(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __rest
             const typename RowVec<D>::T* __restrict__ G, typename RowVec<D>::T* __restrict__ dY,
             typename RowVec<D>::T* __restrict__ part, int* __restrict__ head_col,
             int* __restrict__ tail_col, int n_chunks, int E) {
+  HF_PDL_ENTRY();
   using VT = typename RowVec<D>::T;
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ int s_roff[HF_MAX_R + 1];
@@ -553,6 +559,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_bwd_fix(const typename RowVec<D>::T* __restrict__ part, const int* __restrict__ head_col,
               const int* __restrict__ tail_col, typename RowVec<D>::T* __restrict__ dY,
               int n_chunks) {
+  HF_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (k >= n_chunks) return;
@@ -593,6 +600,7 @@ k_agg_bwd_gat_e(BwdMeta bm, int H, const int* __restrict__ rel_row_off_d,
                 typename RowVec<D>::T* __restrict__ part, float* __restrict__ part_dss,
                 int* __restrict__ head_col, int* __restrict__ tail_col, int n_chunks, int E,
                 const float* __restrict__ att) {
+  HF_PDL_ENTRY();
   using VT = typename RowVec<D>::T;
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int VEC = D / 32;
@@ -694,6 +702,7 @@ k_agg_bwd_gat_fix(int R, int H, const int* __restrict__ rel_y_off,
                   const float* __restrict__ part_dss, const int* __restrict__ head_col,
                   const int* __restrict__ tail_col, float* __restrict__ dYf,
                   float* __restrict__ ds_src, int n_chunks, const float* __restrict__ att) {
+  HF_PDL_ENTRY();
   using VT = typename RowVec<D>::T;
   constexpr int VEC = D / 32;
   const int lane = threadIdx.x & 31;
@@ -733,6 +742,7 @@ k_agg_bwd_gat_rows(BwdMeta bm, const int* __restrict__ rel_row_off_d, long long 
                    const float* __restrict__ s_dst, const float* __restrict__ stats,
                    const float4* __restrict__ G, float* __restrict__ alpha,
                    float* __restrict__ dpre, float* __restrict__ ds_dst) {
+  HF_PDL_ENTRY();
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
   __shared__ int s_roff[HF_MAX_R + 1];
@@ -839,6 +849,7 @@ k_agg_bwd_gat_rows_half(BwdMeta bm, const int* __restrict__ rel_row_off_d, long 
                         const float* __restrict__ stats, const float4* __restrict__ G,
                         float* __restrict__ alpha, float* __restrict__ dpre,
                         float* __restrict__ ds_dst) {
+  HF_PDL_ENTRY();
   __shared__ int s_roff[HF_MAX_R + 1];
   for (int i = threadIdx.x; i <= bm.R; i += blockDim.x) s_roff[i] = rel_row_off_d[i];
   __syncthreads();
@@ -934,6 +945,7 @@ k_agg_fwd_gat_xrel(XrelMeta xm, int dst_rows, int H, float slope, const int* __r
                    const int* __restrict__ col, const float4* __restrict__ Y,
                    const float* __restrict__ s_src, const float* __restrict__ s_dst,
                    float4* __restrict__ Z, float* __restrict__ stats) {
+  HF_PDL_ENTRY();
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
   const int lane = threadIdx.x & 31;
@@ -1027,6 +1039,7 @@ k_agg_bwd_gat_xrel_dst(XrelMeta xm, int dst_rows, int H, float slope,
                        const float* __restrict__ s_dst, const float* __restrict__ stats,
                        const float4* __restrict__ G, float* __restrict__ alpha,
                        float* __restrict__ dpre, float* __restrict__ ds_dst) {
+  HF_PDL_ENTRY();
   constexpr int LPR = D / 4;
   constexpr int NS = 32 / LPR;
   const int lane = threadIdx.x & 31;

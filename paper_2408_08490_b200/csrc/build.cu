@@ -21,10 +21,15 @@
 //               slot_y, y_src, rel_y_off, U -- and col_ptr, because Y rows are
 //               numbered in slot order, so the CSC column of Y row slot_y[s]
 //               starts at the exclusive prefix of the slot counts at s
-//   k_scatter   pos = row_ptr[key] + rank: eperm, col (unsorted inside rows)
-//   k_rows      warp per 32 consecutive rows: their CSR span staged in shared
-//               memory, every row sorted by original column (restores Alg.
-//               2's order: bit-exact and deterministic), then placed into the
+//               Also the runs of each row (stretches of consecutive input
+//               edges with one key) and the first edge of a run
+//   k_scatter   pos = row_ptr[key] + (e - first edge of the run) for a row of
+//               ONE run (input order: the sampler lists a destination's edges
+//               of a relation together), else + rank (unsorted): eperm, col
+//   k_rows      warp per HF_BUILD_ROWS_PER_WARP consecutive rows: their CSR
+//               span staged in shared memory, every row of several runs sorted
+//               by original column (restores Alg. 2's order: bit-exact and
+//               deterministic), then placed into the
 //               CSC (one atomic slot per entry); longer rows by the block
 //   k_cols      warp per 32 consecutive CSC columns: each sorted by CSR
 //               position (lane per column <= 16 entries, warp bitonic <= 32),
@@ -45,12 +50,33 @@ namespace {
 
 constexpr int kBT = 256;               // threads per block
 constexpr int kNW = kBT / 32;
-constexpr int kEdgeTile = 2048;        // edges per classify / scatter block
+// Tiling (compile-time; scripts/build_variants.sh + scripts/sweep_build.py
+// sweep them).  Measured on B200 (eager build call, mag / IMDB / Freebase /
+// DBLP): 2048 edges per block, 16 scan elements per thread, 32 rows per warp
+// -> 75 / 62 / 76 / 74 us; 512 / 4 / 8 -> 62 / 46 / 67 / 53 us: the kernels
+// are latency-bound, so more, smaller blocks (more warps in flight) win.
+#ifndef HF_BUILD_EDGE_TILE
+#define HF_BUILD_EDGE_TILE 512
+#endif
+#ifndef HF_BUILD_SCAN_PER
+#define HF_BUILD_SCAN_PER 4
+#endif
+#ifndef HF_BUILD_ROWS_PER_WARP
+#define HF_BUILD_ROWS_PER_WARP 8
+#endif
+constexpr int kEdgeTile = HF_BUILD_EDGE_TILE;   // edges per classify / scatter block
 constexpr int kEPT = kEdgeTile / kBT;  // edges per thread
-constexpr int kScanPer = 16;           // scan elements per thread
+constexpr int kScanPer = HF_BUILD_SCAN_PER;   // scan elements per thread
 constexpr int kScanTile = kBT * kScanPer;
 constexpr int kSegRows = 32;           // rows / columns per warp in k_rows / k_cols
 constexpr int kSegTile = kNW * kSegRows;
+constexpr int kRowsW = HF_BUILD_ROWS_PER_WARP;  // merged rows per warp in k_rows
+constexpr int kRowsTile = kNW * kRowsW;
+constexpr int kSpanR = kRowsW * 32 < 1024 ? kRowsW * 32 : 1024;   // k_rows staging per warp
+constexpr int kBlockRankR = kRowsW >= 16 ? 4096 : 2048;           // k_rows long-row sort
+constexpr size_t kSmemRows = (size_t)(kNW * kSpanR * 2 > 2 * kBlockRankR ? kNW * kSpanR * 2
+                                                                        : 2 * kBlockRankR) *
+                             sizeof(int);
 constexpr int kSpan = 1024;            // CSR/CSC entries a warp stages in smem
 constexpr int kMaxL = 4;               // layers per launch set (more: further sets)
 constexpr int kWarpRank = 256;
@@ -58,7 +84,8 @@ constexpr int kBlockRank = 4096;
 constexpr int kLongRowBlocks = 16;     // k_rows blocks for rows > 32 (not in workloads)
 constexpr size_t kSmem = (size_t)kNW * kSpan * 2 * sizeof(int);   // 64 KB
 static_assert(kBlockRank * 2 * sizeof(int) <= kSmem, "block rank sort buffer");
-static_assert(2 * (kScanTile + kScanTile / 32) * sizeof(int) + 128 <= kSmem, "scan buffer");
+constexpr size_t kSmemScan = 2 * (kScanTile + kScanTile / 32) * sizeof(int) + 128;
+static_assert(kSmemScan <= kSmem, "scan buffer");
 
 enum Kern { K_CLASSIFY, K_SCAN, K_SCATTER, K_ROWS, K_COLS, kKerns };
 
@@ -77,10 +104,12 @@ struct BLayer {
       *csc_row, *csc_col, *slot_y, *U_dev;
   // workspace: zero zone
   int *cnt, *ccur;                     // cnt = [row counts | slot counts]
+  int* runs;                           // per row: runs of consecutive input edges
   int* lcnt;                           // [0] long rows, [1] long columns
   unsigned long long* sst;             // scan tile status [t_rows | t_slots]
   // workspace: scratch
   int *key_e, *slot_e, *rank_e, *gk, *gv, *long_rows, *long_cols;
+  int* first;                          // per row: first input edge of its (last) run
   int rows_reg, cols_reg;              // regular (non-long) blocks of k_rows / k_cols
   int cols_xtra;                       // extra k_cols blocks for hub columns
 };
@@ -213,14 +242,15 @@ __device__ __forceinline__ void place_entry(const BLayer& L, int row, int p, int
 }
 
 // Block-wide sort of one segment [b, e) of (keys, vals): rank sort in shared
-// memory (<= kBlockRank entries), a global rank sort beyond (never seen in
-// the workloads).  sm: >= 2 kBlockRank ints.  Ends with __syncthreads.
+// memory (<= BR entries), a global rank sort beyond (never seen in the
+// workloads).  sm: >= 2 BR ints.  Ends with __syncthreads.
+template <int BR>
 __device__ void block_sort_segment(int* keys, int* vals, int b, int e, int* sm, int* gk,
                                    int* gv) {
   const int n = e - b;
   int* sk = sm;
-  int* sv = sm + kBlockRank;
-  if (n <= kBlockRank) {
+  int* sv = sm + BR;
+  if (n <= BR) {
     // bitonic sort in shared memory, padded to a power of two (n log^2 n;
     // a rank sort is n^2 -- 30 us for a 1757-entry hub column of ogbn-mag)
     int P2 = 1;
@@ -267,9 +297,34 @@ struct RelSmem {
   int key_base[HF_MAX_R + 1], slot_base[HF_MAX_R + 1], src_lim[HF_MAX_R], dst_lim[HF_MAX_R];
 };
 
+// Merged-row key of input edge e, -3 if the edge is invalid (k_classify's
+// per-edge logic for a single edge: the one before a tile).
+__device__ int edge_key_of(const BPlan& P, const BLayer& L, const RelSmem& rs, int e) {
+  const long long id = L.eid[e];
+  if (id < 0 || id >= P.E) return -3;
+  int r;
+  if (P.rel_off) {
+    int lo = 0, hi = L.R;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (rs.off[mid] <= id) lo = mid; else hi = mid;
+    }
+    r = lo;
+  } else {
+    r = P.edge_type[id];
+  }
+  if (r < 0 || r >= L.R) return -3;
+  const int sv = L.src[e], dv = L.dst[e];
+  if (sv < 0 || sv >= rs.src_lim[r] || dv < 0 || dv >= rs.dst_lim[r]) return -3;
+  return rs.key_base[r] + dv;
+}
+
 __global__ void __launch_bounds__(kBT)
 k_classify(const __grid_constant__ BuildParams bp) {
+  HF_PDL_ENTRY();
   __shared__ RelSmem rs;
+  __shared__ int skey[kEdgeTile];
+  __shared__ int s_prev0;
   const BPlan& P = bp.p;
   int j;
   const BLayer& L = bp.lay[layer_of(P, K_CLASSIFY, &j)];
@@ -304,6 +359,10 @@ k_classify(const __grid_constant__ BuildParams bp) {
     key[q] = -1;
     slot[q] = -1;
     if (id[q] == -2) continue;                     // past the tile
+    if (id[q] == -1) {                             // null (padding) edge: dropped silently
+      key[q] = -3;
+      continue;
+    }
     int bad = 0, r = -1;
     if (id[q] < 0 || id[q] >= P.E) {
       bad = HIFUSE_ST_BAD_EDGE_ID;
@@ -333,6 +392,23 @@ k_classify(const __grid_constant__ BuildParams bp) {
     slot[q] = L.rows + rs.slot_base[r] + sv[q];    // index into cnt
   }
   if (bad_any) atomicOr(P.status, bad_any);
+  // Runs: maximal stretches of consecutive valid input edges with one key.  A
+  // row made of ONE run (sampled blocks list a destination's edges of one
+  // relation together) is placed in input order by k_scatter directly
+  // (position = e - first edge of the run) and needs no sort in k_rows.
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) skey[q * kBT + threadIdx.x] = key[q];
+  if (threadIdx.x == 0) s_prev0 = e0 > 0 ? edge_key_of(P, L, rs, e0 - 1) : -1;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kEPT; q++) {
+    const int i = q * kBT + threadIdx.x;
+    const int prev = i ? skey[i - 1] : s_prev0;
+    if (key[q] >= 0 && prev != key[q]) {
+      L.first[key[q]] = e0 + i;
+      atomicAdd(L.runs + key[q], 1);
+    }
+  }
   // Warp-aggregated atomics: sampled blocks list the edges of a destination
   // (and often of a source) together, so lanes of a warp often share a row
   // or slot -- one atomic per distinct address and warp.  Row: the atomic's
@@ -378,6 +454,7 @@ __device__ __forceinline__ unsigned long long pack(int flag, long long a, long l
 
 __global__ void __launch_bounds__(kBT)
 k_scan(const __grid_constant__ BuildParams bp) {
+  HF_PDL_ENTRY();
   extern __shared__ __align__(16) int sm[];
   int jj;
   const BLayer& L = bp.lay[layer_of(bp.p, K_SCAN, &jj)];
@@ -553,6 +630,7 @@ k_scan(const __grid_constant__ BuildParams bp) {
 // -------------------------------------------------------------- k_scatter --
 __global__ void __launch_bounds__(kBT)
 k_scatter(const __grid_constant__ BuildParams bp) {
+  HF_PDL_ENTRY();
   int j;
   const BLayer& L = bp.lay[layer_of(bp.p, K_SCATTER, &j)];
   const int nvalid = L.row_ptr[L.rows];
@@ -567,7 +645,11 @@ k_scatter(const __grid_constant__ BuildParams bp) {
   }
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
-    pos[q] = key[q] >= 0 ? L.row_ptr[key[q]] + rank[q] : 0;
+    const int e = e0 + q * kBT + threadIdx.x;
+    // one-run row: input order directly; else the arrival rank (k_rows sorts)
+    const int rn = key[q] >= 0 ? L.runs[key[q]] : 0;
+    const int f = rn == 1 ? L.first[key[q]] : 0;
+    pos[q] = key[q] >= 0 ? L.row_ptr[key[q]] + (rn == 1 ? e - f : rank[q]) : 0;
     c[q] = key[q] >= 0 ? L.slot_y[slot[q]] : 0;
   }
 #pragma unroll
@@ -603,6 +685,7 @@ __device__ __forceinline__ void row_sorted(const BLayer& L, bool staged, int* sk
 
 __global__ void __launch_bounds__(kBT)
 k_rows(const __grid_constant__ BuildParams bp) {
+  HF_PDL_ENTRY();
   extern __shared__ __align__(16) int sm[];
   int j;
   const BLayer& L = bp.lay[layer_of(bp.p, K_ROWS, &j)];
@@ -614,25 +697,30 @@ k_rows(const __grid_constant__ BuildParams bp) {
     for (int k = j - L.rows_reg; k < nl; k += kLongRowBlocks) {
       const int row = L.long_rows[k];
       const int b = L.row_ptr[row], e = L.row_ptr[row + 1];
-      block_sort_segment(L.eperm, L.col, b, e, sm, L.gk, L.gv);
+      block_sort_segment<kBlockRankR>(L.eperm, L.col, b, e, sm, L.gk, L.gv);
       if (L.csc)
         for (int p = b + threadIdx.x; p < e; p += kBT) place_entry(L, row, p, L.col[p]);
       __syncthreads();
     }
     return;
   }
-  const int r0 = (j * kNW + w) * kSegRows;
+  const int r0 = (j * kNW + w) * kRowsW;
   if (r0 < L.rows) {
-    const int nr = min(kSegRows, L.rows - r0);
-    int* sk = sm + w * 2 * kSpan;
-    int* sv = sk + kSpan;
+    const int nr = min(kRowsW, L.rows - r0);
+    int* sk = sm + w * 2 * kSpanR;
+    int* sv = sk + kSpanR;
     const int rb = L.row_ptr[r0 + min(lane, nr)];                 // start of row r0+lane
     const int re = L.row_ptr[r0 + min(lane + 1, nr)];             // its end
     const int n = lane < nr ? re - rb : 0;
+    // rows made of several input runs need the sort (one-run rows are in
+    // input order already, k_scatter)
+    const bool multi = n > 1 && L.runs[r0 + lane] > 1;
+    const unsigned need = __ballot_sync(0xffffffffu, multi);
+    if (!need && !L.csc) return;
     const int span_b = __shfl_sync(0xffffffffu, rb, 0);
     const int span_e = __shfl_sync(0xffffffffu, re, nr - 1);
     const int span = span_e - span_b;
-    const bool staged = span <= kSpan;
+    const bool staged = span <= kSpanR;
     if (staged) {
       stage2(L.eperm + span_b, L.col + span_b, span, span, sk, sv, lane, 32);
       __syncwarp();
@@ -644,7 +732,7 @@ k_rows(const __grid_constant__ BuildParams bp) {
       const int src = row < nr ? row : 0;
       const int b = __shfl_sync(0xffffffffu, rb, src);
       const int nn = __shfl_sync(0xffffffffu, n, src);
-      const bool mine = row < nr && nn <= 16;
+      const bool mine = row < nr && nn <= 16 && ((need >> src) & 1u);
       int key = 0x7fffffff, val = 0;
       if (mine && hl < nn) {
         key = staged ? sk[b - span_b + hl] : L.eperm[b + hl];
@@ -655,7 +743,7 @@ k_rows(const __grid_constant__ BuildParams bp) {
       if (mine && hl < nn) row_sorted(L, staged, sk, sv, span_b, b, hl, key, val);
     }
     // rows of 17..32 entries: whole warp, one after another
-    unsigned mid = __ballot_sync(0xffffffffu, lane < nr && n > 16 && n <= 32);
+    unsigned mid = __ballot_sync(0xffffffffu, lane < nr && n > 16 && n <= 32) & need;
     while (mid) {
       const int src = __ffs(mid) - 1;
       mid &= mid - 1;
@@ -728,6 +816,7 @@ k_rows(const __grid_constant__ BuildParams bp) {
 // edges).
 __global__ void __launch_bounds__(kBT)
 k_cols(const __grid_constant__ BuildParams bp) {
+  HF_PDL_ENTRY();
   extern __shared__ __align__(16) int sm[];
   constexpr int kThreadCap = 16;
   int j;
@@ -758,7 +847,7 @@ k_cols(const __grid_constant__ BuildParams bp) {
       const int u = L.long_cols[k];
       const int b = L.col_ptr[u], e = L.col_ptr[u + 1];
       if (e - b <= kWarpRank) continue;
-      block_sort_segment(L.csc_pos, L.csc_row, b, e, sm, L.gk, L.gv);
+      block_sort_segment<kBlockRank>(L.csc_pos, L.csc_row, b, e, sm, L.gk, L.gv);
     }
     return;
   }
@@ -847,11 +936,12 @@ struct LayerWs {
 LayerWs layer_ws_sizes(const LayerMeta& m, bool csc) {
   const long long U_max = umax_of(m);
   LayerWs s;
-  s.zero_bytes = carve_bytes((long long)m.rows + m.S, 4) +
+  s.zero_bytes = carve_bytes((long long)m.rows + m.S, 4) + carve_bytes(m.rows, 4) +
                  (csc ? carve_bytes(U_max + 1, 4) : 0) + carve_bytes(2, 4) +
                  carve_bytes(2ll * (tiles(m.rows, kScanTile) + tiles(m.S, kScanTile)), 4);
   s.scratch_bytes = carve_bytes(m.N, 4) * 5 +              // key_e slot_e rank_e gk gv
-                    carve_bytes(m.rows, 4) + carve_bytes(U_max, 4);   // long lists
+                    carve_bytes(m.rows, 4) + carve_bytes(U_max, 4) +  // long lists
+                    carve_bytes(m.rows, 4);                           // first
   return s;
 }
 
@@ -860,6 +950,7 @@ void carve_layer(const LayerMeta& m, bool csc, char*& zp, char*& sp, BLayer* L) 
   L->t_rows = tiles(m.rows, kScanTile);
   L->t_slots = tiles(m.S, kScanTile);
   L->cnt = carve<int>(zp, (long long)m.rows + m.S);
+  L->runs = carve<int>(zp, m.rows);
   L->ccur = csc ? carve<int>(zp, U_max + 1) : nullptr;
   L->lcnt = carve<int>(zp, 2);
   L->sst = reinterpret_cast<unsigned long long*>(
@@ -871,6 +962,7 @@ void carve_layer(const LayerMeta& m, bool csc, char*& zp, char*& sp, BLayer* L) 
   L->gv = carve<int>(sp, m.N);
   L->long_rows = carve<int>(sp, m.rows);
   L->long_cols = carve<int>(sp, U_max);
+  L->first = carve<int>(sp, m.rows);
 }
 
 }  // namespace
@@ -935,8 +1027,8 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     need = std::max(need, set);
   }
   if (!d_ws || need > ws_bytes) return HIFUSE_ERR_WORKSPACE;
-  set_max_smem((const void*)k_scan, (int)kSmem);
-  set_max_smem((const void*)k_rows, (int)kSmem);
+  set_max_smem((const void*)k_scan, (int)kSmemScan);
+  set_max_smem((const void*)k_rows, (int)kSmemRows);
   set_max_smem((const void*)k_cols, (int)kSmem);
   for (int l0 = 0; l0 < num_layers; l0 += kMaxL) {
     const int nl = std::min(kMaxL, num_layers - l0);
@@ -981,7 +1073,7 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       blocks[K_CLASSIFY][q] = et;
       blocks[K_SCAN][q] = L.t_rows + L.t_slots;
       blocks[K_SCATTER][q] = et;
-      L.rows_reg = m.rows > 0 ? tiles(m.rows, kSegTile) : 0;
+      L.rows_reg = m.rows > 0 ? tiles(m.rows, kRowsTile) : 0;
       L.cols_reg = csc ? tiles((long long)L.U_max + 1, kSegTile) : 0;
       L.cols_xtra = csc && m.N > 0 ? 2 * sm_count() : 0;
       blocks[K_ROWS][q] = L.rows_reg + (m.rows > 0 ? kLongRowBlocks : 0);
@@ -998,9 +1090,9 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     }
     cudaMemsetAsync(d_ws, 0, (size_t)zero_total, s);
     HF_LAUNCH(k_classify, total[K_CLASSIFY], kBT, 0, s, bp);
-    HF_LAUNCH(k_scan, total[K_SCAN], kBT, kSmem, s, bp);
+    HF_LAUNCH(k_scan, total[K_SCAN], kBT, kSmemScan, s, bp);
     HF_LAUNCH(k_scatter, total[K_SCATTER], kBT, 0, s, bp);
-    HF_LAUNCH(k_rows, total[K_ROWS], kBT, kSmem, s, bp);
+    HF_LAUNCH(k_rows, total[K_ROWS], kBT, kSmemRows, s, bp);
     HF_LAUNCH(k_cols, total[K_COLS], kBT, kSmem, s, bp);
   }
   return last_cuda();
@@ -1014,6 +1106,7 @@ namespace {
 // d_rel_edge_off[r] = lower bound of r in the (sorted) edge-type table.
 __global__ void k_et_offsets(const int* __restrict__ et, long long E, int R,
                              long long* __restrict__ off) {
+  HF_PDL_ENTRY();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r > R) return;
   long long lo = 0, hi = E;
@@ -1025,6 +1118,7 @@ __global__ void k_et_offsets(const int* __restrict__ et, long long E, int R,
 }
 
 __global__ void k_et_check(const int* __restrict__ et, long long E, int R, int* __restrict__ status) {
+  HF_PDL_ENTRY();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E) return;
   const int v = et[i];

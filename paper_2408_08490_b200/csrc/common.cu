@@ -193,6 +193,7 @@ __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_lookback(const int* __restrict__ in, long long n, int* __restrict__ out,
                 int* __restrict__ ticket, int* __restrict__ status) {
+  HF_PDL_ENTRY();
   __shared__ int s_tile, s_prefix;
   __shared__ int sm[kScanTile + kScanTile / 32];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
@@ -263,7 +264,8 @@ k_scan_lookback(const int* __restrict__ in, long long n, int* __restrict__ out,
     out[n] = s_prefix + tot;
 }
 
-__global__ void k_scan_empty(int* out) { out[0] = 0; }
+__global__ void k_scan_empty(int* out) {
+  HF_PDL_ENTRY(); out[0] = 0; }
 
 size_t scan_ws_ints(long long n) { return (size_t)ceil_div(n > 0 ? n : 1, kScanTile) + 2; }
 

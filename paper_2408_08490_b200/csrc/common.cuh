@@ -56,10 +56,49 @@ inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 
 inline bool grid_nonempty(long long g) { return g > 0; }
 inline bool grid_nonempty(dim3 g) { return g.x > 0 && g.y > 0 && g.z > 0; }
 
+// Programmatic dependent launch (PDL): every kernel is launched with
+// programmatic stream serialisation and begins with HF_PDL_ENTRY(): it waits
+// for the previous kernel of its stream to complete (griddepcontrol.wait,
+// before ANY global memory access) and then lets the next one launch
+// (griddepcontrol.launch_dependents).  The next kernel's CTAs are thereby
+// dispatched while this one runs, so a chain of short dependent kernels (the
+// latency-bound steps of a mini-batch) loses the launch/dispatch gap at every
+// boundary; correctness is that of plain stream order (each kernel still
+// starts its work after its predecessor's completion and memory flush).
+// Inside CUDA graphs the edges become programmatic edges.
+#ifndef HF_PDL
+#define HF_PDL 1
+#endif
+#define HF_PDL_ENTRY()                                                         \
+  do {                                                                         \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                         \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");            \
+  } while (0)
+
+inline dim3 to_dim3(dim3 g) { return g; }
+inline dim3 to_dim3(long long g) { return dim3((unsigned)g); }
+
+template <typename... KP, typename... A>
+inline void launch_k(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     A&&... a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = HF_PDL ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<A&&>(a)...);
+}
+
 #define HF_LAUNCH(kernel, grid, block, smem, stream, ...)                      \
   do {                                                                         \
     if (hf::grid_nonempty(grid)) {                                             \
-      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+      hf::launch_k(kernel, hf::to_dim3(grid), hf::to_dim3(block), (smem), (stream), \
+                   __VA_ARGS__);                                               \
       hf::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
     }                                                                          \
   } while (0)

@@ -36,6 +36,7 @@ template <bool RELU>
 __global__ void k_fuse(FuseMeta f, const float4* __restrict__ Z, const float4* __restrict__ R0,
                        const float4* __restrict__ bias, float4* __restrict__ H,
                        const float* __restrict__ beta) {
+  HF_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)f.dst_rows * f.D4) return;
   int o = (int)(idx / f.D4), c = (int)(idx % f.D4);
@@ -76,6 +77,7 @@ template <bool RELU>
 __global__ void __launch_bounds__(256)
 k_fuse_bwd_chunks(FuseBwdMeta f, const float4* __restrict__ dH, const float4* __restrict__ Hv,
                   float4* __restrict__ G, float4* __restrict__ partial) {
+  HF_PDL_ENTRY();
   __shared__ float4 red[256];
   int c = blockIdx.x;
   int t = upper_bound_i(f.chunk_off, f.T + 1, c) - 1;
@@ -110,6 +112,7 @@ k_fuse_bwd_chunks(FuseBwdMeta f, const float4* __restrict__ dH, const float4* __
 // one block per type: threads split the type's chunks, fixed-order smem reduce
 __global__ void __launch_bounds__(256)
 k_fuse_bwd_bias(FuseBwdMeta f, const float4* __restrict__ partial, float4* __restrict__ dbias) {
+  HF_PDL_ENTRY();
   __shared__ float4 red[256];
   int t = blockIdx.x;
   int c = threadIdx.x % f.D4, sub = threadIdx.x / f.D4, nsub = 256 / f.D4;
@@ -191,6 +194,7 @@ k_sem_rows(SemMeta sm, const float* __restrict__ Z, const float* __restrict__ Ws
            const float* __restrict__ G, const float* __restrict__ beta,
            const float* __restrict__ coef, float* __restrict__ dZ, float* __restrict__ Ga,
            float* __restrict__ Th) {
+  HF_PDL_ENTRY();
   constexpr int AP = A + 1, KA = A / 32, KD = D / 32, RW = D > A ? D : A;
   extern __shared__ float ssm[];
   float* sW = ssm;                                  // [D][A+1]
@@ -334,6 +338,7 @@ template <bool BWD>
 __global__ void __launch_bounds__(256)
 k_sem_rel(SemMeta sm, const float* __restrict__ s, const float* __restrict__ beta_in,
           float* __restrict__ out, float* __restrict__ w_out) {
+  HF_PDL_ENTRY();
   __shared__ float red[256];
   __shared__ float val[HF_MAX_R];
   for (int r = 0; r < sm.R; r++) {
@@ -373,6 +378,7 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_sem_dd(SemMeta sm, const float* __restrict__ G, const float* __restrict__ Z,
          float* __restrict__ dd) {
+  HF_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int m = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (m >= sm.rows) return;
@@ -399,6 +405,7 @@ template <int D, int A>
 __global__ void __launch_bounds__(256)
 k_sem_wpart(int rows, int chunk, const float* __restrict__ Z, const float* __restrict__ Ga,
             const float* __restrict__ Th, float* __restrict__ partial) {
+  HF_PDL_ENTRY();
   constexpr int DT = D / 16, CT = A / 16;
   __shared__ float zs[kSemStage][D];
   __shared__ float gs[kSemStage][A];
@@ -454,6 +461,7 @@ k_sem_wpart(int rows, int chunk, const float* __restrict__ Z, const float* __res
 __global__ void __launch_bounds__(256)
 k_sem_wred(int nch, int n, const float* __restrict__ partial, float* __restrict__ dWs, int DA,
            int A, float* __restrict__ dbs, float* __restrict__ dq) {
+  HF_PDL_ENTRY();
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= n) return;
   float s = 0.f;

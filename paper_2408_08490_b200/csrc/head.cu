@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(128)
 k_head_logits(int B, int D, int C, const float* __restrict__ Hs, const float* __restrict__ Wc,
               const float* __restrict__ bc, float* __restrict__ lg, int* __restrict__ tickets,
               int ntickets) {
+  HF_PDL_ENTRY();
   if (blockIdx.x == 0 && blockIdx.y == 0)   // tickets of the next two kernels
     for (int i = threadIdx.x; i < ntickets; i += blockDim.x) tickets[i] = 0;
   float acc[4][4];
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(256)
 k_head_softmax(int B, int C, const int* __restrict__ labels, float* __restrict__ lg,
                float* __restrict__ block_loss, int* __restrict__ ticket, float* __restrict__ loss,
                int* __restrict__ status) {
+  HF_PDL_ENTRY();
   __shared__ float s_l[8];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -250,6 +252,7 @@ k_head_small(int B, int C, const float* __restrict__ Hs, const float* __restrict
              const float* __restrict__ bc, const int* __restrict__ labels,
              float* __restrict__ dlog, float* __restrict__ dHs, float* __restrict__ block_loss,
              int* __restrict__ ticket, float* __restrict__ loss, int* __restrict__ status) {
+  HF_PDL_ENTRY();
   constexpr int KPL = D / 32;              // features per lane
   __shared__ float s_l[8];
   __shared__ int s_last;
@@ -325,7 +328,8 @@ k_head_small(int B, int C, const float* __restrict__ Hs, const float* __restrict
   }
 }
 
-__global__ void k_zero_int(int* p) { *p = 0; }
+__global__ void k_zero_int(int* p) {
+  HF_PDL_ENTRY(); *p = 0; }
 
 struct HeadGrid {
   int dh_tiles_n, dh_tiles;       // dHs: [B, D] tiles (n-major), K = C
@@ -342,6 +346,7 @@ __global__ void __cluster_dims__(kSlices, 1, 1) __launch_bounds__(128)
 k_head_grads(int B, int D, int C, HeadGrid hg, const float* __restrict__ Hs,
              const float* __restrict__ Wc, const float* __restrict__ dlog,
              float* __restrict__ dHs, float* __restrict__ dWc, float* __restrict__ dbc) {
+  HF_PDL_ENTRY();
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ float red[128 * 16];      // this CTA's partial, [thread][16 fragment values]
@@ -424,6 +429,7 @@ static HeadGrid head_grid(int B, int D, int C) {
 }
 
 __global__ void k_sgd(float4* __restrict__ p, const float4* __restrict__ g, long long n4, float lr) {
+  HF_PDL_ENTRY();
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   float4 a = p[i], b = g[i];
@@ -433,6 +439,7 @@ __global__ void k_sgd(float4* __restrict__ p, const float4* __restrict__ g, long
 
 __global__ void k_sgd_tail(float* __restrict__ p, const float* __restrict__ g, long long from,
                            long long n, float lr) {
+  HF_PDL_ENTRY();
   long long i = from + threadIdx.x;
   if (i < n) p[i] -= lr * g[i];
 }

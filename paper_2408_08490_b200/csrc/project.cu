@@ -19,6 +19,7 @@ namespace hf {
 // first wgrad chunk (kCH rows); groups: R relations then T root types.
 __global__ void k_group_table(ProjMeta pm, const int* __restrict__ rel_y_off, int* tile_off,
                               int* chunk_off, int BM, int CH) {
+  HF_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   int t_acc = 0, c_acc = 0;
   for (int g = 0; g < pm.R + pm.T; g++) {
@@ -70,6 +71,7 @@ k_proj_fwd_simt(ProjMeta pm, const int* __restrict__ tile_off, const int* __rest
                 const int* __restrict__ y_src, const int* __restrict__ gather_ids,
                 const float* __restrict__ X, const float* __restrict__ W_rel,
                 const float* __restrict__ W_root, float* __restrict__ Y, float* __restrict__ R0) {
+  HF_PDL_ENTRY();
   constexpr int BM = kBM, BK = 32, TN = D / 16;
   __shared__ __align__(16) float As[BK][BM + 4];
   __shared__ __align__(16) float Bs[BK][D];
@@ -143,6 +145,7 @@ k_proj_fwd_simt(ProjMeta pm, const int* __restrict__ tile_off, const int* __rest
 // v[r][k][h] = sum_c W_r[k, h dh + c] a_dst[r, h, c]   (reading C7 fold)
 __global__ void k_att_fold(int R, int K, int D, int H, const float* __restrict__ W_rel,
                            const float* __restrict__ att, float* __restrict__ v) {
+  HF_PDL_ENTRY();
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= R * K * H) return;
   int h = idx % H, k = (idx / H) % K, r = idx / (H * K);
@@ -158,6 +161,7 @@ __global__ void k_att_fold(int R, int K, int D, int H, const float* __restrict__
 __global__ void k_scores_src(int R, int D, int H, const int* __restrict__ U_dev,
                              const int* __restrict__ rel_y_off, const float* __restrict__ Y,
                              const float* __restrict__ att, float* __restrict__ s_src) {
+  HF_PDL_ENTRY();
   __shared__ int s_yoff[HF_MAX_R + 1];
   for (int i = threadIdx.x; i <= R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
   __syncthreads();
@@ -186,6 +190,7 @@ __global__ void __launch_bounds__(256)
 k_scores_dst(ProjMeta pm, int H, const int* __restrict__ gather_ids,
              const float* __restrict__ X, const float* __restrict__ v,
              float* __restrict__ s_dst) {
+  HF_PDL_ENTRY();
   (void)HMAX;
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -213,9 +218,93 @@ k_scores_dst(ProjMeta pm, int H, const int* __restrict__ gather_ids,
   if (c == 0) s_dst[(long long)row * H + h] = p;
 }
 
+// H <= 8: warp per 2 consecutive merged rows (K = 64: both in one step,
+// half a warp each).  The relation's folded weights v[r] ([K][H], <= 4 KB) are
+// staged once per relation change into shared memory TRANSPOSED ([H][K]), so
+// lane l reads the weights of its features 4l..4l+3 as one conflict-free
+// 16-byte load per head; its X features are one coalesced 16-byte load; H
+// partial dots are summed over the row's lanes by a butterfly.  (Reading
+// v[r][4l..4l+3][0..H) from global per lane made every load instruction
+// touch 32 lines: 30 us on IMDB vs 12 for the lane-per-(head, K-chunk) loop.)
+constexpr int kSdRowsPerWarp = 2;   // (8: latency-bound chains of 8 dependent row loads)
+
+template <int K, int H>
+__global__ void __launch_bounds__(256)
+k_scores_dst_v(ProjMeta pm, const int* __restrict__ gather_ids, const float* __restrict__ X,
+               const float* __restrict__ v, float* __restrict__ s_dst) {
+  HF_PDL_ENTRY();
+  constexpr int LPR = K / 4, RPW = 32 / LPR;
+  __shared__ __align__(16) float vT[8][H * K];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, sl = lane % LPR;
+  float* my = vT[w];
+  const int row0 = (blockIdx.x * 8 + w) * kSdRowsPerWarp;
+  int r_cur = -1;
+  for (int it = 0; it < kSdRowsPerWarp; it += RPW) {
+    const int row = row0 + it + lane / LPR;
+    const int rr = row < pm.rows ? row : pm.rows - 1;
+    if (row0 + it >= pm.rows) break;                           // warp-uniform
+    const int r = upper_bound_i(pm.rel_row_off, pm.R + 1, rr) - 1;
+    // (K = 64: the two half-warp rows may differ in relation only at a
+    // boundary -- stage per half then; rare, handled by the generic path)
+    const int r0w = __shfl_sync(0xffffffffu, r, 0);
+    const bool uni = __all_sync(0xffffffffu, r == r0w);
+    if (uni && r0w != r_cur) {
+      __syncwarp();
+      const float4* src = reinterpret_cast<const float4*>(v + (long long)r0w * K * H);
+      for (int q = lane; q < K * H / 4; q += 32) {
+        const float4 x = __ldg(src + q);
+        const float e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          const int idx = 4 * q + c;
+          my[(idx % H) * K + idx / H] = e[c];
+        }
+      }
+      __syncwarp();
+      r_cur = r0w;
+    }
+    float acc[H];
+    const int t = pm.rel_dst[r];
+    const int x = pm.type_src_off[t] + (rr - pm.rel_row_off[r]);
+    const long long xr = gather_ids ? (long long)gather_ids[x] : (long long)x;
+    const float4 xv = __ldg(reinterpret_cast<const float4*>(X + xr * K) + sl);
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      float4 wv;
+      if (uni) {
+        wv = *reinterpret_cast<const float4*>(my + h * K + 4 * sl);
+      } else {
+        const float* vp = v + ((long long)r * K + 4 * sl) * H + h;
+        wv = make_float4(__ldg(vp), __ldg(vp + H), __ldg(vp + 2 * H), __ldg(vp + 3 * H));
+      }
+      float a = __fmul_rn(xv.x, wv.x);
+      a = fmaf(xv.y, wv.y, a);
+      a = fmaf(xv.z, wv.z, a);
+      acc[h] = fmaf(xv.w, wv.w, a);
+    }
+#pragma unroll
+    for (int o = LPR / 2; o; o >>= 1)
+#pragma unroll
+      for (int h = 0; h < H; h++) acc[h] += __shfl_xor_sync(0xffffffffu, acc[h], o);
+    if (row < pm.rows && sl == 0)
+#pragma unroll
+      for (int h = 0; h < H; h++) s_dst[(long long)row * H + h] = acc[h];
+  }
+}
+
 static void launch_scores_dst(const ProjMeta& pm, int rows, int K, int H,
                               const int* gather_ids, const float* X, const float* v,
                               float* s_dst, cudaStream_t s) {
+#define HF_SV(KK, HH)                                                                   \
+  HF_LAUNCH((k_scores_dst_v<KK, HH>), ceil_div(rows, 8 * kSdRowsPerWarp), 256, 0, s, pm, \
+            gather_ids, X, v, s_dst)
+  if (K == 128 && H == 8) { HF_SV(128, 8); return; }
+  if (K == 64 && H == 8) { HF_SV(64, 8); return; }
+  if (K == 128 && H == 4) { HF_SV(128, 4); return; }
+  if (K == 64 && H == 4) { HF_SV(64, 4); return; }
+  if (K == 128 && H == 1) { HF_SV(128, 1); return; }
+  if (K == 64 && H == 1) { HF_SV(64, 1); return; }
+#undef HF_SV
   const unsigned grid = ceil_div(rows, 8);
 #define HF_SD(KK, HH) \
   HF_LAUNCH((k_scores_dst<KK, HH>), grid, 256, 0, s, pm, H, gather_ids, X, v, s_dst)
@@ -229,6 +318,7 @@ static void launch_scores_dst(const ProjMeta& pm, int rows, int K, int H,
 __global__ void __launch_bounds__(256)
 k_dy_score(int R, int D, int H, const int* __restrict__ U_dev, const int* __restrict__ rel_y_off,
            const float* __restrict__ att, const float* __restrict__ ds_src, float4* __restrict__ dY) {
+  HF_PDL_ENTRY();
   __shared__ int s_yoff[HF_MAX_R + 1];
   for (int i = threadIdx.x; i <= R; i += blockDim.x) s_yoff[i] = rel_y_off[i];
   __syncthreads();
@@ -253,6 +343,7 @@ k_wgrad_partial(ProjMeta pm, const int* __restrict__ chunk_off, const int* __res
                 const int* __restrict__ y_src, const int* __restrict__ gather_ids,
                 const float* __restrict__ X, const float* __restrict__ dY,
                 const float* __restrict__ G, float* __restrict__ partial) {
+  HF_PDL_ENTRY();
   constexpr int RB = 32, TM = K / 16, TN = D / 16;
   __shared__ __align__(16) float As[RB][K];
   __shared__ __align__(16) float Bs[RB][D];
@@ -325,8 +416,9 @@ __global__ void k_wgrad_reduce(int R, int T, int KD, const int* __restrict__ chu
                                const float4* __restrict__ partial, float4* __restrict__ dW_rel,
                                float4* __restrict__ dW_root, ProjMeta pm,
                                const int* __restrict__ rel_y_off, int CH,
-                               const float* __restrict__ dv = nullptr,
-                               const float* __restrict__ att = nullptr, int D = 0, int H = 1) {
+                               const float* __restrict__ dv, const float* __restrict__ att,
+                               int D, int H) {
+  HF_PDL_ENTRY();
   // chunk table: from chunk_off (SIMT path) or rebuilt here from rel_y_off
   __shared__ int s_co[HF_MAX_R + HF_MAX_T + 1];
   if (!chunk_off) {
@@ -386,6 +478,7 @@ __global__ void __launch_bounds__(256)
 k_dgrad(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
         const float* __restrict__ G, const float* __restrict__ W_rel,
         const float* __restrict__ W_root, float* __restrict__ dX) {
+  HF_PDL_ENTRY();
   constexpr int BM = kBM, BK = 32, TN = K / 16;
   __shared__ __align__(16) float As[BK][BM + 4];
   __shared__ __align__(16) float Bs[BK][K];
@@ -495,6 +588,7 @@ k_att_partial(int R, int H, int W, int mode, const int* __restrict__ unused,
               const int* __restrict__ row_off, const float* __restrict__ A,
               const float* __restrict__ B, ProjMeta pm, const int* __restrict__ gather_ids,
               float* __restrict__ partial) {
+  HF_PDL_ENTRY();
   __shared__ int s_tab[HF_MAX_R + 1];
   const int* ro = mode == 1 ? pm.rel_row_off : row_off;   // merged rows: host-known offsets
   att_chunk_table(R, ro, s_tab);
@@ -539,6 +633,7 @@ k_att_partial(int R, int H, int W, int mode, const int* __restrict__ unused,
 
 __global__ void k_att_chunks(int R, const int* __restrict__ row_off, ProjMeta pm,
                              int* chunk_off) {
+  HF_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   const int* ro = row_off ? row_off : pm.rel_row_off;
   int acc = 0;
@@ -557,6 +652,7 @@ __global__ void k_att_chunks(int R, const int* __restrict__ row_off, ProjMeta pm
 //   datt[r,1,hc] = sum_k W_r[k,hc] dv[h][k]                      (k_att_da)
 __global__ void k_att_dv(int R, int K, int H, ProjMeta pm, const float* __restrict__ Pdst,
                          float* __restrict__ dv) {
+  HF_PDL_ENTRY();
   __shared__ int s_tab[HF_MAX_R + 1];
   att_chunk_table(R, pm.rel_row_off, s_tab);
   __syncthreads();
@@ -577,6 +673,7 @@ __global__ void k_att_dv(int R, int K, int H, ProjMeta pm, const float* __restri
 // dW_r[k, d] += dv[r, h(d), k] a_dst[r, d]  (the s_dst chain's weight term)
 __global__ void k_att_dw(int R, int K, int D, int H, const float* __restrict__ dv,
                          const float* __restrict__ att, float* __restrict__ dW_rel) {
+  HF_PDL_ENTRY();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)R * K * D) return;
   const int d = (int)(idx % D), k = (int)((idx / D) % K), r = (int)(idx / ((long long)K * D));
@@ -592,6 +689,7 @@ __global__ void __launch_bounds__(256)
 k_att_da(int R, int K, int D, int H, const int* __restrict__ rel_y_off,
          const float* __restrict__ Psrc, const float* __restrict__ dv,
          const float* __restrict__ W_rel, float* __restrict__ datt) {
+  HF_PDL_ENTRY();
   __shared__ int s_tab[HF_MAX_R + 1];
   __shared__ float red[2][8][32];
   att_chunk_table(R, rel_y_off, s_tab);
@@ -623,6 +721,7 @@ k_att_da(int R, int K, int D, int H, const int* __restrict__ rel_y_off,
 // one thread per (destination row of the layer, k), relations in fixed order.
 __global__ void k_dx_sdst(DgradMeta dm, int dst_rows, int K, int H, const float* __restrict__ v,
                           const float* __restrict__ ds_dst, float* __restrict__ dX) {
+  HF_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)dst_rows * K) return;
   int o = (int)(idx / K), k = (int)(idx % K);
@@ -853,10 +952,12 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
   // d_dW_rel == NULL: input gradient only (RGCN; the caller runs the weight
   // gradient as a separate call, e.g. on a parallel stream)
   const bool wgrad = d_dW_rel != nullptr;
-  if (!csr || !d_X || !d_W_rel || !d_dY || x_rows < 0 || (!wgrad && (!d_dX || d_att)) ||
+  // RGAT input gradient alone: only after hifuse_aggregate_bwd_scored (dY
+  // already holds dYt, so the weights call does not apply the score chain twice)
+  if (!csr || !d_X || !d_W_rel || !d_dY || x_rows < 0 || (!wgrad && (!d_dX || (d_att && !scored))) ||
       (d_W_root && (!d_G || (wgrad && !d_dW_root))))
     return HIFUSE_ERR_INVALID_ARG;
-  if (d_att && (!heads_ok2(D, heads) || !d_ds_src || !d_ds_dst || !d_datt || !d_Y))
+  if (d_att && (!heads_ok2(D, heads) || !d_ds_dst || (wgrad && (!d_ds_src || !d_datt || !d_Y))))
     return HIFUSE_ERR_INVALID_ARG;
   if (d_dX && d_gather_ids) return HIFUSE_ERR_UNSUPPORTED;
   if (ws_bytes < hifuse_project_bwd_ws_bytes(shape, K, D, heads) || !d_ws)
@@ -885,12 +986,27 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
   // parallel branch (the dYt it reads is final after k_dy_score)
   DgradMeta dm;
   if (!wgrad) {
+    // RGAT: the s_dst chain's dX term needs v = W a_dst (weights only): the
+    // fold runs on a parallel branch next to the dgrad, k_dx_sdst after both
+    Branch bf;
+    bool fbr = false;
+    if (d_att) {
+      fbr = branch_begin(s, &bf, 1);
+      HF_LAUNCH(k_att_fold, ceil_div((long long)m.R * K * H, 256), 256, 0, fbr ? bf.side : s,
+                m.R, K, D, H, d_W_rel, d_att, v);
+    }
     if (prec == HIFUSE_PREC_TF32) {
       make_dgrad_meta(m, d_W_root != nullptr, &dm, 128);
       rc = dgrad_tc_launch(dm, K, D, csr->slot_y, d_dY, d_G, d_W_rel, d_W_root, d_dX, s, U_max,
                            m.R);
-      return rc != HIFUSE_OK ? rc : last_cuda();
+      if (fbr) branch_end(s, bf);
+      if (rc != HIFUSE_OK) return rc;
+      if (d_att)
+        HF_LAUNCH(k_dx_sdst, ceil_div((long long)m.dst_rows * K, 256), 256, 0, s, dm,
+                  m.dst_rows, K, H, v, d_ds_dst, d_dX);
+      return last_cuda();
     }
+    if (fbr) branch_end(s, bf);
     make_dgrad_meta(m, d_W_root != nullptr, &dm);
     unsigned gd = dm.tile_off[m.T];
 #define HF_DG(KK, DD)                                                                         \
@@ -900,6 +1016,9 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
     else if (K == 64 && D == 128) HF_DG(64, 128);
     else HF_DG(64, 64);
 #undef HF_DG
+    if (d_att)
+      HF_LAUNCH(k_dx_sdst, ceil_div((long long)m.dst_rows * K, 256), 256, 0, s, dm, m.dst_rows,
+                K, H, v, d_ds_dst, d_dX);
     return last_cuda();
   }
   Branch br;
@@ -983,7 +1102,8 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
   // branch, measured +3 us per RGAT layer on IMDB)
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
             prec == HIFUSE_PREC_TF32 ? (const int*)nullptr : (const int*)chunk_off,
-            (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root, pm, csr->rel_y_off, CH);
+            (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root, pm, csr->rel_y_off, CH,
+            (const float*)nullptr, (const float*)nullptr, 0, 1);
   if (d_att) {
     if (abr) branch_end(s, ba);
     HF_LAUNCH(k_att_dw, ceil_div((long long)m.R * K * D, 256), 256, 0, s, m.R, K, D, H, dvb, d_att,
@@ -1116,7 +1236,7 @@ hifuse_status hifuse_project_aggregated_bwd(const hifuse_layer_shape* shape,
   int G = d_dW_root ? m.R + m.T : m.R;
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
             (const int*)nullptr, (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root,
-            pm, csr->rel_row_off, CH);
+            pm, csr->rel_row_off, CH, (const float*)nullptr, (const float*)nullptr, 0, 1);
   return last_cuda();
 }
 

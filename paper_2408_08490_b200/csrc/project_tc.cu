@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(160)
 k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
            const float* __restrict__ G, const float* __restrict__ W_rel,
            const float* __restrict__ W_root, float* __restrict__ dX, int max_out) {
+  HF_PDL_ENTRY();
   // warps 0-3: producers, whole chunks round-robin (warp w loads chunks
   //            w, w + 4, ...: up to four chunks in flight even though each
   //            warp waits for its own cp.async group before the proxy fence);
@@ -254,6 +255,7 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
            const int* __restrict__ y_src, const int* __restrict__ gather_ids,
            const float* __restrict__ X, const float* __restrict__ dY, const float* __restrict__ G,
            float* __restrict__ partial, const float* __restrict__ Xm) {
+  HF_PDL_ENTRY();
   constexpr int MA = 128;                               // padded M (features)
   constexpr uint32_t BLK = 4096;                        // one 32-feature block of 32 rows
   constexpr uint32_t A_STAGE = (MA / 32) * BLK, B_STAGE = (D / 32) * BLK, STAGE = A_STAGE + B_STAGE;
@@ -521,6 +523,7 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
                float* __restrict__ Y, float* __restrict__ R0, const float* __restrict__ att,
                float* __restrict__ s_src, int H, const float* __restrict__ Xm,
                const uint16_t* __restrict__ Wt, uint16_t* __restrict__ Yb) {
+  HF_PDL_ENTRY();
   constexpr int BM = 128, KC = BF ? 64 : 32, NC = K / KC;   // K elements per 128-byte row
   constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
   constexpr uint32_t STAGE = A_STAGE + B_STAGE;
@@ -765,6 +768,7 @@ k_proj_fwd_tcp(ProjMeta pm, const int* __restrict__ rel_y_off, const int* __rest
 // weights (transposed to K-major, the B layout of the BF16 projection).
 __global__ void k_w_bf16t(int R, int T, int K, int D, const float* __restrict__ W_rel,
                           const float* __restrict__ W_root, uint16_t* __restrict__ Wt) {
+  HF_PDL_ENTRY();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long per = (long long)K * D;
   if (i >= (R + T) * per) return;
@@ -804,6 +808,7 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
                 const float* __restrict__ Xm, const float* __restrict__ W_rel,
                 const float* __restrict__ W_root, const float* __restrict__ bias,
                 float* __restrict__ H) {
+  HF_PDL_ENTRY();
   constexpr int BM = 128, NCS = K / 32;                      // chunks per K segment
   constexpr uint32_t A_STAGE = BM * 128, B_BLK = 32 * 128, B_STAGE = (D / 32) * B_BLK;
   constexpr uint32_t STAGE = A_STAGE + B_STAGE;

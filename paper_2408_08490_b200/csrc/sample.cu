@@ -3,7 +3,7 @@
 // documents the contract.  Per hop (innermost layer first), 7 kernels and two
 // scans, independent of R and of the batch:
 //   k_smp_mark_dst  destinations: gen[v] = stamp, loc[v] = local id
-//   k_smp_pairs     thread per (destination, relation into its type): Floyd's
+//   k_smp_pairs     warp per (destination, relation into its type): Floyd's
 //                   uniform k-subset of the in-list (k = min(deg, fanout)),
 //                   sorted; picks go to fixed slots; first sight of a new
 //                   source vertex (atomicExch on gen) sets its bit in a
@@ -16,12 +16,23 @@
 //   k_smp_edges     compaction of the slots into (src_local, dst_local, eid)
 // Randomness: splitmix64 counter hash of (hop key, r, v, j): no RNG state.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 #include "common.cuh"
 
 namespace hf {
 
 static constexpr int kMaxFan = 64;
+
+// Padded (capacity) layout of one hop's block (hifuse_sample_blocks_padded):
+// type t's sources start at off[t] (prefix of the per-type capacities), slots
+// past the sampled ones hold -1 (gather id: the type's first row), edge
+// positions [N, ecap) are null edges (edge_id -1).  on = 0: compact layout.
+struct PadCaps {
+  int on;
+  int off[HF_MAX_T + 1];
+  long long ecap;
+};
 
 struct SmpMeta {
   int T, R, Rmax;
@@ -55,6 +66,7 @@ __device__ __forceinline__ int type_of(const int* fo, int T, int d) {
 }
 
 __global__ void k_smp_init(int T, int target, int B, int* __restrict__ fo) {
+  HF_PDL_ENTRY();
   int t = threadIdx.x;
   if (t <= T) fo[t] = t <= target ? 0 : B;
 }
@@ -62,7 +74,9 @@ __global__ void k_smp_init(int T, int target, int B, int* __restrict__ fo) {
 __global__ void __launch_bounds__(256)
 k_smp_mark_dst(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ front,
                int* __restrict__ gen, int* __restrict__ loc, int stamp,
-               const unsigned long long* __restrict__ d_ctl, int hop, int* __restrict__ status) {
+               const unsigned long long* __restrict__ d_ctl, int hop, int pad,
+               int* __restrict__ status) {
+  HF_PDL_ENTRY();
   __shared__ int fo[HF_MAX_T + 1];
   for (int i = threadIdx.x; i <= m.T; i += blockDim.x) fo[i] = fo_d[i];
   __syncthreads();
@@ -71,6 +85,7 @@ k_smp_mark_dst(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ 
   if (d >= fo[m.T]) return;
   const int t = type_of(fo, m.T, d);
   const int v = front[d];
+  if (pad && v == -1) return;                     // padding slot of the previous hop
   if (v < 0 || v >= m.count[t]) {
     atomicOr(status, HIFUSE_ST_BAD_DST);
     return;
@@ -80,7 +95,20 @@ k_smp_mark_dst(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ 
   loc[g] = d - fo[t];
 }
 
-__global__ void __launch_bounds__(128)
+// Warp per (destination, relation into its type) pair.  Floyd's picks are
+// resolved in order, but the hashes are not sequential: lane i hashes step i
+// (and i + 32), the recurrence then costs one shuffle and one ballot per
+// step, with the selected in-list positions held one per lane (entries n and
+// n + 32 in s0 / s1).  The positions are ranked (ascending in-list order) and
+// each lane does the memory work of its picks -- in-list loads, first-sight
+// atomicExch / bitmap atomicOr, slot stores -- so a pair's k picks cost one
+// round trip.  Measured on ogbn-mag (us per hop, inner / outer): thread per
+// pair with serial picks 56 / 56 (k dependent atomic round trips); warp per
+// pair hashing every step on every lane 10 / 75 (32x redundant hashes);
+// thread per pair + warp-cooperative picks 62 / 66 (32 dependent rounds).
+constexpr int kSmpWarps = 8;
+
+__global__ void __launch_bounds__(kSmpWarps * 32)
 k_smp_pairs(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ front, int P, int f,
             unsigned long long hk, const unsigned long long* __restrict__ d_ctl, int hop,
             const long long* __restrict__ in_ptr,
@@ -88,18 +116,28 @@ k_smp_pairs(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ fro
             int* __restrict__ gen, unsigned* __restrict__ bitmap, int stamp,
             int* __restrict__ slot_src, long long* __restrict__ slot_eid,
             int* __restrict__ pair_cnt) {
+  HF_PDL_ENTRY();
   __shared__ int fo[HF_MAX_T + 1];
+  __shared__ int sorted[kSmpWarps][kMaxFan];
   for (int i = threadIdx.x; i <= m.T; i += blockDim.x) fo[i] = fo_d[i];
   __syncthreads();
   if (d_ctl) {                       // key and stamp base from device memory
     hk = mix64(d_ctl[0] ^ (0x1000ull + (unsigned long long)hop));
     stamp = (int)d_ctl[1] + hop;
   }
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  const int d = p / m.Rmax, q = p % m.Rmax;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // grid-stride over the pairs of the actual frontier (fo[T] destinations;
+  // the host bound P is the worst case: a grid over it spent most of its time
+  // dispatching blocks that exit)
+  const long long Pact = min((long long)P, (long long)fo[m.T] * m.Rmax);
+  for (long long p = Pact + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (long long)gridDim.x * blockDim.x)
+    pair_cnt[p] = 0;                                   // past the frontier (scanned over P)
+  for (long long p = (long long)blockIdx.x * kSmpWarps + w; p < Pact;
+       p += (long long)gridDim.x * kSmpWarps) {
+  const int d = (int)(p / m.Rmax), q = (int)(p % m.Rmax);
   int k = 0;
-  if (d < fo[m.T]) {
+  {
     const int t = type_of(fo, m.T, d);
     const int v = front[d];
     if (q < m.trel_off[t + 1] - m.trel_off[t] && v >= 0 && v < m.count[t]) {
@@ -108,47 +146,68 @@ k_smp_pairs(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ fro
       const long long base = ptr[0];
       const int deg = (int)(ptr[1] - base);
       k = min(deg, f);
-      int sel[kMaxFan];
-      if (deg <= f) {
-        for (int j = 0; j < k; j++) sel[j] = j;
+      int* srt = sorted[w];
+      if (deg <= f) {                                  // every in-edge, in order
+        for (int j = lane; j < k; j += 32) srt[j] = j;
       } else {
-        // Floyd: for j = deg-k .. deg-1, t = U[0, j]; take t unless taken, else j
-        int n = 0;
-        for (int j = deg - k; j < deg; j++) {
-          const int c = rand_upto(hk, r, v, j);
-          bool taken = false;
-          for (int a = 0; a < n; a++) taken |= sel[a] == c;
-          sel[n++] = taken ? j : c;
+        // Floyd: for j = deg-k .. deg-1, c = U[0, j]; take c unless taken, else j
+        const int j0 = deg - k;
+        const int c0 = lane < k ? rand_upto(hk, r, v, j0 + lane) : 0;
+        const int c1 = lane + 32 < k ? rand_upto(hk, r, v, j0 + lane + 32) : 0;
+        int s0 = 0x7fffffff, s1 = 0x7fffffff;
+        for (int i = 0; i < k; i++) {
+          const int c = i < 32 ? __shfl_sync(0xffffffffu, c0, i)
+                               : __shfl_sync(0xffffffffu, c1, i - 32);
+          const bool taken = __any_sync(0xffffffffu, s0 == c || s1 == c);
+          const int val = taken ? j0 + i : c;
+          if (i == lane) s0 = val;
+          else if (i == lane + 32) s1 = val;
         }
-        for (int a = 1; a < k; a++) {                 // ascending in-list order
-          const int x = sel[a];
-          int b = a - 1;
-          while (b >= 0 && sel[b] > x) { sel[b + 1] = sel[b]; b--; }
-          sel[b + 1] = x;
+        // ascending in-list order: rank among the k (distinct) entries
+        int r0 = 0, r1 = 0;
+        const int na = k < 32 ? k : 32;
+        for (int a = 0; a < na; a++) {
+          const int x0 = __shfl_sync(0xffffffffu, s0, a);
+          r0 += x0 < s0;
+          r1 += x0 < s1;
         }
+        if (k > 32)
+          for (int a = 0; a < k - 32; a++) {
+            const int x1 = __shfl_sync(0xffffffffu, s1, a);
+            r0 += x1 < s0;
+            r1 += x1 < s1;
+          }
+        if (lane < k) srt[r0] = s0;
+        if (lane + 32 < k) srt[r1] = s1;
       }
+      __syncwarp();
       const int s = m.rel_src[r];
-      for (int j = 0; j < k; j++) {
-        const long long e = base + sel[j];
+      for (int j = lane; j < k; j += 32) {
+        const long long e = base + srt[j];
         const int u = in_src[e];
+        const long long id = in_eid[e];
         if (atomicExch(gen + m.goff[s] + u, stamp) != stamp)
           atomicOr(bitmap + m.wbase[s] + (u >> 5), 1u << (u & 31));
-        slot_src[(long long)p * f + j] = u;
-        slot_eid[(long long)p * f + j] = in_eid[e];
+        slot_src[p * f + j] = u;
+        slot_eid[p * f + j] = id;
       }
+      __syncwarp();                                    // srt reused by the next pair
     }
   }
-  pair_cnt[p] = k;
+  if (lane == 0) pair_cnt[p] = k;
+  }
 }
 
 __global__ void k_smp_popc(const unsigned* __restrict__ bitmap, int W, int* __restrict__ wcnt) {
+  HF_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < W) wcnt[i] = __popc(bitmap[i]);
 }
 
 __global__ void k_smp_counts(SmpMeta m, const int* __restrict__ fo, const int* __restrict__ wscan,
                              const int* __restrict__ pscan, int P, int* __restrict__ counts,
-                             int* __restrict__ so) {
+                             int* __restrict__ so, PadCaps pc, int* __restrict__ status) {
+  HF_PDL_ENTRY();
   __shared__ int ns[HF_MAX_T];
   const int t = threadIdx.x;
   if (t < m.T) {
@@ -157,13 +216,18 @@ __global__ void k_smp_counts(SmpMeta m, const int* __restrict__ fo, const int* _
     ns[t] = nd + nn;
     counts[t] = nd + nn;
     counts[m.T + t] = nd;
+    if (pc.on && nd + nn > pc.off[t + 1] - pc.off[t]) atomicOr(status, HIFUSE_ST_OVERFLOW);
   }
   __syncthreads();
   if (t == 0) {
     int a = 0;
-    for (int q = 0; q < m.T; q++) { so[q] = a; a += ns[q]; }
-    so[m.T] = a;
+    for (int q = 0; q < m.T; q++) {
+      so[q] = pc.on ? pc.off[q] : a;
+      a += ns[q];
+    }
+    so[m.T] = pc.on ? pc.off[m.T] : a;
     counts[2 * m.T] = pscan[P];
+    if (pc.on && pscan[P] > pc.ecap) atomicOr(status, HIFUSE_ST_OVERFLOW);
   }
 }
 
@@ -171,6 +235,7 @@ __global__ void __launch_bounds__(256)
 k_smp_assign(SmpMeta m, int W, const int* __restrict__ fo_d, const int* __restrict__ so_d,
              const int* __restrict__ front, const unsigned* __restrict__ bitmap,
              const int* __restrict__ wscan, int* __restrict__ loc, int* __restrict__ src_gid) {
+  HF_PDL_ENTRY();
   __shared__ int fo[HF_MAX_T + 1], so[HF_MAX_T + 1];
   for (int i = threadIdx.x; i <= m.T; i += blockDim.x) { fo[i] = fo_d[i]; so[i] = so_d[i]; }
   __syncthreads();
@@ -184,13 +249,14 @@ k_smp_assign(SmpMeta m, int W, const int* __restrict__ fo_d, const int* __restri
     const int nd = fo[s + 1] - fo[s];
     const int r0 = wscan[w] - wscan[m.wbase[s]];
     int k = 0;
+    const int cap = so[s + 1] - so[s];            // (padded layout: overflow past it)
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
       const int u = (w - m.wbase[s]) * 32 + b;
       const int l = nd + r0 + k++;
       loc[m.goff[s] + u] = l;
-      src_gid[so[s] + l] = u;
+      if (l < cap) src_gid[so[s] + l] = u;
     }
   } else {                                       // destinations: the prefix
     const long long d = x - W;
@@ -200,39 +266,62 @@ k_smp_assign(SmpMeta m, int W, const int* __restrict__ fo_d, const int* __restri
   }
 }
 
+// Compaction of the slots into (src_local, dst_local, eid): thread per
+// (pair, pick) slot.  Padded layout: positions [N, ecap) become null edges.
 __global__ void __launch_bounds__(256)
 k_smp_edges(SmpMeta m, int f, long long nslots, const int* __restrict__ fo_d,
-            const int* __restrict__ pair_cnt, const int* __restrict__ pscan,
+            const int* __restrict__ pair_cnt, const int* __restrict__ pscan, int P,
             const int* __restrict__ slot_src, const long long* __restrict__ slot_eid,
             const int* __restrict__ loc, int* __restrict__ src_local,
-            int* __restrict__ dst_local, long long* __restrict__ edge_id) {
-  __shared__ int fo[HF_MAX_T + 1];
-  for (int i = threadIdx.x; i <= m.T; i += blockDim.x) fo[i] = fo_d[i];
+            int* __restrict__ dst_local, long long* __restrict__ edge_id, long long ecap,
+            const int* __restrict__ so_d) {
+  HF_PDL_ENTRY();
+  __shared__ int fo[HF_MAX_T + 1], so[HF_MAX_T + 1];
+  for (int i = threadIdx.x; i <= m.T; i += blockDim.x) { fo[i] = fo_d[i]; so[i] = so_d[i]; }
   __syncthreads();
-  const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nslots) return;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long x0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ecap >= 0)                                  // padded layout: null edges at [N, ecap)
+    for (long long x = pscan[P] + x0; x < ecap; x += nth) {
+      src_local[x] = 0;
+      dst_local[x] = 0;
+      edge_id[x] = -1;
+    }
+  // slots of the actual frontier's pairs (pair_cnt past it was never written)
+  const long long nact = min(nslots, (long long)fo[m.T] * m.Rmax * f);
+  for (long long x = x0; x < nact; x += nth) {
   const int p = (int)(x / f), j = (int)(x % f);
-  if (j >= pair_cnt[p]) return;
+  if (j >= pair_cnt[p]) continue;
   const int pos = pscan[p] + j;
+  if (ecap >= 0 && pos >= ecap) continue;         // overflow (flagged by k_smp_counts)
   const int d = p / m.Rmax, q = p % m.Rmax;
   const int t = type_of(fo, m.T, d);
   const int r = m.trel[m.trel_off[t] + q];
   const int s = m.rel_src[r];
-  src_local[pos] = loc[m.goff[s] + slot_src[x]];
+  const int ls = loc[m.goff[s] + slot_src[x]];
+  if (ecap >= 0 && ls >= so[s + 1] - so[s]) {     // overflowed source: null edge (the block
+    src_local[pos] = 0;                           // stays a valid, truncated one; the caller
+    dst_local[pos] = 0;                           // re-samples it, HIFUSE_ST_OVERFLOW)
+    edge_id[pos] = -1;
+    continue;
+  }
+  src_local[pos] = ls;
   dst_local[pos] = d - fo[t];
   edge_id[pos] = slot_eid[x];
+  }
 }
 
 __global__ void __launch_bounds__(256)
 k_smp_gather(SmpMeta m, const int* __restrict__ so_d, const int* __restrict__ src_gid,
              int* __restrict__ gather_ids) {
+  HF_PDL_ENTRY();
   __shared__ int so[HF_MAX_T + 1];
   for (int i = threadIdx.x; i <= m.T; i += blockDim.x) so[i] = so_d[i];
   __syncthreads();
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= so[m.T]) return;
-  const int t = type_of(so, m.T, x);
-  gather_ids[x] = (int)(m.goff[t] + src_gid[x]);
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < so[m.T]; x += gridDim.x * blockDim.x) {
+    const int t = type_of(so, m.T, x);
+    gather_ids[x] = (int)(m.goff[t] + max(src_gid[x], 0));   // padding slot: the type's row 0
+  }
 }
 
 struct SmpPlan {
@@ -319,16 +408,40 @@ hifuse_status hifuse_sample_caps(const hifuse_graph_csc* g, int num_layers, cons
   return HIFUSE_OK;
 }
 
-hifuse_status hifuse_sample_blocks(const hifuse_graph_csc* g, int num_layers,
-                                   const int32_t* fanout_h, const int32_t* d_seeds,
-                                   int64_t num_seeds, int32_t target_type, uint64_t key,
-                                   const uint64_t* d_ctl, int32_t stamp, hifuse_block* out,
-                                   int32_t* d_state,
-                                   void* d_ws, size_t ws_bytes, int32_t* d_status,
-                                   hifuse_stream_t stream) {
+}  // extern "C"
+
+// Shared body of hifuse_sample_blocks (compact layout: src_cap_h == NULL) and
+// hifuse_sample_blocks_padded (per-type source capacities, padded edge tail).
+static hifuse_status sample_impl(const hifuse_graph_csc* g, int num_layers,
+                                 const int32_t* fanout_h, const int32_t* d_seeds,
+                                 int64_t num_seeds, int32_t target_type, uint64_t key,
+                                 const uint64_t* d_ctl, int32_t stamp, const int64_t* src_cap_h,
+                                 const int64_t* edge_pad_h, hifuse_block* out, int32_t* d_state,
+                                 void* d_ws, size_t ws_bytes, int32_t* d_status,
+                                 hifuse_stream_t stream) {
   SmpPlan pl;
   hifuse_status rc = make_plan(g, num_layers, fanout_h, num_seeds, &pl);
   if (rc != HIFUSE_OK) return rc;
+  const bool padded = src_cap_h != nullptr;
+  if (padded) {
+    // per layer l: caps >= 0, sum <= the worst-case source capacity; the
+    // layer's destinations (layer l+1's sources, or the seeds) fit its sources;
+    // the padded edge count <= the worst-case edge capacity
+    if (!edge_pad_h) return HIFUSE_ERR_INVALID_ARG;
+    for (int h = 0; h < num_layers; h++) {
+      const int l = num_layers - 1 - h;
+      long long tot = 0;
+      for (int t = 0; t < pl.T; t++) {
+        const long long c = src_cap_h[(long long)l * pl.T + t];
+        const long long d = l == num_layers - 1 ? (t == target_type ? num_seeds : 0)
+                                                : src_cap_h[(long long)(l + 1) * pl.T + t];
+        if (c < 0 || c < d) return HIFUSE_ERR_INVALID_ARG;
+        tot += c;
+      }
+      if (tot > pl.S[h] || edge_pad_h[l] < 0 || edge_pad_h[l] > pl.E[h])
+        return HIFUSE_ERR_INVALID_ARG;
+    }
+  }
   if (target_type < 0 || target_type >= pl.T || stamp < 1 || !d_state || !d_status || !out ||
       (num_seeds > 0 && !d_seeds) || !g->d_in_ptr || (pl.R > 0 && (!g->d_in_src || !g->d_in_eid)))
     return HIFUSE_ERR_INVALID_ARG;
@@ -391,26 +504,70 @@ hifuse_status hifuse_sample_blocks(const hifuse_graph_csc* g, int num_layers,
     const int stp = stamp + h;
     hifuse_block& o = out[l];
     const long long D = pl.D[h], P = pl.P[h];
+    PadCaps pc;
+    memset(&pc, 0, sizeof(pc));
+    pc.ecap = -1;
+    long long cap_tot = 0;
+    if (padded) {
+      pc.on = 1;
+      for (int t = 0; t < pl.T; t++) {
+        pc.off[t] = (int)cap_tot;
+        cap_tot += src_cap_h[(long long)l * pl.T + t];
+      }
+      pc.off[pl.T] = (int)cap_tot;
+      pc.ecap = edge_pad_h[l];
+      // padding slots of the type-major source list read -1
+      cudaMemsetAsync(o.src_gid, 0xff, sizeof(int) * std::max(cap_tot, 1ll), s);
+    }
     cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * std::max(pl.W, 1), s);
     HF_LAUNCH(k_smp_mark_dst, ceil_div(D, 256), 256, 0, s, m, fo, front, gen, loc, stp,
-              (const unsigned long long*)d_ctl, h, d_status);
-    HF_LAUNCH(k_smp_pairs, ceil_div(P, 128), 128, 0, s, m, fo, front, (int)P, f, hk,
+              (const unsigned long long*)d_ctl, h, padded && h > 0 ? 1 : 0, d_status);
+    const long long cap_blocks = (long long)sm_count() * 8;   // grid-stride kernels
+    HF_LAUNCH(k_smp_pairs, std::min<long long>(ceil_div(P, kSmpWarps), cap_blocks), kSmpWarps * 32, 0, s, m, fo, front, (int)P, f, hk,
               (const unsigned long long*)d_ctl, h, (const long long*)g->d_in_ptr, g->d_in_src, (const long long*)g->d_in_eid, gen,
               bitmap, stp, slot_src, slot_eid, pair_cnt);
     HF_LAUNCH(k_smp_popc, ceil_div(pl.W, 256), 256, 0, s, bitmap, pl.W, wcnt);
     exclusive_scan(wcnt, wscan, pl.W, wscan_ws, s);
     exclusive_scan(pair_cnt, pscan, P, pscan_ws, s);
-    HF_LAUNCH(k_smp_counts, 1, HF_MAX_T, 0, s, m, fo, wscan, pscan, (int)P, o.counts, so);
+    HF_LAUNCH(k_smp_counts, 1, HF_MAX_T, 0, s, m, fo, wscan, pscan, (int)P, o.counts, so, pc,
+              d_status);
     HF_LAUNCH(k_smp_assign, ceil_div(pl.W + D, 256), 256, 0, s, m, pl.W, fo, so, front, bitmap,
               wscan, loc, o.src_gid);
-    HF_LAUNCH(k_smp_edges, ceil_div(P * f, 256), 256, 0, s, m, f, P * f, fo, pair_cnt, pscan,
-              slot_src, slot_eid, loc, o.src_local, o.dst_local, (long long*)o.edge_id);
+    HF_LAUNCH(k_smp_edges, std::min<long long>(ceil_div(P * f, 256), cap_blocks), 256, 0, s, m, f, P * f, fo, pair_cnt, pscan,
+              (int)P, slot_src, slot_eid, loc, o.src_local, o.dst_local, (long long*)o.edge_id,
+              pc.ecap, so);
     if (o.gather_ids)
-      HF_LAUNCH(k_smp_gather, ceil_div(pl.S[h], 256), 256, 0, s, m, so, o.src_gid, o.gather_ids);
+      HF_LAUNCH(k_smp_gather, std::min<long long>(ceil_div(padded ? std::max(cap_tot, 1ll) : pl.S[h], 256), cap_blocks), 256, 0,
+                s, m, so, o.src_gid, o.gather_ids);
     front = o.src_gid;
     std::swap(fo, so);
   }
   return last_cuda();
 }
 
+extern "C" {
+
+hifuse_status hifuse_sample_blocks(const hifuse_graph_csc* g, int num_layers,
+                                   const int32_t* fanout_h, const int32_t* d_seeds,
+                                   int64_t num_seeds, int32_t target_type, uint64_t key,
+                                   const uint64_t* d_ctl, int32_t stamp, hifuse_block* out,
+                                   int32_t* d_state,
+                                   void* d_ws, size_t ws_bytes, int32_t* d_status,
+                                   hifuse_stream_t stream) {
+  return sample_impl(g, num_layers, fanout_h, d_seeds, num_seeds, target_type, key, d_ctl, stamp,
+                     nullptr, nullptr, out, d_state, d_ws, ws_bytes, d_status, stream);
+}
+
+hifuse_status hifuse_sample_blocks_padded(const hifuse_graph_csc* g, int num_layers,
+                                          const int32_t* fanout_h, const int32_t* d_seeds,
+                                          int64_t num_seeds, int32_t target_type, uint64_t key,
+                                          const uint64_t* d_ctl, int32_t stamp,
+                                          const int64_t* src_cap_h, const int64_t* edge_pad_h,
+                                          hifuse_block* out, int32_t* d_state, void* d_ws,
+                                          size_t ws_bytes, int32_t* d_status,
+                                          hifuse_stream_t stream) {
+  if (!src_cap_h || !edge_pad_h) return HIFUSE_ERR_INVALID_ARG;
+  return sample_impl(g, num_layers, fanout_h, d_seeds, num_seeds, target_type, key, d_ctl, stamp,
+                     src_cap_h, edge_pad_h, out, d_state, d_ws, ws_bytes, d_status, stream);
+}
 }  // extern "C"

@@ -52,6 +52,7 @@ __device__ __forceinline__ int block_excl_scan_1024(int v, int* red, int* total)
 __global__ void __launch_bounds__(kPlanThreads)
 k_shard_plan(const int* __restrict__ ids, int n, const long long* __restrict__ bounds, int W,
              int* __restrict__ counts, int* __restrict__ order, int* __restrict__ status) {
+  HF_PDL_ENTRY();
   __shared__ long long sb[65];
   __shared__ int red[32];
   const int t = threadIdx.x;
@@ -85,6 +86,7 @@ k_shard_plan(const int* __restrict__ ids, int n, const long long* __restrict__ b
 template <typename V>
 __global__ void k_gather_words(const V* __restrict__ src, const int* __restrict__ idx, long long n,
                                int vpr, long long base, V* __restrict__ dst) {
+  HF_PDL_ENTRY();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * vpr) return;
   const long long r = i / vpr, c = i % vpr;
@@ -94,6 +96,7 @@ __global__ void k_gather_words(const V* __restrict__ src, const int* __restrict_
 template <typename V>
 __global__ void k_scatter_words(const V* __restrict__ src, const int* __restrict__ idx,
                                 long long n, int vpr, V* __restrict__ dst) {
+  HF_PDL_ENTRY();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * vpr) return;
   const long long r = i / vpr, c = i % vpr;

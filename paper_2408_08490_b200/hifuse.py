@@ -111,6 +111,8 @@ def lib():
             "hifuse_sample_caps": [vp, i32, vp, i64, vp, vp, vp, vp],
             "hifuse_sample_blocks": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, vp, i32, vp, vp,
                                      vp, sz, vp, vp],
+            "hifuse_sample_blocks_padded": [vp, i32, vp, vp, i64, i32, ctypes.c_uint64, vp, i32,
+                                            vp, vp, vp, vp, vp, sz, vp, vp],
             "hifuse_read_status": [vp, vp, vp],
             "hifuse_sem_att_ws_bytes": [vp, i32, i32],
             "hifuse_aggregate_features_cols_bf16": [vp, vp, i32, i32, vp, i64, vp, vp, vp, vp, vp],
@@ -448,6 +450,20 @@ def sample_blocks(graph, fanout, seeds, target_type, key, stamp, blocks, state, 
         ctypes.byref(graph), len(fan), fan.ctypes.data, _ptr(seeds), seeds.numel(), target_type,
         ctypes.c_uint64(key), _ptr(d_ctl), stamp, arr, _ptr(state), _ptr(ws), ws.numel() * ws.element_size(),
         _ptr(status), _stream(stream)))
+
+
+def sample_blocks_padded(graph, fanout, seeds, target_type, key, stamp, src_cap, edge_pad, blocks,
+                         state, ws, status, stream=None, d_ctl=None):
+    """src_cap: int64 [L, T] per-layer per-type source capacities (outer layer
+    first); edge_pad: int64 [L] padded edge counts (include/hifuse.h)."""
+    fan = np.ascontiguousarray(fanout, np.int32)
+    cap = np.ascontiguousarray(src_cap, np.int64)
+    pad = np.ascontiguousarray(edge_pad, np.int64)
+    arr = (Block * len(blocks))(*blocks)
+    _check("hifuse_sample_blocks_padded", lib().hifuse_sample_blocks_padded(
+        ctypes.byref(graph), len(fan), fan.ctypes.data, _ptr(seeds), seeds.numel(), target_type,
+        ctypes.c_uint64(key), _ptr(d_ctl), stamp, cap.ctypes.data, pad.ctypes.data, arr,
+        _ptr(state), _ptr(ws), ws.numel() * ws.element_size(), _ptr(status), _stream(stream)))
 
 
 def read_status(status, stream=None):

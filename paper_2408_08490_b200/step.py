@@ -444,6 +444,26 @@ class Trainer:
                     hf.project_bwd(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
                                    P["W_root"], None, a["Y"], b["dY"], b["G"], None, None, None,
                                    Gr["W_rel"], Gr["W_root"], None, b["wsw"], prec=self.prec_tc))))
+            elif P["att"] is not None and b["dX"] is not None:
+                # RGAT inner layer: the input gradient (dgrad + the s_dst chain's
+                # dX term) on the critical path, the weight / attention
+                # gradients as a second call on the side stream, overlapping the
+                # outer layer's backward (both calls read the dYt left by
+                # hifuse_aggregate_bwd_scored / _rows)
+                b["wsw"] = self._ws(hf.project_bwd_ws_bytes(sh, a["K"], D, H), key=f"ws_wg{l}")
+                ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P:
+                            hf.project_bwd_scored(sh, c, a["K"], D, H, a["X"], a["gid"],
+                                                  P["W_rel"], P["W_root"], P["att"], a["Y"],
+                                                  b["dY"], b["G"], b["ds_src"], b["ds_dst"],
+                                                  b["dX"], None, None, None, b["wsq"],
+                                                  prec=self.prec_tc)))
+                ops.append((f"project_wgrad.{l}", side_op(
+                    lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr:
+                    hf.project_bwd_scored(sh, c, a["K"], D, H, a["X"], a["gid"], P["W_rel"],
+                                          P["W_root"], P["att"], a["Y"], b["dY"], b["G"],
+                                          b["ds_src"], b["ds_dst"], None, Gr["W_rel"],
+                                          Gr["W_root"], Gr["att"], b["wsw"],
+                                          prec=self.prec_tc))))
             else:
                 pb = hf.project_bwd_scored if P["att"] is not None else hf.project_bwd
                 ops.append((f"project_bwd.{l}", lambda sh=sh, c=csrs[l], a=a, b=b, P=P, Gr=Gr,

@@ -64,6 +64,26 @@ def test_invalid_edges_status_and_drop():
     _check(blk, np.array([0, 0, 0, 7], np.int32), [0], [0])
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_null_edges(seed):
+    """Edge id -1 (capacity padding of the padded GPU sampler, reading C26)
+    interleaved with real edges and as a tail: dropped without a status bit,
+    bit-exact against the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    T, R = 4, 9
+    rs, rd = random_schema(rng, T, R)
+    n_src = rng.integers(20, 300, T)
+    n_dst = np.minimum(rng.integers(5, 200, T), n_src)
+    blk, et = random_block(rng, n_src, n_dst, rs, rd, 3000, hub_frac=0.05)
+    eid = blk.edge_id.copy()
+    eid[rng.random(len(eid)) < 0.2] = -1
+    if seed % 2:
+        eid[-500:] = -1                                  # a padded tail
+    blk = LayerBlock(n_src=blk.n_src, n_dst=blk.n_dst, src_local=blk.src_local,
+                     dst_local=blk.dst_local, edge_id=eid, src_global=blk.src_global)
+    _check(blk, et, rs, rd)
+
+
 @pytest.mark.parametrize("key", ["acm", "dblp", "imdb", "freebase", "mag"])
 def test_sampled_batches(key):
     cfg = CONFIGS[key]

@@ -320,6 +320,28 @@ def test_project_fwd_bwd(K, D, H, att, prec):
         assert torch.equal(dX2, dX) and torch.equal(dW2, dW)
         if dWr is not None:
             assert torch.equal(dWr2, dWr)
+    else:
+        # RGAT split form (Trainer: input gradient on the critical path, the
+        # weight / attention gradients on the side stream), on dYt (dYg now
+        # holds it: the combined call above applied the score chain in place):
+        # bit-identical to the combined scored call
+        outs = []
+        for split in (False, True):
+            dXs = torch.zeros_like(dX)
+            dWs = torch.zeros_like(dW)
+            das = torch.zeros_like(datt)
+            w1, w2 = torch.empty_like(wsb), torch.empty_like(wsb)
+            args = (sh, csr, K, D, H, t(Xl), None, t(W), None, t(A), t(Yl), dYg.clone(), t(Gn),
+                    t(dssn), t(dsdn))
+            if split:
+                hf().project_bwd_scored(*args, dXs, None, None, None, w1, prec=prec)
+                hf().project_bwd_scored(*args, None, dWs, None, das, w2, prec=prec)
+            else:
+                hf().project_bwd_scored(*args, dXs, dWs, None, das, w1, prec=prec)
+            outs.append((dXs, dWs, das))
+        for a_, b_ in zip(*outs):
+            assert torch.equal(a_, b_)
+        row_rel_l2(outs[1][0].cpu().numpy(), ob["dX"], wt, "dX split")
 
 
 @pytest.mark.parametrize("K,D", [(128, 128), (64, 64), (128, 64), (64, 128)])

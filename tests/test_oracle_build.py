@@ -114,3 +114,34 @@ def test_invalid_edges_are_flagged_and_dropped():
     assert c["status"] == (1 | 4 | 8)
     assert c["row_ptr"][-1] == 1 and c["eperm"][0] == 0
     assert (c["eperm"][1:] == -1).all()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_null_edges_are_dropped_silently(seed):
+    """Edge id -1 (capacity padding, reading C26): the build equals
+    the build of the block with those positions removed (eperm re-indexed),
+    and no status bit is set.  Pinned against the brute force on the block
+    without them."""
+    rng = np.random.default_rng(300 + seed)
+    T, R = 3, 7
+    rs, rd = random_schema(rng, T, R)
+    n_src = rng.integers(5, 40, T)
+    n_dst = np.minimum(rng.integers(1, 30, T), n_src)
+    blk, et = random_block(rng, n_src, n_dst, rs, rd, 400, hub_frac=0.1)
+    keep = rng.random(blk.num_edges) > 0.3
+    eid = blk.edge_id.copy()
+    eid[~keep] = -1
+    padded = _blk(blk.src_local, blk.dst_local, eid, n_src, n_dst)
+    sh = oracle.Shape.of(padded, rs, rd)
+    c = oracle.build(sh, padded, et)
+    assert c["status"] == 0
+    kept = np.nonzero(keep)[0]
+    sub = _blk(blk.src_local[kept], blk.dst_local[kept], blk.edge_id[kept], n_src, n_dst)
+    b = brute(sub, et, rs, rd)
+    nv = int(c["row_ptr"][-1])
+    assert nv == len(kept)
+    assert np.array_equal(c["eperm"][:nv], kept[b["eperm"]])
+    for k in ("row_ptr", "rel_row_off", "y_src", "rel_y_off", "col_ptr"):
+        assert np.array_equal(np.asarray(c[k]), np.asarray(b[k])), k
+    assert np.array_equal(c["col"][:nv], b["col"])
+    assert (c["eperm"][nv:] == -1).all() and (c["col"][nv:] == -1).all()
