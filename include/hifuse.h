@@ -274,6 +274,13 @@ hifuse_status hifuse_semantic_fuse_bwd(const hifuse_layer_shape *shape, int D, h
                                        const float *d_dH, const float *d_H, float *d_G,
                                        float *d_dbias, void *d_ws, size_t ws_bytes,
                                        hifuse_stream_t stream);
+/* dbias_t = sum_i G_t[i] from a G formed by hifuse_semantic_fuse_bwd with
+ * d_dbias = NULL: bit-identical to that call's dbias (same chunks, same
+ * orders), so the critical path can form G alone and a parallel stream the
+ * bias gradient.  Workspace: hifuse_fuse_bwd_ws_bytes(). */
+hifuse_status hifuse_semantic_fuse_bwd_bias(const hifuse_layer_shape *shape, int D,
+                                            const float *d_G, float *d_dbias, void *d_ws,
+                                            size_t ws_bytes, hifuse_stream_t stream);
 
 /* A5' / A6a'. HAN semantic-attention fusion (PAPER.md
  * line 123 leaves the fusion rule open; reading C22, HAN's semantic-level
@@ -357,10 +364,13 @@ hifuse_status hifuse_aggregate_bwd_scored(const hifuse_layer_shape *shape, const
  *   dW_rel[r]  = sum_u X_row(u)^T dYt[u] (+ s_dst chain)   dW_root[t] = sum_i X_t[i]^T G_t[i]
  *   datt[r]    = (sum_u ds_src[u,h] Y[u,head h] | sum_i ds_dst v-chain)
  *   dX (optional, NULL for layer 0) = sum of dYt W_r^T + G W_root^T + ds_dst-chain.
- * d_dW_rel = d_dW_root = NULL (RGCN only, d_dX required): the input gradient
- * alone; a second call with d_dX = NULL forms the weight gradients, so the
- * caller can run it on a parallel stream while the next layer's backward
- * proceeds.  Fixed-order chunked reductions (deterministic).  Workspace:
+ * d_dW_rel = d_dW_root = NULL (d_dX required): the input gradient alone
+ * (RGAT: the dgrad plus the s_dst chain's dX term, with the W a_dst fold on a
+ * parallel branch; only through hifuse_project_bwd_scored, whose dY already
+ * holds dYt, so that the score chain is applied once; d_datt may be NULL);
+ * a second call with d_dX = NULL forms the weight (and attention) gradients,
+ * so the caller can run it on a parallel stream while the next layer's
+ * backward proceeds.  Both forms are bit-identical to the combined call.  Fixed-order chunked reductions (deterministic).  Workspace:
  * hifuse_project_bwd_ws_bytes(). */
 size_t hifuse_project_bwd_ws_bytes(const hifuse_layer_shape *shape, int K, int D, int heads);
 hifuse_status hifuse_project_bwd(const hifuse_layer_shape *shape, const hifuse_csr *csr,
