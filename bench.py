@@ -137,7 +137,7 @@ def stage_cost(stage, l, cfg, sz):
         return 4 * K * m + 4 * D * m + 4 * (R + T) * K * D, 2 * K * D * m
     if stage == "project_bwd":
         m = s["U"] + (s["dst"] if root else 0)
-        if cfg.model == "rgcn" and l > 0:     # input gradient only (weights: project_wgrad)
+        if l > 0:     # input gradient only (weights: project_wgrad)
             return 4 * D * m + 4 * s["src"] * K + 4 * (R + T) * K * D, 2 * K * D * m
         f = 2 * K * D * m * (2 if l > 0 else 1)
         return 4 * K * m + 4 * D * m + (4 * s["src"] * K if l > 0 else 0), f
@@ -166,8 +166,10 @@ def stage_cost(stage, l, cfg, sz):
         return 4 * K * m + 4 * D * s["dst"] + 4 * (R + T) * K * D, 2 * K * D * m
     if stage == "fuse":
         return 4 * D * (s["rows"] + 2 * s["dst"]), 0
-    if stage == "fuse_bwd":
+    if stage == "fuse_bwd":      # dH, H read, G written (the bias: fuse_bwd_bias, side stream)
         return 4 * D * 3 * s["dst"], 0
+    if stage == "fuse_bwd_bias":
+        return 4 * D * s["dst"] + 4 * D * T, 0
     if stage == "build":     # all layers: inputs 20 B/edge, CSR+CSC 16 B/edge, offsets, Y ids
         b = 0
         for q in sz:
@@ -689,7 +691,7 @@ def main():
         if name == "aggregate_fwd" and cfg.agg.startswith("gat"):
             mk = ("k_agg_fwd_gat_xrel" if cfg.agg == "gat_xrel" else
                   "k_agg_fwd_gat_half" if cfg.hidden == 64 else "k_agg_fwd_gat")
-        if name == "project_bwd" and cfg.model == "rgcn":
+        if name == "project_bwd" and l > 0:
             mk = "k_dgrad_tc"                 # input gradient only (weights: project_wgrad)
         tr = None if name == "build" else ncu_traffic(mk,
                                                        cfg.num_layers - 1 - l if bwd else l,
@@ -704,7 +706,7 @@ def main():
 
     # the dominant call on the critical path (the build overlaps the compute
     # stream when pipelined and is reported separately)
-    side = ("xent_wgrad", "project_wgrad")      # side-stream calls: off the critical path
+    side = ("xent_wgrad", "project_wgrad", "fuse_bwd_bias")   # side-stream calls
     cand = [k for k in per_step if not (pipelined and k == "build")
             and not k.startswith(side)]
     dom = max(cand, key=lambda k: per_step[k])

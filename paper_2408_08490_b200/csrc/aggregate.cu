@@ -53,9 +53,14 @@ __device__ __forceinline__ float dlogit_dsd(float ss, float sd, float slope) {
   return MUL ? ss : ((ss + sd) > 0.f ? 1.f : slope);
 }
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+// Raw feature rows of the aggregate-first input layer: read once per batch
+// (the batch's distinct rows roughly fill the L2), so they are loaded with
+// the evict-first (streaming) policy and do not push the layer's reused
+// lines (row pointers, column ids, the output) out of the L2.
+__device__ __forceinline__ float4 ldcs4(const float4* p) { return __ldcs(p); }
 
 // ------------------------------------------------------------ forward SUM/MEAN
-template <int D, bool MEAN>
+template <int D, bool MEAN, bool CS = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict__ col,
           const float4* __restrict__ Y, float4* __restrict__ Z) {
@@ -77,7 +82,7 @@ k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) {
         int c = __shfl_sync(0xffffffffu, my_col, k + u * NS + sid);
-        v[u] = ldg4(Y + (long long)c * LPR + sl);
+        v[u] = CS ? ldcs4(Y + (long long)c * LPR + sl) : ldg4(Y + (long long)c * LPR + sl);
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) acc = f4add(acc, v[u]);
@@ -85,7 +90,8 @@ k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict
     for (; k < n; k += NS) {
       int idx = k + sid;
       int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
-      if (idx < n) acc = f4add(acc, ldg4(Y + (long long)c * LPR + sl));
+      if (idx < n)
+        acc = f4add(acc, CS ? ldcs4(Y + (long long)c * LPR + sl) : ldg4(Y + (long long)c * LPR + sl));
     }
   }
 #pragma unroll
@@ -553,6 +559,23 @@ k_agg_bwd_e(BwdMeta bm, const int* __restrict__ rel_row_off_d, const int* __rest
   if (lane == 0) tail_col[k] = tail;
 }
 
+// Number of chunks after k whose head slot continues column t (a hub column
+// split over many short chunks): 32 head_col entries per ballot instead of one
+// dependent load per chunk (the serial walk made the fix-up kernels the
+// longest step of a small layer's backward: ~20 us on IMDB).
+__device__ __forceinline__ int split_run(const int* __restrict__ head_col, int k, int n_chunks,
+                                         int t, int lane) {
+  int n = 0;
+  for (int base = k + 1; base < n_chunks; base += 32) {
+    const int j = base + lane;
+    const unsigned b = __ballot_sync(0xffffffffu, j < n_chunks && __ldg(head_col + j) == t);
+    if (b == 0xffffffffu) { n += 32; continue; }
+    n += __ffs(~b) - 1;
+    break;
+  }
+  return n;
+}
+
 // Split columns: dY[t] = tail[k] + head[k+1] + ... (chunk order).
 template <int D>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -566,8 +589,9 @@ k_agg_bwd_fix(const typename RowVec<D>::T* __restrict__ part, const int* __restr
   const int t = tail_col[k];
   if (t < 0) return;
   auto acc = part[(2ll * k + 1) * 32 + lane];
-  for (int j = k + 1; j < n_chunks && head_col[j] == t; j++)
-    acc = vadd(acc, part[(2ll * j) * 32 + lane]);
+  const int n = split_run(head_col, k, n_chunks, t, lane);
+#pragma unroll 4
+  for (int j = k + 1; j <= k + n; j++) acc = vadd(acc, part[(2ll * j) * 32 + lane]);
   dY[(long long)t * 32 + lane] = acc;
 }
 
@@ -713,7 +737,9 @@ k_agg_bwd_gat_fix(int R, int H, const int* __restrict__ rel_y_off,
   const int dh = D / H, h = lane * VEC / dh;
   VT acc = part[(2ll * k + 1) * 32 + lane];
   float dss = part_dss[(2ll * k + 1) * kGatDss + h];
-  for (int j = k + 1; j < n_chunks && head_col[j] == t; j++) {
+  const int n = split_run(head_col, k, n_chunks, t, lane);
+#pragma unroll 4
+  for (int j = k + 1; j <= k + n; j++) {
     acc = vadd(acc, part[(2ll * j) * 32 + lane]);
     dss += part_dss[(2ll * j) * kGatDss + h];
   }
@@ -1232,7 +1258,7 @@ hifuse_status hifuse_aggregate_features_fwd(const hifuse_layer_shape* shape, con
   const int TB = kWarpsPerBlock * 32;
   const bool mean = agg == HIFUSE_AGG_MEAN;
 #define HF_AGG(DD, MM)                                                                  \
-  HF_LAUNCH((k_agg_fwd<DD, MM>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, col_x, \
+  HF_LAUNCH((k_agg_fwd<DD, MM, true>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, col_x, \
             (const float4*)d_X, (float4*)d_Xagg)
   if (K == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
   else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }
@@ -1273,7 +1299,7 @@ hifuse_status hifuse_aggregate_features_cols(const hifuse_layer_shape* shape,
   const int TB = kWarpsPerBlock * 32;
   const bool mean = agg == HIFUSE_AGG_MEAN;
 #define HF_AGG(DD, MM)                                                                  \
-  HF_LAUNCH((k_agg_fwd<DD, MM>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, d_col_x, \
+  HF_LAUNCH((k_agg_fwd<DD, MM, true>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, d_col_x, \
             (const float4*)d_X, (float4*)d_Xagg)
   if (K == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
   else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }

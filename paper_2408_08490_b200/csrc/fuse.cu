@@ -73,7 +73,9 @@ struct FuseBwdMeta {
   int chunk_off[HF_MAX_T + 1];
 };
 
-template <bool RELU>
+// WRITE_G = false: G is an input (dH = G, no ReLU), only the chunk column
+// sums are formed (hifuse_semantic_fuse_bwd_bias).
+template <bool RELU, bool WRITE_G = true>
 __global__ void __launch_bounds__(256)
 k_fuse_bwd_chunks(FuseBwdMeta f, const float4* __restrict__ dH, const float4* __restrict__ Hv,
                   float4* __restrict__ G, float4* __restrict__ partial) {
@@ -93,7 +95,7 @@ k_fuse_bwd_chunks(FuseBwdMeta f, const float4* __restrict__ dH, const float4* __
       g.x = h.x > 0.f ? g.x : 0.f; g.y = h.y > 0.f ? g.y : 0.f;
       g.z = h.z > 0.f ? g.z : 0.f; g.w = h.w > 0.f ? g.w : 0.f;
     }
-    G[idx] = g;
+    if (WRITE_G) G[idx] = g;
     acc.x += g.x; acc.y += g.y; acc.z += g.z; acc.w += g.w;
   }
   if (!partial) return;
@@ -543,6 +545,27 @@ hifuse_status hifuse_semantic_fuse_bwd(const hifuse_layer_shape* shape, int D, h
   return last_cuda();
 }
 
+
+hifuse_status hifuse_semantic_fuse_bwd_bias(const hifuse_layer_shape* shape, int D,
+                                            const float* d_G, float* d_dbias, void* d_ws,
+                                            size_t ws_bytes, hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (D != 64 && D != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!d_dbias || (m.dst_rows > 0 && !d_G)) return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_G) || !aligned16(d_dbias)) return HIFUSE_ERR_ALIGNMENT;
+  if (ws_bytes < hifuse_fuse_bwd_ws_bytes(shape, D) || !d_ws) return HIFUSE_ERR_WORKSPACE;
+  FuseBwdMeta f;
+  make_fbm(m, D, &f);
+  cudaStream_t s = st(stream);
+  float4* partial = (float4*)d_ws;
+  // the same chunks and orders as hifuse_semantic_fuse_bwd's bias: bit-identical
+  HF_LAUNCH((k_fuse_bwd_chunks<false, false>), f.chunk_off[m.T], 256, 0, s, f,
+            (const float4*)d_G, (const float4*)nullptr, (float4*)nullptr, partial);
+  HF_LAUNCH(k_fuse_bwd_bias, m.T, 256, 0, s, f, partial, (float4*)d_dbias);
+  return last_cuda();
+}
 
 size_t hifuse_sem_att_ws_bytes(const hifuse_layer_shape* shape, int D, int A) {
   LayerMeta m;

@@ -410,8 +410,8 @@ k_wgrad_partial(ProjMeta pm, const int* __restrict__ chunk_off, const int* __res
 }
 
 // dW[g] = sum of group g's chunk partials, in chunk order (deterministic).
-// dv != nullptr (RGAT): the s_dst chain's weight term dW_r[k, d] +=
-// dv[r, h(d), k] a_dst[r, d] is added here (formerly a separate k_att_dw).
+// dv != nullptr: adds dW_r[k, d] += dv[r, h(d), k] a_dst[r, d] (unused by the
+// library's calls: RGAT adds that term in k_att_final, after the reduce).
 __global__ void k_wgrad_reduce(int R, int T, int KD, const int* __restrict__ chunk_off,
                                const float4* __restrict__ partial, float4* __restrict__ dW_rel,
                                float4* __restrict__ dW_root, ProjMeta pm,
@@ -631,87 +631,82 @@ k_att_partial(int R, int H, int W, int mode, const int* __restrict__ unused,
   reinterpret_cast<float4*>(partial + ((long long)c * H + h) * W)[w4] = acc;
 }
 
-__global__ void k_att_chunks(int R, const int* __restrict__ row_off, ProjMeta pm,
-                             int* chunk_off) {
-  HF_PDL_ENTRY();
-  if (threadIdx.x != 0) return;
-  const int* ro = row_off ? row_off : pm.rel_row_off;
-  int acc = 0;
-  for (int r = 0; r < R; r++) {
-    chunk_off[r] = acc;
-    acc += (ro[r + 1] - ro[r] + kCH - 1) / kCH;
-  }
-  chunk_off[R] = acc;
-}
 
-// Final RGAT parameter gradients (three fully parallel kernels).  Per
-// relation r, head h:
-//   dv[r][h][k]  = sum_chunks Pdst[h][k]                       (k_att_dv)
-//   dW_r[k,hc]  += dv[h][k] a_dst[r,h,c]                        (k_att_dw)
-//   datt[r,0,hc] = sum_chunks Psrc[h][hc];
-//   datt[r,1,hc] = sum_k W_r[k,hc] dv[h][k]                      (k_att_da)
-__global__ void k_att_dv(int R, int K, int H, ProjMeta pm, const float* __restrict__ Pdst,
-                         float* __restrict__ dv) {
-  HF_PDL_ENTRY();
-  __shared__ int s_tab[HF_MAX_R + 1];
-  att_chunk_table(R, pm.rel_row_off, s_tab);
-  __syncthreads();
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= R * H * K) return;
-  const int r = idx / (H * K), o = idx % (H * K);
-  float t[4] = {0.f, 0.f, 0.f, 0.f};
-  const int c0 = s_tab[r], c1 = s_tab[r + 1];
-  int c = c0;
-  for (; c + 4 <= c1; c += 4)
-#pragma unroll
-    for (int q = 0; q < 4; q++) t[q] += Pdst[(long long)(c + q) * H * K + o];
-  for (; c < c1; c++) t[0] += Pdst[(long long)c * H * K + o];
-  dv[idx] = (t[0] + t[1]) + (t[2] + t[3]);
-}
-
-
-// dW_r[k, d] += dv[r, h(d), k] a_dst[r, d]  (the s_dst chain's weight term)
-__global__ void k_att_dw(int R, int K, int D, int H, const float* __restrict__ dv,
-                         const float* __restrict__ att, float* __restrict__ dW_rel) {
-  HF_PDL_ENTRY();
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)R * K * D) return;
-  const int d = (int)(idx % D), k = (int)((idx / D) % K), r = (int)(idx / ((long long)K * D));
-  const int h = d / (D / H);
-  dW_rel[idx] += dv[((long long)r * H + h) * K + k] * att[(long long)r * 2 * D + D + d];
-}
-
-// One block per (relation r, 32 consecutive d): lane = d (coalesced Psrc / W
-// reads), the 8 warps split the source chunks and the K loop, partials meet
-// in shared memory in warp order (deterministic).  (Thread per (r, d) left
-// R*D/128 blocks with two long serial loops on the attention critical path.)
+// The three final RGAT parameter-gradient steps in one kernel, after the
+// weight-gradient reduce: block per (relation r, 32 consecutive d) with
+// 256 threads:
+//   dv[r][h][k] for the block's heads (chunk sums of Pdst, the 8 warps
+//               splitting the chunks) into shared memory,
+//   datt[r,0,d] = sum_chunks Psrc, datt[r,1,d] = sum_k W_r[k,d] dv[h(d)][k]
+//               (k_att_da's split and order),
+//   dW_r[k,d] += dv[h(d)][k] a_dst[r,d]  (k_att_dw's expression),
+// so the attention branch ends with its two partial kernels and the chain
+// loses two launches (IMDB input layer: partials -> dv -> da -> dw was the
+// longest branch of the call).
 __global__ void __launch_bounds__(256)
-k_att_da(int R, int K, int D, int H, const int* __restrict__ rel_y_off,
-         const float* __restrict__ Psrc, const float* __restrict__ dv,
-         const float* __restrict__ W_rel, float* __restrict__ datt) {
+k_att_final(int R, int K, int D, int H, const int* __restrict__ rel_y_off, ProjMeta pm,
+            const float* __restrict__ Psrc, const float* __restrict__ Pdst,
+            const float* __restrict__ W_rel, const float* __restrict__ att,
+            float* __restrict__ datt, float* __restrict__ dW_rel) {
   HF_PDL_ENTRY();
-  __shared__ int s_tab[HF_MAX_R + 1];
+  __shared__ int s_tab[HF_MAX_R + 1], s_tab2[HF_MAX_R + 1];
   __shared__ float red[2][8][32];
-  att_chunk_table(R, rel_y_off, s_tab);
-  __syncthreads();
+  __shared__ float sdv[256];
+  __shared__ float red2[8][256];
   const int tiles = D / 32;
-  const int r = blockIdx.x / tiles, d = (blockIdx.x % tiles) * 32 + (threadIdx.x & 31);
-  const int w = threadIdx.x >> 5;
-  if (r >= R) return;
-  const int h = d / (D / H);
+  const int r = blockIdx.x / tiles, d0 = (blockIdx.x % tiles) * 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, d = d0 + lane;
+  const int dh = D / H;
+  const int h0 = d0 / dh, nh = (d0 + 31) / dh - h0 + 1;   // heads of the block's columns
+  // chunk tables: source chunks (Y rows, rel_y_off) and destination chunks
+  // (merged rows, host-known offsets); warp 0 builds both in turn
+  att_chunk_table(R, pm.rel_row_off, s_tab2);
+  __syncthreads();
+  att_chunk_table(R, rel_y_off, s_tab);
+  // dv of the block's heads: nh * K <= 256 contiguous values per chunk
+  // (Pdst is [chunk][H][K]); the 8 warps split the relation's chunks, lane
+  // owns values lane + 32 j, the warp partials meet in warp order
+  {
+    const int nv = nh * K;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[j] = 0.f;
+    const float* pd = Pdst + (long long)h0 * K;
+    for (int c = s_tab2[r] + w; c < s_tab2[r + 1]; c += 8) {
+      const float* pc = pd + (long long)c * H * K;
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        if (lane + 32 * j < nv) acc[j] += __ldg(pc + lane + 32 * j);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) red2[w][lane + 32 * j] = acc[j];
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < nh * K; o += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; q++) t += red2[q][o];
+    sdv[o] = t;
+  }
+  __syncthreads();
+  const int h = d / dh;
+  const float* vv = sdv + (h - h0) * K;
   float u = 0.f;
   for (int c = s_tab[r] + w; c < s_tab[r + 1]; c += 8) u += Psrc[((long long)c * H + h) * D + d];
   float t = 0.f;
   const float* wp = W_rel + (long long)r * K * D + d;
-  const float* vp = dv + ((long long)r * H + h) * K;
-  for (int k = w; k < K; k += 8) t = fmaf(wp[(long long)k * D], vp[k], t);
-  red[0][w][threadIdx.x & 31] = u;
-  red[1][w][threadIdx.x & 31] = t;
+  for (int k = w; k < K; k += 8) t = fmaf(wp[(long long)k * D], vv[k], t);
+  red[0][w][lane] = u;
+  red[1][w][lane] = t;
+  // s_dst chain's weight term
+  const float ad = att[(long long)r * 2 * D + D + d];
+  float* dwp = dW_rel + (long long)r * K * D + d;
+  for (int k = w; k < K; k += 8) dwp[(long long)k * D] += vv[k] * ad;
   __syncthreads();
   if (w == 0) {
     float a = 0.f, b2 = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; q++) { a += red[0][q][threadIdx.x]; b2 += red[1][q][threadIdx.x]; }
+    for (int q = 0; q < 8; q++) { a += red[0][q][lane]; b2 += red[1][q][lane]; }
     datt[(long long)r * 2 * D + d] = a;
     datt[(long long)r * 2 * D + D + d] = b2;
   }
@@ -1052,11 +1047,10 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
 #undef HF_WG
   }
   int G = d_W_root ? m.R + m.T : m.R;
-  // RGAT attention chain (independent of the wgrad partials until k_att_dw
-  // adds into dW_rel): a second parallel branch
+  // RGAT attention chain (independent of the wgrad partials until
+  // k_att_final adds into dW_rel): a second parallel branch
   Branch ba;
   bool abr = false;
-  float* dvb = v + (long long)m.R * K * H;     // dv [R][H][K] after v in the workspace
   if (d_att) {
     // two parallel chains: (a) destination side: partials of ds_dst x X ->
     // dv; (b) source side: the fold v = W a_dst (for k_dx_sdst) and the
@@ -1072,7 +1066,7 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
                 d_W_rel, d_att, v);
     // the s_dst chain's dX term needs only the fold and the dgrad: it runs on
     // the dgrad branch as soon as both are done (not after both attention
-    // chains and k_att_dw)
+    // chains and k_att_final)
     if (d_dX && branched && prec == HIFUSE_PREC_TF32) {
       cudaEvent_t ev = fold_event(s);
       if (ev) {
@@ -1089,25 +1083,23 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
               csr->rel_y_off, d_ds_src, d_Y, pm, d_gather_ids, Psrc);
     HF_LAUNCH(k_att_partial, gdst, H * K / 4, 0, sa, m.R, H, K, 1, (const int*)nullptr,
               (const int*)nullptr, d_ds_dst, d_X, pm, d_gather_ids, Pdst);
-    HF_LAUNCH(k_att_dv, ceil_div((long long)m.R * H * K, 256), 256, 0, sa, m.R, K, H, pm, Pdst, dvb);
     if (bbr) {                          // (a) waits for (b)
       cudaEventRecord(bb.join, bb.side);
       cudaStreamWaitEvent(sa, bb.join, 0);
     }
-    HF_LAUNCH(k_att_da, m.R * (D / 32), 256, 0, sa, m.R, K, D, H, csr->rel_y_off,
-              Psrc, dvb, d_W_rel, d_datt);
   }
-  // (the s_dst term dv (x) a_dst is added by a separate k_att_dw after the
-  // join: folding it into the reduce made the reduce wait for the attention
-  // branch, measured +3 us per RGAT layer on IMDB)
+  // (the s_dst term dv (x) a_dst is added by k_att_final after the join:
+  // folding it into the reduce made the reduce wait for the attention branch,
+  // measured +3 us per RGAT layer on IMDB)
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
             prec == HIFUSE_PREC_TF32 ? (const int*)nullptr : (const int*)chunk_off,
             (const float4*)partial, (float4*)d_dW_rel, (float4*)d_dW_root, pm, csr->rel_y_off, CH,
             (const float*)nullptr, (const float*)nullptr, 0, 1);
   if (d_att) {
     if (abr) branch_end(s, ba);
-    HF_LAUNCH(k_att_dw, ceil_div((long long)m.R * K * D, 256), 256, 0, s, m.R, K, D, H, dvb, d_att,
-              d_dW_rel);
+    // dv, datt and the s_dst chain's dW term (after the reduce wrote dW_rel)
+    HF_LAUNCH(k_att_final, m.R * (D / 32), 256, 0, s, m.R, K, D, H, csr->rel_y_off, pm, Psrc,
+              Pdst, d_W_rel, d_att, d_datt, d_dW_rel);
   }
   if (branched) branch_end(s, br);       // join the dgrad branch
   if (d_dX) {

@@ -133,18 +133,46 @@ k_smp_pairs(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ fro
   for (long long p = Pact + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < P;
        p += (long long)gridDim.x * blockDim.x)
     pair_cnt[p] = 0;                                   // past the frontier (scanned over P)
-  for (long long p = (long long)blockIdx.x * kSmpWarps + w; p < Pact;
-       p += (long long)gridDim.x * kSmpWarps) {
-  const int d = (int)(p / m.Rmax), q = (int)(p % m.Rmax);
+  // Pairs of a warp: p, p + S, p + 2S, ...  The frontier vertex of the pair
+  // two ahead and the in-list pointers of the next pair are loaded before the
+  // current pair is processed, so its two dependent round trips (front ->
+  // in_ptr) overlap the current pair's selection and atomics.
+  const long long S = (long long)gridDim.x * kSmpWarps;
+  struct PairA { int r, v; };                            // relation (-1: none), vertex
+  struct PairB { long long base; int deg; };
+  auto stage_a = [&](long long pp) -> PairA {
+    PairA x{-1, 0};
+    if (pp < Pact) {
+      const int d = (int)(pp / m.Rmax), q = (int)(pp % m.Rmax);
+      const int t = type_of(fo, m.T, d);
+      if (q < m.trel_off[t + 1] - m.trel_off[t]) {
+        const int v = front[d];
+        if (v >= 0 && v < m.count[t]) { x.r = m.trel[m.trel_off[t] + q]; x.v = v; }
+      }
+    }
+    return x;
+  };
+  auto stage_b = [&](const PairA& x) -> PairB {
+    PairB y{0, 0};
+    if (x.r >= 0) {
+      const long long* ptr = in_ptr + m.in_ptr_off[x.r] + x.v;
+      y.base = ptr[0];
+      y.deg = (int)(ptr[1] - y.base);
+    }
+    return y;
+  };
+  long long p = (long long)blockIdx.x * kSmpWarps + w;
+  PairA a0 = stage_a(p), a1 = stage_a(p + S);
+  PairB b0 = stage_b(a0);
+  for (; p < Pact; p += S) {
+  const PairA a2 = stage_a(p + 2 * S);
+  const PairB b1 = stage_b(a1);
   int k = 0;
   {
-    const int t = type_of(fo, m.T, d);
-    const int v = front[d];
-    if (q < m.trel_off[t + 1] - m.trel_off[t] && v >= 0 && v < m.count[t]) {
-      const int r = m.trel[m.trel_off[t] + q];
-      const long long* ptr = in_ptr + m.in_ptr_off[r] + v;
-      const long long base = ptr[0];
-      const int deg = (int)(ptr[1] - base);
+    if (a0.r >= 0) {
+      const int r = a0.r, v = a0.v;
+      const long long base = b0.base;
+      const int deg = b0.deg;
       k = min(deg, f);
       int* srt = sorted[w];
       if (deg <= f) {                                  // every in-edge, in order
@@ -195,6 +223,7 @@ k_smp_pairs(SmpMeta m, const int* __restrict__ fo_d, const int* __restrict__ fro
     }
   }
   if (lane == 0) pair_cnt[p] = k;
+  a0 = a1; b0 = b1; a1 = a2;
   }
 }
 
@@ -522,8 +551,24 @@ static hifuse_status sample_impl(const hifuse_graph_csc* g, int num_layers,
     cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * std::max(pl.W, 1), s);
     HF_LAUNCH(k_smp_mark_dst, ceil_div(D, 256), 256, 0, s, m, fo, front, gen, loc, stp,
               (const unsigned long long*)d_ctl, h, padded && h > 0 ? 1 : 0, d_status);
-    const long long cap_blocks = (long long)sm_count() * 8;   // grid-stride kernels
-    HF_LAUNCH(k_smp_pairs, std::min<long long>(ceil_div(P, kSmpWarps), cap_blocks), kSmpWarps * 32, 0, s, m, fo, front, (int)P, f, hk,
+    // Grid-stride kernels, sized to the frontier's bound: the padded layout
+    // knows it on the host (the seeds, or the previous hop's capacities), so
+    // every warp gets ~4 pairs and then exits -- a persistent grid held every
+    // SM's warp slots for the whole pair kernel and starved the training step
+    // it runs beside (SampledLoop); the compact layout only knows the
+    // worst case and keeps one resident wave.
+    long long front_cap = D;
+    if (padded && h > 0) {
+      front_cap = 0;
+      for (int t = 0; t < pl.T; t++) front_cap += src_cap_h[(long long)(l + 1) * pl.T + t];
+    }
+    const long long pair_bound = std::min<long long>(P, front_cap * pl.Rmax);
+    const long long cap_blocks = (long long)sm_count() * 8;
+    auto gs_grid = [&](long long work, long long per_block) -> long long {
+      const long long g = std::max<long long>(1, (long long)ceil_div(work, per_block));
+      return padded ? g : std::min(g, cap_blocks);
+    };
+    HF_LAUNCH(k_smp_pairs, gs_grid(pair_bound, kSmpWarps * 4), kSmpWarps * 32, 0, s, m, fo, front, (int)P, f, hk,
               (const unsigned long long*)d_ctl, h, (const long long*)g->d_in_ptr, g->d_in_src, (const long long*)g->d_in_eid, gen,
               bitmap, stp, slot_src, slot_eid, pair_cnt);
     HF_LAUNCH(k_smp_popc, ceil_div(pl.W, 256), 256, 0, s, bitmap, pl.W, wcnt);
@@ -533,11 +578,11 @@ static hifuse_status sample_impl(const hifuse_graph_csc* g, int num_layers,
               d_status);
     HF_LAUNCH(k_smp_assign, ceil_div(pl.W + D, 256), 256, 0, s, m, pl.W, fo, so, front, bitmap,
               wscan, loc, o.src_gid);
-    HF_LAUNCH(k_smp_edges, std::min<long long>(ceil_div(P * f, 256), cap_blocks), 256, 0, s, m, f, P * f, fo, pair_cnt, pscan,
+    HF_LAUNCH(k_smp_edges, gs_grid(pair_bound * f, 256 * 4), 256, 0, s, m, f, P * f, fo, pair_cnt, pscan,
               (int)P, slot_src, slot_eid, loc, o.src_local, o.dst_local, (long long*)o.edge_id,
               pc.ecap, so);
     if (o.gather_ids)
-      HF_LAUNCH(k_smp_gather, std::min<long long>(ceil_div(padded ? std::max(cap_tot, 1ll) : pl.S[h], 256), cap_blocks), 256, 0,
+      HF_LAUNCH(k_smp_gather, gs_grid(padded ? std::max(cap_tot, 1ll) : pl.S[h], 256 * 4), 256, 0,
                 s, m, so, o.src_gid, o.gather_ids);
     front = o.src_gid;
     std::swap(fo, so);

@@ -82,6 +82,7 @@ def lib():
             "hifuse_semantic_fuse": [vp, i32, i32, vp, vp, vp, vp, vp],
             "hifuse_fuse_bwd_ws_bytes": [vp, i32],
             "hifuse_semantic_fuse_bwd": [vp, i32, i32, vp, vp, vp, vp, vp, sz, vp],
+            "hifuse_semantic_fuse_bwd_bias": [vp, i32, vp, vp, vp, sz, vp],
             "hifuse_aggregate_bwd_ws_bytes": [vp, i32, i32],
             "hifuse_aggregate_bwd": [vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp,
                                      vp, sz, vp],
@@ -292,6 +293,12 @@ def semantic_fuse_bwd(shape, D, act, dH, H, G, dbias, ws, stream=None):
     _check("hifuse_semantic_fuse_bwd", lib().hifuse_semantic_fuse_bwd(
         shape.ref, D, ACT[act], _ptr(dH), _ptr(H), _ptr(G), _ptr(dbias), _ptr(ws),
         0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def semantic_fuse_bwd_bias(shape, D, G, dbias, ws, stream=None):
+    _check("hifuse_semantic_fuse_bwd_bias", lib().hifuse_semantic_fuse_bwd_bias(
+        shape.ref, D, _ptr(G), _ptr(dbias), _ptr(ws), ws.numel() * ws.element_size(),
+        _stream(stream)))
 
 
 def aggregate_bwd_ws_bytes(shape, agg, heads):

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import hifuse as hf
-from .sampler import GpuSampler, PaddedBatch, SampledBatch, counts_fit
+from .sampler import GpuSampler, PaddedBatch, SampledBatch
 
 
 class SampledLoop:
@@ -54,6 +54,15 @@ class SampledLoop:
         self.ctl_d = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(self.RING + 1)]
         self.cnt_h = [torch.zeros(L * (2 * T + 1), dtype=torch.int32).pin_memory()
                       for _ in range(self.RING + 1)]
+        # host views (numpy) of the pinned buffers: the per-step host work is
+        # a few array operations, not torch indexing calls
+        self.ctl_np = [c.numpy() for c in self.ctl_h]
+        self.cnt_np = [c.numpy().reshape(L, 2 * T + 1) for c in self.cnt_h]
+        lim = np.full((L, 2 * T + 1), np.iinfo(np.int32).max, np.int64)
+        lim[:, :T] = self.src_cap
+        lim[:, 2 * T] = self.edge_pad
+        self.count_lim = lim             # counts <= lim <=> the padded block fits
+        self.ev_ring = [torch.cuda.Event() for _ in range(8)]
         self.pb = {(r, s): PaddedBatch(smp, self.src_cap, self.edge_pad, r, self.labels_d[r],
                                        target_type, slot=s)
                    for r in range(self.RING) for s in range(self.SLOTS)}
@@ -81,8 +90,8 @@ class SampledLoop:
         self.seeds_d[r].copy_(seeds_h, non_blocking=True)
         self.labels_d[r].copy_(labels_h, non_blocking=True)
         key = int(key)
-        self.ctl_h[r][0] = key - (1 << 64) if key >= (1 << 63) else key
-        self.ctl_h[r][1] = self.smp.next_stamp()
+        self.ctl_np[r][0] = key - (1 << 64) if key >= (1 << 63) else key
+        self.ctl_np[r][1] = self.smp.next_stamp()
         self.ctl_d[r].copy_(self.ctl_h[r], non_blocking=True)
 
     def _sample(self, r):
@@ -97,7 +106,7 @@ class SampledLoop:
         return list(self.cnt_h[r].numpy().reshape(self.L, 2 * self.T + 1))
 
     def _fits(self, i):
-        return counts_fit(self._counts(i % self.RING), self.src_cap, self.edge_pad)
+        return bool((self.cnt_np[i % self.RING] <= self.count_lim).all())
 
     # ----------------------------------------------------------- graphs
     def capture(self):
@@ -201,7 +210,7 @@ class SampledLoop:
             self._stage(i + 2)
             self.graphs[i % 6].replay()
             self._copy_counts((i + 2) % self.RING)
-            ev = torch.cuda.Event()
+            ev = self.ev_ring[i % len(self.ev_ring)]   # (waited on two batches later)
             ev.record(main)
             self.done[i] = ev
         return self.tr.loss

@@ -383,8 +383,7 @@ class Trainer:
                 b = dict(dH=dH, G=self._mat(f"G{l}", sh.dst_rows, D),
                          wsf=self._ws(hf.fuse_bwd_ws_bytes(sh, D)),
                          wsq=self._ws(hf.project_aggregated_bwd_ws_bytes(sh, a["K"], D)))
-                ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
-                    sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
+                self._fuse_bwd_ops(ops, l, sh, a, b, Gr, D, side_op)
                 ops.append(("project_aggregated_bwd.0", lambda sh=sh, c=csrs[l], a=a, b=b, Gr=Gr:
                             hf.project_aggregated_bwd(sh, c, a["K"], D, a["Xagg"], a["Xroot"],
                                                       a["gid_root"], b["G"], Gr["W_rel"],
@@ -414,8 +413,7 @@ class Trainer:
                                                   P["att"], b["dY"], b["ds_src"], b["ds_dst"],
                                                   b["wsa"])))
             else:
-                ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b, Gr=Gr: hf.semantic_fuse_bwd(
-                    sh, D, a["act"], b["dH"], a["H"], b["G"], Gr["bias"], b["wsf"])))
+                self._fuse_bwd_ops(ops, l, sh, a, b, Gr, D, side_op)
             if self.fusion == "han":
                 pass                   # aggregation adjoint queued above
             elif P["att"] is not None:   # RGAT: score chain folded into the CSC pass
@@ -482,6 +480,18 @@ class Trainer:
                 self._head_side)))
         self.last = dict(acts=acts, csrs=csrs)
         return ops
+
+    def _fuse_bwd_ops(self, ops, l, sh, a, b, Gr, D, side_op):
+        """Fusion backward: G = dH * act' on the critical path; the bias
+        gradient (column sums of G, bit-identical to the combined call) as a
+        weight-gradient op on the side stream."""
+        ops.append((f"fuse_bwd.{l}", lambda sh=sh, a=a, b=b: hf.semantic_fuse_bwd(
+            sh, D, a["act"], b["dH"], a["H"], b["G"], None, b["wsf"])))
+        b["wsb"] = self._ws(hf.fuse_bwd_ws_bytes(sh, D), key=f"ws_fb{l}")
+        ops.append((f"fuse_bwd_bias.{l}", side_op(lambda sh=sh, b=b, Gr=Gr:
+                                                  hf.semantic_fuse_bwd_bias(sh, D, b["G"],
+                                                                            Gr["bias"],
+                                                                            b["wsb"]))))
 
     # ----------------------------------------------------------------- step
     def step(self, db: DeviceBatch, feat, edge_type, allreduce=None, world=1, update=True,

@@ -251,6 +251,14 @@ def test_fuse_and_fuse_bwd(D):
     assert np.array_equal(G.cpu().numpy(), Gr.astype(np.float32))
     _, dbA = oracle.fuse_bwd(osh, D, 1, np.abs(dH), Hg.cpu().numpy())
     close_scaled(db.cpu().numpy(), dbr, dbA, what="dbias")
+    # split form (the Trainer: G on the critical path, the bias on the side
+    # stream): bit-identical to the combined call
+    G2 = torch.zeros_like(G)
+    db2 = torch.zeros_like(db)
+    ws2 = torch.empty_like(ws)
+    hf().semantic_fuse_bwd(sh, D, "relu", t(dH), Hg, G2, None, ws)
+    hf().semantic_fuse_bwd_bias(sh, D, G2, db2, ws2)
+    assert torch.equal(G2, G) and torch.equal(db2, db)
 
 
 @pytest.mark.parametrize("K,D,H,att", [(128, 128, 1, False), (64, 64, 1, False), (128, 64, 1, False),
