@@ -131,7 +131,9 @@ struct DstConv {
   int dst_off[HF_MAX_T + 1];      // prefix over types of n_dst
 };
 
-template <int D, bool MEAN>
+// CS: evict-first loads of the gathered rows (raw feature-store rows, read
+// once per batch); the BF16-Y path (rows reused by several edges) keeps them.
+template <int D, bool MEAN, bool CS = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_fwd_bf16(long long rows, unsigned agg_blocks, const int* __restrict__ row_ptr,
                const int* __restrict__ col, const uint4* __restrict__ Xb,
@@ -170,7 +172,7 @@ k_agg_fwd_bf16(long long rows, unsigned agg_blocks, const int* __restrict__ row_
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) {
         const int c = __shfl_sync(0xffffffffu, my_col, k + u * NS + sid);
-        v[u] = __ldg(Xb + (long long)c * LPR + sl);
+        v[u] = CS ? __ldcs(Xb + (long long)c * LPR + sl) : __ldg(Xb + (long long)c * LPR + sl);
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; u++) bf16x8_add(v[u], acc);
@@ -178,7 +180,8 @@ k_agg_fwd_bf16(long long rows, unsigned agg_blocks, const int* __restrict__ row_
     for (; k < n; k += NS) {
       const int idx = k + sid;
       const int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
-      if (idx < n) bf16x8_add(__ldg(Xb + (long long)c * LPR + sl), acc);
+      if (idx < n)
+        bf16x8_add(CS ? __ldcs(Xb + (long long)c * LPR + sl) : __ldg(Xb + (long long)c * LPR + sl), acc);
     }
   }
 #pragma unroll
@@ -1337,12 +1340,19 @@ hifuse_status hifuse_aggregate_features_cols_bf16(const hifuse_layer_shape* shap
   for (int t = 0; t <= m.T; t++) dc.type_src_off[t] = m.type_src_off[t];
   const unsigned conv_blocks = d_Xdst ? ceil_div((long long)acc * (K / 8), TB) : 0;
   const bool mean = agg == HIFUSE_AGG_MEAN;
-#define HF_AGGB(DD, MM)                                                                       \
-  HF_LAUNCH((k_agg_fwd_bf16<DD, MM>), agg_blocks + conv_blocks, TB, 0, s, (long long)m.rows,    \
+#define HF_AGGB(DD, MM, CS)                                                                   \
+  HF_LAUNCH((k_agg_fwd_bf16<DD, MM, CS>), agg_blocks + conv_blocks, TB, 0, s, (long long)m.rows, \
             agg_blocks, csr->row_ptr, d_col_x, (const uint4*)d_Xb, (float4*)d_Xagg, dc,        \
             d_gather_ids, (float4*)d_Xdst)
-  if (K == 128) { if (mean) HF_AGGB(128, true); else HF_AGGB(128, false); }
-  else { if (mean) HF_AGGB(64, true); else HF_AGGB(64, false); }
+  // gathered through the feature store's row ids: raw features (evict-first)
+  const bool fs = d_gather_ids != nullptr;
+  if (K == 128) {
+    if (mean) { if (fs) HF_AGGB(128, true, true); else HF_AGGB(128, true, false); }
+    else { if (fs) HF_AGGB(128, false, true); else HF_AGGB(128, false, false); }
+  } else {
+    if (mean) { if (fs) HF_AGGB(64, true, true); else HF_AGGB(64, true, false); }
+    else { if (fs) HF_AGGB(64, false, true); else HF_AGGB(64, false, false); }
+  }
 #undef HF_AGGB
   return last_cuda();
 }

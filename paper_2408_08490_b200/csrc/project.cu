@@ -411,7 +411,7 @@ k_wgrad_partial(ProjMeta pm, const int* __restrict__ chunk_off, const int* __res
 
 // dW[g] = sum of group g's chunk partials, in chunk order (deterministic).
 // dv != nullptr: adds dW_r[k, d] += dv[r, h(d), k] a_dst[r, d] (unused by the
-// library's calls: RGAT adds that term in k_att_final, after the reduce).
+// library's calls: RGAT adds that term in k_att_dw, after the reduce).
 __global__ void k_wgrad_reduce(int R, int T, int KD, const int* __restrict__ chunk_off,
                                const float4* __restrict__ partial, float4* __restrict__ dW_rel,
                                float4* __restrict__ dW_root, ProjMeta pm,
@@ -632,22 +632,19 @@ k_att_partial(int R, int H, int W, int mode, const int* __restrict__ unused,
 }
 
 
-// The three final RGAT parameter-gradient steps in one kernel, after the
-// weight-gradient reduce: block per (relation r, 32 consecutive d) with
-// 256 threads:
-//   dv[r][h][k] for the block's heads (chunk sums of Pdst, the 8 warps
-//               splitting the chunks) into shared memory,
-//   datt[r,0,d] = sum_chunks Psrc, datt[r,1,d] = sum_k W_r[k,d] dv[h(d)][k]
-//               (k_att_da's split and order),
-//   dW_r[k,d] += dv[h(d)][k] a_dst[r,d]  (k_att_dw's expression),
-// so the attention branch ends with its two partial kernels and the chain
-// loses two launches (IMDB input layer: partials -> dv -> da -> dw was the
-// longest branch of the call).
+// dv and datt of the RGAT attention chain in one kernel on the attention
+// branch: block per (relation r, 32 consecutive d), 256 threads:
+//   dv[r][h][k] for the block's heads: chunk sums of Pdst, the 8 warps
+//               splitting the chunks, partials met in warp order (also
+//               written to global for k_att_dw),
+//   datt[r,0,d] = sum_chunks Psrc, datt[r,1,d] = sum_k W_r[k,d] dv[h(d)][k].
+// (Formerly k_att_dv then k_att_da; merging all three final steps behind the
+// weight-gradient reduce lengthened IMDB's input-layer call 31 -> 37 us: dv
+// and datt only wait for the attention partials, k_att_dw for the reduce.)
 __global__ void __launch_bounds__(256)
-k_att_final(int R, int K, int D, int H, const int* __restrict__ rel_y_off, ProjMeta pm,
-            const float* __restrict__ Psrc, const float* __restrict__ Pdst,
-            const float* __restrict__ W_rel, const float* __restrict__ att,
-            float* __restrict__ datt, float* __restrict__ dW_rel) {
+k_att_dvda(int R, int K, int D, int H, const int* __restrict__ rel_y_off, ProjMeta pm,
+           const float* __restrict__ Psrc, const float* __restrict__ Pdst,
+           const float* __restrict__ W_rel, float* __restrict__ datt, float* __restrict__ dv) {
   HF_PDL_ENTRY();
   __shared__ int s_tab[HF_MAX_R + 1], s_tab2[HF_MAX_R + 1];
   __shared__ float red[2][8][32];
@@ -698,10 +695,10 @@ k_att_final(int R, int K, int D, int H, const int* __restrict__ rel_y_off, ProjM
   for (int k = w; k < K; k += 8) t = fmaf(wp[(long long)k * D], vv[k], t);
   red[0][w][lane] = u;
   red[1][w][lane] = t;
-  // s_dst chain's weight term
-  const float ad = att[(long long)r * 2 * D + D + d];
-  float* dwp = dW_rel + (long long)r * K * D + d;
-  for (int k = w; k < K; k += 8) dwp[(long long)k * D] += vv[k] * ad;
+  // dv of the block's heads for k_att_dw (heads wider than 32 columns are
+  // formed identically by each of their blocks: equal values written twice)
+  for (int o = threadIdx.x; o < nh * K; o += blockDim.x)
+    dv[((long long)r * H + h0) * K + o] = sdv[o];
   __syncthreads();
   if (w == 0) {
     float a = 0.f, b2 = 0.f;
@@ -710,6 +707,18 @@ k_att_final(int R, int K, int D, int H, const int* __restrict__ rel_y_off, ProjM
     datt[(long long)r * 2 * D + d] = a;
     datt[(long long)r * 2 * D + D + d] = b2;
   }
+}
+
+// dW_r[k, d] += dv[r, h(d), k] a_dst[r, d]  (the s_dst chain's weight term,
+// after the weight-gradient reduce wrote dW_rel)
+__global__ void k_att_dw(int R, int K, int D, int H, const float* __restrict__ dv,
+                         const float* __restrict__ att, float* __restrict__ dW_rel) {
+  HF_PDL_ENTRY();
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)R * K * D) return;
+  const int d = (int)(idx % D), k = (int)((idx / D) % K), r = (int)(idx / ((long long)K * D));
+  const int h = d / (D / H);
+  dW_rel[idx] += dv[((long long)r * H + h) * K + k] * att[(long long)r * 2 * D + D + d];
 }
 
 // dX_t[i] += sum_{r: t(r)=t} sum_h ds_dst[(r,i),h] v[r][:,h]   (s_dst chain);
@@ -1048,9 +1057,10 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
   }
   int G = d_W_root ? m.R + m.T : m.R;
   // RGAT attention chain (independent of the wgrad partials until
-  // k_att_final adds into dW_rel): a second parallel branch
+  // k_att_dw adds into dW_rel): a second parallel branch
   Branch ba;
   bool abr = false;
+  float* dvb = v + (long long)m.R * K * H;     // dv [R][H][K] after v in the workspace
   if (d_att) {
     // two parallel chains: (a) destination side: partials of ds_dst x X ->
     // dv; (b) source side: the fold v = W a_dst (for k_dx_sdst) and the
@@ -1066,7 +1076,7 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
                 d_W_rel, d_att, v);
     // the s_dst chain's dX term needs only the fold and the dgrad: it runs on
     // the dgrad branch as soon as both are done (not after both attention
-    // chains and k_att_final)
+    // chains and k_att_dw)
     if (d_dX && branched && prec == HIFUSE_PREC_TF32) {
       cudaEvent_t ev = fold_event(s);
       if (ev) {
@@ -1087,8 +1097,10 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
       cudaEventRecord(bb.join, bb.side);
       cudaStreamWaitEvent(sa, bb.join, 0);
     }
+    HF_LAUNCH(k_att_dvda, m.R * (D / 32), 256, 0, sa, m.R, K, D, H, csr->rel_y_off, pm, Psrc,
+              Pdst, d_W_rel, d_datt, dvb);
   }
-  // (the s_dst term dv (x) a_dst is added by k_att_final after the join:
+  // (the s_dst term dv (x) a_dst is added by k_att_dw after the join:
   // folding it into the reduce made the reduce wait for the attention branch,
   // measured +3 us per RGAT layer on IMDB)
   HF_LAUNCH(k_wgrad_reduce, ceil_div((long long)G * K * D / 4, 256), 256, 0, s, m.R, m.T, K * D,
@@ -1097,9 +1109,8 @@ static hifuse_status project_bwd_impl(const hifuse_layer_shape* shape, const hif
             (const float*)nullptr, (const float*)nullptr, 0, 1);
   if (d_att) {
     if (abr) branch_end(s, ba);
-    // dv, datt and the s_dst chain's dW term (after the reduce wrote dW_rel)
-    HF_LAUNCH(k_att_final, m.R * (D / 32), 256, 0, s, m.R, K, D, H, csr->rel_y_off, pm, Psrc,
-              Pdst, d_W_rel, d_att, d_datt, d_dW_rel);
+    HF_LAUNCH(k_att_dw, ceil_div((long long)m.R * K * D, 256), 256, 0, s, m.R, K, D, H, dvb, d_att,
+              d_dW_rel);
   }
   if (branched) branch_end(s, br);       // join the dgrad branch
   if (d_dX) {

@@ -553,7 +553,7 @@ static hifuse_status sample_impl(const hifuse_graph_csc* g, int num_layers,
               (const unsigned long long*)d_ctl, h, padded && h > 0 ? 1 : 0, d_status);
     // Grid-stride kernels, sized to the frontier's bound: the padded layout
     // knows it on the host (the seeds, or the previous hop's capacities), so
-    // every warp gets ~4 pairs and then exits -- a persistent grid held every
+    // every warp gets one pair and then exits -- a persistent grid held every
     // SM's warp slots for the whole pair kernel and starved the training step
     // it runs beside (SampledLoop); the compact layout only knows the
     // worst case and keeps one resident wave.
@@ -568,7 +568,7 @@ static hifuse_status sample_impl(const hifuse_graph_csc* g, int num_layers,
       const long long g = std::max<long long>(1, (long long)ceil_div(work, per_block));
       return padded ? g : std::min(g, cap_blocks);
     };
-    HF_LAUNCH(k_smp_pairs, gs_grid(pair_bound, kSmpWarps * 4), kSmpWarps * 32, 0, s, m, fo, front, (int)P, f, hk,
+    HF_LAUNCH(k_smp_pairs, gs_grid(pair_bound, kSmpWarps), kSmpWarps * 32, 0, s, m, fo, front, (int)P, f, hk,
               (const unsigned long long*)d_ctl, h, (const long long*)g->d_in_ptr, g->d_in_src, (const long long*)g->d_in_eid, gen,
               bitmap, stp, slot_src, slot_eid, pair_cnt);
     HF_LAUNCH(k_smp_popc, ceil_div(pl.W, 256), 256, 0, s, bitmap, pl.W, wcnt);
