@@ -133,7 +133,12 @@ typedef struct {
  * valid count are -1; col_ptr entries past U equal the number of valid edges.
  * The CSC is optional: col_ptr, csc_pos, csc_row and csc_col all NULL skip
  * the transpose (a layer whose aggregation backward is
- * never run, e.g. the input layer of the aggregate-first RGCN). */
+ * never run, e.g. the input layer of the aggregate-first RGCN).
+ * X-row mode: y_src == NULL (the CSC must then be absent too) skips the Y
+ * numbering: col[p] = type_src_off(source type) + source local id, the
+ * source's row in the layer's type-major X (what an aggregation over raw
+ * rows reads: the aggregate-first input layer); rel_y_off, slot_y and U_dev
+ * may be NULL and are not written.  Same rows, positions and eperm. */
 typedef struct {
   int32_t *rel_row_off;  /* [R+1]      */
   int32_t *row_ptr;      /* [rows+1]   */
@@ -443,7 +448,8 @@ hifuse_status hifuse_aggregate_features_cols_bf16(const hifuse_layer_shape *shap
 /* The two halves of hifuse_aggregate_features_fwd, so the first can run with
  * the semantic-graph build (off the critical path):
  *   hifuse_feature_cols: d_col_x [N] = the feature-store row x(e) of every
- *     CSR position (gather_ids NULL: identity);
+ *     CSR position (gather_ids NULL: identity), from a Y-numbered or an
+ *     X-row-mode build;
  *   hifuse_aggregate_features_cols: the aggregation over X rows d_col_x. */
 hifuse_status hifuse_feature_cols(const hifuse_layer_shape *shape, const hifuse_csr *csr,
                                   const int32_t *d_gather_ids, int32_t *d_col_x,

@@ -225,6 +225,17 @@ k_col_to_x(int N, int R, const int* __restrict__ rel_y_off, RelOff so,
   col_x[p] = gather_ids ? gather_ids[x] : x;
 }
 
+// X-row build: col_x[p] = gather_ids[col[p]] (or col[p]); tail (-1) -> 0.
+__global__ void __launch_bounds__(256)
+k_xrow_to_feat(int N, const int* __restrict__ col, const int* __restrict__ gather_ids,
+               int* __restrict__ col_x) {
+  HF_PDL_ENTRY();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= N) return;
+  const int c = col[p];
+  col_x[p] = c < 0 ? 0 : (gather_ids ? gather_ids[c] : c);
+}
+
 // ------------------------------------------------------------- forward GAT
 // Per head h: two passes over the row's edges (rows are short): the max of the
 // logits, then p = exp(l - max), sum p and sum p * Y.  stats = (max, sum p).
@@ -1275,8 +1286,14 @@ hifuse_status hifuse_feature_cols(const hifuse_layer_shape* shape, const hifuse_
   LayerMeta m;
   hifuse_status rc = make_meta(shape, &m);
   if (rc != HIFUSE_OK) return rc;
-  if (!csr || !csr->rel_y_off || !d_col_x || (m.N > 0 && (!csr->col || !csr->y_src)))
-    return HIFUSE_ERR_INVALID_ARG;
+  if (!csr || !d_col_x || (m.N > 0 && !csr->col)) return HIFUSE_ERR_INVALID_ARG;
+  if (!csr->y_src) {
+    // X-row build (no Y numbering): col already is the source's row in X
+    HF_LAUNCH(k_xrow_to_feat, ceil_div(m.N, 256), 256, 0, st(stream), m.N, csr->col,
+              d_gather_ids, d_col_x);
+    return last_cuda();
+  }
+  if (!csr->rel_y_off) return HIFUSE_ERR_INVALID_ARG;
   RelOff ro;
   for (int r = 0; r < m.R; r++) ro.v[r] = m.type_src_off[m.rel_src[r]];
   HF_LAUNCH(k_col_to_x, ceil_div(m.N, 256), 256, 0, st(stream), m.N, m.R, csr->rel_y_off, ro,

@@ -91,10 +91,12 @@ enum Kern { K_CLASSIFY, K_SCAN, K_SCATTER, K_ROWS, K_COLS, kKerns };
 
 struct BLayer {
   int R, N, rows, S, U_max, csc;
+  int ynum;                            // 0: X-row columns (no Y numbering, no slots)
   int t_rows, t_slots;                 // scan tiles per segment
   int key_base[HF_MAX_R + 1];          // rel_row_off
   int slot_base[HF_MAX_R + 1];         // slot_off
   int src_lim[HF_MAX_R];               // n_src of the source type of r
+  int xoff[HF_MAX_R];                  // type_src_off of the source type of r (X-row mode)
   int dst_lim[HF_MAX_R];               // n_dst of the destination type of r
   const int* src;
   const int* dst;
@@ -127,6 +129,7 @@ struct BuildParams {
   BPlan p;
   BLayer lay[kMaxL];
 };
+static_assert(sizeof(BuildParams) <= 32764, "kernel parameter space (32 KB)");
 
 // (layer, tile) of this block in kernel k
 __device__ __forceinline__ int layer_of(const BPlan& P, int k, int* j) {
@@ -295,6 +298,7 @@ __device__ void block_sort_segment(int* keys, int* vals, int b, int e, int* sm, 
 struct RelSmem {
   long long off[HF_MAX_R + 1];         // relation-major edge-id ranges
   int key_base[HF_MAX_R + 1], slot_base[HF_MAX_R + 1], src_lim[HF_MAX_R], dst_lim[HF_MAX_R];
+  int xoff[HF_MAX_R];
 };
 
 // Merged-row key of input edge e, -3 if the edge is invalid (k_classify's
@@ -337,6 +341,7 @@ k_classify(const __grid_constant__ BuildParams bp) {
     if (i < L.R) {
       rs.src_lim[i] = L.src_lim[i];
       rs.dst_lim[i] = L.dst_lim[i];
+      rs.xoff[i] = L.xoff[i];
     }
   }
   __syncthreads();
@@ -389,7 +394,9 @@ k_classify(const __grid_constant__ BuildParams bp) {
       continue;
     }
     key[q] = rs.key_base[r] + dv[q];               // lines 318-319, every r at once
-    slot[q] = L.rows + rs.slot_base[r] + sv[q];    // index into cnt
+    // Y numbering: the (relation, source) slot (index into cnt); X-row mode:
+    // the source's row in the layer's type-major X (the column itself)
+    slot[q] = L.ynum ? L.rows + rs.slot_base[r] + sv[q] : rs.xoff[r] + sv[q];
   }
   if (bad_any) atomicOr(P.status, bad_any);
   // Runs: maximal stretches of consecutive valid input edges with one key.  A
@@ -417,13 +424,13 @@ k_classify(const __grid_constant__ BuildParams bp) {
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
     prow[q] = __match_any_sync(0xffffffffu, key[q] >= 0 ? key[q] : -1 - lane);
-    pslot[q] = __match_any_sync(0xffffffffu, key[q] >= 0 ? slot[q] : -1 - lane);
+    pslot[q] = L.ynum ? __match_any_sync(0xffffffffu, key[q] >= 0 ? slot[q] : -1 - lane) : 0u;
   }
   int base[kEPT];
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
     const bool lead_r = key[q] >= 0 && lane == __ffs(prow[q]) - 1;
-    const bool lead_s = key[q] >= 0 && lane == __ffs(pslot[q]) - 1;
+    const bool lead_s = L.ynum && key[q] >= 0 && lane == __ffs(pslot[q]) - 1;
     base[q] = lead_r ? atomicAdd(L.cnt + key[q], __popc(prow[q])) : 0;
     if (lead_s) atomicAdd(L.cnt + slot[q], __popc(pslot[q]));
   }
@@ -434,7 +441,7 @@ k_classify(const __grid_constant__ BuildParams bp) {
     if (key[q] == -1) continue;
     L.key_e[e] = key[q] >= 0 ? key[q] : -1;
     if (key[q] >= 0) {
-      L.slot_e[e] = slot[q] - L.rows;
+      L.slot_e[e] = L.ynum ? slot[q] - L.rows : slot[q];
       L.rank_e[e] = b + __popc(prow[q] & ((1u << lane) - 1u));
     }
   }
@@ -650,7 +657,7 @@ k_scatter(const __grid_constant__ BuildParams bp) {
     const int rn = key[q] >= 0 ? L.runs[key[q]] : 0;
     const int f = rn == 1 ? L.first[key[q]] : 0;
     pos[q] = key[q] >= 0 ? L.row_ptr[key[q]] + (rn == 1 ? e - f : rank[q]) : 0;
-    c[q] = key[q] >= 0 ? L.slot_y[slot[q]] : 0;
+    c[q] = key[q] >= 0 ? (L.ynum ? L.slot_y[slot[q]] : slot[q]) : 0;
   }
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
@@ -1009,10 +1016,14 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
     if (rc != HIFUSE_OK) return rc;
     const LayerMeta& m = metas[l];
     const hifuse_csr& o = out[l];
-    if (!o.rel_row_off || !o.row_ptr || !o.rel_y_off || !o.U_dev ||
+    // y_src == NULL: X-row mode (col = the source's row in the layer's X, no
+    // Y numbering, no CSC; rel_y_off / U_dev / slot_y unused)
+    const bool ynum = o.y_src != nullptr;
+    if (!o.rel_row_off || !o.row_ptr || (ynum && (!o.rel_y_off || !o.U_dev)) ||
         (m.N > 0 && (!d_src_local[l] || !d_dst_local[l] || !d_edge_id[l] || !o.col ||
-                     !o.eperm || !o.y_src)) ||
-        (!o.col_ptr != !o.csc_pos || !o.col_ptr != !o.csc_row || !o.col_ptr != !o.csc_col) || (m.S > 0 && !o.slot_y))
+                     !o.eperm)) ||
+        (!o.col_ptr != !o.csc_pos || !o.col_ptr != !o.csc_row || !o.col_ptr != !o.csc_col) ||
+        (ynum && m.S > 0 && !o.slot_y) || (!ynum && o.col_ptr))
       return HIFUSE_ERR_INVALID_ARG;
     if (m.N >= (1 << 30) || m.S >= (1 << 30)) return HIFUSE_ERR_UNSUPPORTED;   // status packing
   }
@@ -1052,6 +1063,8 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       BLayer& L = bp.lay[q];
       const bool csc = o.col_ptr != nullptr;
       carve_layer(m, csc, zp, sp, &L);
+      L.ynum = o.y_src != nullptr;
+      if (!L.ynum) L.t_slots = 0;                  // no slot segment to scan
       L.R = m.R; L.N = m.N; L.rows = m.rows; L.S = m.S;
       L.U_max = (int)umax_of(m);
       L.csc = csc;
@@ -1062,6 +1075,7 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       for (int r = 0; r < m.R; r++) {
         L.src_lim[r] = m.n_src[m.rel_src[r]];
         L.dst_lim[r] = m.n_dst[m.rel_dst[r]];
+        L.xoff[r] = m.type_src_off[m.rel_src[r]];
       }
       L.src = d_src_local[l0 + q];
       L.dst = d_dst_local[l0 + q];

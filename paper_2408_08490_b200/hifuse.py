@@ -198,7 +198,9 @@ class Shape:
 class CsrBuffers:
     """Device buffers of one layer's build output (torch int32 tensors)."""
 
-    def __init__(self, shape: Shape, device, cap=None, csc=True):
+    def __init__(self, shape: Shape, device, cap=None, csc=True, xrow=False):
+        """xrow: X-row mode (include/hifuse.h): no Y numbering, no CSC; col
+        holds each position's source row in the layer's X."""
         import torch
         cap = cap or {}
         N = max(cap.get("N", shape.N), 1)
@@ -210,8 +212,11 @@ class CsrBuffers:
         self.t = dict(rel_row_off=z(R + 1), row_ptr=z(rows + 1), col=z(N), eperm=z(N),
                       rel_y_off=z(R + 1), y_src=z(umax), col_ptr=z(umax + 1), csc_pos=z(N),
                       csc_row=z(N), csc_col=z(N), slot_y=z(S), U_dev=z(1))
-        if not csc:     # transpose not built (aggregate-first input layer)
+        if not csc or xrow:     # transpose not built (aggregate-first input layer)
             for k in ("col_ptr", "csc_pos", "csc_row", "csc_col"):
+                self.t[k] = None
+        if xrow:
+            for k in ("rel_y_off", "y_src", "slot_y", "U_dev"):
                 self.t[k] = None
         self.c = Csr(**{k: (v.data_ptr() if v is not None else None) for k, v in self.t.items()})
 

@@ -210,8 +210,10 @@ class Trainer:
         if c is None or any(need[k] > c.cap[k] for k in need):
             cap = {k: int(v * 1.25) + 1 for k, v in need.items()}
             cap["R"] = shape.R
-            # the aggregate-first input layer never runs the transpose
-            c = hf.CsrBuffers(shape, self.device, cap, csc=not (self.agg_first and l == 0))
+            # the aggregate-first input layer never runs the transpose and reads
+            # raw X rows: X-row build (no Y numbering, no slot scan)
+            first = self.agg_first and l == 0
+            c = hf.CsrBuffers(shape, self.device, cap, csc=not first, xrow=first)
             c.cap = cap
             self._bufs[key] = c
         return c

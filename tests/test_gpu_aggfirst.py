@@ -38,6 +38,57 @@ def test_build_without_transpose_is_bit_exact(seed):
         assert np.array_equal(ch[k], np.asarray(ref[k])), k
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_xrow_build(seed):
+    """X-row build (no Y numbering, the aggregate-first input layer's form):
+    rows, positions and eperm bit-exact against the oracle, col = the
+    source's row in the layer's X (type_src_off of the relation's source
+    type + the oracle's y_src of its Y row), null edges included; the
+    feature rows and the aggregation from it equal those of the Y build."""
+    rng = np.random.default_rng(900 + seed)
+    T, R = 4, 9
+    rs, rd = random_schema(rng, T, R)
+    n_src = rng.integers(20, 300, T)
+    n_dst = np.maximum(np.minimum(rng.integers(0, 200, T), n_src), 1)
+    blk, et = random_block(rng, n_src, n_dst, rs, rd, 4000, hub_frac=0.1 * (seed % 2))
+    if seed >= 2:                                   # null (padding) edges
+        from synth.sampler import LayerBlock
+        eid = blk.edge_id.copy()
+        eid[rng.random(len(eid)) < 0.15] = -1
+        blk = LayerBlock(n_src=blk.n_src, n_dst=blk.n_dst, src_local=blk.src_local,
+                         dst_local=blk.dst_local, edge_id=eid, src_global=blk.src_global)
+    sh, csr, st = gpu_build(blk, et, rs, rd, csc=False, xrow=True)
+    assert int(st.item()) == 0
+    ref = oracle.build(oracle.Shape.of(blk, rs, rd), blk, et)
+    g = lambda k, n: csr[k][:n].cpu().numpy()
+    assert np.array_equal(g("rel_row_off", sh.R + 1), np.asarray(ref["rel_row_off"]))
+    assert np.array_equal(g("row_ptr", sh.rows + 1), np.asarray(ref["row_ptr"]))
+    assert np.array_equal(g("eperm", sh.N), np.asarray(ref["eperm"]))
+    nv = int(ref["row_ptr"][-1])
+    col_ref = np.asarray(ref["col"])[:nv]
+    ryo = np.asarray(ref["rel_y_off"])
+    r_of = np.searchsorted(ryo, col_ref, side="right") - 1
+    tso = np.concatenate([[0], np.cumsum(n_src)])
+    want = tso[np.asarray(rs)[r_of]] + np.asarray(ref["y_src"])[col_ref]
+    got = g("col", sh.N)
+    assert np.array_equal(got[:nv], want) and (got[nv:] == -1).all()
+    # feature rows and the aggregation: identical to the Y-numbered build
+    sh2, csr2, _ = gpu_build(blk, et, rs, rd, csc=False)
+    gid = rng.permutation(sh.src_rows + 7)[:sh.src_rows].astype(np.int32)
+    c1 = torch.empty(max(sh.N, 1), dtype=torch.int32, device=DEV)
+    c2 = torch.empty_like(c1)
+    hf().feature_cols(sh, csr, t(gid, torch.int32), c1)
+    hf().feature_cols(sh2, csr2, t(gid, torch.int32), c2)
+    assert torch.equal(c1[:nv], c2[:nv])
+    K = 128
+    X = t(rng.standard_normal((sh.src_rows + 7, K)).astype(np.float32))
+    a1 = torch.zeros(max(sh.rows, 1), K, device=DEV)
+    a2 = torch.zeros_like(a1)
+    hf().aggregate_features_cols(sh, csr, "mean", K, X, c1, a1)
+    hf().aggregate_features_cols(sh2, csr2, "mean", K, X, c2, a2)
+    assert torch.equal(a1, a2)
+
+
 @pytest.mark.parametrize("K", [64, 128])
 @pytest.mark.parametrize("agg", ["sum", "mean"])
 @pytest.mark.parametrize("seed", range(3))
