@@ -113,6 +113,9 @@ def layer_sizes(cfg, g, mb, rs, rd):
     return out
 
 
+BUILD_XROW0 = [False]     # set from the Trainer: the input layer is built in X-row mode
+
+
 def stage_cost(stage, l, cfg, sz):
     """(bytes, flops) an ideal implementation must move / execute per launch
     (DESIGN.md §Roofline)."""
@@ -172,8 +175,11 @@ def stage_cost(stage, l, cfg, sz):
         return 4 * D * s["dst"] + 4 * D * T, 0
     if stage == "build":     # all layers: inputs 20 B/edge, CSR+CSC 16 B/edge, offsets, Y ids
         b = 0
-        for q in sz:
-            b += 36 * q["N"] + 4 * (q["rows"] + 1) + 8 * q["U"] + 4 * q["S"]
+        for qi, q in enumerate(sz):
+            if qi == 0 and BUILD_XROW0[0]:   # X-row input layer: no Y numbering, no CSC
+                b += 28 * q["N"] + 4 * (q["rows"] + 1)
+            else:
+                b += 36 * q["N"] + 4 * (q["rows"] + 1) + 8 * q["U"] + 4 * q["S"]
         return b, 0
     return 0, 0
 
@@ -523,6 +529,7 @@ def main():
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
                  prec=args.prec, order=args.order, fusion=args.fusion,
                  feat_dtype=args.feat_dtype, y_dtype=args.y_dtype)
+    BUILD_XROW0[0] = tr.agg_first      # (stage_cost of the build)
     tr.load_params(params)
     tr.prepare_graph(et_d)           # relation-major edge ids -> R+1 offsets (once per graph)
     # N > 1: per-layer bucketed all-reduce on a comm stream inside the step

@@ -152,6 +152,9 @@ typedef struct {
   int32_t *csc_col;      /* [N]        */
   int32_t *slot_y;       /* [S]        */
   int32_t *U_dev;        /* [1]        */
+  const int32_t *x_gather; /* X-row mode only, nullable: col[p] = x_gather[X row]
+                            * (the feature-store row: the aggregate-first layer
+                            * then reads col directly, no hifuse_feature_cols) */
 } hifuse_csr;
 
 /* Sizes of one layer (host only, no device work, no sync). */
@@ -449,7 +452,8 @@ hifuse_status hifuse_aggregate_features_cols_bf16(const hifuse_layer_shape *shap
  * the semantic-graph build (off the critical path):
  *   hifuse_feature_cols: d_col_x [N] = the feature-store row x(e) of every
  *     CSR position (gather_ids NULL: identity), from a Y-numbered or an
- *     X-row-mode build;
+ *     X-row-mode build (an X-row build with x_gather already wrote exactly
+ *     this map into col: use col directly);
  *   hifuse_aggregate_features_cols: the aggregation over X rows d_col_x. */
 hifuse_status hifuse_feature_cols(const hifuse_layer_shape *shape, const hifuse_csr *csr,
                                   const int32_t *d_gather_ids, int32_t *d_col_x,

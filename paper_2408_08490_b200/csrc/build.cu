@@ -104,6 +104,7 @@ struct BLayer {
   // outputs
   int *o_rel_row_off, *row_ptr, *col, *eperm, *o_rel_y_off, *y_src, *col_ptr, *csc_pos,
       *csc_row, *csc_col, *slot_y, *U_dev;
+  const int* xg;                       // X-row mode: feature-store row of every X row
   // workspace: zero zone
   int *cnt, *ccur;                     // cnt = [row counts | slot counts]
   int* runs;                           // per row: runs of consecutive input edges
@@ -657,7 +658,7 @@ k_scatter(const __grid_constant__ BuildParams bp) {
     const int rn = key[q] >= 0 ? L.runs[key[q]] : 0;
     const int f = rn == 1 ? L.first[key[q]] : 0;
     pos[q] = key[q] >= 0 ? L.row_ptr[key[q]] + (rn == 1 ? e - f : rank[q]) : 0;
-    c[q] = key[q] >= 0 ? (L.ynum ? L.slot_y[slot[q]] : slot[q]) : 0;
+    c[q] = key[q] >= 0 ? (L.ynum ? L.slot_y[slot[q]] : (L.xg ? L.xg[slot[q]] : slot[q])) : 0;
   }
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
@@ -1083,6 +1084,7 @@ hifuse_status hifuse_build_semantic_graphs(const hifuse_layer_shape* shapes, int
       L.o_rel_row_off = o.rel_row_off; L.row_ptr = o.row_ptr; L.col = o.col; L.eperm = o.eperm;
       L.o_rel_y_off = o.rel_y_off; L.y_src = o.y_src; L.col_ptr = o.col_ptr;
       L.csc_pos = o.csc_pos; L.csc_row = o.csc_row; L.csc_col = o.csc_col; L.slot_y = o.slot_y; L.U_dev = o.U_dev;
+      L.xg = L.ynum ? nullptr : o.x_gather;
       const int et = m.N > 0 ? tiles(m.N, kEdgeTile) : 0;
       blocks[K_CLASSIFY][q] = et;
       blocks[K_SCAN][q] = L.t_rows + L.t_slots;

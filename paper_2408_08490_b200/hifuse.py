@@ -39,7 +39,7 @@ class LayerShape(ctypes.Structure):
 class Csr(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("rel_row_off", "row_ptr", "col", "eperm", "rel_y_off", "y_src", "col_ptr",
-                 "csc_pos", "csc_row", "csc_col", "slot_y", "U_dev")]
+                 "csc_pos", "csc_row", "csc_col", "slot_y", "U_dev", "x_gather")]
 
 
 class GraphCsc(ctypes.Structure):
@@ -219,6 +219,11 @@ class CsrBuffers:
             for k in ("rel_y_off", "y_src", "slot_y", "U_dev"):
                 self.t[k] = None
         self.c = Csr(**{k: (v.data_ptr() if v is not None else None) for k, v in self.t.items()})
+
+    def set_x_gather(self, gather_ids):
+        """X-row mode: the build maps every column through these feature-store
+        row ids (col = feature row); None: col = X row."""
+        self.c.x_gather = None if gather_ids is None else gather_ids.data_ptr()
 
     def __getitem__(self, k):
         return self.t[k]

@@ -51,6 +51,15 @@ class SampledLoop:
         self.seeds_d = [i32() for _ in range(self.RING + 1)]
         self.labels_d = [i32() for _ in range(self.RING + 1)]
         self.ctl_h = [torch.zeros(2, dtype=torch.int64).pin_memory() for _ in range(self.RING + 1)]
+        # pinned staging of each ring set's seeds / labels: the host fills it
+        # (numpy) and the graph's own copy nodes move it to the device, so a
+        # step costs the host a few array writes and one replay
+        self.seeds_h = [torch.zeros(B, dtype=torch.int32).pin_memory()
+                        for _ in range(self.RING + 1)]
+        self.labels_h = [torch.zeros(B, dtype=torch.int32).pin_memory()
+                         for _ in range(self.RING + 1)]
+        self.seeds_np = [x.numpy() for x in self.seeds_h]
+        self.labels_np = [x.numpy() for x in self.labels_h]
         self.ctl_d = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(self.RING + 1)]
         self.cnt_h = [torch.zeros(L * (2 * T + 1), dtype=torch.int32).pin_memory()
                       for _ in range(self.RING + 1)]
@@ -80,19 +89,30 @@ class SampledLoop:
     def _batch(self, i):
         return self.pb[(i % self.RING, i % self.SLOTS)]
 
-    def _stage(self, i, ring=None):
-        """Host -> device seeds / labels / {key, stamp} of batch i (current
-        stream, pinned sources)."""
+    def _fill(self, i, ring=None):
+        """Host side of staging batch i: its seeds / labels / {key, stamp}
+        into ring set r's pinned buffers."""
         r = i % self.RING if ring is None else ring
         seeds_h, labels_h, key = self.batch_fn(i)
         if seeds_h.numel() != self.smp.B or labels_h.numel() != self.smp.B:
             raise ValueError("a padded batch has exactly B seeds (drop the last partial batch)")
-        self.seeds_d[r].copy_(seeds_h, non_blocking=True)
-        self.labels_d[r].copy_(labels_h, non_blocking=True)
+        self.seeds_np[r][:] = seeds_h.numpy()
+        self.labels_np[r][:] = labels_h.numpy()
         key = int(key)
         self.ctl_np[r][0] = key - (1 << 64) if key >= (1 << 63) else key
         self.ctl_np[r][1] = self.smp.next_stamp()
+        return r
+
+    def _copy_in(self, r):
+        """Pinned -> device copies of ring set r's staged inputs (current
+        stream; captured into the graphs as copy nodes)."""
+        self.seeds_d[r].copy_(self.seeds_h[r], non_blocking=True)
+        self.labels_d[r].copy_(self.labels_h[r], non_blocking=True)
         self.ctl_d[r].copy_(self.ctl_h[r], non_blocking=True)
+
+    def _stage(self, i, ring=None):
+        """Eager staging of batch i (prime / fallback paths)."""
+        self._copy_in(self._fill(i, ring))
 
     def _sample(self, r):
         self.smp.sample_padded(self.seeds_d[r], self.target, self.src_cap, self.edge_pad,
@@ -130,7 +150,10 @@ class SampledLoop:
                 with torch.cuda.stream(self.side_b):
                     bop()
                 with torch.cuda.stream(self.side_s):
-                    self._sample((c + 2) % self.RING)
+                    rs = (c + 2) % self.RING
+                    self._copy_in(rs)               # seeds / labels / ctl of batch i+2
+                    self._sample(rs)
+                    self._copy_counts(rs)           # its counts -> pinned host
                 for _, fn in ops:
                     fn()
                 hf.sgd(tr.params, tr.grads, tr.lr, 1.0 / max(tr.world, 1))
@@ -207,9 +230,8 @@ class SampledLoop:
             if not self._fits(i):
                 self._fallback(i)
                 continue
-            self._stage(i + 2)
+            self._fill(i + 2)                       # the graph copies it in
             self.graphs[i % 6].replay()
-            self._copy_counts((i + 2) % self.RING)
             ev = self.ev_ring[i % len(self.ev_ring)]   # (waited on two batches later)
             ev.record(main)
             self.done[i] = ev

@@ -248,14 +248,14 @@ class Trainer:
             return lambda: hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"],
                                                     dev["eid"], edge_type, wsb, self.status,
                                                     rel_edge_off=off)
-        # aggregate-first input layer: the feature-store row of every CSR
-        # position is formed with the build (off the critical path)
-        colx = self._buf(f"colx{db.slot}", max(shapes[0].N, 1), torch.int32)
+        # aggregate-first input layer: X-row build whose columns are mapped
+        # through the batch's gather ids, so col holds the feature-store row of
+        # every CSR position (formed with the build, off the critical path)
 
         def op():
+            csrs[0].set_x_gather(dev["gid"])
             hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"], edge_type,
                                      wsb, self.status, rel_edge_off=off)
-            hf.feature_cols(shapes[0], csrs[0], dev["gid"], colx)
         return op
 
     # ----------------------------------------------------------------- plan
@@ -289,8 +289,9 @@ class Trainer:
                      wsp=self._ws(hf.project_ws_bytes(sh, K, D, H)))
             if self.agg_first and l == 0:
                 a.update(Y=None, Xagg=self._mat("Xagg0", sh.rows, K))
-                # colx: written by this batch's build op (hifuse_feature_cols)
-                colx = self._buf(f"colx{db.slot}", max(sh.N, 1), torch.int32)
+                # colx: the feature-store row of every CSR position, written by
+                # this batch's build (X-row mode through the gather ids)
+                colx = csrs[l]["col"]
                 if self.feat_dtype == "bf16":
                     a.update(Xroot=self._mat("Xdst0", sh.src_rows, K), gid_root=None)
                     ops.append(("aggregate_features.0", lambda sh=sh, c=csrs[l], a=a, colx=colx:

@@ -14,12 +14,15 @@ def hf():
     return h
 
 
-def gpu_build(blk, et, rel_src, rel_dst, status=None, csc=True, ranged=False, xrow=False):
+def gpu_build(blk, et, rel_src, rel_dst, status=None, csc=True, ranged=False, xrow=False,
+              x_gather=None):
     """Runs hifuse_build_semantic_graphs on one layer; returns (shape, csr).
     ranged: pass the relation-major offsets of `et` instead of the table."""
     h = hf()
     sh = h.Shape(rel_src, rel_dst, blk.n_src, blk.n_dst, blk.num_edges)
     csr = h.CsrBuffers(sh, DEV, csc=csc, xrow=xrow)
+    if x_gather is not None:
+        csr.set_x_gather(x_gather)
     ws = torch.empty((sh.build_ws + 3) // 4 + 16, dtype=torch.int32, device=DEV)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=DEV)
     t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt)).to(DEV)

@@ -87,6 +87,16 @@ def test_xrow_build(seed):
     hf().aggregate_features_cols(sh, csr, "mean", K, X, c1, a1)
     hf().aggregate_features_cols(sh2, csr2, "mean", K, X, c2, a2)
     assert torch.equal(a1, a2)
+    # x_gather: the build writes the feature-store rows itself (the Trainer's
+    # aggregate-first layer: col is read as the feature-row map directly)
+    gd = t(gid, torch.int32)
+    sh3, csr3, st3 = gpu_build(blk, et, rs, rd, csc=False, xrow=True, x_gather=gd)
+    assert int(st3.item()) == 0
+    assert torch.equal(csr3["col"][:nv], c1[:nv])
+    assert (csr3["col"][nv:sh.N] == -1).all()
+    a3 = torch.zeros_like(a1)
+    hf().aggregate_features_cols(sh3, csr3, "mean", K, X, csr3["col"], a3)
+    assert torch.equal(a3, a1)
 
 
 @pytest.mark.parametrize("K", [64, 128])
