@@ -12,9 +12,8 @@
 // Every kernel covers all layers of the call (a flattened (layer, tile) grid):
 //   memset      per-layer counters (one contiguous zone)
 //   k_classify  EdgeTypeLayer (gather, or binary search of relation-major
-//               edge-id ranges) + validation; row histogram whose atomic
-//               return is the edge's arrival rank in its row (warp-aggregated:
-//               one atomic per distinct row of a warp); per (relation,
+//               edge-id ranges) + validation; row histogram (warp-aggregated
+//               reductions: one per distinct row of a warp); per (relation,
 //               source) slot the number of edges
 //   k_scan      segmented decoupled-look-back scan of the row counts and of
 //               the slot (presence, count) pairs: row_ptr, rel_row_off,
@@ -25,7 +24,9 @@
 //               edges with one key) and the first edge of a run
 //   k_scatter   pos = row_ptr[key] + (e - first edge of the run) for a row of
 //               ONE run (input order: the sampler lists a destination's edges
-//               of a relation together), else + rank (unsorted): eperm, col
+//               of a relation together), else + an arrival ticket (unsorted):
+//               eperm, col.  (k_classify's row histogram is therefore a
+//               fire-and-forget reduction: no atomic round trip per edge.)
 //   k_rows      warp per HF_BUILD_ROWS_PER_WARP consecutive rows: their CSR
 //               span staged in shared memory, every row of several runs sorted
 //               by original column (restores Alg. 2's order: bit-exact and
@@ -108,10 +109,11 @@ struct BLayer {
   // workspace: zero zone
   int *cnt, *ccur;                     // cnt = [row counts | slot counts]
   int* runs;                           // per row: runs of consecutive input edges
+  int* rcur;                           // per row: arrival tickets (rows of several runs)
   int* lcnt;                           // [0] long rows, [1] long columns
   unsigned long long* sst;             // scan tile status [t_rows | t_slots]
   // workspace: scratch
-  int *key_e, *slot_e, *rank_e, *gk, *gv, *long_rows, *long_cols;
+  int *key_e, *slot_e, *gk, *gv, *long_rows, *long_cols;
   int* first;                          // per row: first input edge of its (last) run
   int rows_reg, cols_reg;              // regular (non-long) blocks of k_rows / k_cols
   int cols_xtra;                       // extra k_cols blocks for hub columns
@@ -419,32 +421,29 @@ k_classify(const __grid_constant__ BuildParams bp) {
   }
   // Warp-aggregated atomics: sampled blocks list the edges of a destination
   // (and often of a source) together, so lanes of a warp often share a row
-  // or slot -- one atomic per distinct address and warp.  Row: the atomic's
-  // return is the arrival rank (lane order inside the warp).
+  // or slot -- one atomic per distinct address and warp.
   unsigned prow[kEPT], pslot[kEPT];
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
     prow[q] = __match_any_sync(0xffffffffu, key[q] >= 0 ? key[q] : -1 - lane);
     pslot[q] = L.ynum ? __match_any_sync(0xffffffffu, key[q] >= 0 ? slot[q] : -1 - lane) : 0u;
   }
-  int base[kEPT];
+  // counts only (no return value: fire-and-forget reductions); an edge's
+  // position inside its row is formed by k_scatter -- from its run for a row
+  // of one run, from an arrival ticket for the (rare) rows of several runs
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
     const bool lead_r = key[q] >= 0 && lane == __ffs(prow[q]) - 1;
     const bool lead_s = L.ynum && key[q] >= 0 && lane == __ffs(pslot[q]) - 1;
-    base[q] = lead_r ? atomicAdd(L.cnt + key[q], __popc(prow[q])) : 0;
+    if (lead_r) atomicAdd(L.cnt + key[q], __popc(prow[q]));
     if (lead_s) atomicAdd(L.cnt + slot[q], __popc(pslot[q]));
   }
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
-    const int b = __shfl_sync(0xffffffffu, base[q], __ffs(prow[q]) - 1);
     const int e = e0 + q * kBT + threadIdx.x;
     if (key[q] == -1) continue;
     L.key_e[e] = key[q] >= 0 ? key[q] : -1;
-    if (key[q] >= 0) {
-      L.slot_e[e] = L.ynum ? slot[q] - L.rows : slot[q];
-      L.rank_e[e] = b + __popc(prow[q] & ((1u << lane) - 1u));
-    }
+    if (key[q] >= 0) L.slot_e[e] = L.ynum ? slot[q] - L.rows : slot[q];
   }
 }
 
@@ -643,13 +642,12 @@ k_scatter(const __grid_constant__ BuildParams bp) {
   const BLayer& L = bp.lay[layer_of(bp.p, K_SCATTER, &j)];
   const int nvalid = L.row_ptr[L.rows];
   const int e0 = j * kEdgeTile;
-  int key[kEPT], slot[kEPT], rank[kEPT], pos[kEPT], c[kEPT];
+  int key[kEPT], slot[kEPT], pos[kEPT], c[kEPT];
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
     const int e = e0 + q * kBT + threadIdx.x;
     key[q] = e < L.N ? L.key_e[e] : -1;
     slot[q] = key[q] >= 0 ? L.slot_e[e] : 0;
-    rank[q] = key[q] >= 0 ? L.rank_e[e] : 0;
   }
 #pragma unroll
   for (int q = 0; q < kEPT; q++) {
@@ -657,7 +655,9 @@ k_scatter(const __grid_constant__ BuildParams bp) {
     // one-run row: input order directly; else the arrival rank (k_rows sorts)
     const int rn = key[q] >= 0 ? L.runs[key[q]] : 0;
     const int f = rn == 1 ? L.first[key[q]] : 0;
-    pos[q] = key[q] >= 0 ? L.row_ptr[key[q]] + (rn == 1 ? e - f : rank[q]) : 0;
+    // several runs: an arrival ticket (k_rows sorts those rows)
+    const int rk = (key[q] >= 0 && rn != 1) ? atomicAdd(L.rcur + key[q], 1) : 0;
+    pos[q] = key[q] >= 0 ? L.row_ptr[key[q]] + (rn == 1 ? e - f : rk) : 0;
     c[q] = key[q] >= 0 ? (L.ynum ? L.slot_y[slot[q]] : (L.xg ? L.xg[slot[q]] : slot[q])) : 0;
   }
 #pragma unroll
@@ -944,10 +944,10 @@ struct LayerWs {
 LayerWs layer_ws_sizes(const LayerMeta& m, bool csc) {
   const long long U_max = umax_of(m);
   LayerWs s;
-  s.zero_bytes = carve_bytes((long long)m.rows + m.S, 4) + carve_bytes(m.rows, 4) +
+  s.zero_bytes = carve_bytes((long long)m.rows + m.S, 4) + 2 * carve_bytes(m.rows, 4) +
                  (csc ? carve_bytes(U_max + 1, 4) : 0) + carve_bytes(2, 4) +
                  carve_bytes(2ll * (tiles(m.rows, kScanTile) + tiles(m.S, kScanTile)), 4);
-  s.scratch_bytes = carve_bytes(m.N, 4) * 5 +              // key_e slot_e rank_e gk gv
+  s.scratch_bytes = carve_bytes(m.N, 4) * 4 +              // key_e slot_e gk gv
                     carve_bytes(m.rows, 4) + carve_bytes(U_max, 4) +  // long lists
                     carve_bytes(m.rows, 4);                           // first
   return s;
@@ -959,13 +959,13 @@ void carve_layer(const LayerMeta& m, bool csc, char*& zp, char*& sp, BLayer* L) 
   L->t_slots = tiles(m.S, kScanTile);
   L->cnt = carve<int>(zp, (long long)m.rows + m.S);
   L->runs = carve<int>(zp, m.rows);
+  L->rcur = carve<int>(zp, m.rows);
   L->ccur = csc ? carve<int>(zp, U_max + 1) : nullptr;
   L->lcnt = carve<int>(zp, 2);
   L->sst = reinterpret_cast<unsigned long long*>(
       carve<int>(zp, 2ll * (L->t_rows + L->t_slots)));
   L->key_e = carve<int>(sp, m.N);
   L->slot_e = carve<int>(sp, m.N);
-  L->rank_e = carve<int>(sp, m.N);
   L->gk = carve<int>(sp, m.N);
   L->gv = carve<int>(sp, m.N);
   L->long_rows = carve<int>(sp, m.rows);
