@@ -273,6 +273,23 @@ hifuse_status hifuse_semantic_fuse(const hifuse_layer_shape *shape, int D, hifus
                                    const float *d_Z, const float *d_R0, const float *d_bias,
                                    float *d_H, hifuse_stream_t stream);
 
+/* A4 + A5 in one launch (RGCN sum / mean): hifuse_aggregate_fwd's Z rows
+ * and hifuse_semantic_fuse's H, bit-identical to the two calls.  The warp
+ * completing the last relation row (r, i) of destination (t, i) (a fenced
+ * per-destination arrival counter) sums R0 + bias + the Z rows of t's
+ * relations in relation order; destinations of a type no relation enters get
+ * act(R0 + bias).  Arguments as for the two calls (Z is still written: the
+ * rows of the other relations are read back from it).  Workspace:
+ * hifuse_aggregate_fuse_ws_bytes() ints, ZEROED by the caller before the
+ * first call; every call leaves it zeroed (CUDA-graph safe).  PAPER.md
+ * lines 123 (fusion) and 246-262 (Alg. 1). */
+size_t hifuse_aggregate_fuse_ws_bytes(const hifuse_layer_shape *shape);
+hifuse_status hifuse_aggregate_fuse_fwd(const hifuse_layer_shape *shape, const hifuse_csr *csr,
+                                        hifuse_agg agg, int D, hifuse_act act, const float *d_Y,
+                                        const float *d_R0, const float *d_bias, float *d_Z,
+                                        float *d_H, void *d_ws, size_t ws_bytes,
+                                        hifuse_stream_t stream);
+
 /* A6a. Fusion backward: G = dH * act'(H) (ReLU' = 1[H > 0]); G is dR0 and
  * the gradient of every Z row (r, i) (= G_{t(r)}[i]); dbias_t = sum_i G_t[i]
  * (fixed-order two-stage reduction).  dbias may be NULL.  Workspace:

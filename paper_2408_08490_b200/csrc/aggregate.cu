@@ -14,6 +14,7 @@
 // shuffles; the gathers of UNROLL edges per stream are issued back to back to
 // keep several 256-512 B row loads in flight per warp (HBM latency hiding).
 #include <cuda_bf16.h>
+#include <cstring>
 #include "common.cuh"
 
 namespace hf {
@@ -60,17 +61,15 @@ __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 __device__ __forceinline__ float4 ldcs4(const float4* p) { return __ldcs(p); }
 
 // ------------------------------------------------------------ forward SUM/MEAN
-template <int D, bool MEAN, bool CS = false>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict__ col,
-          const float4* __restrict__ Y, float4* __restrict__ Z) {
-  HF_PDL_ENTRY();
+// One merged row (warp; D = 64: two edge streams of 16 lanes): the row's sum
+// (mean: divided by its degree), in every stream-0 lane's float4 slice.
+template <int D, bool MEAN, bool CS>
+__device__ __forceinline__ float4 agg_row(long long row, const int* __restrict__ row_ptr,
+                                          const int* __restrict__ col,
+                                          const float4* __restrict__ Y, int lane) {
   constexpr int LPR = D / 4;              // lanes per row stream
   constexpr int NS = 32 / LPR;            // edge streams per warp
-  const int lane = threadIdx.x & 31;
   const int sl = lane % LPR, sid = lane / LPR;
-  long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (row >= rows) return;
   const int b = row_ptr[row], e = row_ptr[row + 1];
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int base = b; base < e; base += 32) {
@@ -96,14 +95,105 @@ k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict
   }
 #pragma unroll
   for (int o = LPR; o < 32; o <<= 1) acc = f4add(acc, f4shfl_xor(acc, o));
-  if (sid == 0) {
-    if (MEAN && e > b) {
-      float dg = (float)(e - b);
-      acc = make_float4(__fdiv_rn(acc.x, dg), __fdiv_rn(acc.y, dg), __fdiv_rn(acc.z, dg),
-                        __fdiv_rn(acc.w, dg));
-    }
-    Z[row * LPR + sl] = acc;
+  if (MEAN && e > b) {
+    float dg = (float)(e - b);
+    acc = make_float4(__fdiv_rn(acc.x, dg), __fdiv_rn(acc.y, dg), __fdiv_rn(acc.z, dg),
+                      __fdiv_rn(acc.w, dg));
   }
+  return acc;
+}
+
+template <int D, bool MEAN, bool CS = false>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict__ col,
+          const float4* __restrict__ Y, float4* __restrict__ Z) {
+  HF_PDL_ENTRY();
+  constexpr int LPR = D / 4;
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const float4 acc = agg_row<D, MEAN, CS>(row, row_ptr, col, Y, lane);
+  if (lane < LPR) Z[row * LPR + lane] = acc;
+}
+
+// A5 fused into A4 (hifuse_aggregate_fuse_fwd): the warp that completes the
+// LAST relation row (r, i) of destination (t, i) -- a per-destination arrival
+// counter, fenced -- forms H_t[i] = act(R0 + b + sum_r Z[(r, i)]) in
+// hifuse_semantic_fuse's order (relations in relation order, reading the
+// other rows' Z from L2) and resets the counter (graph-safe).  Destinations of
+// a type no relation enters (no rows) get H = act(R0 + b) from the blocks past
+// the aggregation grid.  Removes the fusion launch and its Z re-read pass.
+struct FuseEpi {
+  int R, relu;
+  unsigned agg_blocks;                 // blocks of the aggregation part
+  int n_orph;                          // destination rows of types without relations
+  int rel_row_off[HF_MAX_R + 1];
+  int rel_dst[HF_MAX_R];
+  int type_dst_off[HF_MAX_T + 1];
+  int list_off[HF_MAX_T + 1];          // relations into type t: rel_rows[list_off[t] ..)
+  int rel_rows[HF_MAX_R];
+  int n_orph_types;
+  int orph_t[HF_MAX_T];                // orphan types and their row prefix
+  int orph_off[HF_MAX_T + 1];
+};
+
+template <int D>
+__device__ __forceinline__ void fuse_dst(const FuseEpi& f, int t, int i, int lane,
+                                         const float4* __restrict__ Z,
+                                         const float4* __restrict__ R0,
+                                         const float4* __restrict__ bias,
+                                         float4* __restrict__ H) {
+  constexpr int LPR = D / 4;
+  if (lane >= LPR) return;
+  const long long o = f.type_dst_off[t] + i;
+  float4 v = R0 ? __ldcg(R0 + o * LPR + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (bias) {
+    const float4 b = bias[t * LPR + lane];
+    v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+  }
+  for (int k = f.list_off[t]; k < f.list_off[t + 1]; k++) {
+    const float4 z = __ldcg(Z + (long long)(f.rel_rows[k] + i) * LPR + lane);
+    v.x += z.x; v.y += z.y; v.z += z.z; v.w += z.w;
+  }
+  if (f.relu) {
+    v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+  }
+  H[o * LPR + lane] = v;
+}
+
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_agg_fuse_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict__ col,
+               const float4* __restrict__ Y, float4* __restrict__ Z, const FuseEpi f,
+               const float4* __restrict__ R0, const float4* __restrict__ bias,
+               float4* __restrict__ H, int* __restrict__ cnt) {
+  HF_PDL_ENTRY();
+  constexpr int LPR = D / 4;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x >= f.agg_blocks) {                 // destinations without relation rows
+    const int q = (blockIdx.x - f.agg_blocks) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (q >= f.n_orph) return;
+    int a = 0;
+    while (a + 1 < f.n_orph_types && f.orph_off[a + 1] <= q) a++;
+    fuse_dst<D>(f, f.orph_t[a], q - f.orph_off[a], lane, Z, R0, bias, H);
+    return;
+  }
+  const long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const float4 acc = agg_row<D, MEAN, false>(row, row_ptr, col, Y, lane);
+  if (lane < LPR) Z[row * LPR + lane] = acc;
+  const int r = upper_bound_i(f.rel_row_off, f.R + 1, (int)row) - 1;
+  const int t = f.rel_dst[r], i = (int)row - f.rel_row_off[r];
+  const int o = f.type_dst_off[t] + i;
+  __threadfence();                                  // publish this Z row
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) last = atomicAdd(cnt + o, 1) == f.list_off[t + 1] - f.list_off[t] - 1;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();                                  // the other rows' Z are visible
+  if (lane == 0) cnt[o] = 0;                        // ready for the next call
+  fuse_dst<D>(f, t, i, lane, Z, R0, bias, H);
 }
 
 
@@ -1210,6 +1300,65 @@ hifuse_status hifuse_aggregate_fwd(const hifuse_csr* csr, int64_t rows, hifuse_a
   } else {
     return HIFUSE_ERR_INVALID_ARG;
   }
+  return last_cuda();
+}
+
+size_t hifuse_aggregate_fuse_ws_bytes(const hifuse_layer_shape* shape) {
+  LayerMeta m;
+  if (make_meta(shape, &m) != HIFUSE_OK) return 0;
+  return carve_bytes(m.dst_rows > 0 ? m.dst_rows : 1, 4);
+}
+
+hifuse_status hifuse_aggregate_fuse_fwd(const hifuse_layer_shape* shape, const hifuse_csr* csr,
+                                        hifuse_agg agg, int D, hifuse_act act, const float* d_Y,
+                                        const float* d_R0, const float* d_bias, float* d_Z,
+                                        float* d_H, void* d_ws, size_t ws_bytes,
+                                        hifuse_stream_t stream) {
+  LayerMeta m;
+  hifuse_status rc = make_meta(shape, &m);
+  if (rc != HIFUSE_OK) return rc;
+  if (agg != HIFUSE_AGG_SUM && agg != HIFUSE_AGG_MEAN) return HIFUSE_ERR_UNSUPPORTED;
+  if (D != 64 && D != 128) return HIFUSE_ERR_UNSUPPORTED;
+  if (!csr || !csr->row_ptr || (m.rows > 0 && (!d_Z || !csr->col || !d_Y)) ||
+      (m.dst_rows > 0 && !d_H))
+    return HIFUSE_ERR_INVALID_ARG;
+  if (!aligned16(d_Y) || !aligned16(d_Z) || !aligned16(d_R0) || !aligned16(d_bias) ||
+      !aligned16(d_H))
+    return HIFUSE_ERR_ALIGNMENT;
+  if (ws_bytes < hifuse_aggregate_fuse_ws_bytes(shape) || !d_ws) return HIFUSE_ERR_WORKSPACE;
+  FuseEpi f;
+  memset(&f, 0, sizeof(f));
+  f.R = m.R;
+  f.relu = act == HIFUSE_ACT_RELU ? 1 : 0;
+  for (int r = 0; r <= m.R; r++) f.rel_row_off[r] = m.rel_row_off[r];
+  for (int r = 0; r < m.R; r++) f.rel_dst[r] = m.rel_dst[r];
+  for (int t = 0; t <= m.T; t++) f.type_dst_off[t] = m.type_dst_off[t];
+  int k = 0, no = 0;
+  for (int t = 0; t < m.T; t++) {
+    f.list_off[t] = k;
+    for (int r = 0; r < m.R; r++)
+      if (m.rel_dst[r] == t) f.rel_rows[k++] = m.rel_row_off[r];
+    if (k == f.list_off[t] && m.n_dst[t] > 0) {      // no relation enters t
+      f.orph_t[f.n_orph_types] = t;
+      f.orph_off[f.n_orph_types++] = no;
+      no += m.n_dst[t];
+    }
+  }
+  f.list_off[m.T] = k;
+  f.orph_off[f.n_orph_types] = no;
+  f.n_orph = no;
+  f.agg_blocks = ceil_div(m.rows, kWarpsPerBlock);
+  const unsigned grid = f.agg_blocks + ceil_div(no, kWarpsPerBlock);
+  cudaStream_t s = st(stream);
+  const int TB = kWarpsPerBlock * 32;
+  const bool mean = agg == HIFUSE_AGG_MEAN;
+#define HF_AF(DD, MM)                                                                          \
+  HF_LAUNCH((k_agg_fuse_fwd<DD, MM>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr,         \
+            csr->col, (const float4*)d_Y, (float4*)d_Z, f, (const float4*)d_R0,               \
+            (const float4*)d_bias, (float4*)d_H, (int*)d_ws)
+  if (D == 128) { if (mean) HF_AF(128, true); else HF_AF(128, false); }
+  else { if (mean) HF_AF(64, true); else HF_AF(64, false); }
+#undef HF_AF
   return last_cuda();
 }
 

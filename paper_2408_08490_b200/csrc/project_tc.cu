@@ -83,12 +83,21 @@ namespace hf {
 // has no edge of that relation); B chunk: W_term[k][d0..d0+32) for the CTA's
 // KN features k, which is already K-major (row k contiguous in d).
 #ifndef HF_DG_STAGES
-#define HF_DG_STAGES 4
+#define HF_DG_STAGES 6
+#endif
+#ifndef HF_DG_PRODUCERS
+#define HF_DG_PRODUCERS 6
 #endif
 static constexpr int kDgStages = HF_DG_STAGES;
+// producer warps: each keeps one chunk in flight (it waits for its own
+// cp.async group before arriving), so the chunks in flight per CTA = the
+// producer count (4 -> 6 with 6 stages: the mag inner-layer dgrad is one
+// 128-row tile per CTA, bound by this load latency)
+static constexpr int kDgProd = HF_DG_PRODUCERS;
+static_assert(kDgProd >= 4 && kDgProd <= kDgStages, "producers: >= 4 (epilogue), <= stages");
 
 template <int K, int D, int KN>
-__global__ void __launch_bounds__(160)
+__global__ void __launch_bounds__((kDgProd + 1) * 32)
 k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
            const float* __restrict__ G, const float* __restrict__ W_rel,
            const float* __restrict__ W_root, float* __restrict__ dX, int max_out) {
@@ -98,7 +107,7 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   //            warp waits for its own cp.async group before the proxy fence);
   //            afterwards the epilogue (TMEM lanes 32w .. 32w + 31)
   // warp 4:    one thread issues the MMAs in chunk order
-  constexpr int BM = 128, DC = D / 32, NS = K / KN, P = 4;
+  constexpr int BM = 128, DC = D / 32, NS = K / KN, P = kDgProd;
   constexpr uint32_t A_STAGE = BM * 128, B_STAGE = KN * 128, STAGE = A_STAGE + B_STAGE;
   constexpr uint32_t IDESC = idesc_tf32(BM, KN, 0, 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -205,8 +214,8 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
     mma_commit(smem_u32(&done));
   }
   __syncwarp();
-  if (warp < P) {
-    // ------------------------------------------------------------- epilogue
+  if (warp < 4) {
+    // -------------------------------------------- epilogue (TMEM lanes 32w..)
     if (NC > 0) {
       mbar_wait(smem_u32(&done), 0);
       tc_fence_after();
@@ -408,7 +417,7 @@ static void launch_dgrad(const DgradMeta& dm, int max_out, const int* slot_y, co
   const int smem = dgrad_smem<K, D, KN>() + max_out * 128 * 4;
   set_max_smem((const void*)k_dgrad_tc<K, D, KN>, smem);
   const unsigned grid = (unsigned)dm.tile_off[dm.T] * (K / KN);
-  HF_LAUNCH((k_dgrad_tc<K, D, KN>), grid, 160, smem, s, dm, slot_y, dY, G, W_rel, W_root, dX,
+  HF_LAUNCH((k_dgrad_tc<K, D, KN>), grid, (kDgProd + 1) * 32, smem, s, dm, slot_y, dY, G, W_rel, W_root, dX,
             max_out);
 }
 

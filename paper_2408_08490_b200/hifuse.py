@@ -83,6 +83,8 @@ def lib():
             "hifuse_fuse_bwd_ws_bytes": [vp, i32],
             "hifuse_semantic_fuse_bwd": [vp, i32, i32, vp, vp, vp, vp, vp, sz, vp],
             "hifuse_semantic_fuse_bwd_bias": [vp, i32, vp, vp, vp, sz, vp],
+            "hifuse_aggregate_fuse_ws_bytes": [vp],
+            "hifuse_aggregate_fuse_fwd": [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp],
             "hifuse_aggregate_bwd_ws_bytes": [vp, i32, i32],
             "hifuse_aggregate_bwd": [vp, vp, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp,
                                      vp, sz, vp],
@@ -137,7 +139,8 @@ def lib():
         for name in ("hifuse_project_ws_bytes", "hifuse_fuse_bwd_ws_bytes",
                      "hifuse_aggregate_bwd_ws_bytes", "hifuse_project_bwd_ws_bytes",
                      "hifuse_xent_ws_bytes", "hifuse_aggregate_features_ws_bytes",
-                     "hifuse_project_aggregated_bwd_ws_bytes", "hifuse_sem_att_ws_bytes"):
+                     "hifuse_project_aggregated_bwd_ws_bytes", "hifuse_sem_att_ws_bytes",
+                     "hifuse_aggregate_fuse_ws_bytes"):
             getattr(L, name).restype = ctypes.c_size_t
         L.hifuse_kernel_launches.restype = ctypes.c_int64
         L.hifuse_status_string.restype = ctypes.c_char_p
@@ -303,6 +306,18 @@ def semantic_fuse_bwd(shape, D, act, dH, H, G, dbias, ws, stream=None):
     _check("hifuse_semantic_fuse_bwd", lib().hifuse_semantic_fuse_bwd(
         shape.ref, D, ACT[act], _ptr(dH), _ptr(H), _ptr(G), _ptr(dbias), _ptr(ws),
         0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def aggregate_fuse_ws_bytes(shape):
+    return int(lib().hifuse_aggregate_fuse_ws_bytes(shape.ref))
+
+
+def aggregate_fuse_fwd(shape, csr, agg, D, act, Y, R0, bias, Z, H, ws, stream=None):
+    """ws: int32 tensor of aggregate_fuse_ws_bytes(shape) bytes, zeroed before
+    the first call (every call leaves it zeroed)."""
+    _check("hifuse_aggregate_fuse_fwd", lib().hifuse_aggregate_fuse_fwd(
+        shape.ref, csr.ref, AGG[agg], D, ACT[act], _ptr(Y), _ptr(R0), _ptr(bias), _ptr(Z),
+        _ptr(H), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def semantic_fuse_bwd_bias(shape, D, G, dbias, ws, stream=None):

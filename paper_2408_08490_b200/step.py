@@ -218,6 +218,15 @@ class Trainer:
             self._bufs[key] = c
         return c
 
+    def _zeros(self, key, n):
+        """int32 buffer of >= n entries, zeroed when (re)allocated (counters
+        the library leaves zeroed after every call)."""
+        t = self._bufs.get(key)
+        if t is None or t.numel() < n:
+            t = torch.zeros(max(int(n * 1.25), 16), dtype=torch.int32, device=self.device)
+            self._bufs[key] = t
+        return t
+
     def _ws(self, nbytes, key="ws"):
         return self._buf(key, (nbytes + 3) // 4 + 64)
 
@@ -334,6 +343,16 @@ class Trainer:
                     a["Y"], a["R0"], a["s_src"], a["s_dst"], a["wsp"], prec=self.prec)))
             if self.y_dtype == "bf16":
                 pass
+            elif self.agg in ("sum", "mean") and self.fusion == "sum":
+                # RGCN: aggregation and fusion in one launch (the last
+                # relation row of a destination forms its H row)
+                a["fcnt"] = self._zeros(f"fcnt{l}", hf.aggregate_fuse_ws_bytes(sh) // 4)
+                ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a, P=P:
+                            hf.aggregate_fuse_fwd(sh, c, self.agg, D, a["act"], a["Y"], a["R0"],
+                                                  P["bias"], a["Z"], a["H"], a["fcnt"])))
+                acts.append(a)
+                X, gid = a["H"], None
+                continue
             elif self.agg == "gat_xrel":     # softmax across relations (NEXT(2))
                 ops.append((f"aggregate_fwd.{l}", lambda sh=sh, c=csrs[l], a=a:
                             hf.aggregate_fwd_xrel(sh, c, D, H, self.slope, a["Y"], a["s_src"],

@@ -735,3 +735,46 @@ def test_semantic_fuse_att(D, act):
     for name, got, ref in (("dWs", dWs, sem["dWs"]), ("dbs", dbs, sem["dbs"]),
                            ("dq", dq, sem["dq"])):
         assert rl2(got.cpu().numpy(), ref) < 5e-5, name
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("agg", ["sum", "mean"])
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_fuse_fwd(seed, agg, D):
+    """hifuse_aggregate_fuse_fwd (A4 + A5 in one launch) is bit-identical to
+    hifuse_aggregate_fwd + hifuse_semantic_fuse, including destinations of a
+    type no relation enters, over repeated calls (the arrival counters reset
+    themselves), with and without ReLU; H checked against the oracle too."""
+    rng = np.random.default_rng(4000 + seed)
+    T, R = 5, 8
+    rs, rd = random_schema(rng, T, R)
+    rd = np.where(rd == T - 1, 0, rd).astype(np.int32)      # type T-1: no relation enters it
+    n_src = rng.integers(30, 300, T)
+    n_dst = np.maximum(np.minimum(rng.integers(0, 200, T), n_src), 1)
+    blk, et = random_block(rng, n_src, n_dst, rs, rd, 3000, hub_frac=0.1 * (seed % 2))
+    sh, csr, st = gpu_build(blk, et, rs, rd)
+    ch = csr_host(sh, csr)
+    U = ch["U"]
+    ws = torch.zeros(hf().aggregate_fuse_ws_bytes(sh) // 4 + 16, dtype=torch.int32, device=DEV)
+    for it, act in enumerate(("relu", "none", "relu")):
+        Y = t(rng.standard_normal((max(U, 1), D)).astype(np.float32))
+        R0 = t(rng.standard_normal((sh.dst_rows, D)).astype(np.float32))
+        b = t(rng.standard_normal((sh.T, D)).astype(np.float32))
+        Z1 = torch.zeros(max(sh.rows, 1), D, device=DEV)
+        H1 = torch.full((sh.dst_rows, D), float("nan"), device=DEV)
+        hf().aggregate_fwd(csr, sh.rows, agg, D, 1, 0.2, Y, None, None, Z1, None)
+        hf().semantic_fuse(sh, D, act, Z1, R0, b, H1)
+        Z2 = torch.zeros_like(Z1)
+        H2 = torch.full_like(H1, float("nan"))
+        hf().aggregate_fuse_fwd(sh, csr, agg, D, act, Y, R0, b, Z2, H2, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(Z1[:sh.rows], Z2[:sh.rows]), it
+        assert torch.equal(H1, H2), it
+        assert int(ws.abs().sum().item()) == 0            # counters left zeroed
+    osh = oracle.Shape.of(blk, rs, rd)
+    Yn = Y.cpu().numpy()[:U]
+    Zr = oracle.aggregate_fwd(osh, blk, et, ch, agg, D, 1, Yn)["Z"]
+    Za = oracle.aggregate_fwd(osh, blk, et, ch, agg, D, 1, np.abs(Yn))["Z"]
+    Hr = oracle.fuse(osh, D, 1, Zr, R0.cpu().numpy(), b.cpu().numpy())
+    Ha = oracle.fuse(osh, D, 0, Za, np.abs(R0.cpu().numpy()), np.abs(b.cpu().numpy()))
+    close_scaled(H2.cpu().numpy(), Hr, Ha, what="H fused")
