@@ -154,7 +154,7 @@ def stage_cost(stage, l, cfg, sz):
         C, B = cfg.num_classes, cfg.batch_size
         return 4 * (2 * B * D + 2 * D * C + 2 * B * C), 2 * 2 * B * D * C
     if stage == "aggregate_features":     # aggregate-first input layer: A4 over raw X
-        if FEAT_BYTES == 2:                   # BF16 store: + fp32 dst rows written
+        if FEAT_BYTES == 2 and l == 0:        # BF16 store: + fp32 dst rows written
             return (2 * K * s["F"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"]
                     + 4 * K * s["dst"]), 0
         return 4 * K * s["F"] + 4 * s["N"] + 4 * (s["rows"] + 1) + 4 * K * s["rows"], 0
@@ -441,6 +441,8 @@ def main():
     ap.add_argument("--config", default="mag", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="hifuse", choices=["hifuse", "reference"])
     ap.add_argument("--pool", type=int, default=16)
+    ap.add_argument("--inner-order", default="agg_first", choices=["project_first", "agg_first"],
+                    help="forward order of the RGCN inner layers under --order agg_first")
     ap.add_argument("--repeats", type=int, default=5,
                     help="the K-step timed region is repeated this many times; value = median")
     ap.add_argument("--prec", default="tf32", choices=["fp32", "tf32", "bf16"])
@@ -528,7 +530,8 @@ def main():
     tr = Trainer(cfg.num_types, cfg.num_rels, rs, rd, cfg.feat_dim, cfg.hidden, cfg.heads,
                  cfg.num_classes, cfg.num_layers, cfg.model, cfg.agg, dev, lr=args.lr,
                  prec=args.prec, order=args.order, fusion=args.fusion,
-                 feat_dtype=args.feat_dtype, y_dtype=args.y_dtype)
+                 feat_dtype=args.feat_dtype, y_dtype=args.y_dtype,
+                 inner_agg_first=args.inner_order == "agg_first")
     BUILD_XROW0[0] = tr.agg_first      # (stage_cost of the build)
     tr.load_params(params)
     tr.prepare_graph(et_d)           # relation-major edge ids -> R+1 offsets (once per graph)

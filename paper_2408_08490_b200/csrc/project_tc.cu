@@ -488,9 +488,32 @@ namespace hf {
 //              8 rows x 64 contiguous bytes per instruction, then `tempty`.
 // The tile table (128-row tiles per group) is built in shared memory from
 // rel_y_off at kernel start.
-static constexpr int kFStages = 3;
-static constexpr int kLag = 2;
-static constexpr int kFwdCtas = 2;
+#ifndef HF_F_STAGES
+#define HF_F_STAGES 3
+#endif
+#ifndef HF_F_LAG
+#define HF_F_LAG 2
+#endif
+#ifndef HF_F_CTAS
+#define HF_F_CTAS 2
+#endif
+static constexpr int kFStages = HF_F_STAGES;
+static constexpr int kLag = HF_F_LAG;
+static constexpr int kFwdCtas = HF_F_CTAS;
+static_assert(kLag < kFStages, "cp.async lag below the stage count");
+// The fused fusion GEMM of the aggregate-first layers (k_fuse_gemm_tcp) has
+// one 128-row tile per CTA (fewer tiles than SMs on every workload) and a long
+// K loop ((1 + R_in) K): one CTA per SM with 4 stages beats two with 3
+// (measured, mag: 16.8 -> 14.7 us); the per-relation projection, with many
+// tiles per CTA, keeps two CTAs per SM (mag project-first: 83 vs 100-108 us
+// with 1 CTA).
+#ifndef HF_G_STAGES
+#define HF_G_STAGES 4
+#endif
+static constexpr int kGStages = HF_G_STAGES;
+static constexpr int kGLag = 2;
+static constexpr int kGCtas = 1;
+static_assert(kGLag < kGStages, "cp.async lag below the stage count");
 
 // Tiles (or chunks) of `step` rows per group -> s_tab[0..G], one warp.
 __device__ __forceinline__ void group_table_warp(const ProjMeta& pm, const int* s_yoff, int step,
@@ -812,7 +835,7 @@ struct FuseGemmMeta {
 };
 
 template <int K, int D, bool RELU>
-__global__ void __launch_bounds__(288, kFwdCtas)
+__global__ void __launch_bounds__(288, kGCtas)
 k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float* __restrict__ X,
                 const float* __restrict__ Xm, const float* __restrict__ W_rel,
                 const float* __restrict__ W_root, const float* __restrict__ bias,
@@ -823,13 +846,13 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
   constexpr uint32_t STAGE = A_STAGE + B_STAGE;
   constexpr uint32_t IDESC = idesc_tf32(BM, D, 0, 1);      // A K-major, B MN-major
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[kFStages], empty[kFStages], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[kGStages], empty[kGStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(16) float stage_ep[4 * 32 * 20];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   if (tid == 0) {
-    for (int q = 0; q < kFStages; q++) {
+    for (int q = 0; q < kGStages; q++) {
       mbar_init(smem_u32(&full[q]), 128);
       mbar_init(smem_u32(&empty[q]), 1);
     }
@@ -888,8 +911,8 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
           }
         }
         for (int c = 0; c < NCS; c++, it++) {
-          const int s = it % kFStages;
-          if (it >= kFStages) mbar_wait(smem_u32(&empty[s]), ((it / kFStages) - 1) & 1);
+          const int s = it % kGStages;
+          if (it >= kGStages) mbar_wait(smem_u32(&empty[s]), ((it / kGStages) - 1) & 1);
           const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
 #pragma unroll
           for (int i = 0; i < 8; i++) {
@@ -904,17 +927,17 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
                        Wg + (long long)(c * 32 + kr) * D + n, 16);
           }
           cp_async_commit();
-          if (it >= kLag) {
-            cp_async_wait<kLag>();
+          if (it >= kGLag) {
+            cp_async_wait<kGLag>();
             fence_proxy_async();
-            mbar_arrive(smem_u32(&full[(it - kLag) % kFStages]));
+            mbar_arrive(smem_u32(&full[(it - kGLag) % kGStages]));
           }
         }
       }
     }
     cp_async_wait<0>();
     fence_proxy_async();
-    for (int j = it - kLag < 0 ? 0 : it - kLag; j < it; j++) mbar_arrive(smem_u32(&full[j % kFStages]));
+    for (int j = it - kGLag < 0 ? 0 : it - kGLag; j < it; j++) mbar_arrive(smem_u32(&full[j % kGStages]));
   } else if (warp < 8) {
     // ------------------------------------------------------------- epilogue
     const int q = warp - 4;
@@ -972,8 +995,8 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
       tc_fence_after();
       const int nc = nseg * NCS;
       for (int c = 0; c < nc; c++, it++) {
-        const int s = it % kFStages;
-        mbar_wait(smem_u32(&full[s]), (it / kFStages) & 1);
+        const int s = it % kGStages;
+        mbar_wait(smem_u32(&full[s]), (it / kGStages) & 1);
         tc_fence_after();
         const uint32_t sa = base + s * STAGE, sb = sa + A_STAGE;
 #pragma unroll
@@ -992,6 +1015,8 @@ k_fuse_gemm_tcp(FuseGemmMeta fm, const int* __restrict__ gather_ids, const float
 
 template <int K, int D>
 static constexpr int fwdp_smem() { return kFStages * (128 * 128 + D * 128) + 1024; }
+template <int K, int D>
+static constexpr int fuseg_smem() { return kGStages * (128 * 128 + D * 128) + 1024; }
 
 template <int K, int D, bool BF, bool YB>
 static void launch_tcp(const ProjMeta& pm, const int* rel_off, const int* y_src,
@@ -1008,8 +1033,8 @@ template <int K, int D, bool RELU>
 static void launch_fuse_gemm(const FuseGemmMeta& fm, const int* gid, const float* X,
                              const float* Xm, const float* W_rel, const float* W_root,
                              const float* bias, float* H, cudaStream_t s) {
-  set_max_smem(reinterpret_cast<const void*>(&k_fuse_gemm_tcp<K, D, RELU>), fwdp_smem<K, D>());
-  HF_LAUNCH((k_fuse_gemm_tcp<K, D, RELU>), sm_count() * kFwdCtas, 288, (fwdp_smem<K, D>()), s, fm,
+  set_max_smem(reinterpret_cast<const void*>(&k_fuse_gemm_tcp<K, D, RELU>), fuseg_smem<K, D>());
+  HF_LAUNCH((k_fuse_gemm_tcp<K, D, RELU>), sm_count() * kGCtas, 288, (fuseg_smem<K, D>()), s, fm,
             gid, X, Xm, W_rel, W_root, bias, H);
 }
 

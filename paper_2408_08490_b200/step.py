@@ -81,7 +81,7 @@ class Trainer:
 
     def __init__(self, T, R, rel_src, rel_dst, K0, D, H, C, L, model, agg, device, lr=0.01,
                  prec="tf32", slope=0.2, order="project_first", fusion="sum", fuse_gemm=True,
-                 feat_dtype="fp32", y_dtype="fp32"):
+                 feat_dtype="fp32", y_dtype="fp32", inner_agg_first=True):
         hf.lib()   # raises if libhifuse.so is missing (no CPU fallback)
         self.T, self.R, self.K0, self.D, self.H, self.C, self.L = T, R, K0, D, H, C, L
         self.rel_src = np.asarray(rel_src, np.int32)
@@ -121,6 +121,11 @@ class Trainer:
         # aggregate-first input layer: projection + fusion as one GEMM per
         # destination type (hifuse_project_fuse_aggregated, NEXT(3))
         self.fuse_gemm = bool(fuse_gemm) and self.agg_first
+        # ... and the inner layers' FORWARD in the same order (their backward
+        # stays project-first: RGCN's transpose SpMM, dgrad and wgrad read only
+        # G, the CSC and the layer input, never Y or Z, so the two forward
+        # orders feed the identical backward; exact by linearity, reading C3')
+        self.agg_first_inner = bool(inner_agg_first) and self.fuse_gemm and y_dtype == "fp32"
         # NEXT(3) byte diet: BF16 storage of the input features (the
         # aggregate-first input layer reads them; its root term reads the
         # destination rows converted to fp32 by the same launch)
@@ -261,10 +266,17 @@ class Trainer:
         # through the batch's gather ids, so col holds the feature-store row of
         # every CSR position (formed with the build, off the critical path)
 
+        colxs = [self._buf(f"colx{db.slot}.{l}", max(shapes[l].N, 1), torch.int32)
+                 for l in range(1, len(shapes))] if self.agg_first_inner else []
+
         def op():
             csrs[0].set_x_gather(dev["gid"])
             hf.build_semantic_graphs(shapes, csrs, dev["src"], dev["dst"], dev["eid"], edge_type,
                                      wsb, self.status, rel_edge_off=off)
+            # inner layers (aggregate-first forward): the X row (previous
+            # layer's H) of every CSR position, from their Y-numbered build
+            for l, cx in enumerate(colxs, start=1):
+                hf.feature_cols(shapes[l], csrs[l], None, cx)
         return op
 
     # ----------------------------------------------------------------- plan
@@ -325,6 +337,22 @@ class Trainer:
                                                       a["R0"], prec=self.prec_tc)))
                     ops.append((f"fuse.{l}", lambda sh=sh, a=a, P=P: hf.semantic_fuse(
                         sh, D, a["act"], a["Z"], a["R0"], P["bias"], a["H"])))
+                acts.append(a)
+                X, gid = a["H"], None
+                continue
+            if self.agg_first_inner and l > 0:
+                # aggregate-first forward of an inner RGCN layer: the previous
+                # layer's H rows aggregated, then one fused GEMM per
+                # destination type (no Y, no Z); backward as project-first
+                a.update(Xagg=self._mat(f"Xagg{l}", sh.rows, K))
+                colx = self._buf(f"colx{db.slot}.{l}", max(sh.N, 1), torch.int32)
+                ops.append((f"aggregate_features.{l}", lambda sh=sh, c=csrs[l], a=a, colx=colx:
+                            hf.aggregate_features_cols(sh, c, self.agg, a["K"], a["X"], colx,
+                                                       a["Xagg"])))
+                ops.append((f"project_fuse_aggregated.{l}", lambda sh=sh, c=csrs[l], a=a, P=P:
+                            hf.project_fuse_aggregated(sh, c, a["K"], D, a["act"], a["Xagg"],
+                                                       a["X"], None, P["W_rel"], P["W_root"],
+                                                       P["bias"], a["H"], prec=self.prec_tc)))
                 acts.append(a)
                 X, gid = a["H"], None
                 continue
