@@ -270,6 +270,9 @@ def config_obj(cfg, args, extra=None):
          "hidden": cfg.hidden, "heads": cfg.heads, "relations": cfg.num_rels,
          "parallelism": f"dp{args.gpus}", "precision": args.prec,
          "order": getattr(args, "order", "project_first"),
+         "inner_order": (getattr(args, "inner_order", "agg_first")
+                         if getattr(args, "order", "") == "agg_first" and cfg.model == "rgcn"
+                         else getattr(args, "order", "project_first")),
          "aggregation": cfg.agg,
          "fusion": getattr(args, "fusion", "sum"),
          "feature_storage": getattr(args, "feat_dtype", "fp32"),
