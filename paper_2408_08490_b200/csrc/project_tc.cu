@@ -511,7 +511,10 @@ static_assert(kLag < kFStages, "cp.async lag below the stage count");
 #define HF_G_STAGES 4
 #endif
 static constexpr int kGStages = HF_G_STAGES;
-static constexpr int kGLag = 2;
+#ifndef HF_G_LAG
+#define HF_G_LAG 2
+#endif
+static constexpr int kGLag = HF_G_LAG;
 static constexpr int kGCtas = 1;
 static_assert(kGLag < kGStages, "cp.async lag below the stage count");
 
