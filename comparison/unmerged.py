@@ -193,7 +193,17 @@ def compare_layers(hf, tr, db, cfg, feat_d, et_d, params, stage_kernels):
     tr.step(db, feat_d, et_d, update=False)
     torch.cuda.synchronize()
     out = {"relations": cfg.num_rels, "layers": []}
-    acts, csrs = tr.last["acts"], tr.last["csrs"]
+    acts = tr.last["acts"]
+    # the arms below compare aggregations over the merged Y layout: a
+    # Y-numbered build (with CSC) of every layer -- the Trainer builds its
+    # aggregate-first input layer in X-row mode (col = feature rows), which a
+    # Y-indexed aggregation must not read
+    csrs = [hf.CsrBuffers(s, dev) for s in db.shapes]
+    ws = torch.empty(sum(s.build_ws for s in db.shapes) // 4 + 64, dtype=torch.int32, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    hf.build_semantic_graphs(db.shapes, csrs, db.dev["src"], db.dev["dst"], db.dev["eid"], et_d,
+                             ws, st, rel_edge_off=tr._et_offsets(et_d))
+    torch.cuda.synchronize()
     X = feat_d[db.dev["gid"].long()]                    # layer-0 input rows (type-major batch order)
     for l, sh in enumerate(db.shapes):
         K = cfg.feat_dim if l == 0 else D
