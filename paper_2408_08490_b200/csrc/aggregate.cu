@@ -21,6 +21,11 @@ namespace hf {
 
 static constexpr int kWarpsPerBlock = 8;
 static constexpr int kUnroll = 4;
+// gathers in flight per stream for the raw-feature (evict-first) aggregation
+#ifndef HF_FEAT_UNROLL
+#define HF_FEAT_UNROLL 4
+#endif
+static constexpr int kFeatUnroll = HF_FEAT_UNROLL;
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
@@ -71,20 +76,21 @@ __device__ __forceinline__ float4 agg_row(long long row, const int* __restrict__
   constexpr int NS = 32 / LPR;            // edge streams per warp
   const int sl = lane % LPR, sid = lane / LPR;
   const int b = row_ptr[row], e = row_ptr[row + 1];
+  constexpr int UN = CS ? kFeatUnroll : kUnroll;     // (same add order at any unroll)
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int base = b; base < e; base += 32) {
     const int n = min(32, e - base);
     const int my_col = lane < n ? __ldg(col + base + lane) : 0;
     int k = 0;
-    for (; k + NS * kUnroll <= n; k += NS * kUnroll) {
-      float4 v[kUnroll];
+    for (; k + NS * UN <= n; k += NS * UN) {
+      float4 v[UN];
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++) {
+      for (int u = 0; u < UN; u++) {
         int c = __shfl_sync(0xffffffffu, my_col, k + u * NS + sid);
         v[u] = CS ? ldcs4(Y + (long long)c * LPR + sl) : ldg4(Y + (long long)c * LPR + sl);
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++) acc = f4add(acc, v[u]);
+      for (int u = 0; u < UN; u++) acc = f4add(acc, v[u]);
     }
     for (; k < n; k += NS) {
       int idx = k + sid;

@@ -24,7 +24,10 @@
 
 namespace hf {
 
-static constexpr int kBK = 32;             // K slab
+#ifndef HF_HEAD_BK
+#define HF_HEAD_BK 32
+#endif
+static constexpr int kBK = HF_HEAD_BK;     // K slab
 static constexpr int kBM = 32, kBN = 64;   // block tile; 4 warps of 16 x 32
 
 __device__ __forceinline__ uint32_t to_tf32(float x) {
@@ -62,17 +65,18 @@ __device__ __forceinline__ void mma_tile(int M, int N, const float* __restrict__
 #pragma unroll
     for (int j = 0; j < 4; j++) acc[i][j] = 0.f;
   float cs = 0.f;
-  float ra[8], rb[16];
+  constexpr int QA = kBM * kBK / 128, QB = kBK * kBN / 128;   // slab loads per thread
+  float ra[QA], rb[QB];
   auto fetch = [&](int k0) {
 #pragma unroll
-    for (int q = 0; q < 8; q++) {                 // A slab: kBM x kBK
+    for (int q = 0; q < QA; q++) {                // A slab: kBM x kBK
       const int i = tid + 128 * q;
       const int kk = TA ? i / kBM : i % kBK, mm = TA ? i % kBM : i / kBK;
       const int m = m0 + mm, k = k0 + kk;
       ra[q] = (m < M && k < kb1) ? (TA ? A[(long long)k * lda + m] : A[(long long)m * lda + k]) : 0.f;
     }
 #pragma unroll
-    for (int q = 0; q < 16; q++) {                // B slab: kBK x kBN
+    for (int q = 0; q < QB; q++) {                // B slab: kBK x kBN
       const int i = tid + 128 * q;
       const int kk = TB ? i % kBK : i / kBN, nn = TB ? i / kBK : i % kBN;
       const int n = n0 + nn, k = k0 + kk;
@@ -82,12 +86,12 @@ __device__ __forceinline__ void mma_tile(int M, int N, const float* __restrict__
   if (kb0 < kb1) fetch(kb0);
   for (int k0 = kb0; k0 < kb1; k0 += kBK) {
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
+    for (int q = 0; q < QA; q++) {
       const int i = tid + 128 * q;
       As[TA ? i % kBM : i / kBK][TA ? i / kBM : i % kBK] = ra[q];
     }
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
+    for (int q = 0; q < QB; q++) {
       const int i = tid + 128 * q;
       Bs[TB ? i % kBK : i / kBN][TB ? i / kBK : i % kBN] = rb[q];
     }

@@ -429,7 +429,10 @@ hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot
   for (int t = 0; t < dm.T; t++) max_out = std::max(max_out, dm.out_off[t + 1] - dm.out_off[t]);
   if (max_out > 128) return HIFUSE_ERR_UNSUPPORTED;
   // split the output features over two CTAs when that still leaves a small grid
-  const bool split = false;   // measured: no gain from splitting the output features
+#ifndef HF_DG_SPLIT
+#define HF_DG_SPLIT 0
+#endif
+  const bool split = HF_DG_SPLIT;   // measured: no gain from splitting the output features
   if (K == 128 && D == 128) {
     if (split) launch_dgrad<128, 128, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
     else launch_dgrad<128, 128, 128>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
