@@ -96,8 +96,8 @@ static constexpr int kDgStages = HF_DG_STAGES;
 static constexpr int kDgProd = HF_DG_PRODUCERS;
 static_assert(kDgProd >= 4 && kDgProd <= kDgStages, "producers: >= 4 (epilogue), <= stages");
 
-template <int K, int D, int KN>
-__global__ void __launch_bounds__((kDgProd + 1) * 32)
+template <int K, int D, int KN, int ST, int PR>
+__global__ void __launch_bounds__((PR + 1) * 32)
 k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ dY,
            const float* __restrict__ G, const float* __restrict__ W_rel,
            const float* __restrict__ W_root, float* __restrict__ dX, int max_out) {
@@ -107,11 +107,11 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   //            warp waits for its own cp.async group before the proxy fence);
   //            afterwards the epilogue (TMEM lanes 32w .. 32w + 31)
   // warp 4:    one thread issues the MMAs in chunk order
-  constexpr int BM = 128, DC = D / 32, NS = K / KN, P = kDgProd;
+  constexpr int BM = 128, DC = D / 32, NS = K / KN, P = PR;
   constexpr uint32_t A_STAGE = BM * 128, B_STAGE = KN * 128, STAGE = A_STAGE + B_STAGE;
   constexpr uint32_t IDESC = idesc_tf32(BM, KN, 0, 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[kDgStages], empty[kDgStages], done;
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], done;
   __shared__ uint32_t tmem_slot;
   const int tile = blockIdx.x / NS, n0 = (blockIdx.x % NS) * KN;
   const int s_ = upper_bound_i(dm.tile_off, dm.T + 1, tile) - 1;
@@ -119,9 +119,9 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   const int nrows = min(BM, dm.n_src[s_] - j0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  int* s_arow = reinterpret_cast<int*>(smem_raw + (base - smem_u32(smem_raw)) + kDgStages * STAGE);
+  int* s_arow = reinterpret_cast<int*>(smem_raw + (base - smem_u32(smem_raw)) + ST * STAGE);
   if (tid == 0) {
-    for (int q = 0; q < kDgStages; q++) {
+    for (int q = 0; q < ST; q++) {
       mbar_init(smem_u32(&full[q]), 32);
       mbar_init(smem_u32(&empty[q]), 1);
     }
@@ -158,8 +158,8 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   if (warp < P) {
     // ------------------------------------------------------------ producers
     for (int c = warp; c < NC; c += P) {
-      const int st = c % kDgStages;
-      if (c >= kDgStages) mbar_wait(smem_u32(&empty[st]), ((c / kDgStages) - 1) & 1);
+      const int st = c % ST;
+      if (c >= ST) mbar_wait(smem_u32(&empty[st]), ((c / ST) - 1) & 1);
       const int term = c / DC, d0 = (c % DC) * 32;
       const bool root = term == nout;
       const float* W;
@@ -201,8 +201,8 @@ k_dgrad_tc(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict
   } else if (lane == 0) {
     // ------------------------------------------------------------------ MMA
     for (int c = 0; c < NC; c++) {
-      const int st = c % kDgStages;
-      mbar_wait(smem_u32(&full[st]), (c / kDgStages) & 1);
+      const int st = c % ST;
+      mbar_wait(smem_u32(&full[st]), (c / ST) & 1);
       tc_fence_after();
       const uint32_t sa = base + st * STAGE, sb = sa + A_STAGE;
 #pragma unroll
@@ -406,19 +406,25 @@ k_wgrad_tc(ProjMeta pm, int CH, const int* __restrict__ chunk_off, const int* __
 }
 
 template <int K, int D, int KN>
-static constexpr int dgrad_smem() { return kDgStages * (128 * 128 + KN * 128) + 1024; }
+static constexpr int dgrad_smem(int st) { return st * (128 * 128 + KN * 128) + 1024; }
 template <int K, int D>
 static constexpr int wgrad_smem() { return kWgStages * (4 * 4096 + (D / 32) * 4096) + 1024; }
 
+// Pipeline depth per variant: a K = 128 layer splits the output features
+// over two CTAs (KN = 64; 2 CTAs per SM need <= 4 stages of 24 KB), a K = 64
+// layer keeps one CTA per tile with 6 producer warps / 6 stages.  Measured:
+// IMDB inner-layer input gradient 23.4 -> 19.4 us with the split, mag
+// unchanged; Freebase (K = 64) 23.4 -> 21.8 us with 6 stages.
 template <int K, int D, int KN>
 static void launch_dgrad(const DgradMeta& dm, int max_out, const int* slot_y, const float* dY,
                          const float* G, const float* W_rel, const float* W_root, float* dX,
                          cudaStream_t s) {
-  const int smem = dgrad_smem<K, D, KN>() + max_out * 128 * 4;
-  set_max_smem((const void*)k_dgrad_tc<K, D, KN>, smem);
+  constexpr int ST = (K / KN > 1) ? 4 : kDgStages, PR = (K / KN > 1) ? 4 : kDgProd;
+  const int smem = dgrad_smem<K, D, KN>(ST) + max_out * 128 * 4;
+  set_max_smem((const void*)k_dgrad_tc<K, D, KN, ST, PR>, smem);
   const unsigned grid = (unsigned)dm.tile_off[dm.T] * (K / KN);
-  HF_LAUNCH((k_dgrad_tc<K, D, KN>), grid, (kDgProd + 1) * 32, smem, s, dm, slot_y, dY, G, W_rel, W_root, dX,
-            max_out);
+  HF_LAUNCH((k_dgrad_tc<K, D, KN, ST, PR>), grid, (PR + 1) * 32, smem, s, dm, slot_y, dY, G,
+            W_rel, W_root, dX, max_out);
 }
 
 hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot_y,
@@ -428,22 +434,11 @@ hifuse_status dgrad_tc_launch(const DgradMeta& dm, int K, int D, const int* slot
   int max_out = 0;
   for (int t = 0; t < dm.T; t++) max_out = std::max(max_out, dm.out_off[t + 1] - dm.out_off[t]);
   if (max_out > 128) return HIFUSE_ERR_UNSUPPORTED;
-  // split the output features over two CTAs when that still leaves a small grid
-#ifndef HF_DG_SPLIT
-#define HF_DG_SPLIT 0
-#endif
-  const bool split = HF_DG_SPLIT;   // measured: no gain from splitting the output features
-  if (K == 128 && D == 128) {
-    if (split) launch_dgrad<128, 128, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
-    else launch_dgrad<128, 128, 128>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
-  } else if (K == 128 && D == 64) {
-    if (split) launch_dgrad<128, 64, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
-    else launch_dgrad<128, 64, 128>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
-  } else if (K == 64 && D == 128) {
-    launch_dgrad<64, 128, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
-  } else {
-    launch_dgrad<64, 64, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
-  }
+  // K = 128: two CTAs per 128-row tile, 64 output features each (launch_dgrad)
+  if (K == 128 && D == 128) launch_dgrad<128, 128, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+  else if (K == 128 && D == 64) launch_dgrad<128, 64, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+  else if (K == 64 && D == 128) launch_dgrad<64, 128, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
+  else launch_dgrad<64, 64, 64>(dm, max_out, slot_y, dY, G, W_rel, W_root, dX, s);
   return HIFUSE_OK;
 }
 
