@@ -422,14 +422,19 @@ __global__ void k_wgrad_reduce(int R, int T, int KD, const int* __restrict__ chu
   // chunk table: from chunk_off (SIMT path) or rebuilt here from rel_y_off
   __shared__ int s_co[HF_MAX_R + HF_MAX_T + 1];
   if (!chunk_off) {
+    // group chunk counts loaded in parallel (one thread per group), then
+    // scanned from shared memory by thread 0 (a serial loop over global
+    // loads here left the block waiting at the barrier: ncu, mag layer 0)
+    const int GG = pm.R + pm.T;
+    if ((int)threadIdx.x < GG) {
+      const int g = threadIdx.x;
+      const int rows = g < pm.R ? rel_y_off[g + 1] - rel_y_off[g] : (pm.has_root ? pm.n_dst[g - pm.R] : 0);
+      s_co[g + 1] = (rows + CH - 1) / CH;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int g = 0; g < pm.R + pm.T; g++) {
-        const int rows = g < pm.R ? rel_y_off[g + 1] - rel_y_off[g] : (pm.has_root ? pm.n_dst[g - pm.R] : 0);
-        s_co[g] = acc;
-        acc += (rows + CH - 1) / CH;
-      }
-      s_co[pm.R + pm.T] = acc;
+      s_co[0] = 0;
+      for (int g = 1; g <= GG; g++) s_co[g] += s_co[g - 1];
     }
     __syncthreads();
     chunk_off = s_co;
