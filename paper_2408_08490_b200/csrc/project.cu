@@ -567,7 +567,10 @@ k_dgrad(DgradMeta dm, const int* __restrict__ slot_y, const float* __restrict__ 
 //   dst (mode 1): P[c][h][w] = sum_i ds_dst[(r,i),h] X_t(r)[i][w] rows = merged rows of r
 // Thread (h, w4) accumulates one float4 of the H x W outer-product sum; every
 // row is read once per block (coalesced float4 rows), 4 rows in flight.
-static constexpr int kCHA = 32;    // attention-gradient chunk rows
+#ifndef HF_CHA
+#define HF_CHA 32
+#endif
+static constexpr int kCHA = HF_CHA;    // attention-gradient chunk rows
 
 // chunk table of kCHA-row chunks per relation into shared memory (warp 0)
 __device__ __forceinline__ void att_chunk_table(int R, const int* ro, int* s_tab) {
