@@ -677,6 +677,7 @@ k_att_dvda(int R, int K, int D, int H, const int* __restrict__ rel_y_off, ProjMe
 #pragma unroll
     for (int j = 0; j < 8; j++) acc[j] = 0.f;
     const float* pd = Pdst + (long long)h0 * K;
+#pragma unroll 2
     for (int c = s_tab2[r] + w; c < s_tab2[r + 1]; c += 8) {
       const float* pc = pd + (long long)c * H * K;
 #pragma unroll
@@ -696,8 +697,23 @@ k_att_dvda(int R, int K, int D, int H, const int* __restrict__ rel_y_off, ProjMe
   __syncthreads();
   const int h = d / dh;
   const float* vv = sdv + (h - h0) * K;
-  float u = 0.f;
-  for (int c = s_tab[r] + w; c < s_tab[r + 1]; c += 8) u += Psrc[((long long)c * H + h) * D + d];
+  // datt src half: the warp's chunks c0+w, +8, ... with four loads in flight
+  // (fixed accumulator pairing: deterministic)
+  float u;
+  {
+    const float* ps = Psrc + (long long)h * D + d;
+    const long long cs = (long long)H * D;
+    float u0 = 0.f, u1 = 0.f, u2 = 0.f, u3 = 0.f;
+    int c = s_tab[r] + w;
+    const int ce = s_tab[r + 1];
+    for (; c + 24 < ce; c += 32) {
+      u0 += ps[c * cs]; u1 += ps[(c + 8) * cs]; u2 += ps[(c + 16) * cs]; u3 += ps[(c + 24) * cs];
+    }
+    if (c < ce) u0 += ps[c * cs];
+    if (c + 8 < ce) u1 += ps[(c + 8) * cs];
+    if (c + 16 < ce) u2 += ps[(c + 16) * cs];
+    u = (u0 + u1) + (u2 + u3);
+  }
   float t = 0.f;
   const float* wp = W_rel + (long long)r * K * D + d;
   for (int k = w; k < K; k += 8) t = fmaf(wp[(long long)k * D], vv[k], t);
