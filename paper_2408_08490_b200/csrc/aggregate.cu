@@ -26,6 +26,17 @@ static constexpr int kUnroll = 4;
 #define HF_FEAT_UNROLL 4
 #endif
 static constexpr int kFeatUnroll = HF_FEAT_UNROLL;
+// feature aggregations of at most kLatRows merged rows (under one wave of
+// warps: latency- not bandwidth-bound, e.g. the inner layer) use the latency
+// variant of agg_row: kLatUnroll loads in flight, predicated tail
+#ifndef HF_LAT_ROWS
+#define HF_LAT_ROWS 8192
+#endif
+#ifndef HF_LAT_UNROLL
+#define HF_LAT_UNROLL 8
+#endif
+static constexpr long long kLatRows = HF_LAT_ROWS;
+static constexpr int kLatUnroll = HF_LAT_UNROLL;
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
@@ -68,7 +79,10 @@ __device__ __forceinline__ float4 ldcs4(const float4* p) { return __ldcs(p); }
 // ------------------------------------------------------------ forward SUM/MEAN
 // One merged row (warp; D = 64: two edge streams of 16 lanes): the row's sum
 // (mean: divided by its degree), in every stream-0 lane's float4 slice.
-template <int D, bool MEAN, bool CS>
+// UNR > 0 (latency variant, small layers): UNR loads in flight and the tail
+// as one predicated batch (masked slots add +0) instead of one dependent load
+// per remaining edge -- same add order.
+template <int D, bool MEAN, bool CS, int UNR = 0>
 __device__ __forceinline__ float4 agg_row(long long row, const int* __restrict__ row_ptr,
                                           const int* __restrict__ col,
                                           const float4* __restrict__ Y, int lane) {
@@ -76,7 +90,7 @@ __device__ __forceinline__ float4 agg_row(long long row, const int* __restrict__
   constexpr int NS = 32 / LPR;            // edge streams per warp
   const int sl = lane % LPR, sid = lane / LPR;
   const int b = row_ptr[row], e = row_ptr[row + 1];
-  constexpr int UN = CS ? kFeatUnroll : kUnroll;     // (same add order at any unroll)
+  constexpr int UN = UNR ? UNR : (CS ? kFeatUnroll : kUnroll);   // (same add order at any unroll)
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int base = b; base < e; base += 32) {
     const int n = min(32, e - base);
@@ -92,11 +106,26 @@ __device__ __forceinline__ float4 agg_row(long long row, const int* __restrict__
 #pragma unroll
       for (int u = 0; u < UN; u++) acc = f4add(acc, v[u]);
     }
-    for (; k < n; k += NS) {
-      int idx = k + sid;
-      int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
-      if (idx < n)
-        acc = f4add(acc, CS ? ldcs4(Y + (long long)c * LPR + sl) : ldg4(Y + (long long)c * LPR + sl));
+    if (UNR > 0) {
+      if (k < n) {
+        float4 v[UN];
+#pragma unroll
+        for (int u = 0; u < UN; u++) {
+          const int idx = k + u * NS + sid;
+          const int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+          v[u] = idx < n ? (CS ? ldcs4(Y + (long long)c * LPR + sl) : ldg4(Y + (long long)c * LPR + sl))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < UN; u++) acc = f4add(acc, v[u]);
+      }
+    } else {
+      for (; k < n; k += NS) {
+        int idx = k + sid;
+        int c = __shfl_sync(0xffffffffu, my_col, idx < n ? idx : 0);
+        if (idx < n)
+          acc = f4add(acc, CS ? ldcs4(Y + (long long)c * LPR + sl) : ldg4(Y + (long long)c * LPR + sl));
+      }
     }
   }
 #pragma unroll
@@ -109,7 +138,7 @@ __device__ __forceinline__ float4 agg_row(long long row, const int* __restrict__
   return acc;
 }
 
-template <int D, bool MEAN, bool CS = false>
+template <int D, bool MEAN, bool CS = false, int UNR = 0>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict__ col,
           const float4* __restrict__ Y, float4* __restrict__ Z) {
@@ -118,7 +147,7 @@ k_agg_fwd(long long rows, const int* __restrict__ row_ptr, const int* __restrict
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (row >= rows) return;
-  const float4 acc = agg_row<D, MEAN, CS>(row, row_ptr, col, Y, lane);
+  const float4 acc = agg_row<D, MEAN, CS, UNR>(row, row_ptr, col, Y, lane);
   if (lane < LPR) Z[row * LPR + lane] = acc;
 }
 
@@ -1427,8 +1456,12 @@ hifuse_status hifuse_aggregate_features_fwd(const hifuse_layer_shape* shape, con
   const int TB = kWarpsPerBlock * 32;
   const bool mean = agg == HIFUSE_AGG_MEAN;
 #define HF_AGG(DD, MM)                                                                  \
-  HF_LAUNCH((k_agg_fwd<DD, MM, true>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, col_x, \
-            (const float4*)d_X, (float4*)d_Xagg)
+  do { if (m.rows <= kLatRows)                                                          \
+    HF_LAUNCH((k_agg_fwd<DD, MM, true, kLatUnroll>), grid, TB, 0, s, (long long)m.rows,  \
+              csr->row_ptr, col_x, (const float4*)d_X, (float4*)d_Xagg);                \
+  else                                                                                  \
+    HF_LAUNCH((k_agg_fwd<DD, MM, true>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, col_x, \
+              (const float4*)d_X, (float4*)d_Xagg); } while (0)
   if (K == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
   else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }
 #undef HF_AGG
@@ -1474,8 +1507,12 @@ hifuse_status hifuse_aggregate_features_cols(const hifuse_layer_shape* shape,
   const int TB = kWarpsPerBlock * 32;
   const bool mean = agg == HIFUSE_AGG_MEAN;
 #define HF_AGG(DD, MM)                                                                  \
-  HF_LAUNCH((k_agg_fwd<DD, MM, true>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, d_col_x, \
-            (const float4*)d_X, (float4*)d_Xagg)
+  do { if (m.rows <= kLatRows)                                                          \
+    HF_LAUNCH((k_agg_fwd<DD, MM, true, kLatUnroll>), grid, TB, 0, s, (long long)m.rows,  \
+              csr->row_ptr, d_col_x, (const float4*)d_X, (float4*)d_Xagg);              \
+  else                                                                                  \
+    HF_LAUNCH((k_agg_fwd<DD, MM, true>), grid, TB, 0, s, (long long)m.rows, csr->row_ptr, d_col_x, \
+              (const float4*)d_X, (float4*)d_Xagg); } while (0)
   if (K == 128) { if (mean) HF_AGG(128, true); else HF_AGG(128, false); }
   else { if (mean) HF_AGG(64, true); else HF_AGG(64, false); }
 #undef HF_AGG
